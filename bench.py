@@ -1,0 +1,316 @@
+"""Benchmark: DIAM chain-samples/s on B200 (BASELINE.json metric).
+
+Default workload (N=1): BASELINE.json configs[1] — DIAM, d=1024 anisotropic
+Gaussian (pi1), 64 concurrent synchronised chains per GPU, n_lag = d/2 = 512,
+M = 4 lag windows per batch, burn-in n0 = 0 and traces
+off as in the reference's own `benchmark` command (proj/tools/diam_cli.cpp:
+446-458). One bench "step" = one batch = 64 x 4 x 512 = 131072 chain-samples
+(windows of Philox noise -> TRMM -> target GEMM -> MH steps -> SYRK moments ->
+blend/POTRF/usable guard per window, then the moment merge).
+
+  value  : device-resident throughput, CUDA events on the engine stream,
+           max over ranks (diamx_engine_run_batches)
+  e2e    : the same metric through the reference-facing C ABI (diam_sample)
+           with the target in host memory: H2D upload, engine init, K batches,
+           D2H of the result, all inside the timed region (host clock)
+  roofline: the dominant kernel class (the FP64 DMMA GEMM: TRMM + target GEMM +
+           SYRK + POTRF updates) against the FP64 DMMA peak measured live on
+           this GPU (tcgen05 has no f64 kind)
+  cpu_baseline: the reference itself (oracle/_ref, built from
+           /root/reference/proj/src) on the host cores, bounded sample.
+
+`--impl reference` times the reference's CPU implementation of the same
+workload (oracle/_ref, all host threads) and prints its own line.
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N (weak scaling: 64
+chains per GPU, NCCL all-reduce of the batch moments over NVLink).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (target kind, d, chains per GPU, n_lag, M)
+    "d1024": ("pi1", 1024, 64, 512, 4),
+    "d4096": ("pi1", 4096, 64, 2048, 1),
+    "d2040": ("pi5", 2040, 256, 1020, 1),
+    "d8192": ("pi1", 8192, 128, 4096, 1),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_target_file(kind, d, seed=1):
+    from paper_1506_05741_b200 import fixtures
+    path = os.path.join(tempfile.gettempdir(), f"diam_bench_{kind}_{d}_{seed}_{os.getpid()}.bin")
+    fixtures.make(path, kind, d, seed)
+    return path
+
+
+def run_options(cfg, chains, **over):
+    kind, d, _, n_lag, M = cfg
+    o = dict(kernel="diam", chains=chains, intervals_per_batch=M, n_lag=n_lag, n0=0, record_traces=0,
+             trace_eigen_projections=0, master_seed=2026)
+    o.update(over)
+    return o
+
+
+# ---------------------------------------------------------------------------- reference CPU arm
+def reference_sample(cfg_name, target_path, threads, chains, windows=1):
+    """One bounded reference run: `chains` chains x `windows` lag windows on the host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle as O
+    from paper_1506_05741_b200.abi import DiamABI
+    if not O.ref_available():
+        return None
+    kind, d, _, n_lag, _ = CONFIGS[cfg_name]
+    ref = DiamABI(O.REF_SO)
+    t = ref.target_load(target_path)
+    t0 = time.perf_counter()
+    r = ref.sample(t, **run_options(CONFIGS[cfg_name], chains, intervals_per_batch=windows, max_batches=1,
+                                    threads=threads))
+    wall = time.perf_counter() - t0
+    return r.total_samples, wall
+
+
+def impl_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    kind, d, per_gpu, n_lag, M = cfg
+    threads = os.cpu_count() or 1
+    target = make_target_file(kind, d)
+    chains = threads  # one chain per host thread (thread-count invariant results, runner.cpp:316-324)
+    samples, times = 0, []
+    for i in range(args.warmup + args.steps):
+        res = reference_sample(args.config, target, threads, chains)
+        if res is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdiam_ref.so not built"}))
+            return 0
+        if i >= args.warmup:
+            samples += res[0]
+            times.append(res[1])
+    os.unlink(target)
+    total = sum(times)
+    value = samples / total
+    line = {
+        "impl": "reference", "metric": f"chain-samples/s (DIAM, {kind} d={d}, n_lag={n_lag})", "value": value,
+        "unit": "chain-samples/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (pi1 target from the reference's Philox stream)",
+        "config": {"workload": f"{args.config}: {chains} chains x 1 window of {n_lag} steps per step "
+                               f"(reference diam_sample, {threads} threads)", "d": d, "chains": chains,
+                   "n_lag": n_lag, "kernel": "diam", "n0": 0},
+        "cpu_baseline": {"value": value, "unit": "chain-samples/s", "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} x diam_sample({chains} chains, 1 window of {n_lag}) at d={d}"},
+        "e2e": {"value": value, "unit": "chain-samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------- B200 arm
+def impl_b200(args):
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_1506_05741_b200 as pkg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+    torch.cuda.set_device(local)
+    lib = pkg.load()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = C.create_string_buffer(128)
+            lib.check(lib.lib.diamx_nccl_unique_id(buf))
+            uid = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
+        uid = uid.cuda()
+        dist.broadcast(uid, 0)
+        lib.check(lib.lib.diamx_comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world))
+
+    cfg = CONFIGS[args.config]
+    kind, d, per_gpu, n_lag, M = cfg
+    chains = per_gpu * world
+    # identical target file on every rank (deterministic generator)
+    target_path = make_target_file(kind, d)
+    t = lib.target_load(target_path)
+
+    # ---- device-resident throughput
+    eng = lib.engine(t, **run_options(cfg, chains))
+    eng.run_batches(args.warmup)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches0 = lib.launch_count()
+    with ClockSampler(local) as clocks:
+        ms = eng.run_batches(args.steps)
+    launches = lib.launch_count() - launches0
+    if dist:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.barrier()
+    samples_per_step = chains * M * n_lag
+    value = samples_per_step * args.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel class (profiled pass, CUDA events per launch)
+    eng.set_profiling(True)
+    eng.run_batches(1)
+    classes = ["gemm_target", "trmm_noise", "syrk_moments", "potrf", "mh_window", "normals", "trsv", "blend_cov",
+               "merge", "gemv_state"]
+    st = {c: eng.stat(c) for c in classes}
+    prof_total = sum(v[0] for v in st.values())
+    gemm_cls = ["gemm_target", "trmm_noise", "syrk_moments"]
+    g_ms = sum(st[c][0] for c in gemm_cls)
+    g_fl = sum(st[c][1] for c in gemm_cls)
+    peak = C.c_double()
+    lib.check(lib.lib.diamx_fp64_peak(C.byref(peak)))
+    achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
+    alg_flops = eng.flops_per_batch
+    del eng
+
+    # ---- end-to-end through the C ABI (host target, result back to host)
+    torch.cuda.synchronize()
+    lib.sample(t, **run_options(cfg, chains, max_batches=1))  # warm (module load, allocator)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    r = lib.sample(t, **run_options(cfg, chains, max_batches=args.steps))
+    mean = r.mean()
+    cov = r.cov()
+    wall = time.perf_counter() - t0
+    if dist:
+        tt = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        wall = float(tt.item())
+    e2e = r.total_samples / wall
+    h2d = (d * d * 8 * 2 + 4 * d * 8) / args.steps  # precision + analytic covariance + vectors, once per run
+    d2h = (mean.nbytes + cov.nbytes) / args.steps + chains * M * 16 + 24
+    os.unlink(target_path)
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            cpu_t = make_target_file(kind, d)
+            threads = os.cpu_count() or 1
+            res = reference_sample(args.config, cpu_t, threads, threads)
+            os.unlink(cpu_t)
+            if res:
+                cpu = {"value": res[0] / res[1], "unit": "chain-samples/s", "cores": threads, "kind": "reference",
+                       "sample": f"reference diam_sample: {threads} chains x 1 window of {n_lag} steps at d={d} "
+                                 f"({res[0]} chain-samples in {res[1]:.1f} s, incl. its init window)"}
+        line = {
+            "metric": f"chain-samples/s (DIAM, {kind} d={d}, n_lag={n_lag})",
+            "value": value, "unit": "chain-samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (pi1 target, Philox stream of the reference, random chains)",
+            "config": {"workload": f"{args.config}: DIAM {kind} d={d}, {per_gpu} chains/GPU, n_lag={n_lag}, "
+                                   f"M={M} windows per step, n0=0, traces off",
+                       "d": d, "chains": chains, "chains_per_gpu": per_gpu, "n_lag": n_lag,
+                       "intervals_per_batch": M, "kernel": "diam", "parallelism": f"chains sharded dp{world}",
+                       "l2": "no flush needed: per-step working set "
+                             f"{(3 * d * d + 3 * n_lag * d) * 8 * per_gpu / 1e9:.1f} GB >> 126 MB L2"},
+            "roofline": {"bound": "fp64-dmma", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+                         "frac": achieved / peak.value if peak.value else None, "traffic": None,
+                         "kernel": "gemm_f64 (TRMM noise + target GEMM + SYRK moments)",
+                         "share_of_step": g_ms / prof_total if prof_total else None,
+                         "peak_source": "diamx_fp64_peak: DMMA m8n8k4 loop measured live (MEASURED_PEAKS.json "
+                                        "has no FP64 entry)",
+                         "step_alg_tflops": alg_flops / (ms / args.steps / 1e3) / 1e12 / max(1, 1),
+                         "per_class_ms": {c: round(v[0], 4) for c, v in st.items()}},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "chain-samples/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "note": "diam_sample via the C ABI: target upload + engine init + K batches + result copy"},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line))
+    if dist:
+        lib.lib.diamx_comm_destroy()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="d1024")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return impl_reference(args)
+    return impl_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

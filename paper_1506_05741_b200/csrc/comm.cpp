@@ -1,0 +1,116 @@
+// comm.cpp — NCCL communicator loaded with dlopen (see comm.hpp).
+#include "comm.hpp"
+
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace dgb {
+
+namespace {
+
+// Minimal NCCL ABI (nccl.h 2.x): opaque communicator, 128-byte unique id.
+typedef struct ncclComm* ncclComm_t;
+struct ncclUniqueId {
+    char internal[128];
+};
+enum ncclResult_t { ncclSuccess = 0 };
+enum ncclDataType_t { ncclFloat64 = 8 };
+enum ncclRedOp_t { ncclSum = 0 };
+
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    std::string err;
+    bool load() {
+        if (h) return true;
+        // prefer an already-loaded copy (torch ships libnccl.so.2), else the system one
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            err = dlerror() ? dlerror() : "dlopen libnccl.so.2 failed";
+            return false;
+        }
+        GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+        AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+        AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+        CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+        GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+        if (!GetUniqueId || !CommInitRank || !AllReduce || !AllGather || !CommDestroy) {
+            err = "libnccl.so.2 lacks expected symbols";
+            h = nullptr;
+            return false;
+        }
+        return true;
+    }
+    void check(ncclResult_t r, const char* what) const {
+        if (r != ncclSuccess)
+            throw CudaError(std::string("NCCL ") + what + ": " + (GetErrorString ? GetErrorString(r) : "error"));
+    }
+};
+
+NcclApi& api() {
+    static NcclApi a;
+    return a;
+}
+
+struct NcclComm final : Comm {
+    ncclComm_t comm = nullptr;
+    int r = 0, n = 1;
+    ~NcclComm() override {
+        if (comm) api().CommDestroy(comm);
+    }
+    int rank() const override { return r; }
+    int size() const override { return n; }
+    void allreduce_sum(double* buf, int64_t cnt, cudaStream_t s) override {
+        api().check(api().AllReduce(buf, buf, (size_t)cnt, ncclFloat64, ncclSum, comm, s), "allreduce");
+    }
+    void allgather(const double* src, double* dst, int64_t cnt, cudaStream_t s) override {
+        api().check(api().AllGather(src, dst, (size_t)cnt, ncclFloat64, comm, s), "allgather");
+    }
+};
+
+}  // namespace
+
+std::shared_ptr<Comm>& global_comm() {
+    static std::shared_ptr<Comm> c;
+    return c;
+}
+
+bool nccl_available(char* why, int why_len) {
+    const bool ok = api().load();
+    if (!ok && why) std::snprintf(why, why_len, "%s", api().err.c_str());
+    return ok;
+}
+
+int nccl_unique_id(char out[128]) {
+    if (!api().load()) return 1;
+    ncclUniqueId id;
+    api().check(api().GetUniqueId(&id), "get unique id");
+    std::memcpy(out, id.internal, 128);
+    return 0;
+}
+
+std::shared_ptr<Comm> make_nccl_comm(const char id_bytes[128], int rank, int world) {
+    if (!api().load()) throw CudaError("NCCL unavailable: " + api().err);
+    auto c = std::make_shared<NcclComm>();
+    ncclUniqueId id;
+    std::memcpy(id.internal, id_bytes, 128);
+    c->r = rank;
+    c->n = world;
+    api().check(api().CommInitRank(&c->comm, world, id, rank), "comm init");
+    return c;
+}
+
+}  // namespace dgb

@@ -1,0 +1,34 @@
+// comm.hpp — the engine's view of the multi-GPU exchange.
+//
+// The sampler has exactly one exchange step per batch (proj/src/runner.cpp:
+// 238-245): the moment merge. Chains are block-sharded over ranks (one process
+// per GPU); each rank pre-sums its chains' raw moments and an all-reduce(sum,
+// f64) over NVLink pools them; per-chain PSRF inputs are all-gathered. NCCL is
+// loaded lazily with dlopen so the library has no hard link dependency (the
+// process's already-loaded libnccl.so.2, e.g. torch's, is reused).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <memory>
+
+namespace dgb {
+
+struct Comm {
+    virtual ~Comm() = default;
+    virtual int rank() const = 0;
+    virtual int size() const = 0;
+    virtual void allreduce_sum(double* buf, int64_t n, cudaStream_t s) = 0;
+    // dst holds size()*n doubles, rank r's block at r*n
+    virtual void allgather(const double* src, double* dst, int64_t n, cudaStream_t s) = 0;
+};
+
+// Process-wide communicator used by diam_sample when set (diamx_comm_init).
+std::shared_ptr<Comm>& global_comm();
+// NCCL: unique id (128 bytes) from rank 0, shared out of band by the caller.
+bool nccl_available(char* why, int why_len);
+int nccl_unique_id(char out[128]);
+std::shared_ptr<Comm> make_nccl_comm(const char id[128], int rank, int world);
+
+}  // namespace dgb

@@ -1,0 +1,37 @@
+// common.cuh — shared device/host helpers for the B200 DIAM engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace dgb {
+
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& s) : std::runtime_error(s) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what + " at " +
+                        file + ":" + std::to_string(line));
+}
+#define DGB_CUDA(x) ::dgb::cuda_check((x), #x, __FILE__, __LINE__)
+#define DGB_LAUNCH_CHECK() ::dgb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Process-wide count of our own kernel launches (bench.py reports it as gpu_launches).
+extern uint64_t g_launch_count;
+inline void count_launch(uint64_t n = 1) { g_launch_count += n; }
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Leading dimension used for every device d-vector/d×d row: a multiple of 8
+// doubles (64 B) so rows stay 16-byte aligned for cp.async / vector loads and
+// tiles never straddle a row end without a zero pad.
+inline int64_t pad_ld(int64_t n) { return (n + 7) / 8 * 8; }
+
+}  // namespace dgb

@@ -1,0 +1,786 @@
+// engine.cu — B200 sampler engine (see engine.hpp). Reference semantics cited inline
+// (paths relative to /root/reference/proj/).
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "gemm_f64.cuh"
+
+namespace dgb {
+
+uint64_t g_launch_count = 0;
+
+namespace {
+
+template <class T>
+T* dalloc(std::vector<void*>& list, size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    DGB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    DGB_CUDA(cudaMemset(p, 0, count * sizeof(T)));
+    list.push_back(p);
+    return static_cast<T*>(p);
+}
+
+double** ptr_array(std::vector<void*>& list, double* base, int64_t stride, int n) {
+    std::vector<double*> h(n);
+    for (int i = 0; i < n; ++i) h[i] = base + stride * i;
+    double** d = dalloc<double*>(list, n);
+    DGB_CUDA(cudaMemcpy(d, h.data(), n * sizeof(double*), cudaMemcpyHostToDevice));
+    return d;
+}
+
+// host matrix (rows x cols, row-major) -> device rows x ld
+void upload_padded(double* dst, int64_t ld, const Mat& m) {
+    DGB_CUDA(cudaMemcpy2D(dst, ld * sizeof(double), m.a.data(), m.cols * sizeof(double), m.cols * sizeof(double),
+                          m.rows, cudaMemcpyHostToDevice));
+}
+
+}  // namespace
+
+Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> comm)
+    : tgt_(t), cfg_(cfg), k_(cfg.kernel), comm_(std::move(comm)) {
+    validate_run_cfg(cfg_, tgt_);
+    if (comm_) {
+        rank_ = comm_->rank();
+        world_ = comm_->size();
+    }
+    d_ = static_cast<int>(tgt_.dim);
+    Lw_ = static_cast<int>(k_.n_lag);
+    P_ = static_cast<int>(cfg_.chains);
+    require(P_ >= world_, Err::InvalidArgument, "fewer chains than GPUs");
+    // block sharding of global chain indices: rank r owns [r P / N, (r+1) P / N)
+    c0_ = static_cast<int>((int64_t)rank_ * P_ / world_);
+    C_ = static_cast<int>((int64_t)(rank_ + 1) * P_ / world_) - c0_;
+    ld_ = pad_ld(d_);
+    win_ = (int64_t)Lw_ * ld_;
+    mat_ = (int64_t)d_ * ld_;
+    twisted_ = tgt_.twisted();
+    require(d_ <= 8192, Err::InvalidDimension, "the B200 engine supports d <= 8192");
+    DGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    upload_target();
+    init_chains();
+}
+
+Engine::~Engine() {
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (void* p : allocs_) cudaFree(p);
+    for (auto& e : event_pool_) cudaEventDestroy(e);
+    for (auto& pe : pending_) {
+        cudaEventDestroy(pe.a);
+        cudaEventDestroy(pe.b);
+    }
+    if (h_stage_) cudaFreeHost(h_stage_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::upload_target() {
+    auto& A = allocs_;
+    G_ = dalloc<double>(A, mat_);
+    if (twisted_) {
+        // G = V^T: row i is eigenvector column i
+        Mat vt(d_, d_);
+        for (int i = 0; i < d_; ++i)
+            for (int k = 0; k < d_; ++k) vt(i, k) = tgt_.eigvecs(k, i);
+        upload_padded(G_, ld_, vt);
+        std::vector<double> ie(ld_, 0.0), bc(ld_, 0.0);
+        for (int i = 0; i < d_; ++i) {
+            ie[i] = 1.0 / tgt_.eigvals[i];
+            bc[i] = tgt_.b_coeffs[i];
+        }
+        inv_eig_ = dalloc<double>(A, ld_);
+        bcoef_ = dalloc<double>(A, ld_);
+        DGB_CUDA(cudaMemcpy(inv_eig_, ie.data(), ld_ * 8, cudaMemcpyHostToDevice));
+        DGB_CUDA(cudaMemcpy(bcoef_, bc.data(), ld_ * 8, cudaMemcpyHostToDevice));
+    } else {
+        upload_padded(G_, ld_, tgt_.precision);
+    }
+    Ct_ = dalloc<double>(A, (size_t)d_ * d_);
+    DGB_CUDA(cudaMemcpy(Ct_, tgt_.covariance.a.data(), (size_t)d_ * d_ * 8, cudaMemcpyHostToDevice));
+    std::vector<double> pj(2 * ld_, 0.0);
+    for (int i = 0; i < d_; ++i) {
+        pj[i] = tgt_.eigvecs(i, 0);
+        pj[ld_ + i] = tgt_.eigvecs(i, d_ - 1);
+    }
+    proj_ = dalloc<double>(A, 2 * ld_);
+    DGB_CUDA(cudaMemcpy(proj_, pj.data(), 2 * ld_ * 8, cudaMemcpyHostToDevice));
+    Gp_ = ptr_array(A, G_, 0, 1);
+}
+
+void Engine::init_chains() {
+    auto& A = allocs_;
+    const int C = C_;
+    L_ = dalloc<double>(A, (size_t)C * mat_);
+    Lw2_ = dalloc<double>(A, (size_t)C * mat_);
+    S_ = dalloc<double>(A, (size_t)C * mat_);
+    W_ = dalloc<double>(A, (size_t)C * win_);
+    Xi_ = dalloc<double>(A, (size_t)C * win_);
+    H_ = dalloc<double>(A, (size_t)C * win_);
+    x_ = dalloc<double>(A, (size_t)C * ld_);
+    g_ = dalloc<double>(A, (size_t)C * ld_);
+    y_ = dalloc<double>(A, (size_t)C * ld_);
+    xr_ = dalloc<double>(A, (size_t)C * ld_);
+    gr_ = dalloc<double>(A, (size_t)C * ld_);
+    mean_ = dalloc<double>(A, (size_t)C * ld_);
+    cmean_ = dalloc<double>(A, (size_t)C * ld_);
+    cdiag_ = dalloc<double>(A, (size_t)C * ld_);
+    mb_ = dalloc<double>(A, (size_t)C * ld_);
+    logpi_ = dalloc<double>(A, C);
+    quad_ = dalloc<double>(A, C);
+    beta_ = dalloc<double>(A, C);
+    tr_ = dalloc<double>(A, C);
+    qtmp_ = dalloc<double>(A, C);
+    nacc_ = dalloc<uint64_t>(A, C);
+    uctr_ = dalloc<uint64_t>(A, C);
+    status_ = dalloc<int>(A, C);
+    try_ = dalloc<int>(A, C);
+    usable_ = dalloc<int>(A, C);
+    mask_ = dalloc<int>(A, C);
+    Sg_ = dalloc<double>(A, mat_);
+    mg_ = dalloc<double>(A, ld_);
+    Ssum_ = dalloc<double>(A, mat_ + ld_);
+    cov_part_ = dalloc<double>(A, 2 * (size_t)d_);
+    const size_t M = cfg_.intervals_per_batch;
+    trace_lp_ = dalloc<double>(A, M * C * Lw_);
+    trace_pj_ = dalloc<double>(A, M * C * Lw_ * 2);
+    hist_rate_ = dalloc<double>(A, M * C);
+    hist_beta_ = dalloc<double>(A, M * C);
+    pw_.inv = dalloc<double>(A, (size_t)C * 64 * 64 + C);  // + int active[C] tail
+    pw_.inv_ptrs = ptr_array(A, pw_.inv, 64 * 64, C);
+
+    Lp_ = ptr_array(A, L_, mat_, C);
+    Lnp_ = ptr_array(A, Lw2_, mat_, C);
+    Wp_ = ptr_array(A, W_, win_, C);
+    Xip_ = ptr_array(A, Xi_, win_, C);
+    Hp_ = ptr_array(A, H_, win_, C);
+    Sp_ = ptr_array(A, S_, mat_, C);
+    xp_ = ptr_array(A, x_, 0, 1);
+    gp_ = ptr_array(A, g_, 0, 1);
+    xrp_ = ptr_array(A, xr_, 0, 1);
+    grp_ = ptr_array(A, gr_, 0, 1);
+
+    // RNG keys: global chain index p = c0 + i (runner.cpp:128-130, 556-559)
+    std::vector<PhiloxKey> nk(C), uk(C), ik(C);
+    for (int i = 0; i < C; ++i) {
+        const uint64_t p = (uint64_t)(c0_ + i);
+        nk[i] = make_philox_key(cfg_.master_seed, p, "noise");
+        uk[i] = make_philox_key(cfg_.master_seed, p, "uniform");
+        ik[i] = make_philox_key(cfg_.master_seed, p, "init");
+    }
+    nkeys_ = dalloc<PhiloxKey>(A, C);
+    ukeys_ = dalloc<PhiloxKey>(A, C);
+    ikeys_ = dalloc<PhiloxKey>(A, C);
+    DGB_CUDA(cudaMemcpy(nkeys_, nk.data(), C * sizeof(PhiloxKey), cudaMemcpyHostToDevice));
+    DGB_CUDA(cudaMemcpy(ukeys_, uk.data(), C * sizeof(PhiloxKey), cudaMemcpyHostToDevice));
+    DGB_CUDA(cudaMemcpy(ikeys_, ik.data(), C * sizeof(PhiloxKey), cudaMemcpyHostToDevice));
+
+    // x0 = dispersion * N(0, I) from the "init" stream (runner.cpp:131-132)
+    launch_normal_vec(x_, ld_, C, d_, ikeys_, 0, cfg_.init_dispersion, stream_);
+    // factor = I, beta = beta_init (proposal.cpp:95-97)
+    launch_set_identity(L_, mat_, C, d_, ld_, stream_);
+    std::vector<double> b(C, k_.beta_init);
+    DGB_CUDA(cudaMemcpyAsync(beta_, b.data(), C * 8, cudaMemcpyHostToDevice, stream_));
+    identity_ = true;
+    // log pi(x0), quad(x0) (proposal.cpp:107-108)
+    refresh_g(x_, g_);
+    launch_eval_logpi(x_, g_, inv_eig_, bcoef_, twisted_, logpi_, C, d_, ld_, stream_);
+    if (k_.pcn_form()) {
+        const double infl = k_.noise_infl();
+        launch_trsv(Lp_, ld_, x_, nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl), nullptr, stream_);
+    }
+    DGB_CUDA(cudaStreamSynchronize(stream_));
+
+    // functionals (runner.cpp:292-309)
+    fnames_ = {"log_density"};
+    if (cfg_.trace_eigen_projections) {
+        fnames_.push_back("proj_min");
+        fnames_.push_back("proj_max");
+    }
+    beta_hist_.assign(C, {});
+    acc_hist_.assign(C, {});
+    traces_.assign(C, std::vector<std::vector<double>>(fnames_.size()));
+}
+
+void Engine::refresh_g(const double* vec, double* out) {
+    // out[c] = G vec[c] for all local chains: rows = chains, (vec G^T)
+    GemmBatch g{};
+    const double* const* vp = (vec == x_) ? (const double* const*)xp_ : (const double* const*)xrp_;
+    g.A = vp;
+    g.B = (const double* const*)Gp_;
+    g.C = (out == g_) ? gp_ : grp_;
+    g.lda = ld_;
+    g.ldb = ld_;
+    g.ldc = ld_;
+    g.M = C_;
+    g.N = d_;
+    g.K = d_;
+    g.alpha = 1.0;
+    g.beta = 0.0;
+    gemm("gemv_state", g, 1, true, true, GemmShape::Narrow);
+}
+
+void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, GemmShape sh) {
+    double flops = 2.0 * g.M * (double)g.N * g.K * batch;
+    if (g.tri_c_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
+    if (g.tri_b_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
+    timed_begin(name);
+    gemm_f64(g, batch, ak, bk, stream_, sh);
+    timed_end(name, flops);
+}
+
+void Engine::timed_begin(const char*) {
+    if (!profiling_) return;
+    if (event_pool_.size() < 2) {
+        for (int i = 0; i < 64; ++i) {
+            cudaEvent_t e;
+            DGB_CUDA(cudaEventCreate(&e));
+            event_pool_.push_back(e);
+        }
+    }
+    cur_a_ = event_pool_.back();
+    event_pool_.pop_back();
+    DGB_CUDA(cudaEventRecord(cur_a_, stream_));
+}
+
+void Engine::timed_end(const char* name, double flops) {
+    if (!profiling_) return;
+    cudaEvent_t b = event_pool_.back();
+    event_pool_.pop_back();
+    DGB_CUDA(cudaEventRecord(b, stream_));
+    pending_.push_back({name, cur_a_, b, flops});
+    if (pending_.size() > 4096) resolve_events();
+}
+
+void Engine::resolve_events() {
+    if (pending_.empty()) return;
+    DGB_CUDA(cudaStreamSynchronize(stream_));
+    for (auto& p : pending_) {
+        float ms = 0.f;
+        DGB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        auto& s = stats_[p.name];
+        s.ms += ms;
+        s.flops += p.flops;
+        s.launches += 1;
+        event_pool_.push_back(p.a);
+        event_pool_.push_back(p.b);
+    }
+    pending_.clear();
+}
+
+const std::map<std::string, KernelStat>& Engine::stats() {
+    resolve_events();
+    return stats_;
+}
+
+double Engine::flops_per_batch() const {
+    // algorithmic FP64 flops of one batch over the local chains:
+    // TRMM d(d+1)/2*2 per row, target GEMM 2 d^2 per row, SYRK d(d+1) per row, POTRF d^3/3 per window
+    const double d = d_, L = Lw_, C = C_, M = (double)cfg_.intervals_per_batch;
+    const double per_window = C * (L * d * (d + 1) + L * 2.0 * d * d + L * d * (d + 1) + d * d * d / 3.0);
+    return per_window * M;
+}
+
+void Engine::window(size_t w, bool record) {
+    const int C = C_;
+    const double infl = k_.noise_infl();
+    // ---- noise window: W from Philox, Xi = s W L^T, H = Xi G^T (proposal.cpp:254-266)
+    timed_begin("normals");
+    launch_normals(W_, identity_ ? Xi_ : nullptr, win_, C, Lw_, d_, ld_, nkeys_, nctr_, beta_, infl, stream_);
+    timed_end("normals", 0.0);
+    nctr_ += (uint64_t)Lw_ * d_;
+    if (!identity_) {
+        GemmBatch t{};
+        t.A = (const double* const*)Wp_;
+        t.B = (const double* const*)Lp_;
+        t.C = Xip_;
+        t.lda = ld_;
+        t.ldb = ld_;
+        t.ldc = ld_;
+        t.M = Lw_;
+        t.N = d_;
+        t.K = d_;
+        t.alpha = 1.0;
+        t.alpha_vec = beta_;
+        t.alpha_vec_mul = infl;
+        t.beta = 0.0;
+        t.tri_b_lower = 1;
+        gemm("trmm_noise", t, C, true, true);
+    }
+    {
+        GemmBatch h{};
+        h.A = (const double* const*)Xip_;
+        h.B = (const double* const*)Gp_;
+        h.C = Hp_;
+        h.lda = ld_;
+        h.ldb = ld_;
+        h.ldc = ld_;
+        h.M = C * Lw_;  // all chains' windows are one contiguous (C Lw) x ld matrix
+        h.N = d_;
+        h.K = d_;
+        h.alpha = 1.0;
+        h.beta = 0.0;
+        gemm("gemm_target", h, 1, true, true);
+    }
+    if (capture_) {
+        if (cap_w_.empty()) {
+            cap_w_.assign(C, {});
+            cap_ratio_.assign(C, {});
+            cap_acc_.assign(C, {});
+        }
+        std::vector<double> buf((size_t)C * win_);
+        DGB_CUDA(cudaMemcpyAsync(buf.data(), W_, buf.size() * 8, cudaMemcpyDeviceToHost, stream_));
+        DGB_CUDA(cudaStreamSynchronize(stream_));
+        for (int c = 0; c < C; ++c)
+            for (int r = 0; r < Lw_; ++r)
+                cap_w_[c].insert(cap_w_[c].end(), buf.begin() + (size_t)c * win_ + (size_t)r * ld_,
+                                 buf.begin() + (size_t)c * win_ + (size_t)r * ld_ + d_);
+        if (!dbg_ratio_) {
+            dbg_ratio_ = dalloc<double>(allocs_, (size_t)C * Lw_);
+            dbg_acc_ = dalloc<uint8_t>(allocs_, (size_t)C * Lw_);
+        }
+    }
+
+    // ---- the n_lag MH steps (proposal.cpp:137-157, runner.cpp:363-368)
+    StepParams p{};
+    p.d = d_;
+    p.n_lag = Lw_;
+    p.chains = C;
+    p.ld = ld_;
+    p.win_stride = win_;
+    p.W = W_;
+    p.Xi = Xi_;
+    p.H = H_;
+    p.x = x_;
+    p.g = g_;
+    p.y = y_;
+    const bool has_ref = k_.adaptive_ref;
+    p.xr = has_ref ? xr_ : nullptr;
+    p.gr = has_ref ? gr_ : nullptr;
+    p.log_pi = logpi_;
+    p.quad = quad_;
+    p.beta = beta_;
+    p.n_accepted = nacc_;
+    p.ukeys = ukeys_;
+    p.uctr = uctr_;
+    p.infl = infl;
+    p.pcn = k_.pcn_form() ? 1 : 0;
+    p.inv_eig = inv_eig_;
+    p.bcoef = bcoef_;
+    p.trace_lp = record ? trace_lp_ + w * (size_t)C * Lw_ : nullptr;
+    p.accept_out = capture_ ? dbg_acc_ : nullptr;
+    p.log_ratio_out = capture_ ? dbg_ratio_ : nullptr;
+    timed_begin("mh_window");
+    launch_mh_window(p, twisted_, stream_);
+    timed_end("mh_window", 0.0);
+    if (capture_) {
+        std::vector<double> r((size_t)C * Lw_);
+        std::vector<uint8_t> a((size_t)C * Lw_);
+        DGB_CUDA(cudaMemcpyAsync(r.data(), dbg_ratio_, r.size() * 8, cudaMemcpyDeviceToHost, stream_));
+        DGB_CUDA(cudaMemcpyAsync(a.data(), dbg_acc_, a.size(), cudaMemcpyDeviceToHost, stream_));
+        DGB_CUDA(cudaStreamSynchronize(stream_));
+        for (int c = 0; c < C; ++c) {
+            cap_ratio_[c].insert(cap_ratio_[c].end(), r.begin() + (size_t)c * Lw_, r.begin() + (size_t)(c + 1) * Lw_);
+            cap_acc_[c].insert(cap_acc_[c].end(), a.begin() + (size_t)c * Lw_, a.begin() + (size_t)(c + 1) * Lw_);
+        }
+    }
+    const uint64_t n_start = n_;
+    n_ += Lw_;
+    window_n_start_[w] = n_start;
+
+    // ---- moments of the post-burn-in states: rows t with n_start + t + 1 > n0 (proposal.cpp:153-155)
+    const int64_t first = std::clamp<int64_t>((int64_t)k_.n0 - (int64_t)n_start, 0, Lw_);
+    const int k = Lw_ - (int)first;
+    if (k > 0) {
+        const double total = (double)cnt_local_ + k;
+        GemmBatch s{};
+        s.A = (const double* const*)Xip_;
+        s.B = (const double* const*)Xip_;
+        s.C = Sp_;
+        s.a_off = first * ld_;
+        s.b_off = first * ld_;
+        s.lda = ld_;
+        s.ldb = ld_;
+        s.ldc = ld_;
+        s.M = d_;
+        s.N = d_;
+        s.K = k;
+        s.alpha = 1.0 / total;
+        s.beta = (double)cnt_local_ / total;
+        s.tri_c_lower = 1;
+        gemm("syrk_moments", s, C, false, false);
+        launch_mean_update(mean_, ld_, Xi_, win_, ld_, C, d_, (int)first, k, (double)cnt_local_, stream_);
+        cnt_local_ += k;
+    }
+    if (record && cfg_.trace_eigen_projections)
+        launch_project_rows(Xi_, win_, ld_, C, Lw_, (int)first, d_, proj_, trace_pj_ + w * (size_t)C * Lw_ * 2,
+                            stream_);
+    lag_update(w);
+}
+
+void Engine::lag_update(size_t w) {
+    const int C = C_;
+    const double infl = k_.noise_infl();
+    // beta against the acceptance band (proposal.cpp:162-173)
+    launch_beta_update(beta_, nacc_, hist_rate_ + w * C, hist_beta_ + w * C, C, Lw_, k_.adapt_beta ? 1 : 0,
+                       k_.band_lo, k_.band_hi, k_.beta_adapt_factor, k_.beta_min, k_.beta_max, stream_);
+    const bool wants = k_.adapts_cov() || k_.adaptive_ref;
+    bool ref_moved = false;
+    if (wants && n_ >= k_.n0) {
+        const uint64_t count = cnt_local_ + cnt_g_;
+        const double wg = count ? (double)cnt_g_ / (double)count : 0.0;
+        const double wl = count ? (double)cnt_local_ / (double)count : 1.0;
+        if (k_.adapts_cov() && count >= 2) {
+            // blend -> covariance into the workspace factor, trace floor, POTRF (proposal.cpp:176-184)
+            timed_begin("blend_cov");
+            launch_blend_cov(Lnp_, Sg_, mg_, S_, mat_, mean_, ld_, wg, wl, mb_, ld_, C, d_, ld_, nullptr, 0.0, nullptr,
+                             stream_);
+            timed_end("blend_cov", 0.0);
+            launch_trace_floor(Lnp_, ld_, mb_, ld_, C, d_, tr_, try_, stream_);
+            DGB_CUDA(cudaMemsetAsync(status_, 0, C * sizeof(int), stream_));
+            timed_begin("potrf");
+            potrf_batched(Lnp_, ld_, d_, C, try_, status_, pw_, stream_);
+            timed_end("potrf", (double)C * d_ * (double)d_ * d_ / 3.0);
+            // jitter escalation for chains whose factorization failed (proposal.cpp:218-239)
+            std::vector<int> st(C), tf(C);
+            DGB_CUDA(cudaMemcpyAsync(st.data(), status_, C * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+            DGB_CUDA(cudaMemcpyAsync(tf.data(), try_, C * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+            DGB_CUDA(cudaStreamSynchronize(stream_));
+            std::vector<int> failing(C, 0);
+            bool any = false;
+            for (int c = 0; c < C; ++c) {
+                failing[c] = tf[c] && st[c];
+                any |= failing[c] != 0;
+            }
+            for (double eps = 1e-10; any && eps <= 1e-4; eps *= 100.0) {
+                DGB_CUDA(cudaMemcpyAsync(mask_, failing.data(), C * sizeof(int), cudaMemcpyHostToDevice, stream_));
+                launch_blend_cov(Lnp_, Sg_, mg_, S_, mat_, mean_, ld_, wg, wl, mb_, ld_, C, d_, ld_, mask_, eps, tr_,
+                                 stream_);
+                // failing chains restart from a clean status; the others keep status 0
+                std::vector<int> zero(C, 0);
+                DGB_CUDA(cudaMemcpyAsync(status_, zero.data(), C * sizeof(int), cudaMemcpyHostToDevice, stream_));
+                potrf_batched(Lnp_, ld_, d_, C, mask_, status_, pw_, stream_);
+                DGB_CUDA(cudaMemcpyAsync(st.data(), status_, C * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+                DGB_CUDA(cudaStreamSynchronize(stream_));
+                any = false;
+                for (int c = 0; c < C; ++c) {
+                    if (failing[c] && !st[c]) failing[c] = 0;
+                    any |= failing[c] != 0;
+                }
+            }
+            if (any) {
+                int c = 0;
+                while (!failing[c]) ++c;
+                double trh = 0.0;
+                DGB_CUDA(cudaMemcpy(&trh, tr_ + c, 8, cudaMemcpyDeviceToHost));
+                fail(Err::NotPositiveDefinite, "chain " + std::to_string(c0_ + c) +
+                                                   ": covariance not factorizable after jitter escalation (dim " +
+                                                   std::to_string(d_) + ", trace " + std::to_string(trh) + ")");
+            }
+            // final status: every tried chain factored
+            DGB_CUDA(cudaMemsetAsync(status_, 0, C * sizeof(int), stream_));
+            double qmax = -1.0;
+            if (k_.pcn_form()) {
+                // usable guard: 1/2 |L'^-1 (x - x_ref)|^2 / infl^2 <= 5 d (proposal.cpp:185-199)
+                launch_trsv(Lnp_, ld_, x_, k_.adaptive_ref ? xr_ : nullptr, ld_, nullptr, qtmp_, C, d_,
+                            0.5 / (infl * infl), try_, stream_);
+                qmax = 5.0 * d_;
+            }
+            launch_accept_factor(Lp_, Lnp_, try_, status_, qtmp_, qmax, C, usable_, stream_);
+            identity_ = false;
+        }
+        // adaptive reference point (proposal.cpp:206-208)
+        if (k_.adaptive_ref && n_ >= k_.n_ref_start && count > 0) {
+            if (!(k_.adapts_cov() && count >= 2))
+                launch_blend_mean(mg_, mean_, wg, wl, mb_, C, d_, ld_, stream_);
+            DGB_CUDA(cudaMemcpyAsync(xr_, mb_, (size_t)C * ld_ * 8, cudaMemcpyDeviceToDevice, stream_));
+            ref_moved = true;
+        }
+    }
+    if (ref_moved) refresh_g(xr_, gr_);
+    // quad with the current factor (proposal.cpp:211) and y for the next window's recursion
+    if (k_.pcn_form()) {
+        timed_begin("trsv");
+        launch_trsv(Lp_, ld_, x_, k_.adaptive_ref ? xr_ : nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl),
+                    nullptr, stream_);
+        timed_end("trsv", 0.0);
+    }
+    // G x re-anchored at every boundary so the step recursion never drifts
+    refresh_g(x_, g_);
+}
+
+void Engine::merge_batch() {
+    // proj/src/moments.cpp:51-88 with the P-chain sum pooled across GPUs
+    const uint64_t incoming = (uint64_t)P_ * cnt_local_;
+    if (incoming > 0) {
+        const double total = (double)(cnt_g_ + incoming);
+        const double keep = (double)cnt_g_ / total;
+        const double wp = (double)cnt_local_ / total;
+        timed_begin("merge");
+        launch_sum_chains(Ssum_, S_, mat_, C_, mat_, 1.0, stream_);
+        launch_sum_chains(Ssum_ + mat_, mean_, ld_, C_, ld_, 1.0, stream_);
+        if (comm_ && world_ > 1) comm_->allreduce_sum(Ssum_, mat_ + ld_, stream_);
+        launch_axpby(Sg_, Ssum_, mat_, wp, keep, stream_);
+        launch_axpby(mg_, Ssum_ + mat_, ld_, wp, keep, stream_);
+        timed_end("merge", 0.0);
+        cnt_g_ += incoming;
+        const double ct = (double)(cum_cnt_ + cnt_local_);
+        launch_cum_fold(cmean_, cdiag_, mean_, S_, mat_, C_, d_, ld_, (double)cum_cnt_ / ct, (double)cnt_local_ / ct,
+                        stream_);
+        cum_cnt_ += cnt_local_;
+    }
+    DGB_CUDA(cudaMemsetAsync(S_, 0, (size_t)C_ * mat_ * 8, stream_));
+    DGB_CUDA(cudaMemsetAsync(mean_, 0, (size_t)C_ * ld_ * 8, stream_));
+    cnt_local_ = 0;
+}
+
+void Engine::batch_stats(double& cov_err, double& mean_err, double& psrf) {
+    cov_err = mean_err = psrf = NAN;
+    if (cnt_g_ >= 2) {  // runner.cpp:249-256
+        launch_cov_error(Sg_, mg_, Ct_, d_, ld_, cov_part_, stream_);
+        std::vector<double> part(2 * (size_t)d_), mg(d_);
+        DGB_CUDA(cudaMemcpyAsync(part.data(), cov_part_, part.size() * 8, cudaMemcpyDeviceToHost, stream_));
+        DGB_CUDA(cudaMemcpyAsync(mg.data(), mg_, d_ * 8, cudaMemcpyDeviceToHost, stream_));
+        DGB_CUDA(cudaStreamSynchronize(stream_));
+        double num = 0.0, den = 0.0;
+        for (int i = 0; i < d_; ++i) {
+            num += part[2 * i];
+            den += part[2 * i + 1];
+        }
+        require(den > 0.0, Err::InvalidArgument, "cov_error: zero reference norm");
+        cov_err = std::sqrt(num / den);
+        double s = 0.0;
+        for (int i = 0; i < d_; ++i) {
+            const double df = mg[i] - tgt_.mean[i];
+            s += df * df;
+        }
+        mean_err = std::sqrt(s);
+    }
+    if (P_ >= 2) {  // runner.cpp:381-396 on (cum mean, cum diag) of every chain
+        std::vector<double> cm, cd;
+        const int64_t nloc = (int64_t)C_ * ld_;
+        if (comm_ && world_ > 1) {
+            // equal shards required for a plain all-gather; pad to the largest shard
+            const int64_t maxc = (P_ + world_ - 1) / world_;
+            if (!gather_) gather_ = dalloc<double>(allocs_, (size_t)2 * maxc * ld_ * (world_ + 1));
+            double* src = gather_;
+            double* dst = gather_ + 2 * maxc * ld_;
+            DGB_CUDA(cudaMemsetAsync(src, 0, 2 * maxc * ld_ * 8, stream_));
+            DGB_CUDA(cudaMemcpyAsync(src, cmean_, nloc * 8, cudaMemcpyDeviceToDevice, stream_));
+            DGB_CUDA(cudaMemcpyAsync(src + maxc * ld_, cdiag_, nloc * 8, cudaMemcpyDeviceToDevice, stream_));
+            comm_->allgather(src, dst, 2 * maxc * ld_, stream_);
+            std::vector<double> all((size_t)world_ * 2 * maxc * ld_);
+            DGB_CUDA(cudaMemcpyAsync(all.data(), dst, all.size() * 8, cudaMemcpyDeviceToHost, stream_));
+            DGB_CUDA(cudaStreamSynchronize(stream_));
+            for (int r = 0; r < world_; ++r) {
+                const int cr = (int)((int64_t)(r + 1) * P_ / world_ - (int64_t)r * P_ / world_);
+                const double* base = all.data() + (size_t)r * 2 * maxc * ld_;
+                cm.insert(cm.end(), base, base + (size_t)cr * ld_);
+                cd.insert(cd.end(), base + maxc * ld_, base + maxc * ld_ + (size_t)cr * ld_);
+            }
+        } else {
+            cm.resize(nloc);
+            cd.resize(nloc);
+            DGB_CUDA(cudaMemcpyAsync(cm.data(), cmean_, nloc * 8, cudaMemcpyDeviceToHost, stream_));
+            DGB_CUDA(cudaMemcpyAsync(cd.data(), cdiag_, nloc * 8, cudaMemcpyDeviceToHost, stream_));
+            DGB_CUDA(cudaStreamSynchronize(stream_));
+        }
+        std::vector<const double*> means, diags;
+        for (int c = 0; c < P_; ++c) {
+            means.push_back(cm.data() + (size_t)c * ld_);
+            diags.push_back(cd.data() + (size_t)c * ld_);
+        }
+        try {
+            psrf = psrf_max(means, diags, d_, cum_cnt_);
+        } catch (const Error& e) {
+            if (e.code != Err::ZeroWithinVariance && e.code != Err::InvalidArgument) throw;
+            psrf = NAN;
+        }
+    }
+}
+
+void Engine::collect_batch_host(size_t windows) {
+    // beta / acceptance histories and the traces of this batch (runner.cpp:365-371)
+    const int C = C_;
+    std::vector<double> rate(windows * C), beta(windows * C);
+    DGB_CUDA(cudaMemcpyAsync(rate.data(), hist_rate_, rate.size() * 8, cudaMemcpyDeviceToHost, stream_));
+    DGB_CUDA(cudaMemcpyAsync(beta.data(), hist_beta_, beta.size() * 8, cudaMemcpyDeviceToHost, stream_));
+    std::vector<double> lp, pj;
+    if (cfg_.record_traces) {
+        lp.resize(windows * C * (size_t)Lw_);
+        DGB_CUDA(cudaMemcpyAsync(lp.data(), trace_lp_, lp.size() * 8, cudaMemcpyDeviceToHost, stream_));
+        if (cfg_.trace_eigen_projections) {
+            pj.resize(windows * C * (size_t)Lw_ * 2);
+            DGB_CUDA(cudaMemcpyAsync(pj.data(), trace_pj_, pj.size() * 8, cudaMemcpyDeviceToHost, stream_));
+        }
+    }
+    DGB_CUDA(cudaStreamSynchronize(stream_));
+    for (size_t w = 0; w < windows; ++w)
+        for (int c = 0; c < C; ++c) {
+            beta_hist_[c].push_back(beta[w * C + c]);
+            acc_hist_[c].push_back(rate[w * C + c]);
+        }
+    if (!cfg_.record_traces) return;
+    for (size_t w = 0; w < windows; ++w) {
+        const uint64_t ns = window_n_start_[w];
+        for (int t = 0; t < Lw_; ++t) {
+            const uint64_t n = ns + t + 1;
+            if (!(n > k_.n0 && (n - k_.n0 - 1) % cfg_.trace_thin == 0)) continue;
+            for (int c = 0; c < C; ++c) {
+                const size_t idx = (w * C + c) * (size_t)Lw_ + t;
+                traces_[c][0].push_back(lp[idx]);
+                if (cfg_.trace_eigen_projections) {
+                    traces_[c][1].push_back(pj[idx * 2]);
+                    traces_[c][2].push_back(pj[idx * 2 + 1]);
+                }
+            }
+        }
+    }
+}
+
+double Engine::run_batches_timed(int k) {
+    const size_t M = cfg_.intervals_per_batch;
+    window_n_start_.assign(M, 0);
+    cudaEvent_t a, b;
+    DGB_CUDA(cudaEventCreate(&a));
+    DGB_CUDA(cudaEventCreate(&b));
+    DGB_CUDA(cudaStreamSynchronize(stream_));
+    DGB_CUDA(cudaEventRecord(a, stream_));
+    for (int i = 0; i < k; ++i) {
+        for (size_t m = 0; m < M; ++m) window(m, false);
+        merge_batch();
+        ++batches_done_;
+    }
+    DGB_CUDA(cudaEventRecord(b, stream_));
+    DGB_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    DGB_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
+}
+
+RunResult Engine::run() {  // runner.cpp:216-279
+    const auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    const size_t M = cfg_.intervals_per_batch;
+    window_n_start_.assign(M, 0);
+    std::string reason;
+    for (;;) {
+        const uint64_t iters = (uint64_t)P_ * M * batches_done_ * k_.n_lag;
+        if (cfg_.max_samples && iters >= *cfg_.max_samples) {
+            reason = "max_samples";
+            break;
+        }
+        if (batches_done_ >= cfg_.max_batches) {
+            reason = "batch_cap";
+            break;
+        }
+        if (cfg_.max_wall_seconds && elapsed() >= *cfg_.max_wall_seconds) {
+            reason = "wall_time";
+            break;
+        }
+        const auto b0 = std::chrono::steady_clock::now();
+        for (size_t m = 0; m < M; ++m) window(m, cfg_.record_traces);
+        merge_batch();
+        collect_batch_host(M);
+        ++batches_done_;
+        double ce, me, ps;
+        batch_stats(ce, me, ps);
+        batch_seconds_.push_back(
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - b0).count());
+        cov_hist_.push_back(ce);
+        mean_hist_.push_back(me);
+        psrf_hist_.push_back(ps);
+        if (cfg_.psrf_tol && std::isfinite(ps) && ps <= *cfg_.psrf_tol) {
+            reason = "psrf";
+            break;
+        }
+        if (cfg_.cov_tol && std::isfinite(ce) && ce <= *cfg_.cov_tol) {
+            reason = "cov_tol";
+            break;
+        }
+        if (cfg_.mean_tol && std::isfinite(me) && me <= *cfg_.mean_tol) {
+            reason = "mean_tol";
+            break;
+        }
+    }
+    return build_result(reason, elapsed());
+}
+
+RunResult Engine::build_result(const std::string& reason, double wall) {  // runner.cpp:459-489
+    RunResult r;
+    r.target_kind = tkind_name(tgt_.kind);
+    r.kernel_name = kkind_name(k_.kind);
+    r.dim = d_;
+    r.chains = P_;
+    r.intervals_per_batch = cfg_.intervals_per_batch;
+    r.n_lag = k_.n_lag;
+    r.master_seed = cfg_.master_seed;
+    r.total_samples = (uint64_t)P_ * cfg_.intervals_per_batch * batches_done_ * k_.n_lag;
+    r.batches = batches_done_;
+    r.wall_seconds = wall;
+    r.batch_seconds = batch_seconds_;
+    r.stop_reason = reason;
+    r.accumulated_samples = cnt_g_;
+    std::vector<double> sg(mat_), mg(ld_);
+    DGB_CUDA(cudaMemcpyAsync(sg.data(), Sg_, mat_ * 8, cudaMemcpyDeviceToHost, stream_));
+    DGB_CUDA(cudaMemcpyAsync(mg.data(), mg_, ld_ * 8, cudaMemcpyDeviceToHost, stream_));
+    DGB_CUDA(cudaStreamSynchronize(stream_));
+    r.global_mean.assign(mg.begin(), mg.begin() + d_);
+    r.global_cov = Mat(d_, d_);
+    for (int i = 0; i < d_; ++i)
+        for (int j = 0; j <= i; ++j) {
+            const double v = sg[(size_t)i * ld_ + j] - mg[i] * mg[j];  // covariance(), moments.cpp:90-101
+            r.global_cov(i, j) = r.global_cov(j, i) = v;
+        }
+    r.final_cov_error = cov_hist_.empty() ? NAN : cov_hist_.back();
+    r.final_mean_error = mean_hist_.empty() ? NAN : mean_hist_.back();
+    r.final_max_psrf = psrf_hist_.empty() ? NAN : psrf_hist_.back();
+    r.cov_error_history = cov_hist_;
+    r.mean_error_history = mean_hist_;
+    r.psrf_history = psrf_hist_;
+    r.functional_names = fnames_;
+    // histories of every chain (gathered across ranks); traces of the local chains only
+    r.beta_history.assign(P_, {});
+    r.acceptance_history.assign(P_, {});
+    r.traces.assign(P_, std::vector<std::vector<double>>(fnames_.size()));
+    const size_t nb = beta_hist_.empty() ? 0 : beta_hist_[0].size();
+    if (comm_ && world_ > 1) {
+        const int64_t maxc = (P_ + world_ - 1) / world_;
+        const int64_t blk = 2 * maxc * (int64_t)nb;
+        std::vector<double> mine(blk, 0.0);
+        for (int c = 0; c < C_; ++c)
+            for (size_t j = 0; j < nb; ++j) {
+                mine[c * nb + j] = beta_hist_[c][j];
+                mine[maxc * nb + c * nb + j] = acc_hist_[c][j];
+            }
+        double* dsrc = dalloc<double>(allocs_, blk);
+        double* ddst = dalloc<double>(allocs_, blk * world_);
+        DGB_CUDA(cudaMemcpyAsync(dsrc, mine.data(), blk * 8, cudaMemcpyHostToDevice, stream_));
+        comm_->allgather(dsrc, ddst, blk, stream_);
+        std::vector<double> all(blk * world_);
+        DGB_CUDA(cudaMemcpyAsync(all.data(), ddst, all.size() * 8, cudaMemcpyDeviceToHost, stream_));
+        DGB_CUDA(cudaStreamSynchronize(stream_));
+        for (int rk = 0; rk < world_; ++rk) {
+            const int base = (int)((int64_t)rk * P_ / world_);
+            const int cr = (int)((int64_t)(rk + 1) * P_ / world_) - base;
+            for (int c = 0; c < cr; ++c) {
+                const double* b = all.data() + rk * blk + c * nb;
+                r.beta_history[base + c].assign(b, b + nb);
+                r.acceptance_history[base + c].assign(b + maxc * nb, b + maxc * nb + nb);
+            }
+        }
+    } else {
+        for (int c = 0; c < C_; ++c) {
+            r.beta_history[c0_ + c] = beta_hist_[c];
+            r.acceptance_history[c0_ + c] = acc_hist_[c];
+        }
+    }
+    for (int c = 0; c < C_; ++c) r.traces[c0_ + c] = std::move(traces_[c]);
+    return r;
+}
+
+}  // namespace dgb

@@ -1,0 +1,154 @@
+// engine.hpp — the B200 sampler engine (C++ host driver over sm_100a kernels).
+//
+// Mirrors the reference Engine (proj/src/runner.cpp:122-279): P chains, batches
+// of M lag windows, a frozen global snapshot per batch, merge at the barrier,
+// convergence diagnostics and OR-composed stopping rules. The per-chain loop
+// of the reference (mh_step x n_lag, lag_update) becomes a per-window sequence
+// of batched kernels over all local chains on one CUDA stream:
+//
+//   noise    W = Philox normals                 (launch_normals)
+//   TRMM     Xi = s * W * L^T                   (gemm_f64, tri B)
+//   target   H = Xi * G^T                       (gemm_f64, all chains one GEMM)
+//   steps    n_lag MH steps, O(d) each          (launch_mh_window)
+//   moments  S = a X^T X + b S, mean            (gemm_f64 tri C + launch_mean_update)
+//   adapt    beta, blend -> POTRF (jitter) -> usable guard -> swap, x_ref,
+//            y = L^-1(x - x_ref), quad, g = G x (trsv, potrf_batched, gemm_f64)
+//
+// and per batch: local moment sum -> all-reduce (multi-GPU) -> merge,
+// cumulative PSRF statistics, cov/mean error.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "comm.hpp"
+#include "gemm_f64.cuh"
+#include "host.hpp"
+#include "kernels.cuh"
+
+namespace dgb {
+
+struct KernelStat {
+    double ms = 0.0;
+    double flops = 0.0;
+    uint64_t launches = 0;
+};
+
+class Engine {
+public:
+    Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> comm);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    RunResult run();                 // full run with the reference's stopping rules
+    double run_batches_timed(int k);  // k batches, no stopping rules; device ms (CUDA events)
+
+    // profiling: per-kernel-class CUDA-event timing (adds events around launches)
+    void set_profiling(bool on) { profiling_ = on; }
+    const std::map<std::string, KernelStat>& stats();
+
+    // debug capture for parity tests: W of every window, accept bits / log ratios of every step
+    void set_capture(bool on) { capture_ = on; }
+    const std::vector<double>& captured_w(int chain) const { return cap_w_.at(chain); }
+    const std::vector<double>& captured_ratio(int chain) const { return cap_ratio_.at(chain); }
+    const std::vector<uint8_t>& captured_accept(int chain) const { return cap_acc_.at(chain); }
+
+    cudaStream_t stream() const { return stream_; }
+    int local_chains() const { return C_; }
+    int dim() const { return d_; }
+    int n_lag() const { return Lw_; }
+    double flops_per_batch() const;  // algorithmic FP64 flops of one batch (all local chains)
+
+private:
+    void upload_target();
+    void init_chains();
+    void window(size_t win_in_batch, bool record);
+    void lag_update(size_t win_in_batch);
+    void merge_batch();
+    void batch_stats(double& cov_err, double& mean_err, double& psrf);
+    void collect_batch_host(size_t windows);
+    void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, GemmShape sh = GemmShape::Big);
+    void refresh_g(const double* vec, double* out);  // out[c] = G * vec[c]
+    void timed_begin(const char* name);
+    void timed_end(const char* name, double flops);
+    void resolve_events();
+    RunResult build_result(const std::string& reason, double wall);
+
+    HostTarget tgt_;
+    RunCfg cfg_;
+    KernelCfg k_;
+    std::shared_ptr<Comm> comm_;
+    int rank_ = 0, world_ = 1;
+    int d_ = 0, Lw_ = 0, C_ = 0, P_ = 0, c0_ = 0;
+    int64_t ld_ = 0, win_ = 0, mat_ = 0;
+    bool twisted_ = false, identity_ = true;
+    cudaStream_t stream_ = nullptr;
+
+    // device memory
+    std::vector<void*> allocs_;
+    double* G_ = nullptr;      // d x ld
+    double* Ct_ = nullptr;     // d x d analytic covariance
+    double* inv_eig_ = nullptr;
+    double* bcoef_ = nullptr;
+    double* proj_ = nullptr;   // 2 x ld
+    double *L_ = nullptr, *Lw2_ = nullptr, *S_ = nullptr;  // C x (d x ld)
+    double *W_ = nullptr, *Xi_ = nullptr, *H_ = nullptr;   // C x (Lw x ld)
+    double *x_ = nullptr, *g_ = nullptr, *y_ = nullptr, *xr_ = nullptr, *gr_ = nullptr;
+    double *mean_ = nullptr, *cmean_ = nullptr, *cdiag_ = nullptr, *mb_ = nullptr;
+    double *logpi_ = nullptr, *quad_ = nullptr, *beta_ = nullptr, *tr_ = nullptr, *qtmp_ = nullptr;
+    uint64_t *nacc_ = nullptr, *uctr_ = nullptr;
+    int *status_ = nullptr, *try_ = nullptr, *usable_ = nullptr, *mask_ = nullptr;
+    PhiloxKey *nkeys_ = nullptr, *ukeys_ = nullptr, *ikeys_ = nullptr;
+    double **Lp_ = nullptr, **Lnp_ = nullptr;  // factor / workspace pointer arrays (swapped on device)
+    double **Wp_ = nullptr, **Xip_ = nullptr, **Sp_ = nullptr, **Gp_ = nullptr, **Hp_ = nullptr;
+    double **xp_ = nullptr, **gp_ = nullptr, **xrp_ = nullptr, **grp_ = nullptr;
+    double *Sg_ = nullptr, *mg_ = nullptr, *Ssum_ = nullptr;  // global snapshot, reduction buffer
+    double *trace_lp_ = nullptr, *trace_pj_ = nullptr;      // per batch: M x C x Lw (x2)
+    double *hist_rate_ = nullptr, *hist_beta_ = nullptr;    // per batch: M x C
+    double* cov_part_ = nullptr;                              // d x 2
+    double* gather_ = nullptr;                                // PSRF all-gather buffer
+    PotrfWork pw_{};
+    // pinned host staging
+    double* h_stage_ = nullptr;
+    size_t h_stage_len_ = 0;
+
+    // host-side counters (uniform across chains)
+    uint64_t n_ = 0;          // iterations per chain
+    uint64_t nctr_ = 0;       // noise stream draw counter
+    uint64_t cnt_local_ = 0;  // samples in the batch accumulators (per chain)
+    uint64_t cnt_g_ = 0;      // global moments count
+    uint64_t cum_cnt_ = 0;    // cumulative per-chain count
+    size_t batches_done_ = 0;
+    std::vector<uint64_t> window_n_start_;  // per window of the current batch
+
+    // result accumulation
+    std::vector<double> batch_seconds_, cov_hist_, mean_hist_, psrf_hist_;
+    std::vector<std::vector<double>> beta_hist_, acc_hist_;  // local chains
+    std::vector<std::vector<std::vector<double>>> traces_;   // local chains x functionals
+    std::vector<std::string> fnames_;
+
+    // profiling
+    bool profiling_ = false;
+    struct Pending {
+        std::string name;
+        cudaEvent_t a, b;
+        double flops;
+    };
+    std::vector<Pending> pending_;
+    std::vector<cudaEvent_t> event_pool_;
+    std::map<std::string, KernelStat> stats_;
+    cudaEvent_t cur_a_ = nullptr;
+
+    bool capture_ = false;
+    std::vector<std::vector<double>> cap_w_, cap_ratio_;
+    std::vector<std::vector<uint8_t>> cap_acc_;
+    double* dbg_ratio_ = nullptr;
+    uint8_t* dbg_acc_ = nullptr;
+};
+
+}  // namespace dgb

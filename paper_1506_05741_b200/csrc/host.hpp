@@ -1,0 +1,131 @@
+// host.hpp — host-side pieces behind the diam.h ABI that are not on the GPU
+// hot path: synthetic targets (construction, DIAMTGT v1 IO, scalar log
+// density), post-hoc trace diagnostics, the quadratic fit, error codes, and
+// the run configuration / result types shared with the engine.
+#pragma once
+
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace dgb {
+
+// Error codes in diam_status order (proj/include/diam/error.hpp:8-19 semantics).
+enum class Err { InvalidArgument = 1, InvalidDimension, DimensionMismatch, NotPositiveDefinite,
+                 SingularDiagonal, ConvergenceFailure, DegenerateTrace, ZeroWithinVariance,
+                 UnequalBatchSizes, Io, Unknown };
+
+struct Error : std::runtime_error {
+    Error(Err c, const std::string& what) : std::runtime_error(what), code(c) {}
+    Err code;
+};
+[[noreturn]] inline void fail(Err c, const std::string& w) { throw Error(c, w); }
+inline void require(bool ok, Err c, const std::string& w) {
+    if (!ok) fail(c, w);
+}
+
+using Vec = std::vector<double>;
+
+// Dense row-major square helpers (host).
+struct Mat {
+    size_t rows = 0, cols = 0;
+    Vec a;
+    Mat() = default;
+    Mat(size_t r, size_t c) : rows(r), cols(c), a(r * c, 0.0) {}
+    double& operator()(size_t i, size_t j) { return a[i * cols + j]; }
+    double operator()(size_t i, size_t j) const { return a[i * cols + j]; }
+};
+
+// ---------------------------------------------------------------- targets
+enum class TKind { Pi1 = 0, Pi2, Pi3, Pi4, Pi5, Pi6 };
+const char* tkind_name(TKind k);
+TKind tkind_from_name(const std::string& s);
+
+struct HostTarget {
+    TKind kind = TKind::Pi1;
+    size_t dim = 0;
+    uint64_t seed = 0;
+    double sigma2 = 0.0, twist_b = 0.0;
+    Mat precision;   // Gaussian kinds
+    Mat covariance;  // analytic
+    Mat eigvecs;     // columns, ascending eigenvalues
+    Vec eigvals, b_coeffs, mean, eigen_mean, eigen_var;
+    bool twisted() const { return kind == TKind::Pi5 || kind == TKind::Pi6; }
+    double log_density(const double* x, size_t n) const;
+};
+
+HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, double twist_b);
+void save_target(const HostTarget& t, const std::string& path);
+HostTarget load_target(const std::string& path);
+
+// ---------------------------------------------------------------- diagnostics
+Vec acf(const double* x, size_t n, size_t max_lag);
+double iact(const double* x, size_t n);
+double ess(const double* x, size_t n);
+struct QuadFit {
+    double coeffs[3] = {0, 0, 0};
+    double quad_share = 0.0, rss = 0.0;
+};
+QuadFit fit_quadratic(const double* xs, const double* ys, size_t n);
+// max_i sqrt(R_i) from per-chain cumulative means / second-moment diagonals
+// (proj/src/diagnostics.cpp:72-119); throws ZeroWithinVariance / InvalidArgument.
+double psrf_max(const std::vector<const double*>& means, const std::vector<const double*>& diags, size_t d,
+                uint64_t n_per_chain);
+
+// ---------------------------------------------------------------- run config / result
+enum class KKind { RW = 0, PCN, AM, DIAM };
+const char* kkind_name(KKind k);
+KKind kkind_from_name(const std::string& s);
+
+struct KernelCfg {
+    KKind kind = KKind::DIAM;
+    size_t dim = 0;
+    double beta_init = 0.0, inflation = 1.0;
+    bool adaptive_ref = false;
+    size_t n_lag = 0;
+    double band_lo = 0.0, band_hi = 0.0;
+    uint64_t n0 = 0, n_ref_start = 0;
+    double beta_adapt_factor = 1.1, beta_min = 1e-6, beta_max = 1.0;
+    bool adapt_beta = true, use_explicit_inverse = false;
+    bool pcn_form() const { return kind == KKind::PCN || kind == KKind::DIAM; }
+    bool adapts_cov() const { return kind == KKind::AM || kind == KKind::DIAM; }
+    double noise_infl() const { return kind == KKind::DIAM ? inflation : 1.0; }
+    static KernelCfg defaults(KKind k, size_t dim);  // proj/src/proposal.cpp:24-45
+};
+
+struct RunCfg {
+    KernelCfg kernel;
+    size_t chains = 1, intervals_per_batch = 1, max_batches = 100;
+    std::optional<double> cov_tol, mean_tol, psrf_tol, max_wall_seconds;
+    std::optional<uint64_t> max_samples;
+    double init_dispersion = 1.0;
+    uint64_t master_seed = 0;
+    bool record_traces = true;
+    size_t trace_thin = 1;
+    bool trace_eigen_projections = true;
+    std::string checkpoint_path;
+    size_t threads = 0;
+};
+void validate_run_cfg(const RunCfg& c, const HostTarget& t);  // proj/src/runner.cpp:507-533
+
+struct RunResult {
+    std::string target_kind, kernel_name;
+    size_t dim = 0, chains = 0, intervals_per_batch = 0, n_lag = 0;
+    uint64_t master_seed = 0, total_samples = 0, accumulated_samples = 0;
+    size_t batches = 0;
+    double wall_seconds = 0.0;
+    Vec batch_seconds;
+    std::string stop_reason;
+    Vec global_mean;
+    Mat global_cov;
+    double final_cov_error = 0, final_mean_error = 0, final_max_psrf = 0;
+    Vec cov_error_history, mean_error_history, psrf_history;
+    std::vector<Vec> beta_history, acceptance_history;  // [chain][boundary]
+    std::vector<std::string> functional_names;
+    std::vector<std::vector<Vec>> traces;  // [chain][functional]
+};
+std::string result_to_json(const RunResult& r);
+
+}  // namespace dgb

@@ -1,0 +1,134 @@
+// kernels.cuh — device kernels of the B200 DIAM engine (launch wrappers).
+//
+// Data layout in HBM (per GPU, C local chains, dimension d, ld = pad_ld(d),
+// window length Lw = n_lag):
+//   target G        d x ld        precision P (Gaussian) or V^T (twisted), shared
+//   factor L_c      d x ld        lower factor, zero upper part (one per chain)
+//   factor' L'_c    d x ld        refactor workspace (blend -> POTRF in place)
+//   moments S_c     d x ld        raw second moment, lower triangle (per chain)
+//   window W_c      Lw x ld       standard normals of the window
+//   window Xi_c     Lw x ld       increments s*W*L^T; overwritten in place by
+//                                 the post-step states X (SYRK input)
+//   window H_c      Lw x ld       G * xi rows (target contraction of Xi)
+//   vectors         C x ld        x, g = G x, y = L^-1 (x - x_ref), x_ref, g_ref,
+//                                 local mean, cumulative mean / diag
+// All pad columns [d, ld) stay zero; every kernel writes only [0, d).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace dgb {
+
+// ---------------------------------------------------------------- draws
+// W[c][r][i] = normal(key_c, start + r*d + i), r < rows (every chain is at the same
+// noise-stream position); if Xi is non-null also Xi = (beta_c * infl) * W, which is
+// exactly tri_matvec(I, w) * scale (identity-factor fast path, bit-exact).
+void launch_normals(double* W, double* Xi, int64_t chain_stride, int chains, int rows, int d,
+                    int64_t ld, const PhiloxKey* keys, uint64_t start, const double* beta,
+                    double infl, cudaStream_t s);
+// out[c][i] = scale * normal(key_c, start + i), i < n   (init dispersion draws)
+void launch_normal_vec(double* out, int64_t stride, int chains, int n, const PhiloxKey* keys,
+                       uint64_t start, double scale, cudaStream_t s);
+// kernel-level parity entry: raw draws of one stream
+void launch_draws(int kind, double* out_f64, uint64_t* out_u64, int64_t n, PhiloxKey key,
+                  uint64_t start, cudaStream_t s);
+
+// ---------------------------------------------------------------- MH window
+struct StepParams {
+    int d, n_lag, chains;
+    int64_t ld, win_stride;
+    const double* W;
+    double* Xi;       // in: increments; out: post-step states (row t <- x after step t)
+    const double* H;  // G * increments
+    double* x;
+    double* g;
+    double* y;
+    const double* xr;  // null: zero reference point
+    const double* gr;
+    double* log_pi;
+    double* quad;
+    const double* beta;
+    uint64_t* n_accepted;
+    const PhiloxKey* ukeys;
+    uint64_t* uctr;  // advanced by n_lag
+    double infl;
+    int pcn;  // pCN-form kernels (pCN, DIAM)
+    const double* inv_eig;  // twisted: 1/sigma^2 (len d)
+    const double* bcoef;    // twisted: twist coefficients (len d)
+    double* trace_lp;       // [chain][n_lag], nullable
+    uint8_t* accept_out;    // [chain][n_lag], nullable
+    double* log_ratio_out;  // [chain][n_lag], nullable (parity tests)
+};
+void launch_mh_window(const StepParams& p, bool twisted, cudaStream_t s);
+
+// ---------------------------------------------------------------- moments
+// S_c/mean_c running update with the window's accepted rows [k_off, n_lag):
+// mean <- (n mean + sum_rows x) / (n + k). (The S part is a SYRK through gemm_f64.)
+void launch_mean_update(double* mean, int64_t mean_stride, const double* X, int64_t win_stride,
+                        int64_t ld, int chains, int d, int k_off, int k, double n_prev, cudaStream_t s);
+// Blend (count weights) and covariance, written as a lower matrix with zero upper part
+// into C_out (the refactor workspace); blended mean -> mb. jitter_eps > 0 adds
+// eps*trace_c/d on the diagonal (trace from tr[c]). mask: chains to process.
+void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg,
+                      const double* Sl, int64_t sl_stride, const double* ml, int64_t ml_stride,
+                      double wg, double wl, double* mb, int64_t mb_stride, int chains, int d,
+                      int64_t ld, const int* mask, double jitter_eps, const double* tr,
+                      cudaStream_t s);
+// tr[c] = sum_i C_ii (sequential order); try[c] = trace > 1e-12(1 + mb.mb) && finite
+void launch_trace_floor(double* const* Cm, int64_t ld, const double* mb, int64_t mb_stride,
+                        int chains, int d, double* tr, int* try_flag, cudaStream_t s);
+// Merge helpers (proj/src/moments.cpp:51-88)
+void launch_sum_chains(double* out, const double* in, int64_t chain_stride, int chains, int64_t n,
+                       double weight, cudaStream_t s);
+void launch_axpby(double* y, const double* x, int64_t n, double a, double b, cudaStream_t s);
+// cum mean/diag fold (merge_into restricted to the PSRF inputs)
+void launch_cum_fold(double* cmean, double* cdiag, const double* lmean, const double* S,
+                     int64_t s_stride, int chains, int d, int64_t ld, double keep, double add,
+                     cudaStream_t s);
+// cov/mean error partial sums for cov_error (proj/src/diagnostics.cpp:121-142)
+void launch_cov_error(const double* Sg, const double* mg, const double* Ctrue, int d, int64_t ld,
+                      double* out2, cudaStream_t s);
+
+// ---------------------------------------------------------------- triangular
+// y_c = L_c^{-1} (x_c - xr_c); quad_c = half_inv_infl2 * sum y^2 (pcn) and, if
+// qmax >= 0, usable_c &= (0.5*y.y/infl^2 <= qmax). mask: chains to process.
+void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr, int64_t vstride,
+                 double* y, double* quad_out, int chains, int d, double half_inv_infl2,
+                 const int* mask, cudaStream_t s);
+// Cholesky of the lower part of A_c (in place), blocked right-looking with the
+// diagonal blocks factored in shared memory, TRSM and SYRK through gemm_f64.
+// status[c] = 0 ok, 1 not positive definite. Only chains with mask[c] != 0.
+struct PotrfWork {
+    double* inv;  // chains x 64 x 64 inverse diagonal blocks
+    double** inv_ptrs;
+};
+void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status,
+                   PotrfWork& w, cudaStream_t s);
+
+// ---------------------------------------------------------------- lag update
+// beta adaptation + rate (proj/src/proposal.cpp:163-173)
+void launch_beta_update(double* beta, uint64_t* n_acc, double* rate_out, double* beta_out,
+                        int chains, int n_lag, int adapt, double lo, double hi, double factor,
+                        double bmin, double bmax, cudaStream_t s);
+// usable[c] = try[c] && status[c]==0 && (qcheck[c] <= qmax); swap factor pointers where usable
+void launch_accept_factor(double** L, double** Lnew, const int* try_flag, const int* status,
+                          const double* q, double qmax, int chains, int* usable, cudaStream_t s);
+// L_c = I
+void launch_set_identity(double* base, int64_t mat_stride, int chains, int d, int64_t ld, cudaStream_t s);
+// log pi from x and g = G x (Gaussian: -1/2 x.g; twisted: -1/2 sum twist(g)^2 / sigma^2)
+void launch_eval_logpi(const double* x, const double* g, const double* inv_eig, const double* bcoef,
+                       bool twisted, double* out, int chains, int d, int64_t ld, cudaStream_t s);
+// mb_c = wg*mg + wl*ml_c
+void launch_blend_mean(const double* mg, const double* ml, double wg, double wl, double* mb, int chains,
+                       int d, int64_t ld, cudaStream_t s);
+// out[c][t][0..1] = proj[0..1] . X_c[t], t in [t0, rows)
+void launch_project_rows(const double* X, int64_t win_stride, int64_t ld, int chains, int rows, int t0,
+                         int d, const double* proj, double* out, cudaStream_t s);
+void launch_copy_vecs(double* dst, const double* src, int64_t n, const int* mask_per_chain,
+                      int64_t stride, int chains, cudaStream_t s);
+
+}  // namespace dgb

@@ -1,0 +1,576 @@
+// linalg.cu — batched triangular solve, blocked Cholesky, moment and lag-update kernels.
+#include <cmath>
+
+#include "gemm_f64.cuh"
+#include "kernels.cuh"
+
+namespace dgb {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ------------------------------------------------------------------ moments
+__global__ void mean_update_kernel(double* mean, int64_t mean_stride, const double* X, int64_t win_stride,
+                                   int64_t ld, int d, int k_off, int k, double keep, double add) {
+    const int c = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d) return;
+    const double* Xc = X + c * win_stride + (int64_t)k_off * ld + i;
+    double s = 0.0;
+    for (int r = 0; r < k; ++r) s += Xc[(int64_t)r * ld];
+    double* m = mean + c * mean_stride + i;
+    *m = keep * *m + add * s;
+}
+
+// C = wg*Sg + wl*Sl - mb mb^T on the lower triangle, 0 above; optional jitter on the diagonal.
+__global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const double* mg, const double* Sl,
+                                 int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl,
+                                 double* mb, int64_t mb_stride, int d, int64_t ld, const int* mask,
+                                 double jitter_eps, const double* tr) {
+    const int c = blockIdx.z;
+    if (mask && !mask[c]) return;
+    const int i = blockIdx.y;  // row
+    double* Crow = C_out[c] + (int64_t)i * ld;
+    const double* Sgr = Sg + (int64_t)i * ld;
+    const double* Slr = Sl + c * sl_stride + (int64_t)i * ld;
+    const double* mlc = ml + c * ml_stride;
+    // blended mean (proj/src/moments.cpp:44); every row block recomputes what it needs
+    const double mbi = wg * mg[i] + wl * mlc[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) mb[c * mb_stride + i] = mbi;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x) {
+        double v = 0.0;
+        if (j <= i) {
+            const double mbj = wg * mg[j] + wl * mlc[j];
+            const double s = wg * Sgr[j] + wl * Slr[j];  // :45-46
+            v = s - mbi * mbj;                         // covariance :90-101 (S exactly symmetric)
+            if (j == i && jitter_eps > 0.0) v += jitter_eps * (tr[c] / (double)d);  // proposal.cpp:229-231
+        }
+        Crow[j] = v;
+    }
+}
+
+__global__ void trace_floor_kernel(double* const* Cm, int64_t ld, const double* mb, int64_t mb_stride, int d,
+                                   double* tr, int* try_flag) {
+    const int c = blockIdx.x;
+    const int lane = threadIdx.x;
+    const double* C = Cm[c];
+    const double* m = mb + c * mb_stride;
+    double t = 0.0, mm = 0.0;
+    for (int i = lane; i < d; i += 32) {
+        t += C[(int64_t)i * ld + i];
+        mm += m[i] * m[i];
+    }
+    t = warp_sum(t);
+    mm = warp_sum(mm);
+    if (lane == 0) {
+        tr[c] = t;
+        const double floor = 1e-12 * (1.0 + mm);  // proj/src/proposal.cpp:181
+        try_flag[c] = (t > floor && isfinite(t)) ? 1 : 0;
+    }
+}
+
+__global__ void sum_chains_kernel(double* out, const double* in, int64_t chain_stride, int chains, int64_t n,
+                                  double weight) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < chains; ++c) s += in[c * chain_stride + e];
+        out[e] = weight * s;
+    }
+}
+
+__global__ void axpby_kernel(double* y, const double* x, int64_t n, double a, double b) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        y[e] = b * y[e] + a * x[e];
+}
+
+__global__ void cum_fold_kernel(double* cmean, double* cdiag, const double* lmean, const double* S,
+                                int64_t s_stride, int d, int64_t ld, double keep, double add) {
+    const int c = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d) return;
+    const int64_t v = c * ld + i;
+    cmean[v] = keep * cmean[v] + add * lmean[v];
+    cdiag[v] = keep * cdiag[v] + add * S[c * s_stride + (int64_t)i * ld + i];
+}
+
+// partial sums for ||C_emp - C*||_F^2 and ||C*||_F^2 over the full symmetric matrix
+__global__ void cov_error_kernel(const double* Sg, const double* mg, const double* Ct, int d, int64_t ld,
+                                 double* partial) {
+    double num = 0.0, den = 0.0;
+    const int i = blockIdx.x;
+    for (int j = threadIdx.x; j <= i; j += blockDim.x) {
+        const double emp = Sg[(int64_t)i * ld + j] - mg[i] * mg[j];
+        const double t = Ct[(int64_t)i * d + j];
+        const double t2 = Ct[(int64_t)j * d + i];
+        num += (emp - t) * (emp - t);
+        den += t * t;
+        if (j != i) {
+            num += (emp - t2) * (emp - t2);
+            den += t2 * t2;
+        }
+    }
+    __shared__ double sn[32], sd[32];
+    num = warp_sum(num);
+    den = warp_sum(den);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        sn[warp] = num;
+        sd[warp] = den;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
+            a += sn[w2];
+            b += sd[w2];
+        }
+        partial[2 * i] = a;
+        partial[2 * i + 1] = b;
+    }
+}
+
+// ------------------------------------------------------------------ triangular solve
+// One CTA per chain: blocked forward substitution y = L^{-1}(x - xr), 64-row blocks.
+constexpr int kTrsvThreads = 256;
+constexpr int kTrsvB = 64;
+
+__global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(double* const* Lm, int64_t ld, const double* x,
+                                                            const double* xr, int64_t vstride, double* y,
+                                                            double* quad_out, int d, double hq, const int* mask) {
+    const int c = blockIdx.x;
+    if (mask && !mask[c]) return;
+    extern __shared__ double sh[];
+    double* ys = sh;                       // d
+    double* blk = sh + ((d + 1) & ~1);     // 64 x 65
+    double* rhs = blk + kTrsvB * (kTrsvB + 1);
+    const double* L = Lm[c];
+    const double* xc = x + c * vstride;
+    const double* xrc = xr ? xr + c * vstride : nullptr;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kTrsvThreads / 32;
+
+    for (int b0 = 0; b0 < d; b0 += kTrsvB) {
+        const int bs = min(kTrsvB, d - b0);
+        // diagonal block -> shared (coalesced rows)
+        for (int e = tid; e < bs * kTrsvB; e += kTrsvThreads) {
+            const int r = e / kTrsvB, j = e % kTrsvB;
+            blk[r * (kTrsvB + 1) + j] = (j <= r && j < bs) ? L[(int64_t)(b0 + r) * ld + b0 + j] : 0.0;
+        }
+        // rhs_i = (x_i - xr_i) - L[i, 0:b0] . y[0:b0]
+        for (int r = warp; r < bs; r += NW) {
+            const double* Lr = L + (int64_t)(b0 + r) * ld;
+            double s = 0.0;
+            for (int j = lane; j < b0; j += 32) s += Lr[j] * ys[j];
+            s = warp_sum(s);
+            if (lane == 0) {
+                const double xi = xc[b0 + r] - (xrc ? xrc[b0 + r] : 0.0);
+                rhs[r] = xi - s;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // column-oriented substitution inside the block: lane owns rows lane, lane+32
+            double r0 = lane < bs ? rhs[lane] : 0.0;
+            double r1 = lane + 32 < bs ? rhs[lane + 32] : 0.0;
+            for (int j = 0; j < bs; ++j) {
+                const int owner = j & 31;
+                double yj;
+                if (j < 32) yj = __shfl_sync(0xffffffffu, r0, owner);
+                else yj = __shfl_sync(0xffffffffu, r1, owner);
+                yj = yj / blk[j * (kTrsvB + 1) + j];
+                if (lane == owner) {
+                    if (j < 32) r0 = yj;
+                    else r1 = yj;
+                }
+                if (lane > j && lane < bs) r0 -= blk[lane * (kTrsvB + 1) + j] * yj;
+                if (lane + 32 > j && lane + 32 < bs) r1 -= blk[(lane + 32) * (kTrsvB + 1) + j] * yj;
+            }
+            if (lane < bs) ys[b0 + lane] = r0;
+            if (lane + 32 < bs) ys[b0 + lane + 32] = r1;
+        }
+        __syncthreads();
+    }
+    // write y and the quad term
+    double s = 0.0;
+    for (int i = tid; i < d; i += kTrsvThreads) {
+        const double v = ys[i];
+        if (y) y[c * vstride + i] = v;
+        s += v * v;
+    }
+    __shared__ double red[NW];
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NW; ++w) t += red[w];
+        quad_out[c] = hq * t;
+    }
+}
+
+// ------------------------------------------------------------------ Cholesky diagonal block
+constexpr int kNb = 64;
+
+__global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
+                                                         const int* mask, int* status, int* active,
+                                                         double* inv_base) {
+    const int c = blockIdx.x;
+    const int tid = threadIdx.x;
+    const bool run = (!mask || mask[c]) && status[c] == 0;
+    if (tid == 0) active[c] = run ? 1 : 0;
+    if (!run) return;
+    extern __shared__ double dsm[];
+    double (*a)[kNb + 1] = reinterpret_cast<double (*)[kNb + 1]>(dsm);
+    double (*inv)[kNb + 1] = reinterpret_cast<double (*)[kNb + 1]>(dsm + kNb * (kNb + 1));
+    __shared__ int bad;
+    double* A = Am[c] + (int64_t)j0 * ld + j0;
+    for (int e = tid; e < jb * kNb; e += blockDim.x) {
+        const int r = e / kNb, j = e % kNb;
+        a[r][j] = (j <= r && j < jb) ? A[(int64_t)r * ld + j] : 0.0;
+    }
+    if (tid == 0) bad = 0;
+    __syncthreads();
+    for (int k = 0; k < jb; ++k) {
+        const double pivot = a[k][k];
+        if (!(pivot > 0.0) || !isfinite(pivot)) {  // proj/src/linalg.cpp:82-84
+            if (tid == 0) bad = 1;
+            break;
+        }
+        const double lkk = sqrt(pivot);
+        __syncthreads();
+        if (tid == 0) a[k][k] = lkk;
+        for (int i = k + 1 + tid; i < jb; i += blockDim.x) a[i][k] = a[i][k] / lkk;
+        __syncthreads();
+        // right-looking update of the block's trailing lower part
+        const int rem = jb - k - 1;
+        for (int e = tid; e < rem * rem; e += blockDim.x) {
+            const int i = k + 1 + e / rem, j = k + 1 + e % rem;
+            if (j <= i) a[i][j] -= a[i][k] * a[j][k];
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    if (bad) {
+        if (tid == 0) {
+            status[c] = 1;
+            active[c] = 0;
+        }
+        return;
+    }
+    for (int e = tid; e < jb * kNb; e += blockDim.x) {
+        const int r = e / kNb, j = e % kNb;
+        if (j <= r && j < jb) A[(int64_t)r * ld + j] = a[r][j];
+    }
+    // explicit inverse of the 64x64 block for the TRSM (one column per thread)
+    if (tid < kNb) {
+        const int j = tid;
+        for (int i = 0; i < kNb; ++i) inv[i][j] = 0.0;
+        if (j < jb) {
+            for (int i = j; i < jb; ++i) {
+                double s = (i == j) ? 1.0 : 0.0;
+                for (int k = j; k < i; ++k) s -= a[i][k] * inv[k][j];
+                inv[i][j] = s / a[i][i];
+            }
+        }
+    }
+    __syncthreads();
+    double* out = inv_base + (int64_t)c * kNb * kNb;
+    for (int e = tid; e < kNb * kNb; e += blockDim.x) out[e] = inv[e / kNb][e % kNb];
+}
+
+__global__ void beta_update_kernel(double* beta, uint64_t* n_acc, double* rate_out, double* beta_out, int chains,
+                                   int n_lag, int adapt, double lo, double hi, double factor, double bmin,
+                                   double bmax) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= chains) return;
+    const double rate = (double)n_acc[c] / (double)n_lag;  // proj/src/proposal.cpp:162-172
+    double b = beta[c];
+    if (adapt) {
+        if (rate > hi) b *= factor;
+        else if (rate < lo) b /= factor;
+        b = b < bmin ? bmin : (b > bmax ? bmax : b);
+    }
+    beta[c] = b;
+    n_acc[c] = 0;
+    if (rate_out) rate_out[c] = rate;
+    if (beta_out) beta_out[c] = b;
+}
+
+__global__ void accept_factor_kernel(double** L, double** Lnew, const int* try_flag, const int* status,
+                                     const double* q, double qmax, int chains, int* usable) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= chains) return;
+    bool ok = try_flag[c] && status[c] == 0;
+    if (ok && qmax >= 0.0) ok = q[c] <= qmax;  // proj/src/proposal.cpp:185-199
+    if (ok) {
+        double* t = L[c];
+        L[c] = Lnew[c];
+        Lnew[c] = t;
+    }
+    if (usable) usable[c] = ok ? 1 : 0;
+}
+
+__global__ void copy_vecs_kernel(double* dst, const double* src, int64_t n, const int* mask, int64_t stride) {
+    const int c = blockIdx.y;
+    if (mask && !mask[c]) return;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        dst[c * stride + e] = src[c * stride + e];
+}
+
+__global__ void set_identity_kernel(double* base, int64_t mat_stride, int d, int64_t ld) {
+    const int c = blockIdx.y;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)d * ld;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / ld, j = e % ld;
+        base[c * mat_stride + e] = (i == j) ? 1.0 : 0.0;
+    }
+}
+
+__global__ void eval_logpi_kernel(const double* x, const double* g, const double* inv_eig, const double* bcoef,
+                                  int twisted, double* out, int d, int64_t ld) {
+    const int c = blockIdx.x;
+    const double* xc = x + c * ld;
+    const double* gc = g + c * ld;
+    double s = 0.0;
+    for (int i = 2 * threadIdx.x; i < d; i += 2 * blockDim.x) {
+        const double g0 = gc[i], g1 = i + 1 < d ? gc[i + 1] : 0.0;
+        if (twisted) {
+            const double w1 = g1 + bcoef[i] * g0 * g0;
+            s += g0 * g0 * inv_eig[i] + (i + 1 < d ? w1 * w1 * inv_eig[i + 1] : 0.0);
+        } else {
+            s += xc[i] * g0 + (i + 1 < d ? xc[i + 1] * g1 : 0.0);
+        }
+    }
+    __shared__ double red[32];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        out[c] = -0.5 * t;
+    }
+}
+
+__global__ void blend_mean_kernel(const double* mg, const double* ml, double wg, double wl, double* mb, int d,
+                                  int64_t ld) {
+    const int c = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < d) mb[c * ld + i] = wg * mg[i] + wl * ml[c * ld + i];
+}
+
+__global__ void project_rows_kernel(const double* X, int64_t win_stride, int64_t ld, int rows, int t0, int d,
+                                    const double* proj, double* out) {
+    const int c = blockIdx.y;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int t = t0 + warp;
+    if (t >= rows) return;
+    const double* xr = X + c * win_stride + (int64_t)t * ld;
+    double a = 0.0, b = 0.0;
+    for (int i = lane; i < d; i += 32) {
+        a += proj[i] * xr[i];
+        b += proj[ld + i] * xr[i];
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+        out[((int64_t)c * rows + t) * 2] = a;
+        out[((int64_t)c * rows + t) * 2 + 1] = b;
+    }
+}
+
+unsigned grid_for(int64_t n, int threads, int cap_per_sm = 8) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), (int64_t)kNumSMs * cap_per_sm));
+}
+
+}  // namespace
+
+void launch_mean_update(double* mean, int64_t mean_stride, const double* X, int64_t win_stride, int64_t ld,
+                        int chains, int d, int k_off, int k, double n_prev, cudaStream_t s) {
+    if (k <= 0) return;
+    const double total = n_prev + k;
+    dim3 grid((unsigned)ceil_div(d, 128), chains);
+    mean_update_kernel<<<grid, 128, 0, s>>>(mean, mean_stride, X, win_stride, ld, d, k_off, k, n_prev / total,
+                                            1.0 / total);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg, const double* Sl,
+                      int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl, double* mb,
+                      int64_t mb_stride, int chains, int d, int64_t ld, const int* mask, double jitter_eps,
+                      const double* tr, cudaStream_t s) {
+    dim3 grid((unsigned)ceil_div(d, 256), d, chains);
+    blend_cov_kernel<<<grid, 256, 0, s>>>(C_out, Sg, mg, Sl, sl_stride, ml, ml_stride, wg, wl, mb, mb_stride, d, ld,
+                                          mask, jitter_eps, tr);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_trace_floor(double* const* Cm, int64_t ld, const double* mb, int64_t mb_stride, int chains, int d,
+                        double* tr, int* try_flag, cudaStream_t s) {
+    trace_floor_kernel<<<chains, 32, 0, s>>>(Cm, ld, mb, mb_stride, d, tr, try_flag);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_sum_chains(double* out, const double* in, int64_t chain_stride, int chains, int64_t n, double weight,
+                       cudaStream_t s) {
+    sum_chains_kernel<<<grid_for(n, 256), 256, 0, s>>>(out, in, chain_stride, chains, n, weight);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_axpby(double* y, const double* x, int64_t n, double a, double b, cudaStream_t s) {
+    axpby_kernel<<<grid_for(n, 256), 256, 0, s>>>(y, x, n, a, b);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_cum_fold(double* cmean, double* cdiag, const double* lmean, const double* S, int64_t s_stride,
+                     int chains, int d, int64_t ld, double keep, double add, cudaStream_t s) {
+    dim3 grid((unsigned)ceil_div(d, 128), chains);
+    cum_fold_kernel<<<grid, 128, 0, s>>>(cmean, cdiag, lmean, S, s_stride, d, ld, keep, add);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_cov_error(const double* Sg, const double* mg, const double* Ctrue, int d, int64_t ld, double* out2,
+                      cudaStream_t s) {
+    cov_error_kernel<<<d, 256, 0, s>>>(Sg, mg, Ctrue, d, ld, out2);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr, int64_t vstride, double* y,
+                 double* quad_out, int chains, int d, double half_inv_infl2, const int* mask, cudaStream_t s) {
+    const size_t smem = sizeof(double) * (((d + 1) & ~1) + kTrsvB * (kTrsvB + 1) + kTrsvB);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        DGB_CUDA(cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+    }
+    trsv_kernel<<<chains, kTrsvThreads, smem, s>>>(L, ld, x, xr, vstride, y, quad_out, d, half_inv_infl2, mask);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status, PotrfWork& w,
+                   cudaStream_t s) {
+    // w.inv holds chains*64*64 doubles, followed (by the caller's allocation) by an int active[chains]
+    int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kNb * kNb);
+    for (int j0 = 0; j0 < d; j0 += kNb) {
+        const int jb = std::min(kNb, d - j0);
+        constexpr int smem = 2 * kNb * (kNb + 1) * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            DGB_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr = true;
+        }
+        potrf_diag_kernel<<<chains, 256, smem, s>>>(A, ld, j0, jb, mask, status, active, w.inv);
+        DGB_LAUNCH_CHECK();
+        count_launch();
+        const int rest = d - j0 - jb;
+        if (rest <= 0) break;
+        // TRSM in place: L21 = A21 * inv(L11)^T  (one 64-wide column tile per CTA -> safe in place)
+        GemmBatch t{};
+        t.A = (const double* const*)A;
+        t.B = (const double* const*)w.inv_ptrs;
+        t.C = A;
+        t.a_off = (int64_t)(j0 + jb) * ld + j0;
+        t.b_off = 0;
+        t.c_off = t.a_off;
+        t.lda = ld;
+        t.ldb = kNb;
+        t.ldc = ld;
+        t.M = rest;
+        t.N = jb;
+        t.K = jb;
+        t.alpha = 1.0;
+        t.beta = 0.0;
+        t.active = active;
+        gemm_f64(t, chains, true, true, s, GemmShape::Narrow);
+        // trailing update A22 -= L21 L21^T (lower tiles only)
+        GemmBatch u{};
+        u.A = (const double* const*)A;
+        u.B = (const double* const*)A;
+        u.C = A;
+        u.a_off = t.a_off;
+        u.b_off = t.a_off;
+        u.c_off = (int64_t)(j0 + jb) * ld + (j0 + jb);
+        u.lda = ld;
+        u.ldb = ld;
+        u.ldc = ld;
+        u.M = rest;
+        u.N = rest;
+        u.K = jb;
+        u.alpha = -1.0;
+        u.beta = 1.0;
+        u.active = active;
+        u.tri_c_lower = 1;
+        gemm_f64(u, chains, true, true, s);
+    }
+}
+
+void launch_beta_update(double* beta, uint64_t* n_acc, double* rate_out, double* beta_out, int chains, int n_lag,
+                        int adapt, double lo, double hi, double factor, double bmin, double bmax, cudaStream_t s) {
+    beta_update_kernel<<<(unsigned)ceil_div(chains, 128), 128, 0, s>>>(beta, n_acc, rate_out, beta_out, chains, n_lag,
+                                                                      adapt, lo, hi, factor, bmin, bmax);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_accept_factor(double** L, double** Lnew, const int* try_flag, const int* status, const double* q,
+                          double qmax, int chains, int* usable, cudaStream_t s) {
+    accept_factor_kernel<<<(unsigned)ceil_div(chains, 128), 128, 0, s>>>(L, Lnew, try_flag, status, q, qmax, chains,
+                                                                        usable);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_set_identity(double* base, int64_t mat_stride, int chains, int d, int64_t ld, cudaStream_t s) {
+    dim3 grid(grid_for((int64_t)d * ld, 256, 1), chains);
+    set_identity_kernel<<<grid, 256, 0, s>>>(base, mat_stride, d, ld);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_eval_logpi(const double* x, const double* g, const double* inv_eig, const double* bcoef, bool twisted,
+                       double* out, int chains, int d, int64_t ld, cudaStream_t s) {
+    eval_logpi_kernel<<<chains, 256, 0, s>>>(x, g, inv_eig, bcoef, twisted ? 1 : 0, out, d, ld);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_blend_mean(const double* mg, const double* ml, double wg, double wl, double* mb, int chains, int d,
+                       int64_t ld, cudaStream_t s) {
+    dim3 grid((unsigned)ceil_div(d, 128), chains);
+    blend_mean_kernel<<<grid, 128, 0, s>>>(mg, ml, wg, wl, mb, d, ld);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_project_rows(const double* X, int64_t win_stride, int64_t ld, int chains, int rows, int t0, int d,
+                         const double* proj, double* out, cudaStream_t s) {
+    if (t0 >= rows) return;
+    const int warps = rows - t0;
+    dim3 grid((unsigned)ceil_div((int64_t)warps * 32, 256), chains);
+    project_rows_kernel<<<grid, 256, 0, s>>>(X, win_stride, ld, rows, t0, d, proj, out);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_copy_vecs(double* dst, const double* src, int64_t n, const int* mask, int64_t stride, int chains,
+                      cudaStream_t s) {
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 32)), chains);
+    copy_vecs_kernel<<<grid, 256, 0, s>>>(dst, src, n, mask, stride);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+}  // namespace dgb

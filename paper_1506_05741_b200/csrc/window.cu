@@ -1,0 +1,280 @@
+// window.cu — Philox draws and the sequential MH window kernel.
+//
+// The MH window is the only inherently sequential part of the sampler: step
+// t+1 of a chain depends on step t's accept decision. Everything O(d^2) per
+// step in the reference (SYMV log density, TRSV quad term, SYR moments) has
+// been moved into window-level dense contractions (gemm_f64), so one step is
+// O(d) work: with x' = x_ref + c (x - x_ref) + xi_t,
+//   G x'            = G x_ref + c (G x - G x_ref) + (G Xi^T)_t      [H rows]
+//   L^-1 (x'-x_ref) = c y + s w_t   (xi_t = s L w_t, y = L^-1 (x - x_ref))
+//   log pi(x')      = -1/2 x'.(G x')  or  -1/2 sum twist(z')^2/sigma^2
+//   quad(x')        = 1/2 |L^-1(x'-x_ref)|^2 / infl^2
+// One CTA owns one chain for the whole window, its state vectors in registers;
+// each step is one fused pass (candidate, two dot products, CTA reduction with
+// a single barrier, accept/reject from the chain's Philox uniform) — the
+// "fused warp-level accept/reject" of the design.
+#include "kernels.cuh"
+
+namespace dgb {
+
+namespace {
+
+__global__ void normals_kernel(double* W, double* Xi, int64_t chain_stride, int chains, int rows,
+                               int d, int64_t ld, const PhiloxKey* keys, uint64_t start,
+                               const double* beta, double infl) {
+    const int64_t per_chain = (int64_t)rows * d;
+    const int64_t total = per_chain * chains;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e / per_chain);
+        const int64_t rem = e - c * per_chain;
+        const int r = (int)(rem / d);
+        const int i = (int)(rem - (int64_t)r * d);
+        const double z = philox_normal(keys[c], start + (uint64_t)rem);
+        const int64_t off = c * chain_stride + r * ld + i;
+        W[off] = z;
+        if (Xi) Xi[off] = (beta[c] * infl) * z;
+    }
+}
+
+__global__ void normal_vec_kernel(double* out, int64_t stride, int chains, int n, const PhiloxKey* keys,
+                                  uint64_t start, double scale) {
+    const int c = blockIdx.y;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[c * stride + i] = scale * philox_normal(keys[c], start + (uint64_t)i);
+}
+
+__global__ void draws_kernel(int kind, double* out_f64, uint64_t* out_u64, int64_t n, PhiloxKey key,
+                             uint64_t start) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (kind == 0) out_u64[i] = philox_u64(key, start + i);
+        else if (kind == 1) out_f64[i] = philox_uniform_open(key, start + i);
+        else out_f64[i] = philox_normal(key, start + i);
+    }
+}
+
+constexpr int kStepThreads = 512;
+constexpr int kStepWarps = kStepThreads / 32;
+
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
+// R = double2 pairs per thread; PREF = prefetch the next step's rows into registers
+template <int R, bool TWISTED, bool PREF>
+__global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p) {
+    const int c = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int d = p.d;
+    const int64_t ld = p.ld;
+    __shared__ double red[2][kStepWarps][2];
+
+    const double beta = p.beta[c];
+    const bool pcn = p.pcn != 0;
+    const double cc = pcn ? sqrt(fmax(0.0, 1.0 - beta * beta)) : 1.0;  // proj/src/proposal.cpp:120
+    const double sc = beta * p.infl;
+    const double hq = 0.5 / (p.infl * p.infl);
+
+    const double* Wc = p.W + c * p.win_stride;
+    double* Xc = p.Xi + c * p.win_stride;
+    const double* Hc = p.H + c * p.win_stride;
+
+    double2 x[R], g[R], y[R], xr[R], gr[R], ie[R], bc[R];
+    bool valid[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = 2 * (tid + r * kStepThreads);
+        valid[r] = e < d;
+        const double2 z2 = make_double2(0.0, 0.0);
+        x[r] = valid[r] ? ld2(p.x + c * ld + e) : z2;
+        g[r] = valid[r] ? ld2(p.g + c * ld + e) : z2;
+        y[r] = (valid[r] && pcn) ? ld2(p.y + c * ld + e) : z2;
+        xr[r] = (valid[r] && p.xr) ? ld2(p.xr + c * ld + e) : z2;
+        gr[r] = (valid[r] && p.gr) ? ld2(p.gr + c * ld + e) : z2;
+        if (TWISTED) {
+            ie[r] = valid[r] ? ld2(p.inv_eig + e) : z2;
+            bc[r] = valid[r] ? ld2(p.bcoef + e) : z2;
+        }
+    }
+    double lp = p.log_pi[c], q = pcn ? p.quad[c] : 0.0;
+    uint64_t nacc = p.n_accepted[c];
+    const PhiloxKey uk = p.ukeys[c];
+    const uint64_t u0 = p.uctr[c];
+
+    double2 xi[R], w[R], h[R];
+    auto load_row = [&](int t, double2 (&a)[R], double2 (&b)[R], double2 (&hh)[R]) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = 2 * (tid + r * kStepThreads);
+            if (valid[r]) {
+                a[r] = ld2(Xc + (int64_t)t * ld + e);
+                b[r] = pcn ? ld2(Wc + (int64_t)t * ld + e) : make_double2(0.0, 0.0);
+                hh[r] = ld2(Hc + (int64_t)t * ld + e);
+            } else {
+                a[r] = b[r] = hh[r] = make_double2(0.0, 0.0);
+            }
+        }
+    };
+    load_row(0, xi, w, h);
+
+    for (int t = 0; t < p.n_lag; ++t) {
+        double2 nxi[R], nw[R], nh[R];
+        if (PREF && t + 1 < p.n_lag) load_row(t + 1, nxi, nw, nh);
+        const double logu = log(philox_uniform_open(uk, u0 + (uint64_t)t));
+
+        double2 xc[R], gc[R], yc[R];
+        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            // candidate exactly as proj/src/proposal.cpp:119-124 (x_ref + c (x - x_ref) + xi)
+            // explicit _rn ops: no FMA contraction, so x' has the reference's exact bits
+            xc[r].x = __dadd_rn(__dadd_rn(xr[r].x, __dmul_rn(cc, __dadd_rn(x[r].x, -xr[r].x))), xi[r].x);
+            xc[r].y = __dadd_rn(__dadd_rn(xr[r].y, __dmul_rn(cc, __dadd_rn(x[r].y, -xr[r].y))), xi[r].y);
+            gc[r].x = gr[r].x + cc * (g[r].x - gr[r].x) + h[r].x;
+            gc[r].y = gr[r].y + cc * (g[r].y - gr[r].y) + h[r].y;
+            if (TWISTED) {
+                // w_{2j+1} = z_{2j+1} + b_{2j} z_{2j}^2 (proj/src/target.cpp:167-173)
+                const double w0 = gc[r].x;
+                const double w1 = gc[r].y + bc[r].x * gc[r].x * gc[r].x;
+                sa += w0 * w0 * ie[r].x + w1 * w1 * ie[r].y;
+            } else {
+                sa += xc[r].x * gc[r].x + xc[r].y * gc[r].y;
+            }
+            if (pcn) {
+                yc[r].x = cc * y[r].x + sc * w[r].x;
+                yc[r].y = cc * y[r].y + sc * w[r].y;
+                sb += yc[r].x * yc[r].x + yc[r].y * yc[r].y;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+            sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        }
+        const int buf = t & 1;
+        if (lane == 0) {
+            red[buf][warp][0] = sa;
+            red[buf][warp][1] = sb;
+        }
+        __syncthreads();
+        double ta = 0.0, tb = 0.0;
+#pragma unroll
+        for (int k = 0; k < kStepWarps; ++k) {
+            ta += red[buf][k][0];
+            tb += red[buf][k][1];
+        }
+        const double lpc = -0.5 * ta;
+        const double qc = pcn ? hq * tb : 0.0;
+        const double ratio = pcn ? (lpc + qc) - (lp + q) : lpc - lp;  // proj/src/proposal.cpp:77-82
+        const bool acc = logu < ratio;                               // strict, :146
+        if (acc) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                x[r] = xc[r];
+                g[r] = gc[r];
+                if (pcn) y[r] = yc[r];
+            }
+            lp = lpc;
+            q = qc;
+            ++nacc;
+        }
+        // post-step state -> row t of the window (SYRK / trace input); xi row t is consumed
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = 2 * (tid + r * kStepThreads);
+            if (valid[r]) {
+                if (e + 1 < d) st2(Xc + (int64_t)t * ld + e, x[r]);
+                else Xc[(int64_t)t * ld + e] = x[r].x;
+            }
+        }
+        if (tid == 0) {
+            if (p.trace_lp) p.trace_lp[(int64_t)c * p.n_lag + t] = lp;
+            if (p.accept_out) p.accept_out[(int64_t)c * p.n_lag + t] = acc ? 1 : 0;
+            if (p.log_ratio_out) p.log_ratio_out[(int64_t)c * p.n_lag + t] = ratio;
+        }
+        if (PREF) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                xi[r] = nxi[r];
+                w[r] = nw[r];
+                h[r] = nh[r];
+            }
+        } else if (t + 1 < p.n_lag) {
+            load_row(t + 1, xi, w, h);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = 2 * (tid + r * kStepThreads);
+        if (!valid[r]) continue;
+        if (e + 1 < d) {
+            st2(p.x + c * ld + e, x[r]);
+            st2(p.g + c * ld + e, g[r]);
+            if (pcn) st2(p.y + c * ld + e, y[r]);
+        } else {
+            p.x[c * ld + e] = x[r].x;
+            p.g[c * ld + e] = g[r].x;
+            if (pcn) p.y[c * ld + e] = y[r].x;
+        }
+    }
+    if (tid == 0) {
+        p.log_pi[c] = lp;
+        if (pcn) p.quad[c] = q;
+        p.n_accepted[c] = nacc;
+        p.uctr[c] = u0 + (uint64_t)p.n_lag;
+    }
+}
+
+template <bool TW>
+void launch_r(const StepParams& p, cudaStream_t s) {
+    const int pairs = (p.d + 1) / 2;
+    const int R = (pairs + kStepThreads - 1) / kStepThreads;
+    dim3 grid(p.chains), block(kStepThreads);
+    if (R <= 1) mh_window_kernel<1, TW, true><<<grid, block, 0, s>>>(p);
+    else if (R <= 2) mh_window_kernel<2, TW, true><<<grid, block, 0, s>>>(p);
+    else if (R <= 4) mh_window_kernel<4, TW, true><<<grid, block, 0, s>>>(p);
+    else if (R <= 8) mh_window_kernel<8, TW, false><<<grid, block, 0, s>>>(p);
+    else throw CudaError("mh_window: dimension above 8192 is not supported by this build");
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+}  // namespace
+
+void launch_normals(double* W, double* Xi, int64_t chain_stride, int chains, int rows, int d, int64_t ld,
+                    const PhiloxKey* keys, uint64_t start, const double* beta, double infl,
+                    cudaStream_t s) {
+    const int64_t total = (int64_t)chains * rows * d;
+    if (total == 0) return;
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>(ceil_div(total, threads), (int64_t)kNumSMs * 16);
+    normals_kernel<<<(unsigned)blocks, threads, 0, s>>>(W, Xi, chain_stride, chains, rows, d, ld, keys, start,
+                                                        beta, infl);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_normal_vec(double* out, int64_t stride, int chains, int n, const PhiloxKey* keys, uint64_t start,
+                       double scale, cudaStream_t s) {
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 64)), chains);
+    normal_vec_kernel<<<grid, 256, 0, s>>>(out, stride, chains, n, keys, start, scale);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_draws(int kind, double* out_f64, uint64_t* out_u64, int64_t n, PhiloxKey key, uint64_t start,
+                  cudaStream_t s) {
+    if (n <= 0) return;
+    const int64_t blocks = std::min<int64_t>(ceil_div(n, 256), (int64_t)kNumSMs * 8);
+    draws_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, out_f64, out_u64, n, key, start);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_mh_window(const StepParams& p, bool twisted, cudaStream_t s) {
+    if (p.chains <= 0 || p.n_lag <= 0) return;
+    if (twisted) launch_r<true>(p, s);
+    else launch_r<false>(p, s);
+}
+
+}  // namespace dgb

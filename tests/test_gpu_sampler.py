@@ -1,0 +1,171 @@
+"""End-to-end parity of the B200 sampler through the diam.h ABI.
+
+1. Lockstep on identical draws: the engine records every window's standard
+   normals W (GPU Philox + CUDA libm); the CPU oracle (restating
+   proj/src/proposal.cpp + runner.cpp) is then driven with exactly those W and
+   its own bit-exact Philox uniforms. Accept/reject decisions and accept counts
+   (hence every beta/acceptance history entry) must be identical; log alpha
+   must agree to 1e-9 (absolute, |log alpha| ~ O(1)); any decision difference
+   is allowed only at a near-tie |log u - log alpha| <= 1e-9 and is reported.
+   Global moments must agree to 1e-10 relative (FP64, different summation
+   order: DMMA GEMMs vs sequential loops).
+2. Chain-level statistics vs the reference library on its own draws
+   (independent seeds): acceptance rate and covariance error within 3 sigma
+   of the Monte Carlo spread.
+3. ABI semantics on the GPU path: stopping rules, histories, traces, JSON.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import _oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def lockstep(b200, tmp_path, target_kind, d, kern, P, M, K, n_lag, n0, seed, **extra):
+    t = b200.target_build(target_kind, d, 17) if isinstance(target_kind, str) else target_kind
+    path = str(tmp_path / "t.bin")
+    t.save(path)
+    td = O.read_target(path)
+    res, cap = b200.sample_capture(t, kernel=kern, chains=P, intervals_per_batch=M, max_batches=K, n_lag=n_lag,
+                                   n0=n0, master_seed=seed, record_traces=0, **extra)
+    windows = K * M
+    ws = []
+    for p in range(P):
+        w = cap.get(p, "w")
+        assert w.size == windows * n_lag * d
+        ws.append(np.concatenate([w, np.zeros(n_lag * d)]))  # + the never-consumed final window
+    o = O.run(td, kind=kern, chains=P, M=M, K=K, seed=seed, inject_w=ws, record_decisions=True, n_lag=n_lag,
+              n0=n0, **extra)
+    ties = 0
+    for p in range(P):
+        acc_g = cap.get(p, "accept")
+        lr_g = cap.get(p, "log_ratio")
+        acc_o = o["accept_bits"][p]
+        lr_o = o["log_ratio"][p]
+        lu = o["log_u"][p]
+        diff = np.nonzero(acc_g != acc_o)[0]
+        if diff.size:
+            first = diff[0]
+            assert abs(lu[first] - lr_o[first]) <= 1e-9, f"chain {p}: decision mismatch at step {first} off a tie"
+            ties += 1
+            continue  # trajectories legitimately diverge after a tie flip
+        assert np.max(np.abs(lr_g - lr_o)) <= 1e-9 * max(1.0, np.max(np.abs(lr_o)))
+        assert np.array_equal(res.chain_history(p, "beta"), o["beta_hist"][p])
+        assert np.array_equal(res.chain_history(p, "acceptance"), o["acc_hist"][p])
+    if ties == 0:
+        gm, om = res.mean(), o["global_mean"]
+        gc, oc = res.cov(), o["global_cov"]
+        assert np.linalg.norm(gm - om) <= 1e-10 * max(1.0, np.linalg.norm(om))
+        assert np.linalg.norm(gc - oc) <= 1e-10 * np.linalg.norm(oc)
+        ce = res.history("cov_error")
+        assert np.allclose(ce, o["cov_error_hist"], rtol=1e-9, equal_nan=True)
+        assert np.allclose(res.history("psrf"), o["psrf_hist"], rtol=1e-9, equal_nan=True)
+        assert res.accumulated_samples == o["accumulated_samples"]
+    return res, o, ties
+
+
+@pytest.mark.parametrize("kern", ["diam", "am", "rw", "pcn"])
+def test_lockstep_gaussian(b200, tmp_path, kern):
+    # n_lag > d so the first adapted covariance is full rank (no rounding-decided jitter)
+    _, _, ties = lockstep(b200, tmp_path, "pi2", 16, kern, P=4, M=3, K=3, n_lag=40, n0=30, seed=11)
+    assert ties == 0
+
+
+def test_lockstep_twisted_pi5(b200, tmp_path):
+    _, _, ties = lockstep(b200, tmp_path, "pi5", 20, "diam", P=3, M=2, K=3, n_lag=48, n0=0, seed=5, inflation=1.2)
+    assert ties == 0
+
+
+def test_lockstep_adaptive_reference(b200, tmp_path):
+    _, _, ties = lockstep(b200, tmp_path, "pi1", 12, "diam", P=2, M=2, K=3, n_lag=30, n0=0, seed=3,
+                          adaptive_ref=1, n_ref_start=40)
+    assert ties == 0
+
+
+def test_lockstep_odd_dimension_and_multi_tile(b200, tmp_path):
+    # d not a multiple of 8 (padded rows) and > one 128-wide GEMM tile
+    _, _, ties = lockstep(b200, tmp_path, "pi2", 133, "diam", P=2, M=2, K=2, n_lag=150, n0=0, seed=9)
+    assert ties == 0
+
+
+def test_golden_target_runs_statistics(b200):
+    """The reference's own golden runs (tests/golden/runs.npz): same config on the GPU."""
+    import sys
+    sys.path.insert(0, GOLD)
+    from make_golden import RUNS
+    g = np.load(os.path.join(GOLD, "runs.npz"))
+    for i, (tf, kern, P, M, K, nl, n0, seed, extra) in enumerate(RUNS):
+        t = b200.target_load(os.path.join(GOLD, tf))
+        r = b200.sample(t, kernel=kern, chains=P, intervals_per_batch=M, max_batches=K, n_lag=nl, n0=n0,
+                        master_seed=seed, **extra)
+        assert r.accumulated_samples == int(g[f"r{i}_accumulated"][0])
+        assert r.history("cov_error").shape == g[f"r{i}_cov_error"].shape
+        for p in range(P):
+            assert r.chain_history(p, "beta").shape == g[f"r{i}_beta"][p].shape
+        # same initial state x0 (bit-exact init stream) -> same first log pi to rounding
+        tr = r.trace(0, 0)
+        assert tr.shape == g[f"r{i}_trace_logpi_c0"].shape
+
+
+def test_chain_statistics_vs_reference(b200, ref_abi, tmp_path):
+    """Acceptance rate and cov error agree with the reference within Monte Carlo error."""
+    d = 32
+    t_ref = ref_abi.target_build("pi2", d, 4)
+    p = str(tmp_path / "t.bin")
+    t_ref.save(p)
+    t = b200.target_load(p)
+    kw = dict(kernel="diam", chains=4, intervals_per_batch=4, max_batches=6, n_lag=64, n0=0, record_traces=0)
+    stats = {"gpu": [], "ref": []}
+    for seed in range(10):
+        for name, lib, tt in (("gpu", b200, t), ("ref", ref_abi, t_ref)):
+            r = lib.sample(tt, master_seed=100 + seed, threads=4, **kw) if name == "ref" else \
+                lib.sample(tt, master_seed=100 + seed, **kw)
+            acc = np.mean([r.chain_history(c, "acceptance")[-8:].mean() for c in range(4)])
+            stats[name].append((acc, r.final_cov_error))
+    a = np.array(stats["gpu"])
+    b = np.array(stats["ref"])
+    for j, what in enumerate(["acceptance", "cov_error"]):
+        se = np.sqrt(a[:, j].var(ddof=1) / len(a) + b[:, j].var(ddof=1) / len(b))
+        print(f"{what}: gpu {a[:, j].mean():.4f} ref {b[:, j].mean():.4f} (3se {3 * se:.4f})")
+        assert abs(a[:, j].mean() - b[:, j].mean()) <= 3 * se + 1e-12
+
+
+def test_stopping_rules_and_histories(b200, tmp_path):
+    t = b200.target_build("pi2", 10, 2)
+    r = b200.sample(t, kernel="diam", chains=3, intervals_per_batch=2, max_batches=50, n_lag=20, n0=0,
+                    cov_tol=0.5, master_seed=1)
+    assert r.stop_reason in ("cov_tol", "batch_cap")
+    n = r.batches
+    assert r.history("cov_error").shape == (n,)
+    assert r.history("psrf").shape == (n,)
+    assert r.history("batch_seconds").shape == (n,)
+    assert r.total_samples == 3 * 2 * n * 20
+    assert r.chain_history(2, "beta").shape == (2 * n,)
+    if r.stop_reason == "cov_tol":
+        assert r.final_cov_error <= 0.5
+    r2 = b200.sample(t, kernel="rw", chains=2, max_batches=100, n_lag=10, max_samples=200, master_seed=1)
+    assert r2.stop_reason == "max_samples" and r2.total_samples == 200
+    # traces: log density + two eigen projections, recorded after burn-in only
+    r3 = b200.sample(t, kernel="diam", chains=2, intervals_per_batch=2, max_batches=3, n_lag=10, n0=15,
+                     trace_thin=2, master_seed=4)
+    assert r3.functional_names() == ["log_density", "proj_min", "proj_max"]
+    total = 2 * 3 * 10
+    want = len([n for n in range(1, total + 1) if n > 15 and (n - 15 - 1) % 2 == 0])
+    assert r3.trace(1, 0).shape == (want,) and r3.trace(1, 2).shape == (want,)
+    assert np.all(r3.trace(1, 0) <= 0)
+    js = str(tmp_path / "r.json")
+    r3.write_json(js)
+    doc = json.load(open(js))
+    assert doc["schema"] == "diam-run-result/1" and doc["batches"] == 3 and len(doc["iact"]) == 2
+
+
+def test_launch_counter_moves(b200):
+    t = b200.target_build("pi1", 8, 1)
+    before = b200.launch_count()
+    b200.sample(t, chains=2, max_batches=1, n_lag=4, record_traces=0)
+    assert b200.launch_count() > before
