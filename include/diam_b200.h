@@ -32,6 +32,15 @@ uint64_t diamx_launch_count(void);        /* kernels this process launched throu
  * communicator is set, diam_sample shards `chains` over the ranks and pools the
  * batch moments with an NCCL all-reduce (the reference's merge_batch,
  * proj/src/moments.cpp:51-75). */
+/* host logic the engine uses for the sharded path (CPU-callable, tested with gloo):
+ * block sharding of global chain indices and the batch-merge weights */
+void diamx_shard_range(int64_t chains, int world, int rank, int64_t* first, int64_t* count);
+void diamx_merge_weights(uint64_t global_count, uint64_t chains, uint64_t per_chain, double* keep,
+                         double* wp);
+/* max_i sqrt(R_i) from per-chain cumulative means / second-moment diagonals
+ * (chains x d each, row-major), as the engine computes it after the all-gather */
+diam_status diamx_psrf_max(const double* means, const double* diags, int64_t chains, int64_t d,
+                           uint64_t samples_per_chain, double* out);
 diam_status diamx_nccl_unique_id(char out[128]);
 diam_status diamx_comm_init(const char id[128], int rank, int world);
 void diamx_comm_destroy(void);

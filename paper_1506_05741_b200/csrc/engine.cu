@@ -53,8 +53,10 @@ Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> com
     P_ = static_cast<int>(cfg_.chains);
     require(P_ >= world_, Err::InvalidArgument, "fewer chains than GPUs");
     // block sharding of global chain indices: rank r owns [r P / N, (r+1) P / N)
-    c0_ = static_cast<int>((int64_t)rank_ * P_ / world_);
-    C_ = static_cast<int>((int64_t)(rank_ + 1) * P_ / world_) - c0_;
+    int64_t first = 0, count = 0;
+    shard_range(P_, world_, rank_, &first, &count);
+    c0_ = static_cast<int>(first);
+    C_ = static_cast<int>(count);
     ld_ = pad_ld(d_);
     win_ = (int64_t)Lw_ * ld_;
     mat_ = (int64_t)d_ * ld_;
@@ -515,9 +517,8 @@ void Engine::merge_batch() {
     // proj/src/moments.cpp:51-88 with the P-chain sum pooled across GPUs
     const uint64_t incoming = (uint64_t)P_ * cnt_local_;
     if (incoming > 0) {
-        const double total = (double)(cnt_g_ + incoming);
-        const double keep = (double)cnt_g_ / total;
-        const double wp = (double)cnt_local_ / total;
+        double keep = 1.0, wp = 0.0;
+        merge_weights(cnt_g_, (uint64_t)P_, cnt_local_, &keep, &wp);
         timed_begin("merge");
         launch_sum_chains(Ssum_, S_, mat_, C_, mat_, 1.0, stream_);
         launch_sum_chains(Ssum_ + mat_, mean_, ld_, C_, ld_, 1.0, stream_);

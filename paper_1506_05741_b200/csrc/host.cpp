@@ -548,6 +548,20 @@ double psrf_max(const std::vector<const double*>& means, const std::vector<const
     return mx;
 }
 
+// ------------------------------------------------------------------ multi-GPU host logic
+void shard_range(int64_t P, int world, int rank, int64_t* first, int64_t* count) {
+    const int64_t a = P * rank / world, b = P * (rank + 1) / world;
+    *first = a;
+    *count = b - a;
+}
+
+void merge_weights(uint64_t global_count, uint64_t chains, uint64_t per_chain, double* keep, double* wp) {
+    const uint64_t incoming = chains * per_chain;
+    const double total = static_cast<double>(global_count + incoming);
+    *keep = incoming ? static_cast<double>(global_count) / total : 1.0;
+    *wp = incoming ? static_cast<double>(per_chain) / total : 0.0;
+}
+
 // ------------------------------------------------------------------ configuration
 const char* kkind_name(KKind k) {
     static const char* names[] = {"rw", "pcn", "am", "diam"};

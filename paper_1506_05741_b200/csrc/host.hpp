@@ -74,6 +74,14 @@ QuadFit fit_quadratic(const double* xs, const double* ys, size_t n);
 double psrf_max(const std::vector<const double*>& means, const std::vector<const double*>& diags, size_t d,
                 uint64_t n_per_chain);
 
+// ---------------------------------------------------------------- multi-GPU host logic
+// Block sharding of P global chains over `world` ranks: rank r owns
+// [r P / world, (r+1) P / world). RNG streams stay keyed by the global index.
+void shard_range(int64_t P, int world, int rank, int64_t* first, int64_t* count);
+// Weights of the batch merge (proj/src/moments.cpp:63-74): global <- keep*global
+// + wp * sum_p local_p, with every chain holding `per_chain` samples.
+void merge_weights(uint64_t global_count, uint64_t chains, uint64_t per_chain, double* keep, double* wp);
+
 // ---------------------------------------------------------------- run config / result
 enum class KKind { RW = 0, PCN, AM, DIAM };
 const char* kkind_name(KKind k);

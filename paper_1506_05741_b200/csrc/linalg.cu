@@ -219,42 +219,85 @@ constexpr int kNb = 64;
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
                                                          const int* mask, int* status, int* active,
                                                          double* inv_base) {
+    // Register-blocked right-looking Cholesky of the 64x64 diagonal block, fused with
+    // the explicit inverse of the factor (for the DMMA TRSM that follows). Thread
+    // (ty, tx) of a 16x16 grid owns rows ty+16a and columns tx+16b (a, b < 4) of
+    // both L and L^{-1} in registers; each column step broadcasts the new column of
+    // L and the finished row of L^{-1} through shared memory: two barriers per column.
     const int c = blockIdx.x;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const bool run = (!mask || mask[c]) && status[c] == 0;
     if (tid == 0) active[c] = run ? 1 : 0;
     if (!run) return;
-    extern __shared__ double dsm[];
-    double (*a)[kNb + 1] = reinterpret_cast<double (*)[kNb + 1]>(dsm);
-    double (*inv)[kNb + 1] = reinterpret_cast<double (*)[kNb + 1]>(dsm + kNb * (kNb + 1));
+    __shared__ double colk[2][kNb], xrow[2][kNb];
+    __shared__ double piv;
     __shared__ int bad;
     double* A = Am[c] + (int64_t)j0 * ld + j0;
-    for (int e = tid; e < jb * kNb; e += blockDim.x) {
-        const int r = e / kNb, j = e % kNb;
-        a[r][j] = (j <= r && j < jb) ? A[(int64_t)r * ld + j] : 0.0;
-    }
+    double v[4][4], x[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int r = ty + 16 * a, q = tx + 16 * b;
+            // rows/cols past jb are padded with the identity so the 64x64 factorization stays valid
+            v[a][b] = (r < jb && q <= r) ? A[(int64_t)r * ld + q] : (r == q ? 1.0 : 0.0);
+            x[a][b] = (r == q) ? 1.0 : 0.0;
+        }
     if (tid == 0) bad = 0;
-    __syncthreads();
-    for (int k = 0; k < jb; ++k) {
-        const double pivot = a[k][k];
-        if (!(pivot > 0.0) || !isfinite(pivot)) {  // proj/src/linalg.cpp:82-84
-            if (tid == 0) bad = 1;
-            break;
-        }
-        const double lkk = sqrt(pivot);
-        __syncthreads();
-        if (tid == 0) a[k][k] = lkk;
-        for (int i = k + 1 + tid; i < jb; i += blockDim.x) a[i][k] = a[i][k] / lkk;
-        __syncthreads();
-        // right-looking update of the block's trailing lower part
-        const int rem = jb - k - 1;
-        for (int e = tid; e < rem * rem; e += blockDim.x) {
-            const int i = k + 1 + e / rem, j = k + 1 + e % rem;
-            if (j <= i) a[i][j] -= a[i][k] * a[j][k];
+    for (int k = 0; k < kNb; ++k) {
+        const int ks = k & 15, kb = k >> 4, buf = k & 1;
+        if (ty == ks && tx == ks) {
+            double p = 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                if (a == kb) p = v[a][a];
+            // NotPositiveDefinite: pivot <= 0 or non-finite (proj/src/linalg.cpp:82-84)
+            if (!(p > 0.0) || !isfinite(p)) bad = 1;
+            const double l = sqrt(p);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                if (a == kb) v[a][a] = l;
+            piv = l;
         }
         __syncthreads();
+        if (bad) break;
+        const double lkk = piv;
+        if (tx == ks) {  // column k of L below the diagonal
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int r = ty + 16 * a;
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if (b == kb) {
+                        if (r > k) v[a][b] = v[a][b] / lkk;
+                        if (r >= k) colk[buf][r] = v[a][b];
+                    }
+            }
+        }
+        if (ty == ks) {  // row k of L^{-1} is final once divided by l_kk
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                if (a == kb)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        x[a][b] = x[a][b] / lkk;
+                        xrow[buf][tx + 16 * b] = x[a][b];
+                    }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int r = ty + 16 * a;
+            if (r <= k) continue;
+            const double lr = colk[buf][r];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int q = tx + 16 * b;
+                if (q > k && q <= r) v[a][b] -= lr * colk[buf][q];
+                x[a][b] -= lr * xrow[buf][q];
+            }
+        }
     }
-    __syncthreads();
     if (bad) {
         if (tid == 0) {
             status[c] = 1;
@@ -262,25 +305,15 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int6
         }
         return;
     }
-    for (int e = tid; e < jb * kNb; e += blockDim.x) {
-        const int r = e / kNb, j = e % kNb;
-        if (j <= r && j < jb) A[(int64_t)r * ld + j] = a[r][j];
-    }
-    // explicit inverse of the 64x64 block for the TRSM (one column per thread)
-    if (tid < kNb) {
-        const int j = tid;
-        for (int i = 0; i < kNb; ++i) inv[i][j] = 0.0;
-        if (j < jb) {
-            for (int i = j; i < jb; ++i) {
-                double s = (i == j) ? 1.0 : 0.0;
-                for (int k = j; k < i; ++k) s -= a[i][k] * inv[k][j];
-                inv[i][j] = s / a[i][i];
-            }
-        }
-    }
-    __syncthreads();
     double* out = inv_base + (int64_t)c * kNb * kNb;
-    for (int e = tid; e < kNb * kNb; e += blockDim.x) out[e] = inv[e / kNb][e % kNb];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int r = ty + 16 * a, q = tx + 16 * b;
+            if (r < jb && q <= r) A[(int64_t)r * ld + q] = v[a][b];
+            out[r * kNb + q] = (r < jb && q < jb && q <= r) ? x[a][b] : 0.0;
+        }
 }
 
 __global__ void beta_update_kernel(double* beta, uint64_t* n_acc, double* rate_out, double* beta_out, int chains,
@@ -466,13 +499,7 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kNb * kNb);
     for (int j0 = 0; j0 < d; j0 += kNb) {
         const int jb = std::min(kNb, d - j0);
-        constexpr int smem = 2 * kNb * (kNb + 1) * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            DGB_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr = true;
-        }
-        potrf_diag_kernel<<<chains, 256, smem, s>>>(A, ld, j0, jb, mask, status, active, w.inv);
+        potrf_diag_kernel<<<chains, 256, 0, s>>>(A, ld, j0, jb, mask, status, active, w.inv);
         DGB_LAUNCH_CHECK();
         count_launch();
         const int rest = d - j0 - jb;

@@ -26,7 +26,7 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
-def lockstep(b200, tmp_path, target_kind, d, kern, P, M, K, n_lag, n0, seed, **extra):
+def lockstep(b200, tmp_path, target_kind, d, kern, P, M, K, n_lag, n0, seed, lr_tol=1e-9, **extra):
     t = b200.target_build(target_kind, d, 17) if isinstance(target_kind, str) else target_kind
     path = str(tmp_path / "t.bin")
     t.save(path)
@@ -54,10 +54,10 @@ def lockstep(b200, tmp_path, target_kind, d, kern, P, M, K, n_lag, n0, seed, **e
             assert abs(lu[first] - lr_o[first]) <= 1e-9, f"chain {p}: decision mismatch at step {first} off a tie"
             ties += 1
             continue  # trajectories legitimately diverge after a tie flip
-        assert np.max(np.abs(lr_g - lr_o)) <= 1e-9 * max(1.0, np.max(np.abs(lr_o)))
+        assert np.max(np.abs(lr_g - lr_o)) <= lr_tol * max(1.0, np.max(np.abs(lr_o)))
         assert np.array_equal(res.chain_history(p, "beta"), o["beta_hist"][p])
         assert np.array_equal(res.chain_history(p, "acceptance"), o["acc_hist"][p])
-    if ties == 0:
+    if ties == 0 and lr_tol <= 1e-9:
         gm, om = res.mean(), o["global_mean"]
         gc, oc = res.cov(), o["global_cov"]
         assert np.linalg.norm(gm - om) <= 1e-10 * max(1.0, np.linalg.norm(om))
@@ -71,8 +71,17 @@ def lockstep(b200, tmp_path, target_kind, d, kern, P, M, K, n_lag, n0, seed, **e
 
 @pytest.mark.parametrize("kern", ["diam", "am", "rw", "pcn"])
 def test_lockstep_gaussian(b200, tmp_path, kern):
-    # n_lag > d so the first adapted covariance is full rank (no rounding-decided jitter)
-    _, _, ties = lockstep(b200, tmp_path, "pi2", 16, kern, P=4, M=3, K=3, n_lag=40, n0=30, seed=11)
+    # n_lag > d and n0 on a window boundary: the first adapted covariance is full
+    # rank, so no factorization depends on rounding (no jitter ladder)
+    _, _, ties = lockstep(b200, tmp_path, "pi2", 16, kern, P=4, M=3, K=3, n_lag=40, n0=40, seed=11)
+    assert ties == 0
+
+
+def test_lockstep_rank_deficient_jitter(b200, tmp_path):
+    # the first adaptation sees 10 < d samples: the covariance is singular and whether
+    # the jitter ladder stops at eps=1e-10 or 1e-8 is decided by rounding;
+    # decisions must still agree, log alpha to the jitter scale
+    _, _, ties = lockstep(b200, tmp_path, "pi2", 16, "am", P=4, M=3, K=3, n_lag=40, n0=30, seed=11, lr_tol=1e-6)
     assert ties == 0
 
 
