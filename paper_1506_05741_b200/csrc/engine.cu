@@ -60,6 +60,7 @@ Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> com
     ld_ = pad_ld(d_);
     win_ = (int64_t)Lw_ * ld_;
     mat_ = (int64_t)d_ * ld_;
+    fmat_ = (int64_t)(d_ + 1) * ld_;
     twisted_ = tgt_.twisted();
     require(d_ <= 8192, Err::InvalidDimension, "the B200 engine supports d <= 8192");
     DGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -115,8 +116,8 @@ void Engine::upload_target() {
 void Engine::init_chains() {
     auto& A = allocs_;
     const int C = C_;
-    L_ = dalloc<double>(A, (size_t)C * mat_);
-    Lw2_ = dalloc<double>(A, (size_t)C * mat_);
+    L_ = dalloc<double>(A, (size_t)C * fmat_);
+    Lw2_ = dalloc<double>(A, (size_t)C * fmat_);
     S_ = dalloc<double>(A, (size_t)C * mat_);
     W_ = dalloc<double>(A, (size_t)C * win_);
     Xi_ = dalloc<double>(A, (size_t)C * win_);
@@ -153,8 +154,8 @@ void Engine::init_chains() {
     pw_.inv = dalloc<double>(A, (size_t)C * 64 * 64 + C);  // + int active[C] tail
     pw_.inv_ptrs = ptr_array(A, pw_.inv, 64 * 64, C);
 
-    Lp_ = ptr_array(A, L_, mat_, C);
-    Lnp_ = ptr_array(A, Lw2_, mat_, C);
+    Lp_ = ptr_array(A, L_, fmat_, C);
+    Lnp_ = ptr_array(A, Lw2_, fmat_, C);
     Wp_ = ptr_array(A, W_, win_, C);
     Xip_ = ptr_array(A, Xi_, win_, C);
     Hp_ = ptr_array(A, H_, win_, C);
@@ -182,7 +183,7 @@ void Engine::init_chains() {
     // x0 = dispersion * N(0, I) from the "init" stream (runner.cpp:131-132)
     launch_normal_vec(x_, ld_, C, d_, ikeys_, 0, cfg_.init_dispersion, stream_);
     // factor = I, beta = beta_init (proposal.cpp:95-97)
-    launch_set_identity(L_, mat_, C, d_, ld_, stream_);
+    launch_set_identity(L_, fmat_, C, d_, ld_, stream_);
     std::vector<double> b(C, k_.beta_init);
     DGB_CUDA(cudaMemcpyAsync(beta_, b.data(), C * 8, cudaMemcpyHostToDevice, stream_));
     identity_ = true;
@@ -435,15 +436,20 @@ void Engine::lag_update(size_t w) {
         const double wg = count ? (double)cnt_g_ / (double)count : 0.0;
         const double wl = count ? (double)cnt_local_ / (double)count : 1.0;
         if (k_.adapts_cov() && count >= 2) {
-            // blend -> covariance into the workspace factor, trace floor, POTRF (proposal.cpp:176-184)
+            // blend -> covariance into the workspace factor, trace floor, POTRF (proposal.cpp:176-184).
+            // pCN-form kernels append r = x - x_ref as row d: the factorization then also
+            // delivers L'^{-1} r for the usable guard (no separate triangular solve).
+            const bool aug = k_.pcn_form();
+            const double* ax = aug ? x_ : nullptr;
+            const double* axr = aug && k_.adaptive_ref ? xr_ : nullptr;
             timed_begin("blend_cov");
             launch_blend_cov(Lnp_, Sg_, mg_, S_, mat_, mean_, ld_, wg, wl, mb_, ld_, C, d_, ld_, nullptr, 0.0, nullptr,
-                             stream_);
+                             stream_, ax, axr);
             timed_end("blend_cov", 0.0);
             launch_trace_floor(Lnp_, ld_, mb_, ld_, C, d_, tr_, try_, stream_);
             DGB_CUDA(cudaMemsetAsync(status_, 0, C * sizeof(int), stream_));
             timed_begin("potrf");
-            potrf_batched(Lnp_, ld_, d_, C, try_, status_, pw_, stream_);
+            potrf_batched(Lnp_, ld_, d_, C, try_, status_, pw_, stream_, aug ? 1 : 0);
             timed_end("potrf", (double)C * d_ * (double)d_ * d_ / 3.0);
             // jitter escalation for chains whose factorization failed (proposal.cpp:218-239)
             std::vector<int> st(C), tf(C);
@@ -459,11 +465,11 @@ void Engine::lag_update(size_t w) {
             for (double eps = 1e-10; any && eps <= 1e-4; eps *= 100.0) {
                 DGB_CUDA(cudaMemcpyAsync(mask_, failing.data(), C * sizeof(int), cudaMemcpyHostToDevice, stream_));
                 launch_blend_cov(Lnp_, Sg_, mg_, S_, mat_, mean_, ld_, wg, wl, mb_, ld_, C, d_, ld_, mask_, eps, tr_,
-                                 stream_);
+                                 stream_, ax, axr);
                 // failing chains restart from a clean status; the others keep status 0
                 std::vector<int> zero(C, 0);
                 DGB_CUDA(cudaMemcpyAsync(status_, zero.data(), C * sizeof(int), cudaMemcpyHostToDevice, stream_));
-                potrf_batched(Lnp_, ld_, d_, C, mask_, status_, pw_, stream_);
+                potrf_batched(Lnp_, ld_, d_, C, mask_, status_, pw_, stream_, aug ? 1 : 0);
                 DGB_CUDA(cudaMemcpyAsync(st.data(), status_, C * sizeof(int), cudaMemcpyDeviceToHost, stream_));
                 DGB_CUDA(cudaStreamSynchronize(stream_));
                 any = false;
@@ -484,13 +490,15 @@ void Engine::lag_update(size_t w) {
             // final status: every tried chain factored
             DGB_CUDA(cudaMemsetAsync(status_, 0, C * sizeof(int), stream_));
             double qmax = -1.0;
-            if (k_.pcn_form()) {
-                // usable guard: 1/2 |L'^-1 (x - x_ref)|^2 / infl^2 <= 5 d (proposal.cpp:185-199)
-                launch_trsv(Lnp_, ld_, x_, k_.adaptive_ref ? xr_ : nullptr, ld_, nullptr, qtmp_, C, d_,
-                            0.5 / (infl * infl), try_, stream_);
+            if (aug) {
+                // usable guard: 1/2 |L'^-1 (x - x_ref)|^2 / infl^2 <= 5 d (proposal.cpp:185-199),
+                // L'^-1 (x - x_ref) being the augmented row the POTRF just solved
+                launch_aug_quad(Lnp_, ld_, d_, C, 0.5 / (infl * infl), try_, qtmp_, stream_);
                 qmax = 5.0 * d_;
             }
             launch_accept_factor(Lp_, Lnp_, try_, status_, qtmp_, qmax, C, usable_, stream_);
+            // adopted factors come with y = L^-1 (x - x_ref) and the quad term for free
+            if (aug && !k_.adaptive_ref) launch_aug_adopt(Lp_, ld_, d_, C, usable_, qtmp_, y_, quad_, stream_);
             identity_ = false;
         }
         // adaptive reference point (proposal.cpp:206-208)
@@ -502,8 +510,11 @@ void Engine::lag_update(size_t w) {
         }
     }
     if (ref_moved) refresh_g(xr_, gr_);
-    // quad with the current factor (proposal.cpp:211) and y for the next window's recursion
-    if (k_.pcn_form()) {
+    // quad with the current factor (proposal.cpp:211) and y for the next window's recursion.
+    // With a fixed reference point y = L^-1 (x - x_ref) is carried exactly through the
+    // steps (c y + s w) and re-anchored from the augmented POTRF row whenever the factor
+    // changes, so only a moving reference point needs a fresh triangular solve.
+    if (k_.pcn_form() && k_.adaptive_ref) {
         timed_begin("trsv");
         launch_trsv(Lp_, ld_, x_, k_.adaptive_ref ? xr_ : nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl),
                     nullptr, stream_);

@@ -86,6 +86,7 @@ private:
     int rank_ = 0, world_ = 1;
     int d_ = 0, Lw_ = 0, C_ = 0, P_ = 0, c0_ = 0;
     int64_t ld_ = 0, win_ = 0, mat_ = 0;
+    int64_t fmat_ = 0;  // factor stride: d rows + the augmented row r = x - x_ref
     bool twisted_ = false, identity_ = true;
     cudaStream_t stream_ = nullptr;
 

@@ -77,7 +77,7 @@ void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg,
                       const double* Sl, int64_t sl_stride, const double* ml, int64_t ml_stride,
                       double wg, double wl, double* mb, int64_t mb_stride, int chains, int d,
                       int64_t ld, const int* mask, double jitter_eps, const double* tr,
-                      cudaStream_t s);
+                      cudaStream_t s, const double* aug_x = nullptr, const double* aug_xr = nullptr);
 // tr[c] = sum_i C_ii (sequential order); try[c] = trace > 1e-12(1 + mb.mb) && finite
 void launch_trace_floor(double* const* Cm, int64_t ld, const double* mb, int64_t mb_stride,
                         int chains, int d, double* tr, int* try_flag, cudaStream_t s);
@@ -107,7 +107,13 @@ struct PotrfWork {
     double** inv_ptrs;
 };
 void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status,
-                   PotrfWork& w, cudaStream_t s);
+                   PotrfWork& w, cudaStream_t s, int extra_rows = 0);
+// q_c = half_inv_infl2 * |row d of L_c|^2 (the augmented row = L^{-1}(x - x_ref))
+void launch_aug_quad(double* const* L, int64_t ld, int d, int chains, double half_inv_infl2, const int* mask,
+                     double* q, cudaStream_t s);
+// for chains with usable[c]: y_c = row d of L_c (post-swap), quad_c = q_c
+void launch_aug_adopt(double* const* L, int64_t ld, int d, int chains, const int* usable, const double* q,
+                      double* y, double* quad, cudaStream_t s);
 
 // ---------------------------------------------------------------- lag update
 // beta adaptation + rate (proj/src/proposal.cpp:163-173)

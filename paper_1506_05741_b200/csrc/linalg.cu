@@ -31,11 +31,16 @@ __global__ void mean_update_kernel(double* mean, int64_t mean_stride, const doub
 __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const double* mg, const double* Sl,
                                  int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl,
                                  double* mb, int64_t mb_stride, int d, int64_t ld, const int* mask,
-                                 double jitter_eps, const double* tr) {
+                                 double jitter_eps, const double* tr, const double* ax, const double* axr) {
     const int c = blockIdx.z;
     if (mask && !mask[c]) return;
     const int i = blockIdx.y;  // row
     double* Crow = C_out[c] + (int64_t)i * ld;
+    if (i == d) {  // augmented row r = x - x_ref (solved by the POTRF for the usable guard)
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x)
+            Crow[j] = ax[c * ld + j] - (axr ? axr[c * ld + j] : 0.0);
+        return;
+    }
     const double* Sgr = Sg + (int64_t)i * ld;
     const double* Slr = Sl + c * sl_stride + (int64_t)i * ld;
     const double* mlc = ml + c * ml_stride;
@@ -244,45 +249,38 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int6
             x[a][b] = (r == q) ? 1.0 : 0.0;
         }
     if (tid == 0) bad = 0;
+    // Fully unrolled over the 64 columns so every register index is static. A bad
+    // pivot only raises `bad`; the (discarded) arithmetic runs on to the end.
+#pragma unroll
     for (int k = 0; k < kNb; ++k) {
         const int ks = k & 15, kb = k >> 4, buf = k & 1;
         if (ty == ks && tx == ks) {
-            double p = 0.0;
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-                if (a == kb) p = v[a][a];
+            const double p = v[kb][kb];
             // NotPositiveDefinite: pivot <= 0 or non-finite (proj/src/linalg.cpp:82-84)
             if (!(p > 0.0) || !isfinite(p)) bad = 1;
             const double l = sqrt(p);
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-                if (a == kb) v[a][a] = l;
-            piv = l;
+            v[kb][kb] = l;
+            piv = 1.0 / l;
+            colk[buf][k] = l;
         }
         __syncthreads();
-        if (bad) break;
-        const double lkk = piv;
+        const double rl = piv;
         if (tx == ks) {  // column k of L below the diagonal
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
                 const int r = ty + 16 * a;
-#pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    if (b == kb) {
-                        if (r > k) v[a][b] = v[a][b] / lkk;
-                        if (r >= k) colk[buf][r] = v[a][b];
-                    }
+                if (r > k) {
+                    v[a][kb] *= rl;
+                    colk[buf][r] = v[a][kb];
+                }
             }
         }
-        if (ty == ks) {  // row k of L^{-1} is final once divided by l_kk
+        if (ty == ks) {  // row k of L^{-1} is final once scaled by 1/l_kk
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
-                if (a == kb)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        x[a][b] = x[a][b] / lkk;
-                        xrow[buf][tx + 16 * b] = x[a][b];
-                    }
+            for (int b = 0; b < 4; ++b) {
+                x[kb][b] *= rl;
+                xrow[buf][tx + 16 * b] = x[kb][b];
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -311,9 +309,36 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int6
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int r = ty + 16 * a, q = tx + 16 * b;
-            if (r < jb && q <= r) A[(int64_t)r * ld + q] = v[a][b];
+            // the block's strict upper part holds left-looking GEMM garbage: store exact zeros
+            if (r < jb && q < jb) A[(int64_t)r * ld + q] = q <= r ? v[a][b] : 0.0;
             out[r * kNb + q] = (r < jb && q < jb && q <= r) ? x[a][b] : 0.0;
         }
+}
+
+__global__ void aug_quad_kernel(double* const* Lm, int64_t ld, int d, double hq, const int* mask, double* q) {
+    const int c = blockIdx.x;
+    if (mask && !mask[c]) return;
+    const double* row = Lm[c] + (int64_t)d * ld;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) s += row[i] * row[i];
+    __shared__ double red[32];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        q[c] = hq * t;
+    }
+}
+
+__global__ void aug_adopt_kernel(double* const* Lm, int64_t ld, int d, const int* usable, const double* q, double* y,
+                                 double* quad) {
+    const int c = blockIdx.y;
+    if (!usable[c]) return;
+    const double* row = Lm[c] + (int64_t)d * ld;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x) y[c * ld + i] = row[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) quad[c] = q[c];
 }
 
 __global__ void beta_update_kernel(double* beta, uint64_t* n_acc, double* rate_out, double* beta_out, int chains,
@@ -437,10 +462,10 @@ void launch_mean_update(double* mean, int64_t mean_stride, const double* X, int6
 void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg, const double* Sl,
                       int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl, double* mb,
                       int64_t mb_stride, int chains, int d, int64_t ld, const int* mask, double jitter_eps,
-                      const double* tr, cudaStream_t s) {
-    dim3 grid((unsigned)ceil_div(d, 256), d, chains);
+                      const double* tr, cudaStream_t s, const double* aug_x, const double* aug_xr) {
+    dim3 grid((unsigned)ceil_div(d, 256), d + (aug_x ? 1 : 0), chains);
     blend_cov_kernel<<<grid, 256, 0, s>>>(C_out, Sg, mg, Sl, sl_stride, ml, ml_stride, wg, wl, mb, mb_stride, d, ld,
-                                          mask, jitter_eps, tr);
+                                          mask, jitter_eps, tr, aug_x, aug_xr);
     DGB_LAUNCH_CHECK();
     count_launch();
 }
@@ -494,15 +519,43 @@ void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr
 }
 
 void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status, PotrfWork& w,
-                   cudaStream_t s) {
+                   cudaStream_t s, int extra_rows) {
+    // Left-looking blocked Cholesky, 64-wide block columns J = [j0, j0+64):
+    //   (1) A[j0:, J] -= L[j0:, :j0] L[J, :j0]^T   DMMA GEMM, K = j0 (large), N = 64
+    //   (2) L[J, J] = chol(A[J, J]), inv(L[J, J])  one CTA per chain, registers
+    //   (3) L[j0+64:, J] = A[j0+64:, J] inv(L[J,J])^T   DMMA GEMM (TRSM via the inverse)
+    // `extra_rows` augmented rows r^T below row d-1 ride along as ordinary rows of the
+    // GEMMs and TRSMs and come out as (L^{-1} r)^T: the forward substitution of the
+    // usable-factor guard (proj/src/proposal.cpp:185-199) costs no extra pass over L.
     // w.inv holds chains*64*64 doubles, followed (by the caller's allocation) by an int active[chains]
     int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kNb * kNb);
+    const int rows = d + extra_rows;
     for (int j0 = 0; j0 < d; j0 += kNb) {
         const int jb = std::min(kNb, d - j0);
+        if (j0 > 0) {
+            GemmBatch p{};
+            p.A = (const double* const*)A;
+            p.B = (const double* const*)A;
+            p.C = A;
+            p.a_off = (int64_t)j0 * ld;
+            p.b_off = (int64_t)j0 * ld;
+            p.c_off = (int64_t)j0 * ld + j0;
+            p.lda = ld;
+            p.ldb = ld;
+            p.ldc = ld;
+            p.M = rows - j0;
+            p.N = jb;
+            p.K = j0;
+            p.alpha = -1.0;
+            p.beta = 1.0;
+            p.active = active;
+            // the diagonal block only needs its lower triangle, but rows below need all of J
+            gemm_f64(p, chains, true, true, s, GemmShape::Narrow);
+        }
         potrf_diag_kernel<<<chains, 256, 0, s>>>(A, ld, j0, jb, mask, status, active, w.inv);
         DGB_LAUNCH_CHECK();
         count_launch();
-        const int rest = d - j0 - jb;
+        const int rest = rows - j0 - jb;
         if (rest <= 0) break;
         // TRSM in place: L21 = A21 * inv(L11)^T  (one 64-wide column tile per CTA -> safe in place)
         GemmBatch t{};
@@ -522,26 +575,22 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
         t.beta = 0.0;
         t.active = active;
         gemm_f64(t, chains, true, true, s, GemmShape::Narrow);
-        // trailing update A22 -= L21 L21^T (lower tiles only)
-        GemmBatch u{};
-        u.A = (const double* const*)A;
-        u.B = (const double* const*)A;
-        u.C = A;
-        u.a_off = t.a_off;
-        u.b_off = t.a_off;
-        u.c_off = (int64_t)(j0 + jb) * ld + (j0 + jb);
-        u.lda = ld;
-        u.ldb = ld;
-        u.ldc = ld;
-        u.M = rest;
-        u.N = rest;
-        u.K = jb;
-        u.alpha = -1.0;
-        u.beta = 1.0;
-        u.active = active;
-        u.tri_c_lower = 1;
-        gemm_f64(u, chains, true, true, s);
     }
+}
+
+void launch_aug_quad(double* const* L, int64_t ld, int d, int chains, double half_inv_infl2, const int* mask,
+                     double* q, cudaStream_t s) {
+    aug_quad_kernel<<<chains, 256, 0, s>>>(L, ld, d, half_inv_infl2, mask, q);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_aug_adopt(double* const* L, int64_t ld, int d, int chains, const int* usable, const double* q, double* y,
+                      double* quad, cudaStream_t s) {
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(d, 256), 16)), chains);
+    aug_adopt_kernel<<<grid, 256, 0, s>>>(L, ld, d, usable, q, y, quad);
+    DGB_LAUNCH_CHECK();
+    count_launch();
 }
 
 void launch_beta_update(double* beta, uint64_t* n_acc, double* rate_out, double* beta_out, int chains, int n_lag,
