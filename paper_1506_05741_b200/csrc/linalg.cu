@@ -226,9 +226,11 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int6
                                                          double* inv_base) {
     // Register-blocked right-looking Cholesky of the 64x64 diagonal block, fused with
     // the explicit inverse of the factor (for the DMMA TRSM that follows). Thread
-    // (ty, tx) of a 16x16 grid owns rows ty+16a and columns tx+16b (a, b < 4) of
-    // both L and L^{-1} in registers; each column step broadcasts the new column of
-    // L and the finished row of L^{-1} through shared memory: two barriers per column.
+    // (ty, tx) of a 16x16 grid owns the contiguous 4x4 sub-block rows 4ty+a, columns
+    // 4tx+b of both L and L^{-1} in registers. Columns are processed 4 at a time with
+    // the 4 steps unrolled, so register indices are static and the loop body stays
+    // small; each column step broadcasts the new column of L and the finished row of
+    // L^{-1} through shared memory (two barriers per column).
     const int c = blockIdx.x;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const bool run = (!mask || mask[c]) && status[c] == 0;
@@ -243,59 +245,69 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int6
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const int r = ty + 16 * a, q = tx + 16 * b;
+            const int r = 4 * ty + a, q = 4 * tx + b;
             // rows/cols past jb are padded with the identity so the 64x64 factorization stays valid
             v[a][b] = (r < jb && q <= r) ? A[(int64_t)r * ld + q] : (r == q ? 1.0 : 0.0);
             x[a][b] = (r == q) ? 1.0 : 0.0;
         }
     if (tid == 0) bad = 0;
-    // Fully unrolled over the 64 columns so every register index is static. A bad
-    // pivot only raises `bad`; the (discarded) arithmetic runs on to the end.
+    for (int kg = 0; kg < kNb / 4; ++kg) {
 #pragma unroll
-    for (int k = 0; k < kNb; ++k) {
-        const int ks = k & 15, kb = k >> 4, buf = k & 1;
-        if (ty == ks && tx == ks) {
-            const double p = v[kb][kb];
-            // NotPositiveDefinite: pivot <= 0 or non-finite (proj/src/linalg.cpp:82-84)
-            if (!(p > 0.0) || !isfinite(p)) bad = 1;
-            const double l = sqrt(p);
-            v[kb][kb] = l;
-            piv = 1.0 / l;
-            colk[buf][k] = l;
-        }
-        __syncthreads();
-        const double rl = piv;
-        if (tx == ks) {  // column k of L below the diagonal
+        for (int kk = 0; kk < 4; ++kk) {
+            const int k = 4 * kg + kk, buf = kk & 1;
+            if (ty == kg && tx == kg) {
+                const double p = v[kk][kk];
+                // NotPositiveDefinite: pivot <= 0 or non-finite (proj/src/linalg.cpp:82-84);
+                // a bad pivot only raises `bad`, the discarded arithmetic runs on
+                if (!(p > 0.0) || !isfinite(p)) bad = 1;
+                const double l = __dsqrt_rn(p);
+                v[kk][kk] = l;
+                piv = __drcp_rn(l);
+                colk[buf][k] = l;
+            }
+            __syncthreads();
+            const double rl = piv;
+            if (tx == kg) {  // column k of L below the diagonal
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const int r = ty + 16 * a;
-                if (r > k) {
-                    v[a][kb] *= rl;
-                    colk[buf][r] = v[a][kb];
+                for (int a = 0; a < 4; ++a) {
+                    const int r = 4 * ty + a;
+                    if (r > k) {
+                        v[a][kk] *= rl;
+                        colk[buf][r] = v[a][kk];
+                    }
+                }
+            }
+            if (ty == kg) {  // row k of L^{-1} is final once scaled by 1/l_kk
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    x[kk][b] *= rl;
+                    xrow[buf][4 * tx + b] = x[kk][b];
+                }
+            }
+            __syncthreads();
+            if (4 * ty + 3 > k) {
+                double cq[4], xq[4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    cq[b] = colk[buf][4 * tx + b];
+                    xq[b] = xrow[buf][4 * tx + b];
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const int r = 4 * ty + a;
+                    if (r <= k) continue;
+                    const double lr = colk[buf][r];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int q = 4 * tx + b;
+                        if (q > k && q <= r) v[a][b] -= lr * cq[b];
+                        x[a][b] -= lr * xq[b];
+                    }
                 }
             }
         }
-        if (ty == ks) {  // row k of L^{-1} is final once scaled by 1/l_kk
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                x[kb][b] *= rl;
-                xrow[buf][tx + 16 * b] = x[kb][b];
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int r = ty + 16 * a;
-            if (r <= k) continue;
-            const double lr = colk[buf][r];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int q = tx + 16 * b;
-                if (q > k && q <= r) v[a][b] -= lr * colk[buf][q];
-                x[a][b] -= lr * xrow[buf][q];
-            }
-        }
     }
+    __syncthreads();
     if (bad) {
         if (tid == 0) {
             status[c] = 1;
@@ -305,14 +317,16 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int6
     }
     double* out = inv_base + (int64_t)c * kNb * kNb;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a) {
+        const int r = 4 * ty + a;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const int r = ty + 16 * a, q = tx + 16 * b;
+            const int q = 4 * tx + b;
             // the block's strict upper part holds left-looking GEMM garbage: store exact zeros
             if (r < jb && q < jb) A[(int64_t)r * ld + q] = q <= r ? v[a][b] : 0.0;
             out[r * kNb + q] = (r < jb && q < jb && q <= r) ? x[a][b] : 0.0;
         }
+    }
 }
 
 __global__ void aug_quad_kernel(double* const* Lm, int64_t ld, int d, double hq, const int* mask, double* q) {
@@ -530,51 +544,61 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     // w.inv holds chains*64*64 doubles, followed (by the caller's allocation) by an int active[chains]
     int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kNb * kNb);
     const int rows = d + extra_rows;
-    for (int j0 = 0; j0 < d; j0 += kNb) {
-        const int jb = std::min(kNb, d - j0);
-        if (j0 > 0) {
-            GemmBatch p{};
-            p.A = (const double* const*)A;
-            p.B = (const double* const*)A;
-            p.C = A;
-            p.a_off = (int64_t)j0 * ld;
-            p.b_off = (int64_t)j0 * ld;
-            p.c_off = (int64_t)j0 * ld + j0;
-            p.lda = ld;
-            p.ldb = ld;
-            p.ldc = ld;
-            p.M = rows - j0;
-            p.N = jb;
-            p.K = j0;
-            p.alpha = -1.0;
-            p.beta = 1.0;
-            p.active = active;
-            // the diagonal block only needs its lower triangle, but rows below need all of J
-            gemm_f64(p, chains, true, true, s, GemmShape::Narrow);
-        }
-        potrf_diag_kernel<<<chains, 256, 0, s>>>(A, ld, j0, jb, mask, status, active, w.inv);
+    // A[r0:rows, c0:c0+n] -= L[r0:rows, k0:k0+k] L[c0:c0+n, k0:k0+k]^T
+    auto update = [&](int r0, int c0, int n, int k0, int k, GemmShape shape) {
+        GemmBatch p{};
+        p.A = (const double* const*)A;
+        p.B = (const double* const*)A;
+        p.C = A;
+        p.a_off = (int64_t)r0 * ld + k0;
+        p.b_off = (int64_t)c0 * ld + k0;
+        p.c_off = (int64_t)r0 * ld + c0;
+        p.lda = p.ldb = p.ldc = ld;
+        p.M = rows - r0;
+        p.N = n;
+        p.K = k;
+        p.alpha = -1.0;
+        p.beta = 1.0;
+        p.active = active;
+        gemm_f64(p, chains, true, true, s, shape);
+    };
+    // factor the 64-wide diagonal block at (c0, c0) and solve the rows below it (in place)
+    auto factor_and_solve = [&](int c0, int n) {
+        potrf_diag_kernel<<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv);
         DGB_LAUNCH_CHECK();
         count_launch();
-        const int rest = rows - j0 - jb;
-        if (rest <= 0) break;
-        // TRSM in place: L21 = A21 * inv(L11)^T  (one 64-wide column tile per CTA -> safe in place)
+        const int rest = rows - c0 - n;
+        if (rest <= 0) return;
+        // TRSM: L21 = A21 inv(L11)^T  (one 64-wide column tile per CTA -> safe in place)
         GemmBatch t{};
         t.A = (const double* const*)A;
         t.B = (const double* const*)w.inv_ptrs;
         t.C = A;
-        t.a_off = (int64_t)(j0 + jb) * ld + j0;
-        t.b_off = 0;
+        t.a_off = (int64_t)(c0 + n) * ld + c0;
         t.c_off = t.a_off;
         t.lda = ld;
         t.ldb = kNb;
         t.ldc = ld;
         t.M = rest;
-        t.N = jb;
-        t.K = jb;
+        t.N = n;
+        t.K = n;
         t.alpha = 1.0;
         t.beta = 0.0;
         t.active = active;
         gemm_f64(t, chains, true, true, s, GemmShape::Narrow);
+    };
+    // 128-wide block columns: the bulk of the flops is one left-looking DMMA GEMM per
+    // block column with K = j0 on full 128x128 tiles; inside, two 64-wide halves are
+    // factored right-looking (diag + TRSM, 64-deep update of the second half).
+    for (int j0 = 0; j0 < d; j0 += 2 * kNb) {
+        const int jb = std::min(2 * kNb, d - j0);
+        if (j0 > 0) update(j0, j0, jb, 0, j0, GemmShape::Big);
+        const int h1 = std::min(kNb, jb);
+        factor_and_solve(j0, h1);
+        if (jb > kNb) {
+            update(j0 + kNb, j0 + kNb, jb - kNb, j0, kNb, GemmShape::Narrow);
+            factor_and_solve(j0 + kNb, jb - kNb);
+        }
     }
 }
 

@@ -57,6 +57,9 @@ __global__ void draws_kernel(int kind, double* out_f64, uint64_t* out_u64, int64
 constexpr int kStepThreads = 512;
 constexpr int kStepWarps = kStepThreads / 32;
 
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 
@@ -225,11 +228,225 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// TMA-fed variant: one elected thread streams the window rows (xi_t, w_t, h_t) into an
+// NS-deep shared-memory ring with cp.async.bulk (1-D TMA) and mbarrier transaction
+// counts, NS-1 steps ahead of the consumers, so the step loop never waits on HBM.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+template <int R, bool TWISTED>
+__global__ void __launch_bounds__(kStepThreads, 1) mh_window_tma_kernel(StepParams p, int NS) {
+    const int c = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int d = p.d;
+    const int64_t ld = p.ld;
+    const bool pcn = p.pcn != 0;
+    const int nrows = pcn ? 3 : 2;  // xi, h (+ w for the pCN-form y recursion)
+    extern __shared__ __align__(128) double ring[];
+    __shared__ __align__(8) uint64_t full[8];
+    __shared__ double red[2][kStepWarps][2];
+    const uint32_t row_bytes = (uint32_t)(ld * sizeof(double));
+    double* stage0 = ring;
+    const int64_t stage_len = (int64_t)nrows * ld;
+
+    const double beta = p.beta[c];
+    const double cc = pcn ? sqrt(fmax(0.0, 1.0 - beta * beta)) : 1.0;  // proj/src/proposal.cpp:120
+    const double sc = beta * p.infl;
+    const double hq = 0.5 / (p.infl * p.infl);
+    const double* Wc = p.W + c * p.win_stride;
+    double* Xc = p.Xi + c * p.win_stride;
+    const double* Hc = p.H + c * p.win_stride;
+
+    auto issue = [&](int t) {  // producer: row t of the window into stage t % NS
+        const int s = t % NS;
+        double* st = stage0 + s * stage_len;
+        mbar_expect_tx(&full[s], row_bytes * nrows);
+        tma_row(st, Xc + (int64_t)t * ld, row_bytes, &full[s]);
+        tma_row(st + ld, Hc + (int64_t)t * ld, row_bytes, &full[s]);
+        if (pcn) tma_row(st + 2 * ld, Wc + (int64_t)t * ld, row_bytes, &full[s]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int t = 0; t < NS && t < p.n_lag; ++t) issue(t);
+
+    double2 x[R], g[R], y[R], xr[R], gr[R], ie[R], bc[R];
+    bool valid[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = 2 * (tid + r * kStepThreads);
+        valid[r] = e < d;
+        const double2 z2 = make_double2(0.0, 0.0);
+        x[r] = valid[r] ? ld2(p.x + c * ld + e) : z2;
+        g[r] = valid[r] ? ld2(p.g + c * ld + e) : z2;
+        y[r] = (valid[r] && pcn) ? ld2(p.y + c * ld + e) : z2;
+        xr[r] = (valid[r] && p.xr) ? ld2(p.xr + c * ld + e) : z2;
+        gr[r] = (valid[r] && p.gr) ? ld2(p.gr + c * ld + e) : z2;
+        if (TWISTED) {
+            ie[r] = valid[r] ? ld2(p.inv_eig + e) : z2;
+            bc[r] = valid[r] ? ld2(p.bcoef + e) : z2;
+        }
+    }
+    double lp = p.log_pi[c], q = pcn ? p.quad[c] : 0.0;
+    uint64_t nacc = p.n_accepted[c];
+    const PhiloxKey uk = p.ukeys[c];
+    const uint64_t u0 = p.uctr[c];
+
+    for (int t = 0; t < p.n_lag; ++t) {
+        const double logu = log(philox_uniform_open(uk, u0 + (uint64_t)t));
+        const int s = t % NS;
+        mbar_wait(&full[s], (uint32_t)((t / NS) & 1));
+        const double* st = stage0 + s * stage_len;
+        double2 xc[R], gc[R], yc[R];
+        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = 2 * (tid + r * kStepThreads);
+            const double2 xi = valid[r] ? ld2(st + e) : make_double2(0.0, 0.0);
+            const double2 h = valid[r] ? ld2(st + ld + e) : make_double2(0.0, 0.0);
+            // exact reference candidate (proj/src/proposal.cpp:119-124), no FMA contraction
+            xc[r].x = __dadd_rn(__dadd_rn(xr[r].x, __dmul_rn(cc, __dadd_rn(x[r].x, -xr[r].x))), xi.x);
+            xc[r].y = __dadd_rn(__dadd_rn(xr[r].y, __dmul_rn(cc, __dadd_rn(x[r].y, -xr[r].y))), xi.y);
+            gc[r].x = gr[r].x + cc * (g[r].x - gr[r].x) + h.x;
+            gc[r].y = gr[r].y + cc * (g[r].y - gr[r].y) + h.y;
+            if (TWISTED) {
+                const double w0 = gc[r].x;
+                const double w1 = gc[r].y + bc[r].x * gc[r].x * gc[r].x;
+                sa += w0 * w0 * ie[r].x + w1 * w1 * ie[r].y;
+            } else {
+                sa += xc[r].x * gc[r].x + xc[r].y * gc[r].y;
+            }
+            if (pcn) {
+                const double2 w = valid[r] ? ld2(st + 2 * ld + e) : make_double2(0.0, 0.0);
+                yc[r].x = cc * y[r].x + sc * w.x;
+                yc[r].y = cc * y[r].y + sc * w.y;
+                sb += yc[r].x * yc[r].x + yc[r].y * yc[r].y;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+            sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        }
+        const int buf = t & 1;
+        if (lane == 0) {
+            red[buf][warp][0] = sa;
+            red[buf][warp][1] = sb;
+        }
+        __syncthreads();
+        // every thread is done with stage s: refill it NS steps ahead
+        if (tid == 0 && t + NS < p.n_lag) issue(t + NS);
+        double ta = 0.0, tb = 0.0;
+#pragma unroll
+        for (int k = 0; k < kStepWarps; ++k) {
+            ta += red[buf][k][0];
+            tb += red[buf][k][1];
+        }
+        const double lpc = -0.5 * ta;
+        const double qc = pcn ? hq * tb : 0.0;
+        const double ratio = pcn ? (lpc + qc) - (lp + q) : lpc - lp;  // proj/src/proposal.cpp:77-82
+        const bool acc = logu < ratio;                               // strict, :146
+        if (acc) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                x[r] = xc[r];
+                g[r] = gc[r];
+                if (pcn) y[r] = yc[r];
+            }
+            lp = lpc;
+            q = qc;
+            ++nacc;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = 2 * (tid + r * kStepThreads);
+            if (valid[r]) {
+                if (e + 1 < d) st2(Xc + (int64_t)t * ld + e, x[r]);
+                else Xc[(int64_t)t * ld + e] = x[r].x;
+            }
+        }
+        if (tid == 0) {
+            if (p.trace_lp) p.trace_lp[(int64_t)c * p.n_lag + t] = lp;
+            if (p.accept_out) p.accept_out[(int64_t)c * p.n_lag + t] = acc ? 1 : 0;
+            if (p.log_ratio_out) p.log_ratio_out[(int64_t)c * p.n_lag + t] = ratio;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = 2 * (tid + r * kStepThreads);
+        if (!valid[r]) continue;
+        if (e + 1 < d) {
+            st2(p.x + c * ld + e, x[r]);
+            st2(p.g + c * ld + e, g[r]);
+            if (pcn) st2(p.y + c * ld + e, y[r]);
+        } else {
+            p.x[c * ld + e] = x[r].x;
+            p.g[c * ld + e] = g[r].x;
+            if (pcn) p.y[c * ld + e] = y[r].x;
+        }
+    }
+    if (tid == 0) {
+        p.log_pi[c] = lp;
+        if (pcn) p.quad[c] = q;
+        p.n_accepted[c] = nacc;
+        p.uctr[c] = u0 + (uint64_t)p.n_lag;
+    }
+}
+
+template <int R, bool TW>
+bool try_tma(const StepParams& p, cudaStream_t s) {
+    const int nrows = p.pcn ? 3 : 2;
+    const size_t stage = (size_t)nrows * p.ld * sizeof(double);
+    constexpr size_t kMaxSmem = 200 * 1024;
+    const int NS = (int)std::min<size_t>(8, kMaxSmem / stage);
+    if (NS < 2) return false;
+    const size_t smem = NS * stage;
+    auto kern = mh_window_tma_kernel<R, TW>;
+    DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<p.chains, kStepThreads, smem, s>>>(p, NS);
+    return true;
+}
+
 template <bool TW>
 void launch_r(const StepParams& p, cudaStream_t s) {
     const int pairs = (p.d + 1) / 2;
     const int R = (pairs + kStepThreads - 1) / kStepThreads;
     dim3 grid(p.chains), block(kStepThreads);
+    bool done = false;
+    if (R <= 1) done = try_tma<1, TW>(p, s);
+    else if (R <= 2) done = try_tma<2, TW>(p, s);
+    else if (R <= 4) done = try_tma<4, TW>(p, s);
+    if (done) {
+        DGB_LAUNCH_CHECK();
+        count_launch();
+        return;
+    }
     if (R <= 1) mh_window_kernel<1, TW, true><<<grid, block, 0, s>>>(p);
     else if (R <= 2) mh_window_kernel<2, TW, true><<<grid, block, 0, s>>>(p);
     else if (R <= 4) mh_window_kernel<4, TW, true><<<grid, block, 0, s>>>(p);
