@@ -223,7 +223,7 @@ constexpr int kNb = 64;
 
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
                                                          const int* mask, int* status, int* active,
-                                                         double* inv_base) {
+                                                         double* inv_base, int zero_above) {
     // Register-blocked right-looking Cholesky of the 64x64 diagonal block, fused with
     // the explicit inverse of the factor (for the DMMA TRSM that follows). Thread
     // (ty, tx) of a 16x16 grid owns the contiguous 4x4 sub-block rows 4ty+a, columns
@@ -325,6 +325,9 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int6
             // the block's strict upper part holds left-looking GEMM garbage: store exact zeros
             if (r < jb && q < jb) A[(int64_t)r * ld + q] = q <= r ? v[a][b] : 0.0;
             out[r * kNb + q] = (r < jb && q < jb && q <= r) ? x[a][b] : 0.0;
+            // second half of a 128-wide block column: the 64 rows above this block were
+            // also touched by the block column's GEMM and lie above the diagonal
+            if (zero_above && q < jb) A[(int64_t)(r - kNb) * ld + q] = 0.0;
         }
     }
 }
@@ -563,8 +566,8 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
         gemm_f64(p, chains, true, true, s, shape);
     };
     // factor the 64-wide diagonal block at (c0, c0) and solve the rows below it (in place)
-    auto factor_and_solve = [&](int c0, int n) {
-        potrf_diag_kernel<<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv);
+    auto factor_and_solve = [&](int c0, int n, int zero_above) {
+        potrf_diag_kernel<<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
         DGB_LAUNCH_CHECK();
         count_launch();
         const int rest = rows - c0 - n;
@@ -594,10 +597,10 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
         const int jb = std::min(2 * kNb, d - j0);
         if (j0 > 0) update(j0, j0, jb, 0, j0, GemmShape::Big);
         const int h1 = std::min(kNb, jb);
-        factor_and_solve(j0, h1);
+        factor_and_solve(j0, h1, 0);
         if (jb > kNb) {
             update(j0 + kNb, j0 + kNb, jb - kNb, j0, kNb, GemmShape::Narrow);
-            factor_and_solve(j0 + kNb, jb - kNb);
+            factor_and_solve(j0 + kNb, jb - kNb, j0 > 0 ? 1 : 0);
         }
     }
 }

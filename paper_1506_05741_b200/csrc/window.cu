@@ -257,17 +257,18 @@ __device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t byt
                  : "memory");
 }
 
-template <int R, bool TWISTED>
-__global__ void __launch_bounds__(kStepThreads, 1) mh_window_tma_kernel(StepParams p, int NS) {
+template <int R, bool TWISTED, int T>
+__global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int NS) {
+    constexpr int NW = T / 32;
     const int c = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int d = p.d;
     const int64_t ld = p.ld;
     const bool pcn = p.pcn != 0;
     const int nrows = pcn ? 3 : 2;  // xi, h (+ w for the pCN-form y recursion)
-    extern __shared__ __align__(128) double ring[];
+    extern __shared__ __align__(128) double ring[];  // NS stages, then the log-uniform table
     __shared__ __align__(8) uint64_t full[8];
-    __shared__ double red[2][kStepWarps][2];
+    __shared__ double red[2][NW][2];
     const uint32_t row_bytes = (uint32_t)(ld * sizeof(double));
     double* stage0 = ring;
     const int64_t stage_len = (int64_t)nrows * ld;
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_tma_kernel(StepPara
     bool valid[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int e = 2 * (tid + r * kStepThreads);
+        const int e = 2 * (tid + r * T);
         valid[r] = e < d;
         const double2 z2 = make_double2(0.0, 0.0);
         x[r] = valid[r] ? ld2(p.x + c * ld + e) : z2;
@@ -317,9 +318,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_tma_kernel(StepPara
     uint64_t nacc = p.n_accepted[c];
     const PhiloxKey uk = p.ukeys[c];
     const uint64_t u0 = p.uctr[c];
+    // log u of every step of the window, from the chain's uniform stream (bit-exact u),
+    // computed once in parallel instead of redundantly by every thread every step
+    double* logu_tab = ring + (int64_t)NS * stage_len;
+    for (int t = tid; t < p.n_lag; t += T) logu_tab[t] = log(philox_uniform_open(uk, u0 + (uint64_t)t));
+    __syncthreads();
 
     for (int t = 0; t < p.n_lag; ++t) {
-        const double logu = log(philox_uniform_open(uk, u0 + (uint64_t)t));
+        const double logu = logu_tab[t];
         const int s = t % NS;
         mbar_wait(&full[s], (uint32_t)((t / NS) & 1));
         const double* st = stage0 + s * stage_len;
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_tma_kernel(StepPara
         double sa = 0.0, sb = 0.0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int e = 2 * (tid + r * kStepThreads);
+            const int e = 2 * (tid + r * T);
             const double2 xi = valid[r] ? ld2(st + e) : make_double2(0.0, 0.0);
             const double2 h = valid[r] ? ld2(st + ld + e) : make_double2(0.0, 0.0);
             // exact reference candidate (proj/src/proposal.cpp:119-124), no FMA contraction
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_tma_kernel(StepPara
         if (tid == 0 && t + NS < p.n_lag) issue(t + NS);
         double ta = 0.0, tb = 0.0;
 #pragma unroll
-        for (int k = 0; k < kStepWarps; ++k) {
+        for (int k = 0; k < NW; ++k) {
             ta += red[buf][k][0];
             tb += red[buf][k][1];
         }
@@ -385,7 +391,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_tma_kernel(StepPara
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int e = 2 * (tid + r * kStepThreads);
+            const int e = 2 * (tid + r * T);
             if (valid[r]) {
                 if (e + 1 < d) st2(Xc + (int64_t)t * ld + e, x[r]);
                 else Xc[(int64_t)t * ld + e] = x[r].x;
@@ -399,7 +405,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_tma_kernel(StepPara
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int e = 2 * (tid + r * kStepThreads);
+        const int e = 2 * (tid + r * T);
         if (!valid[r]) continue;
         if (e + 1 < d) {
             st2(p.x + c * ld + e, x[r]);
@@ -419,17 +425,18 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_tma_kernel(StepPara
     }
 }
 
-template <int R, bool TW>
+template <int R, bool TW, int T>
 bool try_tma(const StepParams& p, cudaStream_t s) {
     const int nrows = p.pcn ? 3 : 2;
     const size_t stage = (size_t)nrows * p.ld * sizeof(double);
-    constexpr size_t kMaxSmem = 200 * 1024;
-    const int NS = (int)std::min<size_t>(8, kMaxSmem / stage);
-    if (NS < 2) return false;
-    const size_t smem = NS * stage;
-    auto kern = mh_window_tma_kernel<R, TW>;
+    const size_t table = (size_t)p.n_lag * sizeof(double);
+    constexpr size_t kMaxSmem = 220 * 1024;
+    if (table + 2 * stage > kMaxSmem) return false;
+    const int NS = (int)std::min<size_t>(8, (kMaxSmem - table) / stage);
+    const size_t smem = NS * stage + table;
+    auto kern = mh_window_tma_kernel<R, TW, T>;
     DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<p.chains, kStepThreads, smem, s>>>(p, NS);
+    kern<<<p.chains, T, smem, s>>>(p, NS);
     return true;
 }
 
@@ -438,10 +445,13 @@ void launch_r(const StepParams& p, cudaStream_t s) {
     const int pairs = (p.d + 1) / 2;
     const int R = (pairs + kStepThreads - 1) / kStepThreads;
     dim3 grid(p.chains), block(kStepThreads);
+    // 256 threads (2 double2 pairs each) up to d = 1024, then 512 threads: fewer warps per
+    // step barrier and reduction for the small dimensions where the step loop matters most
     bool done = false;
-    if (R <= 1) done = try_tma<1, TW>(p, s);
-    else if (R <= 2) done = try_tma<2, TW>(p, s);
-    else if (R <= 4) done = try_tma<4, TW>(p, s);
+    if (pairs <= 256) done = try_tma<1, TW, 256>(p, s);
+    else if (pairs <= 512) done = try_tma<2, TW, 256>(p, s);
+    else if (R <= 2) done = try_tma<2, TW, 512>(p, s);
+    else if (R <= 4) done = try_tma<4, TW, 512>(p, s);
     if (done) {
         DGB_LAUNCH_CHECK();
         count_launch();
