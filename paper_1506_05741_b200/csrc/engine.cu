@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "gemm_f64.cuh"
@@ -64,19 +65,32 @@ Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> com
     twisted_ = tgt_.twisted();
     require(d_ <= 8192, Err::InvalidDimension, "the B200 engine supports d <= 8192");
     DGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    DGB_CUDA(cudaEventCreateWithFlags(&main_ev_, cudaEventDisableTiming));
     upload_target();
     init_chains();
+    // two chain groups on two streams overlap one group's latency-bound pieces with the
+    // other's GEMMs (DIAM_B200_GROUPS overrides, 1 = a single stream)
+    int ng = C_ >= 8 ? 2 : 1;
+    if (const char* e = std::getenv("DIAM_B200_GROUPS")) ng = std::max(1, std::min(C_, std::atoi(e)));
+    make_groups(ng);
 }
 
 Engine::~Engine() {
     if (stream_) cudaStreamSynchronize(stream_);
+    for (auto& g : groups_) {
+        if (g.s) {
+            cudaStreamSynchronize(g.s);
+            cudaStreamDestroy(g.s);
+        }
+        if (g.done) cudaEventDestroy(g.done);
+    }
     for (void* p : allocs_) cudaFree(p);
     for (auto& e : event_pool_) cudaEventDestroy(e);
     for (auto& pe : pending_) {
         cudaEventDestroy(pe.a);
         cudaEventDestroy(pe.b);
     }
-    if (h_stage_) cudaFreeHost(h_stage_);
+    if (main_ev_) cudaEventDestroy(main_ev_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -141,7 +155,7 @@ void Engine::init_chains() {
     status_ = dalloc<int>(A, C);
     try_ = dalloc<int>(A, C);
     usable_ = dalloc<int>(A, C);
-    mask_ = dalloc<int>(A, C);
+    fatal_ = dalloc<int>(A, 1);
     Sg_ = dalloc<double>(A, mat_);
     mg_ = dalloc<double>(A, ld_);
     Ssum_ = dalloc<double>(A, mat_ + ld_);
@@ -151,19 +165,12 @@ void Engine::init_chains() {
     trace_pj_ = dalloc<double>(A, M * C * Lw_ * 2);
     hist_rate_ = dalloc<double>(A, M * C);
     hist_beta_ = dalloc<double>(A, M * C);
-    pw_.inv = dalloc<double>(A, (size_t)C * 64 * 64 + C);  // + int active[C] tail
-    pw_.inv_ptrs = ptr_array(A, pw_.inv, 64 * 64, C);
 
     Lp_ = ptr_array(A, L_, fmat_, C);
     Lnp_ = ptr_array(A, Lw2_, fmat_, C);
     Wp_ = ptr_array(A, W_, win_, C);
     Xip_ = ptr_array(A, Xi_, win_, C);
-    Hp_ = ptr_array(A, H_, win_, C);
     Sp_ = ptr_array(A, S_, mat_, C);
-    xp_ = ptr_array(A, x_, 0, 1);
-    gp_ = ptr_array(A, g_, 0, 1);
-    xrp_ = ptr_array(A, xr_, 0, 1);
-    grp_ = ptr_array(A, gr_, 0, 1);
 
     // RNG keys: global chain index p = c0 + i (runner.cpp:128-130, 556-559)
     std::vector<PhiloxKey> nk(C), uk(C), ik(C);
@@ -188,7 +195,9 @@ void Engine::init_chains() {
     DGB_CUDA(cudaMemcpyAsync(beta_, b.data(), C * 8, cudaMemcpyHostToDevice, stream_));
     identity_ = true;
     // log pi(x0), quad(x0) (proposal.cpp:107-108)
-    refresh_g(x_, g_);
+    double** xp = ptr_array(A, x_, 0, 1);
+    double** gp = ptr_array(A, g_, 0, 1);
+    refresh_g(xp, gp, C, stream_);
     launch_eval_logpi(x_, g_, inv_eig_, bcoef_, twisted_, logpi_, C, d_, ld_, stream_);
     if (k_.pcn_form()) {
         const double infl = k_.noise_infl();
@@ -207,34 +216,59 @@ void Engine::init_chains() {
     traces_.assign(C, std::vector<std::vector<double>>(fnames_.size()));
 }
 
-void Engine::refresh_g(const double* vec, double* out) {
-    // out[c] = G vec[c] for all local chains: rows = chains, (vec G^T)
+void Engine::make_groups(int n) {
+    auto& A = allocs_;
+    groups_.resize(n);
+    for (int i = 0; i < n; ++i) {
+        Group& g = groups_[i];
+        g.off = (int)((int64_t)C_ * i / n);
+        g.C = (int)((int64_t)C_ * (i + 1) / n) - g.off;
+        DGB_CUDA(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking));
+        DGB_CUDA(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
+        g.Lp = Lp_ + g.off;
+        g.Lnp = Lnp_ + g.off;
+        g.Wp = Wp_ + g.off;
+        g.Xip = Xip_ + g.off;
+        g.Sp = Sp_ + g.off;
+        g.xp = ptr_array(A, x_ + g.off * ld_, 0, 1);
+        g.gp = ptr_array(A, g_ + g.off * ld_, 0, 1);
+        g.xrp = ptr_array(A, xr_ + g.off * ld_, 0, 1);
+        g.grp = ptr_array(A, gr_ + g.off * ld_, 0, 1);
+        g.Xib = ptr_array(A, Xi_ + g.off * win_, 0, 1);
+        g.Hb = ptr_array(A, H_ + g.off * win_, 0, 1);
+        // per-group inverse-block scratch (+ int active[C] tail): groups factor concurrently
+        g.pw.inv = dalloc<double>(A, (size_t)g.C * 64 * 64 + g.C);
+        g.pw.inv_ptrs = ptr_array(A, g.pw.inv, 64 * 64, g.C);
+    }
+}
+
+void Engine::refresh_g(double* const* vec, double* const* out, int chains, cudaStream_t s) {
+    // out = vec G^T: rows = chains (G x for every chain of the group)
     GemmBatch g{};
-    const double* const* vp = (vec == x_) ? (const double* const*)xp_ : (const double* const*)xrp_;
-    g.A = vp;
+    g.A = (const double* const*)vec;
     g.B = (const double* const*)Gp_;
-    g.C = (out == g_) ? gp_ : grp_;
+    g.C = out;
     g.lda = ld_;
     g.ldb = ld_;
     g.ldc = ld_;
-    g.M = C_;
+    g.M = chains;
     g.N = d_;
     g.K = d_;
     g.alpha = 1.0;
     g.beta = 0.0;
-    gemm("gemv_state", g, 1, true, true, GemmShape::Narrow);
+    gemm("gemv_state", g, 1, true, true, s, GemmShape::Narrow);
 }
 
-void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, GemmShape sh) {
+void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s, GemmShape sh) {
     double flops = 2.0 * g.M * (double)g.N * g.K * batch;
     if (g.tri_c_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
     if (g.tri_b_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
-    timed_begin(name);
-    gemm_f64(g, batch, ak, bk, stream_, sh);
-    timed_end(name, flops);
+    timed_begin(s);
+    gemm_f64(g, batch, ak, bk, s, sh);
+    timed_end(name, flops, s);
 }
 
-void Engine::timed_begin(const char*) {
+void Engine::timed_begin(cudaStream_t s) {
     if (!profiling_) return;
     if (event_pool_.size() < 2) {
         for (int i = 0; i < 64; ++i) {
@@ -243,30 +277,31 @@ void Engine::timed_begin(const char*) {
             event_pool_.push_back(e);
         }
     }
-    cur_a_ = event_pool_.back();
+    cudaEvent_t a = event_pool_.back();
     event_pool_.pop_back();
-    DGB_CUDA(cudaEventRecord(cur_a_, stream_));
+    DGB_CUDA(cudaEventRecord(a, s));
+    open_[s] = a;
 }
 
-void Engine::timed_end(const char* name, double flops) {
+void Engine::timed_end(const char* name, double flops, cudaStream_t s) {
     if (!profiling_) return;
     cudaEvent_t b = event_pool_.back();
     event_pool_.pop_back();
-    DGB_CUDA(cudaEventRecord(b, stream_));
-    pending_.push_back({name, cur_a_, b, flops});
+    DGB_CUDA(cudaEventRecord(b, s));
+    pending_.push_back({name, open_.at(s), b, flops});
     if (pending_.size() > 4096) resolve_events();
 }
 
 void Engine::resolve_events() {
     if (pending_.empty()) return;
-    DGB_CUDA(cudaStreamSynchronize(stream_));
+    DGB_CUDA(cudaDeviceSynchronize());
     for (auto& p : pending_) {
         float ms = 0.f;
         DGB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
-        auto& s = stats_[p.name];
-        s.ms += ms;
-        s.flops += p.flops;
-        s.launches += 1;
+        auto& st = stats_[p.name];
+        st.ms += ms;
+        st.flops += p.flops;
+        st.launches += 1;
         event_pool_.push_back(p.a);
         event_pool_.push_back(p.b);
     }
@@ -279,26 +314,70 @@ const std::map<std::string, KernelStat>& Engine::stats() {
 }
 
 double Engine::flops_per_batch() const {
-    // algorithmic FP64 flops of one batch over the local chains (DESIGN.md §4):
-    // TRMM d(d+1)/2*2 per row, target GEMM 2 d^2 per row, SYRK d(d+1) per row, POTRF d^3/3 per window
+    // algorithmic FP64 flops of one batch over the local chains (DESIGN.md §2):
+    // TRMM d(d+1) per row, target GEMM 2 d^2 per row, SYRK d(d+1) per row, POTRF d^3/3 per window
     const double d = d_, L = Lw_, C = C_, M = (double)cfg_.intervals_per_batch;
     const double per_window = C * (L * d * (d + 1) + L * 2.0 * d * d + L * d * (d + 1) + d * d * d / 3.0);
     return per_window * M;
 }
 
-void Engine::window(size_t w, bool record) {
-    const int C = C_;
+void Engine::fork_groups() {
+    DGB_CUDA(cudaEventRecord(main_ev_, stream_));
+    for (auto& g : groups_) DGB_CUDA(cudaStreamWaitEvent(g.s, main_ev_, 0));
+}
+
+void Engine::join_groups() {
+    for (auto& g : groups_) {
+        DGB_CUDA(cudaEventRecord(g.done, g.s));
+        DGB_CUDA(cudaStreamWaitEvent(stream_, g.done, 0));
+    }
+}
+
+Engine::WindowPlan Engine::plan_window(size_t w, bool record) const {
+    WindowPlan p;
+    p.w = w;
+    p.record = record;
+    p.n_start = n_;
+    p.n_end = n_ + Lw_;
+    p.nctr = nctr_;
+    // post-burn-in rows: step t counts iff n_start + t + 1 > n0 (proposal.cpp:153-155)
+    p.first = (int)std::clamp<int64_t>((int64_t)k_.n0 - (int64_t)p.n_start, 0, Lw_);
+    p.k = Lw_ - p.first;
+    p.cnt_before = cnt_local_;
+    p.cnt_after = cnt_local_ + (uint64_t)p.k;
+    const bool wants = k_.adapts_cov() || k_.adaptive_ref;
+    if (wants && p.n_end >= k_.n0) {  // proposal.cpp:174-209, with counts after this window
+        const uint64_t count = p.cnt_after + cnt_g_;
+        p.wg = count ? (double)cnt_g_ / (double)count : 0.0;
+        p.wl = count ? (double)p.cnt_after / (double)count : 1.0;
+        p.refactor = k_.adapts_cov() && count >= 2;
+        p.move_ref = k_.adaptive_ref && p.n_end >= k_.n_ref_start && count > 0;
+    }
+    return p;
+}
+
+void Engine::commit_window(const WindowPlan& p) {
+    n_ = p.n_end;
+    nctr_ += (uint64_t)Lw_ * d_;
+    cnt_local_ = p.cnt_after;
+    window_n_start_[p.w] = p.n_start;
+    if (p.refactor) identity_ = false;
+}
+
+void Engine::enqueue_window(Group& g, const WindowPlan& p) {
+    const int C = g.C, o = g.off;
+    const cudaStream_t s = g.s;
     const double infl = k_.noise_infl();
     // ---- noise window: W from Philox, Xi = s W L^T, H = Xi G^T (proposal.cpp:254-266)
-    timed_begin("normals");
-    launch_normals(W_, identity_ ? Xi_ : nullptr, win_, C, Lw_, d_, ld_, nkeys_, nctr_, beta_, infl, stream_);
-    timed_end("normals", 0.0);
-    nctr_ += (uint64_t)Lw_ * d_;
+    timed_begin(s);
+    launch_normals(W_ + o * win_, identity_ ? Xi_ + o * win_ : nullptr, win_, C, Lw_, d_, ld_, nkeys_ + o, p.nctr,
+                   beta_ + o, infl, s);
+    timed_end("normals", 0.0, s);
     if (!identity_) {
         GemmBatch t{};
-        t.A = (const double* const*)Wp_;
-        t.B = (const double* const*)Lp_;
-        t.C = Xip_;
+        t.A = (const double* const*)g.Wp;
+        t.B = (const double* const*)g.Lp;
+        t.C = g.Xip;
         t.lda = ld_;
         t.ldb = ld_;
         t.ldc = ld_;
@@ -306,222 +385,162 @@ void Engine::window(size_t w, bool record) {
         t.N = d_;
         t.K = d_;
         t.alpha = 1.0;
-        t.alpha_vec = beta_;
+        t.alpha_vec = beta_ + o;
         t.alpha_vec_mul = infl;
         t.beta = 0.0;
         t.tri_b_lower = 1;
-        gemm("trmm_noise", t, C, true, true);
+        gemm("trmm_noise", t, C, true, true, s);
     }
     {
         GemmBatch h{};
-        h.A = (const double* const*)Xip_;
+        h.A = (const double* const*)g.Xib;
         h.B = (const double* const*)Gp_;
-        h.C = Hp_;
+        h.C = g.Hb;
         h.lda = ld_;
         h.ldb = ld_;
         h.ldc = ld_;
-        h.M = C * Lw_;  // all chains' windows are one contiguous (C Lw) x ld matrix
+        h.M = C * Lw_;  // the group's windows are one contiguous (C Lw) x ld matrix
         h.N = d_;
         h.K = d_;
         h.alpha = 1.0;
         h.beta = 0.0;
-        gemm("gemm_target", h, 1, true, true);
-    }
-    if (capture_) {
-        if (cap_w_.empty()) {
-            cap_w_.assign(C, {});
-            cap_ratio_.assign(C, {});
-            cap_acc_.assign(C, {});
-        }
-        std::vector<double> buf((size_t)C * win_);
-        DGB_CUDA(cudaMemcpyAsync(buf.data(), W_, buf.size() * 8, cudaMemcpyDeviceToHost, stream_));
-        DGB_CUDA(cudaStreamSynchronize(stream_));
-        for (int c = 0; c < C; ++c)
-            for (int r = 0; r < Lw_; ++r)
-                cap_w_[c].insert(cap_w_[c].end(), buf.begin() + (size_t)c * win_ + (size_t)r * ld_,
-                                 buf.begin() + (size_t)c * win_ + (size_t)r * ld_ + d_);
-        if (!dbg_ratio_) {
-            dbg_ratio_ = dalloc<double>(allocs_, (size_t)C * Lw_);
-            dbg_acc_ = dalloc<uint8_t>(allocs_, (size_t)C * Lw_);
-        }
+        gemm("gemm_target", h, 1, true, true, s);
     }
 
     // ---- the n_lag MH steps (proposal.cpp:137-157, runner.cpp:363-368)
-    StepParams p{};
-    p.d = d_;
-    p.n_lag = Lw_;
-    p.chains = C;
-    p.ld = ld_;
-    p.win_stride = win_;
-    p.W = W_;
-    p.Xi = Xi_;
-    p.H = H_;
-    p.x = x_;
-    p.g = g_;
-    p.y = y_;
-    const bool has_ref = k_.adaptive_ref;
-    p.xr = has_ref ? xr_ : nullptr;
-    p.gr = has_ref ? gr_ : nullptr;
-    p.log_pi = logpi_;
-    p.quad = quad_;
-    p.beta = beta_;
-    p.n_accepted = nacc_;
-    p.ukeys = ukeys_;
-    p.uctr = uctr_;
-    p.infl = infl;
-    p.pcn = k_.pcn_form() ? 1 : 0;
-    p.inv_eig = inv_eig_;
-    p.bcoef = bcoef_;
-    p.trace_lp = record ? trace_lp_ + w * (size_t)C * Lw_ : nullptr;
-    p.accept_out = capture_ ? dbg_acc_ : nullptr;
-    p.log_ratio_out = capture_ ? dbg_ratio_ : nullptr;
-    timed_begin("mh_window");
-    launch_mh_window(p, twisted_, stream_);
-    timed_end("mh_window", 0.0);
-    if (capture_) {
-        std::vector<double> r((size_t)C * Lw_);
-        std::vector<uint8_t> a((size_t)C * Lw_);
-        DGB_CUDA(cudaMemcpyAsync(r.data(), dbg_ratio_, r.size() * 8, cudaMemcpyDeviceToHost, stream_));
-        DGB_CUDA(cudaMemcpyAsync(a.data(), dbg_acc_, a.size(), cudaMemcpyDeviceToHost, stream_));
-        DGB_CUDA(cudaStreamSynchronize(stream_));
-        for (int c = 0; c < C; ++c) {
-            cap_ratio_[c].insert(cap_ratio_[c].end(), r.begin() + (size_t)c * Lw_, r.begin() + (size_t)(c + 1) * Lw_);
-            cap_acc_[c].insert(cap_acc_[c].end(), a.begin() + (size_t)c * Lw_, a.begin() + (size_t)(c + 1) * Lw_);
-        }
-    }
-    const uint64_t n_start = n_;
-    n_ += Lw_;
-    window_n_start_[w] = n_start;
+    StepParams sp{};
+    sp.d = d_;
+    sp.n_lag = Lw_;
+    sp.chains = C;
+    sp.ld = ld_;
+    sp.win_stride = win_;
+    sp.W = W_ + o * win_;
+    sp.Xi = Xi_ + o * win_;
+    sp.H = H_ + o * win_;
+    sp.x = x_ + o * ld_;
+    sp.g = g_ + o * ld_;
+    sp.y = y_ + o * ld_;
+    sp.xr = k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
+    sp.gr = k_.adaptive_ref ? gr_ + o * ld_ : nullptr;
+    sp.log_pi = logpi_ + o;
+    sp.quad = quad_ + o;
+    sp.beta = beta_ + o;
+    sp.n_accepted = nacc_ + o;
+    sp.ukeys = ukeys_ + o;
+    sp.uctr = uctr_ + o;
+    sp.infl = infl;
+    sp.pcn = k_.pcn_form() ? 1 : 0;
+    sp.inv_eig = inv_eig_;
+    sp.bcoef = bcoef_;
+    sp.trace_lp = p.record ? trace_lp_ + (p.w * C_ + o) * (size_t)Lw_ : nullptr;
+    sp.accept_out = capture_ ? dbg_acc_ + (size_t)o * Lw_ : nullptr;
+    sp.log_ratio_out = capture_ ? dbg_ratio_ + (size_t)o * Lw_ : nullptr;
+    timed_begin(s);
+    launch_mh_window(sp, twisted_, s);
+    timed_end("mh_window", 0.0, s);
 
-    // ---- moments of the post-burn-in states: rows t with n_start + t + 1 > n0 (proposal.cpp:153-155)
-    const int64_t first = std::clamp<int64_t>((int64_t)k_.n0 - (int64_t)n_start, 0, Lw_);
-    const int k = Lw_ - (int)first;
-    if (k > 0) {
-        const double total = (double)cnt_local_ + k;
-        GemmBatch s{};
-        s.A = (const double* const*)Xip_;
-        s.B = (const double* const*)Xip_;
-        s.C = Sp_;
-        s.a_off = first * ld_;
-        s.b_off = first * ld_;
-        s.lda = ld_;
-        s.ldb = ld_;
-        s.ldc = ld_;
-        s.M = d_;
-        s.N = d_;
-        s.K = k;
-        s.alpha = 1.0 / total;
-        s.beta = (double)cnt_local_ / total;
-        s.tri_c_lower = 1;
-        gemm("syrk_moments", s, C, false, false);
-        launch_mean_update(mean_, ld_, Xi_, win_, ld_, C, d_, (int)first, k, (double)cnt_local_, stream_);
-        cnt_local_ += k;
+    // ---- moments of the post-burn-in states (proposal.cpp:153-155)
+    if (p.k > 0) {
+        const double total = (double)p.cnt_after;
+        GemmBatch m{};
+        m.A = (const double* const*)g.Xip;
+        m.B = (const double* const*)g.Xip;
+        m.C = g.Sp;
+        m.a_off = (int64_t)p.first * ld_;
+        m.b_off = (int64_t)p.first * ld_;
+        m.lda = ld_;
+        m.ldb = ld_;
+        m.ldc = ld_;
+        m.M = d_;
+        m.N = d_;
+        m.K = p.k;
+        m.alpha = 1.0 / total;
+        m.beta = (double)p.cnt_before / total;
+        m.tri_c_lower = 1;
+        gemm("syrk_moments", m, C, false, false, s);
+        launch_mean_update(mean_ + o * ld_, ld_, Xi_ + o * win_, win_, ld_, C, d_, p.first, p.k,
+                           (double)p.cnt_before, s);
     }
-    if (record && cfg_.trace_eigen_projections)
-        launch_project_rows(Xi_, win_, ld_, C, Lw_, (int)first, d_, proj_, trace_pj_ + w * (size_t)C * Lw_ * 2,
-                            stream_);
-    lag_update(w);
-}
+    if (p.record && cfg_.trace_eigen_projections)
+        launch_project_rows(Xi_ + o * win_, win_, ld_, C, Lw_, p.first, d_, proj_,
+                            trace_pj_ + (p.w * C_ + o) * (size_t)Lw_ * 2, s);
 
-void Engine::lag_update(size_t w) {
-    const int C = C_;
-    const double infl = k_.noise_infl();
-    // beta against the acceptance band (proposal.cpp:162-173)
-    launch_beta_update(beta_, nacc_, hist_rate_ + w * C, hist_beta_ + w * C, C, Lw_, k_.adapt_beta ? 1 : 0,
-                       k_.band_lo, k_.band_hi, k_.beta_adapt_factor, k_.beta_min, k_.beta_max, stream_);
-    const bool wants = k_.adapts_cov() || k_.adaptive_ref;
-    bool ref_moved = false;
-    if (wants && n_ >= k_.n0) {
-        const uint64_t count = cnt_local_ + cnt_g_;
-        const double wg = count ? (double)cnt_g_ / (double)count : 0.0;
-        const double wl = count ? (double)cnt_local_ / (double)count : 1.0;
-        if (k_.adapts_cov() && count >= 2) {
-            // blend -> covariance into the workspace factor, trace floor, POTRF (proposal.cpp:176-184).
-            // pCN-form kernels append r = x - x_ref as row d: the factorization then also
-            // delivers L'^{-1} r for the usable guard (no separate triangular solve).
-            const bool aug = k_.pcn_form();
-            const double* ax = aug ? x_ : nullptr;
-            const double* axr = aug && k_.adaptive_ref ? xr_ : nullptr;
-            timed_begin("blend_cov");
-            launch_blend_cov(Lnp_, Sg_, mg_, S_, mat_, mean_, ld_, wg, wl, mb_, ld_, C, d_, ld_, nullptr, 0.0, nullptr,
-                             stream_, ax, axr);
-            timed_end("blend_cov", 0.0);
-            launch_trace_floor(Lnp_, ld_, mb_, ld_, C, d_, tr_, try_, stream_);
-            DGB_CUDA(cudaMemsetAsync(status_, 0, C * sizeof(int), stream_));
-            timed_begin("potrf");
-            potrf_batched(Lnp_, ld_, d_, C, try_, status_, pw_, stream_, aug ? 1 : 0);
-            timed_end("potrf", (double)C * d_ * (double)d_ * d_ / 3.0);
-            // jitter escalation for chains whose factorization failed (proposal.cpp:218-239)
-            std::vector<int> st(C), tf(C);
-            DGB_CUDA(cudaMemcpyAsync(st.data(), status_, C * sizeof(int), cudaMemcpyDeviceToHost, stream_));
-            DGB_CUDA(cudaMemcpyAsync(tf.data(), try_, C * sizeof(int), cudaMemcpyDeviceToHost, stream_));
-            DGB_CUDA(cudaStreamSynchronize(stream_));
-            std::vector<int> failing(C, 0);
-            bool any = false;
-            for (int c = 0; c < C; ++c) {
-                failing[c] = tf[c] && st[c];
-                any |= failing[c] != 0;
-            }
-            for (double eps = 1e-10; any && eps <= 1e-4; eps *= 100.0) {
-                DGB_CUDA(cudaMemcpyAsync(mask_, failing.data(), C * sizeof(int), cudaMemcpyHostToDevice, stream_));
-                launch_blend_cov(Lnp_, Sg_, mg_, S_, mat_, mean_, ld_, wg, wl, mb_, ld_, C, d_, ld_, mask_, eps, tr_,
-                                 stream_, ax, axr);
-                // failing chains restart from a clean status; the others keep status 0
-                std::vector<int> zero(C, 0);
-                DGB_CUDA(cudaMemcpyAsync(status_, zero.data(), C * sizeof(int), cudaMemcpyHostToDevice, stream_));
-                potrf_batched(Lnp_, ld_, d_, C, mask_, status_, pw_, stream_, aug ? 1 : 0);
-                DGB_CUDA(cudaMemcpyAsync(st.data(), status_, C * sizeof(int), cudaMemcpyDeviceToHost, stream_));
-                DGB_CUDA(cudaStreamSynchronize(stream_));
-                any = false;
-                for (int c = 0; c < C; ++c) {
-                    if (failing[c] && !st[c]) failing[c] = 0;
-                    any |= failing[c] != 0;
-                }
-            }
-            if (any) {
-                int c = 0;
-                while (!failing[c]) ++c;
-                double trh = 0.0;
-                DGB_CUDA(cudaMemcpy(&trh, tr_ + c, 8, cudaMemcpyDeviceToHost));
-                fail(Err::NotPositiveDefinite, "chain " + std::to_string(c0_ + c) +
-                                                   ": covariance not factorizable after jitter escalation (dim " +
-                                                   std::to_string(d_) + ", trace " + std::to_string(trh) + ")");
-            }
-            // final status: every tried chain factored
-            DGB_CUDA(cudaMemsetAsync(status_, 0, C * sizeof(int), stream_));
-            double qmax = -1.0;
-            if (aug) {
-                // usable guard: 1/2 |L'^-1 (x - x_ref)|^2 / infl^2 <= 5 d (proposal.cpp:185-199),
-                // L'^-1 (x - x_ref) being the augmented row the POTRF just solved
-                launch_aug_quad(Lnp_, ld_, d_, C, 0.5 / (infl * infl), try_, qtmp_, stream_);
-                qmax = 5.0 * d_;
-            }
-            launch_accept_factor(Lp_, Lnp_, try_, status_, qtmp_, qmax, C, usable_, stream_);
-            // adopted factors come with y = L^-1 (x - x_ref) and the quad term for free
-            if (aug && !k_.adaptive_ref) launch_aug_adopt(Lp_, ld_, d_, C, usable_, qtmp_, y_, quad_, stream_);
-            identity_ = false;
+    // ---- lag update (proposal.cpp:159-216)
+    launch_beta_update(beta_ + o, nacc_ + o, hist_rate_ + p.w * C_ + o, hist_beta_ + p.w * C_ + o, C, Lw_,
+                       k_.adapt_beta ? 1 : 0, k_.band_lo, k_.band_hi, k_.beta_adapt_factor, k_.beta_min, k_.beta_max,
+                       s);
+    if (p.refactor) {
+        // blend -> covariance into the workspace factor, trace floor, POTRF (proposal.cpp:176-184).
+        // pCN-form kernels append r = x - x_ref as row d: the factorization then also
+        // delivers L'^{-1} r for the usable guard (no separate triangular solve).
+        const bool aug = k_.pcn_form();
+        const double* ax = aug ? x_ + o * ld_ : nullptr;
+        const double* axr = aug && k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
+        timed_begin(s);
+        launch_blend_cov(g.Lnp, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, mb_ + o * ld_, ld_, C,
+                         d_, ld_, nullptr, 0.0, nullptr, s, ax, axr);
+        timed_end("blend_cov", 0.0, s);
+        launch_trace_floor(g.Lnp, ld_, mb_ + o * ld_, ld_, C, d_, tr_ + o, try_ + o, s);
+        DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
+        timed_begin(s);
+        potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+        timed_end("potrf", (double)C * d_ * (double)d_ * d_ / 3.0, s);
+        // jitter escalation for chains whose factorization failed, on the device (proposal.cpp:218-239)
+        launch_potrf_rescue(g.Lnp, ld_, d_, aug ? 1 : 0, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg,
+                            p.wl, tr_ + o, ax, axr, status_ + o, fatal_, C, s);
+        double qmax = -1.0;
+        if (aug) {
+            // usable guard: 1/2 |L'^-1 (x - x_ref)|^2 / infl^2 <= 5 d (proposal.cpp:185-199),
+            // L'^-1 (x - x_ref) being the augmented row the POTRF just solved
+            launch_aug_quad(g.Lnp, ld_, d_, C, 0.5 / (infl * infl), try_ + o, qtmp_ + o, s);
+            qmax = 5.0 * d_;
         }
-        // adaptive reference point (proposal.cpp:206-208)
-        if (k_.adaptive_ref && n_ >= k_.n_ref_start && count > 0) {
-            if (!(k_.adapts_cov() && count >= 2))
-                launch_blend_mean(mg_, mean_, wg, wl, mb_, C, d_, ld_, stream_);
-            DGB_CUDA(cudaMemcpyAsync(xr_, mb_, (size_t)C * ld_ * 8, cudaMemcpyDeviceToDevice, stream_));
-            ref_moved = true;
-        }
+        launch_accept_factor(g.Lp, g.Lnp, try_ + o, status_ + o, qtmp_ + o, qmax, C, usable_ + o, s);
+        // adopted factors come with y = L^-1 (x - x_ref) and the quad term for free
+        if (aug && !k_.adaptive_ref)
+            launch_aug_adopt(g.Lp, ld_, d_, C, usable_ + o, qtmp_ + o, y_ + o * ld_, quad_ + o, s);
     }
-    if (ref_moved) refresh_g(xr_, gr_);
+    // adaptive reference point (proposal.cpp:206-208)
+    if (p.move_ref) {
+        if (!p.refactor) launch_blend_mean(mg_, mean_ + o * ld_, p.wg, p.wl, mb_ + o * ld_, C, d_, ld_, s);
+        DGB_CUDA(cudaMemcpyAsync(xr_ + o * ld_, mb_ + o * ld_, (size_t)C * ld_ * 8, cudaMemcpyDeviceToDevice, s));
+        refresh_g(g.xrp, g.grp, C, s);
+    }
     // quad with the current factor (proposal.cpp:211) and y for the next window's recursion.
     // With a fixed reference point y = L^-1 (x - x_ref) is carried exactly through the
     // steps (c y + s w) and re-anchored from the augmented POTRF row whenever the factor
     // changes, so only a moving reference point needs a fresh triangular solve.
     if (k_.pcn_form() && k_.adaptive_ref) {
-        timed_begin("trsv");
-        launch_trsv(Lp_, ld_, x_, k_.adaptive_ref ? xr_ : nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl),
-                    nullptr, stream_);
-        timed_end("trsv", 0.0);
+        timed_begin(s);
+        launch_trsv(g.Lp, ld_, x_ + o * ld_, xr_ + o * ld_, ld_, y_ + o * ld_, quad_ + o, C, d_, 0.5 / (infl * infl),
+                    nullptr, s);
+        timed_end("trsv", 0.0, s);
     }
     // G x re-anchored at every boundary so the step recursion never drifts
-    refresh_g(x_, g_);
+    refresh_g(g.xp, g.gp, C, s);
+}
+
+void Engine::capture_window(size_t) {
+    // parity-test capture: needs the window's W (still resident) and the step records
+    DGB_CUDA(cudaDeviceSynchronize());
+    const int C = C_;
+    if (cap_w_.empty()) {
+        cap_w_.assign(C, {});
+        cap_ratio_.assign(C, {});
+        cap_acc_.assign(C, {});
+    }
+    std::vector<double> buf((size_t)C * win_), r((size_t)C * Lw_);
+    std::vector<uint8_t> a((size_t)C * Lw_);
+    DGB_CUDA(cudaMemcpy(buf.data(), W_, buf.size() * 8, cudaMemcpyDeviceToHost));
+    DGB_CUDA(cudaMemcpy(r.data(), dbg_ratio_, r.size() * 8, cudaMemcpyDeviceToHost));
+    DGB_CUDA(cudaMemcpy(a.data(), dbg_acc_, a.size(), cudaMemcpyDeviceToHost));
+    for (int c = 0; c < C; ++c) {
+        for (int row = 0; row < Lw_; ++row)
+            cap_w_[c].insert(cap_w_[c].end(), buf.begin() + (size_t)c * win_ + (size_t)row * ld_,
+                             buf.begin() + (size_t)c * win_ + (size_t)row * ld_ + d_);
+        cap_ratio_[c].insert(cap_ratio_[c].end(), r.begin() + (size_t)c * Lw_, r.begin() + (size_t)(c + 1) * Lw_);
+        cap_acc_[c].insert(cap_acc_[c].end(), a.begin() + (size_t)c * Lw_, a.begin() + (size_t)(c + 1) * Lw_);
+    }
 }
 
 void Engine::merge_batch() {
@@ -530,13 +549,13 @@ void Engine::merge_batch() {
     if (incoming > 0) {
         double keep = 1.0, wp = 0.0;
         merge_weights(cnt_g_, (uint64_t)P_, cnt_local_, &keep, &wp);
-        timed_begin("merge");
+        timed_begin(stream_);
         launch_sum_chains(Ssum_, S_, mat_, C_, mat_, 1.0, stream_);
         launch_sum_chains(Ssum_ + mat_, mean_, ld_, C_, ld_, 1.0, stream_);
         if (comm_ && world_ > 1) comm_->allreduce_sum(Ssum_, mat_ + ld_, stream_);
         launch_axpby(Sg_, Ssum_, mat_, wp, keep, stream_);
         launch_axpby(mg_, Ssum_ + mat_, ld_, wp, keep, stream_);
-        timed_end("merge", 0.0);
+        timed_end("merge", 0.0, stream_);
         cnt_g_ += incoming;
         const double ct = (double)(cum_cnt_ + cnt_local_);
         launch_cum_fold(cmean_, cdiag_, mean_, S_, mat_, C_, d_, ld_, (double)cum_cnt_ / ct, (double)cnt_local_ / ct,
@@ -546,6 +565,19 @@ void Engine::merge_batch() {
     DGB_CUDA(cudaMemsetAsync(S_, 0, (size_t)C_ * mat_ * 8, stream_));
     DGB_CUDA(cudaMemsetAsync(mean_, 0, (size_t)C_ * ld_ * 8, stream_));
     cnt_local_ = 0;
+}
+
+void Engine::check_fatal() {
+    int f = 0;
+    DGB_CUDA(cudaMemcpyAsync(&f, fatal_, sizeof f, cudaMemcpyDeviceToHost, stream_));
+    DGB_CUDA(cudaStreamSynchronize(stream_));
+    if (f == 0) return;
+    const int c = f - 1;
+    double trh = 0.0;
+    DGB_CUDA(cudaMemcpy(&trh, tr_ + c, 8, cudaMemcpyDeviceToHost));
+    fail(Err::NotPositiveDefinite, "chain " + std::to_string(c0_ + c) +
+                                       ": covariance not factorizable after jitter escalation (dim " +
+                                       std::to_string(d_) + ", trace " + std::to_string(trh) + ")");
 }
 
 void Engine::batch_stats(double& cov_err, double& mean_err, double& psrf) {
@@ -587,7 +619,8 @@ void Engine::batch_stats(double& cov_err, double& mean_err, double& psrf) {
             DGB_CUDA(cudaMemcpyAsync(all.data(), dst, all.size() * 8, cudaMemcpyDeviceToHost, stream_));
             DGB_CUDA(cudaStreamSynchronize(stream_));
             for (int r = 0; r < world_; ++r) {
-                const int cr = (int)((int64_t)(r + 1) * P_ / world_ - (int64_t)r * P_ / world_);
+                int64_t f = 0, cr = 0;
+                shard_range(P_, world_, r, &f, &cr);
                 const double* base = all.data() + (size_t)r * 2 * maxc * ld_;
                 cm.insert(cm.end(), base, base + (size_t)cr * ld_);
                 cd.insert(cd.end(), base + maxc * ld_, base + maxc * ld_ + (size_t)cr * ld_);
@@ -658,10 +691,16 @@ double Engine::run_batches_timed(int k) {
     cudaEvent_t a, b;
     DGB_CUDA(cudaEventCreate(&a));
     DGB_CUDA(cudaEventCreate(&b));
-    DGB_CUDA(cudaStreamSynchronize(stream_));
+    DGB_CUDA(cudaDeviceSynchronize());
     DGB_CUDA(cudaEventRecord(a, stream_));
     for (int i = 0; i < k; ++i) {
-        for (size_t m = 0; m < M; ++m) window(m, false);
+        fork_groups();
+        for (size_t m = 0; m < M; ++m) {
+            const WindowPlan p = plan_window(m, false);
+            for (auto& g : groups_) enqueue_window(g, p);
+            commit_window(p);
+        }
+        join_groups();
         merge_batch();
         ++batches_done_;
     }
@@ -671,6 +710,7 @@ double Engine::run_batches_timed(int k) {
     DGB_CUDA(cudaEventElapsedTime(&ms, a, b));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    check_fatal();
     return ms;
 }
 
@@ -679,6 +719,10 @@ RunResult Engine::run() {  // runner.cpp:216-279
     auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     const size_t M = cfg_.intervals_per_batch;
     window_n_start_.assign(M, 0);
+    if (capture_ && !dbg_ratio_) {
+        dbg_ratio_ = dalloc<double>(allocs_, (size_t)C_ * Lw_);
+        dbg_acc_ = dalloc<uint8_t>(allocs_, (size_t)C_ * Lw_);
+    }
     std::string reason;
     for (;;) {
         const uint64_t iters = (uint64_t)P_ * M * batches_done_ * k_.n_lag;
@@ -695,14 +739,21 @@ RunResult Engine::run() {  // runner.cpp:216-279
             break;
         }
         const auto b0 = std::chrono::steady_clock::now();
-        for (size_t m = 0; m < M; ++m) window(m, cfg_.record_traces);
+        fork_groups();
+        for (size_t m = 0; m < M; ++m) {
+            const WindowPlan p = plan_window(m, cfg_.record_traces);
+            for (auto& g : groups_) enqueue_window(g, p);
+            commit_window(p);
+            if (capture_) capture_window(m);
+        }
+        join_groups();
         merge_batch();
+        check_fatal();
         collect_batch_host(M);
         ++batches_done_;
         double ce, me, ps;
         batch_stats(ce, me, ps);
-        batch_seconds_.push_back(
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - b0).count());
+        batch_seconds_.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - b0).count());
         cov_hist_.push_back(ce);
         mean_hist_.push_back(me);
         psrf_hist_.push_back(ps);
@@ -763,7 +814,7 @@ RunResult Engine::build_result(const std::string& reason, double wall) {  // run
     if (comm_ && world_ > 1) {
         const int64_t maxc = (P_ + world_ - 1) / world_;
         const int64_t blk = 2 * maxc * (int64_t)nb;
-        std::vector<double> mine(blk, 0.0);
+        std::vector<double> mine(std::max<int64_t>(blk, 1), 0.0);
         for (int c = 0; c < C_; ++c)
             for (size_t j = 0; j < nb; ++j) {
                 mine[c * nb + j] = beta_hist_[c][j];
@@ -777,8 +828,8 @@ RunResult Engine::build_result(const std::string& reason, double wall) {  // run
         DGB_CUDA(cudaMemcpyAsync(all.data(), ddst, all.size() * 8, cudaMemcpyDeviceToHost, stream_));
         DGB_CUDA(cudaStreamSynchronize(stream_));
         for (int rk = 0; rk < world_; ++rk) {
-            const int base = (int)((int64_t)rk * P_ / world_);
-            const int cr = (int)((int64_t)(rk + 1) * P_ / world_) - base;
+            int64_t base = 0, cr = 0;
+            shard_range(P_, world_, rk, &base, &cr);
             for (int c = 0; c < cr; ++c) {
                 const double* b = all.data() + rk * blk + c * nb;
                 r.beta_history[base + c].assign(b, b + nb);

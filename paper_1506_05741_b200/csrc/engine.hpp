@@ -4,17 +4,20 @@
 // of M lag windows, a frozen global snapshot per batch, merge at the barrier,
 // convergence diagnostics and OR-composed stopping rules. The per-chain loop
 // of the reference (mh_step x n_lag, lag_update) becomes a per-window sequence
-// of batched kernels over all local chains on one CUDA stream:
+// of batched kernels over a GROUP of local chains on the group's CUDA stream:
 //
 //   noise    W = Philox normals                 (launch_normals)
 //   TRMM     Xi = s * W * L^T                   (gemm_f64, tri B)
-//   target   H = Xi * G^T                       (gemm_f64, all chains one GEMM)
-//   steps    n_lag MH steps, O(d) each          (launch_mh_window)
+//   target   H = Xi * G^T                       (gemm_f64, the group's windows as one GEMM)
+//   steps    n_lag MH steps, O(d) each          (launch_mh_window, TMA-fed ring)
 //   moments  S = a X^T X + b S, mean            (gemm_f64 tri C + launch_mean_update)
-//   adapt    beta, blend -> POTRF (jitter) -> usable guard -> swap, x_ref,
-//            y = L^-1(x - x_ref), quad, g = G x (trsv, potrf_batched, gemm_f64)
+//   adapt    beta, blend -> POTRF (+ device jitter ladder, augmented usable-guard row)
+//            -> swap, x_ref, g = G x            (potrf_batched, gemm_f64)
 //
-// and per batch: local moment sum -> all-reduce (multi-GPU) -> merge,
+// The local chains are split into groups on separate streams with no host
+// round trip inside a batch, so one group's latency-bound pieces (MH steps,
+// diagonal factorizations) overlap the other group's DMMA GEMMs. Per batch:
+// join the groups, local moment sum -> all-reduce (multi-GPU) -> merge,
 // cumulative PSRF statistics, cov/mean error.
 #pragma once
 
@@ -45,7 +48,7 @@ public:
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
 
-    RunResult run();                 // full run with the reference's stopping rules
+    RunResult run();                  // full run with the reference's stopping rules
     double run_batches_timed(int k);  // k batches, no stopping rules; device ms (CUDA events)
 
     // profiling: per-kernel-class CUDA-event timing (adds events around launches)
@@ -62,20 +65,47 @@ public:
     int local_chains() const { return C_; }
     int dim() const { return d_; }
     int n_lag() const { return Lw_; }
+    int groups() const { return (int)groups_.size(); }
     double flops_per_batch() const;  // algorithmic FP64 flops of one batch (all local chains)
 
 private:
+    struct Group {
+        int off = 0, C = 0;
+        cudaStream_t s = nullptr;
+        cudaEvent_t done = nullptr;
+        double **Lp = nullptr, **Lnp = nullptr, **Wp = nullptr, **Xip = nullptr, **Sp = nullptr;
+        double **xp = nullptr, **gp = nullptr, **xrp = nullptr, **grp = nullptr;  // 1-element arrays
+        double **Xib = nullptr, **Hb = nullptr;                                     // 1-element arrays
+        PotrfWork pw{};
+    };
+    // host-side scalars of one lag window, identical for every chain
+    struct WindowPlan {
+        size_t w = 0;
+        uint64_t n_start = 0, n_end = 0, nctr = 0;
+        int first = 0, k = 0;  // accumulated rows [first, n_lag)
+        uint64_t cnt_before = 0, cnt_after = 0;
+        bool record = false, refactor = false, move_ref = false;
+        double wg = 0.0, wl = 1.0;
+    };
+
     void upload_target();
     void init_chains();
-    void window(size_t win_in_batch, bool record);
-    void lag_update(size_t win_in_batch);
+    void make_groups(int n);
+    WindowPlan plan_window(size_t w, bool record) const;
+    void commit_window(const WindowPlan& p);
+    void enqueue_window(Group& g, const WindowPlan& p);
+    void capture_window(size_t w);
+    void fork_groups();  // groups wait for the main stream
+    void join_groups();  // main stream waits for every group
     void merge_batch();
+    void check_fatal();
     void batch_stats(double& cov_err, double& mean_err, double& psrf);
     void collect_batch_host(size_t windows);
-    void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, GemmShape sh = GemmShape::Big);
-    void refresh_g(const double* vec, double* out);  // out[c] = G * vec[c]
-    void timed_begin(const char* name);
-    void timed_end(const char* name, double flops);
+    void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s,
+              GemmShape sh = GemmShape::Big);
+    void refresh_g(double* const* vec, double* const* out, int chains, cudaStream_t s);
+    void timed_begin(cudaStream_t s);
+    void timed_end(const char* name, double flops, cudaStream_t s);
     void resolve_events();
     RunResult build_result(const std::string& reason, double wall);
 
@@ -89,6 +119,8 @@ private:
     int64_t fmat_ = 0;  // factor stride: d rows + the augmented row r = x - x_ref
     bool twisted_ = false, identity_ = true;
     cudaStream_t stream_ = nullptr;
+    cudaEvent_t main_ev_ = nullptr;
+    std::vector<Group> groups_;
 
     // device memory
     std::vector<void*> allocs_;
@@ -97,26 +129,21 @@ private:
     double* inv_eig_ = nullptr;
     double* bcoef_ = nullptr;
     double* proj_ = nullptr;   // 2 x ld
-    double *L_ = nullptr, *Lw2_ = nullptr, *S_ = nullptr;  // C x (d x ld)
+    double *L_ = nullptr, *Lw2_ = nullptr, *S_ = nullptr;  // C x ((d+1) or d) x ld
     double *W_ = nullptr, *Xi_ = nullptr, *H_ = nullptr;   // C x (Lw x ld)
     double *x_ = nullptr, *g_ = nullptr, *y_ = nullptr, *xr_ = nullptr, *gr_ = nullptr;
     double *mean_ = nullptr, *cmean_ = nullptr, *cdiag_ = nullptr, *mb_ = nullptr;
     double *logpi_ = nullptr, *quad_ = nullptr, *beta_ = nullptr, *tr_ = nullptr, *qtmp_ = nullptr;
     uint64_t *nacc_ = nullptr, *uctr_ = nullptr;
-    int *status_ = nullptr, *try_ = nullptr, *usable_ = nullptr, *mask_ = nullptr;
+    int *status_ = nullptr, *try_ = nullptr, *usable_ = nullptr, *fatal_ = nullptr;
     PhiloxKey *nkeys_ = nullptr, *ukeys_ = nullptr, *ikeys_ = nullptr;
     double **Lp_ = nullptr, **Lnp_ = nullptr;  // factor / workspace pointer arrays (swapped on device)
-    double **Wp_ = nullptr, **Xip_ = nullptr, **Sp_ = nullptr, **Gp_ = nullptr, **Hp_ = nullptr;
-    double **xp_ = nullptr, **gp_ = nullptr, **xrp_ = nullptr, **grp_ = nullptr;
+    double **Wp_ = nullptr, **Xip_ = nullptr, **Sp_ = nullptr, **Gp_ = nullptr;
     double *Sg_ = nullptr, *mg_ = nullptr, *Ssum_ = nullptr;  // global snapshot, reduction buffer
     double *trace_lp_ = nullptr, *trace_pj_ = nullptr;      // per batch: M x C x Lw (x2)
     double *hist_rate_ = nullptr, *hist_beta_ = nullptr;    // per batch: M x C
     double* cov_part_ = nullptr;                              // d x 2
     double* gather_ = nullptr;                                // PSRF all-gather buffer
-    PotrfWork pw_{};
-    // pinned host staging
-    double* h_stage_ = nullptr;
-    size_t h_stage_len_ = 0;
 
     // host-side counters (uniform across chains)
     uint64_t n_ = 0;          // iterations per chain
@@ -143,7 +170,7 @@ private:
     std::vector<Pending> pending_;
     std::vector<cudaEvent_t> event_pool_;
     std::map<std::string, KernelStat> stats_;
-    cudaEvent_t cur_a_ = nullptr;
+    std::map<cudaStream_t, cudaEvent_t> open_;
 
     bool capture_ = false;
     std::vector<std::vector<double>> cap_w_, cap_ratio_;
