@@ -91,6 +91,9 @@ Engine::~Engine() {
         cudaEventDestroy(pe.b);
     }
     if (main_ev_) cudaEventDestroy(main_ev_);
+    for (auto& g : groups_)
+        if (g.status_ev) cudaEventDestroy(g.status_ev);
+    if (h_flags_) cudaFreeHost(h_flags_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -155,7 +158,9 @@ void Engine::init_chains() {
     status_ = dalloc<int>(A, C);
     try_ = dalloc<int>(A, C);
     usable_ = dalloc<int>(A, C);
+    mask_ = dalloc<int>(A, C);
     fatal_ = dalloc<int>(A, 1);
+    DGB_CUDA(cudaMallocHost(&h_flags_, 2 * (size_t)C * sizeof(int)));
     Sg_ = dalloc<double>(A, mat_);
     mg_ = dalloc<double>(A, ld_);
     Ssum_ = dalloc<double>(A, mat_ + ld_);
@@ -225,6 +230,7 @@ void Engine::make_groups(int n) {
         g.C = (int)((int64_t)C_ * (i + 1) / n) - g.off;
         DGB_CUDA(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking));
         DGB_CUDA(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
+        DGB_CUDA(cudaEventCreateWithFlags(&g.status_ev, cudaEventDisableTiming));
         g.Lp = Lp_ + g.off;
         g.Lnp = Lnp_ + g.off;
         g.Wp = Wp_ + g.off;
@@ -340,6 +346,7 @@ Engine::WindowPlan Engine::plan_window(size_t w, bool record) const {
     p.n_start = n_;
     p.n_end = n_ + Lw_;
     p.nctr = nctr_;
+    p.identity = identity_;
     // post-burn-in rows: step t counts iff n_start + t + 1 > n0 (proposal.cpp:153-155)
     p.first = (int)std::clamp<int64_t>((int64_t)k_.n0 - (int64_t)p.n_start, 0, Lw_);
     p.k = Lw_ - p.first;
@@ -364,16 +371,47 @@ void Engine::commit_window(const WindowPlan& p) {
     if (p.refactor) identity_ = false;
 }
 
-void Engine::enqueue_window(Group& g, const WindowPlan& p) {
+void Engine::run_batch_windows(bool record) {
+    const size_t M = cfg_.intervals_per_batch;
+    std::vector<WindowPlan> plans;
+    plans.reserve(M);
+    auto next_plan = [&](size_t m) {
+        plans.push_back(plan_window(m, record));
+        commit_window(plans.back());
+    };
+    if (capture_) {
+        // parity capture: strictly ordered windows (W must still be resident when copied)
+        for (size_t m = 0; m < M; ++m) {
+            next_plan(m);
+            for (auto& g : groups_) enqueue_head(g, plans[m]);
+            for (auto& g : groups_) enqueue_tail(g, plans[m]);
+            capture_window(m);
+        }
+        return;
+    }
+    // software pipeline over groups: while the host reads group g's POTRF statuses for
+    // window m, the other group's kernels keep the GPU busy; g's next head follows at once
+    next_plan(0);
+    for (auto& g : groups_) enqueue_head(g, plans[0]);
+    for (size_t m = 0; m < M; ++m) {
+        if (m + 1 < M) next_plan(m + 1);
+        for (auto& g : groups_) {
+            enqueue_tail(g, plans[m]);
+            if (m + 1 < M) enqueue_head(g, plans[m + 1]);
+        }
+    }
+}
+
+void Engine::enqueue_head(Group& g, const WindowPlan& p) {
     const int C = g.C, o = g.off;
     const cudaStream_t s = g.s;
     const double infl = k_.noise_infl();
     // ---- noise window: W from Philox, Xi = s W L^T, H = Xi G^T (proposal.cpp:254-266)
     timed_begin(s);
-    launch_normals(W_ + o * win_, identity_ ? Xi_ + o * win_ : nullptr, win_, C, Lw_, d_, ld_, nkeys_ + o, p.nctr,
+    launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, Lw_, d_, ld_, nkeys_ + o, p.nctr,
                    beta_ + o, infl, s);
     timed_end("normals", 0.0, s);
-    if (!identity_) {
+    if (!p.identity) {
         GemmBatch t{};
         t.A = (const double* const*)g.Wp;
         t.B = (const double* const*)g.Lp;
@@ -485,9 +523,55 @@ void Engine::enqueue_window(Group& g, const WindowPlan& p) {
         timed_begin(s);
         potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
         timed_end("potrf", (double)C * d_ * (double)d_ * d_ / 3.0, s);
-        // jitter escalation for chains whose factorization failed, on the device (proposal.cpp:218-239)
-        launch_potrf_rescue(g.Lnp, ld_, d_, aug ? 1 : 0, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg,
-                            p.wl, tr_ + o, ax, axr, status_ + o, fatal_, C, s);
+        DGB_CUDA(cudaMemcpyAsync(h_flags_ + o, status_ + o, C * sizeof(int), cudaMemcpyDeviceToHost, s));
+        DGB_CUDA(cudaMemcpyAsync(h_flags_ + C_ + o, try_ + o, C * sizeof(int), cudaMemcpyDeviceToHost, s));
+        DGB_CUDA(cudaEventRecord(g.status_ev, s));
+    }
+}
+
+void Engine::enqueue_tail(Group& g, const WindowPlan& p) {
+    const int C = g.C, o = g.off;
+    const cudaStream_t s = g.s;
+    const double infl = k_.noise_infl();
+    if (p.refactor) {
+        const bool aug = k_.pcn_form();
+        const double* ax = aug ? x_ + o * ld_ : nullptr;
+        const double* axr = aug && k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
+        // jitter escalation for chains whose factorization failed (proposal.cpp:218-239):
+        // eps = 1e-10, 1e-8, 1e-6, 9.999e-5 — the reference's floating loop — with the same
+        // blocked POTRF restricted to the failing chains
+        DGB_CUDA(cudaEventSynchronize(g.status_ev));
+        std::vector<int> failing(C, 0);
+        bool any = false;
+        for (int c = 0; c < C; ++c) {
+            failing[c] = h_flags_[C_ + o + c] && h_flags_[o + c];
+            any |= failing[c] != 0;
+        }
+        for (double eps = 1e-10; any && eps <= 1e-4; eps *= 100.0) {
+            DGB_CUDA(cudaMemcpyAsync(mask_ + o, failing.data(), C * sizeof(int), cudaMemcpyHostToDevice, s));
+            launch_blend_cov(g.Lnp, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, mb_ + o * ld_,
+                             ld_, C, d_, ld_, mask_ + o, eps, tr_ + o, s, ax, axr);
+            DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
+            potrf_batched(g.Lnp, ld_, d_, C, mask_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+            DGB_CUDA(cudaMemcpyAsync(h_flags_ + o, status_ + o, C * sizeof(int), cudaMemcpyDeviceToHost, s));
+            DGB_CUDA(cudaStreamSynchronize(s));
+            any = false;
+            for (int c = 0; c < C; ++c) {
+                if (failing[c] && !h_flags_[o + c]) failing[c] = 0;
+                any |= failing[c] != 0;
+            }
+        }
+        if (any) {
+            int c = 0;
+            while (!failing[c]) ++c;
+            double trh = 0.0;
+            DGB_CUDA(cudaMemcpy(&trh, tr_ + o + c, 8, cudaMemcpyDeviceToHost));
+            fail(Err::NotPositiveDefinite, "chain " + std::to_string(c0_ + o + c) +
+                                               ": covariance not factorizable after jitter escalation (dim " +
+                                               std::to_string(d_) + ", trace " + std::to_string(trh) + ")");
+        }
+        // every tried chain has factored by now
+        DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
         double qmax = -1.0;
         if (aug) {
             // usable guard: 1/2 |L'^-1 (x - x_ref)|^2 / infl^2 <= 5 d (proposal.cpp:185-199),
@@ -695,11 +779,7 @@ double Engine::run_batches_timed(int k) {
     DGB_CUDA(cudaEventRecord(a, stream_));
     for (int i = 0; i < k; ++i) {
         fork_groups();
-        for (size_t m = 0; m < M; ++m) {
-            const WindowPlan p = plan_window(m, false);
-            for (auto& g : groups_) enqueue_window(g, p);
-            commit_window(p);
-        }
+        run_batch_windows(false);
         join_groups();
         merge_batch();
         ++batches_done_;
@@ -740,12 +820,7 @@ RunResult Engine::run() {  // runner.cpp:216-279
         }
         const auto b0 = std::chrono::steady_clock::now();
         fork_groups();
-        for (size_t m = 0; m < M; ++m) {
-            const WindowPlan p = plan_window(m, cfg_.record_traces);
-            for (auto& g : groups_) enqueue_window(g, p);
-            commit_window(p);
-            if (capture_) capture_window(m);
-        }
+        run_batch_windows(cfg_.record_traces);
         join_groups();
         merge_batch();
         check_fatal();

@@ -77,6 +77,7 @@ private:
         double **xp = nullptr, **gp = nullptr, **xrp = nullptr, **grp = nullptr;  // 1-element arrays
         double **Xib = nullptr, **Hb = nullptr;                                     // 1-element arrays
         PotrfWork pw{};
+        cudaEvent_t status_ev = nullptr;  // POTRF statuses of the group's last window landed in h_status_
     };
     // host-side scalars of one lag window, identical for every chain
     struct WindowPlan {
@@ -85,6 +86,7 @@ private:
         int first = 0, k = 0;  // accumulated rows [first, n_lag)
         uint64_t cnt_before = 0, cnt_after = 0;
         bool record = false, refactor = false, move_ref = false;
+        bool identity = false;  // every factor is still the initial identity (noise = s W)
         double wg = 0.0, wl = 1.0;
     };
 
@@ -93,7 +95,13 @@ private:
     void make_groups(int n);
     WindowPlan plan_window(size_t w, bool record) const;
     void commit_window(const WindowPlan& p);
-    void enqueue_window(Group& g, const WindowPlan& p);
+    // a window is enqueued in two parts: the head (noise .. POTRF, statuses copied to the
+    // host asynchronously) and the tail (jitter ladder if any chain failed, usable guard,
+    // factor swap, reference point, G x). Between them the host reads the group's
+    // statuses while the other group keeps the GPU busy.
+    void enqueue_head(Group& g, const WindowPlan& p);
+    void enqueue_tail(Group& g, const WindowPlan& p);
+    void run_batch_windows(bool record);
     void capture_window(size_t w);
     void fork_groups();  // groups wait for the main stream
     void join_groups();  // main stream waits for every group
@@ -135,7 +143,8 @@ private:
     double *mean_ = nullptr, *cmean_ = nullptr, *cdiag_ = nullptr, *mb_ = nullptr;
     double *logpi_ = nullptr, *quad_ = nullptr, *beta_ = nullptr, *tr_ = nullptr, *qtmp_ = nullptr;
     uint64_t *nacc_ = nullptr, *uctr_ = nullptr;
-    int *status_ = nullptr, *try_ = nullptr, *usable_ = nullptr, *fatal_ = nullptr;
+    int *status_ = nullptr, *try_ = nullptr, *usable_ = nullptr, *fatal_ = nullptr, *mask_ = nullptr;
+    int* h_flags_ = nullptr;  // pinned host mirror: status[C] then try[C]
     PhiloxKey *nkeys_ = nullptr, *ukeys_ = nullptr, *ikeys_ = nullptr;
     double **Lp_ = nullptr, **Lnp_ = nullptr;  // factor / workspace pointer arrays (swapped on device)
     double **Wp_ = nullptr, **Xip_ = nullptr, **Sp_ = nullptr, **Gp_ = nullptr;
