@@ -8,6 +8,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "gemm_f64.cuh"
 
 namespace dgb {
@@ -269,9 +271,11 @@ void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool
     double flops = 2.0 * g.M * (double)g.N * g.K * batch;
     if (g.tri_c_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
     if (g.tri_b_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
+    nvtxRangePushA(name);  // `ncu --nvtx --nvtx-include "<name>/"` selects one GEMM class
     timed_begin(s);
     gemm_f64(g, batch, ak, bk, s, sh);
     timed_end(name, flops, s);
+    nvtxRangePop();
 }
 
 void Engine::timed_begin(cudaStream_t s) {
@@ -520,9 +524,11 @@ void Engine::enqueue_head(Group& g, const WindowPlan& p) {
         timed_end("blend_cov", 0.0, s);
         launch_trace_floor(g.Lnp, ld_, mb_ + o * ld_, ld_, C, d_, tr_ + o, try_ + o, s);
         DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
+        nvtxRangePushA("potrf");
         timed_begin(s);
         potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
         timed_end("potrf", (double)C * d_ * (double)d_ * d_ / 3.0, s);
+        nvtxRangePop();
         DGB_CUDA(cudaMemcpyAsync(h_flags_ + o, status_ + o, C * sizeof(int), cudaMemcpyDeviceToHost, s));
         DGB_CUDA(cudaMemcpyAsync(h_flags_ + C_ + o, try_ + o, C * sizeof(int), cudaMemcpyDeviceToHost, s));
         DGB_CUDA(cudaEventRecord(g.status_ev, s));

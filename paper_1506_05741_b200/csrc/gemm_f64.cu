@@ -1,6 +1,8 @@
 // gemm_f64.cu — batched FP64 DMMA GEMM (see gemm_f64.cuh for the contract).
 #include "gemm_f64.cuh"
 
+#include <cstdlib>
+
 namespace dgb {
 
 namespace {
@@ -25,11 +27,13 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
-template <int BM_, int BN_, int BK_, int STAGES_, bool AK, bool BKM>
+template <int BM_, int BN_, int BK_, int STAGES_, bool AK, bool BKM, int WARPS_M_ = 2, int WARPS_N_ = 4,
+          int MINB_ = 1>
 struct Cfg {
     static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_;
     static constexpr int THREADS = 256;
-    static constexpr int WARPS_M = 2, WARPS_N = 4;
+    static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+    static constexpr int MINB = MINB_;  // CTAs resident per SM (register budget 64K / (256 * MINB))
     static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
     static constexpr int MI = WM / 8, NI = WN / 8;
     // shared layout: the global-contiguous dimension stays contiguous; stride = 4 mod 16
@@ -66,7 +70,7 @@ __device__ __forceinline__ void load_tile(double* s, const double* g, int64_t ld
 }
 
 template <class CF, bool AK, bool BKM>
-__global__ void __launch_bounds__(256, 1) gemm_f64_kernel(GemmBatch p) {
+__global__ void __launch_bounds__(256, CF::MINB) gemm_f64_kernel(GemmBatch p) {
     const int b = blockIdx.z;
     if (p.active && !p.active[b]) return;
     const int n0 = blockIdx.x * CF::BN;
@@ -200,6 +204,17 @@ void launch(const GemmBatch& g, int batch, cudaStream_t stream) {
 
 template <bool AK, bool BKM>
 void dispatch_shape(const GemmBatch& g, int batch, cudaStream_t stream, GemmShape shape) {
+    // tile configuration: 0 = 128x128 (1 CTA/SM, 8 warps of 64x32), 1 = 128x64 with two
+    // resident CTAs per SM (8 warps of 32x32) so one CTA's epilogue overlaps the other's
+    // DMMA main loop; DIAM_B200_GEMM_CFG selects for experiments
+    static const int cfg = [] {
+        const char* e = std::getenv("DIAM_B200_GEMM_CFG");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (cfg == 1) {
+        launch<Cfg<128, 64, 16, 3, AK, BKM, 4, 2, 2>, AK, BKM>(g, batch, stream);
+        return;
+    }
     if (shape == GemmShape::Narrow)
         launch<Cfg<128, 64, 16, 4, AK, BKM>, AK, BKM>(g, batch, stream);
     else
