@@ -219,7 +219,15 @@ def impl_b200(args):
     samples_per_step = chains * M * n_lag
     value = samples_per_step * args.steps / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel class (profiled pass, CUDA events per launch)
+    groups = eng.abi.lib.diamx_engine_local_chains(eng.h)  # noqa: F841 (keeps eng alive)
+    del eng
+    # ---- roofline of the dominant kernel class: a profiled pass on a single-stream engine
+    # (CUDA events around every launch; with one chain group nothing overlaps, so each
+    # event pair times its kernel alone)
+    os.environ["DIAM_B200_GROUPS"] = "1"
+    eng = lib.engine(t, **run_options(cfg, chains))
+    del os.environ["DIAM_B200_GROUPS"]
+    eng.run_batches(max(1, args.warmup))
     eng.set_profiling(True)
     eng.run_batches(1)
     classes = ["gemm_target", "trmm_noise", "syrk_moments", "potrf", "mh_window", "normals", "trsv", "blend_cov",

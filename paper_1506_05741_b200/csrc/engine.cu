@@ -18,12 +18,30 @@ uint64_t g_launch_count = 0;
 
 namespace {
 
+// Engine buffers come from the device's stream-ordered memory pool, kept resident
+// between runs (release threshold = max): a second diam_sample on the same GPU reuses
+// the first one's HBM instead of paying cudaMalloc/cudaFree for gigabytes again.
+void keep_pool_resident() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    DGB_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    DGB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = ~0ull;
+    DGB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    done = true;
+}
+
 template <class T>
 T* dalloc(std::vector<void*>& list, size_t count) {
     void* p = nullptr;
     if (count == 0) count = 1;
-    DGB_CUDA(cudaMalloc(&p, count * sizeof(T)));
-    DGB_CUDA(cudaMemset(p, 0, count * sizeof(T)));
+    keep_pool_resident();
+    DGB_CUDA(cudaMallocAsync(&p, count * sizeof(T), 0));
+    DGB_CUDA(cudaMemsetAsync(p, 0, count * sizeof(T), 0));
+    // the engine's streams are non-blocking: make the zeroed buffer visible to them now
+    DGB_CUDA(cudaStreamSynchronize(0));
     list.push_back(p);
     return static_cast<T*>(p);
 }
@@ -32,7 +50,8 @@ double** ptr_array(std::vector<void*>& list, double* base, int64_t stride, int n
     std::vector<double*> h(n);
     for (int i = 0; i < n; ++i) h[i] = base + stride * i;
     double** d = dalloc<double*>(list, n);
-    DGB_CUDA(cudaMemcpy(d, h.data(), n * sizeof(double*), cudaMemcpyHostToDevice));
+    DGB_CUDA(cudaMemcpyAsync(d, h.data(), n * sizeof(double*), cudaMemcpyHostToDevice, 0));
+    DGB_CUDA(cudaStreamSynchronize(0));  // h is a stack buffer
     return d;
 }
 
@@ -72,7 +91,7 @@ Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> com
     init_chains();
     // two chain groups on two streams overlap one group's latency-bound pieces with the
     // other's GEMMs (DIAM_B200_GROUPS overrides, 1 = a single stream)
-    int ng = C_ >= 8 ? 2 : 1;
+    int ng = C_ >= 32 ? 4 : (C_ >= 8 ? 2 : 1);
     if (const char* e = std::getenv("DIAM_B200_GROUPS")) ng = std::max(1, std::min(C_, std::atoi(e)));
     make_groups(ng);
 }
@@ -86,7 +105,8 @@ Engine::~Engine() {
         }
         if (g.done) cudaEventDestroy(g.done);
     }
-    for (void* p : allocs_) cudaFree(p);
+    for (void* p : allocs_) cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
     for (auto& e : event_pool_) cudaEventDestroy(e);
     for (auto& pe : pending_) {
         cudaEventDestroy(pe.a);

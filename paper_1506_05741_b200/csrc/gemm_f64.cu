@@ -204,12 +204,13 @@ void launch(const GemmBatch& g, int batch, cudaStream_t stream) {
 
 template <bool AK, bool BKM>
 void dispatch_shape(const GemmBatch& g, int batch, cudaStream_t stream, GemmShape shape) {
-    // tile configuration: 0 = 128x128 (1 CTA/SM, 8 warps of 64x32), 1 = 128x64 with two
-    // resident CTAs per SM (8 warps of 32x32) so one CTA's epilogue overlaps the other's
-    // DMMA main loop; DIAM_B200_GEMM_CFG selects for experiments
+    // tile configuration: 1 (default) = 128x64 with two resident CTAs per SM (8 warps of
+    // 32x32) so one CTA's epilogue and pipeline fill overlap the other's DMMA main loop
+    // (measured 9% faster per batch than 0); 0 = 128x128, 1 CTA/SM, 8 warps of 64x32.
+    // DIAM_B200_GEMM_CFG selects for experiments.
     static const int cfg = [] {
         const char* e = std::getenv("DIAM_B200_GEMM_CFG");
-        return e ? std::atoi(e) : 0;
+        return e ? std::atoi(e) : 1;
     }();
     if (cfg == 1) {
         launch<Cfg<128, 64, 16, 3, AK, BKM, 4, 2, 2>, AK, BKM>(g, batch, stream);
