@@ -60,39 +60,52 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
-        self._stop = threading.Event()
+        self.samples = []  # (time, fields)
+        self.window = None
+        self._proc = None
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                parts = [p.strip() for p in out.stdout.strip().split(",")]
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                           "--format=csv,noheader,nounits", "-lms", "50"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            for line in self._proc.stdout:
+                parts = [p.strip() for p in line.strip().split(",")]
                 if len(parts) == 6:
-                    self.samples.append(parts)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+                    self.samples.append((time.perf_counter(), parts))
+        except Exception:
+            pass
 
-    def __enter__(self):
+    def start(self):
         self._t.start()
+        time.sleep(0.3)  # nvidia-smi start-up
         return self
 
-    def __exit__(self, *exc):
-        self._stop.set()
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def stop(self):
+        if self._proc:
+            self._proc.terminate()
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.samples:
+        samples = self.samples
+        if self.window and samples:
+            t0, t1 = self.window
+            inside = [s for s in samples if t0 <= s[0] <= t1]
+            # a sample is a snapshot: keep the ones inside, else the nearest after the start
+            samples = inside or [min(samples, key=lambda s: abs(s[0] - t0))]
+        rows = [s[1] for s in samples]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in rows if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in rows if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        reasons = sorted({names[i] for s in rows for i in range(4) if s[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def make_target_file(kind, d, seed=1):
@@ -202,14 +215,17 @@ def impl_b200(args):
     t = lib.target_load(target_path)
 
     # ---- device-resident throughput
+    clocks = ClockSampler(local).start()
     eng = lib.engine(t, **run_options(cfg, chains))
     eng.run_batches(args.warmup)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     launches0 = lib.launch_count()
-    with ClockSampler(local) as clocks:
-        ms = eng.run_batches(args.steps)
+    t_start = time.perf_counter()
+    ms = eng.run_batches(args.steps)
+    clocks.mark(t_start, time.perf_counter())
+    clocks.stop()
     launches = lib.launch_count() - launches0
     if dist:
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -309,7 +325,7 @@ def impl_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="d1024")
