@@ -250,62 +250,143 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int6
             v[a][b] = (r < jb && q <= r) ? A[(int64_t)r * ld + q] : (r == q ? 1.0 : 0.0);
             x[a][b] = (r == q) ? 1.0 : 0.0;
         }
+    // Blocked by the 4x4 register tiles: step kg finalises block column kg of L and block
+    // row kg of L^{-1} with two barriers (32 in total instead of two per column):
+    //   A  thread (kg,kg) factors its diagonal 4x4 tile and inverts it (all in registers)
+    //   B  column-owners solve their tile L_ik = A_ik L_kk^-T; row-owners finish block row
+    //      kg of the inverse X_k = L_kk^-1 Y_k; both publish through shared memory
+    //   C  everyone applies the rank-4 updates A_ij -= L_ik L_jk^T and Y_i -= L_ik X_k
+    __shared__ double s_inv[4][4];
+    __shared__ double s_col[2][kNb][4];  // block column kg of L, rows 0..63
+    __shared__ double s_row[2][4][kNb];  // block row kg of L^{-1}
+    (void)colk;
+    (void)xrow;
+    (void)piv;
     if (tid == 0) bad = 0;
     for (int kg = 0; kg < kNb / 4; ++kg) {
+        const int buf = kg & 1;
+        if (ty == kg && tx == kg) {
+            // A: 4x4 Cholesky of the diagonal tile; NotPositiveDefinite on a pivot <= 0 or
+            // non-finite (proj/src/linalg.cpp:82-84) only raises `bad`, the discarded
+            // arithmetic runs on
+            double rdiag[4];
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-            const int k = 4 * kg + kk, buf = kk & 1;
-            if (ty == kg && tx == kg) {
-                const double p = v[kk][kk];
-                // NotPositiveDefinite: pivot <= 0 or non-finite (proj/src/linalg.cpp:82-84);
-                // a bad pivot only raises `bad`, the discarded arithmetic runs on
+            for (int cc = 0; cc < 4; ++cc) {
+                double p = v[cc][cc];
+#pragma unroll
+                for (int n = 0; n < cc; ++n) p -= v[cc][n] * v[cc][n];
                 if (!(p > 0.0) || !isfinite(p)) bad = 1;
-                // one reciprocal square root on the critical path instead of sqrt + divide
-                const double rl = rsqrt(p);
-                const double l = p * rl;
-                v[kk][kk] = l;
-                piv = rl;
-                colk[buf][k] = l;
-            }
-            __syncthreads();
-            const double rl = piv;
-            if (tx == kg) {  // column k of L below the diagonal
+                const double rl = rsqrt(p);  // one reciprocal square root per pivot
+                rdiag[cc] = rl;
+                v[cc][cc] = p * rl;
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    const int r = 4 * ty + a;
-                    if (r > k) {
-                        v[a][kk] *= rl;
-                        colk[buf][r] = v[a][kk];
+                for (int rr = cc + 1; rr < 4; ++rr) {
+                    double s = v[rr][cc];
+#pragma unroll
+                    for (int n = 0; n < cc; ++n) s -= v[rr][n] * v[cc][n];
+                    v[rr][cc] = s * rl;
+                }
+            }
+            // inverse of the 4x4 lower tile by forward substitution
+            double w[4][4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (i < j) {
+                        w[i][j] = 0.0;
+                        continue;
                     }
-                }
-            }
-            if (ty == kg) {  // row k of L^{-1} is final once scaled by 1/l_kk
+                    double s = (i == j) ? 1.0 : 0.0;
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    x[kk][b] *= rl;
-                    xrow[buf][4 * tx + b] = x[kk][b];
+                    for (int n = j; n < i; ++n) s -= v[i][n] * w[n][j];
+                    w[i][j] = s * rdiag[i];
                 }
-            }
-            __syncthreads();
-            if (4 * ty + 3 > k) {
-                double cq[4], xq[4];
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    cq[b] = colk[buf][4 * tx + b];
-                    xq[b] = xrow[buf][4 * tx + b];
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    s_inv[i][j] = w[i][j];
+                    if (j > i) v[i][j] = 0.0;
+                }
+        }
+        __syncthreads();
+        if (tx == kg) {  // B: tiles of block column kg (the diagonal tile is already final)
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int r = 4 * ty + a;
+                if (ty > kg) {
+                    double t[4];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int n = 0; n <= m; ++n) s += v[a][n] * s_inv[m][n];
+                        t[m] = s;
+                    }
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) v[a][m] = t[m];
+                }
+                if (ty >= kg)
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) s_col[buf][r][m] = v[a][m];
+            }
+        }
+        if (ty == kg) {  // B: block row kg of L^{-1}
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                double t[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int n = 0; n <= a; ++n) s += s_inv[a][n] * x[n][b];
+                    t[a] = s;
                 }
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
-                    const int r = 4 * ty + a;
-                    if (r <= k) continue;
-                    const double lr = colk[buf][r];
+                    x[a][b] = t[a];
+                    s_row[buf][a][4 * tx + b] = t[a];
+                }
+            }
+        }
+        __syncthreads();
+        if (ty > kg) {  // C: rank-4 updates of the rows below block row kg
+            double lr[4][4], xk[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) lr[a][m] = s_col[buf][4 * ty + a][m];
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) xk[m][b] = s_row[buf][m][4 * tx + b];
+            if (tx > kg && tx <= ty) {
+                double lq[4][4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) lq[b][m] = s_col[buf][4 * tx + b][m];
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
-                        const int q = 4 * tx + b;
-                        if (q > k && q <= r) v[a][b] -= lr * cq[b];
-                        x[a][b] -= lr * xq[b];
+                        double s = v[a][b];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) s -= lr[a][m] * lq[b][m];
+                        v[a][b] = s;
                     }
-                }
+            }
+            if (tx <= kg) {  // Y_i -= L_ik X_k (X_k is zero right of block column kg)
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        double s = x[a][b];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) s -= lr[a][m] * xk[m][b];
+                        x[a][b] = s;
+                    }
             }
         }
     }
