@@ -662,7 +662,7 @@ void Engine::merge_batch() {
         timed_begin(stream_);
         launch_sum_chains(Ssum_, S_, mat_, C_, mat_, 1.0, stream_);
         launch_sum_chains(Ssum_ + mat_, mean_, ld_, C_, ld_, 1.0, stream_);
-        if (comm_ && world_ > 1) comm_->allreduce_sum(Ssum_, mat_ + ld_, stream_);
+        if (comm_) comm_->allreduce_sum(Ssum_, mat_ + ld_, stream_);
         launch_axpby(Sg_, Ssum_, mat_, wp, keep, stream_);
         launch_axpby(mg_, Ssum_ + mat_, ld_, wp, keep, stream_);
         timed_end("merge", 0.0, stream_);
@@ -715,7 +715,7 @@ void Engine::batch_stats(double& cov_err, double& mean_err, double& psrf) {
     if (P_ >= 2) {  // runner.cpp:381-396 on (cum mean, cum diag) of every chain
         std::vector<double> cm, cd;
         const int64_t nloc = (int64_t)C_ * ld_;
-        if (comm_ && world_ > 1) {
+        if (comm_) {
             // equal shards required for a plain all-gather; pad to the largest shard
             const int64_t maxc = (P_ + world_ - 1) / world_;
             if (!gather_) gather_ = dalloc<double>(allocs_, (size_t)2 * maxc * ld_ * (world_ + 1));
@@ -912,7 +912,7 @@ RunResult Engine::build_result(const std::string& reason, double wall) {  // run
     r.acceptance_history.assign(P_, {});
     r.traces.assign(P_, std::vector<std::vector<double>>(fnames_.size()));
     const size_t nb = beta_hist_.empty() ? 0 : beta_hist_[0].size();
-    if (comm_ && world_ > 1) {
+    if (comm_) {
         const int64_t maxc = (P_ + world_ - 1) / world_;
         const int64_t blk = 2 * maxc * (int64_t)nb;
         std::vector<double> mine(std::max<int64_t>(blk, 1), 0.0);

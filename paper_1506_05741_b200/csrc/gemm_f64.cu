@@ -73,7 +73,10 @@ template <class CF, bool AK, bool BKM>
 __global__ void __launch_bounds__(256, CF::MINB) gemm_f64_kernel(GemmBatch p) {
     const int b = blockIdx.z;
     if (p.active && !p.active[b]) return;
-    const int n0 = blockIdx.x * CF::BN;
+    // triangular B: tile n has K = (n+1) BN, so hand out the longest tiles first
+    // (longest-processing-time order shortens the tail of the launch)
+    const int nt = p.tri_b_lower ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
+    const int n0 = nt * CF::BN;
     const int m0 = blockIdx.y * CF::BM;
     if (n0 >= p.N || m0 >= p.M) return;
     if (p.tri_c_lower && n0 > m0 + CF::BM - 1) return;
@@ -91,6 +94,15 @@ __global__ void __launch_bounds__(256, CF::MINB) gemm_f64_kernel(GemmBatch p) {
     const int KT = (K + CF::BK - 1) / CF::BK;
 
     const int tid = threadIdx.x;
+    if (p.beta != 0.0) {
+        // read-modify-write epilogue: pull the C tile towards L2 while the main loop runs
+        constexpr int LINES_PER_ROW = (CF::BN * 8 + 127) / 128;
+        for (int li = tid; li < CF::BM * LINES_PER_ROW; li += CF::THREADS) {
+            const int r = m0 + li / LINES_PER_ROW, cc = n0 + (li % LINES_PER_ROW) * 16;
+            if (r < p.M && cc < p.N)
+                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Cp + (int64_t)r * p.ldc + cc));
+        }
+    }
     const int warp = tid >> 5, lane = tid & 31;
     const int wm0 = (warp / CF::WARPS_N) * CF::WM;
     const int wn0 = (warp % CF::WARPS_N) * CF::WN;

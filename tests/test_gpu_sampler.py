@@ -179,3 +179,25 @@ def test_launch_counter_moves(b200):
     before = b200.launch_count()
     b200.sample(t, chains=2, max_batches=1, n_lag=4, record_traces=0)
     assert b200.launch_count() > before
+
+
+def test_nccl_sharded_path_single_rank(b200, tmp_path):
+    """The multi-GPU code path (NCCL all-reduce of the batch moments, all-gather of the
+    PSRF inputs and of the chain histories) on a one-rank communicator must reproduce
+    the single-GPU run exactly: a one-rank all-reduce is the identity."""
+    import ctypes as C
+    t = b200.target_build("pi2", 24, 5)
+    kw = dict(kernel="diam", chains=4, intervals_per_batch=2, max_batches=3, n_lag=30, n0=0, master_seed=8,
+              record_traces=0)
+    r0 = b200.sample(t, **kw)
+    uid = C.create_string_buffer(128)
+    b200.check(b200.lib.diamx_nccl_unique_id(uid))
+    b200.check(b200.lib.diamx_comm_init(uid.raw, 0, 1))
+    try:
+        r1 = b200.sample(t, **kw)
+    finally:
+        b200.lib.diamx_comm_destroy()
+    assert np.array_equal(r0.mean(), r1.mean()) and np.array_equal(r0.cov(), r1.cov())
+    assert np.array_equal(r0.history("psrf"), r1.history("psrf"), equal_nan=True)
+    for p in range(4):
+        assert np.array_equal(r0.chain_history(p, "beta"), r1.chain_history(p, "beta"))
