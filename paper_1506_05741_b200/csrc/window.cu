@@ -13,6 +13,8 @@
 // each step is one fused pass (candidate, two dot products, CTA reduction with
 // a single barrier, accept/reject from the chain's Philox uniform) — the
 // "fused warp-level accept/reject" of the design.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace dgb {
@@ -448,7 +450,15 @@ void launch_r(const StepParams& p, cudaStream_t s) {
     // 256 threads (2 double2 pairs each) up to d = 1024, then 512 threads: fewer warps per
     // step barrier and reduction for the small dimensions where the step loop matters most
     bool done = false;
-    if (pairs <= 256) done = try_tma<1, TW, 256>(p, s);
+    static const int small_threads = [] {
+        const char* e = std::getenv("DIAM_B200_STEP_THREADS");  // experiments: 128 | 256
+        return e ? std::atoi(e) : 256;
+    }();
+    if (small_threads == 128 && pairs <= 512) {
+        if (pairs <= 128) done = try_tma<1, TW, 128>(p, s);
+        else if (pairs <= 256) done = try_tma<2, TW, 128>(p, s);
+        else done = try_tma<4, TW, 128>(p, s);
+    } else if (pairs <= 256) done = try_tma<1, TW, 256>(p, s);
     else if (pairs <= 512) done = try_tma<2, TW, 256>(p, s);
     else if (R <= 2) done = try_tma<2, TW, 512>(p, s);
     else if (R <= 4) done = try_tma<4, TW, 512>(p, s);
