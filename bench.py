@@ -123,6 +123,34 @@ def run_options(cfg, chains, **over):
     return o
 
 
+def time_to_cov_error(lib, with_reference: bool):
+    """BASELINE.json's second metric: wall time until the pooled covariance error first
+    reaches a tolerance. d=100 pi2 (config 1's target), 8 chains, M=2, n0=0, cov_tol 0.3 —
+    reachable by the reference in seconds (it converges slowly) — same seeds
+    on both sides; the reference on 8 host threads."""
+    kw = dict(kernel="diam", chains=8, intervals_per_batch=2, max_batches=5000, n0=0, cov_tol=0.3,
+              master_seed=3, record_traces=0, trace_eigen_projections=0)
+    t = lib.target_build("pi2", 100, 1)
+    lib.sample(t, **dict(kw, max_batches=1))  # warm
+    t0 = time.perf_counter()
+    r = lib.sample(t, **kw)
+    out = {"target": "pi2 d=100 seed 1", "chains": 8, "cov_tol": 0.3, "gpu_seconds": time.perf_counter() - t0,
+           "gpu_samples": r.total_samples, "gpu_stop": r.stop_reason, "gpu_final_cov_error": r.final_cov_error}
+    if with_reference:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import _oracle as O
+        from paper_1506_05741_b200.abi import DiamABI
+        if O.ref_available():
+            ref = DiamABI(O.REF_SO)
+            tr = ref.target_build("pi2", 100, 1)
+            t0 = time.perf_counter()
+            rr = ref.sample(tr, threads=8, **kw)
+            out.update(reference_seconds=time.perf_counter() - t0, reference_samples=rr.total_samples,
+                       reference_stop=rr.stop_reason, reference_final_cov_error=rr.final_cov_error,
+                       reference_threads=8)
+    return out
+
+
 # ---------------------------------------------------------------------------- reference CPU arm
 def reference_sample(cfg_name, target_path, threads, chains, windows=1):
     """One bounded reference run: `chains` chains x `windows` lag windows on the host cores."""
@@ -315,6 +343,8 @@ def impl_b200(args):
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }
+        if world == 1 and not args.no_cpu_baseline:
+            line["time_to_cov_error"] = time_to_cov_error(lib, with_reference=True)
         print(json.dumps(line))
     if dist:
         lib.lib.diamx_comm_destroy()

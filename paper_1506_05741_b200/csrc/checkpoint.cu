@@ -1,0 +1,382 @@
+// checkpoint.cu — DIAMCKPT v1 save/restore of the GPU engine state.
+//
+// Layout: proj/src/runner.cpp:398-457 (writer) and :139-207 (reader), field by field,
+// so a checkpoint written here is readable by the reference and vice versa; the
+// engine state lives on the device and is staged through host memory. After the
+// reference's fields we append a "B200EXT1" block with each chain's
+// y = L^-1 (x - x_ref): the step recursion carries y exactly, so restoring it
+// (instead of re-solving) makes a resumed run continue bit-for-bit.
+#include <cmath>
+#include <cstring>
+
+#include "engine.hpp"
+
+namespace dgb {
+
+namespace {
+
+constexpr char kCkptMagic[8] = {'D', 'I', 'A', 'M', 'C', 'K', 'P', 'T'};
+constexpr char kExtMagic[8] = {'B', '2', '0', '0', 'E', 'X', 'T', '1'};
+constexpr uint32_t kVersion = 1;
+constexpr uint32_t kEndian = 0x01020304u;
+
+void write_opt(BinOut& w, const std::optional<double>& v) {
+    w.pod<uint32_t>(v ? 1 : 0);
+    w.pod<double>(v.value_or(0.0));
+}
+
+std::optional<double> read_opt(BinIn& r) {
+    const bool has = r.pod<uint32_t>() != 0;
+    const double v = r.pod<double>();
+    return has ? std::optional<double>(v) : std::nullopt;
+}
+
+// KernelConfig (proj/src/runner.cpp:37-61): RefMode 0 Zero / 1 Fixed / 2 AdaptiveMean
+void write_kernel(BinOut& w, const KernelCfg& k) {
+    w.pod<uint32_t>(static_cast<uint32_t>(k.kind));
+    w.pod<uint64_t>(k.dim);
+    w.pod<double>(k.beta_init);
+    w.pod<double>(k.inflation);
+    w.pod<uint32_t>(k.adaptive_ref ? 2u : 0u);
+    w.vec(Vec{});  // fixed_ref (RefMode::Fixed is not reachable through the C ABI)
+    w.pod<uint64_t>(k.n_lag);
+    w.pod<double>(k.band_lo);
+    w.pod<double>(k.band_hi);
+    w.pod<uint64_t>(k.n0);
+    w.pod<uint64_t>(k.n_ref_start);
+    w.pod<double>(k.beta_adapt_factor);
+    w.pod<double>(k.beta_min);
+    w.pod<double>(k.beta_max);
+    w.pod<uint32_t>(k.adapt_beta ? 1 : 0);
+    w.pod<uint32_t>(k.use_explicit_inverse ? 1 : 0);
+    w.pod<uint32_t>(0);  // proposal_cov absent
+    w.pod<double>(1e-10);
+    w.pod<double>(100.0);
+    w.pod<double>(1e-4);
+}
+
+KernelCfg read_kernel(BinIn& r) {
+    KernelCfg k;
+    const uint32_t kind = r.pod<uint32_t>();
+    require(kind < 4, Err::Io, "corrupt checkpoint: kernel kind");
+    k.kind = static_cast<KKind>(kind);
+    k.dim = r.pod<uint64_t>();
+    k.beta_init = r.pod<double>();
+    k.inflation = r.pod<double>();
+    const uint32_t ref_mode = r.pod<uint32_t>();
+    require(ref_mode == 0 || ref_mode == 2, Err::Io, "checkpoint uses a fixed reference point (unsupported)");
+    k.adaptive_ref = ref_mode == 2;
+    r.vec();
+    k.n_lag = r.pod<uint64_t>();
+    k.band_lo = r.pod<double>();
+    k.band_hi = r.pod<double>();
+    k.n0 = r.pod<uint64_t>();
+    k.n_ref_start = r.pod<uint64_t>();
+    k.beta_adapt_factor = r.pod<double>();
+    k.beta_min = r.pod<double>();
+    k.beta_max = r.pod<double>();
+    k.adapt_beta = r.pod<uint32_t>() != 0;
+    k.use_explicit_inverse = r.pod<uint32_t>() != 0;
+    require(r.pod<uint32_t>() == 0, Err::Io, "checkpoint carries a proposal covariance (unsupported)");
+    const double e0 = r.pod<double>(), g = r.pod<double>(), em = r.pod<double>();
+    require(e0 == 1e-10 && g == 100.0 && em == 1e-4, Err::Io, "checkpoint uses a non-default jitter ladder");
+    return k;
+}
+
+void write_acc(BinOut& w, size_t d, uint64_t count, const Vec& mean, const Mat& second) {
+    w.pod<uint64_t>(d);
+    w.pod<uint64_t>(count);
+    w.vec(mean);
+    w.mat(second);
+}
+
+// lower-triangle device rows (ld stride) -> full symmetric host matrix
+Mat mirror_lower(const double* h, int d, int64_t ld) {
+    Mat m(d, d);
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j <= i; ++j) m(i, j) = m(j, i) = h[(size_t)i * ld + j];
+    return m;
+}
+
+}  // namespace
+
+void Engine::save_checkpoint(double wall) {
+    require(!comm_, Err::InvalidArgument, "checkpointing a multi-GPU run is not supported yet");
+    DGB_CUDA(cudaDeviceSynchronize());
+    const int C = C_;
+    auto fetch = [&](const void* src, size_t bytes) {
+        std::vector<char> buf(bytes);
+        DGB_CUDA(cudaMemcpy(buf.data(), src, bytes, cudaMemcpyDeviceToHost));
+        return buf;
+    };
+    auto fetch_d = [&](const double* src, size_t n) {
+        std::vector<double> v(n);
+        DGB_CUDA(cudaMemcpy(v.data(), src, n * 8, cudaMemcpyDeviceToHost));
+        return v;
+    };
+    const auto x = fetch_d(x_, (size_t)C * ld_), xr = fetch_d(xr_, (size_t)C * ld_), y = fetch_d(y_, (size_t)C * ld_);
+    const auto lp = fetch_d(logpi_, C), qd = fetch_d(quad_, C), bt = fetch_d(beta_, C);
+    const auto mean = fetch_d(mean_, (size_t)C * ld_), cm = fetch_d(cmean_, (size_t)C * ld_);
+    const auto sg = fetch_d(Sg_, mat_), mg = fetch_d(mg_, ld_);
+    std::vector<uint64_t> uc(C);
+    DGB_CUDA(cudaMemcpy(uc.data(), uctr_, C * 8, cudaMemcpyDeviceToHost));
+    std::vector<double*> lptr(C);
+    DGB_CUDA(cudaMemcpy(lptr.data(), Lp_, C * sizeof(double*), cudaMemcpyDeviceToHost));
+
+    BinOut w(cfg_.checkpoint_path);
+    w.raw(kCkptMagic, 8);
+    w.pod<uint32_t>(kVersion);
+    w.pod<uint32_t>(kEndian);
+    write_target_blob(w, tgt_);
+    write_kernel(w, k_);
+    w.pod<uint64_t>(cfg_.chains);
+    w.pod<uint64_t>(cfg_.intervals_per_batch);
+    w.pod<uint64_t>(cfg_.max_batches);
+    write_opt(w, cfg_.cov_tol);
+    write_opt(w, cfg_.mean_tol);
+    write_opt(w, cfg_.psrf_tol);
+    w.pod<uint32_t>(cfg_.max_samples ? 1 : 0);
+    w.pod<uint64_t>(cfg_.max_samples.value_or(0));
+    write_opt(w, cfg_.max_wall_seconds);
+    w.pod<double>(cfg_.init_dispersion);
+    w.pod<uint64_t>(cfg_.master_seed);
+    w.pod<uint32_t>(cfg_.record_traces ? 1 : 0);
+    w.pod<uint64_t>(cfg_.trace_thin);
+    w.pod<uint32_t>(cfg_.trace_eigen_projections ? 1 : 0);
+    w.pod<uint64_t>(0);  // no extra eigen trace indices through the C ABI
+    w.str(cfg_.checkpoint_path);
+    w.pod<uint64_t>(cfg_.threads);
+
+    w.pod<uint64_t>(batches_done_);
+    w.pod<uint64_t>(batches_done_);  // global.batches: one merge per finished batch
+    w.pod<uint64_t>(cnt_g_);
+    w.vec(Vec(mg.begin(), mg.begin() + d_));
+    w.mat(mirror_lower(sg.data(), d_, ld_));
+    w.pod<double>(wall);
+    w.vec(batch_seconds_);
+    w.vec(cov_hist_);
+    w.vec(mean_hist_);
+    w.vec(psrf_hist_);
+
+    w.pod<uint64_t>((uint64_t)C);
+    const uint64_t nctr = nctr_;
+    for (int c = 0; c < C; ++c) {
+        w.vec(Vec(x.begin() + (size_t)c * ld_, x.begin() + (size_t)c * ld_ + d_));
+        w.pod<double>(lp[c]);
+        w.pod<double>(k_.pcn_form() ? qd[c] : 0.0);
+        w.pod<double>(bt[c]);
+        w.pod<uint64_t>(n_);
+        w.pod<uint64_t>(0);  // n_accepted: reset at every lag boundary
+        const auto L = fetch_d(lptr[c], (size_t)d_ * ld_);
+        w.pod<uint64_t>(d_);
+        for (int i = 0; i < d_; ++i)
+            for (int j = 0; j < d_; ++j) w.pod<double>(j <= i ? L[(size_t)i * ld_ + j] : 0.0);
+        w.pod<uint32_t>(0);  // no explicit inverse kept
+        w.vec(k_.adaptive_ref ? Vec(xr.begin() + (size_t)c * ld_, xr.begin() + (size_t)c * ld_ + d_) : Vec(d_, 0.0));
+        w.pod<uint64_t>(nctr);
+        w.pod<uint64_t>(uc[c]);
+        // batch accumulator (empty at a batch boundary unless resumed mid-batch)
+        const auto S = fetch_d(S_ + (size_t)c * mat_, mat_);
+        write_acc(w, d_, cnt_local_, Vec(mean.begin() + (size_t)c * ld_, mean.begin() + (size_t)c * ld_ + d_),
+                  mirror_lower(S.data(), d_, ld_));
+        // cumulative accumulator
+        Mat cs(d_, d_);
+        if (cS_) {
+            const auto cum = fetch_d(cS_ + (size_t)c * mat_, mat_);
+            cs = mirror_lower(cum.data(), d_, ld_);
+        }
+        write_acc(w, d_, cum_cnt_, Vec(cm.begin() + (size_t)c * ld_, cm.begin() + (size_t)c * ld_ + d_), cs);
+        w.vec(beta_hist_[c]);
+        w.vec(acc_hist_[c]);
+        w.pod<uint64_t>(fnames_.size());
+        for (size_t f = 0; f < fnames_.size(); ++f) w.vec(traces_[c][f]);
+    }
+    // B200 extension: the recursively carried y
+    w.raw(kExtMagic, 8);
+    for (int c = 0; c < C; ++c) w.vec(Vec(y.begin() + (size_t)c * ld_, y.begin() + (size_t)c * ld_ + d_));
+    w.close();
+}
+
+void Engine::read_checkpoint_header(BinIn& r, HostTarget& t, RunCfg& cfg) {
+    char magic[8];
+    r.raw(magic, 8);
+    require(std::memcmp(magic, kCkptMagic, 8) == 0, Err::Io, "not a checkpoint file");
+    require(r.pod<uint32_t>() == kVersion, Err::Io, "unsupported checkpoint version");
+    require(r.pod<uint32_t>() == kEndian, Err::Io, "endianness mismatch in checkpoint");
+    t = read_target_blob(r);
+    cfg.kernel = read_kernel(r);
+    cfg.chains = r.pod<uint64_t>();
+    cfg.intervals_per_batch = r.pod<uint64_t>();
+    cfg.max_batches = r.pod<uint64_t>();
+    cfg.cov_tol = read_opt(r);
+    cfg.mean_tol = read_opt(r);
+    cfg.psrf_tol = read_opt(r);
+    const bool has_ms = r.pod<uint32_t>() != 0;
+    const uint64_t ms = r.pod<uint64_t>();
+    if (has_ms) cfg.max_samples = ms;
+    cfg.max_wall_seconds = read_opt(r);
+    cfg.init_dispersion = r.pod<double>();
+    cfg.master_seed = r.pod<uint64_t>();
+    cfg.record_traces = r.pod<uint32_t>() != 0;
+    cfg.trace_thin = r.pod<uint64_t>();
+    cfg.trace_eigen_projections = r.pod<uint32_t>() != 0;
+    const uint64_t extra = r.pod<uint64_t>();
+    require(extra == 0, Err::Io, "checkpoint traces extra eigen directions (unsupported)");
+    cfg.checkpoint_path = r.str();
+    cfg.threads = r.pod<uint64_t>();
+}
+
+void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
+    const int C = C_;
+    require(world_ == 1 && C == P_, Err::InvalidArgument, "resuming a multi-GPU run is not supported yet");
+    batches_done_ = r.pod<uint64_t>();
+    r.pod<uint64_t>();  // global.batches
+    cnt_g_ = r.pod<uint64_t>();
+    const Vec gmean = r.vec();
+    const Mat gsec = r.mat();
+    require(gmean.size() == (size_t)d_ && gsec.rows == (size_t)d_, Err::Io, "corrupt checkpoint: global moments");
+    wall_accum_ = r.pod<double>();
+    batch_seconds_ = r.vec();
+    cov_hist_ = r.vec();
+    mean_hist_ = r.vec();
+    psrf_hist_ = r.vec();
+    require(r.pod<uint64_t>() == (uint64_t)C, Err::Io, "checkpoint chain count mismatch");
+
+    auto put = [&](double* dst, const double* src, size_t n) {
+        DGB_CUDA(cudaMemcpy(dst, src, n * 8, cudaMemcpyHostToDevice));
+    };
+    auto put_lower = [&](double* dst, const Mat& m) {  // full host -> lower device rows (upper zero)
+        std::vector<double> buf((size_t)d_ * ld_, 0.0);
+        for (int i = 0; i < d_; ++i)
+            for (int j = 0; j <= i; ++j) buf[(size_t)i * ld_ + j] = m(i, j);
+        put(dst, buf.data(), buf.size());
+    };
+    {
+        std::vector<double> m(ld_, 0.0);
+        std::copy(gmean.begin(), gmean.end(), m.begin());
+        put(mg_, m.data(), ld_);
+        put_lower(Sg_, gsec);
+    }
+    std::vector<double> lp(C), qd(C), bt(C);
+    std::vector<uint64_t> uc(C);
+    uint64_t nctr = 0, n = 0, cnt_local = 0, cum = 0;
+    std::vector<double*> lptr(C);
+    DGB_CUDA(cudaMemcpy(lptr.data(), Lp_, C * sizeof(double*), cudaMemcpyDeviceToHost));
+    bool all_identity = true;
+    for (int c = 0; c < C; ++c) {
+        std::vector<double> row(ld_, 0.0);
+        const Vec x = r.vec();
+        require(x.size() == (size_t)d_, Err::Io, "corrupt checkpoint: state");
+        std::copy(x.begin(), x.end(), row.begin());
+        put(x_ + (size_t)c * ld_, row.data(), ld_);
+        lp[c] = r.pod<double>();
+        qd[c] = r.pod<double>();
+        bt[c] = r.pod<double>();
+        const uint64_t nc = r.pod<uint64_t>();
+        require(c == 0 || nc == n, Err::Io, "chains at different iteration counts");
+        n = nc;
+        r.pod<uint64_t>();  // n_accepted
+        const uint64_t dim = r.pod<uint64_t>();
+        require(dim == (uint64_t)d_, Err::Io, "corrupt checkpoint: factor");
+        Mat L(d_, d_);
+        r.raw(L.a.data(), L.a.size() * 8);
+        for (int i = 0; i < d_ && all_identity; ++i)
+            for (int j = 0; j <= i; ++j)
+                if (L(i, j) != (i == j ? 1.0 : 0.0)) {
+                    all_identity = false;
+                    break;
+                }
+        put_lower(lptr[c], L);
+        if (r.pod<uint32_t>() != 0) {  // explicit inverse: not needed by this engine
+            r.pod<uint64_t>();
+            std::vector<double> skip((size_t)d_ * d_);
+            r.raw(skip.data(), skip.size() * 8);
+        }
+        const Vec xr = r.vec();
+        std::fill(row.begin(), row.end(), 0.0);
+        std::copy(xr.begin(), xr.end(), row.begin());
+        put(xr_ + (size_t)c * ld_, row.data(), ld_);
+        const uint64_t nc_ctr = r.pod<uint64_t>();
+        require(c == 0 || nc_ctr == nctr, Err::Io, "chains at different noise-stream positions");
+        nctr = nc_ctr;
+        uc[c] = r.pod<uint64_t>();
+        for (int which = 0; which < 2; ++which) {  // batch, then cumulative accumulator
+            r.pod<uint64_t>();
+            const uint64_t cnt = r.pod<uint64_t>();
+            const Vec m = r.vec();
+            const Mat s = r.mat();
+            std::fill(row.begin(), row.end(), 0.0);
+            std::copy(m.begin(), m.end(), row.begin());
+            if (which == 0) {
+                cnt_local = cnt;
+                put(mean_ + (size_t)c * ld_, row.data(), ld_);
+                put_lower(S_ + (size_t)c * mat_, s);
+            } else {
+                cum = cnt;
+                put(cmean_ + (size_t)c * ld_, row.data(), ld_);
+                std::vector<double> dg(ld_, 0.0);
+                for (int i = 0; i < d_; ++i) dg[i] = s(i, i);
+                put(cdiag_ + (size_t)c * ld_, dg.data(), ld_);
+                if (cS_) put_lower(cS_ + (size_t)c * mat_, s);
+            }
+        }
+        beta_hist_[c] = r.vec();
+        acc_hist_[c] = r.vec();
+        const uint64_t nf = r.pod<uint64_t>();
+        require(nf == fnames_.size(), Err::Io, "checkpoint functional count mismatch");
+        for (size_t f = 0; f < nf; ++f) traces_[c][f] = r.vec();
+    }
+    put(logpi_, lp.data(), C);
+    put(quad_, qd.data(), C);
+    put(beta_, bt.data(), C);
+    DGB_CUDA(cudaMemcpy(uctr_, uc.data(), C * 8, cudaMemcpyHostToDevice));
+    n_ = n;
+    nctr_ = nctr;
+    cnt_local_ = cnt_local;
+    cum_cnt_ = cum;
+    identity_ = all_identity;
+
+    // derived device state: G x, G x_ref and y = L^-1 (x - x_ref)
+    {
+        double** dp = nullptr;  // {x, g, x_ref, g_ref} as one-element operand arrays
+        DGB_CUDA(cudaMalloc(&dp, 4 * sizeof(double*)));
+        double* hp[4] = {x_, g_, xr_, gr_};
+        DGB_CUDA(cudaMemcpy(dp, hp, sizeof hp, cudaMemcpyHostToDevice));
+        refresh_g(dp, dp + 1, C, stream_);
+        if (k_.adaptive_ref) refresh_g(dp + 2, dp + 3, C, stream_);
+        DGB_CUDA(cudaStreamSynchronize(stream_));
+        cudaFree(dp);
+    }
+    bool have_y = false;
+    if (!r.at_end()) {
+        char magic[8];
+        r.raw(magic, 8);
+        if (std::memcmp(magic, kExtMagic, 8) == 0) {
+            for (int c = 0; c < C; ++c) {
+                const Vec y = r.vec();
+                std::vector<double> row(ld_, 0.0);
+                std::copy(y.begin(), y.end(), row.begin());
+                put(y_ + (size_t)c * ld_, row.data(), ld_);
+            }
+            have_y = true;
+        }
+    }
+    if (k_.pcn_form() && !have_y) {
+        // reference-written checkpoint: solve y; keep the saved quad (the reference's value)
+        const double infl = k_.noise_infl();
+        launch_trsv(Lp_, ld_, x_, k_.adaptive_ref ? xr_ : nullptr, ld_, y_, qtmp_, C, d_, 0.5 / (infl * infl),
+                    nullptr, stream_);
+    }
+    DGB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::override_stop(const RunCfg& c) {
+    cfg_.cov_tol = c.cov_tol;
+    cfg_.mean_tol = c.mean_tol;
+    cfg_.psrf_tol = c.psrf_tol;
+    cfg_.max_samples = c.max_samples;
+    cfg_.max_wall_seconds = c.max_wall_seconds;
+    validate_run_cfg(cfg_, tgt_);
+}
+
+}  // namespace dgb

@@ -187,6 +187,7 @@ void Engine::init_chains() {
     mg_ = dalloc<double>(A, ld_);
     Ssum_ = dalloc<double>(A, mat_ + ld_);
     cov_part_ = dalloc<double>(A, 2 * (size_t)d_);
+    if (!cfg_.checkpoint_path.empty()) cS_ = dalloc<double>(A, (size_t)C * mat_);
     const size_t M = cfg_.intervals_per_batch;
     trace_lp_ = dalloc<double>(A, M * C * Lw_);
     trace_pj_ = dalloc<double>(A, M * C * Lw_ * 2);
@@ -670,6 +671,9 @@ void Engine::merge_batch() {
         const double ct = (double)(cum_cnt_ + cnt_local_);
         launch_cum_fold(cmean_, cdiag_, mean_, S_, mat_, C_, d_, ld_, (double)cum_cnt_ / ct, (double)cnt_local_ / ct,
                         stream_);
+        // full cumulative second moments only when they must be checkpointed (merge_into,
+        // proj/src/moments.cpp:77-88); the PSRF needs just the diagonal kept above
+        if (cS_) launch_axpby(cS_, S_, (int64_t)C_ * mat_, (double)cnt_local_ / ct, (double)cum_cnt_ / ct, stream_);
         cum_cnt_ += cnt_local_;
     }
     DGB_CUDA(cudaMemsetAsync(S_, 0, (size_t)C_ * mat_ * 8, stream_));
@@ -822,7 +826,10 @@ double Engine::run_batches_timed(int k) {
 
 RunResult Engine::run() {  // runner.cpp:216-279
     const auto t0 = std::chrono::steady_clock::now();
-    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    // wall time includes earlier segments of a resumed run (runner.cpp:217-218)
+    auto elapsed = [&] {
+        return wall_accum_ + std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
     const size_t M = cfg_.intervals_per_batch;
     window_n_start_.assign(M, 0);
     if (capture_ && !dbg_ratio_) {
@@ -858,6 +865,7 @@ RunResult Engine::run() {  // runner.cpp:216-279
         cov_hist_.push_back(ce);
         mean_hist_.push_back(me);
         psrf_hist_.push_back(ps);
+        if (!cfg_.checkpoint_path.empty()) save_checkpoint(elapsed());  // runner.cpp:259
         if (cfg_.psrf_tol && std::isfinite(ps) && ps <= *cfg_.psrf_tol) {
             reason = "psrf";
             break;
@@ -871,7 +879,10 @@ RunResult Engine::run() {  // runner.cpp:216-279
             break;
         }
     }
-    return build_result(reason, elapsed());
+    const double wall = elapsed();
+    wall_accum_ = wall;
+    if (!cfg_.checkpoint_path.empty()) save_checkpoint(wall);  // runner.cpp:276-277
+    return build_result(reason, wall);
 }
 
 RunResult Engine::build_result(const std::string& reason, double wall) {  // runner.cpp:459-489

@@ -51,6 +51,15 @@ public:
     RunResult run();                  // full run with the reference's stopping rules
     double run_batches_timed(int k);  // k batches, no stopping rules; device ms (CUDA events)
 
+    // DIAMCKPT v1 checkpoints (proj/src/runner.cpp:398-457 / 139-207), written after every
+    // batch when cfg.checkpoint_path is set. The file is the reference's layout followed by
+    // a "B200EXT1" block carrying each chain's y = L^-1 (x - x_ref) so that a resumed run
+    // continues bit-for-bit; a reference-written file (no block) gets y re-solved.
+    static void read_checkpoint_header(BinIn& r, HostTarget& t, RunCfg& cfg);
+    void restore(BinIn& r);  // after construction from the header's target/config
+    void override_stop(const RunCfg& c);
+    void override_max_batches(size_t k) { cfg_.max_batches = k; }
+
     // profiling: per-kernel-class CUDA-event timing (adds events around launches)
     void set_profiling(bool on) { profiling_ = on; }
     const std::map<std::string, KernelStat>& stats();
@@ -109,6 +118,7 @@ private:
     void check_fatal();
     void batch_stats(double& cov_err, double& mean_err, double& psrf);
     void collect_batch_host(size_t windows);
+    void save_checkpoint(double wall);
     void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s,
               GemmShape sh = GemmShape::Big);
     void refresh_g(double* const* vec, double* const* out, int chains, cudaStream_t s);
@@ -153,6 +163,8 @@ private:
     double *hist_rate_ = nullptr, *hist_beta_ = nullptr;    // per batch: M x C
     double* cov_part_ = nullptr;                              // d x 2
     double* gather_ = nullptr;                                // PSRF all-gather buffer
+    double* cS_ = nullptr;  // cumulative raw second moments (lower), kept only for checkpoints
+    double wall_accum_ = 0.0;  // wall seconds of earlier (checkpointed) segments of the run
 
     // host-side counters (uniform across chains)
     uint64_t n_ = 0;          // iterations per chain

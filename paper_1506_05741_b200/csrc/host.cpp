@@ -216,64 +216,8 @@ void finish_gaussian(HostTarget& t) {
     t.b_coeffs.assign(t.dim, 0.0);
 }
 
-// ------------------------------------------------------------------ binary IO (little endian)
-struct Out {
-    std::ofstream f;
-    std::string path;
-    explicit Out(const std::string& p) : f(p, std::ios::binary), path(p) {
-        require(f.good(), Err::Io, "cannot open for writing: " + p);
-    }
-    void raw(const void* p, size_t n) { f.write(static_cast<const char*>(p), (std::streamsize)n); }
-    template <class T>
-    void pod(T v) { raw(&v, sizeof v); }
-    void vec(const Vec& v) {
-        pod<uint64_t>(v.size());
-        raw(v.data(), v.size() * 8);
-    }
-    void mat(const Mat& m) {
-        pod<uint64_t>(m.rows);
-        pod<uint64_t>(m.cols);
-        raw(m.a.data(), m.a.size() * 8);
-    }
-    void close() {
-        f.flush();
-        require(f.good(), Err::Io, "write failed: " + path);
-    }
-};
-
-struct In {
-    std::ifstream f;
-    std::string path;
-    explicit In(const std::string& p) : f(p, std::ios::binary), path(p) {
-        require(f.good(), Err::Io, "cannot open for reading: " + p);
-    }
-    void raw(void* p, size_t n) {
-        f.read(static_cast<char*>(p), (std::streamsize)n);
-        require(f.gcount() == (std::streamsize)n, Err::Io, "truncated file: " + path);
-    }
-    template <class T>
-    T pod() {
-        T v;
-        raw(&v, sizeof v);
-        return v;
-    }
-    size_t count() {
-        const uint64_t n = pod<uint64_t>();
-        require(n <= (1ull << 32), Err::Io, "implausible field size in " + path);
-        return (size_t)n;
-    }
-    Vec vec() {
-        Vec v(count());
-        raw(v.data(), v.size() * 8);
-        return v;
-    }
-    Mat mat() {
-        const size_t r = count(), c = count();
-        Mat m(r, c);
-        raw(m.a.data(), m.a.size() * 8);
-        return m;
-    }
-};
+using Out = BinOut;
+using In = BinIn;
 
 static_assert(std::endian::native == std::endian::little, "DIAMTGT is little-endian");
 constexpr char kMagic[8] = {'D', 'I', 'A', 'M', 'T', 'G', 'T', '\0'};
@@ -385,8 +329,18 @@ HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, do
     return t;
 }
 
-void save_target(const HostTarget& t, const std::string& path) {  // proj/src/target.cpp:187-204
+void save_target(const HostTarget& t, const std::string& path) {
     Out o(path);
+    write_target_blob(o, t);
+    o.close();
+}
+
+HostTarget load_target(const std::string& path) {
+    In r(path);
+    return read_target_blob(r);
+}
+
+void write_target_blob(BinOut& o, const HostTarget& t) {  // proj/src/target.cpp:187-204
     o.raw(kMagic, 8);
     o.pod<uint32_t>(1);
     o.pod<uint32_t>(0x01020304u);
@@ -403,11 +357,9 @@ void save_target(const HostTarget& t, const std::string& path) {  // proj/src/ta
     o.vec(t.mean);
     o.vec(t.eigen_mean);
     o.vec(t.eigen_var);
-    o.close();
 }
 
-HostTarget load_target(const std::string& path) {  // proj/src/target.cpp:206-231
-    In r(path);
+HostTarget read_target_blob(BinIn& r) {  // proj/src/target.cpp:206-231
     char magic[8];
     r.raw(magic, 8);
     require(std::memcmp(magic, kMagic, 8) == 0, Err::Io, "not a target file");

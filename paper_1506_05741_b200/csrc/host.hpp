@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <fstream>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -38,6 +39,82 @@ struct Mat {
     double operator()(size_t i, size_t j) const { return a[i * cols + j]; }
 };
 
+// ---------------------------------------------------------------- little-endian binary IO
+// (the DIAMTGT / DIAMCKPT field encodings of proj/src/binio.hpp: u32/u64/f64 raw,
+// vectors as u64 length + data, matrices as u64 rows, u64 cols + row-major data)
+struct BinOut {
+    std::ofstream f;
+    std::string path;
+    explicit BinOut(const std::string& p) : f(p, std::ios::binary), path(p) {
+        require(f.good(), Err::Io, "cannot open for writing: " + p);
+    }
+    void raw(const void* p, size_t n) { f.write(static_cast<const char*>(p), (std::streamsize)n); }
+    template <class T>
+    void pod(T v) {
+        raw(&v, sizeof v);
+    }
+    void vec(const Vec& v) {
+        pod<uint64_t>(v.size());
+        raw(v.data(), v.size() * 8);
+    }
+    void mat(const Mat& m) {
+        pod<uint64_t>(m.rows);
+        pod<uint64_t>(m.cols);
+        raw(m.a.data(), m.a.size() * 8);
+    }
+    void str(const std::string& s) {
+        pod<uint64_t>(s.size());
+        raw(s.data(), s.size());
+    }
+    void close() {
+        f.flush();
+        require(f.good(), Err::Io, "write failed: " + path);
+        f.close();
+    }
+};
+
+struct BinIn {
+    std::ifstream f;
+    std::string path;
+    explicit BinIn(const std::string& p) : f(p, std::ios::binary), path(p) {
+        require(f.good(), Err::Io, "cannot open for reading: " + p);
+    }
+    void raw(void* p, size_t n) {
+        f.read(static_cast<char*>(p), (std::streamsize)n);
+        require(f.gcount() == (std::streamsize)n, Err::Io, "truncated file: " + path);
+    }
+    template <class T>
+    T pod() {
+        T v;
+        raw(&v, sizeof v);
+        return v;
+    }
+    size_t count() {
+        const uint64_t n = pod<uint64_t>();
+        require(n <= (1ull << 32), Err::Io, "implausible field size in " + path);
+        return (size_t)n;
+    }
+    Vec vec() {
+        Vec v(count());
+        raw(v.data(), v.size() * 8);
+        return v;
+    }
+    Mat mat() {
+        const size_t r = count(), c = count();
+        Mat m(r, c);
+        raw(m.a.data(), m.a.size() * 8);
+        return m;
+    }
+    std::string str() {
+        std::string s(count(), '\0');
+        raw(s.data(), s.size());
+        return s;
+    }
+    bool at_end() {
+        return f.peek() == std::char_traits<char>::eof();
+    }
+};
+
 // ---------------------------------------------------------------- targets
 enum class TKind { Pi1 = 0, Pi2, Pi3, Pi4, Pi5, Pi6 };
 const char* tkind_name(TKind k);
@@ -59,6 +136,8 @@ struct HostTarget {
 HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, double twist_b);
 void save_target(const HostTarget& t, const std::string& path);
 HostTarget load_target(const std::string& path);
+void write_target_blob(BinOut& o, const HostTarget& t);  // embedded in DIAMCKPT files
+HostTarget read_target_blob(BinIn& r);
 
 // ---------------------------------------------------------------- diagnostics
 Vec acf(const double* x, size_t n, size_t max_lag);

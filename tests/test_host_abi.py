@@ -136,14 +136,16 @@ def test_diagnostics_match_reference(b200, ref_abi):
     assert ref_abi.lib.diam_iact(c.ctypes.data_as(dp), 100, C.byref(out)) == 7
 
 
-def test_checkpoint_and_resume_are_reported_not_silently_ignored(b200):
-    t = b200.target_build("pi1", 4, 1)
+def test_resume_rejects_missing_and_foreign_files(b200, tmp_path):
     with pytest.raises(DiamError) as e:
-        b200.sample(t, checkpoint_path="/tmp/x.ckpt")
-    assert e.value.status == 1 and "checkpoint" in e.value.message
-    with pytest.raises(DiamError) as e:
-        b200.resume("/tmp/x.ckpt")
+        b200.resume(str(tmp_path / "missing.ckpt"))
     assert e.value.status == 10
+    t = b200.target_build("pi1", 4, 1)
+    p = str(tmp_path / "target.bin")
+    t.save(p)  # a DIAMTGT file is not a DIAMCKPT file
+    with pytest.raises(DiamError) as e:
+        b200.resume(p)
+    assert e.value.status == 10 and "not a checkpoint" in e.value.message
 
 
 @pytest.mark.skipif(has_cuda(), reason="checks the no-GPU failure path")
