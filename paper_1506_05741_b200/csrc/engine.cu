@@ -91,7 +91,8 @@ Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> com
     init_chains();
     // two chain groups on two streams overlap one group's latency-bound pieces with the
     // other's GEMMs (DIAM_B200_GROUPS overrides, 1 = a single stream)
-    int ng = C_ >= 32 ? 4 : (C_ >= 8 ? 2 : 1);
+    // (small problems are launch-latency bound: one stream, fewer launches)
+    int ng = (C_ >= 32 && d_ >= 512) ? 4 : ((C_ >= 8 && d_ >= 256) ? 2 : 1);
     if (const char* e = std::getenv("DIAM_B200_GROUPS")) ng = std::max(1, std::min(C_, std::atoi(e)));
     make_groups(ng);
 }
