@@ -320,13 +320,16 @@ void Engine::timed_end(const char* name, double flops, cudaStream_t s) {
     cudaEvent_t b = event_pool_.back();
     event_pool_.pop_back();
     DGB_CUDA(cudaEventRecord(b, s));
-    pending_.push_back({name, open_.at(s), b, flops});
+    pending_.push_back({name, open_.at(s), b, flops, s});
     if (pending_.size() > 4096) resolve_events();
 }
 
 void Engine::resolve_events() {
     if (pending_.empty()) return;
     DGB_CUDA(cudaDeviceSynchronize());
+    static const char* tl_path = std::getenv("DIAM_B200_TIMELINE");  // CSV: name,stream,start_ms,end_ms
+    FILE* tl = nullptr;
+    if (tl_path && timeline_base_) tl = std::fopen(tl_path, "a");
     for (auto& p : pending_) {
         float ms = 0.f;
         DGB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
@@ -334,9 +337,15 @@ void Engine::resolve_events() {
         st.ms += ms;
         st.flops += p.flops;
         st.launches += 1;
+        if (tl) {
+            float t0 = 0.f;
+            DGB_CUDA(cudaEventElapsedTime(&t0, timeline_base_, p.a));
+            std::fprintf(tl, "%s,%p,%.4f,%.4f\n", p.name.c_str(), (void*)p.s, t0, t0 + ms);
+        }
         event_pool_.push_back(p.a);
         event_pool_.push_back(p.b);
     }
+    if (tl) std::fclose(tl);
     pending_.clear();
 }
 
@@ -808,6 +817,11 @@ double Engine::run_batches_timed(int k) {
     DGB_CUDA(cudaEventCreate(&b));
     DGB_CUDA(cudaDeviceSynchronize());
     DGB_CUDA(cudaEventRecord(a, stream_));
+    if (profiling_) {
+        resolve_events();
+        if (!timeline_base_) DGB_CUDA(cudaEventCreate(&timeline_base_));
+        DGB_CUDA(cudaEventRecord(timeline_base_, stream_));
+    }
     for (int i = 0; i < k; ++i) {
         fork_groups();
         run_batch_windows(false);

@@ -187,7 +187,9 @@ private:
         std::string name;
         cudaEvent_t a, b;
         double flops;
+        cudaStream_t s;
     };
+    cudaEvent_t timeline_base_ = nullptr;  // profiling: origin of the optional timeline dump
     std::vector<Pending> pending_;
     std::vector<cudaEvent_t> event_pool_;
     std::map<std::string, KernelStat> stats_;
