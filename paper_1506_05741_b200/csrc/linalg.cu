@@ -221,7 +221,8 @@ __global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(double* const* Lm, i
 // ------------------------------------------------------------------ Cholesky diagonal block
 constexpr int kNb = 64;
 
-__global__ void __launch_bounds__(256) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
+// (<= 128 registers: a diagonal-block CTA can share its SM with a GEMM CTA of another group)
+__global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
                                                          const int* mask, int* status, int* active,
                                                          double* inv_base, int zero_above) {
     // Register-blocked right-looking Cholesky of the 64x64 diagonal block, fused with

@@ -434,7 +434,13 @@ bool try_tma(const StepParams& p, cudaStream_t s) {
     const size_t table = (size_t)p.n_lag * sizeof(double);
     constexpr size_t kMaxSmem = 220 * 1024;
     if (table + 2 * stage > kMaxSmem) return false;
-    const int NS = (int)std::min<size_t>(8, (kMaxSmem - table) / stage);
+    // ring depth: deep enough to hide HBM latency, shallow enough that a 92 KB GEMM CTA of
+    // another chain group can share the SM (DIAM_B200_STEP_STAGES overrides)
+    static const int max_ns = [] {
+        const char* e = std::getenv("DIAM_B200_STEP_STAGES");
+        return e ? std::max(2, std::atoi(e)) : 8;
+    }();
+    const int NS = (int)std::min<size_t>((size_t)max_ns, (kMaxSmem - table) / stage);
     const size_t smem = NS * stage + table;
     auto kern = mh_window_tma_kernel<R, TW, T>;
     DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
