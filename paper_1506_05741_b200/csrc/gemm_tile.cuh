@@ -1,0 +1,196 @@
+// gemm_tile.cuh — one CTA tile of the FP64 DMMA GEMM, as a device function.
+//
+// Shared by the batched GEMM kernel (gemm_f64.cu) and the persistent per-chain
+// Cholesky kernel (linalg.cu). C[m][n] = alpha * sum_k A(m,k) B(k,n) + beta * C[m][n]
+// for the tile at (m0, n0):
+//   AK : A(m,k) = A[m*lda + k]   else A[k*lda + m]
+//   BKM: B(k,n) = B[n*ldb + k]   else B[k*ldb + n]
+// BK-deep stages stream global->shared with 16-byte cp.async (zero-filled edges)
+// through a STAGES-deep ring; 8 warps each own a WM x WN sub-tile of 8x8 DMMA
+// (mma.sync.m8n8k4.f64, SASS DMMA.8x8x4) accumulators in registers; shared
+// strides are 4 (mod 16) doubles so the per-lane fragment loads are conflict free.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dgb {
+namespace tile {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+template <int BM_, int BN_, int BK_, int STAGES_, bool AK, bool BKM, int WARPS_M_ = 2, int WARPS_N_ = 4,
+          int MINB_ = 1>
+struct Cfg {
+    static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_;
+    static constexpr int THREADS = 256;
+    static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+    static constexpr int MINB = MINB_;  // CTAs resident per SM (register budget 64K / (256 * MINB))
+    static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
+    static constexpr int MI = WM / 8, NI = WN / 8;
+    // shared layout: the global-contiguous dimension stays contiguous; stride = 4 mod 16
+    static constexpr int A_ROWS = AK ? BM : BK;
+    static constexpr int A_COLS = AK ? BK : BM;
+    static constexpr int A_STRIDE = A_COLS + 4;
+    static constexpr int B_ROWS = BKM ? BN : BK;
+    static constexpr int B_COLS = BKM ? BK : BN;
+    static constexpr int B_STRIDE = B_COLS + 4;
+    static constexpr int A_STAGE = A_ROWS * A_STRIDE;
+    static constexpr int B_STAGE = B_ROWS * B_STRIDE;
+    static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
+    static_assert(A_STRIDE % 16 == 4 && B_STRIDE % 16 == 4, "bank-conflict-free stride");
+    static_assert((A_ROWS * A_COLS / 2) % THREADS == 0 && (B_ROWS * B_COLS / 2) % THREADS == 0, "copy split");
+};
+
+// Copy one rows x cols tile (cols contiguous in global) into shared memory.
+// rows_valid / cols_valid are the in-bounds extents relative to the tile origin.
+template <int ROWS, int COLS, int STRIDE, int THREADS>
+__device__ __forceinline__ void load_tile(double* s, const double* g, int64_t ld, int rows_valid, int cols_valid,
+                                          int tid) {
+    constexpr int CHUNKS_PER_ROW = COLS / 2;
+    constexpr int TOTAL = ROWS * CHUNKS_PER_ROW;
+#pragma unroll
+    for (int i = 0; i < TOTAL / THREADS; ++i) {
+        const int c = tid + i * THREADS;
+        const int r = c / CHUNKS_PER_ROW;
+        const int cc = (c % CHUNKS_PER_ROW) * 2;
+        int bytes = 0;
+        if (r < rows_valid) bytes = cc + 1 < cols_valid ? 16 : (cc < cols_valid ? 8 : 0);
+        const double* src = bytes ? g + r * ld + cc : g;
+        cp_async16(s + r * STRIDE + cc, src, bytes);
+    }
+}
+
+// One BM x BN tile of C. K is the (possibly triangle-clipped) contraction length.
+// Starts with a barrier so back-to-back calls may reuse the shared ring.
+template <class CF, bool AK, bool BKM>
+__device__ __forceinline__ void gemm_tile(const double* A, const double* B, double* Cp, int64_t lda, int64_t ldb,
+                                          int64_t ldc, int M, int N, int K, int m0, int n0, double alpha,
+                                          double beta, bool tri_c_lower, double* smem) {
+    __syncthreads();
+    double* sA = smem;
+    double* sB = smem + CF::STAGES * CF::A_STAGE;
+    const int KT = (K + CF::BK - 1) / CF::BK;
+    const int tid = threadIdx.x;
+    if (beta != 0.0) {
+        // read-modify-write epilogue: pull the C tile towards L2 while the main loop runs
+        constexpr int LINES_PER_ROW = (CF::BN * 8 + 127) / 128;
+        for (int li = tid; li < CF::BM * LINES_PER_ROW; li += CF::THREADS) {
+            const int r = m0 + li / LINES_PER_ROW, cc = n0 + (li % LINES_PER_ROW) * 16;
+            if (r < M && cc < N) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Cp + (int64_t)r * ldc + cc));
+        }
+    }
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wm0 = (warp / CF::WARPS_N) * CF::WM;
+    const int wn0 = (warp % CF::WARPS_N) * CF::WN;
+
+    auto issue = [&](int kt, int stage) {
+        const int k0 = kt * CF::BK;
+        double* a_s = sA + stage * CF::A_STAGE;
+        double* b_s = sB + stage * CF::B_STAGE;
+        if (AK)
+            load_tile<CF::A_ROWS, CF::A_COLS, CF::A_STRIDE, 256>(a_s, A + (int64_t)m0 * lda + k0, lda, M - m0,
+                                                                 K - k0, tid);
+        else
+            load_tile<CF::A_ROWS, CF::A_COLS, CF::A_STRIDE, 256>(a_s, A + (int64_t)k0 * lda + m0, lda, K - k0,
+                                                                 M - m0, tid);
+        if (BKM)
+            load_tile<CF::B_ROWS, CF::B_COLS, CF::B_STRIDE, 256>(b_s, B + (int64_t)n0 * ldb + k0, ldb, N - n0,
+                                                                 K - k0, tid);
+        else
+            load_tile<CF::B_ROWS, CF::B_COLS, CF::B_STRIDE, 256>(b_s, B + (int64_t)k0 * ldb + n0, ldb, K - k0,
+                                                                 N - n0, tid);
+    };
+
+    double acc[CF::MI][CF::NI][2];
+#pragma unroll
+    for (int i = 0; i < CF::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < CF::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < CF::STAGES - 1; ++s) {
+        if (s < KT) issue(s, s);
+        cp_async_commit();
+    }
+
+    const int fr = lane >> 2;  // fragment row (A) / col (B)
+    const int fk = lane & 3;   // fragment k
+    for (int kt = 0; kt < KT; ++kt) {
+        cp_async_wait<CF::STAGES - 2>();
+        __syncthreads();
+        {
+            const int nk = kt + CF::STAGES - 1;
+            if (nk < KT) issue(nk, nk % CF::STAGES);
+            cp_async_commit();
+        }
+        const double* a_s = sA + (kt % CF::STAGES) * CF::A_STAGE;
+        const double* b_s = sB + (kt % CF::STAGES) * CF::B_STAGE;
+#pragma unroll
+        for (int kk = 0; kk < CF::BK; kk += 4) {
+            double af[CF::MI], bf[CF::NI];
+#pragma unroll
+            for (int i = 0; i < CF::MI; ++i) {
+                const int m = wm0 + i * 8 + fr, k = kk + fk;
+                af[i] = AK ? a_s[m * CF::A_STRIDE + k] : a_s[k * CF::A_STRIDE + m];
+            }
+#pragma unroll
+            for (int j = 0; j < CF::NI; ++j) {
+                const int n = wn0 + j * 8 + fr, k = kk + fk;
+                bf[j] = BKM ? b_s[n * CF::B_STRIDE + k] : b_s[k * CF::B_STRIDE + n];
+            }
+#pragma unroll
+            for (int i = 0; i < CF::MI; ++i)
+#pragma unroll
+                for (int j = 0; j < CF::NI; ++j) dmma(acc[i][j], af[i], bf[j]);
+        }
+    }
+    cp_async_wait<0>();
+
+#pragma unroll
+    for (int i = 0; i < CF::MI; ++i) {
+        const int r = m0 + wm0 + i * 8 + fr;
+        if (r >= M) continue;
+        double* crow = Cp + (int64_t)r * ldc;
+#pragma unroll
+        for (int j = 0; j < CF::NI; ++j) {
+            const int c0 = n0 + wn0 + j * 8 + fk * 2;
+            const bool ok0 = c0 < N && (!tri_c_lower || c0 <= r);
+            const bool ok1 = c0 + 1 < N && (!tri_c_lower || c0 + 1 <= r);
+            if (ok0 && ok1) {
+                double2 v = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+                if (beta != 0.0) {
+                    const double2 o = *reinterpret_cast<const double2*>(crow + c0);
+                    v.x += beta * o.x;
+                    v.y += beta * o.y;
+                }
+                *reinterpret_cast<double2*>(crow + c0) = v;
+            } else if (ok0) {
+                double v = alpha * acc[i][j][0];
+                if (beta != 0.0) v += beta * crow[c0];
+                crow[c0] = v;
+            }
+        }
+    }
+}
+
+}  // namespace tile
+}  // namespace dgb

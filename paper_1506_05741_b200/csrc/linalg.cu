@@ -1,7 +1,10 @@
 // linalg.cu — batched triangular solve, blocked Cholesky, moment and lag-update kernels.
 #include <cmath>
 
+#include <cstdlib>
+
 #include "gemm_f64.cuh"
+#include "gemm_tile.cuh"
 #include "kernels.cuh"
 
 namespace dgb {
@@ -221,26 +224,17 @@ __global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(double* const* Lm, i
 // ------------------------------------------------------------------ Cholesky diagonal block
 constexpr int kNb = 64;
 
-// (<= 128 registers: a diagonal-block CTA can share its SM with a GEMM CTA of another group)
-__global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
-                                                         const int* mask, int* status, int* active,
-                                                         double* inv_base, int zero_above) {
-    // Register-blocked right-looking Cholesky of the 64x64 diagonal block, fused with
-    // the explicit inverse of the factor (for the DMMA TRSM that follows). Thread
-    // (ty, tx) of a 16x16 grid owns the contiguous 4x4 sub-block rows 4ty+a, columns
-    // 4tx+b of both L and L^{-1} in registers. Columns are processed 4 at a time with
-    // the 4 steps unrolled, so register indices are static and the loop body stays
-    // small; each column step broadcasts the new column of L and the finished row of
-    // L^{-1} through shared memory (two barriers per column).
-    const int c = blockIdx.x;
+// Register-blocked right-looking Cholesky of one 64x64 diagonal block (at A, stride ld,
+// jb <= 64 valid rows/cols), fused with the explicit inverse of the factor (for the DMMA
+// TRSM that follows), by the 256 threads of a CTA. Thread (ty, tx) of a 16x16 grid owns
+// the contiguous 4x4 sub-block rows 4ty+a, columns 4tx+b of both L and L^{-1} in
+// registers. Writes L (zero strict upper part) back to A and the inverse to `out`
+// (64x64 row-major). Returns nonzero (uniformly) on a bad pivot.
+__device__ __forceinline__ int diag64_block(double* A, int64_t ld, int jb, double* out, int zero_above) {
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const bool run = (!mask || mask[c]) && status[c] == 0;
-    if (tid == 0) active[c] = run ? 1 : 0;
-    if (!run) return;
     __shared__ double colk[2][kNb], xrow[2][kNb];
     __shared__ double piv;
     __shared__ int bad;
-    double* A = Am[c] + (int64_t)j0 * ld + j0;
     double v[4][4], x[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -392,14 +386,8 @@ __global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, i
         }
     }
     __syncthreads();
-    if (bad) {
-        if (tid == 0) {
-            status[c] = 1;
-            active[c] = 0;
-        }
-        return;
-    }
-    double* out = inv_base + (int64_t)c * kNb * kNb;
+    const int failed = bad;
+    if (failed) return failed;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const int r = 4 * ty + a;
@@ -413,6 +401,75 @@ __global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, i
             // also touched by the block column's GEMM and lie above the diagonal
             if (zero_above && q < jb) A[(int64_t)(r - kNb) * ld + q] = 0.0;
         }
+    }
+    return 0;
+}
+
+// (<= 128 registers: a diagonal-block CTA can share its SM with a GEMM CTA of another group)
+__global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
+                                                         const int* mask, int* status, int* active,
+                                                         double* inv_base, int zero_above) {
+    const int c = blockIdx.x;
+    const bool run = (!mask || mask[c]) && status[c] == 0;
+    if (threadIdx.x == 0) active[c] = run ? 1 : 0;
+    if (!run) return;
+    if (diag64_block(Am[c] + (int64_t)j0 * ld + j0, ld, jb, inv_base + (int64_t)c * kNb * kNb, zero_above) &&
+        threadIdx.x == 0) {
+        status[c] = 1;
+        active[c] = 0;
+    }
+}
+
+// ------------------------------------------------------------------ persistent per-chain POTRF
+// One 2-CTA cluster per chain walks the whole left-looking factorization (64-wide block
+// columns): both CTAs split the panel-update and TRSM tiles of a block column, CTA 0
+// factors the diagonal block in between, and cluster barriers (release/acquire at cluster
+// scope) order the phases. One launch per factorization instead of three per block column,
+// and a group of chains occupies only 2 SMs per chain, leaving the rest of the GPU to the
+// other chain groups' GEMMs.
+using PotrfTile = tile::Cfg<128, 64, 16, 4, true, true, 4, 2, 1>;  // 123 KB ring: one CTA per SM
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    potrf_cluster_kernel(double* const* Am, int64_t ld, int d, int rows, const int* mask, int* status,
+                         double* inv_base) {
+    const int c = blockIdx.x >> 1;
+    const int rank = (int)cluster_rank();
+    if ((mask && !mask[c]) || status[c] != 0) return;  // uniform for both CTAs of the cluster
+    extern __shared__ __align__(16) double ring[];
+    double* A = Am[c];
+    double* inv = inv_base + (int64_t)c * kNb * kNb;
+    for (int j0 = 0; j0 < d; j0 += kNb) {
+        const int jb = min(kNb, d - j0);
+        if (j0 > 0) {  // A[j0:, J] -= L[j0:, :j0] L[J, :j0]^T, row tiles split over the pair
+            const int M = rows - j0;
+            for (int t = rank; t * PotrfTile::BM < M; t += 2)
+                tile::gemm_tile<PotrfTile, true, true>(A + (int64_t)j0 * ld, A + (int64_t)j0 * ld,
+                                                       A + (int64_t)j0 * ld + j0, ld, ld, ld, M, jb, j0,
+                                                       t * PotrfTile::BM, 0, -1.0, 1.0, false, ring);
+        }
+        cluster_sync_all();
+        if (rank == 0) {
+            const int failed = diag64_block(A + (int64_t)j0 * ld + j0, ld, jb, inv, 0);
+            if (failed && threadIdx.x == 0) status[c] = 1;
+        }
+        cluster_sync_all();
+        if (*(volatile int*)(status + c) != 0) return;  // both CTAs leave at the same point
+        const int M3 = rows - j0 - jb;
+        for (int t = rank; t * PotrfTile::BM < M3; t += 2)  // L21 = A21 inv(L11)^T in place
+            tile::gemm_tile<PotrfTile, true, true>(A + (int64_t)(j0 + jb) * ld + j0, inv,
+                                                   A + (int64_t)(j0 + jb) * ld + j0, ld, kNb, ld, M3, jb, jb,
+                                                   t * PotrfTile::BM, 0, 1.0, 0.0, false, ring);
+        cluster_sync_all();
     }
 }
 
@@ -706,6 +763,22 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     // w.inv holds chains*64*64 doubles, followed (by the caller's allocation) by an int active[chains]
     int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kNb * kNb);
     const int rows = d + extra_rows;
+    static const bool blocked = [] {
+        const char* e = std::getenv("DIAM_B200_POTRF");  // "blocked": the launch-per-phase path
+        return e && std::string(e) == "blocked";
+    }();
+    if (!blocked) {
+        static bool attr = false;
+        if (!attr) {
+            DGB_CUDA(cudaFuncSetAttribute(potrf_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          PotrfTile::SMEM_BYTES));
+            attr = true;
+        }
+        potrf_cluster_kernel<<<2 * chains, 256, PotrfTile::SMEM_BYTES, s>>>(A, ld, d, rows, mask, status, w.inv);
+        DGB_LAUNCH_CHECK();
+        count_launch();
+        return;
+    }
     // A[r0:rows, c0:c0+n] -= L[r0:rows, k0:k0+k] L[c0:c0+n, k0:k0+k]^T
     auto update = [&](int r0, int c0, int n, int k0, int k, GemmShape shape) {
         GemmBatch p{};
