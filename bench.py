@@ -263,13 +263,16 @@ def impl_b200(args):
     samples_per_step = chains * M * n_lag
     value = samples_per_step * args.steps / (ms / 1e3)
 
-    groups = eng.abi.lib.diamx_engine_local_chains(eng.h)  # noqa: F841 (keeps eng alive)
+    layout = eng.layout
+    alg_flops = eng.flops_per_batch
     del eng
     # ---- roofline of the dominant kernel class: a profiled pass on a single-stream engine
     # (CUDA events around every launch; with one chain group nothing overlaps, so each
-    # event pair times its kernel alone)
+    # event pair times its kernel alone). A run that needed the shared refactor workspace
+    # (d=8192) is profiled with half the chains, which fit on one stream.
+    prof_chains = chains if layout["pool_factors"] == 0 else max(1, chains // 2)
     os.environ["DIAM_B200_GROUPS"] = "1"
-    eng = lib.engine(t, **run_options(cfg, chains))
+    eng = lib.engine(t, **run_options(cfg, prof_chains))
     del os.environ["DIAM_B200_GROUPS"]
     eng.run_batches(max(1, args.warmup))
     eng.set_profiling(True)
@@ -284,7 +287,6 @@ def impl_b200(args):
     peak = C.c_double()
     lib.check(lib.lib.diamx_fp64_peak(C.byref(peak)))
     achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
-    alg_flops = eng.flops_per_batch
     del eng
 
     # ---- end-to-end through the C ABI (host target, result back to host)
@@ -326,6 +328,7 @@ def impl_b200(args):
                                    f"M={M} windows per step, n0=0, traces off",
                        "d": d, "chains": chains, "chains_per_gpu": per_gpu, "n_lag": n_lag,
                        "intervals_per_batch": M, "kernel": "diam", "parallelism": f"chains sharded dp{world}",
+                       "memory_plan": layout,
                        "l2": "no flush needed: per-step working set "
                              f"{(3 * d * d + 3 * n_lag * d) * 8 * per_gpu / 1e9:.1f} GB >> 126 MB L2"},
             "roofline": {"bound": "fp64-dmma", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
@@ -334,7 +337,8 @@ def impl_b200(args):
                          "share_of_step": g_ms / prof_total if prof_total else None,
                          "peak_source": "diamx_fp64_peak: DMMA m8n8k4 loop measured live (MEASURED_PEAKS.json "
                                         "has no FP64 entry)",
-                         "step_alg_tflops": alg_flops / (ms / args.steps / 1e3) / 1e12 / max(1, 1),
+                         "step_alg_tflops": alg_flops / (ms / args.steps / 1e3) / 1e12,
+                         "profile_chains": prof_chains,
                          "per_class_ms": {c: round(v[0], 4) for c, v in st.items()}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "chain-samples/s", "h2d_bytes_per_step": int(h2d),

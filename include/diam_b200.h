@@ -59,6 +59,11 @@ diam_status diamx_engine_stat(diamx_engine* e, const char* name, double* ms, dou
                               int64_t* launches);
 double diamx_engine_flops_per_batch(const diamx_engine* e);
 int64_t diamx_engine_local_chains(const diamx_engine* e);
+/* memory plan of an engine: chain groups (streams), rows per window chunk (= n_lag when
+ * the whole window is resident) and the shared refactor workspace size (0 = one
+ * workspace factor per chain) */
+diam_status diamx_engine_layout(const diamx_engine* e, int64_t* groups, int64_t* chunk_rows,
+                                int64_t* pool_factors);
 void diamx_engine_free(diamx_engine* e);
 
 /* parity capture: run a full diam_sample-equivalent and keep every window's

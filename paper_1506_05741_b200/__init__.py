@@ -59,6 +59,7 @@ class B200(DiamABI):
             "diamx_engine_stat": (st, [_vp, C.c_char_p, _dp, _dp, C.POINTER(i64)]),
             "diamx_engine_flops_per_batch": (C.c_double, [_vp]),
             "diamx_engine_local_chains": (i64, [_vp]),
+            "diamx_engine_layout": (st, [_vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
             "diamx_engine_free": (None, [_vp]),
             "diamx_sample_capture": (st, [_vp, C.POINTER(RunOptions), C.POINTER(_vp), C.POINTER(_vp)]),
             "diamx_capture_len": (i64, [_vp, i64, C.c_char_p]),
@@ -122,6 +123,12 @@ class Engine:
     @property
     def local_chains(self) -> int:
         return self.abi.lib.diamx_engine_local_chains(self.h)
+
+    @property
+    def layout(self) -> dict:
+        g, lc, pf = C.c_int64(), C.c_int64(), C.c_int64()
+        self.abi.check(self.abi.lib.diamx_engine_layout(self.h, C.byref(g), C.byref(lc), C.byref(pf)))
+        return {"groups": g.value, "chunk_rows": lc.value, "pool_factors": pf.value}
 
 
 class Capture(Engine):

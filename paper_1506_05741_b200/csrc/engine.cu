@@ -80,7 +80,6 @@ Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> com
     c0_ = static_cast<int>(first);
     C_ = static_cast<int>(count);
     ld_ = pad_ld(d_);
-    win_ = (int64_t)Lw_ * ld_;
     mat_ = (int64_t)d_ * ld_;
     fmat_ = (int64_t)(d_ + 1) * ld_;
     twisted_ = tgt_.twisted();
@@ -88,13 +87,86 @@ Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> com
     DGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     DGB_CUDA(cudaEventCreateWithFlags(&main_ev_, cudaEventDisableTiming));
     upload_target();
+    const int ng = plan_memory();
     init_chains();
-    // two chain groups on two streams overlap one group's latency-bound pieces with the
-    // other's GEMMs (DIAM_B200_GROUPS overrides, 1 = a single stream)
-    // (small problems are launch-latency bound: one stream, fewer launches)
-    int ng = (C_ >= 32 && d_ >= 512) ? 4 : ((C_ >= 8 && d_ >= 256) ? 2 : 1);
-    if (const char* e = std::getenv("DIAM_B200_GROUPS")) ng = std::max(1, std::min(C_, std::atoi(e)));
     make_groups(ng);
+}
+
+int Engine::plan_memory() {
+    // chain groups on separate streams overlap one group's latency-bound pieces (MH steps,
+    // diagonal factorizations) with the others' GEMMs; small problems are launch-latency
+    // bound and keep one stream (DIAM_B200_GROUPS overrides, 1 = a single stream)
+    int ng = (C_ >= 32 && d_ >= 512) ? 4 : ((C_ >= 8 && d_ >= 256) ? 2 : 1);
+    const char* eg = std::getenv("DIAM_B200_GROUPS");
+    if (eg) ng = std::max(1, std::min(C_, std::atoi(eg)));
+
+    // Device bytes for a window of lc rows per chain, with or without a shared refactor
+    // workspace. Free memory counts what the (resident) stream-ordered pool holds unused.
+    size_t free_b = 0, total_b = 0;
+    DGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    {
+        int dev = 0;
+        DGB_CUDA(cudaGetDevice(&dev));
+        cudaMemPool_t mp;
+        DGB_CUDA(cudaDeviceGetDefaultMemPool(&mp, dev));
+        uint64_t reserved = 0, used = 0;
+        DGB_CUDA(cudaMemPoolGetAttribute(mp, cudaMemPoolAttrReservedMemCurrent, &reserved));
+        DGB_CUDA(cudaMemPoolGetAttribute(mp, cudaMemPoolAttrUsedMemCurrent, &used));
+        if (reserved > used) free_b += reserved - used;
+    }
+    const double budget = 0.97 * (double)free_b - 1.5e9;  // context growth, NCCL, small buffers
+    const double M = (double)cfg_.intervals_per_batch;
+    auto need = [&](int lc, int ws_factors) {
+        double n = (double)C_ * fmat_;            // factors L
+        n += (double)ws_factors * fmat_;          // refactor workspace
+        n += (double)C_ * mat_;                   // local moments S
+        n += 3.0 * C_ * (double)lc * ld_;         // W, Xi, H
+        if (!cfg_.checkpoint_path.empty()) n += (double)C_ * mat_;  // cumulative S
+        n += 2.0 * mat_ + 3.0 * ld_;              // global snapshot, reduction buffer
+        n += 3.0 * M * C_ * Lw_;                  // per-batch traces
+        n += 16.0 * C_ * ld_ + 4096.0 * C_;       // chain vectors, POTRF inverse blocks
+        return 8.0 * n;
+    };
+    auto gmax = [&](int groups) { return (C_ + groups - 1) / groups; };
+
+    int lc = Lw_;
+    bool pool = false;
+    const char* ec = std::getenv("DIAM_B200_CHUNK");  // rows per window chunk (experiments, tests)
+    const char* ep = std::getenv("DIAM_B200_POOL");   // 1: shared refactor workspace
+    if (ec || ep) {
+        if (ec) lc = std::max(1, std::min(Lw_, std::atoi(ec)));
+        pool = ep && std::atoi(ep) != 0;
+    } else if (need(Lw_, C_) > budget) {
+        // 1) chunk the window (a divisor of n_lag keeps the target GEMM one matrix);
+        // 2) then share one refactor workspace between the groups, which refactor in turn
+        std::vector<int> divs;
+        for (int c = Lw_; c >= 1; --c)
+            if (Lw_ % c == 0) divs.push_back(c);
+        bool found = false;
+        for (int pass = 0; pass < 2 && !found; ++pass) {
+            const bool pl = pass == 1;
+            const int groups = pl && !eg ? std::max(ng, std::min(8, C_)) : ng;
+            for (int c : divs) {
+                if (c < (pl ? 64 : 256)) break;
+                if (need(c, pl ? gmax(groups) : C_) <= budget) {
+                    lc = c;
+                    pool = pl;
+                    ng = groups;
+                    found = true;
+                    break;
+                }
+            }
+        }
+        require(found, Err::InvalidArgument,
+                "run does not fit in device memory: " + std::to_string(C_) + " chains of dim " + std::to_string(d_) +
+                    " need " + std::to_string(need(64, gmax(std::min(8, C_))) / 1e9) + " GB, " +
+                    std::to_string(std::max(0.0, budget) / 1e9) + " GB available");
+    }
+    Lc_ = lc;
+    win_ = (int64_t)Lc_ * ld_;
+    pool_ = pool && ng > 1;
+    pool_n_ = pool_ ? gmax(ng) : 0;
+    return ng;
 }
 
 Engine::~Engine() {
@@ -105,6 +177,7 @@ Engine::~Engine() {
             cudaStreamDestroy(g.s);
         }
         if (g.done) cudaEventDestroy(g.done);
+        if (g.pool_ev) cudaEventDestroy(g.pool_ev);
     }
     for (void* p : allocs_) cudaFreeAsync(p, 0);
     cudaStreamSynchronize(0);
@@ -157,7 +230,8 @@ void Engine::init_chains() {
     auto& A = allocs_;
     const int C = C_;
     L_ = dalloc<double>(A, (size_t)C * fmat_);
-    Lw2_ = dalloc<double>(A, (size_t)C * fmat_);
+    const int nws = pool_ ? pool_n_ : C;  // refactor workspace factors
+    Lw2_ = dalloc<double>(A, (size_t)nws * fmat_);
     S_ = dalloc<double>(A, (size_t)C * mat_);
     W_ = dalloc<double>(A, (size_t)C * win_);
     Xi_ = dalloc<double>(A, (size_t)C * win_);
@@ -196,9 +270,10 @@ void Engine::init_chains() {
     hist_beta_ = dalloc<double>(A, M * C);
 
     Lp_ = ptr_array(A, L_, fmat_, C);
-    Lnp_ = ptr_array(A, Lw2_, fmat_, C);
+    Lnp_ = ptr_array(A, Lw2_, fmat_, nws);
     Wp_ = ptr_array(A, W_, win_, C);
     Xip_ = ptr_array(A, Xi_, win_, C);
+    Hp_ = ptr_array(A, H_, win_, C);
     Sp_ = ptr_array(A, S_, mat_, C);
 
     // RNG keys: global chain index p = c0 + i (runner.cpp:128-130, 556-559)
@@ -255,8 +330,11 @@ void Engine::make_groups(int n) {
         DGB_CUDA(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking));
         DGB_CUDA(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
         DGB_CUDA(cudaEventCreateWithFlags(&g.status_ev, cudaEventDisableTiming));
+        DGB_CUDA(cudaEventCreateWithFlags(&g.pool_ev, cudaEventDisableTiming));
         g.Lp = Lp_ + g.off;
-        g.Lnp = Lnp_ + g.off;
+        // pool mode: every group factors into the same workspace (slot i <-> the group's
+        // chain i); accepted factors swap pointers with their slot as before
+        g.Lnp = pool_ ? Lnp_ : Lnp_ + g.off;
         g.Wp = Wp_ + g.off;
         g.Xip = Xip_ + g.off;
         g.Sp = Sp_ + g.off;
@@ -415,12 +493,30 @@ void Engine::run_batch_windows(bool record) {
         commit_window(plans.back());
     };
     if (capture_) {
-        // parity capture: strictly ordered windows (W must still be resident when copied)
+        // parity capture: strictly ordered windows and groups (W is copied chunk by chunk)
         for (size_t m = 0; m < M; ++m) {
             next_plan(m);
-            for (auto& g : groups_) enqueue_head(g, plans[m]);
-            for (auto& g : groups_) enqueue_tail(g, plans[m]);
+            for (auto& g : groups_) {
+                enqueue_head(g, plans[m]);
+                enqueue_tail(g, plans[m]);
+            }
             capture_window(m);
+        }
+        return;
+    }
+    if (pool_) {
+        // shared refactor workspace: group g refactors after group g-1's tail released the
+        // workspace, so g's refactor is enqueued after that tail; the other groups' steps
+        // keep the GPU busy meanwhile
+        next_plan(0);
+        for (auto& g : groups_) enqueue_steps(g, plans[0]);
+        for (size_t m = 0; m < M; ++m) {
+            if (m + 1 < M) next_plan(m + 1);
+            for (auto& g : groups_) {
+                enqueue_refactor(g, plans[m]);
+                enqueue_tail(g, plans[m]);
+                if (m + 1 < M) enqueue_steps(g, plans[m + 1]);
+            }
         }
         return;
     }
@@ -437,14 +533,28 @@ void Engine::run_batch_windows(bool record) {
     }
 }
 
-void Engine::enqueue_head(Group& g, const WindowPlan& p) {
+void Engine::enqueue_steps(Group& g, const WindowPlan& p) {
+    for (int r0 = 0; r0 < Lw_; r0 += Lc_) enqueue_chunk(g, p, r0, std::min(Lc_, Lw_ - r0));
+    // ---- lag update (proposal.cpp:159-216): beta from the window's acceptance rate
+    const int o = g.off;
+    launch_beta_update(beta_ + o, nacc_ + o, hist_rate_ + p.w * C_ + o, hist_beta_ + p.w * C_ + o, g.C, Lw_,
+                       k_.adapt_beta ? 1 : 0, k_.band_lo, k_.band_hi, k_.beta_adapt_factor, k_.beta_min, k_.beta_max,
+                       g.s);
+}
+
+// Rows [r0, r0 + rows) of the window: noise, target GEMM, the MH steps, and the moments
+// of the chunk's post-burn-in states. The step recursion's state (x, G x, y, log pi,
+// counters) lives in global memory, so consecutive chunks continue one another exactly;
+// only the running-average moment update is split at chunk boundaries (rounding).
+void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     const int C = g.C, o = g.off;
     const cudaStream_t s = g.s;
     const double infl = k_.noise_infl();
-    // ---- noise window: W from Philox, Xi = s W L^T, H = Xi G^T (proposal.cpp:254-266)
+    // ---- noise: W from Philox, Xi = s W L^T, H = Xi G^T (proposal.cpp:254-266); row r of
+    // the window draws counters nctr + r d .. nctr + (r + 1) d - 1 of the chain's stream
     timed_begin(s);
-    launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, Lw_, d_, ld_, nkeys_ + o, p.nctr,
-                   beta_ + o, infl, s);
+    launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, rows, d_, ld_, nkeys_ + o,
+                   p.nctr + (uint64_t)r0 * d_, beta_ + o, infl, s);
     timed_end("normals", 0.0, s);
     if (!p.identity) {
         GemmBatch t{};
@@ -454,7 +564,7 @@ void Engine::enqueue_head(Group& g, const WindowPlan& p) {
         t.lda = ld_;
         t.ldb = ld_;
         t.ldc = ld_;
-        t.M = Lw_;
+        t.M = rows;
         t.N = d_;
         t.K = d_;
         t.alpha = 1.0;
@@ -466,24 +576,32 @@ void Engine::enqueue_head(Group& g, const WindowPlan& p) {
     }
     {
         GemmBatch h{};
-        h.A = (const double* const*)g.Xib;
         h.B = (const double* const*)Gp_;
-        h.C = g.Hb;
         h.lda = ld_;
         h.ldb = ld_;
         h.ldc = ld_;
-        h.M = C * Lw_;  // the group's windows are one contiguous (C Lw) x ld matrix
         h.N = d_;
         h.K = d_;
         h.alpha = 1.0;
         h.beta = 0.0;
-        gemm("gemm_target", h, 1, true, true, s);
+        if (rows == Lc_) {
+            h.A = (const double* const*)g.Xib;
+            h.C = g.Hb;
+            h.M = C * Lc_;  // the group's window chunks are one contiguous (C Lc) x ld matrix
+            gemm("gemm_target", h, 1, true, true, s);
+        } else {            // ragged last chunk: per-chain pieces
+            h.A = (const double* const*)g.Xip;
+            h.C = Hp_ + o;
+            h.M = rows;
+            gemm("gemm_target", h, C, true, true, s);
+        }
     }
 
-    // ---- the n_lag MH steps (proposal.cpp:137-157, runner.cpp:363-368)
+    // ---- the chunk's MH steps (proposal.cpp:137-157, runner.cpp:363-368)
     StepParams sp{};
     sp.d = d_;
-    sp.n_lag = Lw_;
+    sp.n_lag = rows;
+    sp.out_ld = Lw_;
     sp.chains = C;
     sp.ld = ld_;
     sp.win_stride = win_;
@@ -505,43 +623,47 @@ void Engine::enqueue_head(Group& g, const WindowPlan& p) {
     sp.pcn = k_.pcn_form() ? 1 : 0;
     sp.inv_eig = inv_eig_;
     sp.bcoef = bcoef_;
-    sp.trace_lp = p.record ? trace_lp_ + (p.w * C_ + o) * (size_t)Lw_ : nullptr;
-    sp.accept_out = capture_ ? dbg_acc_ + (size_t)o * Lw_ : nullptr;
-    sp.log_ratio_out = capture_ ? dbg_ratio_ + (size_t)o * Lw_ : nullptr;
+    sp.trace_lp = p.record ? trace_lp_ + (p.w * C_ + o) * (size_t)Lw_ + r0 : nullptr;
+    sp.accept_out = capture_ ? dbg_acc_ + (size_t)o * Lw_ + r0 : nullptr;
+    sp.log_ratio_out = capture_ ? dbg_ratio_ + (size_t)o * Lw_ + r0 : nullptr;
     timed_begin(s);
     launch_mh_window(sp, twisted_, s);
     timed_end("mh_window", 0.0, s);
+    if (capture_) capture_chunk(g, r0, rows);
 
-    // ---- moments of the post-burn-in states (proposal.cpp:153-155)
-    if (p.k > 0) {
-        const double total = (double)p.cnt_after;
+    // ---- moments of the chunk's post-burn-in states (proposal.cpp:153-155): window rows
+    // t >= first count, so the chunk holds rows [lf, rows) after cb earlier samples
+    const int lf = std::clamp(p.first - r0, 0, rows);
+    const int kc = rows - lf;
+    const uint64_t cb = p.cnt_before + (uint64_t)std::max(0, r0 - p.first);
+    if (kc > 0) {
+        const double total = (double)(cb + (uint64_t)kc);
         GemmBatch m{};
         m.A = (const double* const*)g.Xip;
         m.B = (const double* const*)g.Xip;
         m.C = g.Sp;
-        m.a_off = (int64_t)p.first * ld_;
-        m.b_off = (int64_t)p.first * ld_;
+        m.a_off = (int64_t)lf * ld_;
+        m.b_off = (int64_t)lf * ld_;
         m.lda = ld_;
         m.ldb = ld_;
         m.ldc = ld_;
         m.M = d_;
         m.N = d_;
-        m.K = p.k;
+        m.K = kc;
         m.alpha = 1.0 / total;
-        m.beta = (double)p.cnt_before / total;
+        m.beta = (double)cb / total;
         m.tri_c_lower = 1;
         gemm("syrk_moments", m, C, false, false, s);
-        launch_mean_update(mean_ + o * ld_, ld_, Xi_ + o * win_, win_, ld_, C, d_, p.first, p.k,
-                           (double)p.cnt_before, s);
+        launch_mean_update(mean_ + o * ld_, ld_, Xi_ + o * win_, win_, ld_, C, d_, lf, kc, (double)cb, s);
     }
     if (p.record && cfg_.trace_eigen_projections)
-        launch_project_rows(Xi_ + o * win_, win_, ld_, C, Lw_, p.first, d_, proj_,
-                            trace_pj_ + (p.w * C_ + o) * (size_t)Lw_ * 2, s);
+        launch_project_rows(Xi_ + o * win_, win_, ld_, C, rows, lf, d_, proj_,
+                            trace_pj_ + ((p.w * C_ + o) * (size_t)Lw_ + r0) * 2, Lw_, s);
+}
 
-    // ---- lag update (proposal.cpp:159-216)
-    launch_beta_update(beta_ + o, nacc_ + o, hist_rate_ + p.w * C_ + o, hist_beta_ + p.w * C_ + o, C, Lw_,
-                       k_.adapt_beta ? 1 : 0, k_.band_lo, k_.band_hi, k_.beta_adapt_factor, k_.beta_min, k_.beta_max,
-                       s);
+void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {
+    const int C = g.C, o = g.off;
+    const cudaStream_t s = g.s;
     if (p.refactor) {
         // blend -> covariance into the workspace factor, trace floor, POTRF (proposal.cpp:176-184).
         // pCN-form kernels append r = x - x_ref as row d: the factorization then also
@@ -549,6 +671,8 @@ void Engine::enqueue_head(Group& g, const WindowPlan& p) {
         const bool aug = k_.pcn_form();
         const double* ax = aug ? x_ + o * ld_ : nullptr;
         const double* axr = aug && k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
+        // shared workspace: wait until the previous group's tail has released it
+        if (pool_ && pool_last_) DGB_CUDA(cudaStreamWaitEvent(s, pool_last_, 0));
         timed_begin(s);
         launch_blend_cov(g.Lnp, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, mb_ + o * ld_, ld_, C,
                          d_, ld_, nullptr, 0.0, nullptr, s, ax, axr);
@@ -617,6 +741,10 @@ void Engine::enqueue_tail(Group& g, const WindowPlan& p) {
             qmax = 5.0 * d_;
         }
         launch_accept_factor(g.Lp, g.Lnp, try_ + o, status_ + o, qtmp_ + o, qmax, C, usable_ + o, s);
+        if (pool_) {  // the shared workspace is free for the next group
+            DGB_CUDA(cudaEventRecord(g.pool_ev, s));
+            pool_last_ = g.pool_ev;
+        }
         // adopted factors come with y = L^-1 (x - x_ref) and the quad term for free
         if (aug && !k_.adaptive_ref)
             launch_aug_adopt(g.Lp, ld_, d_, C, usable_ + o, qtmp_ + o, y_ + o * ld_, quad_ + o, s);
@@ -641,8 +769,19 @@ void Engine::enqueue_tail(Group& g, const WindowPlan& p) {
     refresh_g(g.xp, g.gp, C, s);
 }
 
+void Engine::capture_chunk(const Group& g, int r0, int rows) {
+    // parity-test capture: the chunk's W rows of the group's chains, before the next
+    // chunk overwrites them
+    DGB_CUDA(cudaStreamSynchronize(g.s));
+    if (cap_wbuf_.empty()) cap_wbuf_.assign((size_t)C_ * Lw_ * d_, 0.0);
+    for (int c = 0; c < g.C; ++c)
+        DGB_CUDA(cudaMemcpy2D(cap_wbuf_.data() + ((size_t)(g.off + c) * Lw_ + r0) * d_, (size_t)d_ * 8,
+                              W_ + (g.off + c) * win_, (size_t)ld_ * 8, (size_t)d_ * 8, rows,
+                              cudaMemcpyDeviceToHost));
+}
+
 void Engine::capture_window(size_t) {
-    // parity-test capture: needs the window's W (still resident) and the step records
+    // parity-test capture: the window's W (captured chunk by chunk) and the step records
     DGB_CUDA(cudaDeviceSynchronize());
     const int C = C_;
     if (cap_w_.empty()) {
@@ -650,15 +789,13 @@ void Engine::capture_window(size_t) {
         cap_ratio_.assign(C, {});
         cap_acc_.assign(C, {});
     }
-    std::vector<double> buf((size_t)C * win_), r((size_t)C * Lw_);
+    std::vector<double> r((size_t)C * Lw_);
     std::vector<uint8_t> a((size_t)C * Lw_);
-    DGB_CUDA(cudaMemcpy(buf.data(), W_, buf.size() * 8, cudaMemcpyDeviceToHost));
     DGB_CUDA(cudaMemcpy(r.data(), dbg_ratio_, r.size() * 8, cudaMemcpyDeviceToHost));
     DGB_CUDA(cudaMemcpy(a.data(), dbg_acc_, a.size(), cudaMemcpyDeviceToHost));
     for (int c = 0; c < C; ++c) {
-        for (int row = 0; row < Lw_; ++row)
-            cap_w_[c].insert(cap_w_[c].end(), buf.begin() + (size_t)c * win_ + (size_t)row * ld_,
-                             buf.begin() + (size_t)c * win_ + (size_t)row * ld_ + d_);
+        cap_w_[c].insert(cap_w_[c].end(), cap_wbuf_.begin() + (size_t)c * Lw_ * d_,
+                         cap_wbuf_.begin() + (size_t)(c + 1) * Lw_ * d_);
         cap_ratio_[c].insert(cap_ratio_[c].end(), r.begin() + (size_t)c * Lw_, r.begin() + (size_t)(c + 1) * Lw_);
         cap_acc_[c].insert(cap_acc_[c].end(), a.begin() + (size_t)c * Lw_, a.begin() + (size_t)(c + 1) * Lw_);
     }

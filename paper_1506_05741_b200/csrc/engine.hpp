@@ -75,6 +75,8 @@ public:
     int dim() const { return d_; }
     int n_lag() const { return Lw_; }
     int groups() const { return (int)groups_.size(); }
+    int chunk_rows() const { return Lc_; }
+    int pool_factors() const { return pool_ ? pool_n_ : 0; }
     double flops_per_batch() const;  // algorithmic FP64 flops of one batch (all local chains)
 
 private:
@@ -87,6 +89,7 @@ private:
         double **Xib = nullptr, **Hb = nullptr;                                     // 1-element arrays
         PotrfWork pw{};
         cudaEvent_t status_ev = nullptr;  // POTRF statuses of the group's last window landed in h_status_
+        cudaEvent_t pool_ev = nullptr;    // shared refactor workspace released (pool mode)
     };
     // host-side scalars of one lag window, identical for every chain
     struct WindowPlan {
@@ -100,6 +103,7 @@ private:
     };
 
     void upload_target();
+    int plan_memory();  // window chunk rows, shared refactor workspace; returns the group count
     void init_chains();
     void make_groups(int n);
     WindowPlan plan_window(size_t w, bool record) const;
@@ -107,10 +111,18 @@ private:
     // a window is enqueued in two parts: the head (noise .. POTRF, statuses copied to the
     // host asynchronously) and the tail (jitter ladder if any chain failed, usable guard,
     // factor swap, reference point, G x). Between them the host reads the group's
-    // statuses while the other group keeps the GPU busy.
-    void enqueue_head(Group& g, const WindowPlan& p);
+    // statuses while the other group keeps the GPU busy. The head is the window's steps
+    // (chunk by chunk) followed by the refactorization.
+    void enqueue_head(Group& g, const WindowPlan& p) {
+        enqueue_steps(g, p);
+        enqueue_refactor(g, p);
+    }
+    void enqueue_steps(Group& g, const WindowPlan& p);
+    void enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows);
+    void enqueue_refactor(Group& g, const WindowPlan& p);
     void enqueue_tail(Group& g, const WindowPlan& p);
     void run_batch_windows(bool record);
+    void capture_chunk(const Group& g, int r0, int rows);
     void capture_window(size_t w);
     void fork_groups();  // groups wait for the main stream
     void join_groups();  // main stream waits for every group
@@ -133,6 +145,13 @@ private:
     std::shared_ptr<Comm> comm_;
     int rank_ = 0, world_ = 1;
     int d_ = 0, Lw_ = 0, C_ = 0, P_ = 0, c0_ = 0;
+    // memory plan (plan_memory): window buffers hold Lc_ rows per chain (Lc_ < Lw_: the
+    // window runs in chunks); pool_: the chain groups share one refactor workspace of
+    // pool_n_ factors and refactor one after another
+    int Lc_ = 0;
+    bool pool_ = false;
+    int pool_n_ = 0;
+    cudaEvent_t pool_last_ = nullptr;  // latest release of the shared workspace
     int64_t ld_ = 0, win_ = 0, mat_ = 0;
     int64_t fmat_ = 0;  // factor stride: d rows + the augmented row r = x - x_ref
     bool twisted_ = false, identity_ = true;
@@ -148,7 +167,7 @@ private:
     double* bcoef_ = nullptr;
     double* proj_ = nullptr;   // 2 x ld
     double *L_ = nullptr, *Lw2_ = nullptr, *S_ = nullptr;  // C x ((d+1) or d) x ld
-    double *W_ = nullptr, *Xi_ = nullptr, *H_ = nullptr;   // C x (Lw x ld)
+    double *W_ = nullptr, *Xi_ = nullptr, *H_ = nullptr;   // C x (Lc x ld)
     double *x_ = nullptr, *g_ = nullptr, *y_ = nullptr, *xr_ = nullptr, *gr_ = nullptr;
     double *mean_ = nullptr, *cmean_ = nullptr, *cdiag_ = nullptr, *mb_ = nullptr;
     double *logpi_ = nullptr, *quad_ = nullptr, *beta_ = nullptr, *tr_ = nullptr, *qtmp_ = nullptr;
@@ -157,7 +176,7 @@ private:
     int* h_flags_ = nullptr;  // pinned host mirror: status[C] then try[C]
     PhiloxKey *nkeys_ = nullptr, *ukeys_ = nullptr, *ikeys_ = nullptr;
     double **Lp_ = nullptr, **Lnp_ = nullptr;  // factor / workspace pointer arrays (swapped on device)
-    double **Wp_ = nullptr, **Xip_ = nullptr, **Sp_ = nullptr, **Gp_ = nullptr;
+    double **Wp_ = nullptr, **Xip_ = nullptr, **Hp_ = nullptr, **Sp_ = nullptr, **Gp_ = nullptr;
     double *Sg_ = nullptr, *mg_ = nullptr, *Ssum_ = nullptr;  // global snapshot, reduction buffer
     double *trace_lp_ = nullptr, *trace_pj_ = nullptr;      // per batch: M x C x Lw (x2)
     double *hist_rate_ = nullptr, *hist_beta_ = nullptr;    // per batch: M x C
@@ -198,6 +217,7 @@ private:
     bool capture_ = false;
     std::vector<std::vector<double>> cap_w_, cap_ratio_;
     std::vector<std::vector<uint8_t>> cap_acc_;
+    std::vector<double> cap_wbuf_;  // C x n_lag x d: the current window's W, filled chunk by chunk
     double* dbg_ratio_ = nullptr;
     uint8_t* dbg_acc_ = nullptr;
 };

@@ -59,9 +59,11 @@ struct StepParams {
     int pcn;  // pCN-form kernels (pCN, DIAM)
     const double* inv_eig;  // twisted: 1/sigma^2 (len d)
     const double* bcoef;    // twisted: twist coefficients (len d)
-    double* trace_lp;       // [chain][n_lag], nullable
-    uint8_t* accept_out;    // [chain][n_lag], nullable
-    double* log_ratio_out;  // [chain][n_lag], nullable (parity tests)
+    double* trace_lp;       // [chain][out_ld], nullable
+    uint8_t* accept_out;    // [chain][out_ld], nullable
+    double* log_ratio_out;  // [chain][out_ld], nullable (parity tests)
+    int out_ld;             // per-chain stride of the outputs above (the window length: a
+                            // chunk of a window writes at its row offset); 0 = n_lag
 };
 void launch_mh_window(const StepParams& p, bool twisted, cudaStream_t s);
 
@@ -139,7 +141,7 @@ void launch_blend_mean(const double* mg, const double* ml, double wg, double wl,
                        int d, int64_t ld, cudaStream_t s);
 // out[c][t][0..1] = proj[0..1] . X_c[t], t in [t0, rows)
 void launch_project_rows(const double* X, int64_t win_stride, int64_t ld, int chains, int rows, int t0,
-                         int d, const double* proj, double* out, cudaStream_t s);
+                         int d, const double* proj, double* out, int out_ld, cudaStream_t s);
 void launch_copy_vecs(double* dst, const double* src, int64_t n, const int* mask_per_chain,
                       int64_t stride, int chains, cudaStream_t s);
 

@@ -656,7 +656,7 @@ __global__ void blend_mean_kernel(const double* mg, const double* ml, double wg,
 }
 
 __global__ void project_rows_kernel(const double* X, int64_t win_stride, int64_t ld, int rows, int t0, int d,
-                                    const double* proj, double* out) {
+                                    const double* proj, double* out, int out_ld) {
     const int c = blockIdx.y;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int t = t0 + warp;
@@ -670,8 +670,8 @@ __global__ void project_rows_kernel(const double* X, int64_t win_stride, int64_t
     a = warp_sum(a);
     b = warp_sum(b);
     if (lane == 0) {
-        out[((int64_t)c * rows + t) * 2] = a;
-        out[((int64_t)c * rows + t) * 2 + 1] = b;
+        out[((int64_t)c * out_ld + t) * 2] = a;
+        out[((int64_t)c * out_ld + t) * 2 + 1] = b;
     }
 }
 
@@ -905,11 +905,11 @@ void launch_blend_mean(const double* mg, const double* ml, double wg, double wl,
 }
 
 void launch_project_rows(const double* X, int64_t win_stride, int64_t ld, int chains, int rows, int t0, int d,
-                         const double* proj, double* out, cudaStream_t s) {
+                         const double* proj, double* out, int out_ld, cudaStream_t s) {
     if (t0 >= rows) return;
     const int warps = rows - t0;
     dim3 grid((unsigned)ceil_div((int64_t)warps * 32, 256), chains);
-    project_rows_kernel<<<grid, 256, 0, s>>>(X, win_stride, ld, rows, t0, d, proj, out);
+    project_rows_kernel<<<grid, 256, 0, s>>>(X, win_stride, ld, rows, t0, d, proj, out, out_ld);
     DGB_LAUNCH_CHECK();
     count_launch();
 }

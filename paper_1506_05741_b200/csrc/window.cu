@@ -193,9 +193,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
             }
         }
         if (tid == 0) {
-            if (p.trace_lp) p.trace_lp[(int64_t)c * p.n_lag + t] = lp;
-            if (p.accept_out) p.accept_out[(int64_t)c * p.n_lag + t] = acc ? 1 : 0;
-            if (p.log_ratio_out) p.log_ratio_out[(int64_t)c * p.n_lag + t] = ratio;
+            if (p.trace_lp) p.trace_lp[(int64_t)c * p.out_ld + t] = lp;
+            if (p.accept_out) p.accept_out[(int64_t)c * p.out_ld + t] = acc ? 1 : 0;
+            if (p.log_ratio_out) p.log_ratio_out[(int64_t)c * p.out_ld + t] = ratio;
         }
         if (PREF) {
 #pragma unroll
@@ -400,9 +400,9 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
             }
         }
         if (tid == 0) {
-            if (p.trace_lp) p.trace_lp[(int64_t)c * p.n_lag + t] = lp;
-            if (p.accept_out) p.accept_out[(int64_t)c * p.n_lag + t] = acc ? 1 : 0;
-            if (p.log_ratio_out) p.log_ratio_out[(int64_t)c * p.n_lag + t] = ratio;
+            if (p.trace_lp) p.trace_lp[(int64_t)c * p.out_ld + t] = lp;
+            if (p.accept_out) p.accept_out[(int64_t)c * p.out_ld + t] = acc ? 1 : 0;
+            if (p.log_ratio_out) p.log_ratio_out[(int64_t)c * p.out_ld + t] = ratio;
         }
     }
 #pragma unroll
@@ -516,8 +516,10 @@ void launch_draws(int kind, double* out_f64, uint64_t* out_u64, int64_t n, Philo
 
 void launch_mh_window(const StepParams& p, bool twisted, cudaStream_t s) {
     if (p.chains <= 0 || p.n_lag <= 0) return;
-    if (twisted) launch_r<true>(p, s);
-    else launch_r<false>(p, s);
+    StepParams q = p;
+    if (q.out_ld <= 0) q.out_ld = q.n_lag;
+    if (twisted) launch_r<true>(q, s);
+    else launch_r<false>(q, s);
 }
 
 }  // namespace dgb

@@ -103,6 +103,43 @@ def test_lockstep_odd_dimension_and_multi_tile(b200, tmp_path):
     assert ties == 0
 
 
+@pytest.mark.parametrize("chunk,pool,groups", [(37, 0, 1), (37, 1, 2), (50, 1, 4)])
+def test_lockstep_chunked_windows_shared_workspace(b200, tmp_path, monkeypatch, chunk, pool, groups):
+    # the large-d memory plan: windows run in chunks of `chunk` rows (37: ragged last
+    # chunk) and the chain groups share one refactor workspace, refactoring in turn
+    monkeypatch.setenv("DIAM_B200_CHUNK", str(chunk))
+    monkeypatch.setenv("DIAM_B200_POOL", str(pool))
+    monkeypatch.setenv("DIAM_B200_GROUPS", str(groups))
+    _, _, ties = lockstep(b200, tmp_path, "pi2", 133, "diam", P=4, M=2, K=2, n_lag=150, n0=60, seed=9)
+    assert ties == 0
+
+
+def test_chunked_run_matches_resident_run(b200, monkeypatch):
+    """Chunked windows + shared workspace change only the moment update's rounding:
+    decisions, histories and traces (log density, eigen projections) match the
+    resident-window run; moments agree to 1e-12."""
+    t = b200.target_build("pi1", 40, 3)
+    kw = dict(kernel="diam", chains=6, intervals_per_batch=3, max_batches=2, n_lag=64, n0=50, master_seed=21,
+              trace_thin=3)
+    monkeypatch.setenv("DIAM_B200_GROUPS", "3")
+    r0 = b200.sample(t, **kw)
+    monkeypatch.setenv("DIAM_B200_CHUNK", "24")
+    monkeypatch.setenv("DIAM_B200_POOL", "1")
+    eng = b200.engine(t, **kw)
+    assert eng.layout == {"groups": 3, "chunk_rows": 24, "pool_factors": 2}
+    del eng
+    r1 = b200.sample(t, **kw)
+    for p in range(6):
+        assert np.array_equal(r0.chain_history(p, "acceptance"), r1.chain_history(p, "acceptance"))
+        assert np.array_equal(r0.chain_history(p, "beta"), r1.chain_history(p, "beta"))
+        for f in range(3):
+            a, b = r0.trace(p, f), r1.trace(p, f)
+            assert a.shape == b.shape
+            assert np.max(np.abs(a - b)) <= 1e-9 * max(1.0, np.max(np.abs(a)))
+    assert np.linalg.norm(r0.cov() - r1.cov()) <= 1e-12 * np.linalg.norm(r0.cov())
+    assert np.linalg.norm(r0.mean() - r1.mean()) <= 1e-12 * max(1.0, np.linalg.norm(r0.mean()))
+
+
 def test_golden_target_runs_statistics(b200):
     """The reference's own golden runs (tests/golden/runs.npz): same config on the GPU."""
     import sys

@@ -25,6 +25,7 @@ def main():
     path = bench.make_target_file(kind, d)
     t = lib.target_load(path)
     eng = lib.engine(t, **bench.run_options(cfg, args.chains or per_gpu))
+    print(f"layout {eng.layout}", flush=True)
     eng.run_batches(1)
     ms = eng.run_batches(args.batches)
     os.unlink(path)
