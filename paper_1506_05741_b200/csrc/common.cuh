@@ -21,7 +21,15 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
                         file + ":" + std::to_string(line));
 }
 #define DGB_CUDA(x) ::dgb::cuda_check((x), #x, __FILE__, __LINE__)
-#define DGB_LAUNCH_CHECK() ::dgb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// DIAM_B200_SYNC_CHECK=1: synchronize after every launch so a device fault is reported
+// at the kernel that caused it (debugging only)
+bool sync_check_enabled();
+inline void launch_check(const char* file, int line) {
+    cuda_check(cudaGetLastError(), "kernel launch", file, line);
+    if (sync_check_enabled()) cuda_check(cudaDeviceSynchronize(), "kernel execution", file, line);
+}
+#define DGB_LAUNCH_CHECK() ::dgb::launch_check(__FILE__, __LINE__)
 
 // Process-wide count of our own kernel launches (bench.py reports it as gpu_launches).
 extern uint64_t g_launch_count;

@@ -16,6 +16,14 @@ namespace dgb {
 
 uint64_t g_launch_count = 0;
 
+bool sync_check_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DIAM_B200_SYNC_CHECK");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 namespace {
 
 // Engine buffers come from the device's stream-ordered memory pool, kept resident
@@ -274,6 +282,7 @@ void Engine::init_chains() {
     Wp_ = ptr_array(A, W_, win_, C);
     Xip_ = ptr_array(A, Xi_, win_, C);
     Hp_ = ptr_array(A, H_, win_, C);
+    Gpc_ = ptr_array(A, G_, 0, C);  // G once per chain (batched GEMMs)
     Sp_ = ptr_array(A, S_, mat_, C);
 
     // RNG keys: global chain index p = c0 + i (runner.cpp:128-130, 556-559)
@@ -590,6 +599,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
             h.M = C * Lc_;  // the group's window chunks are one contiguous (C Lc) x ld matrix
             gemm("gemm_target", h, 1, true, true, s);
         } else {            // ragged last chunk: per-chain pieces
+            h.B = (const double* const*)Gpc_;
             h.A = (const double* const*)g.Xip;
             h.C = Hp_ + o;
             h.M = rows;

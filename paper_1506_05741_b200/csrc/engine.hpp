@@ -176,7 +176,7 @@ private:
     int* h_flags_ = nullptr;  // pinned host mirror: status[C] then try[C]
     PhiloxKey *nkeys_ = nullptr, *ukeys_ = nullptr, *ikeys_ = nullptr;
     double **Lp_ = nullptr, **Lnp_ = nullptr;  // factor / workspace pointer arrays (swapped on device)
-    double **Wp_ = nullptr, **Xip_ = nullptr, **Hp_ = nullptr, **Sp_ = nullptr, **Gp_ = nullptr;
+    double **Wp_ = nullptr, **Xip_ = nullptr, **Hp_ = nullptr, **Sp_ = nullptr, **Gp_ = nullptr, **Gpc_ = nullptr;
     double *Sg_ = nullptr, *mg_ = nullptr, *Ssum_ = nullptr;  // global snapshot, reduction buffer
     double *trace_lp_ = nullptr, *trace_pj_ = nullptr;      // per batch: M x C x Lw (x2)
     double *hist_rate_ = nullptr, *hist_beta_ = nullptr;    // per batch: M x C
