@@ -16,6 +16,7 @@
 #include <fstream>
 #include <numeric>
 #include <sstream>
+#include <thread>
 
 #include "philox.cuh"
 
@@ -193,10 +194,28 @@ Mat eigen_product(const Mat& v, const Vec& w) {  // v diag(w) v^T, proj/src/lina
     return out;
 }
 
-Mat gram(size_t d, size_t r, uint64_t seed) {  // A A^T with A ~ N(0,1) d x r, proj/src/target.cpp:18-31
+}  // namespace
+
+// d x r standard normals of the target stream, element e = i r + k at counter e
+// (proj/src/target.cpp:18-31), through the host libm as the reference
+void target_normals(size_t d, size_t r, uint64_t seed, double* out) {
     const PhiloxKey key = make_philox_key(seed, 0, "target");
+    const size_t n = d * r;
+    // counter-indexed draws: split over host threads for the large targets
+    const size_t nt = n < (size_t(1) << 20) ? 1 : std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (size_t t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+            for (size_t e = n * t / nt; e < n * (t + 1) / nt; ++e) out[e] = host_normal(key, e);
+        });
+    for (auto& th : pool) th.join();
+}
+
+namespace {
+
+Mat gram(size_t d, size_t r, uint64_t seed) {  // A A^T with A ~ N(0,1) d x r, proj/src/target.cpp:18-31
     Mat a(d, r);
-    for (size_t e = 0; e < d * r; ++e) a.a[e] = host_normal(key, e);
+    target_normals(d, r, seed, a.a.data());
     Mat b(d, d);
     for (size_t i = 0; i < d; ++i)
         for (size_t j = 0; j <= i; ++j) {
@@ -207,9 +226,13 @@ Mat gram(size_t d, size_t r, uint64_t seed) {  // A A^T with A ~ N(0,1) d x r, p
     return b;
 }
 
-void finish_gaussian(HostTarget& t) {
-    t.covariance = spd_inverse(t.precision);
-    jacobi_eigen(t.covariance, t.eigvecs, t.eigvals);
+void finish_gaussian(HostTarget& t, const TargetOps* ops) {
+    if (ops) {
+        ops->inverse_and_eigen(t.precision, t.covariance, t.eigvecs, t.eigvals);
+    } else {
+        t.covariance = spd_inverse(t.precision);
+        jacobi_eigen(t.covariance, t.eigvecs, t.eigvals);
+    }
     t.mean.assign(t.dim, 0.0);
     t.eigen_mean.assign(t.dim, 0.0);
     t.eigen_var = t.eigvals;
@@ -257,7 +280,7 @@ double HostTarget::log_density(const double* x, size_t n) const {  // proj/src/t
     return -0.5 * s;
 }
 
-HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, double twist_b) {
+HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, double twist_b, const TargetOps* ops) {
     require(dim >= 2, Err::InvalidDimension, "target dimension must be >= 2");
     HostTarget t;
     t.kind = kind;
@@ -272,19 +295,19 @@ HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, do
                 require(dim >= 10, Err::InvalidDimension, "pi3 needs d >= 10 so that r = d/10 >= 1");
                 rank = dim / 10;
             }
-            Mat b = gram(dim, rank, seed);
+            Mat b = ops ? ops->gram(dim, rank, seed) : gram(dim, rank, seed);
             if (kind == TKind::Pi2) {
                 const double s = 1.0 / static_cast<double>(dim);
                 for (double& v : b.a) v *= s;
             }
             for (size_t i = 0; i < dim; ++i) b(i, i) += 1.0;
             t.precision = std::move(b);
-            finish_gaussian(t);
+            finish_gaussian(t, ops);
             break;
         }
         case TKind::Pi4: {
             t.sigma2 = sigma2 > 0.0 ? sigma2 : 1.0 / static_cast<double>(dim);
-            HostTarget base = build_target(TKind::Pi1, dim, seed, 0.0, -1.0);
+            HostTarget base = build_target(TKind::Pi1, dim, seed, 0.0, -1.0, ops);
             const double inv_s2 = 1.0 / t.sigma2;
             Vec ce(dim), pe(dim);
             for (size_t n = 1; n <= dim; ++n) {
@@ -292,8 +315,8 @@ HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, do
                 pe[n - 1] = inv_s2 / (nd * nd * nd * nd) + 1.0;
                 ce[n - 1] = 1.0 / pe[n - 1];
             }
-            t.precision = eigen_product(base.eigvecs, pe);
-            t.covariance = eigen_product(base.eigvecs, ce);
+            t.precision = ops ? ops->eigen_product(base.eigvecs, pe) : eigen_product(base.eigvecs, pe);
+            t.covariance = ops ? ops->eigen_product(base.eigvecs, ce) : eigen_product(base.eigvecs, ce);
             t.eigvecs = std::move(base.eigvecs);
             t.eigvals = ce;
             t.mean.assign(dim, 0.0);
@@ -306,7 +329,7 @@ HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, do
         case TKind::Pi6: {
             require(dim % 20 == 0, Err::InvalidDimension, "twisted targets need d divisible by 20");
             t.twist_b = twist_b >= 0.0 ? twist_b : (kind == TKind::Pi5 ? 0.3 : 2.0);
-            HostTarget base = build_target(TKind::Pi1, dim, seed, 0.0, -1.0);
+            HostTarget base = build_target(TKind::Pi1, dim, seed, 0.0, -1.0, ops);
             t.eigvecs = std::move(base.eigvecs);
             t.eigvals = std::move(base.eigvals);
             const size_t m = dim / 10;
@@ -322,7 +345,7 @@ HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, do
             }
             t.mean.assign(dim, 0.0);
             for (size_t i = 0; i < dim; ++i) t.mean[i] = dot4(&t.eigvecs.a[i * dim], t.eigen_mean.data(), dim);
-            t.covariance = eigen_product(t.eigvecs, t.eigen_var);
+            t.covariance = ops ? ops->eigen_product(t.eigvecs, t.eigen_var) : eigen_product(t.eigvecs, t.eigen_var);
             break;
         }
     }

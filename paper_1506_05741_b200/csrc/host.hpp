@@ -133,7 +133,23 @@ struct HostTarget {
     double log_density(const double* x, size_t n) const;
 };
 
-HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, double twist_b);
+// The O(d^3) pieces of target construction. The default (null) is the host restatement
+// of the reference (bit-identical files, cyclic Jacobi: practical up to d ~ 1000);
+// gpu_target_ops() runs them on the GPU for the benchmark sizes (target_gpu.cu).
+struct TargetOps {
+    virtual ~TargetOps() = default;
+    // A A^T, A = d x r standard normals of the (seed, 0, "target") stream
+    virtual Mat gram(size_t d, size_t r, uint64_t seed) const = 0;
+    // covariance = precision^-1 and its eigenpairs (ascending, largest-|component| positive)
+    virtual void inverse_and_eigen(const Mat& precision, Mat& covariance, Mat& eigvecs, Vec& eigvals) const = 0;
+    // v diag(w) v^T
+    virtual Mat eigen_product(const Mat& v, const Vec& w) const = 0;
+};
+const TargetOps* gpu_target_ops();  // null when no GPU / no cuSOLVER
+void target_normals(size_t d, size_t r, uint64_t seed, double* out);  // the reference's A, bit-exact
+
+HostTarget build_target(TKind kind, size_t dim, uint64_t seed, double sigma2, double twist_b,
+                        const TargetOps* ops = nullptr);
 void save_target(const HostTarget& t, const std::string& path);
 HostTarget load_target(const std::string& path);
 void write_target_blob(BinOut& o, const HostTarget& t);  // embedded in DIAMCKPT files

@@ -213,3 +213,63 @@ def test_trsv_vs_oracle(lib, d):
         assert L.or_tri_solve(l.ctypes.data, d, x.ctypes.data, yr.ctypes.data) == 0
         assert np.linalg.norm(y[i, :d] - yr) / np.linalg.norm(yr) < 1e-12
         assert abs(q[i] - 0.5 * yr @ yr) / (0.5 * yr @ yr) < 1e-12
+
+
+# ------------------------------------------------------------------ target builder (large d)
+@pytest.mark.parametrize("kind", ["pi1", "pi2", "pi3", "pi4", "pi5", "pi6"])
+def test_gpu_target_builder_matches_host(b200, tmp_path, monkeypatch, kind):
+    """diam_target_build's GPU path (DMMA Gram/products + cuSOLVER eigensolver) against the
+    host restatement, which is bit-identical to the reference's builder."""
+    d, seed = 200, 3
+    h = b200.target_build(kind, d, seed)  # d < 1024: host path
+    ph = str(tmp_path / "h.bin")
+    h.save(ph)
+    monkeypatch.setenv("DIAM_B200_TARGET_BUILD", "gpu")
+    g = b200.target_build(kind, d, seed)
+    pg = str(tmp_path / "g.bin")
+    g.save(pg)
+    a, b = O.read_target(ph), O.read_target(pg)
+    assert (a.kind, a.dim, a.seed) == (b.kind, b.dim, b.seed)
+    rel = lambda x, y: np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300)
+    if a.precision.size:
+        assert rel(b.precision, a.precision) <= (1e-12 if kind in ("pi1", "pi2", "pi3") else 1e-10)
+    assert rel(b.covariance, a.covariance) <= 1e-10
+    assert np.max(np.abs(b.eigvals - a.eigvals) / a.eigvals) <= 1e-10
+    # eigenvectors: same sign convention, accuracy ~ eps / relative gap; inside a
+    # repeated eigenvalue (pi3: rank d/10 + I) only the invariant subspace is defined
+    lam = a.eigvals
+    start = 0
+    while start < d:
+        end = start + 1
+        while end < d and lam[end] - lam[end - 1] <= 1e-9 * lam[end]:
+            end += 1
+        va, vb = a.eigvecs[:, start:end], b.eigvecs[:, start:end]
+        if end - start == 1:
+            assert np.max(np.abs(vb - va)) <= 1e-8
+        else:
+            assert np.max(np.abs(vb @ vb.T - va @ va.T)) <= 1e-8
+        start = end
+    assert np.max(np.abs(b.mean - a.mean)) <= 1e-10 * max(1.0, np.max(np.abs(a.mean)))
+    assert rel(b.eigen_var, a.eigen_var) <= 1e-10
+    assert np.array_equal(b.b_coeffs == 0, a.b_coeffs == 0)
+
+
+def test_gpu_target_builder_large_d(b200, tmp_path):
+    """d >= 1024 goes to the GPU builder by default: a d=2048 pi1 target in seconds
+    (the reference's Jacobi takes hours), internally consistent."""
+    import time
+    t0 = time.perf_counter()
+    t = b200.target_build("pi1", 2048, 7)
+    secs = time.perf_counter() - t0
+    p = str(tmp_path / "t.bin")
+    t.save(p)
+    td = O.read_target(p)
+    P, Cv, V, lam = td.precision, td.covariance, td.eigvecs, td.eigvals
+    print(f"d=2048 target build {secs:.1f} s")
+    assert secs < 120
+    assert np.all(np.diff(lam) >= 0) and lam[0] > 0
+    assert np.linalg.norm(P @ Cv - np.eye(2048)) <= 1e-9 * np.sqrt(2048)
+    assert np.linalg.norm(V.T @ V - np.eye(2048)) <= 1e-10 * 2048
+    assert np.linalg.norm(Cv @ V - V * lam) <= 1e-10 * np.linalg.norm(Cv)
+    idx = np.argmax(np.abs(V), axis=0)
+    assert np.all(V[idx, np.arange(2048)] > 0)
