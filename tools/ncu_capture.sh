@@ -1,0 +1,26 @@
+#!/usr/bin/env bash
+# One `ncu --set full` capture per hot kernel of the d=1024 bench batch, on a single
+# stream (DIAM_B200_GROUPS=1: nothing overlaps, so each launch is the kernel alone).
+#   gpurun -- 'bash tools/ncu_capture.sh <tag>'   -> gpurun_out/<tag>_<kernel>.ncu-rep
+# then, locally: python tools/ncu_summary.py <tag>  -> profiles/<tag>_ncu_<kernel>.csv
+set -euo pipefail
+tag=${1:-r01}
+export DIAM_B200_GROUPS=1
+mkdir -p gpurun_out
+cmd="python tools/profile_step.py --batches 1"
+# the plain run first (ncu only after the same command exited 0 without it)
+$cmd > gpurun_out/${tag}_plain.log 2>&1
+full="ncu --set full --clock-control none --import-source on -f -c 1"
+for cls in gemm_target trmm_noise syrk_moments; do
+    # skip the warm-up batch's launches of the class (4 windows; TRMM: 3, window 0 is the identity)
+    $full --nvtx --nvtx-include "$cls/" -k regex:gemm_f64 -s 3 -o gpurun_out/${tag}_${cls} $cmd \
+        > gpurun_out/${tag}_${cls}.log 2>&1
+done
+# the POTRF's largest left-looking update (block column 512 of 1024) and a diagonal block
+$full --nvtx --nvtx-include "potrf/" -k regex:gemm_f64 -s 15 -o gpurun_out/${tag}_potrf_update $cmd \
+    > gpurun_out/${tag}_potrf_update.log 2>&1
+$full -k regex:potrf_diag -s 40 -o gpurun_out/${tag}_potrf_diag $cmd > gpurun_out/${tag}_potrf_diag.log 2>&1
+for k in mh_window normals blend_cov; do
+    $full -k regex:$k -s 4 -o gpurun_out/${tag}_${k} $cmd > gpurun_out/${tag}_${k}.log 2>&1
+done
+echo captured
