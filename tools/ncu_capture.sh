@@ -5,22 +5,29 @@
 # then, locally: python tools/ncu_summary.py <tag>  -> profiles/<tag>_ncu_<kernel>.csv
 set -euo pipefail
 tag=${1:-r01}
+only=${2:-all}   # "potrf": just the two POTRF captures
 export DIAM_B200_GROUPS=1
 mkdir -p gpurun_out
 cmd="python tools/profile_step.py --batches 1"
+full="ncu --set full --clock-control none --import-source on -f -c 1"
+if [ "$only" = all ]; then
 # the plain run first (ncu only after the same command exited 0 without it)
 $cmd > gpurun_out/${tag}_plain.log 2>&1
-full="ncu --set full --clock-control none --import-source on -f -c 1"
 for cls in gemm_target trmm_noise syrk_moments; do
     # skip the warm-up batch's launches of the class (4 windows; TRMM: 3, window 0 is the identity)
     $full --nvtx --nvtx-include "$cls/" -k regex:gemm_f64 -s 3 -o gpurun_out/${tag}_${cls} $cmd \
         > gpurun_out/${tag}_${cls}.log 2>&1
 done
-# the POTRF's largest left-looking update (block column 512 of 1024) and a diagonal block
-$full --nvtx --nvtx-include "potrf/" -k regex:gemm_f64 -s 15 -o gpurun_out/${tag}_potrf_update $cmd \
-    > gpurun_out/${tag}_potrf_update.log 2>&1
-$full -k regex:potrf_diag -s 40 -o gpurun_out/${tag}_potrf_diag $cmd > gpurun_out/${tag}_potrf_diag.log 2>&1
 for k in mh_window normals blend_cov; do
     $full -k regex:$k -s 4 -o gpurun_out/${tag}_${k} $cmd > gpurun_out/${tag}_${k}.log 2>&1
 done
+fi
+# the POTRF's largest left-looking update (block column 512 of 1024) and a diagonal block,
+# from the third batch (the first batch's adaptations are rank-deficient: jitter ladder,
+# chains that fail early skip the remaining launches)
+cmd3="python tools/profile_step.py --batches 2"
+$cmd3 > gpurun_out/${tag}_plain3.log 2>&1
+$full --nvtx --nvtx-include "potrf/" -k regex:gemm_f64 -s 325 -o gpurun_out/${tag}_potrf_update $cmd3 \
+    > gpurun_out/${tag}_potrf_update.log 2>&1
+$full -k regex:potrf_diag -s 200 -o gpurun_out/${tag}_potrf_diag $cmd3 > gpurun_out/${tag}_potrf_diag.log 2>&1
 echo captured

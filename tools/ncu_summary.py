@@ -22,7 +22,9 @@ METRICS = [
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
-    "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+    "sm__ops_path_tensor_src_fp64.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread",
@@ -43,11 +45,13 @@ def raw(rep):
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     reps = sorted(glob.glob(os.path.join(ROOT, "gpurun_out", f"{tag}_*.ncu-rep")))
-    lines = ["| kernel | launch | time (us) | DRAM read MB | DRAM write MB | SM thr % | DMMA pipe % | warps active % |",
+    lines = ["| kernel | launch | time (us) | DRAM read MB | DRAM write MB | SM thr % | FP64 tensor ops % of peak | warps active % |",
              "|---|---|---:|---:|---:|---:|---:|---:|"]
     for rep in reps:
         name = os.path.basename(rep)[len(tag) + 1:-len(".ncu-rep")]
         hdr, units, rows = raw(rep)
+        # section-prefixed names ("TPC.TriageCompute.sm__...") -> bare metric names
+        hdr = [next((m for m in METRICS if h == m or h.endswith("." + m)), h) for h in hdr]
         keep = [i for i, h in enumerate(hdr) if h in METRICS or h in ("Kernel Name", "Grid Size", "Block Size")]
         path = os.path.join(ROOT, "profiles", f"{tag}_ncu_{name}.csv")
         with open(path, "w", newline="") as f:
@@ -81,7 +85,7 @@ def main():
         kname = r[hdr.index("Kernel Name")][:60]
         lines.append(f"| {name} | `{kname}` | {get('gpu__time_duration.sum')} | {get('dram__bytes_read.sum')} | "
                      f"{get('dram__bytes_write.sum')} | {get('sm__throughput.avg.pct_of_peak_sustained_elapsed')} | "
-                     f"{get('sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active')} | "
+                     f"{get('sm__ops_path_tensor_src_fp64.avg.pct_of_peak_sustained_elapsed')} | "
                      f"{get('sm__warps_active.avg.pct_of_peak_sustained_active')} |")
         print("wrote", path)
     md = os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md")
