@@ -134,6 +134,9 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
 
     const int fr = lane >> 2;  // fragment row (A) / col (B)
     const int fk = lane & 3;   // fragment k
+    // a warp whose sub-tile lies entirely outside C (ragged edge tiles, e.g. the factor's
+    // single augmented row) only helps with the copies
+    const bool compute = (m0 + wm0 < M) && (n0 + wn0 < N);
     for (int kt = 0; kt < KT; ++kt) {
         cp_async_wait<CF::STAGES - 2>();
         __syncthreads();
@@ -142,6 +145,7 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
             if (nk < KT) issue(nk, nk % CF::STAGES);
             cp_async_commit();
         }
+        if (!compute) continue;
         const double* a_s = sA + (kt % CF::STAGES) * CF::A_STAGE;
         const double* b_s = sB + (kt % CF::STAGES) * CF::B_STAGE;
 #pragma unroll
