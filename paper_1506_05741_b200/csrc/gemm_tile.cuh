@@ -135,8 +135,9 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
     const int fr = lane >> 2;  // fragment row (A) / col (B)
     const int fk = lane & 3;   // fragment k
     // a warp whose sub-tile lies entirely outside C (ragged edge tiles, e.g. the factor's
-    // single augmented row) only helps with the copies
-    const bool compute = (m0 + wm0 < M) && (n0 + wn0 < N);
+    // single augmented row) or, for a lower-triangular C, entirely above the diagonal only
+    // helps with the copies (its DMMA issue slots go to the SM's other CTA)
+    const bool compute = (m0 + wm0 < M) && (n0 + wn0 < N) && !(tri_c_lower && m0 + wm0 + CF::WM - 1 < n0 + wn0);
     for (int kt = 0; kt < KT; ++kt) {
         cp_async_wait<CF::STAGES - 2>();
         __syncthreads();

@@ -50,14 +50,15 @@ __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const d
     // blended mean (proj/src/moments.cpp:44); every row block recomputes what it needs
     const double mbi = wg * mg[i] + wl * mlc[i];
     if (blockIdx.x == 0 && threadIdx.x == 0) mb[c * mb_stride + i] = mbi;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x) {
-        double v = 0.0;
-        if (j <= i) {
-            const double mbj = wg * mg[j] + wl * mlc[j];
-            const double s = wg * Sgr[j] + wl * Slr[j];  // :45-46
-            v = s - mbi * mbj;                         // covariance :90-101 (S exactly symmetric)
-            if (j == i && jitter_eps > 0.0) v += jitter_eps * (tr[c] / (double)d);  // proposal.cpp:229-231
-        }
+    // Lower triangle only. The strict upper part of a workspace factor is zero already
+    // (zeroed at allocation and by set_identity; the POTRF zeroes the strict upper part of
+    // every diagonal block it factors, the only upper entries its GEMMs touch), and it
+    // stays zero through factor/workspace pointer swaps.
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= i; j += gridDim.x * blockDim.x) {
+        const double mbj = wg * mg[j] + wl * mlc[j];
+        const double s = wg * Sgr[j] + wl * Slr[j];  // :45-46
+        double v = s - mbi * mbj;                    // covariance :90-101 (S exactly symmetric)
+        if (j == i && jitter_eps > 0.0) v += jitter_eps * (tr[c] / (double)d);  // proposal.cpp:229-231
         Crow[j] = v;
     }
 }
