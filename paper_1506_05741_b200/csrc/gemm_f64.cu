@@ -47,14 +47,21 @@ void launch(const GemmBatch& g, int batch, cudaStream_t stream) {
 
 template <bool AK, bool BKM>
 void dispatch_shape(const GemmBatch& g, int batch, cudaStream_t stream, GemmShape shape) {
-    // tile configuration: 1 (default) = 128x64 with two resident CTAs per SM (8 warps of
-    // 32x32) so one CTA's epilogue and pipeline fill overlap the other's DMMA main loop
-    // (measured 9% faster per batch than 0); 0 = 128x128, 1 CTA/SM, 8 warps of 64x32.
+    // tile configuration: 2 (default) = 128x64 tiles, 32-deep K stages double-buffered,
+    // two resident CTAs per SM (8 warps of 32x32) so one CTA's epilogue and pipeline fill
+    // overlap the other's DMMA main loop; 1 = the same with 16-deep stages, 3-deep ring
+    // (1.2% slower per batch: twice the barriers per flop); 0 = 128x128, 1 CTA/SM, 8 warps
+    // of 64x32 (9% slower). Measured alternatives, slower still: 128x128 with 32-deep
+    // stages (1 CTA/SM), 128x64 with a 3-deep 32-wide ring (1 CTA/SM).
     // DIAM_B200_GEMM_CFG selects for experiments.
     static const int cfg = [] {
         const char* e = std::getenv("DIAM_B200_GEMM_CFG");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 2;
     }();
+    if (cfg == 2) {
+        launch<Cfg<128, 64, 32, 2, AK, BKM, 4, 2, 2>, AK, BKM>(g, batch, stream);
+        return;
+    }
     if (cfg == 1) {
         launch<Cfg<128, 64, 16, 3, AK, BKM, 4, 2, 2>, AK, BKM>(g, batch, stream);
         return;

@@ -248,13 +248,15 @@ __device__ __forceinline__ int diag64_block(double* A, int64_t ld, int jb, doubl
         }
     // Blocked by the 4x4 register tiles: step kg finalises block column kg of L and block
     // row kg of L^{-1} with two barriers (32 in total instead of two per column):
-    //   A  thread (kg,kg) factors its diagonal 4x4 tile and inverts it (all in registers)
-    //   B  column-owners solve their tile L_ik = A_ik L_kk^-T; row-owners finish block row
-    //      kg of the inverse X_k = L_kk^-1 Y_k; both publish through shared memory
+    //   A  thread (kg,kg) factors its diagonal 4x4 tile (in registers) and publishes it
+    //      with the reciprocal pivots -- the only serial piece, so nothing else happens here
+    //   B  column-owners solve their tile L_ik = A_ik L_kk^-T and row-owners finish block
+    //      row kg of the inverse X_k = L_kk^-1 Y_k, both by 4-step forward substitution;
+    //      both publish through shared memory
     //   C  everyone applies the rank-4 updates A_ij -= L_ik L_jk^T and Y_i -= L_ik X_k
-    __shared__ double s_inv[4][4];
-    __shared__ double s_col[2][kNb][4];  // block column kg of L, rows 0..63
-    __shared__ double s_row[2][4][kNb];  // block row kg of L^{-1}
+    __shared__ double s_l[4][4], s_rd[4];  // L_kk (lower) and 1 / diag(L_kk)
+    __shared__ double s_col[2][kNb][4];    // block column kg of L, rows 0..63
+    __shared__ double s_row[2][4][kNb];    // block row kg of L^{-1}
     (void)colk;
     (void)xrow;
     (void)piv;
@@ -265,7 +267,6 @@ __device__ __forceinline__ int diag64_block(double* A, int64_t ld, int jb, doubl
             // A: 4x4 Cholesky of the diagonal tile; NotPositiveDefinite on a pivot <= 0 or
             // non-finite (proj/src/linalg.cpp:82-84) only raises `bad`, the discarded
             // arithmetic runs on
-            double rdiag[4];
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
                 double p = v[cc][cc];
@@ -273,7 +274,7 @@ __device__ __forceinline__ int diag64_block(double* A, int64_t ld, int jb, doubl
                 for (int n = 0; n < cc; ++n) p -= v[cc][n] * v[cc][n];
                 if (!(p > 0.0) || !isfinite(p)) bad = 1;
                 const double rl = rsqrt(p);  // one reciprocal square root per pivot
-                rdiag[cc] = rl;
+                s_rd[cc] = rl;
                 v[cc][cc] = p * rl;
 #pragma unroll
                 for (int rr = cc + 1; rr < 4; ++rr) {
@@ -283,67 +284,60 @@ __device__ __forceinline__ int diag64_block(double* A, int64_t ld, int jb, doubl
                     v[rr][cc] = s * rl;
                 }
             }
-            // inverse of the 4x4 lower tile by forward substitution
-            double w[4][4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    if (i < j) {
-                        w[i][j] = 0.0;
-                        continue;
-                    }
-                    double s = (i == j) ? 1.0 : 0.0;
-#pragma unroll
-                    for (int n = j; n < i; ++n) s -= v[i][n] * w[n][j];
-                    w[i][j] = s * rdiag[i];
-                }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    s_inv[i][j] = w[i][j];
                     if (j > i) v[i][j] = 0.0;
+                    s_l[i][j] = v[i][j];
                 }
         }
         __syncthreads();
         if (tx == kg) {  // B: tiles of block column kg (the diagonal tile is already final)
+            double lk[4][4], rd[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                rd[m] = s_rd[m];
+#pragma unroll
+                for (int n = 0; n < m; ++n) lk[m][n] = s_l[m][n];
+            }
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
                 const int r = 4 * ty + a;
                 if (ty > kg) {
-                    double t[4];
+                    // row a of A_ik L_kk^-T: t L_kk^T = v  (forward substitution along the row)
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
-                        double s = 0.0;
+                        double s = v[a][m];
 #pragma unroll
-                        for (int n = 0; n <= m; ++n) s += v[a][n] * s_inv[m][n];
-                        t[m] = s;
+                        for (int n = 0; n < m; ++n) s -= v[a][n] * lk[m][n];
+                        v[a][m] = s * rd[m];
                     }
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) v[a][m] = t[m];
                 }
                 if (ty >= kg)
 #pragma unroll
                     for (int m = 0; m < 4; ++m) s_col[buf][r][m] = v[a][m];
             }
         }
-        if (ty == kg) {  // B: block row kg of L^{-1}
+        if (ty == kg) {  // B: block row kg of L^{-1}: L_kk X_k = Y_k, column by column
+            double lk[4][4], rd[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                rd[m] = s_rd[m];
+#pragma unroll
+                for (int n = 0; n < m; ++n) lk[m][n] = s_l[m][n];
+            }
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                double t[4];
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
-                    double s = 0.0;
+                    double s = x[a][b];
 #pragma unroll
-                    for (int n = 0; n <= a; ++n) s += s_inv[a][n] * x[n][b];
-                    t[a] = s;
+                    for (int n = 0; n < a; ++n) s -= lk[a][n] * x[n][b];
+                    x[a][b] = s * rd[a];
                 }
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    x[a][b] = t[a];
-                    s_row[buf][a][4 * tx + b] = t[a];
-                }
+                for (int a = 0; a < 4; ++a) s_row[buf][a][4 * tx + b] = x[a][b];
             }
         }
         __syncthreads();
@@ -406,10 +400,12 @@ __device__ __forceinline__ int diag64_block(double* A, int64_t ld, int jb, doubl
     return 0;
 }
 
-// (<= 128 registers: a diagonal-block CTA can share its SM with a GEMM CTA of another group)
-__global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
-                                                         const int* mask, int* status, int* active,
-                                                         double* inv_base, int zero_above) {
+// MINB 2: <= 128 registers (spills a little) so a diagonal-block CTA can share its SM with
+// a GEMM CTA of another group; MINB 1: 190 registers, no spills
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
+                                                            const int* mask, int* status, int* active,
+                                                            double* inv_base, int zero_above) {
     const int c = blockIdx.x;
     const bool run = (!mask || mask[c]) && status[c] == 0;
     if (threadIdx.x == 0) active[c] = run ? 1 : 0;
@@ -804,7 +800,14 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     };
     // factor the 64-wide diagonal block at (c0, c0) and solve the rows below it (in place)
     auto factor_and_solve = [&](int c0, int n, int zero_above) {
-        potrf_diag_kernel<<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
+        static const int minb = [] {
+            const char* e = std::getenv("DIAM_B200_DIAG_MINB");
+            return e ? std::atoi(e) : 2;
+        }();
+        if (minb == 1)
+            potrf_diag_kernel<1><<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
+        else
+            potrf_diag_kernel<2><<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
         DGB_LAUNCH_CHECK();
         count_launch();
         const int rest = rows - c0 - n;

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--config", default="d1024", choices=sorted(bench.CONFIGS))
     ap.add_argument("--batches", type=int, default=1)
     ap.add_argument("--chains", type=int, default=0)
+    ap.add_argument("--classes", action="store_true", help="per-kernel-class CUDA-event times of one more batch")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     kind, d, per_gpu, n_lag, M = cfg
@@ -31,6 +32,13 @@ def main():
     os.unlink(path)
     n = (args.chains or per_gpu) * M * n_lag * args.batches
     print(f"{args.config}: {args.batches} batch(es) {ms:.2f} ms -> {n / ms * 1e3:.0f} chain-samples/s")
+    if args.classes:
+        eng.set_profiling(True)
+        eng.run_batches(1)
+        for c in ["gemm_target", "trmm_noise", "syrk_moments", "potrf", "mh_window", "normals", "blend_cov",
+                  "gemv_state", "trsv", "merge"]:
+            t, fl, k = eng.stat(c)
+            print(f"  {c:14s} {t:8.3f} ms {k:5d} launches" + (f" {fl / t / 1e9:6.2f} TFLOP/s" if fl and t else ""))
 
 
 if __name__ == "__main__":
