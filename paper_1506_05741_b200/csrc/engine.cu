@@ -266,7 +266,7 @@ void Engine::init_chains() {
     usable_ = dalloc<int>(A, C);
     mask_ = dalloc<int>(A, C);
     fatal_ = dalloc<int>(A, 1);
-    DGB_CUDA(cudaMallocHost(&h_flags_, 2 * (size_t)C * sizeof(int)));
+    DGB_CUDA(cudaMallocHost(&h_flags_, 3 * (size_t)C * sizeof(int)));
     Sg_ = dalloc<double>(A, mat_);
     mg_ = dalloc<double>(A, ld_);
     Ssum_ = dalloc<double>(A, mat_ + ld_);
@@ -531,14 +531,34 @@ void Engine::run_batch_windows(bool record) {
         return;
     }
     // software pipeline over groups: while the host reads group g's POTRF statuses for
-    // window m, the other group's kernels keep the GPU busy; g's next head follows at once
+    // window m, the other group's kernels keep the GPU busy; g's next head follows at once.
+    // Groups whose factorization needs the jitter ladder are set aside and stepped
+    // together, so their retries run concurrently instead of one group after another.
     next_plan(0);
     for (auto& g : groups_) enqueue_head(g, plans[0]);
+    std::vector<Ladder> lad(groups_.size());
     for (size_t m = 0; m < M; ++m) {
         if (m + 1 < M) next_plan(m + 1);
-        for (auto& g : groups_) {
-            enqueue_tail(g, plans[m]);
-            if (m + 1 < M) enqueue_head(g, plans[m + 1]);
+        std::vector<size_t> pending;
+        for (size_t i = 0; i < groups_.size(); ++i) {
+            if (!tail_begin(groups_[i], plans[m], lad[i])) {
+                pending.push_back(i);
+                continue;
+            }
+            tail_finish(groups_[i], plans[m]);
+            if (m + 1 < M) enqueue_head(groups_[i], plans[m + 1]);
+        }
+        while (!pending.empty()) {
+            std::vector<size_t> still;
+            for (size_t i : pending) {
+                if (!tail_step(groups_[i], plans[m], lad[i])) {
+                    still.push_back(i);
+                    continue;
+                }
+                tail_finish(groups_[i], plans[m]);
+                if (m + 1 < M) enqueue_head(groups_[i], plans[m + 1]);
+            }
+            pending.swap(still);
         }
     }
 }
@@ -702,46 +722,81 @@ void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {
 }
 
 void Engine::enqueue_tail(Group& g, const WindowPlan& p) {
+    Ladder st;
+    if (!tail_begin(g, p, st))
+        while (!tail_step(g, p, st)) {
+        }
+    tail_finish(g, p);
+}
+
+// Jitter escalation for chains whose factorization failed (proposal.cpp:218-239):
+// eps = 1e-10, 1e-8, 1e-6, 9.999e-5 -- the reference's floating loop -- with the same
+// blocked POTRF restricted to the failing chains. tail_begin reads the first attempt's
+// statuses; each tail_step reads one retry's and enqueues the next; true = every tried
+// chain of the group has factored.
+bool Engine::tail_begin(Group& g, const WindowPlan& p, Ladder& st) {
+    if (!p.refactor) return true;
+    const int C = g.C, o = g.off;
+    DGB_CUDA(cudaEventSynchronize(g.status_ev));
+    st.failing.assign(C, 0);
+    bool any = false;
+    for (int c = 0; c < C; ++c) {
+        st.failing[c] = h_flags_[C_ + o + c] && h_flags_[o + c];
+        any |= st.failing[c] != 0;
+    }
+    if (!any) return true;
+    st.eps = 1e-10;
+    ladder_retry(g, p, st);
+    return false;
+}
+
+bool Engine::tail_step(Group& g, const WindowPlan& p, Ladder& st) {
+    const int C = g.C, o = g.off;
+    DGB_CUDA(cudaEventSynchronize(g.status_ev));
+    bool any = false;
+    for (int c = 0; c < C; ++c) {
+        if (st.failing[c] && !h_flags_[o + c]) st.failing[c] = 0;
+        any |= st.failing[c] != 0;
+    }
+    if (!any) return true;
+    st.eps *= 100.0;
+    if (st.eps > 1e-4) {
+        int c = 0;
+        while (!st.failing[c]) ++c;
+        double trh = 0.0;
+        DGB_CUDA(cudaMemcpy(&trh, tr_ + o + c, 8, cudaMemcpyDeviceToHost));
+        fail(Err::NotPositiveDefinite, "chain " + std::to_string(c0_ + o + c) +
+                                           ": covariance not factorizable after jitter escalation (dim " +
+                                           std::to_string(d_) + ", trace " + std::to_string(trh) + ")");
+    }
+    ladder_retry(g, p, st);
+    return false;
+}
+
+void Engine::ladder_retry(Group& g, const WindowPlan& p, Ladder& st) {
+    const int C = g.C, o = g.off;
+    const cudaStream_t s = g.s;
+    const bool aug = k_.pcn_form();
+    const double* ax = aug ? x_ + o * ld_ : nullptr;
+    const double* axr = aug && k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
+    // mask through the pinned status mirror's third block (the copy is stream-ordered)
+    int* hm = h_flags_ + 2 * C_ + o;
+    std::copy(st.failing.begin(), st.failing.end(), hm);
+    DGB_CUDA(cudaMemcpyAsync(mask_ + o, hm, C * sizeof(int), cudaMemcpyHostToDevice, s));
+    launch_blend_cov(g.Lnp, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, mb_ + o * ld_, ld_, C,
+                     d_, ld_, mask_ + o, st.eps, tr_ + o, s, ax, axr);
+    DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
+    potrf_batched(g.Lnp, ld_, d_, C, mask_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+    DGB_CUDA(cudaMemcpyAsync(h_flags_ + o, status_ + o, C * sizeof(int), cudaMemcpyDeviceToHost, s));
+    DGB_CUDA(cudaEventRecord(g.status_ev, s));
+}
+
+void Engine::tail_finish(Group& g, const WindowPlan& p) {
     const int C = g.C, o = g.off;
     const cudaStream_t s = g.s;
     const double infl = k_.noise_infl();
     if (p.refactor) {
         const bool aug = k_.pcn_form();
-        const double* ax = aug ? x_ + o * ld_ : nullptr;
-        const double* axr = aug && k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
-        // jitter escalation for chains whose factorization failed (proposal.cpp:218-239):
-        // eps = 1e-10, 1e-8, 1e-6, 9.999e-5 — the reference's floating loop — with the same
-        // blocked POTRF restricted to the failing chains
-        DGB_CUDA(cudaEventSynchronize(g.status_ev));
-        std::vector<int> failing(C, 0);
-        bool any = false;
-        for (int c = 0; c < C; ++c) {
-            failing[c] = h_flags_[C_ + o + c] && h_flags_[o + c];
-            any |= failing[c] != 0;
-        }
-        for (double eps = 1e-10; any && eps <= 1e-4; eps *= 100.0) {
-            DGB_CUDA(cudaMemcpyAsync(mask_ + o, failing.data(), C * sizeof(int), cudaMemcpyHostToDevice, s));
-            launch_blend_cov(g.Lnp, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, mb_ + o * ld_,
-                             ld_, C, d_, ld_, mask_ + o, eps, tr_ + o, s, ax, axr);
-            DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
-            potrf_batched(g.Lnp, ld_, d_, C, mask_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
-            DGB_CUDA(cudaMemcpyAsync(h_flags_ + o, status_ + o, C * sizeof(int), cudaMemcpyDeviceToHost, s));
-            DGB_CUDA(cudaStreamSynchronize(s));
-            any = false;
-            for (int c = 0; c < C; ++c) {
-                if (failing[c] && !h_flags_[o + c]) failing[c] = 0;
-                any |= failing[c] != 0;
-            }
-        }
-        if (any) {
-            int c = 0;
-            while (!failing[c]) ++c;
-            double trh = 0.0;
-            DGB_CUDA(cudaMemcpy(&trh, tr_ + o + c, 8, cudaMemcpyDeviceToHost));
-            fail(Err::NotPositiveDefinite, "chain " + std::to_string(c0_ + o + c) +
-                                               ": covariance not factorizable after jitter escalation (dim " +
-                                               std::to_string(d_) + ", trace " + std::to_string(trh) + ")");
-        }
         // every tried chain has factored by now
         DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
         double qmax = -1.0;

@@ -11,7 +11,7 @@
 //   target   H = Xi * G^T                       (gemm_f64, the group's windows as one GEMM)
 //   steps    n_lag MH steps, O(d) each          (launch_mh_window, TMA-fed ring)
 //   moments  S = a X^T X + b S, mean            (gemm_f64 tri C + launch_mean_update)
-//   adapt    beta, blend -> POTRF (+ device jitter ladder, augmented usable-guard row)
+//   adapt    beta, blend -> POTRF (+ jitter ladder stepped by the host, augmented usable-guard row)
 //            -> swap, x_ref, g = G x            (potrf_batched, gemm_f64)
 //
 // The local chains are split into groups on separate streams with no host
@@ -120,7 +120,15 @@ private:
     void enqueue_steps(Group& g, const WindowPlan& p);
     void enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows);
     void enqueue_refactor(Group& g, const WindowPlan& p);
-    void enqueue_tail(Group& g, const WindowPlan& p);
+    void enqueue_tail(Group& g, const WindowPlan& p);  // tail_begin/step.../finish, blocking
+    struct Ladder {  // one group's jitter escalation in flight
+        std::vector<int> failing;
+        double eps = 0.0;
+    };
+    bool tail_begin(Group& g, const WindowPlan& p, Ladder& st);
+    bool tail_step(Group& g, const WindowPlan& p, Ladder& st);
+    void ladder_retry(Group& g, const WindowPlan& p, Ladder& st);
+    void tail_finish(Group& g, const WindowPlan& p);
     void run_batch_windows(bool record);
     void capture_chunk(const Group& g, int r0, int rows);
     void capture_window(size_t w);
@@ -173,7 +181,7 @@ private:
     double *logpi_ = nullptr, *quad_ = nullptr, *beta_ = nullptr, *tr_ = nullptr, *qtmp_ = nullptr;
     uint64_t *nacc_ = nullptr, *uctr_ = nullptr;
     int *status_ = nullptr, *try_ = nullptr, *usable_ = nullptr, *fatal_ = nullptr, *mask_ = nullptr;
-    int* h_flags_ = nullptr;  // pinned host mirror: status[C] then try[C]
+    int* h_flags_ = nullptr;  // pinned host mirror: status[C], try[C], ladder mask[C]
     PhiloxKey *nkeys_ = nullptr, *ukeys_ = nullptr, *ikeys_ = nullptr;
     double **Lp_ = nullptr, **Lnp_ = nullptr;  // factor / workspace pointer arrays (swapped on device)
     double **Wp_ = nullptr, **Xip_ = nullptr, **Hp_ = nullptr, **Sp_ = nullptr, **Gp_ = nullptr, **Gpc_ = nullptr;
