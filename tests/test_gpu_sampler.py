@@ -103,6 +103,22 @@ def test_lockstep_odd_dimension_and_multi_tile(b200, tmp_path):
     assert ties == 0
 
 
+@pytest.mark.parametrize("d,P,n_lag,M,K,kern,n0", [
+    (2, 1, 1, 3, 4, "diam", 0),     # smallest dimension, one chain, one-step windows
+    (3, 2, 5, 2, 3, "am", 3),       # burn-in inside the first window
+    (9, 5, 7, 1, 4, "pcn", 0),      # fixed-factor pCN, odd sizes
+    (17, 3, 64, 2, 2, "rw", 100),   # burn-in spanning windows, RW form
+    (256, 33, 16, 1, 2, "diam", 0),  # odd chain count split over two chain groups (streams)
+])
+def test_lockstep_edge_cases(b200, tmp_path, d, P, n_lag, M, K, kern, n0):
+    # early adaptations see fewer samples than d: rank-deficient covariances factor only
+    # with the 1e-10 * tr/d jitter, whose ~1e-5 pivots carry O(eps ||C||) rounding, i.e.
+    # ~1e-6 relative in the proposal scale -- decisions must agree, log alpha to 1e-4
+    _, _, ties = lockstep(b200, tmp_path, "pi2", d, kern, P=P, M=M, K=K, n_lag=n_lag, n0=n0, seed=d + P,
+                          lr_tol=1e-4)
+    assert ties == 0
+
+
 @pytest.mark.parametrize("chunk,pool,groups", [(37, 0, 1), (37, 1, 2), (50, 1, 4)])
 def test_lockstep_chunked_windows_shared_workspace(b200, tmp_path, monkeypatch, chunk, pool, groups):
     # the large-d memory plan: windows run in chunks of `chunk` rows (37: ragged last
