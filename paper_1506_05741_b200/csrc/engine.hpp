@@ -90,6 +90,7 @@ private:
         PotrfWork pw{};
         cudaEvent_t status_ev = nullptr;  // POTRF statuses of the group's last window landed in h_status_
         cudaEvent_t pool_ev = nullptr;    // shared refactor workspace released (pool mode)
+        cudaEvent_t steps_ev = nullptr;   // the group's first window steps of a batch are done
     };
     // host-side scalars of one lag window, identical for every chain
     struct WindowPlan {

@@ -18,6 +18,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="d1024")
+    ap.add_argument("--phases", action="store_true", help="per-stream start/end of every class")
     args = ap.parse_args()
     path = os.path.join(tempfile.gettempdir(), f"diam_timeline_{os.getpid()}.csv")
     os.environ["DIAM_B200_TIMELINE"] = path
@@ -59,6 +60,10 @@ def main():
     for n, v in sorted(per.items(), key=lambda kv: -kv[1]):
         print(f"  {n:14s} {v:8.2f} ms summed over streams")
     streams = sorted({r[1] for r in rows})
+    if args.phases:
+        for si, st in enumerate(streams):
+            rs = [r for r in rows if r[1] == st]
+            print(f"stream {si}: " + " ".join(f"{n[:4]}@{a:.1f}-{b:.1f}" for n, _, a, b in rs))
     for s in streams:
         rs = [r for r in rows if r[1] == s]
         span = rs[-1][3] - rs[0][2]
