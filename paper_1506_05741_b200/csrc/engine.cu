@@ -134,6 +134,7 @@ int Engine::plan_memory() {
         n += 2.0 * mat_ + 3.0 * ld_;              // global snapshot, reduction buffer
         n += 3.0 * M * C_ * Lw_;                  // per-batch traces
         n += 16.0 * C_ * ld_ + 4096.0 * C_;       // chain vectors, POTRF inverse blocks
+        n += (double)potrf_dag_bytes(d_, C_) / 8;  // task-graph POTRF inverse tiles
         return 8.0 * n;
     };
     auto gmax = [&](int groups) { return (C_ + groups - 1) / groups; };
@@ -188,6 +189,7 @@ Engine::~Engine() {
         if (g.done) cudaEventDestroy(g.done);
         if (g.pool_ev) cudaEventDestroy(g.pool_ev);
         if (g.steps_ev) cudaEventDestroy(g.steps_ev);
+        potrf_work_release(g.pw);
     }
     for (void* p : allocs_) cudaFreeAsync(p, 0);
     cudaStreamSynchronize(0);
@@ -359,6 +361,9 @@ void Engine::make_groups(int n) {
         // per-group inverse-block scratch (+ int active[C] tail): groups factor concurrently
         g.pw.inv = dalloc<double>(A, (size_t)g.C * 64 * 64 + g.C);
         g.pw.inv_ptrs = ptr_array(A, g.pw.inv, 64 * 64, g.C);
+        // task-graph POTRF: the groups refactor at about the same time, so each gets its
+        // share of the SMs as persistent workers
+        g.pw.workers = std::max(8, 2 * ((kNumSMs + n - 1) / n));  // two resident per SM
     }
 }
 
@@ -756,6 +761,7 @@ bool Engine::tail_begin(Group& g, const WindowPlan& p, Ladder& st) {
     if (!p.refactor) return true;
     const int C = g.C, o = g.off;
     DGB_CUDA(cudaEventSynchronize(g.status_ev));
+    require(!potrf_dag_aborted(g.pw), Err::Unknown, "task-graph POTRF aborted (dependency wait limit)");
     st.failing.assign(C, 0);
     bool any = false;
     for (int c = 0; c < C; ++c) {
@@ -771,6 +777,7 @@ bool Engine::tail_begin(Group& g, const WindowPlan& p, Ladder& st) {
 bool Engine::tail_step(Group& g, const WindowPlan& p, Ladder& st) {
     const int C = g.C, o = g.off;
     DGB_CUDA(cudaEventSynchronize(g.status_ev));
+    require(!potrf_dag_aborted(g.pw), Err::Unknown, "task-graph POTRF aborted (dependency wait limit)");
     bool any = false;
     for (int c = 0; c < C; ++c) {
         if (st.failing[c] && !h_flags_[o + c]) st.failing[c] = 0;

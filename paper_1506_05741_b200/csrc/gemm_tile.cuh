@@ -183,14 +183,16 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
             if (ok0 && ok1) {
                 double2 v = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
                 if (beta != 0.0) {
-                    const double2 o = *reinterpret_cast<const double2*>(crow + c0);
+                    // through L2: in the task-graph POTRF the tile may have been rewritten
+                    // by another SM since this one cached it
+                    const double2 o = __ldcg(reinterpret_cast<const double2*>(crow + c0));
                     v.x += beta * o.x;
                     v.y += beta * o.y;
                 }
                 *reinterpret_cast<double2*>(crow + c0) = v;
             } else if (ok0) {
                 double v = alpha * acc[i][j][0];
-                if (beta != 0.0) v += beta * crow[c0];
+                if (beta != 0.0) v += beta * __ldcg(crow + c0);
                 crow[c0] = v;
             }
         }

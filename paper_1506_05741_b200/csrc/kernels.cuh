@@ -104,12 +104,22 @@ void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr
 // Cholesky of the lower part of A_c (in place), blocked right-looking with the
 // diagonal blocks factored in shared memory, TRSM and SYRK through gemm_f64.
 // status[c] = 0 ok, 1 not positive definite. Only chains with mask[c] != 0.
+struct DagState;
 struct PotrfWork {
     double* inv;  // chains x 64 x 64 inverse diagonal blocks
     double** inv_ptrs;
+    int workers = 0;          // task-graph POTRF: persistent CTAs (0 = one per SM)
+    DagState* dag = nullptr;  // task-graph POTRF: task order, flags, inverse tiles (lazy)
 };
 void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status,
                    PotrfWork& w, cudaStream_t s, int extra_rows = 0);
+// the task-graph POTRF (potrf_dag.cu); potrf_batched routes here unless DIAM_B200_POTRF
+// selects the launch-per-phase paths
+void potrf_dag(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status, PotrfWork& w,
+               cudaStream_t s, int extra_rows);
+bool potrf_dag_aborted(const PotrfWork& w);  // valid once the POTRF's stream work completed
+size_t potrf_dag_bytes(int d, int chains);   // inverse tiles kept per factorization
+void potrf_work_release(PotrfWork& w);
 // device-side jitter ladder for chains with status 1 (see linalg.cu); fatal <- first chain+1
 // whose ladder is exhausted (status 2)
 void launch_potrf_rescue(double* const* C_out, int64_t ld, int d, int extra, const double* Sg, const double* mg,

@@ -5,6 +5,7 @@
 
 #include "gemm_f64.cuh"
 #include "gemm_tile.cuh"
+#include "diag_block.cuh"
 #include "kernels.cuh"
 
 namespace dgb {
@@ -223,182 +224,8 @@ __global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(double* const* Lm, i
 }
 
 // ------------------------------------------------------------------ Cholesky diagonal block
-constexpr int kNb = 64;
+constexpr int kNb = kDiagNb;
 
-// Register-blocked right-looking Cholesky of one 64x64 diagonal block (at A, stride ld,
-// jb <= 64 valid rows/cols), fused with the explicit inverse of the factor (for the DMMA
-// TRSM that follows), by the 256 threads of a CTA. Thread (ty, tx) of a 16x16 grid owns
-// the contiguous 4x4 sub-block rows 4ty+a, columns 4tx+b of both L and L^{-1} in
-// registers. Writes L (zero strict upper part) back to A and the inverse to `out`
-// (64x64 row-major). Returns nonzero (uniformly) on a bad pivot.
-__device__ __forceinline__ int diag64_block(double* A, int64_t ld, int jb, double* out, int zero_above) {
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    __shared__ double colk[2][kNb], xrow[2][kNb];
-    __shared__ double piv;
-    __shared__ int bad;
-    double v[4][4], x[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int r = 4 * ty + a, q = 4 * tx + b;
-            // rows/cols past jb are padded with the identity so the 64x64 factorization stays valid
-            v[a][b] = (r < jb && q <= r) ? A[(int64_t)r * ld + q] : (r == q ? 1.0 : 0.0);
-            x[a][b] = (r == q) ? 1.0 : 0.0;
-        }
-    // Blocked by the 4x4 register tiles: step kg finalises block column kg of L and block
-    // row kg of L^{-1} with two barriers (32 in total instead of two per column):
-    //   A  thread (kg,kg) factors its diagonal 4x4 tile (in registers) and publishes it
-    //      with the reciprocal pivots -- the only serial piece, so nothing else happens here
-    //   B  column-owners solve their tile L_ik = A_ik L_kk^-T and row-owners finish block
-    //      row kg of the inverse X_k = L_kk^-1 Y_k, both by 4-step forward substitution;
-    //      both publish through shared memory
-    //   C  everyone applies the rank-4 updates A_ij -= L_ik L_jk^T and Y_i -= L_ik X_k
-    __shared__ double s_l[4][4], s_rd[4];  // L_kk (lower) and 1 / diag(L_kk)
-    __shared__ double s_col[2][kNb][4];    // block column kg of L, rows 0..63
-    __shared__ double s_row[2][4][kNb];    // block row kg of L^{-1}
-    (void)colk;
-    (void)xrow;
-    (void)piv;
-    if (tid == 0) bad = 0;
-    for (int kg = 0; kg < kNb / 4; ++kg) {
-        const int buf = kg & 1;
-        if (ty == kg && tx == kg) {
-            // A: 4x4 Cholesky of the diagonal tile; NotPositiveDefinite on a pivot <= 0 or
-            // non-finite (proj/src/linalg.cpp:82-84) only raises `bad`, the discarded
-            // arithmetic runs on
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-                double p = v[cc][cc];
-#pragma unroll
-                for (int n = 0; n < cc; ++n) p -= v[cc][n] * v[cc][n];
-                if (!(p > 0.0) || !isfinite(p)) bad = 1;
-                const double rl = rsqrt(p);  // one reciprocal square root per pivot
-                s_rd[cc] = rl;
-                v[cc][cc] = p * rl;
-#pragma unroll
-                for (int rr = cc + 1; rr < 4; ++rr) {
-                    double s = v[rr][cc];
-#pragma unroll
-                    for (int n = 0; n < cc; ++n) s -= v[rr][n] * v[cc][n];
-                    v[rr][cc] = s * rl;
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (j > i) v[i][j] = 0.0;
-                    s_l[i][j] = v[i][j];
-                }
-        }
-        __syncthreads();
-        if (tx == kg) {  // B: tiles of block column kg (the diagonal tile is already final)
-            double lk[4][4], rd[4];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                rd[m] = s_rd[m];
-#pragma unroll
-                for (int n = 0; n < m; ++n) lk[m][n] = s_l[m][n];
-            }
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const int r = 4 * ty + a;
-                if (ty > kg) {
-                    // row a of A_ik L_kk^-T: t L_kk^T = v  (forward substitution along the row)
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        double s = v[a][m];
-#pragma unroll
-                        for (int n = 0; n < m; ++n) s -= v[a][n] * lk[m][n];
-                        v[a][m] = s * rd[m];
-                    }
-                }
-                if (ty >= kg)
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) s_col[buf][r][m] = v[a][m];
-            }
-        }
-        if (ty == kg) {  // B: block row kg of L^{-1}: L_kk X_k = Y_k, column by column
-            double lk[4][4], rd[4];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                rd[m] = s_rd[m];
-#pragma unroll
-                for (int n = 0; n < m; ++n) lk[m][n] = s_l[m][n];
-            }
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-#pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    double s = x[a][b];
-#pragma unroll
-                    for (int n = 0; n < a; ++n) s -= lk[a][n] * x[n][b];
-                    x[a][b] = s * rd[a];
-                }
-#pragma unroll
-                for (int a = 0; a < 4; ++a) s_row[buf][a][4 * tx + b] = x[a][b];
-            }
-        }
-        __syncthreads();
-        if (ty > kg) {  // C: rank-4 updates of the rows below block row kg
-            double lr[4][4], xk[4][4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int m = 0; m < 4; ++m) lr[a][m] = s_col[buf][4 * ty + a][m];
-#pragma unroll
-            for (int m = 0; m < 4; ++m)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) xk[m][b] = s_row[buf][m][4 * tx + b];
-            if (tx > kg && tx <= ty) {
-                double lq[4][4];
-#pragma unroll
-                for (int b = 0; b < 4; ++b)
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) lq[b][m] = s_col[buf][4 * tx + b][m];
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        double s = v[a][b];
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) s -= lr[a][m] * lq[b][m];
-                        v[a][b] = s;
-                    }
-            }
-            if (tx <= kg) {  // Y_i -= L_ik X_k (X_k is zero right of block column kg)
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        double s = x[a][b];
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) s -= lr[a][m] * xk[m][b];
-                        x[a][b] = s;
-                    }
-            }
-        }
-    }
-    __syncthreads();
-    const int failed = bad;
-    if (failed) return failed;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int r = 4 * ty + a;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int q = 4 * tx + b;
-            // the block's strict upper part holds left-looking GEMM garbage: store exact zeros
-            if (r < jb && q < jb) A[(int64_t)r * ld + q] = q <= r ? v[a][b] : 0.0;
-            out[r * kNb + q] = (r < jb && q < jb && q <= r) ? x[a][b] : 0.0;
-            // second half of a 128-wide block column: the 64 rows above this block were
-            // also touched by the block column's GEMM and lie above the diagonal
-            if (zero_above && q < jb) A[(int64_t)(r - kNb) * ld + q] = 0.0;
-        }
-    }
-    return 0;
-}
 
 // MINB 2: <= 128 registers (spills a little) so a diagonal-block CTA can share its SM with
 // a GEMM CTA of another group; MINB 1: 190 registers, no spills
@@ -760,15 +587,19 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     // w.inv holds chains*64*64 doubles, followed (by the caller's allocation) by an int active[chains]
     int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kNb * kNb);
     const int rows = d + extra_rows;
-    // Default: the launch-per-phase blocked path below. DIAM_B200_POTRF=cluster selects the
-    // persistent 2-CTA-cluster kernel: one launch per factorization, but each chain then
-    // advances at 2 SMs' pace with one SM idle during the diagonal factorizations; measured
-    // 6% slower per batch at d=1024 with 4 chain groups, 2% slower on one stream.
-    static const bool blocked = [] {
-        const char* e = std::getenv("DIAM_B200_POTRF");
-        return !(e && std::string(e) == "cluster");
-    }();
-    if (!blocked) {
+    // Default: the launch-per-phase blocked path below. DIAM_B200_POTRF (read per call):
+    //   dag     the task-graph POTRF (potrf_dag.cu): one persistent launch per factorization;
+    //           faster on one stream (7.7 vs 9.1 ms per d=1024 batch), equal with 8 chain
+    //           groups, 12% slower at d=4096 (K=128 tile updates vs the long-K updates here)
+    //   cluster the persistent 2-CTA-cluster kernel: 6% slower at d=1024 with 4 groups
+    const char* pe = std::getenv("DIAM_B200_POTRF");
+    const std::string pm = pe ? pe : "";
+    const int mode = pm == "dag" ? 0 : (pm == "cluster" ? 2 : 1);
+    if (mode == 0) {
+        potrf_dag(A, ld, d, chains, mask, status, w, s, extra_rows);
+        return;
+    }
+    if (mode == 2) {
         static bool attr = false;
         if (!attr) {
             DGB_CUDA(cudaFuncSetAttribute(potrf_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -130,6 +130,16 @@ def test_lockstep_chunked_windows_shared_workspace(b200, tmp_path, monkeypatch, 
     assert ties == 0
 
 
+@pytest.mark.parametrize("mode", ["dag", "cluster"])
+def test_lockstep_alternative_potrf(b200, tmp_path, monkeypatch, mode):
+    # the alternative factorization paths under the full engine (augmented usable-guard
+    # row, a ragged last tile: d = 133 = 128 + 5, two chain groups)
+    monkeypatch.setenv("DIAM_B200_POTRF", mode)
+    monkeypatch.setenv("DIAM_B200_GROUPS", "2")
+    _, _, ties = lockstep(b200, tmp_path, "pi2", 133, "diam", P=4, M=2, K=2, n_lag=150, n0=0, seed=9)
+    assert ties == 0
+
+
 def test_chunked_run_matches_resident_run(b200, monkeypatch):
     """Chunked windows + shared workspace change only the moment update's rounding:
     decisions, histories and traces (log density, eigen projections) match the

@@ -41,7 +41,9 @@ namespace {
 // experimental copy of diag64_block: F bit 0 skips phase A, 1 phase B, 2 phase C,
 // 3 the barrier after A, 4 the barrier after B (timing only: results are wrong)
 template <int F>
-__device__ __forceinline__ int diag_exp(double* A, int64_t ld, int jb, double* out, int zero_above) {
+__device__ __forceinline__ int diag_exp(double* A, int64_t ld, int jb, double* out, int zero_above,
+                                        long long* cyc = nullptr) {
+    long long tA = 0, tStep = 0, tPrev = 0, tB = 0;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     __shared__ double colk[2][kNb], xrow[2][kNb];
     __shared__ double piv;
@@ -73,6 +75,7 @@ __device__ __forceinline__ int diag_exp(double* A, int64_t ld, int jb, double* o
     if (tid == 0) bad = 0;
     for (int kg = 0; kg < kNb / 4; ++kg) {
         const int buf = kg & 1;
+        long long a0 = clock64();
         if ((F & 1) == 0 && ty == kg && tx == kg) {
             // A: 4x4 Cholesky of the diagonal tile; NotPositiveDefinite on a pivot <= 0 or
             // non-finite (proj/src/linalg.cpp:82-84) only raises `bad`, the discarded
@@ -102,8 +105,14 @@ __device__ __forceinline__ int diag_exp(double* A, int64_t ld, int jb, double* o
                     s_l[i][j] = v[i][j];
                 }
         }
+        if (ty == kg && tx == kg) tA += clock64() - a0;
         if ((F & 8) == 0) __syncthreads();
-        if ((F & 2) == 0 && tx == kg) {  // B: tiles of block column kg (the diagonal tile is already final)
+        long long b0 = clock64();
+        if (tid == 0) {
+            if (kg > 0) tStep += b0 - tPrev;
+            tPrev = b0;
+        }
+        if ((F & 2) == 0 && (F & 64) == 0 && tx == kg) {  // B: tiles of block column kg (the diagonal tile is already final)
             double lk[4][4], rd[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
@@ -129,7 +138,7 @@ __device__ __forceinline__ int diag_exp(double* A, int64_t ld, int jb, double* o
                     for (int m = 0; m < 4; ++m) s_col[buf][r][m] = v[a][m];
             }
         }
-        if ((F & 2) == 0 && ty == kg) {  // B: block row kg of L^{-1}: L_kk X_k = Y_k, column by column
+        if ((F & 2) == 0 && (F & 32) == 0 && ty == kg) {  // B: block row kg of L^{-1}: L_kk X_k = Y_k, column by column
             double lk[4][4], rd[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
@@ -151,6 +160,7 @@ __device__ __forceinline__ int diag_exp(double* A, int64_t ld, int jb, double* o
             }
         }
         if ((F & 16) == 0) __syncthreads();
+        if (tid == 0) tB += clock64() - b0;
         if ((F & 4) == 0 && ty > kg) {  // C: rank-4 updates of the rows below block row kg
             double lr[4][4], xk[4][4];
 #pragma unroll
@@ -191,6 +201,10 @@ __device__ __forceinline__ int diag_exp(double* A, int64_t ld, int jb, double* o
         }
     }
     __syncthreads();
+    if (cyc && blockIdx.x == 0) {
+        if (tid == 0) { cyc[0] = tStep; cyc[1] = tB; }
+        if (tx == ty) atomicAdd((unsigned long long*)&cyc[2], (unsigned long long)tA);
+    }
     const int failed = bad;
     if (failed) return failed;
 #pragma unroll
@@ -211,9 +225,10 @@ __device__ __forceinline__ int diag_exp(double* A, int64_t ld, int jb, double* o
 }
 
 template <int F>
-__global__ void __launch_bounds__(256, 2) diag_exp_kernel(double* const* Am, int64_t ld, int jb, int* status, double* inv) {
+__global__ void __launch_bounds__(256, 2) diag_exp_kernel(double* const* Am, int64_t ld, int jb, int* status, double* inv,
+                                                         long long* cyc = nullptr) {
     const int c = blockIdx.x;
-    if (diag_exp<F>(Am[c], ld, jb, inv + (int64_t)c * 64 * 64, 0) && threadIdx.x == 0) status[c] = 1;
+    if (diag_exp<F>(Am[c], ld, jb, inv + (int64_t)c * 64 * 64, 0, cyc) && threadIdx.x == 0) status[c] = 1;
 }
 }  // namespace
 }  // namespace dgb
@@ -284,6 +299,33 @@ int main() {
     timeit([&] { potrf_diag_kernel<2><<<chains, 256>>>(Ap, ld, 0, 32, nullptr, status, active, inv, 0); },
            "diag64 jb=32 (minb 2)");
     timeit([&] { diag_exp_kernel<0><<<chains, 256>>>(Ap, ld, 64, status, inv); }, "exp full");
+    auto cyc = [&](auto launch, const char* name) {
+        long long* cy;
+        cudaMalloc(&cy, 4 * 8);
+        cudaMemset(cy, 0, 32);
+        cudaMemcpy(A, A0, h.size() * 8, cudaMemcpyDeviceToDevice);
+        cudaMemset(status, 0, chains * 4);
+        launch(cy);
+        long long hc[4];
+        cudaMemcpy(hc, cy, 32, cudaMemcpyDeviceToHost);
+        printf("%-20s cycles per step %.0f, B %.0f, A %.0f\n", name, hc[0] / 15.0, hc[1] / 16.0, hc[2] / 16.0);
+        cudaFree(cy);
+    };
+    cyc([&](long long* cy) { diag_exp_kernel<32><<<chains, 256>>>(Ap, ld, 64, status, inv, cy); }, "no row-owner B");
+    cyc([&](long long* cy) { diag_exp_kernel<64><<<chains, 256>>>(Ap, ld, 64, status, inv, cy); }, "no col-owner B");
+    cyc([&](long long* cy) { diag_exp_kernel<96><<<chains, 256>>>(Ap, ld, 64, status, inv, cy); }, "no B at all");
+    {
+        long long* cy;
+        cudaMalloc(&cy, 4 * 8);
+        cudaMemset(cy, 0, 32);
+        cudaMemcpy(A, A0, h.size() * 8, cudaMemcpyDeviceToDevice);
+        cudaMemset(status, 0, chains * 4);
+        diag_exp_kernel<0><<<chains, 256>>>(Ap, ld, 64, status, inv, cy);
+        long long hc[4];
+        cudaMemcpy(hc, cy, 32, cudaMemcpyDeviceToHost);
+        printf("cycles: 15 steps %lld (%.0f per step), phase B (barrier to barrier) %lld (%.0f per step), phase A total %lld (%.0f per step)\n",
+               hc[0], hc[0] / 15.0, hc[1], hc[1] / 16.0, hc[2], hc[2] / 16.0);
+    }
     timeit([&] { diag_exp_kernel<1><<<chains, 256>>>(Ap, ld, 64, status, inv); }, "exp no A");
     timeit([&] { diag_exp_kernel<2><<<chains, 256>>>(Ap, ld, 64, status, inv); }, "exp no B");
     timeit([&] { diag_exp_kernel<4><<<chains, 256>>>(Ap, ld, 64, status, inv); }, "exp no C");
