@@ -94,6 +94,7 @@ Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> com
     require(d_ <= 8192, Err::InvalidDimension, "the B200 engine supports d <= 8192");
     DGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     DGB_CUDA(cudaEventCreateWithFlags(&main_ev_, cudaEventDisableTiming));
+    if (const char* e = std::getenv("DIAM_B200_PRENOISE")) prenoise_ = std::atoi(e) != 0;
     upload_target();
     const int ng = plan_memory();
     init_chains();
@@ -189,6 +190,12 @@ Engine::~Engine() {
         if (g.done) cudaEventDestroy(g.done);
         if (g.pool_ev) cudaEventDestroy(g.pool_ev);
         if (g.steps_ev) cudaEventDestroy(g.steps_ev);
+        if (g.s2) {
+            cudaStreamSynchronize(g.s2);
+            cudaStreamDestroy(g.s2);
+        }
+        if (g.ev_free) cudaEventDestroy(g.ev_free);
+        if (g.ev_noise) cudaEventDestroy(g.ev_noise);
         potrf_work_release(g.pw);
     }
     for (void* p : allocs_) cudaFreeAsync(p, 0);
@@ -345,6 +352,9 @@ void Engine::make_groups(int n) {
         DGB_CUDA(cudaEventCreateWithFlags(&g.status_ev, cudaEventDisableTiming));
         DGB_CUDA(cudaEventCreateWithFlags(&g.pool_ev, cudaEventDisableTiming));
         DGB_CUDA(cudaEventCreateWithFlags(&g.steps_ev, cudaEventDisableTiming));
+        DGB_CUDA(cudaStreamCreateWithFlags(&g.s2, cudaStreamNonBlocking));
+        DGB_CUDA(cudaEventCreateWithFlags(&g.ev_free, cudaEventDisableTiming));
+        DGB_CUDA(cudaEventCreateWithFlags(&g.ev_noise, cudaEventDisableTiming));
         g.Lp = Lp_ + g.off;
         // pool mode: every group factors into the same workspace (slot i <-> the group's
         // chain i); accepted factors swap pointers with their slot as before
@@ -545,7 +555,13 @@ void Engine::run_batch_windows(bool record) {
     // half has finished its first window's steps, so one half's refactorization overlaps
     // the other half's GEMMs (measured 0.8% slower at d=1024 and 1.6% at d=4096: the
     // start and end offsets cost more than the overlap gains; off by default).
-    next_plan(0);
+    // All plans up front (host counters only): window m+1's first noise chunk is drawn on
+    // the group's side stream while window m refactors -- the noise depends on neither the
+    // new factor nor beta's next value unless the factor is still the identity.
+    for (size_t m = 0; m < M; ++m) {
+        next_plan(m);
+        plans[m].pre_noise = m > 0 && prenoise_;
+    }
     const size_t G = groups_.size();
     static const bool stagger = [] {
         const char* e = std::getenv("DIAM_B200_STAGGER");
@@ -557,11 +573,16 @@ void Engine::run_batch_windows(bool record) {
         if (half && i >= half) DGB_CUDA(cudaStreamWaitEvent(g.s, groups_[i - half].steps_ev, 0));
         enqueue_steps(g, plans[0]);
         if (half && i < half) DGB_CUDA(cudaEventRecord(g.steps_ev, g.s));
+        if (M > 1 && plans[1].pre_noise) enqueue_prenoise(g, plans[1]);
         enqueue_refactor(g, plans[0]);
     }
+    auto head = [&](Group& g, size_t m) {  // window m's steps, m+1's early noise, m's refactor
+        enqueue_steps(g, plans[m]);
+        if (m + 1 < M && plans[m + 1].pre_noise) enqueue_prenoise(g, plans[m + 1]);
+        enqueue_refactor(g, plans[m]);
+    };
     std::vector<Ladder> lad(groups_.size());
     for (size_t m = 0; m < M; ++m) {
-        if (m + 1 < M) next_plan(m + 1);
         std::vector<size_t> pending;
         for (size_t i = 0; i < groups_.size(); ++i) {
             if (!tail_begin(groups_[i], plans[m], lad[i])) {
@@ -569,7 +590,7 @@ void Engine::run_batch_windows(bool record) {
                 continue;
             }
             tail_finish(groups_[i], plans[m]);
-            if (m + 1 < M) enqueue_head(groups_[i], plans[m + 1]);
+            if (m + 1 < M) head(groups_[i], m + 1);
         }
         while (!pending.empty()) {
             std::vector<size_t> still;
@@ -579,7 +600,7 @@ void Engine::run_batch_windows(bool record) {
                     continue;
                 }
                 tail_finish(groups_[i], plans[m]);
-                if (m + 1 < M) enqueue_head(groups_[i], plans[m + 1]);
+                if (m + 1 < M) head(groups_[i], m + 1);
             }
             pending.swap(still);
         }
@@ -595,6 +616,19 @@ void Engine::enqueue_steps(Group& g, const WindowPlan& p) {
                        g.s);
 }
 
+// The next window's first chunk of noise on the side stream, once this window's last
+// readers of W / Xi (and the beta update) are done.
+void Engine::enqueue_prenoise(Group& g, const WindowPlan& next) {
+    const int o = g.off;
+    DGB_CUDA(cudaEventRecord(g.ev_free, g.s));
+    DGB_CUDA(cudaStreamWaitEvent(g.s2, g.ev_free, 0));
+    timed_begin(g.s2);
+    launch_normals(W_ + o * win_, next.identity ? Xi_ + o * win_ : nullptr, win_, g.C, std::min(Lc_, Lw_), d_, ld_,
+                   nkeys_ + o, next.nctr, beta_ + o, k_.noise_infl(), g.s2);
+    timed_end("normals", 0.0, g.s2);
+    DGB_CUDA(cudaEventRecord(g.ev_noise, g.s2));
+}
+
 // Rows [r0, r0 + rows) of the window: noise, target GEMM, the MH steps, and the moments
 // of the chunk's post-burn-in states. The step recursion's state (x, G x, y, log pi,
 // counters) lives in global memory, so consecutive chunks continue one another exactly;
@@ -605,10 +639,14 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     const double infl = k_.noise_infl();
     // ---- noise: W from Philox, Xi = s W L^T, H = Xi G^T (proposal.cpp:254-266); row r of
     // the window draws counters nctr + r d .. nctr + (r + 1) d - 1 of the chain's stream
-    timed_begin(s);
-    launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, rows, d_, ld_, nkeys_ + o,
-                   p.nctr + (uint64_t)r0 * d_, beta_ + o, infl, s);
-    timed_end("normals", 0.0, s);
+    if (r0 == 0 && p.pre_noise) {
+        DGB_CUDA(cudaStreamWaitEvent(s, g.ev_noise, 0));
+    } else {
+        timed_begin(s);
+        launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, rows, d_, ld_, nkeys_ + o,
+                       p.nctr + (uint64_t)r0 * d_, beta_ + o, infl, s);
+        timed_end("normals", 0.0, s);
+    }
     if (!p.identity) {
         GemmBatch t{};
         t.A = (const double* const*)g.Wp;

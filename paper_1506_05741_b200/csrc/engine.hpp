@@ -91,6 +91,8 @@ private:
         cudaEvent_t status_ev = nullptr;  // POTRF statuses of the group's last window landed in h_status_
         cudaEvent_t pool_ev = nullptr;    // shared refactor workspace released (pool mode)
         cudaEvent_t steps_ev = nullptr;   // the group's first window steps of a batch are done
+        cudaStream_t s2 = nullptr;        // side stream: the next window's noise during the refactor
+        cudaEvent_t ev_free = nullptr, ev_noise = nullptr;
     };
     // host-side scalars of one lag window, identical for every chain
     struct WindowPlan {
@@ -100,6 +102,7 @@ private:
         uint64_t cnt_before = 0, cnt_after = 0;
         bool record = false, refactor = false, move_ref = false;
         bool identity = false;  // every factor is still the initial identity (noise = s W)
+        bool pre_noise = false;  // the first chunk's normals were drawn early on the side stream
         double wg = 0.0, wl = 1.0;
     };
 
@@ -120,6 +123,7 @@ private:
     }
     void enqueue_steps(Group& g, const WindowPlan& p);
     void enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows);
+    void enqueue_prenoise(Group& g, const WindowPlan& next);
     void enqueue_refactor(Group& g, const WindowPlan& p);
     void enqueue_tail(Group& g, const WindowPlan& p);  // tail_begin/step.../finish, blocking
     struct Ladder {  // one group's jitter escalation in flight
@@ -161,6 +165,10 @@ private:
     bool pool_ = false;
     int pool_n_ = 0;
     cudaEvent_t pool_last_ = nullptr;  // latest release of the shared workspace
+    // early next-window noise on a side stream during the refactor (DIAM_B200_PRENOISE=1);
+    // measured 2.7% slower at d=1024 with 8 groups (the other groups' GEMMs lose SMs to
+    // it), neutral at d=4096: off by default
+    bool prenoise_ = false;
     int64_t ld_ = 0, win_ = 0, mat_ = 0;
     int64_t fmat_ = 0;  // factor stride: d rows + the augmented row r = x - x_ref
     bool twisted_ = false, identity_ = true;
