@@ -123,6 +123,34 @@ def run_options(cfg, chains, **over):
     return o
 
 
+def ncu_gemm_traffic(cfg_name, chains, d, n_lag):
+    """DRAM bytes per launch of the three DMMA GEMM classes from the committed `ncu --set
+    full` captures (profiles/r01_ncu_<class>.csv, tools/ncu_capture.sh: d=1024, 64 chains),
+    against their algorithmic bytes (operands in once, results out once)."""
+    import csv
+    if cfg_name != "d1024" or chains != 64:
+        return None
+    out, alg = {}, {}
+    w = chains * n_lag * d * 8       # one window matrix (W, Xi, H or X) of all chains
+    tri = chains * d * (d + 1) // 2 * 8  # the lower triangles of all chains' L or S
+    alg_bytes = {"gemm_target": 2 * w + d * d * 8, "trmm_noise": 2 * w + tri, "syrk_moments": w + 2 * tri}
+    for cls in ("gemm_target", "trmm_noise", "syrk_moments"):
+        path = os.path.join(ROOT, "profiles", f"r01_ncu_{cls}.csv")
+        if not os.path.exists(path):
+            return None
+        rows = list(csv.reader(open(path)))
+        h, u, v = rows[0], rows[1], rows[2]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(m)
+            tot += float(v[i].replace(",", "")) * scale.get(u[i], 1)
+        out[cls] = tot
+        alg[cls] = alg_bytes[cls]
+    return {"dram_bytes_per_launch": out, "algorithmic_bytes_per_launch": alg,
+            "source": "profiles/r01_ncu_*.csv (one steady-state launch each, single stream)"}
+
+
 def time_to_cov_error(lib, with_reference: bool):
     """BASELINE.json's second metric: wall time until the pooled covariance error first
     reaches a tolerance. d=100 pi2 (config 1's target), 8 chains, M=2, n0=0, cov_tol 0.3 —
@@ -340,7 +368,8 @@ def impl_b200(args):
                        "l2": "no flush needed: per-step working set "
                              f"{(3 * d * d + 3 * n_lag * d) * 8 * per_gpu / 1e9:.1f} GB >> 126 MB L2"},
             "roofline": {"bound": "fp64-dmma", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                         "frac": achieved / peak.value if peak.value else None, "traffic": None,
+                         "frac": achieved / peak.value if peak.value else None,
+                         "traffic": ncu_gemm_traffic(args.config, per_gpu, d, n_lag),
                          "kernel": "gemm_f64 (TRMM noise + target GEMM + SYRK moments)",
                          "share_of_step": g_ms / prof_total if prof_total else None,
                          "peak_source": "diamx_fp64_peak: DMMA m8n8k4 loop measured live (MEASURED_PEAKS.json "

@@ -10,6 +10,23 @@
 
 __global__ void empty_kernel() {}
 
+// barrier round trips: 256 threads, 64 iterations of (smem write by one thread, barrier,
+// everyone reads it, barrier)
+__global__ void barrier_kernel(long long* cyc, double* out) {
+    __shared__ double v;
+    double acc = 0.0;
+    long long t0 = clock64();
+    for (int i = 0; i < 64; ++i) {
+        if (threadIdx.x == (i & 255)) v = acc + i;
+        __syncthreads();
+        acc += v;
+        __syncthreads();
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0 && blockIdx.x == 0) cyc[3] = (t1 - t0) / 64;
+    if (acc == -1.0) out[0] = acc;
+}
+
 // dependent-chain latencies (cycles per op), one thread
 __global__ void lat_kernel(double* out, long long* cyc, double a, double b) {
     double x = a;
@@ -288,6 +305,10 @@ int main() {
         lat_kernel<<<1, 1>>>(o, cy, 0.5, 0.999);
         long long hc[4];
         cudaMemcpy(hc, cy, 32, cudaMemcpyDeviceToHost);
+        barrier_kernel<<<64, 256>>>(cy, o);
+        long long hb[4];
+        cudaMemcpy(hb, cy, 32, cudaMemcpyDeviceToHost);
+        printf("two barriers + smem broadcast per iteration: %lld cycles\n", hb[3]);
         printf("latency (cycles, incl. loop): dfma %lld, rsqrt(double)+add %lld, div(double)+add %lld, ffma %lld\n",
                hc[0], hc[1], hc[2], hc[3]);
     }
