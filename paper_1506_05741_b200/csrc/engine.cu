@@ -563,16 +563,20 @@ void Engine::run_batch_windows(bool record) {
         plans[m].pre_noise = m > 0 && prenoise_;
     }
     const size_t G = groups_.size();
-    static const bool stagger = [] {
+    // (1: the offset is the first half's whole first-window steps; 2: only up to its
+    // first target GEMM)
+    static const int stagger = [] {
         const char* e = std::getenv("DIAM_B200_STAGGER");
-        return e && std::atoi(e) != 0;
+        return e ? std::atoi(e) : 0;
     }();
     const size_t half = (stagger && G >= 4 && plans[0].refactor) ? G / 2 : 0;
     for (size_t i = 0; i < G; ++i) {
         Group& g = groups_[i];
         if (half && i >= half) DGB_CUDA(cudaStreamWaitEvent(g.s, groups_[i - half].steps_ev, 0));
+        g.mark_target = half && i < half && stagger == 2;
         enqueue_steps(g, plans[0]);
-        if (half && i < half) DGB_CUDA(cudaEventRecord(g.steps_ev, g.s));
+        g.mark_target = false;
+        if (half && i < half && stagger != 2) DGB_CUDA(cudaEventRecord(g.steps_ev, g.s));
         if (M > 1 && plans[1].pre_noise) enqueue_prenoise(g, plans[1]);
         enqueue_refactor(g, plans[0]);
     }
@@ -680,6 +684,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
             h.C = g.Hb;
             h.M = C * Lc_;  // the group's window chunks are one contiguous (C Lc) x ld matrix
             gemm("gemm_target", h, 1, true, true, s);
+            if (g.mark_target && r0 == 0) DGB_CUDA(cudaEventRecord(g.steps_ev, s));
         } else {            // ragged last chunk: per-chain pieces
             h.B = (const double* const*)Gpc_;
             h.A = (const double* const*)g.Xip;

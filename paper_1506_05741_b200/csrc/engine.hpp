@@ -91,6 +91,7 @@ private:
         cudaEvent_t status_ev = nullptr;  // POTRF statuses of the group's last window landed in h_status_
         cudaEvent_t pool_ev = nullptr;    // shared refactor workspace released (pool mode)
         cudaEvent_t steps_ev = nullptr;   // the group's first window steps of a batch are done
+        bool mark_target = false;         // record steps_ev after the next target GEMM instead
         cudaStream_t s2 = nullptr;        // side stream: the next window's noise during the refactor
         cudaEvent_t ev_free = nullptr, ev_noise = nullptr;
     };
