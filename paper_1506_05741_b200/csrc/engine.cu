@@ -41,6 +41,11 @@ void keep_pool_resident() {
     done = true;
 }
 
+// While an engine is being built, allocations are zeroed on stream 0 without a sync
+// each; the constructor synchronizes once before the engine's (non-blocking) streams
+// touch them. Later allocations synchronize at once.
+thread_local bool g_defer_alloc_sync = false;
+
 template <class T>
 T* dalloc(std::vector<void*>& list, size_t count) {
     void* p = nullptr;
@@ -48,8 +53,7 @@ T* dalloc(std::vector<void*>& list, size_t count) {
     keep_pool_resident();
     DGB_CUDA(cudaMallocAsync(&p, count * sizeof(T), 0));
     DGB_CUDA(cudaMemsetAsync(p, 0, count * sizeof(T), 0));
-    // the engine's streams are non-blocking: make the zeroed buffer visible to them now
-    DGB_CUDA(cudaStreamSynchronize(0));
+    if (!g_defer_alloc_sync) DGB_CUDA(cudaStreamSynchronize(0));
     list.push_back(p);
     return static_cast<T*>(p);
 }
@@ -58,10 +62,16 @@ double** ptr_array(std::vector<void*>& list, double* base, int64_t stride, int n
     std::vector<double*> h(n);
     for (int i = 0; i < n; ++i) h[i] = base + stride * i;
     double** d = dalloc<double*>(list, n);
+    // from pageable memory: returns once h is staged, so h may go out of scope
     DGB_CUDA(cudaMemcpyAsync(d, h.data(), n * sizeof(double*), cudaMemcpyHostToDevice, 0));
-    DGB_CUDA(cudaStreamSynchronize(0));  // h is a stack buffer
+    if (!g_defer_alloc_sync) DGB_CUDA(cudaStreamSynchronize(0));
     return d;
 }
+
+struct DeferAllocSync {
+    DeferAllocSync() { g_defer_alloc_sync = true; }
+    ~DeferAllocSync() { g_defer_alloc_sync = false; }
+};
 
 // host matrix (rows x cols, row-major) -> device rows x ld
 void upload_padded(double* dst, int64_t ld, const Mat& m) {
@@ -71,8 +81,8 @@ void upload_padded(double* dst, int64_t ld, const Mat& m) {
 
 }  // namespace
 
-Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> comm)
-    : tgt_(t), cfg_(cfg), k_(cfg.kernel), comm_(std::move(comm)) {
+Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shared_ptr<Comm> comm)
+    : tgtp_(std::move(t)), tgt_(*tgtp_), cfg_(cfg), k_(cfg.kernel), comm_(std::move(comm)) {
     validate_run_cfg(cfg_, tgt_);
     if (comm_) {
         rank_ = comm_->rank();
@@ -95,10 +105,12 @@ Engine::Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> com
     DGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     DGB_CUDA(cudaEventCreateWithFlags(&main_ev_, cudaEventDisableTiming));
     if (const char* e = std::getenv("DIAM_B200_PRENOISE")) prenoise_ = std::atoi(e) != 0;
+    DeferAllocSync defer;
     upload_target();
     const int ng = plan_memory();
     init_chains();
     make_groups(ng);
+    DGB_CUDA(cudaStreamSynchronize(0));
 }
 
 int Engine::plan_memory() {
@@ -311,6 +323,9 @@ void Engine::init_chains() {
     DGB_CUDA(cudaMemcpy(ukeys_, uk.data(), C * sizeof(PhiloxKey), cudaMemcpyHostToDevice));
     DGB_CUDA(cudaMemcpy(ikeys_, ik.data(), C * sizeof(PhiloxKey), cudaMemcpyHostToDevice));
 
+    double** xp = ptr_array(A, x_, 0, 1);
+    double** gp = ptr_array(A, g_, 0, 1);
+    DGB_CUDA(cudaStreamSynchronize(0));  // the buffers above are zeroed before stream_ uses them
     // x0 = dispersion * N(0, I) from the "init" stream (runner.cpp:131-132)
     launch_normal_vec(x_, ld_, C, d_, ikeys_, 0, cfg_.init_dispersion, stream_);
     // factor = I, beta = beta_init (proposal.cpp:95-97)
@@ -319,8 +334,6 @@ void Engine::init_chains() {
     DGB_CUDA(cudaMemcpyAsync(beta_, b.data(), C * 8, cudaMemcpyHostToDevice, stream_));
     identity_ = true;
     // log pi(x0), quad(x0) (proposal.cpp:107-108)
-    double** xp = ptr_array(A, x_, 0, 1);
-    double** gp = ptr_array(A, g_, 0, 1);
     refresh_g(xp, gp, C, stream_);
     launch_eval_logpi(x_, g_, inv_eig_, bcoef_, twisted_, logpi_, C, d_, ld_, stream_);
     if (k_.pcn_form()) {

@@ -43,7 +43,12 @@ struct KernelStat {
 
 class Engine {
 public:
-    Engine(const HostTarget& t, const RunCfg& cfg, std::shared_ptr<Comm> comm);
+    // The target is shared, not copied (3 d x d matrices): a blocking call passes a
+    // non-owning pointer (borrow()), an engine handle that outlives the call an owning one.
+    Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shared_ptr<Comm> comm);
+    static std::shared_ptr<const HostTarget> borrow(const HostTarget& t) {
+        return std::shared_ptr<const HostTarget>(&t, [](const HostTarget*) {});
+    }
     ~Engine();
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -153,7 +158,8 @@ private:
     void resolve_events();
     RunResult build_result(const std::string& reason, double wall);
 
-    HostTarget tgt_;
+    std::shared_ptr<const HostTarget> tgtp_;
+    const HostTarget& tgt_;
     RunCfg cfg_;
     KernelCfg k_;
     std::shared_ptr<Comm> comm_;
