@@ -21,21 +21,21 @@ namespace dgb {
 
 namespace {
 
-__global__ void normals_kernel(double* W, double* Xi, int64_t chain_stride, int chains, int rows,
-                               int d, int64_t ld, const PhiloxKey* keys, uint64_t start,
-                               const double* beta, double infl) {
-    const int64_t per_chain = (int64_t)rows * d;
-    const int64_t total = per_chain * chains;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(e / per_chain);
-        const int64_t rem = e - c * per_chain;
-        const int r = (int)(rem / d);
-        const int i = (int)(rem - (int64_t)r * d);
-        const double z = philox_normal(keys[c], start + (uint64_t)rem);
-        const int64_t off = c * chain_stride + r * ld + i;
-        W[off] = z;
-        if (Xi) Xi[off] = (beta[c] * infl) * z;
+// grid: x over rows, y over chains; threads over the row's d entries (no index division)
+__global__ void normals_kernel(double* W, double* Xi, int64_t chain_stride, int rows, int d, int64_t ld,
+                               const PhiloxKey* keys, uint64_t start, const double* beta, double infl) {
+    const int c = blockIdx.y;
+    const PhiloxKey key = keys[c];
+    const double scale = Xi ? beta[c] * infl : 0.0;
+    double* Wc = W + c * chain_stride;
+    double* Xc = Xi ? Xi + c * chain_stride : nullptr;
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+        const uint64_t base = start + (uint64_t)r * d;
+        for (int i = threadIdx.x; i < d; i += blockDim.x) {
+            const double z = philox_normal(key, base + (uint64_t)i);
+            Wc[(int64_t)r * ld + i] = z;
+            if (Xc) Xc[(int64_t)r * ld + i] = scale * z;
+        }
     }
 }
 
@@ -487,12 +487,12 @@ void launch_r(const StepParams& p, cudaStream_t s) {
 void launch_normals(double* W, double* Xi, int64_t chain_stride, int chains, int rows, int d, int64_t ld,
                     const PhiloxKey* keys, uint64_t start, const double* beta, double infl,
                     cudaStream_t s) {
-    const int64_t total = (int64_t)chains * rows * d;
-    if (total == 0) return;
+    if ((int64_t)chains * rows * d == 0) return;
     const int threads = 256;
-    const int64_t blocks = std::min<int64_t>(ceil_div(total, threads), (int64_t)kNumSMs * 16);
-    normals_kernel<<<(unsigned)blocks, threads, 0, s>>>(W, Xi, chain_stride, chains, rows, d, ld, keys, start,
-                                                        beta, infl);
+    // about 16 resident 256-thread blocks per SM over all chains
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(rows, ceil_div((int64_t)kNumSMs * 16, chains)));
+    normals_kernel<<<dim3((unsigned)gx, (unsigned)chains), threads, 0, s>>>(W, Xi, chain_stride, rows, d, ld, keys,
+                                                                          start, beta, infl);
     DGB_LAUNCH_CHECK();
     count_launch();
 }
