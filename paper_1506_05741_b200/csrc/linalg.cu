@@ -55,12 +55,22 @@ __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const d
     // (zeroed at allocation and by set_identity; the POTRF zeroes the strict upper part of
     // every diagonal block it factors, the only upper entries its GEMMs touch), and it
     // stays zero through factor/workspace pointer swaps.
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= i; j += gridDim.x * blockDim.x) {
-        const double mbj = wg * mg[j] + wl * mlc[j];
-        const double s = wg * Sgr[j] + wl * Slr[j];  // :45-46
-        double v = s - mbi * mbj;                    // covariance :90-101 (S exactly symmetric)
-        if (j == i && jitter_eps > 0.0) v += jitter_eps * (tr[c] / (double)d);  // proposal.cpp:229-231
-        Crow[j] = v;
+    // Pairs of columns per thread (rows are 64-byte aligned: ld is a multiple of 8).
+    const double jit = jitter_eps > 0.0 ? jitter_eps * (tr[c] / (double)d) : 0.0;  // proposal.cpp:229-231
+    for (int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x); j <= i; j += 2 * gridDim.x * blockDim.x) {
+        const double2 sg = *reinterpret_cast<const double2*>(Sgr + j);
+        const double2 sl = *reinterpret_cast<const double2*>(Slr + j);
+        const double2 g2 = *reinterpret_cast<const double2*>(mg + j);
+        const double2 l2 = *reinterpret_cast<const double2*>(mlc + j);
+        // covariance :90-101 (S exactly symmetric) of the blend :45-46
+        double v0 = (wg * sg.x + wl * sl.x) - mbi * (wg * g2.x + wl * l2.x);
+        double v1 = (wg * sg.y + wl * sl.y) - mbi * (wg * g2.y + wl * l2.y);
+        if (j == i) v0 += jit;
+        if (j + 1 == i) v1 += jit;
+        if (j + 1 <= i)
+            *reinterpret_cast<double2*>(Crow + j) = make_double2(v0, v1);
+        else
+            Crow[j] = v0;
     }
 }
 
@@ -520,7 +530,7 @@ void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg, 
                       int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl, double* mb,
                       int64_t mb_stride, int chains, int d, int64_t ld, const int* mask, double jitter_eps,
                       const double* tr, cudaStream_t s, const double* aug_x, const double* aug_xr) {
-    dim3 grid((unsigned)ceil_div(d, 256), d + (aug_x ? 1 : 0), chains);
+    dim3 grid((unsigned)ceil_div(ceil_div(d, 2), 256), d + (aug_x ? 1 : 0), chains);
     blend_cov_kernel<<<grid, 256, 0, s>>>(C_out, Sg, mg, Sl, sl_stride, ml, ml_stride, wg, wl, mb, mb_stride, d, ld,
                                           mask, jitter_eps, tr, aug_x, aug_xr);
     DGB_LAUNCH_CHECK();
