@@ -10,6 +10,35 @@
 
 __global__ void empty_kernel() {}
 
+// pure dependent-chain latencies, unrolled (no loop overhead): 128 DFMA, 128 LDS.64 chase
+__global__ void lat2_kernel(long long* cyc, double* out, double a, double b) {
+    __shared__ double sh[256];
+    __shared__ int idx[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        sh[i] = 1.0 + i;
+        idx[i] = (i * 7 + 1) & 255;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double x = a;
+    long long t0 = clock64();
+#pragma unroll
+    for (int i = 0; i < 128; ++i) x = fma(x, b, a);
+    long long t1 = clock64();
+    int j = 0;
+#pragma unroll
+    for (int i = 0; i < 128; ++i) j = idx[j];
+    long long t2 = clock64();
+    double y = x;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) y = rsqrt(y + 1.0);
+    long long t3 = clock64();
+    cyc[0] = (t1 - t0) / 128;
+    cyc[1] = (t2 - t1) / 128;
+    cyc[2] = (t3 - t2) / 32;
+    out[0] = x + j + y;
+}
+
 // barrier round trips: 256 threads, 64 iterations of (smem write by one thread, barrier,
 // everyone reads it, barrier)
 __global__ void barrier_kernel(long long* cyc, double* out) {
@@ -305,6 +334,10 @@ int main() {
         lat_kernel<<<1, 1>>>(o, cy, 0.5, 0.999);
         long long hc[4];
         cudaMemcpy(hc, cy, 32, cudaMemcpyDeviceToHost);
+        lat2_kernel<<<1, 256>>>(cy, o, 0.5, 0.999);
+        long long hl[4];
+        cudaMemcpy(hl, cy, 32, cudaMemcpyDeviceToHost);
+        printf("unrolled dependent latency: DFMA %lld cycles, LDS.32 chase %lld, rsqrt(double)+add %lld\n", hl[0], hl[1], hl[2]);
         barrier_kernel<<<64, 256>>>(cy, o);
         long long hb[4];
         cudaMemcpy(hb, cy, 32, cudaMemcpyDeviceToHost);
