@@ -239,7 +239,7 @@ constexpr int kNb = kDiagNb;
 
 // MINB 2: <= 128 registers (spills a little) so a diagonal-block CTA can share its SM with
 // a GEMM CTA of another group; MINB 1: 190 registers, no spills
-template <int MINB>
+template <int MINB, bool FAST>
 __global__ void __launch_bounds__(256, MINB) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
                                                             const int* mask, int* status, int* active,
                                                             double* inv_base, int zero_above) {
@@ -247,8 +247,10 @@ __global__ void __launch_bounds__(256, MINB) potrf_diag_kernel(double* const* Am
     const bool run = (!mask || mask[c]) && status[c] == 0;
     if (threadIdx.x == 0) active[c] = run ? 1 : 0;
     if (!run) return;
-    if (diag64_block(Am[c] + (int64_t)j0 * ld + j0, ld, jb, inv_base + (int64_t)c * kNb * kNb, zero_above) &&
-        threadIdx.x == 0) {
+    double* Ab = Am[c] + (int64_t)j0 * ld + j0;
+    double* out = inv_base + (int64_t)c * kNb * kNb;
+    const int bad = FAST ? diag64_fast(Ab, ld, jb, out, zero_above) : diag64_block(Ab, ld, jb, out, zero_above);
+    if (bad && threadIdx.x == 0) {
         status[c] = 1;
         active[c] = 0;
     }
@@ -641,14 +643,16 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     };
     // factor the 64-wide diagonal block at (c0, c0) and solve the rows below it (in place)
     auto factor_and_solve = [&](int c0, int n, int zero_above) {
-        static const int minb = [] {
-            const char* e = std::getenv("DIAM_B200_DIAG_MINB");
-            return e ? std::atoi(e) : 2;
-        }();
-        if (minb == 1)
-            potrf_diag_kernel<1><<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
+        // DIAM_B200_DIAG (read per call): "fast" = one barrier per step (diag64_fast), else
+        // the two-barrier register-blocked version. Both take ~34 us per 64x64 block on a
+        // B200: the cost is each warp's dependent instruction stream (~300 instructions per
+        // block step at ~9-15 cycles each), not the barriers
+        const char* de = std::getenv("DIAM_B200_DIAG");
+        const bool fast = de && std::string(de) == "fast";
+        if (fast)
+            potrf_diag_kernel<1, true><<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
         else
-            potrf_diag_kernel<2><<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
+            potrf_diag_kernel<2, false><<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
         DGB_LAUNCH_CHECK();
         count_launch();
         const int rest = rows - c0 - n;

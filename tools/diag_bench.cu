@@ -346,12 +346,14 @@ int main() {
                hc[0], hc[1], hc[2], hc[3]);
     }
     timeit([&] { empty_kernel<<<chains, 256>>>(); }, "empty launch");
-    timeit([&] { potrf_diag_kernel<2><<<chains, 256>>>(Ap, ld, 0, 64, nullptr, status, active, inv, 0); },
+    timeit([&] { potrf_diag_kernel<2, false><<<chains, 256>>>(Ap, ld, 0, 64, nullptr, status, active, inv, 0); },
            "diag64 (minb 2)");
-    timeit([&] { potrf_diag_kernel<1><<<chains, 256>>>(Ap, ld, 0, 64, nullptr, status, active, inv, 0); },
+    timeit([&] { potrf_diag_kernel<1, false><<<chains, 256>>>(Ap, ld, 0, 64, nullptr, status, active, inv, 0); },
            "diag64 (minb 1)");
-    timeit([&] { potrf_diag_kernel<2><<<chains, 256>>>(Ap, ld, 0, 32, nullptr, status, active, inv, 0); },
-           "diag64 jb=32 (minb 2)");
+    timeit([&] { potrf_diag_kernel<1, true><<<chains, 256>>>(Ap, ld, 0, 64, nullptr, status, active, inv, 0); },
+           "diag64 FAST (minb 1)");
+    timeit([&] { potrf_diag_kernel<2, true><<<chains, 256>>>(Ap, ld, 0, 64, nullptr, status, active, inv, 0); },
+           "diag64 FAST (minb 2)");
     timeit([&] { diag_exp_kernel<0><<<chains, 256>>>(Ap, ld, 64, status, inv); }, "exp full");
     auto cyc = [&](auto launch, const char* name) {
         long long* cy;
