@@ -228,7 +228,7 @@ def impl_reference(args):
     value = samples / total
     line = {
         "impl": "reference", "metric": f"chain-samples/s (DIAM, {kind} d={d}, n_lag={n_lag})", "value": value,
-        "unit": "chain-samples/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "unit": "chain-samples/s", "n_gpus": int(os.environ.get("WORLD_SIZE", args.gpus)), "device": "host cpu", "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (pi1 target from the reference's Philox stream)",
         "config": {"workload": f"{args.config}: {chains} chains x 1 window of {n_lag} steps per step "
