@@ -104,7 +104,6 @@ Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shar
     require(d_ <= 8192, Err::InvalidDimension, "the B200 engine supports d <= 8192");
     DGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     DGB_CUDA(cudaEventCreateWithFlags(&main_ev_, cudaEventDisableTiming));
-    if (const char* e = std::getenv("DIAM_B200_PRENOISE")) prenoise_ = std::atoi(e) != 0;
     DeferAllocSync defer;
     upload_target();
     const int ng = plan_memory();
@@ -201,13 +200,6 @@ Engine::~Engine() {
         }
         if (g.done) cudaEventDestroy(g.done);
         if (g.pool_ev) cudaEventDestroy(g.pool_ev);
-        if (g.steps_ev) cudaEventDestroy(g.steps_ev);
-        if (g.s2) {
-            cudaStreamSynchronize(g.s2);
-            cudaStreamDestroy(g.s2);
-        }
-        if (g.ev_free) cudaEventDestroy(g.ev_free);
-        if (g.ev_noise) cudaEventDestroy(g.ev_noise);
         potrf_work_release(g.pw);
     }
     for (void* p : allocs_) cudaFreeAsync(p, 0);
@@ -287,7 +279,6 @@ void Engine::init_chains() {
     try_ = dalloc<int>(A, C);
     usable_ = dalloc<int>(A, C);
     mask_ = dalloc<int>(A, C);
-    fatal_ = dalloc<int>(A, 1);
     DGB_CUDA(cudaMallocHost(&h_flags_, 3 * (size_t)C * sizeof(int)));
     Sg_ = dalloc<double>(A, mat_);
     mg_ = dalloc<double>(A, ld_);
@@ -364,10 +355,6 @@ void Engine::make_groups(int n) {
         DGB_CUDA(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
         DGB_CUDA(cudaEventCreateWithFlags(&g.status_ev, cudaEventDisableTiming));
         DGB_CUDA(cudaEventCreateWithFlags(&g.pool_ev, cudaEventDisableTiming));
-        DGB_CUDA(cudaEventCreateWithFlags(&g.steps_ev, cudaEventDisableTiming));
-        DGB_CUDA(cudaStreamCreateWithFlags(&g.s2, cudaStreamNonBlocking));
-        DGB_CUDA(cudaEventCreateWithFlags(&g.ev_free, cudaEventDisableTiming));
-        DGB_CUDA(cudaEventCreateWithFlags(&g.ev_noise, cudaEventDisableTiming));
         g.Lp = Lp_ + g.off;
         // pool mode: every group factors into the same workspace (slot i <-> the group's
         // chain i); accepted factors swap pointers with their slot as before
@@ -564,40 +551,11 @@ void Engine::run_batch_windows(bool record) {
     // window m, the other group's kernels keep the GPU busy; g's next head follows at once.
     // Groups whose factorization needs the jitter ladder are set aside and stepped
     // together, so their retries run concurrently instead of one group after another.
-    // DIAM_B200_STAGGER=1: the second half of the groups begins the batch when the first
-    // half has finished its first window's steps, so one half's refactorization overlaps
-    // the other half's GEMMs (measured 0.8% slower at d=1024 and 1.6% at d=4096: the
-    // start and end offsets cost more than the overlap gains; off by default).
-    // All plans up front (host counters only): window m+1's first noise chunk is drawn on
-    // the group's side stream while window m refactors -- the noise depends on neither the
-    // new factor nor beta's next value unless the factor is still the identity.
-    for (size_t m = 0; m < M; ++m) {
-        next_plan(m);
-        plans[m].pre_noise = m > 0 && prenoise_;
-    }
-    const size_t G = groups_.size();
-    // (1: the offset is the first half's whole first-window steps; 2: only up to its
-    // first target GEMM)
-    static const int stagger = [] {
-        const char* e = std::getenv("DIAM_B200_STAGGER");
-        return e ? std::atoi(e) : 0;
-    }();
-    const size_t half = (stagger && G >= 4 && plans[0].refactor) ? G / 2 : 0;
-    for (size_t i = 0; i < G; ++i) {
-        Group& g = groups_[i];
-        if (half && i >= half) DGB_CUDA(cudaStreamWaitEvent(g.s, groups_[i - half].steps_ev, 0));
-        g.mark_target = half && i < half && stagger == 2;
-        enqueue_steps(g, plans[0]);
-        g.mark_target = false;
-        if (half && i < half && stagger != 2) DGB_CUDA(cudaEventRecord(g.steps_ev, g.s));
-        if (M > 1 && plans[1].pre_noise) enqueue_prenoise(g, plans[1]);
-        enqueue_refactor(g, plans[0]);
-    }
-    auto head = [&](Group& g, size_t m) {  // window m's steps, m+1's early noise, m's refactor
-        enqueue_steps(g, plans[m]);
-        if (m + 1 < M && plans[m + 1].pre_noise) enqueue_prenoise(g, plans[m + 1]);
-        enqueue_refactor(g, plans[m]);
-    };
+    // (Measured and dropped: staggering the groups' start by half a window, and drawing
+    // the next window's noise on a side stream during the refactorization -- neither
+    // beat this plain order at d=1024 or d=4096.)
+    for (size_t m = 0; m < M; ++m) next_plan(m);
+    for (auto& g : groups_) enqueue_head(g, plans[0]);
     std::vector<Ladder> lad(groups_.size());
     for (size_t m = 0; m < M; ++m) {
         std::vector<size_t> pending;
@@ -607,7 +565,7 @@ void Engine::run_batch_windows(bool record) {
                 continue;
             }
             tail_finish(groups_[i], plans[m]);
-            if (m + 1 < M) head(groups_[i], m + 1);
+            if (m + 1 < M) enqueue_head(groups_[i], plans[m + 1]);
         }
         while (!pending.empty()) {
             std::vector<size_t> still;
@@ -617,7 +575,7 @@ void Engine::run_batch_windows(bool record) {
                     continue;
                 }
                 tail_finish(groups_[i], plans[m]);
-                if (m + 1 < M) head(groups_[i], m + 1);
+                if (m + 1 < M) enqueue_head(groups_[i], plans[m + 1]);
             }
             pending.swap(still);
         }
@@ -633,19 +591,6 @@ void Engine::enqueue_steps(Group& g, const WindowPlan& p) {
                        g.s);
 }
 
-// The next window's first chunk of noise on the side stream, once this window's last
-// readers of W / Xi (and the beta update) are done.
-void Engine::enqueue_prenoise(Group& g, const WindowPlan& next) {
-    const int o = g.off;
-    DGB_CUDA(cudaEventRecord(g.ev_free, g.s));
-    DGB_CUDA(cudaStreamWaitEvent(g.s2, g.ev_free, 0));
-    timed_begin(g.s2);
-    launch_normals(W_ + o * win_, next.identity ? Xi_ + o * win_ : nullptr, win_, g.C, std::min(Lc_, Lw_), d_, ld_,
-                   nkeys_ + o, next.nctr, beta_ + o, k_.noise_infl(), g.s2);
-    timed_end("normals", 0.0, g.s2);
-    DGB_CUDA(cudaEventRecord(g.ev_noise, g.s2));
-}
-
 // Rows [r0, r0 + rows) of the window: noise, target GEMM, the MH steps, and the moments
 // of the chunk's post-burn-in states. The step recursion's state (x, G x, y, log pi,
 // counters) lives in global memory, so consecutive chunks continue one another exactly;
@@ -656,14 +601,10 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     const double infl = k_.noise_infl();
     // ---- noise: W from Philox, Xi = s W L^T, H = Xi G^T (proposal.cpp:254-266); row r of
     // the window draws counters nctr + r d .. nctr + (r + 1) d - 1 of the chain's stream
-    if (r0 == 0 && p.pre_noise) {
-        DGB_CUDA(cudaStreamWaitEvent(s, g.ev_noise, 0));
-    } else {
-        timed_begin(s);
-        launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, rows, d_, ld_, nkeys_ + o,
-                       p.nctr + (uint64_t)r0 * d_, beta_ + o, infl, s);
-        timed_end("normals", 0.0, s);
-    }
+    timed_begin(s);
+    launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, rows, d_, ld_, nkeys_ + o,
+                   p.nctr + (uint64_t)r0 * d_, beta_ + o, infl, s);
+    timed_end("normals", 0.0, s);
     if (!p.identity) {
         GemmBatch t{};
         t.A = (const double* const*)g.Wp;
@@ -697,7 +638,6 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
             h.C = g.Hb;
             h.M = C * Lc_;  // the group's window chunks are one contiguous (C Lc) x ld matrix
             gemm("gemm_target", h, 1, true, true, s);
-            if (g.mark_target && r0 == 0) DGB_CUDA(cudaEventRecord(g.steps_ev, s));
         } else {            // ragged last chunk: per-chain pieces
             h.B = (const double* const*)Gpc_;
             h.A = (const double* const*)g.Xip;
@@ -975,19 +915,6 @@ void Engine::merge_batch() {
     cnt_local_ = 0;
 }
 
-void Engine::check_fatal() {
-    int f = 0;
-    DGB_CUDA(cudaMemcpyAsync(&f, fatal_, sizeof f, cudaMemcpyDeviceToHost, stream_));
-    DGB_CUDA(cudaStreamSynchronize(stream_));
-    if (f == 0) return;
-    const int c = f - 1;
-    double trh = 0.0;
-    DGB_CUDA(cudaMemcpy(&trh, tr_ + c, 8, cudaMemcpyDeviceToHost));
-    fail(Err::NotPositiveDefinite, "chain " + std::to_string(c0_ + c) +
-                                       ": covariance not factorizable after jitter escalation (dim " +
-                                       std::to_string(d_) + ", trace " + std::to_string(trh) + ")");
-}
-
 void Engine::batch_stats(double& cov_err, double& mean_err, double& psrf) {
     cov_err = mean_err = psrf = NAN;
     if (cnt_g_ >= 2) {  // runner.cpp:249-256
@@ -1119,7 +1046,6 @@ double Engine::run_batches_timed(int k) {
     DGB_CUDA(cudaEventElapsedTime(&ms, a, b));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    check_fatal();
     return ms;
 }
 
@@ -1155,7 +1081,6 @@ RunResult Engine::run() {  // runner.cpp:216-279
         run_batch_windows(cfg_.record_traces);
         join_groups();
         merge_batch();
-        check_fatal();
         collect_batch_host(M);
         ++batches_done_;
         double ce, me, ps;

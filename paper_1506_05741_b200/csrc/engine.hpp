@@ -95,10 +95,6 @@ private:
         PotrfWork pw{};
         cudaEvent_t status_ev = nullptr;  // POTRF statuses of the group's last window landed in h_status_
         cudaEvent_t pool_ev = nullptr;    // shared refactor workspace released (pool mode)
-        cudaEvent_t steps_ev = nullptr;   // the group's first window steps of a batch are done
-        bool mark_target = false;         // record steps_ev after the next target GEMM instead
-        cudaStream_t s2 = nullptr;        // side stream: the next window's noise during the refactor
-        cudaEvent_t ev_free = nullptr, ev_noise = nullptr;
     };
     // host-side scalars of one lag window, identical for every chain
     struct WindowPlan {
@@ -108,7 +104,6 @@ private:
         uint64_t cnt_before = 0, cnt_after = 0;
         bool record = false, refactor = false, move_ref = false;
         bool identity = false;  // every factor is still the initial identity (noise = s W)
-        bool pre_noise = false;  // the first chunk's normals were drawn early on the side stream
         double wg = 0.0, wl = 1.0;
     };
 
@@ -129,7 +124,6 @@ private:
     }
     void enqueue_steps(Group& g, const WindowPlan& p);
     void enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows);
-    void enqueue_prenoise(Group& g, const WindowPlan& next);
     void enqueue_refactor(Group& g, const WindowPlan& p);
     void enqueue_tail(Group& g, const WindowPlan& p);  // tail_begin/step.../finish, blocking
     struct Ladder {  // one group's jitter escalation in flight
@@ -146,7 +140,6 @@ private:
     void fork_groups();  // groups wait for the main stream
     void join_groups();  // main stream waits for every group
     void merge_batch();
-    void check_fatal();
     void batch_stats(double& cov_err, double& mean_err, double& psrf);
     void collect_batch_host(size_t windows);
     void save_checkpoint(double wall);
@@ -172,10 +165,6 @@ private:
     bool pool_ = false;
     int pool_n_ = 0;
     cudaEvent_t pool_last_ = nullptr;  // latest release of the shared workspace
-    // early next-window noise on a side stream during the refactor (DIAM_B200_PRENOISE=1);
-    // measured 2.7% slower at d=1024 with 8 groups (the other groups' GEMMs lose SMs to
-    // it), neutral at d=4096: off by default
-    bool prenoise_ = false;
     int64_t ld_ = 0, win_ = 0, mat_ = 0;
     int64_t fmat_ = 0;  // factor stride: d rows + the augmented row r = x - x_ref
     bool twisted_ = false, identity_ = true;
@@ -196,7 +185,7 @@ private:
     double *mean_ = nullptr, *cmean_ = nullptr, *cdiag_ = nullptr, *mb_ = nullptr;
     double *logpi_ = nullptr, *quad_ = nullptr, *beta_ = nullptr, *tr_ = nullptr, *qtmp_ = nullptr;
     uint64_t *nacc_ = nullptr, *uctr_ = nullptr;
-    int *status_ = nullptr, *try_ = nullptr, *usable_ = nullptr, *fatal_ = nullptr, *mask_ = nullptr;
+    int *status_ = nullptr, *try_ = nullptr, *usable_ = nullptr, *mask_ = nullptr;
     int* h_flags_ = nullptr;  // pinned host mirror: status[C], try[C], ladder mask[C]
     PhiloxKey *nkeys_ = nullptr, *ukeys_ = nullptr, *ikeys_ = nullptr;
     double **Lp_ = nullptr, **Lnp_ = nullptr;  // factor / workspace pointer arrays (swapped on device)

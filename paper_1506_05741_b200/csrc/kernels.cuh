@@ -120,12 +120,6 @@ void potrf_dag(double* const* A, int64_t ld, int d, int chains, const int* mask,
 bool potrf_dag_aborted(const PotrfWork& w);  // valid once the POTRF's stream work completed
 size_t potrf_dag_bytes(int d, int chains);   // inverse tiles kept per factorization
 void potrf_work_release(PotrfWork& w);
-// device-side jitter ladder for chains with status 1 (see linalg.cu); fatal <- first chain+1
-// whose ladder is exhausted (status 2)
-void launch_potrf_rescue(double* const* C_out, int64_t ld, int d, int extra, const double* Sg, const double* mg,
-                         const double* Sl, int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl,
-                         const double* tr, const double* ax, const double* axr, int* status, int* fatal, int chains,
-                         cudaStream_t s);
 // q_c = half_inv_infl2 * |row d of L_c|^2 (the augmented row = L^{-1}(x - x_ref))
 void launch_aug_quad(double* const* L, int64_t ld, int d, int chains, double half_inv_infl2, const int* mask,
                      double* q, cudaStream_t s);

@@ -309,81 +309,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
 }
 
-// Jitter escalation on the device (proj/src/proposal.cpp:218-239): one CTA per chain whose
-// blocked factorization reported a bad pivot (status 1) rebuilds C + eps*(tr/d) I for
-// eps = 1e-10, 1e-8, 1e-6, 9.999e-5 (the reference's floating loop) and refactors it with a
-// left-looking column Cholesky (one warp per row dot product), augmented rows included.
-// Chains that already factored exit at once, so the launch is free in the common case and
-// the window pipeline needs no host round trip. status: 0 factored, 2 ladder exhausted.
-__global__ void __launch_bounds__(256) potrf_rescue_kernel(double* const* Cm, int64_t ld, int d, int extra,
-                                                           const double* Sg, const double* mg, const double* Sl,
-                                                           int64_t sl_stride, const double* ml, int64_t ml_stride,
-                                                           double wg, double wl, const double* tr, const double* ax,
-                                                           const double* axr, int* status, int* fatal) {
-    const int c = blockIdx.x;
-    if (status[c] != 1) return;
-    double* A = Cm[c];
-    const int rows = d + extra;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = 256 / 32;
-    const double* Slc = Sl + c * sl_stride;
-    const double* mlc = ml + c * ml_stride;
-    __shared__ double s_piv;
-    __shared__ int s_bad;
-    for (double eps = 1e-10; eps <= 1e-4; eps *= 100.0) {
-        const double jit = eps * (tr[c] / (double)d);
-        for (int64_t e = tid; e < (int64_t)rows * d; e += blockDim.x) {
-            const int i = (int)(e / d), j = (int)(e % d);
-            double v = 0.0;
-            if (i >= d) {
-                v = ax[c * ld + j] - (axr ? axr[c * ld + j] : 0.0);
-            } else if (j <= i) {
-                const double mbi = wg * mg[i] + wl * mlc[i], mbj = wg * mg[j] + wl * mlc[j];
-                v = (wg * Sg[(int64_t)i * ld + j] + wl * Slc[(int64_t)i * ld + j]) - mbi * mbj;
-                if (i == j) v += jit;
-            }
-            A[(int64_t)i * ld + j] = v;
-        }
-        if (tid == 0) s_bad = 0;
-        __syncthreads();
-        for (int j = 0; j < d; ++j) {
-            const double* Aj = A + (int64_t)j * ld;
-            if (warp == 0) {
-                double s = 0.0;
-                for (int k = lane; k < j; k += 32) s += Aj[k] * Aj[k];
-                s = warp_sum(s);
-                if (lane == 0) {
-                    const double p = Aj[j] - s;
-                    if (!(p > 0.0) || !isfinite(p)) s_bad = 1;
-                    const double l = sqrt(p);
-                    A[(int64_t)j * ld + j] = l;
-                    s_piv = l;
-                }
-            }
-            __syncthreads();
-            if (s_bad) break;
-            const double l = s_piv;
-            for (int i = j + 1 + warp; i < rows; i += NW) {
-                double* Ai = A + (int64_t)i * ld;
-                double s = 0.0;
-                for (int k = lane; k < j; k += 32) s += Ai[k] * Aj[k];
-                s = warp_sum(s);
-                if (lane == 0) Ai[j] = (Ai[j] - s) / l;
-            }
-            __syncthreads();
-        }
-        if (!s_bad) {
-            if (tid == 0) status[c] = 0;
-            return;
-        }
-        __syncthreads();
-    }
-    if (tid == 0) {
-        status[c] = 2;
-        atomicCAS(fatal, 0, c + 1);
-    }
-}
-
 __global__ void aug_quad_kernel(double* const* Lm, int64_t ld, int d, double hq, const int* mask, double* q) {
     const int c = blockIdx.x;
     if (mask && !mask[c]) return;
@@ -688,16 +613,6 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
             factor_and_solve(j0 + kNb, jb - kNb, j0 > 0 ? 1 : 0);
         }
     }
-}
-
-void launch_potrf_rescue(double* const* C_out, int64_t ld, int d, int extra, const double* Sg, const double* mg,
-                         const double* Sl, int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl,
-                         const double* tr, const double* ax, const double* axr, int* status, int* fatal, int chains,
-                         cudaStream_t s) {
-    potrf_rescue_kernel<<<chains, 256, 0, s>>>(C_out, ld, d, extra, Sg, mg, Sl, sl_stride, ml, ml_stride, wg, wl, tr,
-                                               ax, axr, status, fatal);
-    DGB_LAUNCH_CHECK();
-    count_launch();
 }
 
 void launch_aug_quad(double* const* L, int64_t ld, int d, int chains, double half_inv_infl2, const int* mask,
