@@ -66,6 +66,12 @@ diam_status diamx_engine_layout(const diamx_engine* e, int64_t* groups, int64_t*
                                 int64_t* pool_factors);
 void diamx_engine_free(diamx_engine* e);
 
+/* the sharded multi-GPU engine path on ONE GPU: `world` engines (ranks) driven by host
+ * threads, exchanging through an in-process communicator instead of NCCL; returns rank
+ * 0's result (chain histories all-gathered, traces merged). For parity tests. */
+diam_status diamx_sample_threads(const diam_target* target, const diam_run_options* options, int world,
+                                 diam_result** out);
+
 /* parity capture: run a full diam_sample-equivalent and keep every window's
  * standard normals W (n_windows x n_lag x d per chain) and per-step log alpha /
  * accept bits, so the CPU oracle can be driven on identical draws. */

@@ -62,6 +62,7 @@ class B200(DiamABI):
             "diamx_engine_layout": (st, [_vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
             "diamx_engine_free": (None, [_vp]),
             "diamx_sample_capture": (st, [_vp, C.POINTER(RunOptions), C.POINTER(_vp), C.POINTER(_vp)]),
+            "diamx_sample_threads": (st, [_vp, C.POINTER(RunOptions), C.c_int, C.POINTER(_vp)]),
             "diamx_capture_len": (i64, [_vp, i64, C.c_char_p]),
             "diamx_capture_copy": (st, [_vp, i64, C.c_char_p, _dp, i64]),
             "diamx_draws": (st, [C.c_int, _vp, _vp, i64, u64, u64, C.c_char_p, u64, _vp]),
@@ -88,6 +89,14 @@ class B200(DiamABI):
         r, e = C.c_void_p(), C.c_void_p()
         self.check(self.lib.diamx_sample_capture(target.h, C.byref(o), C.byref(r), C.byref(e)))
         return Result(self, r), Capture(self, e)
+
+    def sample_threads(self, target, world: int, **opts):
+        """The sharded engine path (`world` ranks) on one GPU, in-process exchange."""
+        from .abi import Result
+        o = self.options(**opts)
+        r = C.c_void_p()
+        self.check(self.lib.diamx_sample_threads(target.h, C.byref(o), world, C.byref(r)))
+        return Result(self, r)
 
     def launch_count(self) -> int:
         return int(self.lib.diamx_launch_count())

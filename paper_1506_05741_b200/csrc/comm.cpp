@@ -3,9 +3,13 @@
 
 #include <dlfcn.h>
 
+#include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -81,7 +85,74 @@ struct NcclComm final : Comm {
     }
 };
 
+// ---------------------------------------------------------------- in-process ranks
+struct ThreadShared {
+    int world = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t generation = 0;
+    std::vector<std::vector<double>> stage;  // one host buffer per rank
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const uint64_t gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+            return;
+        }
+        if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return generation != gen; }))
+            throw CudaError("thread communicator: a rank did not reach the exchange");
+    }
+};
+
+struct ThreadComm final : Comm {
+    std::shared_ptr<ThreadShared> sh;
+    int r = 0;
+    int rank() const override { return r; }
+    int size() const override { return sh->world; }
+    void allreduce_sum(double* buf, int64_t cnt, cudaStream_t s) override {
+        auto& mine = sh->stage[r];
+        mine.resize(cnt);
+        DGB_CUDA(cudaMemcpyAsync(mine.data(), buf, cnt * 8, cudaMemcpyDeviceToHost, s));
+        DGB_CUDA(cudaStreamSynchronize(s));
+        sh->barrier();
+        std::vector<double> sum(cnt, 0.0);
+        for (int k = 0; k < sh->world; ++k)  // rank order, the same on every rank
+            for (int64_t e = 0; e < cnt; ++e) sum[e] += sh->stage[k][e];
+        sh->barrier();  // everyone has read every stage
+        DGB_CUDA(cudaMemcpyAsync(buf, sum.data(), cnt * 8, cudaMemcpyHostToDevice, s));
+        DGB_CUDA(cudaStreamSynchronize(s));
+    }
+    void allgather(const double* src, double* dst, int64_t cnt, cudaStream_t s) override {
+        auto& mine = sh->stage[r];
+        mine.resize(cnt);
+        DGB_CUDA(cudaMemcpyAsync(mine.data(), src, cnt * 8, cudaMemcpyDeviceToHost, s));
+        DGB_CUDA(cudaStreamSynchronize(s));
+        sh->barrier();
+        for (int k = 0; k < sh->world; ++k)
+            DGB_CUDA(cudaMemcpyAsync(dst + k * cnt, sh->stage[k].data(), cnt * 8, cudaMemcpyHostToDevice, s));
+        DGB_CUDA(cudaStreamSynchronize(s));
+        sh->barrier();
+    }
+};
+
 }  // namespace
+
+std::vector<std::shared_ptr<Comm>> make_thread_comms(int world) {
+    auto sh = std::make_shared<ThreadShared>();
+    sh->world = world;
+    sh->stage.resize(world);
+    std::vector<std::shared_ptr<Comm>> out;
+    for (int r = 0; r < world; ++r) {
+        auto c = std::make_shared<ThreadComm>();
+        c->sh = sh;
+        c->r = r;
+        out.push_back(c);
+    }
+    return out;
+}
 
 std::shared_ptr<Comm>& global_comm() {
     static std::shared_ptr<Comm> c;

@@ -12,6 +12,7 @@
 #include <stdint.h>
 
 #include <memory>
+#include <vector>
 
 namespace dgb {
 
@@ -30,5 +31,9 @@ std::shared_ptr<Comm>& global_comm();
 bool nccl_available(char* why, int why_len);
 int nccl_unique_id(char out[128]);
 std::shared_ptr<Comm> make_nccl_comm(const char id[128], int rank, int world);
+// In-process communicator for `world` engines driven by `world` host threads on one GPU
+// (parity tests of the sharded engine: the same exchange steps as NCCL, summed on the
+// host in rank order; a rank that stops arriving makes the others fail, not hang).
+std::vector<std::shared_ptr<Comm>> make_thread_comms(int world);
 
 }  // namespace dgb

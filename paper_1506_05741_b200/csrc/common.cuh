@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -32,8 +33,8 @@ inline void launch_check(const char* file, int line) {
 #define DGB_LAUNCH_CHECK() ::dgb::launch_check(__FILE__, __LINE__)
 
 // Process-wide count of our own kernel launches (bench.py reports it as gpu_launches).
-extern uint64_t g_launch_count;
-inline void count_launch(uint64_t n = 1) { g_launch_count += n; }
+extern std::atomic<uint64_t> g_launch_count;
+inline void count_launch(uint64_t n = 1) { g_launch_count.fetch_add(n, std::memory_order_relaxed); }
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

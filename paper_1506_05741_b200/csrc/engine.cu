@@ -14,7 +14,7 @@
 
 namespace dgb {
 
-uint64_t g_launch_count = 0;
+std::atomic<uint64_t> g_launch_count{0};
 
 bool sync_check_enabled() {
     static const bool on = [] {

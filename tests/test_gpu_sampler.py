@@ -244,6 +244,31 @@ def test_launch_counter_moves(b200):
     assert b200.launch_count() > before
 
 
+@pytest.mark.parametrize("world,P,kern", [(2, 6, "diam"), (3, 7, "diam"), (4, 9, "pcn")])
+def test_sharded_engine_in_process_ranks(b200, world, P, kern):
+    """The multi-GPU engine path -- block-sharded chains, the batch-moment all-reduce,
+    the PSRF and history all-gathers, merge weights over ranks -- with `world` engines on
+    one GPU exchanging in process (uneven shards for P % world != 0). Draws are keyed by
+    global chain index, so every chain's decisions and histories equal the single-engine
+    run; pooled moments agree to summation order (parity across G is at
+    tolerance)."""
+    t = b200.target_build("pi1", 48, 6)
+    kw = dict(kernel=kern, chains=P, intervals_per_batch=2, max_batches=3, n_lag=40, n0=20, master_seed=12,
+              trace_thin=5)
+    r1 = b200.sample(t, **kw)
+    rw = b200.sample_threads(t, world, **kw)
+    assert rw.total_samples == r1.total_samples and rw.accumulated_samples == r1.accumulated_samples
+    for p in range(P):
+        assert np.array_equal(rw.chain_history(p, "beta"), r1.chain_history(p, "beta"))
+        assert np.array_equal(rw.chain_history(p, "acceptance"), r1.chain_history(p, "acceptance"))
+        a, b = r1.trace(p, 0), rw.trace(p, 0)
+        assert a.shape == b.shape and np.max(np.abs(a - b)) <= 1e-9 * max(1.0, np.max(np.abs(a)))
+    assert np.linalg.norm(rw.cov() - r1.cov()) <= 1e-12 * np.linalg.norm(r1.cov())
+    assert np.linalg.norm(rw.mean() - r1.mean()) <= 1e-12 * max(1.0, np.linalg.norm(r1.mean()))
+    assert np.allclose(rw.history("cov_error"), r1.history("cov_error"), rtol=1e-10, equal_nan=True)
+    assert np.allclose(rw.history("psrf"), r1.history("psrf"), rtol=1e-10, equal_nan=True)
+
+
 def test_nccl_sharded_path_single_rank(b200, tmp_path):
     """The multi-GPU code path (NCCL all-reduce of the batch moments, all-gather of the
     PSRF inputs and of the chain histories) on a one-rank communicator must reproduce
