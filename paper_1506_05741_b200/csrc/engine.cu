@@ -213,6 +213,7 @@ Engine::~Engine() {
     for (auto& g : groups_)
         if (g.status_ev) cudaEventDestroy(g.status_ev);
     if (h_flags_) cudaFreeHost(h_flags_);
+    if (h_stats_) cudaFreeHost(h_stats_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -244,6 +245,10 @@ void Engine::upload_target() {
         pj[i] = tgt_.eigvecs(i, 0);
         pj[ld_ + i] = tgt_.eigvecs(i, d_ - 1);
     }
+    tmean_ = dalloc<double>(A, ld_);
+    DGB_CUDA(cudaMemcpy(tmean_, tgt_.mean.data(), d_ * 8, cudaMemcpyHostToDevice));
+    dstats_ = dalloc<double>(A, 4);
+    DGB_CUDA(cudaMallocHost(&h_stats_, 4 * sizeof(double)));
     proj_ = dalloc<double>(A, 2 * ld_);
     DGB_CUDA(cudaMemcpy(proj_, pj.data(), 2 * ld_ * 8, cudaMemcpyHostToDevice));
     Gp_ = ptr_array(A, G_, 0, 1);
@@ -917,6 +922,21 @@ void Engine::merge_batch() {
 
 void Engine::batch_stats(double& cov_err, double& mean_err, double& psrf) {
     cov_err = mean_err = psrf = NAN;
+    if (!comm_) {
+        // one GPU: everything on the device, four scalars back (same summation orders as
+        // the host path below, which the sharded run keeps for its gathered shards)
+        const bool want_err = cnt_g_ >= 2, want_psrf = P_ >= 2 && cum_cnt_ >= 2;
+        if (want_err) launch_cov_error(Sg_, mg_, Ct_, d_, ld_, cov_part_, stream_);
+        launch_batch_stats(cov_part_, mg_, tmean_, d_, cmean_, cdiag_, ld_, C_, cum_cnt_, want_err, want_psrf,
+                           dstats_, stream_);
+        DGB_CUDA(cudaMemcpyAsync(h_stats_, dstats_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+        DGB_CUDA(cudaStreamSynchronize(stream_));
+        require(!((int)h_stats_[3] & 1), Err::InvalidArgument, "cov_error: zero reference norm");
+        cov_err = h_stats_[0];
+        mean_err = h_stats_[1];
+        psrf = h_stats_[2];
+        return;
+    }
     if (cnt_g_ >= 2) {  // runner.cpp:249-256
         launch_cov_error(Sg_, mg_, Ct_, d_, ld_, cov_part_, stream_);
         std::vector<double> part(2 * (size_t)d_), mg(d_);

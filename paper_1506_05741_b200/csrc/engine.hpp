@@ -194,6 +194,8 @@ private:
     double *trace_lp_ = nullptr, *trace_pj_ = nullptr;      // per batch: M x C x Lw (x2)
     double *hist_rate_ = nullptr, *hist_beta_ = nullptr;    // per batch: M x C
     double* cov_part_ = nullptr;                              // d x 2
+    double *tmean_ = nullptr, *dstats_ = nullptr;             // target mean; batch statistics (4)
+    double* h_stats_ = nullptr;                               // pinned mirror of dstats_
     double* gather_ = nullptr;                                // PSRF all-gather buffer
     double* cS_ = nullptr;  // cumulative raw second moments (lower), kept only for checkpoints
     double wall_accum_ = 0.0;  // wall seconds of earlier (checkpointed) segments of the run

@@ -91,6 +91,11 @@ void launch_axpby(double* y, const double* x, int64_t n, double a, double b, cud
 void launch_cum_fold(double* cmean, double* cdiag, const double* lmean, const double* S,
                      int64_t s_stride, int chains, int d, int64_t ld, double keep, double add,
                      cudaStream_t s);
+// the batch's convergence statistics on the device (single GPU): out4 = {cov error, mean
+// error, max sqrt(R) (PSRF), flags: 1 zero reference norm, 2 zero within-chain variance}
+void launch_batch_stats(const double* part2, const double* mg, const double* tmean, int d, const double* cmean,
+                        const double* cdiag, int64_t ld, int chains, uint64_t n_per_chain, bool want_err,
+                        bool want_psrf, double* out4, cudaStream_t s);
 // cov/mean error partial sums for cov_error (proj/src/diagnostics.cpp:121-142)
 void launch_cov_error(const double* Sg, const double* mg, const double* Ctrue, int d, int64_t ld,
                       double* out2, cudaStream_t s);

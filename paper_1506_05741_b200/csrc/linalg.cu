@@ -492,6 +492,80 @@ void launch_cum_fold(double* cmean, double* cdiag, const double* lmean, const do
     count_launch();
 }
 
+// out[0] cov error, out[1] mean error, out[2] max sqrt(R), out[3] flags (1: zero reference
+// norm, 2: zero within-chain variance). The same summation orders as the host versions
+// (Engine::batch_stats, psrf_max in host.cpp), no FMA contraction.
+__global__ void batch_stats_kernel(const double* part2, const double* mg, const double* tmean, int d,
+                                   const double* cmean, const double* cdiag, int64_t ld, int chains, double n,
+                                   int want_err, int want_psrf, double* out) {
+    __shared__ double smax[256];
+    __shared__ int sbad[256];
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        out[0] = out[1] = out[2] = nan("");
+        out[3] = 0.0;
+        if (want_err) {  // proj/src/diagnostics.cpp:121-142, proj/src/runner.cpp:249-256
+            double num = 0.0, den = 0.0;
+            for (int i = 0; i < d; ++i) {
+                num = __dadd_rn(num, part2[2 * i]);
+                den = __dadd_rn(den, part2[2 * i + 1]);
+            }
+            if (den > 0.0) out[0] = sqrt(__ddiv_rn(num, den));
+            else out[3] = 1.0;
+            double s = 0.0;
+            for (int i = 0; i < d; ++i) {
+                const double df = __dadd_rn(mg[i], -tmean[i]);
+                s = __dadd_rn(s, __dmul_rn(df, df));
+            }
+            out[1] = sqrt(s);
+        }
+    }
+    if (!want_psrf) return;
+    // proj/src/diagnostics.cpp:72-119 per direction, then the max
+    const double pd = (double)chains, inv_p = __ddiv_rn(1.0, pd);
+    double mx = 0.0;
+    int bad = 0;
+    for (int i = tid; i < d; i += blockDim.x) {
+        double gm = 0.0;
+        for (int c = 0; c < chains; ++c) gm = __dadd_rn(gm, __dmul_rn(inv_p, cmean[(int64_t)c * ld + i]));
+        double between = 0.0, within = 0.0;
+        for (int c = 0; c < chains; ++c) {
+            const double m = cmean[(int64_t)c * ld + i];
+            const double dl = __dadd_rn(m, -gm);
+            between = __dadd_rn(between, __dmul_rn(dl, dl));
+            within = __dadd_rn(within, __dadd_rn(cdiag[(int64_t)c * ld + i], -__dmul_rn(m, m)));
+        }
+        const double b = __dmul_rn(__ddiv_rn(n, __dadd_rn(pd, -1.0)), between);
+        const double w = __dmul_rn(__ddiv_rn(n, __dmul_rn(__dadd_rn(n, -1.0), pd)), within);
+        if (!(w > 0.0)) bad = 1;
+        const double r = sqrt(__dadd_rn(__ddiv_rn(__dadd_rn(n, -1.0), n),
+                                        __dmul_rn(__ddiv_rn(__dadd_rn(pd, 1.0), __dmul_rn(pd, n)), __ddiv_rn(b, w))));
+        mx = r > mx ? r : mx;  // std::max(mx, r): a NaN r leaves mx
+    }
+    smax[tid] = mx;
+    sbad[tid] = bad;
+    __syncthreads();
+    if (tid == 0) {
+        double m = 0.0;
+        int anybad = 0;
+        for (int k = 0; k < (int)blockDim.x; ++k) {
+            m = smax[k] > m ? smax[k] : m;
+            anybad |= sbad[k];
+        }
+        if (anybad) out[3] = (double)((int)out[3] | 2);
+        else out[2] = m;
+    }
+}
+
+void launch_batch_stats(const double* part2, const double* mg, const double* tmean, int d, const double* cmean,
+                        const double* cdiag, int64_t ld, int chains, uint64_t n_per_chain, bool want_err,
+                        bool want_psrf, double* out4, cudaStream_t s) {
+    batch_stats_kernel<<<1, 256, 0, s>>>(part2, mg, tmean, d, cmean, cdiag, ld, chains, (double)n_per_chain,
+                                         want_err ? 1 : 0, want_psrf ? 1 : 0, out4);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
 void launch_cov_error(const double* Sg, const double* mg, const double* Ctrue, int d, int64_t ld, double* out2,
                       cudaStream_t s) {
     cov_error_kernel<<<d, 256, 0, s>>>(Sg, mg, Ctrue, d, ld, out2);
