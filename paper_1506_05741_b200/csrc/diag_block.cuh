@@ -194,219 +194,4 @@ __device__ __forceinline__ int diag64_block(double* A, int64_t ld, int jb, doubl
     return diag64_block_sc(sc, A, ld, jb, out, zero_above, out_ld);
 }
 
-// ------------------------------------------------------------------ one barrier per step
-// The same factorization (L and X = L^-1 by 4x4 register tiles) with ONE barrier per block
-// step and every thread busy:
-//   * thread (ty, tx), tx <= ty, owns L tile (ty, tx); thread (ty, tx), tx > ty, owns X tile
-//     (tx, ty) (the transposed position: X is lower triangular too); the diagonal threads
-//     also own X tile (ty, ty);
-//   * before the barrier of step kg the owners publish what step kg consumes: the diagonal
-//     thread its 4x4 Cholesky L_kk (and reciprocal pivots), the owners of column kg of the
-//     trailing matrix their tiles A_ik, the owners of row kg of Y (X before its final
-//     triangular solve) their tiles Y_kj;
-//   * after the barrier every thread solves, redundantly and in parallel, the panel tiles
-//     it needs (L_ik = A_ik L_kk^-T, X_kj = L_kk^-1 Y_kj) and applies its rank-4 update;
-//     then it publishes for step kg+1 and the next diagonal thread factors its tile.
-struct DiagFastScratch {
-    double lkk[2][4][4], rd[2][4];
-    double col[2][16][4][4];  // A_{i,kg}, i > kg
-    double row[2][16][4][4];  // Y_{kg,j}, j < kg
-    int bad;
-};
-
-__device__ __forceinline__ void dfast_chol4(double (&v)[4][4], double (&lkk)[4][4], double (&rd)[4], int& bad) {
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-        double p = v[cc][cc];
-#pragma unroll
-        for (int n = 0; n < cc; ++n) p -= v[cc][n] * v[cc][n];
-        if (!(p > 0.0) || !isfinite(p)) bad = 1;  // proj/src/linalg.cpp:82-84
-        const double rl = rsqrt(p);
-        rd[cc] = rl;
-        v[cc][cc] = p * rl;
-#pragma unroll
-        for (int rr = cc + 1; rr < 4; ++rr) {
-            double s = v[rr][cc];
-#pragma unroll
-            for (int n = 0; n < cc; ++n) s -= v[rr][n] * v[cc][n];
-            v[rr][cc] = s * rl;
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (j > i) v[i][j] = 0.0;
-            lkk[i][j] = v[i][j];
-        }
-}
-
-// t <- t L^-T (rows), L given by lower lk and reciprocal diagonal rd
-__device__ __forceinline__ void dfast_solve_rows(double (&t)[4][4], const double (&lk)[4][4], const double (&rd)[4]) {
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            double s = t[a][m];
-#pragma unroll
-            for (int n = 0; n < m; ++n) s -= t[a][n] * lk[m][n];
-            t[a][m] = s * rd[m];
-        }
-}
-
-// t <- L^-1 t (columns)
-__device__ __forceinline__ void dfast_solve_cols(double (&t)[4][4], const double (&lk)[4][4], const double (&rd)[4]) {
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            double s = t[a][b];
-#pragma unroll
-            for (int n = 0; n < a; ++n) s -= lk[a][n] * t[n][b];
-            t[a][b] = s * rd[a];
-        }
-}
-
-__device__ __forceinline__ int diag64_fast_sc(DiagFastScratch& sc, double* A, int64_t ld, int jb, double* out,
-                                              int zero_above, int out_ld) {
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const bool lthr = tx <= ty;                 // owns L tile (ty, tx)
-    const int ti = lthr ? ty : tx, tj = lthr ? tx : ty;  // the tile this thread owns (row ti >= col tj)
-    const bool diag = tx == ty;
-    double v[4][4], xd[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int r = 4 * ti + a, q = 4 * tj + b;
-            // rows/cols past jb are padded with the identity so the 64x64 factorization stays valid
-            v[a][b] = lthr ? ((r < jb && q <= r) ? __ldcg(A + (int64_t)r * ld + q) : (r == q ? 1.0 : 0.0)) : 0.0;
-            xd[a][b] = (a == b) ? 1.0 : 0.0;
-        }
-    int bad = 0;
-    // step 0's inputs
-    if (diag && ti == 0) dfast_chol4(v, sc.lkk[0], sc.rd[0], bad);
-    if (lthr && tj == 0 && ti > 0)
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) sc.col[0][ti][a][b] = v[a][b];
-    if (tid == 0) sc.bad = 0;
-    __syncthreads();
-    for (int kg = 0; kg < 16; ++kg) {
-        const int bf = kg & 1, nb = bf ^ 1;
-        double lk[4][4], rd[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            rd[m] = sc.rd[bf][m];
-#pragma unroll
-            for (int n = 0; n < 4; ++n) lk[m][n] = sc.lkk[bf][m][n];
-        }
-        if (lthr) {
-            if (tj == kg && ti > kg) {
-                dfast_solve_rows(v, lk, rd);  // final L_{i,kg}
-            } else if (tj > kg) {
-                double li[4][4], lj[4][4];
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        li[a][b] = sc.col[bf][ti][a][b];
-                        lj[a][b] = sc.col[bf][tj][a][b];
-                    }
-                dfast_solve_rows(li, lk, rd);
-                dfast_solve_rows(lj, lk, rd);
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        double s = v[a][b];
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) s -= li[a][m] * lj[b][m];
-                        v[a][b] = s;
-                    }
-            }
-            if (diag && ti == kg) {  // X_kk = L_kk^-1
-                dfast_solve_cols(xd, lk, rd);
-            }
-            if (diag && ti > kg) {  // Y_ii is the identity until step i: nothing to update
-            }
-        } else {
-            // X tile (ti, tj), ti > tj
-            if (ti == kg) {
-                dfast_solve_cols(v, lk, rd);  // final X_{kg,j}
-            } else if (ti > kg && tj <= kg) {
-                double li[4][4], xk[4][4];
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        li[a][b] = sc.col[bf][ti][a][b];
-                        xk[a][b] = tj == kg ? (a == b ? 1.0 : 0.0) : sc.row[bf][tj][a][b];
-                    }
-                dfast_solve_rows(li, lk, rd);
-                dfast_solve_cols(xk, lk, rd);
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        double s = v[a][b];
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) s -= li[a][m] * xk[m][b];
-                        v[a][b] = s;
-                    }
-            }
-        }
-        if (kg + 1 < 16) {
-            // publish step kg+1's inputs
-            if (lthr && tj == kg + 1 && ti > kg + 1)
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) sc.col[nb][ti][a][b] = v[a][b];
-            if (!lthr && ti == kg + 1)
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) sc.row[nb][tj][a][b] = v[a][b];
-            if (diag && ti == kg + 1) dfast_chol4(v, sc.lkk[nb], sc.rd[nb], bad);
-        }
-        __syncthreads();
-    }
-    if (bad) sc.bad = 1;
-    __syncthreads();
-    if (sc.bad) return 1;
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int r = 4 * ti + a, q = 4 * tj + b;
-            if (lthr) {
-                // the block's strict upper part holds left-looking GEMM garbage: exact zeros
-                if (r < jb && q < jb) A[(int64_t)r * ld + q] = q <= r ? v[a][b] : 0.0;
-                if (!diag && q < jb && r < jb) A[(int64_t)q * ld + r] = 0.0;  // transposed (upper) tile
-                if (diag) out[r * out_ld + q] = (r < jb && q <= r) ? xd[a][b] : 0.0;
-                else out[q * out_ld + r] = 0.0;  // upper tile of X
-            } else {
-                out[r * out_ld + q] = (r < jb && q < jb) ? v[a][b] : 0.0;
-            }
-        }
-    if (zero_above) {  // second half of a 128-wide block column (see diag64_block_sc)
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int r = 4 * ty + a, q = 4 * tx + b;
-                if (q < jb) A[(int64_t)(r - kDiagNb) * ld + q] = 0.0;
-            }
-    }
-    return 0;
-}
-
-__device__ __forceinline__ int diag64_fast(double* A, int64_t ld, int jb, double* out, int zero_above,
-                                           int out_ld = kDiagNb) {
-    __shared__ DiagFastScratch sc;
-    return diag64_fast_sc(sc, A, ld, jb, out, zero_above, out_ld);
-}
-
 }  // namespace dgb

@@ -1,0 +1,191 @@
+// diag_tc.cuh — Cholesky + inverse of one 64x64 diagonal block in shared memory, with the
+// serial part on one warp and the rest on the FP64 tensor pipe (DMMA m8n8k4).
+//
+// The register-blocked factorization (diag_block.cuh) spends ~3500 cycles per 4-column
+// step: every warp runs a long dependent instruction stream for its 4x4 tiles. Here the
+// 64 columns are taken 8 at a time (left-looking, proj/src/linalg.cpp:74-93 reordered):
+//   (a) panel update  A[k0:, k0:k0+8] -= L[k0:, :k0] L[k0:k0+8, :k0]^T    one 8x8 DMMA tile
+//       per warp, K = k0;
+//   (b) panel factor  the 8 columns of rows k0..63 by ONE warp (two rows per lane):
+//       per column one rsqrt on the pivot's lane, a broadcast, and the rank-1 update of the
+//       panel's remaining columns through shuffles -- no barriers inside the panel;
+// then X = L^-1 by block forward substitution: the eight 8x8 diagonal inverses in
+// parallel (one warp each), then block rows 1..7 in turn, each X_ij = -X_ii sum L_im X_mj
+// on the DMMA pipe. Same interface and results (to rounding) as diag64_block.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "diag_block.cuh"
+#include "gemm_tile.cuh"
+
+namespace dgb {
+
+constexpr int kTcS = 68;
+#ifdef DIAG_TC_PROFILE
+__device__ long long g_tc_prof[16];
+#define TC_MARK(i)                                                        \
+    do {                                                                  \
+        if (threadIdx.x == 0 && blockIdx.x == 0) g_tc_prof[i] = clock64(); \
+    } while (0)
+#else
+#define TC_MARK(i) \
+    do {           \
+    } while (0)
+#endif  // shared stride (doubles): 4 mod 16, conflict-free DMMA fragment loads
+
+struct DiagTcScratch {
+    double a[64 * kTcS];  // the block, then L
+    double x[64 * kTcS];  // X = L^-1
+    double t[8][64];      // per-warp staging of an 8x8 product
+    int bad;
+};
+
+// 8x8 DMMA tile C (+)= A_rows[r0.., k..] * B_rows[n0.., k..]^T over k in [0, K), both
+// operands row-major in shared memory with stride kTcS. acc: lane holds C[lane/4][2(lane%4)+{0,1}].
+__device__ __forceinline__ void tc_tile(double (&acc)[2], const double* A, int r0, const double* B, int n0, int K,
+                                        int lane) {
+    const int fr = lane >> 2, fk = lane & 3;
+    double e[2] = {0.0, 0.0}, o[2] = {0.0, 0.0};  // two chains: halve the dependent DMMA latency
+    int k = 0;
+    for (; k + 8 <= K; k += 8) {
+        tile::dmma(e, A[(r0 + fr) * kTcS + k + fk], B[(n0 + fr) * kTcS + k + fk]);
+        tile::dmma(o, A[(r0 + fr) * kTcS + k + 4 + fk], B[(n0 + fr) * kTcS + k + 4 + fk]);
+    }
+    if (k < K) tile::dmma(e, A[(r0 + fr) * kTcS + k + fk], B[(n0 + fr) * kTcS + k + fk]);
+    acc[0] = e[0] + o[0];
+    acc[1] = e[1] + o[1];
+}
+
+__device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_t ld, int jb, double* out,
+                                            int zero_above, int out_ld) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int fr = lane >> 2, fk = lane & 3;
+    constexpr unsigned kAll = 0xffffffffu;
+    double* sa = sc.a;
+    double* sx = sc.x;
+    // load the lower part; rows/cols past jb are the identity (a valid 64x64 factorization)
+    for (int e = tid; e < 64 * 64; e += 256) {
+        const int r = e >> 6, q = e & 63;
+        sa[r * kTcS + q] = (r < jb && q <= r) ? __ldcg(A + (int64_t)r * ld + q) : (r == q ? 1.0 : 0.0);
+    }
+    if (tid == 0) sc.bad = 0;
+    TC_MARK(0);
+    __syncthreads();
+    TC_MARK(1);
+    for (int p = 0; p < 8; ++p) {
+        const int k0 = 8 * p;
+        if (p > 0 && warp < 8 - p) {  // (a) row tile i = p + warp of the panel
+            const int i = p + warp;
+            double acc[2];
+            tc_tile(acc, sa, 8 * i, sa, k0, k0, lane);
+            sa[(8 * i + fr) * kTcS + k0 + 2 * fk] -= acc[0];
+            sa[(8 * i + fr) * kTcS + k0 + 2 * fk + 1] -= acc[1];
+        }
+        __syncthreads();
+        if (p == 3) TC_MARK(2);
+        if (warp == 0) {  // (b) the panel: rows k0 + lane and k0 + 32 + lane
+            const int r1 = k0 + lane, r2 = k0 + 32 + lane;
+            const bool v1 = r1 < 64, v2 = r2 < 64;
+            double pa[8], pb[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                pa[j] = v1 ? sa[r1 * kTcS + k0 + j] : 0.0;
+                pb[j] = v2 ? sa[r2 * kTcS + k0 + j] : 0.0;
+            }
+            int bad = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                double rl = 0.0;
+                if (lane == c) {
+                    const double piv = pa[c];
+                    if (!(piv > 0.0) || !isfinite(piv)) bad = 1;  // proj/src/linalg.cpp:82-84
+                    rl = rsqrt(piv);
+                    pa[c] = piv * rl;
+                }
+                rl = __shfl_sync(kAll, rl, c);
+                if (lane > c) pa[c] *= rl;
+                pb[c] *= rl;
+#pragma unroll
+                for (int j = c + 1; j < 8; ++j) {
+                    const double lj = __shfl_sync(kAll, pa[c], j);  // L[k0+j][k0+c]
+                    pa[j] -= pa[c] * lj;
+                    pb[j] -= pb[c] * lj;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (v1) sa[r1 * kTcS + k0 + j] = (lane >= j) ? pa[j] : 0.0;
+                if (v2) sa[r2 * kTcS + k0 + j] = pb[j];
+            }
+            bad = __any_sync(kAll, bad);
+            if (lane == 0 && bad) sc.bad = 1;
+        }
+        if (p == 3) TC_MARK(3);
+        __syncthreads();
+    }
+    TC_MARK(4);
+    if (sc.bad) return 1;
+    // X = L^-1. Diagonal blocks: warp w inverts L_ww by columns (lane j < 8: column j).
+    {
+        const int b0 = 8 * warp;
+        if (lane < 8) {
+            const int j = lane;
+            double xcol[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double s = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+                for (int k = 0; k < i; ++k) s -= sa[(b0 + i) * kTcS + b0 + k] * xcol[k];
+                xcol[i] = s / sa[(b0 + i) * kTcS + b0 + i];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) sx[(b0 + i) * kTcS + b0 + j] = (i >= j) ? xcol[i] : 0.0;
+        }
+        // the strict upper blocks of X are zero
+        for (int e = lane; e < 8 * 64; e += 32) {
+            const int r = b0 + (e >> 6), q = e & 63;
+            if (q >= b0 + 8) sx[r * kTcS + q] = 0.0;
+        }
+    }
+    __syncthreads();
+    TC_MARK(5);
+    // block rows i = 1..7: X_ij = -X_ii sum_{m=j}^{i-1} L_im X_mj, j < i (tile j by warp j)
+    for (int i = 1; i < 8; ++i) {
+        if (warp < i) {
+            const int j = warp;
+            // T = sum_m L_im X_mj: rows 8i.. of L times columns 8j.. of X, K over 8j..8i
+            const double* Lr = sa + 8 * i * kTcS;
+            double te[2] = {0.0, 0.0}, to[2] = {0.0, 0.0};
+            for (int k = 8 * j; k < 8 * i; k += 8) {
+                // A(m,k) = L[8i+m][k], B(k,n) = X[k][8j+n]
+                tile::dmma(te, Lr[fr * kTcS + k + fk], sx[(k + fk) * kTcS + 8 * j + fr]);
+                tile::dmma(to, Lr[fr * kTcS + k + 4 + fk], sx[(k + 4 + fk) * kTcS + 8 * j + fr]);
+            }
+            double* st = sc.t[warp];
+            st[fr * 8 + 2 * fk] = te[0] + to[0];
+            st[fr * 8 + 2 * fk + 1] = te[1] + to[1];
+            __syncwarp();
+            // X_ij = -X_ii T: A(m,k) = X[8i+m][8i+k], B(k,n) = T[k][n]
+            double xe[2] = {0.0, 0.0};
+            tile::dmma(xe, sx[(8 * i + fr) * kTcS + 8 * i + fk], st[fk * 8 + fr]);
+            tile::dmma(xe, sx[(8 * i + fr) * kTcS + 8 * i + 4 + fk], st[(4 + fk) * 8 + fr]);
+            sx[(8 * i + fr) * kTcS + 8 * j + 2 * fk] = -xe[0];
+            sx[(8 * i + fr) * kTcS + 8 * j + 2 * fk + 1] = -xe[1];
+        }
+        __syncthreads();
+    }
+    TC_MARK(6);
+    // store L (exact zeros above the diagonal: the left-looking GEMM's garbage) and X
+    for (int e = tid; e < 64 * 64; e += 256) {
+        const int r = e >> 6, q = e & 63;
+        if (r < jb && q < jb) A[(int64_t)r * ld + q] = q <= r ? sa[r * kTcS + q] : 0.0;
+        out[r * out_ld + q] = (r < jb && q < jb && q <= r) ? sx[r * kTcS + q] : 0.0;
+        if (zero_above && q < jb) A[(int64_t)(r - kDiagNb) * ld + q] = 0.0;
+    }
+    TC_MARK(7);
+    return 0;
+}
+
+}  // namespace dgb

@@ -6,6 +6,7 @@
 #include "gemm_f64.cuh"
 #include "gemm_tile.cuh"
 #include "diag_block.cuh"
+#include "diag_tc.cuh"
 #include "kernels.cuh"
 
 namespace dgb {
@@ -239,17 +240,19 @@ constexpr int kNb = kDiagNb;
 
 // MINB 2: <= 128 registers (spills a little) so a diagonal-block CTA can share its SM with
 // a GEMM CTA of another group; MINB 1: 190 registers, no spills
-template <int MINB, bool FAST>
+template <int MINB, bool TC>
 __global__ void __launch_bounds__(256, MINB) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
                                                             const int* mask, int* status, int* active,
                                                             double* inv_base, int zero_above) {
+    extern __shared__ __align__(16) double dyn_smem[];
     const int c = blockIdx.x;
     const bool run = (!mask || mask[c]) && status[c] == 0;
     if (threadIdx.x == 0) active[c] = run ? 1 : 0;
     if (!run) return;
     double* Ab = Am[c] + (int64_t)j0 * ld + j0;
     double* out = inv_base + (int64_t)c * kNb * kNb;
-    const int bad = FAST ? diag64_fast(Ab, ld, jb, out, zero_above) : diag64_block(Ab, ld, jb, out, zero_above);
+    const int bad = TC ? diag64_tc_sc(*reinterpret_cast<DiagTcScratch*>(dyn_smem), Ab, ld, jb, out, zero_above, kNb)
+                       : diag64_block(Ab, ld, jb, out, zero_above);
     if (bad && threadIdx.x == 0) {
         status[c] = 1;
         active[c] = 0;
@@ -642,16 +645,23 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     };
     // factor the 64-wide diagonal block at (c0, c0) and solve the rows below it (in place)
     auto factor_and_solve = [&](int c0, int n, int zero_above) {
-        // DIAM_B200_DIAG (read per call): "fast" = one barrier per step (diag64_fast), else
-        // the two-barrier register-blocked version. Both take ~34 us per 64x64 block on a
-        // B200: the cost is each warp's dependent instruction stream (~300 instructions per
-        // block step at ~9-15 cycles each), not the barriers
+        // the diagonal block: panel-by-warp + DMMA (diag_tc.cuh, default: 23 vs 27 us per
+        // block, 4.5% off the POTRF), or DIAM_B200_DIAG=block (read per call) for the
+        // register-blocked version (diag_block.cuh)
         const char* de = std::getenv("DIAM_B200_DIAG");
-        const bool fast = de && std::string(de) == "fast";
-        if (fast)
-            potrf_diag_kernel<1, true><<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
-        else
+        const bool tc = !(de && std::string(de) == "block");
+        if (tc) {
+            static bool attr = false;
+            if (!attr) {
+                DGB_CUDA(cudaFuncSetAttribute(potrf_diag_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)sizeof(DiagTcScratch)));
+                attr = true;
+            }
+            potrf_diag_kernel<1, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(A, ld, c0, n, mask, status, active,
+                                                                                  w.inv, zero_above);
+        } else {
             potrf_diag_kernel<2, false><<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
+        }
         DGB_LAUNCH_CHECK();
         count_launch();
         const int rest = rows - c0 - n;

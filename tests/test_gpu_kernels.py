@@ -141,15 +141,15 @@ def oracle_chol(m):
     return st, out
 
 
-@pytest.mark.parametrize("mode", ["blocked", "blocked+fastdiag", "dag", "cluster"])
+@pytest.mark.parametrize("mode", ["blocked", "blocked+regdiag", "dag", "cluster"])
 @pytest.mark.parametrize("d", [1, 5, 64, 65, 130, 257, 520])
 def test_potrf_batched_vs_oracle(lib, monkeypatch, d, mode):
-    # every factorization path: the launch-per-phase blocked POTRF (default; also with the
-    # one-barrier-per-step diagonal kernel), the task-graph persistent kernel
-    # (potrf_dag.cu), the 2-CTA-cluster kernel
+    # every factorization path: the launch-per-phase blocked POTRF (default, with the
+    # DMMA diagonal block of diag_tc.cuh; also with the register-blocked one), the
+    # task-graph persistent kernel (potrf_dag.cu), the 2-CTA-cluster kernel
     monkeypatch.setenv("DIAM_B200_POTRF", mode.split("+")[0])
-    if mode.endswith("fastdiag"):
-        monkeypatch.setenv("DIAM_B200_DIAG", "fast")
+    if mode.endswith("regdiag"):
+        monkeypatch.setenv("DIAM_B200_DIAG", "block")
     rng = np.random.default_rng(d)
     batch = 3
     ld = (d + 7) // 8 * 8

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <vector>
 
+#define DIAG_TC_PROFILE
 #include "../paper_1506_05741_b200/csrc/linalg.cu"
 
 __global__ void empty_kernel() {}
@@ -350,10 +351,18 @@ int main() {
            "diag64 (minb 2)");
     timeit([&] { potrf_diag_kernel<1, false><<<chains, 256>>>(Ap, ld, 0, 64, nullptr, status, active, inv, 0); },
            "diag64 (minb 1)");
-    timeit([&] { potrf_diag_kernel<1, true><<<chains, 256>>>(Ap, ld, 0, 64, nullptr, status, active, inv, 0); },
-           "diag64 FAST (minb 1)");
-    timeit([&] { potrf_diag_kernel<2, true><<<chains, 256>>>(Ap, ld, 0, 64, nullptr, status, active, inv, 0); },
-           "diag64 FAST (minb 2)");
+    cudaFuncSetAttribute(potrf_diag_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(DiagTcScratch));
+    timeit([&] { potrf_diag_kernel<1, true><<<chains, 256, sizeof(DiagTcScratch)>>>(Ap, ld, 0, 64, nullptr, status,
+                                                                                     active, inv, 0); },
+           "diag64 TC");
+    {
+        long long pr[16];
+        cudaMemcpyFromSymbol(pr, dgb::g_tc_prof, sizeof pr);
+        printf("TC phases (cycles): load %lld, panels 0-2 + (a)3 %lld, (b)3 %lld, panels 4-7 %lld, diag inv %lld, "
+               "block rows %lld, store %lld\n", pr[1] - pr[0], pr[2] - pr[1], pr[3] - pr[2], pr[4] - pr[3],
+               pr[5] - pr[4], pr[6] - pr[5], pr[7] - pr[6]);
+    }
     timeit([&] { diag_exp_kernel<0><<<chains, 256>>>(Ap, ld, 64, status, inv); }, "exp full");
     auto cyc = [&](auto launch, const char* name) {
         long long* cy;
