@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include <nvtx3/nvToolsExt.h>
@@ -105,11 +106,24 @@ Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shar
     DGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     DGB_CUDA(cudaEventCreateWithFlags(&main_ev_, cudaEventDisableTiming));
     DeferAllocSync defer;
+    static const bool tinit = std::getenv("DIAM_B200_INIT_TIMING") != nullptr;  // phases to stderr
+    auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!tinit) return;
+        DGB_CUDA(cudaDeviceSynchronize());
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "engine init %-14s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    };
     upload_target();
+    mark("upload_target");
     const int ng = plan_memory();
+    mark("plan_memory");
     init_chains();
+    mark("init_chains");
     make_groups(ng);
     DGB_CUDA(cudaStreamSynchronize(0));
+    mark("make_groups");
 }
 
 int Engine::plan_memory() {
