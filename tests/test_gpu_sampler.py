@@ -289,3 +289,20 @@ def test_nccl_sharded_path_single_rank(b200, tmp_path):
     assert np.array_equal(r0.history("psrf"), r1.history("psrf"), equal_nan=True)
     for p in range(4):
         assert np.array_equal(r0.chain_history(p, "beta"), r1.chain_history(p, "beta"))
+
+
+def test_engine_error_paths(b200):
+    """Errors surface as diam statuses with messages, never as crashes: unknown kernel,
+    a run that cannot fit in device memory (the memory planner refuses it up front)."""
+    from paper_1506_05741_b200.abi import DiamError
+    t = b200.target_build("pi1", 64, 2)
+    with pytest.raises(DiamError) as e:
+        b200.sample(t, kernel="nope", chains=2, max_batches=1, n_lag=8)
+    assert e.value.status == 1
+    big = b200.target_build("pi1", 1024, 2)
+    with pytest.raises(DiamError) as e:
+        b200.sample(big, kernel="diam", chains=200000, max_batches=1, n_lag=512, n0=0)
+    assert "does not fit in device memory" in e.value.message
+    # the library stays usable afterwards
+    r = b200.sample(t, kernel="diam", chains=2, max_batches=1, n_lag=8, n0=0)
+    assert r.batches == 1
