@@ -1,0 +1,51 @@
+"""Kernel-class shares of one steady-state batch from an `ncu --metrics
+gpu__time_duration.sum` launch list (cold-cache, serialised), next to bench.py's own
+CUDA-event per-class times (`roofline.per_class_ms`, single stream).
+
+    python tools/launch_shares.py profiles/r01_launches_d1024.csv profiles/r01_bench_d1024.json
+"""
+import collections
+import csv
+import json
+import sys
+
+
+def cls(name, grid):
+    if "gemm_f64_kernel" in name:
+        gx, gy, gz = eval(grid)  # "(x, y, z)"
+        if ", 0, 0," in name:
+            return "syrk_moments"  # the only MN-major x MN-major GEMM
+        if gz == 1 and gy >= 8:
+            return "gemm_target"  # one (chains x n_lag) x d GEMM
+        if gz > 1 and gx == 16 and gy == 4:
+            return "trmm_noise"  # batched n_lag x d per chain
+        if gz == 1 and gy == 1:
+            return "gemv_state"
+        return "potrf"  # the factorization's update / TRSM GEMMs
+    for k in ("potrf_diag", "mh_window", "normals", "blend_cov", "mean_update", "trace_floor", "sum_chains"):
+        if k in name:
+            return "potrf" if k == "potrf_diag" else k
+    return "other"
+
+
+def main():
+    rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
+    h, rows = rows[0], rows[1:]
+    ki, gi, vi = h.index("Kernel Name"), h.index("Grid Size"), h.index("Metric Value")
+    starts = [i for i, r in enumerate(rows) if "normals_kernel" in r[ki]]
+    first = starts[4] if len(starts) > 4 else 0  # the second batch (4 windows per batch)
+    agg = collections.defaultdict(float)
+    for r in rows[first:]:
+        agg[cls(r[ki], r[gi])] += float(r[vi].replace(",", ""))
+    tot = sum(agg.values())
+    bench = json.load(open(sys.argv[2]))["roofline"]["per_class_ms"]
+    btot = sum(bench.values())
+    print("| class | ncu launch list share | bench CUDA-event share |")
+    print("|---|---:|---:|")
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1]):
+        b = bench.get(k)
+        print(f"| {k} | {100 * v / tot:.1f}% | " + (f"{100 * b / btot:.1f}% |" if b else "– |"))
+
+
+if __name__ == "__main__":
+    main()
