@@ -29,6 +29,10 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# before any CUDA context exists: 32 hardware queues for the engine's 2 streams per chain
+# group (libdiam.so sets the same default when it loads; see csrc/capi.cpp)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import statistics
 import subprocess
 import sys

@@ -130,8 +130,10 @@ int Engine::plan_memory() {
     // chain groups on separate streams overlap one group's latency-bound pieces (MH steps,
     // diagonal factorizations) with the others' GEMMs; small problems are launch-latency
     // bound and keep one stream (DIAM_B200_GROUPS overrides, 1 = a single stream)
-    // (d=1024, 64 chains: 1 group 33.7, 2: 32.1, 4: 30.8, 8: 30.4, 16: 35.2 ms per batch)
-    int ng = d_ < 256 ? 1 : (C_ >= 64 && d_ >= 512) ? 8 : (C_ >= 32 && d_ >= 512) ? 4 : (C_ >= 8 ? 2 : 1);
+    // (d=1024, 64 chains, each group on a low-priority steps stream and a high-priority
+    // refactor stream, 32 hardware queues: 4 groups 28.5, 8: 27.9, 12: 27.8, 16: 27.4,
+    // 24: 27.4, 32: 32.0 ms per batch; neutral at d=2040 / 4096)
+    int ng = d_ < 256 ? 1 : d_ >= 512 ? std::max(1, std::min(16, C_ / 4)) : (C_ >= 8 ? 2 : 1);
     const char* eg = std::getenv("DIAM_B200_GROUPS");
     if (eg) ng = std::max(1, std::min(C_, std::atoi(eg)));
 
@@ -181,7 +183,7 @@ int Engine::plan_memory() {
         bool found = false;
         for (int pass = 0; pass < 2 && !found; ++pass) {
             const bool pl = pass == 1;
-            const int groups = pl && !eg ? std::max(ng, std::min(8, C_)) : ng;
+            const int groups = pl && !eg ? std::min(8, C_) : ng;  // refactors take turns: 8 groups
             for (int c : divs) {
                 if (c < (pl ? 64 : 256)) break;
                 if (need(c, pl ? gmax(groups) : C_) <= budget) {
@@ -208,10 +210,16 @@ int Engine::plan_memory() {
 Engine::~Engine() {
     if (stream_) cudaStreamSynchronize(stream_);
     for (auto& g : groups_) {
+        if (g.sr && g.sr != g.s) {
+            cudaStreamSynchronize(g.sr);
+            cudaStreamDestroy(g.sr);
+        }
         if (g.s) {
             cudaStreamSynchronize(g.s);
             cudaStreamDestroy(g.s);
         }
+        if (g.ev_steps) cudaEventDestroy(g.ev_steps);
+        if (g.ev_ref) cudaEventDestroy(g.ev_ref);
         if (g.done) cudaEventDestroy(g.done);
         if (g.pool_ev) cudaEventDestroy(g.pool_ev);
         potrf_work_release(g.pw);
@@ -370,7 +378,23 @@ void Engine::make_groups(int n) {
         Group& g = groups_[i];
         g.off = (int)((int64_t)C_ * i / n);
         g.C = (int)((int64_t)C_ * (i + 1) / n) - g.off;
-        DGB_CUDA(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking));
+        {
+            // steps at the lowest priority, the refactorization at the highest
+            // (DIAM_B200_PRIO=0: one stream per group)
+            static const int prio = [] {
+                const char* e = std::getenv("DIAM_B200_PRIO");
+                return e ? std::atoi(e) : 1;
+            }();
+            int least = 0, greatest = 0;
+            DGB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            const int ps = prio == 1 ? least : (prio == 2 ? greatest : 0);
+            const int pr = prio == 1 ? greatest : (prio == 2 ? least : 0);
+            DGB_CUDA(cudaStreamCreateWithPriority(&g.s, cudaStreamNonBlocking, ps));
+            if (prio) DGB_CUDA(cudaStreamCreateWithPriority(&g.sr, cudaStreamNonBlocking, pr));
+            else g.sr = g.s;
+            DGB_CUDA(cudaEventCreateWithFlags(&g.ev_steps, cudaEventDisableTiming));
+            DGB_CUDA(cudaEventCreateWithFlags(&g.ev_ref, cudaEventDisableTiming));
+        }
         DGB_CUDA(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
         DGB_CUDA(cudaEventCreateWithFlags(&g.status_ev, cudaEventDisableTiming));
         DGB_CUDA(cudaEventCreateWithFlags(&g.pool_ev, cudaEventDisableTiming));
@@ -732,7 +756,11 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
 
 void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {
     const int C = g.C, o = g.off;
-    const cudaStream_t s = g.s;
+    const cudaStream_t s = g.sr;
+    if (g.sr != g.s) {  // the refactor stream continues after the window's steps
+        DGB_CUDA(cudaEventRecord(g.ev_steps, g.s));
+        DGB_CUDA(cudaStreamWaitEvent(g.sr, g.ev_steps, 0));
+    }
     if (p.refactor) {
         // blend -> covariance into the workspace factor, trace floor, POTRF (proposal.cpp:176-184).
         // pCN-form kernels append r = x - x_ref as row d: the factorization then also
@@ -815,7 +843,7 @@ bool Engine::tail_step(Group& g, const WindowPlan& p, Ladder& st) {
 
 void Engine::ladder_retry(Group& g, const WindowPlan& p, Ladder& st) {
     const int C = g.C, o = g.off;
-    const cudaStream_t s = g.s;
+    const cudaStream_t s = g.sr;
     const bool aug = k_.pcn_form();
     const double* ax = aug ? x_ + o * ld_ : nullptr;
     const double* axr = aug && k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
@@ -833,7 +861,7 @@ void Engine::ladder_retry(Group& g, const WindowPlan& p, Ladder& st) {
 
 void Engine::tail_finish(Group& g, const WindowPlan& p) {
     const int C = g.C, o = g.off;
-    const cudaStream_t s = g.s;
+    const cudaStream_t s = g.sr;
     const double infl = k_.noise_infl();
     if (p.refactor) {
         const bool aug = k_.pcn_form();
@@ -873,6 +901,10 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
     }
     // G x re-anchored at every boundary so the step recursion never drifts
     refresh_g(g.xp, g.gp, C, s);
+    if (g.sr != g.s) {  // the next window's steps follow the tail
+        DGB_CUDA(cudaEventRecord(g.ev_ref, g.sr));
+        DGB_CUDA(cudaStreamWaitEvent(g.s, g.ev_ref, 0));
+    }
 }
 
 void Engine::capture_chunk(const Group& g, int r0, int rows) {

@@ -95,6 +95,10 @@ private:
         PotrfWork pw{};
         cudaEvent_t status_ev = nullptr;  // POTRF statuses of the group's last window landed in h_status_
         cudaEvent_t pool_ev = nullptr;    // shared refactor workspace released (pool mode)
+        // refactorization + tail on their own high-priority stream: the latency-bound
+        // POTRF launches of one group are scheduled ahead of the other groups' GEMMs
+        cudaStream_t sr = nullptr;
+        cudaEvent_t ev_steps = nullptr, ev_ref = nullptr;
     };
     // host-side scalars of one lag window, identical for every chain
     struct WindowPlan {
