@@ -47,19 +47,30 @@ void keep_pool_resident() {
 // touch them. Later allocations synchronize at once.
 thread_local bool g_defer_alloc_sync = false;
 
-template <class T>
-T* dalloc(std::vector<void*>& list, size_t count) {
-    void* p = nullptr;
+template <class M, class T = double>
+T* dalloc_impl(M& mem, size_t count) {
     if (count == 0) count = 1;
+    const size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+    void* p = nullptr;
+    if (mem.arena && mem.used + bytes <= mem.size) {  // carve (the arena is zeroed once)
+        p = mem.arena + mem.used;
+        mem.used += bytes;
+        return static_cast<T*>(p);
+    }
     keep_pool_resident();
-    DGB_CUDA(cudaMallocAsync(&p, count * sizeof(T), 0));
-    DGB_CUDA(cudaMemsetAsync(p, 0, count * sizeof(T), 0));
+    DGB_CUDA(cudaMallocAsync(&p, bytes, 0));
+    DGB_CUDA(cudaMemsetAsync(p, 0, bytes, 0));
     if (!g_defer_alloc_sync) DGB_CUDA(cudaStreamSynchronize(0));
-    list.push_back(p);
+    mem.blocks.push_back(p);
     return static_cast<T*>(p);
 }
+template <class T, class M>
+T* dalloc(M& mem, size_t count) {
+    return dalloc_impl<M, T>(mem, count);
+}
 
-double** ptr_array(std::vector<void*>& list, double* base, int64_t stride, int n) {
+template <class M>
+double** ptr_array(M& list, double* base, int64_t stride, int n) {
     std::vector<double*> h(n);
     for (int i = 0; i < n; ++i) h[i] = base + stride * i;
     double** d = dalloc<double*>(list, n);
@@ -118,6 +129,17 @@ Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shar
     upload_target();
     mark("upload_target");
     const int ng = plan_memory();
+    {  // the arena: everything init_chains / make_groups allocate, plus slack
+        size_t bytes = arena_bytes_ + ((size_t)64 << 20);
+        bytes = (bytes + 255) & ~size_t(255);
+        keep_pool_resident();
+        void* p = nullptr;
+        DGB_CUDA(cudaMallocAsync(&p, bytes, 0));
+        DGB_CUDA(cudaMemsetAsync(p, 0, bytes, 0));
+        allocs_.blocks.push_back(p);
+        allocs_.arena = static_cast<char*>(p);
+        allocs_.size = bytes;
+    }
     mark("plan_memory");
     init_chains();
     mark("init_chains");
@@ -204,10 +226,18 @@ int Engine::plan_memory() {
     win_ = (int64_t)Lc_ * ld_;
     pool_ = pool && ng > 1;
     pool_n_ = pool_ ? gmax(ng) : 0;
+    arena_bytes_ = (size_t)need(lc, pool_ ? pool_n_ : C_);
     return ng;
 }
 
 Engine::~Engine() {
+    static const bool tinit = std::getenv("DIAM_B200_INIT_TIMING") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (tinit)
+            std::fprintf(stderr, "engine free %-14s %8.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    };
     if (stream_) cudaStreamSynchronize(stream_);
     for (auto& g : groups_) {
         if (g.sr && g.sr != g.s) {
@@ -224,8 +254,10 @@ Engine::~Engine() {
         if (g.pool_ev) cudaEventDestroy(g.pool_ev);
         potrf_work_release(g.pw);
     }
-    for (void* p : allocs_) cudaFreeAsync(p, 0);
+    mark("streams");
+    for (void* p : allocs_.blocks) cudaFreeAsync(p, 0);
     cudaStreamSynchronize(0);
+    mark("buffers");
     for (auto& e : event_pool_) cudaEventDestroy(e);
     for (auto& pe : pending_) {
         cudaEventDestroy(pe.a);
@@ -237,6 +269,7 @@ Engine::~Engine() {
     if (h_flags_) cudaFreeHost(h_flags_);
     if (h_stats_) cudaFreeHost(h_stats_);
     if (stream_) cudaStreamDestroy(stream_);
+    mark("done");
 }
 
 void Engine::upload_target() {

@@ -168,6 +168,7 @@ private:
     int Lc_ = 0;
     bool pool_ = false;
     int pool_n_ = 0;
+    size_t arena_bytes_ = 0;  // device bytes the plan needs after the target upload
     cudaEvent_t pool_last_ = nullptr;  // latest release of the shared workspace
     int64_t ld_ = 0, win_ = 0, mat_ = 0;
     int64_t fmat_ = 0;  // factor stride: d rows + the augmented row r = x - x_ref
@@ -177,7 +178,15 @@ private:
     std::vector<Group> groups_;
 
     // device memory
-    std::vector<void*> allocs_;
+    // device memory: one arena per engine sized by the memory plan (a single block that
+    // the stream-ordered pool hands to the next engine of the same shape, instead of
+    // dozens of buffers that fragment it), plus individual blocks for what does not fit
+    struct DevMem {
+        std::vector<void*> blocks;
+        char* arena = nullptr;
+        size_t size = 0, used = 0;
+    };
+    DevMem allocs_;
     double* G_ = nullptr;      // d x ld
     double* Ct_ = nullptr;     // d x d analytic covariance
     double* inv_eig_ = nullptr;
