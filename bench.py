@@ -343,6 +343,10 @@ def impl_b200(args):
         tt = torch.tensor([wall], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         wall = float(tt.item())
+    bsec = r.history("batch_seconds")
+    log(f"e2e: {wall * 1e3:.1f} ms wall, batches {bsec.sum() * 1e3:.1f} ms "
+        f"(first {bsec[0] * 1e3:.1f}, median {float(sorted(bsec)[len(bsec) // 2]) * 1e3:.1f}), "
+        f"fixed costs {(wall - bsec.sum()) * 1e3:.1f} ms")
     e2e = r.total_samples / wall
     h2d = (d * d * 8 * 2 + 4 * d * 8) / args.steps  # precision + analytic covariance + vectors, once per run
     d2h = (mean.nbytes + cov.nbytes) / args.steps + chains * M * 16 + 24

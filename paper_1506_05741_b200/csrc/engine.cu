@@ -8,6 +8,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -78,6 +80,38 @@ double** ptr_array(M& list, double* base, int64_t stride, int n) {
     DGB_CUDA(cudaMemcpyAsync(d, h.data(), n * sizeof(double*), cudaMemcpyHostToDevice, 0));
     if (!g_defer_alloc_sync) DGB_CUDA(cudaStreamSynchronize(0));
     return d;
+}
+
+// Pinned host buffers are kept for the process and handed from engine to engine:
+// cudaMallocHost / cudaFreeHost per run cost milliseconds to hundreds of milliseconds
+// (page pinning, an implicit device synchronization) at random.
+std::mutex g_pinned_mu;
+std::multimap<size_t, void*> g_pinned_free;
+std::map<void*, size_t> g_pinned_size;
+
+void* pinned_acquire(size_t bytes, bool zero = true) {
+    bytes = (bytes + 4095) & ~size_t(4095);
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        auto it = g_pinned_free.lower_bound(bytes);
+        if (it != g_pinned_free.end()) {
+            void* p = it->second;
+            g_pinned_free.erase(it);
+            if (zero) std::memset(p, 0, bytes);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    DGB_CUDA(cudaMallocHost(&p, bytes));
+    std::memset(p, 0, bytes);
+    g_pinned_size[p] = bytes;
+    return p;
+}
+
+void pinned_release(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.emplace(g_pinned_size[p], p);
 }
 
 struct DeferAllocSync {
@@ -266,8 +300,8 @@ Engine::~Engine() {
     if (main_ev_) cudaEventDestroy(main_ev_);
     for (auto& g : groups_)
         if (g.status_ev) cudaEventDestroy(g.status_ev);
-    if (h_flags_) cudaFreeHost(h_flags_);
-    if (h_stats_) cudaFreeHost(h_stats_);
+    pinned_release(h_flags_);
+    pinned_release(h_stats_);
     if (stream_) cudaStreamDestroy(stream_);
     mark("done");
 }
@@ -303,7 +337,7 @@ void Engine::upload_target() {
     tmean_ = dalloc<double>(A, ld_);
     DGB_CUDA(cudaMemcpy(tmean_, tgt_.mean.data(), d_ * 8, cudaMemcpyHostToDevice));
     dstats_ = dalloc<double>(A, 4);
-    DGB_CUDA(cudaMallocHost(&h_stats_, 4 * sizeof(double)));
+    h_stats_ = static_cast<double*>(pinned_acquire(4 * sizeof(double)));
     proj_ = dalloc<double>(A, 2 * ld_);
     DGB_CUDA(cudaMemcpy(proj_, pj.data(), 2 * ld_ * 8, cudaMemcpyHostToDevice));
     Gp_ = ptr_array(A, G_, 0, 1);
@@ -339,7 +373,7 @@ void Engine::init_chains() {
     try_ = dalloc<int>(A, C);
     usable_ = dalloc<int>(A, C);
     mask_ = dalloc<int>(A, C);
-    DGB_CUDA(cudaMallocHost(&h_flags_, 3 * (size_t)C * sizeof(int)));
+    h_flags_ = static_cast<int*>(pinned_acquire(3 * (size_t)C * sizeof(int)));
     Sg_ = dalloc<double>(A, mat_);
     mg_ = dalloc<double>(A, ld_);
     Ssum_ = dalloc<double>(A, mat_ + ld_);
@@ -1223,17 +1257,29 @@ RunResult Engine::build_result(const std::string& reason, double wall) {  // run
     r.batch_seconds = batch_seconds_;
     r.stop_reason = reason;
     r.accumulated_samples = cnt_g_;
-    std::vector<double> sg(mat_), mg(ld_);
-    DGB_CUDA(cudaMemcpyAsync(sg.data(), Sg_, mat_ * 8, cudaMemcpyDeviceToHost, stream_));
-    DGB_CUDA(cudaMemcpyAsync(mg.data(), mg_, ld_ * 8, cudaMemcpyDeviceToHost, stream_));
-    DGB_CUDA(cudaStreamSynchronize(stream_));
-    r.global_mean.assign(mg.begin(), mg.begin() + d_);
+    // moments through a pinned staging buffer (a pageable d2h of d^2 doubles plus the
+    // element-wise mirror cost ~10 ms at d=1024); the result matrix is allocated while
+    // the copy runs
+    double* hs = static_cast<double*>(pinned_acquire((size_t)(mat_ + ld_) * 8, false));
+    const double* sg = hs;
+    const double* mg = hs + mat_;
+    DGB_CUDA(cudaMemcpyAsync(hs, Sg_, mat_ * 8, cudaMemcpyDeviceToHost, stream_));
+    DGB_CUDA(cudaMemcpyAsync(hs + mat_, mg_, ld_ * 8, cudaMemcpyDeviceToHost, stream_));
     r.global_cov = Mat(d_, d_);
-    for (int i = 0; i < d_; ++i)
-        for (int j = 0; j <= i; ++j) {
-            const double v = sg[(size_t)i * ld_ + j] - mg[i] * mg[j];  // covariance(), moments.cpp:90-101
-            r.global_cov(i, j) = r.global_cov(j, i) = v;
+    DGB_CUDA(cudaStreamSynchronize(stream_));
+    r.global_mean.assign(mg, mg + d_);
+    // covariance(), moments.cpp:90-101: lower triangle of S - m m^T, mirrored by 64x64 tiles
+    constexpr int kT = 64;
+    double* cv = r.global_cov.a.data();
+    for (int i0 = 0; i0 < d_; i0 += kT)
+        for (int j0 = 0; j0 <= i0; j0 += kT) {
+            const int i1 = std::min(d_, i0 + kT), j1 = std::min(d_, j0 + kT);
+            for (int i = i0; i < i1; ++i)
+                for (int j = j0; j < std::min(j1, i + 1); ++j) cv[(size_t)i * d_ + j] = sg[(size_t)i * ld_ + j] - mg[i] * mg[j];
+            for (int j = j0; j < j1; ++j)
+                for (int i = std::max(i0, j + 1); i < i1; ++i) cv[(size_t)j * d_ + i] = cv[(size_t)i * d_ + j];
         }
+    pinned_release(hs);
     r.final_cov_error = cov_hist_.empty() ? NAN : cov_hist_.back();
     r.final_mean_error = mean_hist_.empty() ? NAN : mean_hist_.back();
     r.final_max_psrf = psrf_hist_.empty() ? NAN : psrf_hist_.back();

@@ -18,4 +18,9 @@ for i in range(6):
     t0 = time.perf_counter()
     r = lib.sample(t, **bench.run_options(cfg, 64, max_batches=0))
     print("diam_sample, 0 batches:", round((time.perf_counter() - t0) * 1e3, 2), "ms", flush=True)
+for i in range(3):
+    t0 = time.perf_counter()
+    r = lib.sample(t, **bench.run_options(cfg, 64, max_batches=4))
+    print("diam_sample, 4 batches:", round((time.perf_counter() - t0) * 1e3, 2), "ms; batches",
+          [round(x * 1e3, 2) for x in r.history("batch_seconds")], flush=True)
 os.unlink(path)
