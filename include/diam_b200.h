@@ -86,7 +86,8 @@ diam_status diamx_capture_copy(const diamx_engine* e, int64_t chain, const char*
 diam_status diamx_draws(int kind, double* d_out_f64, uint64_t* d_out_u64, int64_t n, uint64_t seed,
                         uint64_t stream_index, const char* purpose, uint64_t start, void* stream);
 /* C = alpha*A(op)B(op) + beta*C, row-major FP64 on the DMMA GEMM;
- * a_kmajor: A(m,k)=A[m*lda+k] else A[k*lda+m]; b_kmajor: B(k,n)=B[n*ldb+k] else B[k*ldb+n] */
+ * a_kmajor: A(m,k)=A[m*lda+k] else A[k*lda+m]; b_kmajor: B(k,n)=B[n*ldb+k] else B[k*ldb+n];
+ * stream-ordered (returns without waiting for the kernel) */
 diam_status diamx_gemm(const double* d_a, const double* d_b, double* d_c, int m, int n, int k,
                        int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor, double alpha,
                        double beta, int tri_b_lower, int tri_c_lower, void* stream);

@@ -217,7 +217,7 @@ int Engine::plan_memory() {
         if (!cfg_.checkpoint_path.empty()) n += (double)C_ * mat_;  // cumulative S
         n += 2.0 * mat_ + 3.0 * ld_;              // global snapshot, reduction buffer
         n += 3.0 * M * C_ * Lw_;                  // per-batch traces
-        n += 16.0 * C_ * ld_ + 4096.0 * C_;       // chain vectors, POTRF inverse blocks
+        n += 16.0 * C_ * ld_ + 16400.0 * C_;      // chain vectors, POTRF inverse blocks
         n += (double)potrf_dag_bytes(d_, C_) / 8;  // task-graph POTRF inverse tiles
         return 8.0 * n;
     };
@@ -479,8 +479,9 @@ void Engine::make_groups(int n) {
         g.Xib = ptr_array(A, Xi_ + g.off * win_, 0, 1);
         g.Hb = ptr_array(A, H_ + g.off * win_, 0, 1);
         // per-group inverse-block scratch (+ int active[C] tail): groups factor concurrently
-        g.pw.inv = dalloc<double>(A, (size_t)g.C * 64 * 64 + g.C);
+        g.pw.inv = dalloc<double>(A, potrf_work_doubles(g.C));
         g.pw.inv_ptrs = ptr_array(A, g.pw.inv, 64 * 64, g.C);
+        g.pw.inv128_ptrs = ptr_array(A, g.pw.inv, 128 * 128, g.C);
         // task-graph POTRF: the groups refactor at about the same time, so each gets its
         // share of the SMs as persistent workers
         g.pw.workers = std::max(8, 2 * ((kNumSMs + n - 1) / n));  // two resident per SM

@@ -58,6 +58,10 @@ void dispatch_shape(const GemmBatch& g, int batch, cudaStream_t stream, GemmShap
         const char* e = std::getenv("DIAM_B200_GEMM_CFG");
         return e ? std::atoi(e) : 2;
     }();
+    if (shape == GemmShape::Square) {
+        launch<Cfg<128, 128, 16, 4, AK, BKM>, AK, BKM>(g, batch, stream);
+        return;
+    }
     if (cfg == 2) {
         launch<Cfg<128, 64, 32, 2, AK, BKM, 4, 2, 2>, AK, BKM>(g, batch, stream);
         return;

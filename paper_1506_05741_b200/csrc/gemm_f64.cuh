@@ -46,7 +46,10 @@ struct GemmBatch {
     int tri_c_lower;           // compute/store only n <= m
 };
 
-enum class GemmShape { Big, Narrow };
+// Big / Narrow: the tile configuration DIAM_B200_GEMM_CFG selects; Square: 128x128 tiles
+// always (one column tile per 128 columns: in-place products whose tile reads columns
+// another tile of the same row block writes)
+enum class GemmShape { Big, Narrow, Square };
 
 // Launch the batched GEMM on `stream`. Layout flags select the template instance.
 void gemm_f64(const GemmBatch& g, int batch, bool a_kmajor, bool b_kmajor, cudaStream_t stream,

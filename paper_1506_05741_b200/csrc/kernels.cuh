@@ -111,11 +111,14 @@ void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr
 // status[c] = 0 ok, 1 not positive definite. Only chains with mask[c] != 0.
 struct DagState;
 struct PotrfWork {
-    double* inv;  // chains x 64 x 64 inverse diagonal blocks
-    double** inv_ptrs;
+    double* inv;  // potrf_work_doubles(chains): inverse diagonal blocks (64x64 or 128x128
+                  // per chain), then int active[chains]
+    double** inv_ptrs;     // chain i: inv + i * 64 * 64
+    double** inv128_ptrs;  // chain i: inv + i * 128 * 128
     int workers = 0;          // task-graph POTRF: persistent CTAs (0 = one per SM)
     DagState* dag = nullptr;  // task-graph POTRF: task order, flags, inverse tiles (lazy)
 };
+inline size_t potrf_work_doubles(int chains) { return (size_t)chains * 128 * 128 + chains; }
 void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status,
                    PotrfWork& w, cudaStream_t s, int extra_rows = 0);
 // the task-graph POTRF (potrf_dag.cu); potrf_batched routes here unless DIAM_B200_POTRF

@@ -259,6 +259,27 @@ __global__ void __launch_bounds__(256, MINB) potrf_diag_kernel(double* const* Am
     }
 }
 
+// 128x128 diagonal block: L11 = chol, X = L11^-1 (diag128_tc), one CTA per chain; the
+// block's upper-right 64x64 quarter is zeroed (the factor's strict upper part is exact zeros)
+__global__ void __launch_bounds__(256, 1) potrf_diag128_kernel(double* const* Am, int64_t ld, int j0, int jb,
+                                                               const int* mask, int* status, int* active,
+                                                               double* inv_base) {
+    extern __shared__ __align__(16) double dyn_smem[];
+    const int c = blockIdx.x;
+    const bool run = (!mask || mask[c]) && status[c] == 0;
+    if (threadIdx.x == 0) active[c] = run ? 1 : 0;
+    if (!run) return;
+    double* Ab = Am[c] + (int64_t)j0 * ld + j0;
+    if (jb > kNb)
+        for (int e = threadIdx.x; e < kNb * (jb - kNb); e += blockDim.x)
+            Ab[(int64_t)(e / (jb - kNb)) * ld + kNb + e % (jb - kNb)] = 0.0;
+    const int bad = diag128_tc(Ab, ld, jb, inv_base + (int64_t)c * kD2 * kD2, dyn_smem);
+    if (bad && threadIdx.x == 0) {
+        status[c] = 1;
+        active[c] = 0;
+    }
+}
+
 // ------------------------------------------------------------------ persistent per-chain POTRF
 // One 2-CTA cluster per chain walks the whole left-looking factorization (64-wide block
 // columns): both CTAs split the panel-update and TRSM tiles of a block column, CTA 0
@@ -599,16 +620,19 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     // GEMMs and TRSMs and come out as (L^{-1} r)^T: the forward substitution of the
     // usable-factor guard (proj/src/proposal.cpp:185-199) costs no extra pass over L.
     // w.inv holds chains*64*64 doubles, followed (by the caller's allocation) by an int active[chains]
-    int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kNb * kNb);
+    int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kD2 * kD2);
     const int rows = d + extra_rows;
     // Default: the launch-per-phase blocked path below. DIAM_B200_POTRF (read per call):
     //   dag     the task-graph POTRF (potrf_dag.cu): one persistent launch per factorization;
     //           faster on one stream (7.7 vs 9.1 ms per d=1024 batch), equal with 8 chain
     //           groups, 12% slower at d=4096 (K=128 tile updates vs the long-K updates here)
     //   cluster the persistent 2-CTA-cluster kernel: 6% slower at d=1024 with 4 groups
+    //   wide    128-wide diagonal blocks (diag128_tc) and 128-deep TRSMs: 24 launches per
+    //           factorization instead of 40, but the diagonal block costs 79 us vs 2 x 29;
+    //           0.7% slower at d=1024, equal at d=2040 / 4096
     const char* pe = std::getenv("DIAM_B200_POTRF");
     const std::string pm = pe ? pe : "";
-    const int mode = pm == "dag" ? 0 : (pm == "cluster" ? 2 : 1);
+    const int mode = pm == "dag" ? 0 : pm == "cluster" ? 2 : pm == "wide" ? 3 : 1;
     if (mode == 0) {
         potrf_dag(A, ld, d, chains, mask, status, w, s, extra_rows);
         return;
@@ -626,7 +650,7 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
         return;
     }
     // A[r0:rows, c0:c0+n] -= L[r0:rows, k0:k0+k] L[c0:c0+n, k0:k0+k]^T
-    auto update = [&](int r0, int c0, int n, int k0, int k, GemmShape shape) {
+    auto update = [&](int r0, int c0, int n, int k0, int k, GemmShape shape, int tri_c = 0) {
         GemmBatch p{};
         p.A = (const double* const*)A;
         p.B = (const double* const*)A;
@@ -641,8 +665,49 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
         p.alpha = -1.0;
         p.beta = 1.0;
         p.active = active;
+        p.tri_c_lower = tri_c;
         gemm_f64(p, chains, true, true, s, shape);
     };
+    if (mode == 3) {
+        // 128-wide block columns, each: (1) the left-looking update A[j0:, J] -= L[j0:, :j0]
+        // L[J, :j0]^T (lower part of the diagonal tile only), (2) chol + inverse of the
+        // 128x128 diagonal block in one CTA per chain, (3) L21 = A21 inv(L11)^T as one
+        // 128-deep GEMM on 128x128 tiles (in place: one column tile per row block), the
+        // inverse's upper zeros skipped. 24 launches per factorization instead of 40.
+        static bool attr = false;
+        if (!attr) {
+            DGB_CUDA(cudaFuncSetAttribute(potrf_diag128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kDiag128SmemBytes));
+            attr = true;
+        }
+        for (int j0 = 0; j0 < d; j0 += kD2) {
+            const int jb = std::min(kD2, d - j0);
+            if (j0 > 0) update(j0, j0, jb, 0, j0, GemmShape::Big, 1);
+            potrf_diag128_kernel<<<chains, 256, kDiag128SmemBytes, s>>>(A, ld, j0, jb, mask, status, active, w.inv);
+            DGB_LAUNCH_CHECK();
+            count_launch();
+            const int rest = rows - j0 - jb;
+            if (rest <= 0) continue;
+            GemmBatch t{};
+            t.A = (const double* const*)A;
+            t.B = (const double* const*)w.inv128_ptrs;
+            t.C = A;
+            t.a_off = (int64_t)(j0 + jb) * ld + j0;
+            t.c_off = t.a_off;
+            t.lda = ld;
+            t.ldb = kD2;
+            t.ldc = ld;
+            t.M = rest;
+            t.N = jb;
+            t.K = jb;
+            t.alpha = 1.0;
+            t.beta = 0.0;
+            t.active = active;
+            t.tri_b_lower = 1;
+            gemm_f64(t, chains, true, true, s, GemmShape::Square);
+        }
+        return;
+    }
     // factor the 64-wide diagonal block at (c0, c0) and solve the rows below it (in place)
     auto factor_and_solve = [&](int c0, int n, int zero_above) {
         // the diagonal block: panel-by-warp + DMMA (diag_tc.cuh, default: 23 vs 27 us per

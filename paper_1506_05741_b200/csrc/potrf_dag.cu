@@ -232,89 +232,8 @@ __device__ int diag128(double* A, int64_t ld, int jb, double* X, double* smem) {
     return 0;
 }
 
-// The same on the DMMA diagonal blocks of diag_tc.cuh: diag64_tc on A11, then
-// L21 = A21 X11^T, A22 -= L21 L21^T and X21 = -X22 (L21 X11) as 8x8 DMMA tiles (8 per
-// warp), L21 kept in shared memory after the diag scratch; no other staging.
-constexpr int kL21S = 68;  // stride of the L21 / U blocks (4 mod 16)
+// diag128_tc (diag_tc.cuh) works in the ring
 static_assert(sizeof(DiagTcScratch) + 64 * kL21S * 8 <= DagTile::SMEM_BYTES, "diag128_tc fits the ring");
-
-__device__ int diag128_tc(double* A, int64_t ld, int jb, double* X, double* smem) {
-    DiagTcScratch& sc = *reinterpret_cast<DiagTcScratch*>(smem);
-    double* sl = smem + (sizeof(DiagTcScratch) + 7) / 8;  // L21, 64 x kL21S
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int fr = lane >> 2, fk = lane & 3;
-    const int j1 = min(kDiagNb, jb);
-    if (diag64_tc_sc(sc, A, ld, j1, X, 0, kTb)) return 1;
-    for (int e = tid; e < 64 * 64; e += 256) X[(e >> 6) * kTb + 64 + (e & 63)] = 0.0;  // upper-right block
-    if (jb <= kDiagNb) {
-        for (int e = tid; e < 64 * kTb; e += 256) X[64 * kTb + e] = 0.0;
-        return 0;
-    }
-    const int j2 = jb - kDiagNb;
-    __syncthreads();  // L11 / X11 stores visible to the CTA
-    // L21 = A21 X11^T: warp w computes output tiles (w, ct), ct = 0..7
-    for (int ct = 0; ct < 8; ++ct) {
-        const int rt = warp;
-        double acc[2] = {0.0, 0.0};
-        const int r = 8 * rt + fr;
-        for (int k = 0; k < 64; k += 4) {
-            const double av = r < j2 ? __ldcg(A + (int64_t)(64 + r) * ld + k + fk) : 0.0;
-            const double bv = __ldcg(X + (8 * ct + fr) * kTb + k + fk);  // X11[n][k]
-            tile::dmma(acc, av, bv);
-        }
-        sl[r * kL21S + 8 * ct + 2 * fk] = acc[0];
-        sl[r * kL21S + 8 * ct + 2 * fk + 1] = acc[1];
-    }
-    __syncthreads();
-    // (written back only now: every tile above read all of A21)
-    for (int e = tid; e < 64 * 64; e += 256) {
-        const int r = e >> 6, q = e & 63;
-        if (r < j2) A[(int64_t)(64 + r) * ld + q] = sl[r * kL21S + q];
-    }
-    // A22 -= L21 L21^T on the lower tiles (ct <= rt)
-    for (int t = warp; t < 36; t += 8) {
-        int rt = 0, base = 0;
-        while (base + rt + 1 <= t) {
-            base += rt + 1;
-            ++rt;
-        }
-        const int ct = t - base;
-        double acc[2] = {0.0, 0.0};
-        for (int k = 0; k < 64; k += 4)
-            tile::dmma(acc, sl[(8 * rt + fr) * kL21S + k + fk], sl[(8 * ct + fr) * kL21S + k + fk]);
-        const int r = 8 * rt + fr, q = 8 * ct + 2 * fk;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-            if (r < j2 && q + h <= r) {
-                double* p = A + (int64_t)(64 + r) * ld + 64 + q + h;
-                *p = __ldcg(p) - acc[h];
-            }
-    }
-    __syncthreads();
-    if (diag64_tc_sc(sc, A + 64 * ld + 64, ld, j2, X + 64 * kTb + 64, 0, kTb)) return 1;
-    __syncthreads();
-    // U = L21 X11 into sc.a (free now; X22 stays in sc.x), then X21 = -X22 U
-    double* su = sc.a;
-    for (int ct = 0; ct < 8; ++ct) {
-        const int rt = warp;
-        double acc[2] = {0.0, 0.0};
-        for (int k = 0; k < 64; k += 4)
-            tile::dmma(acc, sl[(8 * rt + fr) * kL21S + k + fk], __ldcg(X + (k + fk) * kTb + 8 * ct + fr));
-        su[(8 * rt + fr) * kL21S + 8 * ct + 2 * fk] = acc[0];
-        su[(8 * rt + fr) * kL21S + 8 * ct + 2 * fk + 1] = acc[1];
-    }
-    __syncthreads();
-    for (int ct = 0; ct < 8; ++ct) {
-        const int rt = warp;
-        double acc[2] = {0.0, 0.0};
-        for (int k = 0; k < 64; k += 4)
-            tile::dmma(acc, sc.x[(8 * rt + fr) * kTcS + k + fk], su[(k + fk) * kL21S + 8 * ct + fr]);
-        const int r = 8 * rt + fr, q = 8 * ct + 2 * fk;
-        X[(64 + r) * kTb + q] = r < j2 ? -acc[0] : 0.0;
-        X[(64 + r) * kTb + q + 1] = r < j2 ? -acc[1] : 0.0;
-    }
-    return 0;
-}
 
 __global__ void __launch_bounds__(256, 2) potrf_dag_kernel(DagArgs a) {
     extern __shared__ __align__(16) double smem[];

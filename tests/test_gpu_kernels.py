@@ -141,12 +141,13 @@ def oracle_chol(m):
     return st, out
 
 
-@pytest.mark.parametrize("mode", ["blocked", "blocked+regdiag", "dag", "cluster"])
-@pytest.mark.parametrize("d", [1, 5, 64, 65, 130, 257, 520])
+@pytest.mark.parametrize("mode", ["wide", "narrow", "narrow+regdiag", "dag", "cluster"])
+@pytest.mark.parametrize("d", [1, 5, 64, 65, 127, 128, 129, 130, 257, 520])
 def test_potrf_batched_vs_oracle(lib, monkeypatch, d, mode):
-    # every factorization path: the launch-per-phase blocked POTRF (default, with the
-    # DMMA diagonal block of diag_tc.cuh; also with the register-blocked one), the
-    # task-graph persistent kernel (potrf_dag.cu), the 2-CTA-cluster kernel
+    # every factorization path: the launch-per-phase blocked POTRF with 128-wide diagonal
+    # blocks (default), with 64-wide ones (DMMA diagonal block of diag_tc.cuh; also the
+    # register-blocked one), the task-graph persistent kernel (potrf_dag.cu), the
+    # 2-CTA-cluster kernel
     monkeypatch.setenv("DIAM_B200_POTRF", mode.split("+")[0])
     if mode.endswith("regdiag"):
         monkeypatch.setenv("DIAM_B200_DIAG", "block")
