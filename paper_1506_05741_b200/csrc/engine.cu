@@ -732,7 +732,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         t.alpha_vec_mul = infl;
         t.beta = 0.0;
         t.tri_b_lower = 1;
-        gemm("trmm_noise", t, C, true, true, s);
+        gemm("trmm_noise", t, C, true, true, s, GemmShape::Stream);
     }
     {
         GemmBatch h{};
@@ -748,13 +748,13 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
             h.A = (const double* const*)g.Xib;
             h.C = g.Hb;
             h.M = C * Lc_;  // the group's window chunks are one contiguous (C Lc) x ld matrix
-            gemm("gemm_target", h, 1, true, true, s);
+            gemm("gemm_target", h, 1, true, true, s, GemmShape::Stream);
         } else {            // ragged last chunk: per-chain pieces
             h.B = (const double* const*)Gpc_;
             h.A = (const double* const*)g.Xip;
             h.C = Hp_ + o;
             h.M = rows;
-            gemm("gemm_target", h, C, true, true, s);
+            gemm("gemm_target", h, C, true, true, s, GemmShape::Stream);
         }
     }
 

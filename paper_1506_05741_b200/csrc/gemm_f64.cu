@@ -12,7 +12,7 @@ namespace {
 using tile::Cfg;
 
 template <class CF, bool AK, bool BKM>
-__global__ void __launch_bounds__(256, CF::MINB) gemm_f64_kernel(GemmBatch p) {
+__global__ void __launch_bounds__(CF::THREADS, CF::MINB) gemm_f64_kernel(GemmBatch p) {
     const int b = blockIdx.z;
     if (p.active && !p.active[b]) return;
     // triangular B: tile n has K = (n+1) BN, so hand out the longest tiles first
@@ -47,26 +47,36 @@ void launch(const GemmBatch& g, int batch, cudaStream_t stream) {
 
 template <bool AK, bool BKM>
 void dispatch_shape(const GemmBatch& g, int batch, cudaStream_t stream, GemmShape shape) {
-    // tile configuration: 2 (default) = 128x64 tiles, 32-deep K stages double-buffered,
-    // two resident CTAs per SM (8 warps of 32x32) so one CTA's epilogue and pipeline fill
-    // overlap the other's DMMA main loop; 1 = the same with 16-deep stages, 3-deep ring
-    // (1.2% slower per batch: twice the barriers per flop); 0 = 128x128, 1 CTA/SM, 8 warps
-    // of 64x32 (9% slower). Measured alternatives, slower still: 128x128 with 32-deep
-    // stages (1 CTA/SM), 128x64 with a 3-deep 32-wide ring (1 CTA/SM).
-    // DIAM_B200_GEMM_CFG selects for experiments.
+    // Tile configurations (tools/gemm_k_sweep.py: C = A B, 32768 x 1024, K = 512 / 1024):
+    //   2  128x64 tiles, 8 warps of 32x32, 32-deep K stages double-buffered, 2 CTAs/SM:
+    //      beta=0 85.0 / 87.8% of the DMMA peak, beta=1 83.9 / 87.0%; the default
+    //   4  128x64 tiles, 4 warps of 64x32 (half the fragment loads per DMMA), 16-deep
+    //      stages in a 3-deep ring, 2 CTAs/SM: beta=0 86.7 / 89.5%, beta=1 83.9 / 87.9%;
+    //      the Stream shape (the window products) -- slower on the factorization's
+    //      short, ragged updates and on the SYRK in the engine
+    //   1  as 2 with 16-deep stages in a 3-deep ring (1.2% slower per batch)
+    //   0  128x128 (Big) / 128x64 (Narrow) tiles, 1 CTA/SM, 16-deep 4-deep ring (9% slower)
+    // Measured and dropped: 64x128 tiles of 4 warps of 32x64 (16- or 32-deep), 4 warps
+    // with 32-deep double-buffered stages, 128x128 with 32-deep stages (1 CTA/SM).
+    // DIAM_B200_GEMM_CFG forces one configuration for every shape but Square.
     static const int cfg = [] {
         const char* e = std::getenv("DIAM_B200_GEMM_CFG");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : -1;
     }();
+    const int c = cfg >= 0 ? cfg : shape == GemmShape::Stream ? 4 : 2;
     if (shape == GemmShape::Square) {
         launch<Cfg<128, 128, 16, 4, AK, BKM>, AK, BKM>(g, batch, stream);
         return;
     }
-    if (cfg == 2) {
+    if (c == 2) {
         launch<Cfg<128, 64, 32, 2, AK, BKM, 4, 2, 2>, AK, BKM>(g, batch, stream);
         return;
     }
-    if (cfg == 1) {
+    if (c == 4) {
+        launch<Cfg<128, 64, 16, 3, AK, BKM, 2, 2, 2>, AK, BKM>(g, batch, stream);
+        return;
+    }
+    if (c == 1) {
         launch<Cfg<128, 64, 16, 3, AK, BKM, 4, 2, 2>, AK, BKM>(g, batch, stream);
         return;
     }

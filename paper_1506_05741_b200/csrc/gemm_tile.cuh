@@ -41,9 +41,9 @@ template <int BM_, int BN_, int BK_, int STAGES_, bool AK, bool BKM, int WARPS_M
           int MINB_ = 1>
 struct Cfg {
     static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_;
-    static constexpr int THREADS = 256;
+    static constexpr int THREADS = 32 * WARPS_M_ * WARPS_N_;
     static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
-    static constexpr int MINB = MINB_;  // CTAs resident per SM (register budget 64K / (256 * MINB))
+    static constexpr int MINB = MINB_;  // CTAs resident per SM (register budget 64K / (THREADS * MINB))
     static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
     static constexpr int MI = WM / 8, NI = WN / 8;
     // shared layout: the global-contiguous dimension stays contiguous; stride = 4 mod 16
@@ -107,16 +107,16 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
         double* a_s = sA + stage * CF::A_STAGE;
         double* b_s = sB + stage * CF::B_STAGE;
         if (AK)
-            load_tile<CF::A_ROWS, CF::A_COLS, CF::A_STRIDE, 256>(a_s, A + (int64_t)m0 * lda + k0, lda, M - m0,
+            load_tile<CF::A_ROWS, CF::A_COLS, CF::A_STRIDE, CF::THREADS>(a_s, A + (int64_t)m0 * lda + k0, lda, M - m0,
                                                                  K - k0, tid);
         else
-            load_tile<CF::A_ROWS, CF::A_COLS, CF::A_STRIDE, 256>(a_s, A + (int64_t)k0 * lda + m0, lda, K - k0,
+            load_tile<CF::A_ROWS, CF::A_COLS, CF::A_STRIDE, CF::THREADS>(a_s, A + (int64_t)k0 * lda + m0, lda, K - k0,
                                                                  M - m0, tid);
         if (BKM)
-            load_tile<CF::B_ROWS, CF::B_COLS, CF::B_STRIDE, 256>(b_s, B + (int64_t)n0 * ldb + k0, ldb, N - n0,
+            load_tile<CF::B_ROWS, CF::B_COLS, CF::B_STRIDE, CF::THREADS>(b_s, B + (int64_t)n0 * ldb + k0, ldb, N - n0,
                                                                  K - k0, tid);
         else
-            load_tile<CF::B_ROWS, CF::B_COLS, CF::B_STRIDE, 256>(b_s, B + (int64_t)k0 * ldb + n0, ldb, K - k0,
+            load_tile<CF::B_ROWS, CF::B_COLS, CF::B_STRIDE, CF::THREADS>(b_s, B + (int64_t)k0 * ldb + n0, ldb, K - k0,
                                                                  N - n0, tid);
     };
 
@@ -170,30 +170,47 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
     }
     cp_async_wait<0>();
 
+    // Epilogue in batches of IC fragment rows: all of a batch's C loads are issued before
+    // its stores (a store to C may alias a later load, so the compiler would otherwise
+    // serialise one L2 round trip per fragment).
+    constexpr int IC = CF::MI >= 2 ? 2 : 1;
 #pragma unroll
-    for (int i = 0; i < CF::MI; ++i) {
-        const int r = m0 + wm0 + i * 8 + fr;
-        if (r >= M) continue;
-        double* crow = Cp + (int64_t)r * ldc;
+    for (int i0 = 0; i0 < CF::MI; i0 += IC) {
+        double2 old[IC][CF::NI];
 #pragma unroll
-        for (int j = 0; j < CF::NI; ++j) {
-            const int c0 = n0 + wn0 + j * 8 + fk * 2;
-            const bool ok0 = c0 < N && (!tri_c_lower || c0 <= r);
-            const bool ok1 = c0 + 1 < N && (!tri_c_lower || c0 + 1 <= r);
-            if (ok0 && ok1) {
-                double2 v = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+        for (int ii = 0; ii < IC; ++ii) {
+            const int r = m0 + wm0 + (i0 + ii) * 8 + fr;
+#pragma unroll
+            for (int j = 0; j < CF::NI; ++j) {
+                const int c0 = n0 + wn0 + j * 8 + fk * 2;
+                old[ii][j] = make_double2(0.0, 0.0);
+                if (beta == 0.0 || r >= M) continue;
+                // through L2: in the task-graph POTRF the tile may have been rewritten by
+                // another SM since this one cached it
+                const double* src = Cp + (int64_t)r * ldc + c0;
+                const bool ok0 = c0 < N && (!tri_c_lower || c0 <= r);
+                const bool ok1 = c0 + 1 < N && (!tri_c_lower || c0 + 1 <= r);
+                if (ok0 && ok1) old[ii][j] = __ldcg(reinterpret_cast<const double2*>(src));
+                else if (ok0) old[ii][j].x = __ldcg(src);
+            }
+        }
+#pragma unroll
+        for (int ii = 0; ii < IC; ++ii) {
+            const int r = m0 + wm0 + (i0 + ii) * 8 + fr;
+            if (r >= M) continue;
+            double* crow = Cp + (int64_t)r * ldc;
+#pragma unroll
+            for (int j = 0; j < CF::NI; ++j) {
+                const int c0 = n0 + wn0 + j * 8 + fk * 2;
+                const bool ok0 = c0 < N && (!tri_c_lower || c0 <= r);
+                const bool ok1 = c0 + 1 < N && (!tri_c_lower || c0 + 1 <= r);
+                double2 v = make_double2(alpha * acc[i0 + ii][j][0], alpha * acc[i0 + ii][j][1]);
                 if (beta != 0.0) {
-                    // through L2: in the task-graph POTRF the tile may have been rewritten
-                    // by another SM since this one cached it
-                    const double2 o = __ldcg(reinterpret_cast<const double2*>(crow + c0));
-                    v.x += beta * o.x;
-                    v.y += beta * o.y;
+                    v.x += beta * old[ii][j].x;
+                    v.y += beta * old[ii][j].y;
                 }
-                *reinterpret_cast<double2*>(crow + c0) = v;
-            } else if (ok0) {
-                double v = alpha * acc[i][j][0];
-                if (beta != 0.0) v += beta * __ldcg(crow + c0);
-                crow[c0] = v;
+                if (ok0 && ok1) *reinterpret_cast<double2*>(crow + c0) = v;
+                else if (ok0) crow[c0] = v.x;
             }
         }
     }
