@@ -65,10 +65,21 @@ __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_
     constexpr unsigned kAll = 0xffffffffu;
     double* sa = sc.a;
     double* sx = sc.x;
-    // load the lower part; rows/cols past jb are the identity (a valid 64x64 factorization)
-    for (int e = tid; e < 64 * 64; e += 256) {
-        const int r = e >> 6, q = e & 63;
-        sa[r * kTcS + q] = (r < jb && q <= r) ? __ldcg(A + (int64_t)r * ld + q) : (r == q ? 1.0 : 0.0);
+    // load the lower part; rows/cols past jb are the identity (a valid 64x64 factorization).
+    // All 16 loads of a thread are in flight together (a loop that stores each value
+    // before the next load would pay one L2 round trip per element: ~9000 cycles).
+    {
+        double v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int e = tid + 256 * i, r = e >> 6, q = e & 63;
+            v[i] = (r < jb && q <= r) ? __ldcg(A + (int64_t)r * ld + q) : (r == q ? 1.0 : 0.0);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int e = tid + 256 * i;
+            sa[(e >> 6) * kTcS + (e & 63)] = v[i];
+        }
     }
     if (tid == 0) sc.bad = 0;
     TC_MARK(0);
@@ -193,10 +204,14 @@ constexpr int kD2 = 128;
 // L = chol(A) and X = L^-1 of one 128x128 diagonal block (jb <= 128 valid rows) by the
 // 256 threads of a CTA, X row-major with stride kD2, zero outside the lower jb x jb part;
 // `smem` holds a DiagTcScratch followed by a 64 x kL21S block (kDiag128SmemBytes).
-// The same on the DMMA diagonal blocks of diag_tc.cuh: diag64_tc on A11, then
-// L21 = A21 X11^T, A22 -= L21 L21^T and X21 = -X22 (L21 X11) as 8x8 DMMA tiles (8 per
-// warp), L21 kept in shared memory after the diag scratch; no other staging.
-constexpr int kL21S = 68;  // stride of the L21 / U blocks (4 mod 16)
+// Two DMMA diagonal blocks (diag64_tc_sc) joined by 8x8 DMMA tiles with every operand in
+// shared memory (8 row tiles per product, one per warp):
+//   L21 = A21 X11^T                (A21 staged over L11, X11 still in the scratch)
+//   A22 -= L21 L21^T, U = L21 X11  (U parked in X's X21 block)
+//   chol / inverse of A22          (X22 in the scratch)
+//   X21 = -X22 U                   (U staged over L22)
+// The triangular factors' zero blocks are skipped in every K loop.
+constexpr int kL21S = 68;  // stride of the L21 block (4 mod 16)
 
 __device__ __forceinline__ int diag128_tc(double* A, int64_t ld, int jb, double* X, double* smem) {
     DiagTcScratch& sc = *reinterpret_cast<DiagTcScratch*>(smem);
@@ -204,75 +219,120 @@ __device__ __forceinline__ int diag128_tc(double* A, int64_t ld, int jb, double*
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int fr = lane >> 2, fk = lane & 3;
     const int j1 = min(kDiagNb, jb);
+    TC_MARK(8);
     if (diag64_tc_sc(sc, A, ld, j1, X, 0, kD2)) return 1;
+    TC_MARK(9);
     for (int e = tid; e < 64 * 64; e += 256) X[(e >> 6) * kD2 + 64 + (e & 63)] = 0.0;  // upper-right block
     if (jb <= kDiagNb) {
         for (int e = tid; e < 64 * kD2; e += 256) X[64 * kD2 + e] = 0.0;
         return 0;
     }
     const int j2 = jb - kDiagNb;
-    __syncthreads();  // L11 / X11 stores visible to the CTA
-    // L21 = A21 X11^T: warp w computes output tiles (w, ct), ct = 0..7
-    for (int ct = 0; ct < 8; ++ct) {
-        const int rt = warp;
-        double acc[2] = {0.0, 0.0};
-        const int r = 8 * rt + fr;
-        for (int k = 0; k < 64; k += 4) {
-            const double av = r < j2 ? __ldcg(A + (int64_t)(64 + r) * ld + k + fk) : 0.0;
-            const double bv = __ldcg(X + (8 * ct + fr) * kD2 + k + fk);  // X11[n][k]
-            tile::dmma(acc, av, bv);
+    const int rt = warp, r = 8 * rt + fr;
+    {
+        double v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int e = tid + 256 * i, rr = e >> 6, q = e & 63;
+            v[i] = rr < j2 ? __ldcg(A + (int64_t)(64 + rr) * ld + q) : 0.0;
         }
+        __syncthreads();  // diag64_tc_sc's stores have read sc.a
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int e = tid + 256 * i;
+            sc.a[(e >> 6) * kTcS + (e & 63)] = v[i];
+        }
+    }
+    __syncthreads();
+    // L21 = A21 X11^T (X11[n][k] = 0 for k > n)
+    for (int ct = 0; ct < 8; ++ct) {
+        double acc[2];
+        tc_tile(acc, sc.a, 8 * rt, sc.x, 8 * ct, 8 * ct + 8, lane);
         sl[r * kL21S + 8 * ct + 2 * fk] = acc[0];
         sl[r * kL21S + 8 * ct + 2 * fk + 1] = acc[1];
     }
     __syncthreads();
-    // (written back only now: every tile above read all of A21)
+    TC_MARK(10);
     for (int e = tid; e < 64 * 64; e += 256) {
-        const int r = e >> 6, q = e & 63;
-        if (r < j2) A[(int64_t)(64 + r) * ld + q] = sl[r * kL21S + q];
+        const int rr = e >> 6, q = e & 63;
+        if (rr < j2) A[(int64_t)(64 + rr) * ld + q] = sl[rr * kL21S + q];
     }
-    // A22 -= L21 L21^T on the lower tiles (ct <= rt)
-    for (int t = warp; t < 36; t += 8) {
-        int rt = 0, base = 0;
-        while (base + rt + 1 <= t) {
-            base += rt + 1;
-            ++rt;
-        }
-        const int ct = t - base;
-        double acc[2] = {0.0, 0.0};
-        for (int k = 0; k < 64; k += 4)
-            tile::dmma(acc, sl[(8 * rt + fr) * kL21S + k + fk], sl[(8 * ct + fr) * kL21S + k + fk]);
-        const int r = 8 * rt + fr, q = 8 * ct + 2 * fk;
+    // A22 -= L21 L21^T on the lower tiles (ct <= rt), in place in global memory: a warp's
+    // (up to 5) tiles are multiplied first, then all their loads issued, then the stores
+    {
+        double acc[5][2], old[5][2];
+        int tr[5], tc[5];
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-            if (r < j2 && q + h <= r) {
-                double* p = A + (int64_t)(64 + r) * ld + 64 + q + h;
-                *p = __ldcg(p) - acc[h];
+        for (int u = 0; u < 5; ++u) {
+            const int t = warp + 8 * u;
+            int a = 0, base = 0;
+            while (base + a + 1 <= t) {
+                base += a + 1;
+                ++a;
+            }
+            tr[u] = a;
+            tc[u] = t - base;
+            acc[u][0] = acc[u][1] = 0.0;
+            if (t < 36) tc_tile(acc[u], sl, 8 * tr[u], sl, 8 * tc[u], 64, lane);
+        }
+#pragma unroll
+        for (int u = 0; u < 5; ++u)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int rr = 8 * tr[u] + fr, q = 8 * tc[u] + 2 * fk + h;
+                old[u][h] = (warp + 8 * u < 36 && rr < j2 && q <= rr) ? __ldcg(A + (int64_t)(64 + rr) * ld + 64 + q) : 0.0;
+            }
+#pragma unroll
+        for (int u = 0; u < 5; ++u)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int rr = 8 * tr[u] + fr, q = 8 * tc[u] + 2 * fk + h;
+                if (warp + 8 * u < 36 && rr < j2 && q <= rr) A[(int64_t)(64 + rr) * ld + 64 + q] = old[u][h] - acc[u][h];
             }
     }
-    __syncthreads();
+    // U = L21 X11 (X11[k][n] = 0 for k < n), parked in X21
+    for (int ct = 0; ct < 8; ++ct) {
+        double e[2] = {0.0, 0.0}, o[2] = {0.0, 0.0};
+        int k = 8 * ct;
+        for (; k + 8 <= 64; k += 8) {
+            tile::dmma(e, sl[r * kL21S + k + fk], sc.x[(k + fk) * kTcS + 8 * ct + fr]);
+            tile::dmma(o, sl[r * kL21S + k + 4 + fk], sc.x[(k + 4 + fk) * kTcS + 8 * ct + fr]);
+        }
+        X[(64 + r) * kD2 + 8 * ct + 2 * fk] = e[0] + o[0];
+        X[(64 + r) * kD2 + 8 * ct + 2 * fk + 1] = e[1] + o[1];
+    }
+    __syncthreads();  // A22 and U stores visible to the CTA; sc.x (X11) no longer read
+    TC_MARK(11);
     if (diag64_tc_sc(sc, A + 64 * ld + 64, ld, j2, X + 64 * kD2 + 64, 0, kD2)) return 1;
-    __syncthreads();
-    // U = L21 X11 into sc.a (free now; X22 stays in sc.x), then X21 = -X22 U
-    double* su = sc.a;
-    for (int ct = 0; ct < 8; ++ct) {
-        const int rt = warp;
-        double acc[2] = {0.0, 0.0};
-        for (int k = 0; k < 64; k += 4)
-            tile::dmma(acc, sl[(8 * rt + fr) * kL21S + k + fk], __ldcg(X + (k + fk) * kD2 + 8 * ct + fr));
-        su[(8 * rt + fr) * kL21S + 8 * ct + 2 * fk] = acc[0];
-        su[(8 * rt + fr) * kL21S + 8 * ct + 2 * fk + 1] = acc[1];
+    {
+        double v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int e = tid + 256 * i;
+            v[i] = __ldcg(X + (64 + (e >> 6)) * kD2 + (e & 63));
+        }
+        __syncthreads();  // the second diag64_tc_sc has read sc.a
+        TC_MARK(12);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int e = tid + 256 * i;
+            sc.a[(e >> 6) * kTcS + (e & 63)] = v[i];
+        }
     }
     __syncthreads();
+    // X21 = -X22 U (X22[r][k] = 0 for k > r)
     for (int ct = 0; ct < 8; ++ct) {
-        const int rt = warp;
-        double acc[2] = {0.0, 0.0};
-        for (int k = 0; k < 64; k += 4)
-            tile::dmma(acc, sc.x[(8 * rt + fr) * kTcS + k + fk], su[(k + fk) * kL21S + 8 * ct + fr]);
-        const int r = 8 * rt + fr, q = 8 * ct + 2 * fk;
-        X[(64 + r) * kD2 + q] = r < j2 ? -acc[0] : 0.0;
-        X[(64 + r) * kD2 + q + 1] = r < j2 ? -acc[1] : 0.0;
+        double e[2] = {0.0, 0.0}, o[2] = {0.0, 0.0};
+        int k = 0;
+        for (; k + 8 <= 8 * rt + 8; k += 8) {
+            tile::dmma(e, sc.x[r * kTcS + k + fk], sc.a[(k + fk) * kTcS + 8 * ct + fr]);
+            tile::dmma(o, sc.x[r * kTcS + k + 4 + fk], sc.a[(k + 4 + fk) * kTcS + 8 * ct + fr]);
+        }
+        const int q = 8 * ct + 2 * fk;
+        X[(64 + r) * kD2 + q] = r < j2 ? -(e[0] + o[0]) : 0.0;
+        X[(64 + r) * kD2 + q + 1] = r < j2 ? -(e[1] + o[1]) : 0.0;
     }
+    TC_MARK(13);
     return 0;
 }
 

@@ -628,8 +628,9 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     //           groups, 12% slower at d=4096 (K=128 tile updates vs the long-K updates here)
     //   cluster the persistent 2-CTA-cluster kernel: 6% slower at d=1024 with 4 groups
     //   wide    128-wide diagonal blocks (diag128_tc) and 128-deep TRSMs: 24 launches per
-    //           factorization instead of 40, but the diagonal block costs 79 us vs 2 x 29;
-    //           0.7% slower at d=1024, equal at d=2040 / 4096
+    //           factorization instead of 40; its diagonal block (61 us) costs about as much
+    //           as two 64-wide ones plus the 64-deep update between them: equal at d=1024,
+    //           2040 and 4096
     const char* pe = std::getenv("DIAM_B200_POTRF");
     const std::string pm = pe ? pe : "";
     const int mode = pm == "dag" ? 0 : pm == "cluster" ? 2 : pm == "wide" ? 3 : 1;

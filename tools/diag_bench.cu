@@ -363,6 +363,44 @@ int main() {
                "block rows %lld, store %lld\n", pr[1] - pr[0], pr[2] - pr[1], pr[3] - pr[2], pr[4] - pr[3],
                pr[5] - pr[4], pr[6] - pr[5], pr[7] - pr[6]);
     }
+    {  // 128x128 diagonal block (diag128_tc): phases
+        const int n2 = 128;
+        std::vector<double> h2((size_t)chains * n2 * n2, 0.0);
+        for (int c = 0; c < chains; ++c)
+            for (int i = 0; i < n2; ++i)
+                for (int j = 0; j <= i; ++j)
+                    h2[(size_t)c * n2 * n2 + i * n2 + j] = (i == j ? n2 : 0.0) + 1.0 / (1.0 + i + j + c);
+        double *B, *inv2;
+        double** Bp;
+        cudaMalloc(&B, h2.size() * 8);
+        cudaMalloc(&inv2, (size_t)chains * 128 * 128 * 8);
+        std::vector<double*> hb(chains);
+        for (int c = 0; c < chains; ++c) hb[c] = B + (size_t)c * n2 * n2;
+        cudaMalloc(&Bp, chains * sizeof(double*));
+        cudaMemcpy(Bp, hb.data(), chains * sizeof(double*), cudaMemcpyHostToDevice);
+        cudaFuncSetAttribute(potrf_diag128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiag128SmemBytes);
+        float tot = 0.f;
+        for (int r = 0; r < 13; ++r) {
+            cudaMemcpy(B, h2.data(), h2.size() * 8, cudaMemcpyHostToDevice);
+            cudaMemset(status, 0, chains * 4);
+            cudaDeviceSynchronize();
+            cudaEventRecord(e0);
+            potrf_diag128_kernel<<<chains, 256, kDiag128SmemBytes>>>(Bp, n2, 0, n2, nullptr, status, active, inv2);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (r >= 3) tot += ms;
+        }
+        int st = 0;
+        cudaMemcpy(&st, status, 4, cudaMemcpyDeviceToHost);
+        long long pr[16];
+        cudaMemcpyFromSymbol(pr, dgb::g_tc_prof, sizeof pr);
+        printf("diag128 TC %8.2f us (status %d, %s); cycles: diag A11 %lld, L21 %lld, A22/U %lld, diag A22 %lld, "
+               "X21 %lld; inside the last diag64: panels %lld, inverse %lld, store %lld\n",
+               tot / 10 * 1e3, st, cudaGetErrorString(cudaGetLastError()), pr[9] - pr[8], pr[10] - pr[9],
+               pr[11] - pr[10], pr[12] - pr[11], pr[13] - pr[12], pr[4] - pr[1], pr[6] - pr[4], pr[7] - pr[6]);
+    }
     timeit([&] { diag_exp_kernel<0><<<chains, 256>>>(Ap, ld, 64, status, inv); }, "exp full");
     auto cyc = [&](auto launch, const char* name) {
         long long* cy;
