@@ -336,6 +336,7 @@ def impl_b200(args):
         dist.barrier()
     t0 = time.perf_counter()
     r = lib.sample(t, **run_options(cfg, chains, max_batches=args.steps))
+    t1 = time.perf_counter()
     mean = r.mean()
     cov = r.cov()
     wall = time.perf_counter() - t0
@@ -346,7 +347,8 @@ def impl_b200(args):
     bsec = r.history("batch_seconds")
     log(f"e2e: {wall * 1e3:.1f} ms wall, batches {bsec.sum() * 1e3:.1f} ms "
         f"(first {bsec[0] * 1e3:.1f}, median {float(sorted(bsec)[len(bsec) // 2]) * 1e3:.1f}), "
-        f"fixed costs {(wall - bsec.sum()) * 1e3:.1f} ms")
+        f"fixed costs {(wall - bsec.sum()) * 1e3:.1f} ms (diam_sample {(t1 - t0) * 1e3:.1f} ms, "
+        f"result copies {(wall - (t1 - t0)) * 1e3:.1f} ms)")
     e2e = r.total_samples / wall
     h2d = (d * d * 8 * 2 + 4 * d * 8) / args.steps  # precision + analytic covariance + vectors, once per run
     d2h = (mean.nbytes + cov.nbytes) / args.steps + chains * M * 16 + 24

@@ -302,6 +302,8 @@ Engine::~Engine() {
         if (g.status_ev) cudaEventDestroy(g.status_ev);
     pinned_release(h_flags_);
     pinned_release(h_stats_);
+    pinned_release(h_out_);
+    if (out_ev_) cudaEventDestroy(out_ev_);
     if (stream_) cudaStreamDestroy(stream_);
     mark("done");
 }
@@ -665,8 +667,24 @@ void Engine::run_batch_windows(bool record) {
     // (Measured and dropped: staggering the groups' start by half a window, and drawing
     // the next window's noise on a side stream during the refactorization -- neither
     // beat this plain order at d=1024 or d=4096.)
-    for (size_t m = 0; m < M; ++m) next_plan(m);
-    for (auto& g : groups_) enqueue_head(g, plans[0]);
+    begin_windows(record);
+    end_windows();
+}
+
+void Engine::begin_windows(bool record) {
+    const size_t M = cfg_.intervals_per_batch;
+    bplans_.clear();
+    bplans_.reserve(M);
+    for (size_t m = 0; m < M; ++m) {
+        bplans_.push_back(plan_window(m, record));
+        commit_window(bplans_.back());
+    }
+    for (auto& g : groups_) enqueue_head(g, bplans_[0]);
+}
+
+void Engine::end_windows() {
+    const size_t M = cfg_.intervals_per_batch;
+    const std::vector<WindowPlan>& plans = bplans_;
     std::vector<Ladder> lad(groups_.size());
     for (size_t m = 0; m < M; ++m) {
         std::vector<size_t> pending;
@@ -1131,6 +1149,12 @@ void Engine::collect_batch_host(size_t windows) {
         }
     }
     DGB_CUDA(cudaStreamSynchronize(stream_));
+    collect_histories(windows, window_n_start_, rate.data(), beta.data(), lp.data(), pj.data());
+}
+
+void Engine::collect_histories(size_t windows, const std::vector<uint64_t>& n_start, const double* rate,
+                               const double* beta, const double* lp, const double* pj) {
+    const int C = C_;
     for (size_t w = 0; w < windows; ++w)
         for (int c = 0; c < C; ++c) {
             beta_hist_[c].push_back(beta[w * C + c]);
@@ -1138,7 +1162,7 @@ void Engine::collect_batch_host(size_t windows) {
         }
     if (!cfg_.record_traces) return;
     for (size_t w = 0; w < windows; ++w) {
-        const uint64_t ns = window_n_start_[w];
+        const uint64_t ns = n_start[w];
         for (int t = 0; t < Lw_; ++t) {
             const uint64_t n = ns + t + 1;
             if (!(n > k_.n0 && (n - k_.n0 - 1) % cfg_.trace_thin == 0)) continue;
@@ -1152,6 +1176,40 @@ void Engine::collect_batch_host(size_t windows) {
             }
         }
     }
+}
+
+void Engine::enqueue_batch_outputs(size_t windows) {
+    // one GPU only (the sharded run gathers on the host: batch_stats / collect_batch_host)
+    const int C = C_;
+    const size_t mc = windows * C, tr = cfg_.record_traces ? mc * (size_t)Lw_ : 0;
+    if (!h_out_) {
+        h_out_ = static_cast<double*>(pinned_acquire((2 * mc + 3 * tr + 1) * sizeof(double), false));
+        DGB_CUDA(cudaEventCreateWithFlags(&out_ev_, cudaEventDisableTiming));
+    }
+    const bool want_err = cnt_g_ >= 2, want_psrf = P_ >= 2 && cum_cnt_ >= 2;
+    if (want_err) launch_cov_error(Sg_, mg_, Ct_, d_, ld_, cov_part_, stream_);
+    launch_batch_stats(cov_part_, mg_, tmean_, d_, cmean_, cdiag_, ld_, C_, cum_cnt_, want_err, want_psrf, dstats_,
+                       stream_);
+    DGB_CUDA(cudaMemcpyAsync(h_stats_, dstats_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    DGB_CUDA(cudaMemcpyAsync(h_out_, hist_rate_, mc * 8, cudaMemcpyDeviceToHost, stream_));
+    DGB_CUDA(cudaMemcpyAsync(h_out_ + mc, hist_beta_, mc * 8, cudaMemcpyDeviceToHost, stream_));
+    if (tr) {
+        DGB_CUDA(cudaMemcpyAsync(h_out_ + 2 * mc, trace_lp_, tr * 8, cudaMemcpyDeviceToHost, stream_));
+        if (cfg_.trace_eigen_projections)
+            DGB_CUDA(cudaMemcpyAsync(h_out_ + 2 * mc + tr, trace_pj_, 2 * tr * 8, cudaMemcpyDeviceToHost, stream_));
+    }
+    DGB_CUDA(cudaEventRecord(out_ev_, stream_));
+    out_n_start_ = window_n_start_;  // the next batch's plans overwrite window_n_start_
+}
+
+void Engine::read_batch_outputs(size_t windows, double& cov_err, double& mean_err, double& psrf) {
+    const size_t mc = windows * C_, tr = cfg_.record_traces ? mc * (size_t)Lw_ : 0;
+    DGB_CUDA(cudaEventSynchronize(out_ev_));
+    require(!((int)h_stats_[3] & 1), Err::InvalidArgument, "cov_error: zero reference norm");
+    cov_err = h_stats_[0];
+    mean_err = h_stats_[1];
+    psrf = h_stats_[2];
+    collect_histories(windows, out_n_start_, h_out_, h_out_ + mc, h_out_ + 2 * mc, h_out_ + 2 * mc + tr);
 }
 
 double Engine::run_batches_timed(int k) {
@@ -1172,6 +1230,9 @@ double Engine::run_batches_timed(int k) {
         run_batch_windows(false);
         join_groups();
         merge_batch();
+        // the batch statistics and the history copies of a diam_sample batch (on one GPU;
+        // the host reads nothing here)
+        if (!comm_) enqueue_batch_outputs(M);
         ++batches_done_;
     }
     DGB_CUDA(cudaEventRecord(b, stream_));
@@ -1195,15 +1256,23 @@ RunResult Engine::run() {  // runner.cpp:216-279
         dbg_ratio_ = dalloc<double>(allocs_, (size_t)C_ * Lw_);
         dbg_acc_ = dalloc<uint8_t>(allocs_, (size_t)C_ * Lw_);
     }
+    // Pipelined on one GPU when no rule needs a batch's statistics or state before the next
+    // batch may start (no tolerance, wall-clock limit or checkpoint): the next batch's first
+    // windows are enqueued before the host waits for this batch's outputs, so the GPU does
+    // not idle while the host reads them. Otherwise batch by batch, as runner.cpp:216-279.
+    const bool pipelined = !comm_ && !capture_ && !pool_ && cfg_.checkpoint_path.empty() && !cfg_.max_wall_seconds &&
+                           !cfg_.psrf_tol && !cfg_.cov_tol && !cfg_.mean_tol;
+    auto cap_reason = [&](size_t done) -> const char* {  // loop-top rules known without the GPU
+        const uint64_t iters = (uint64_t)P_ * M * done * k_.n_lag;
+        if (cfg_.max_samples && iters >= *cfg_.max_samples) return "max_samples";
+        if (done >= cfg_.max_batches) return "batch_cap";
+        return nullptr;
+    };
+    bool head_queued = false;  // the next batch's plans and first windows are enqueued
     std::string reason;
     for (;;) {
-        const uint64_t iters = (uint64_t)P_ * M * batches_done_ * k_.n_lag;
-        if (cfg_.max_samples && iters >= *cfg_.max_samples) {
-            reason = "max_samples";
-            break;
-        }
-        if (batches_done_ >= cfg_.max_batches) {
-            reason = "batch_cap";
+        if (const char* cr = cap_reason(batches_done_)) {
+            reason = cr;
             break;
         }
         if (cfg_.max_wall_seconds && elapsed() >= *cfg_.max_wall_seconds) {
@@ -1211,14 +1280,32 @@ RunResult Engine::run() {  // runner.cpp:216-279
             break;
         }
         const auto b0 = std::chrono::steady_clock::now();
-        fork_groups();
-        run_batch_windows(cfg_.record_traces);
-        join_groups();
-        merge_batch();
-        collect_batch_host(M);
-        ++batches_done_;
         double ce, me, ps;
-        batch_stats(ce, me, ps);
+        if (pipelined) {
+            if (!head_queued) {
+                fork_groups();
+                begin_windows(cfg_.record_traces);
+            }
+            end_windows();
+            join_groups();
+            merge_batch();
+            enqueue_batch_outputs(M);
+            ++batches_done_;
+            head_queued = cap_reason(batches_done_) == nullptr;
+            if (head_queued) {
+                fork_groups();
+                begin_windows(cfg_.record_traces);
+            }
+            read_batch_outputs(M, ce, me, ps);
+        } else {
+            fork_groups();
+            run_batch_windows(cfg_.record_traces);
+            join_groups();
+            merge_batch();
+            collect_batch_host(M);
+            ++batches_done_;
+            batch_stats(ce, me, ps);
+        }
         batch_seconds_.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - b0).count());
         cov_hist_.push_back(ce);
         mean_hist_.push_back(me);

@@ -139,13 +139,26 @@ private:
     void ladder_retry(Group& g, const WindowPlan& p, Ladder& st);
     void tail_finish(Group& g, const WindowPlan& p);
     void run_batch_windows(bool record);
+    // run_batch_windows split for the pipelined run loop (no capture, no shared workspace):
+    // begin_windows plans the batch and enqueues every group's first window; end_windows
+    // runs the tails and the remaining windows
+    void begin_windows(bool record);
+    void end_windows();
+    std::vector<WindowPlan> bplans_;
     void capture_chunk(const Group& g, int r0, int rows);
     void capture_window(size_t w);
     void fork_groups();  // groups wait for the main stream
     void join_groups();  // main stream waits for every group
     void merge_batch();
     void batch_stats(double& cov_err, double& mean_err, double& psrf);
+    // the same in two halves on one GPU: enqueue the statistics kernels and every per-batch
+    // output's copy into pinned memory (stream order), then read them once the stream got there
+    void enqueue_batch_outputs(size_t windows);
+    void read_batch_outputs(size_t windows, double& cov_err, double& mean_err, double& psrf);
     void collect_batch_host(size_t windows);
+    void collect_histories(size_t windows, const std::vector<uint64_t>& n_start, const double* rate,
+                           const double* beta, const double* lp, const double* pj);
+    std::vector<uint64_t> out_n_start_;  // window start counts of the batch in h_out_
     void save_checkpoint(double wall);
     void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s,
               GemmShape sh = GemmShape::Big);
@@ -209,6 +222,8 @@ private:
     double* cov_part_ = nullptr;                              // d x 2
     double *tmean_ = nullptr, *dstats_ = nullptr;             // target mean; batch statistics (4)
     double* h_stats_ = nullptr;                               // pinned mirror of dstats_
+    double* h_out_ = nullptr;  // pinned per-batch outputs: rate, beta (M x C), traces (M x C x Lw x 3)
+    cudaEvent_t out_ev_ = nullptr;  // the copies into h_out_ / h_stats_ are done
     double* gather_ = nullptr;                                // PSRF all-gather buffer
     double* cS_ = nullptr;  // cumulative raw second moments (lower), kept only for checkpoints
     double wall_accum_ = 0.0;  // wall seconds of earlier (checkpointed) segments of the run

@@ -47,23 +47,25 @@ void launch(const GemmBatch& g, int batch, cudaStream_t stream) {
 
 template <bool AK, bool BKM>
 void dispatch_shape(const GemmBatch& g, int batch, cudaStream_t stream, GemmShape shape) {
-    // Tile configurations (tools/gemm_k_sweep.py: C = A B, 32768 x 1024, K = 512 / 1024):
+    // Tile configurations (tools/gemm_k_sweep.py: C = A B, 32768 x 1024, K = 512 / 1024,
+    // % of the live DMMA peak; the next stage's copies issued behind the first DMMAs):
     //   2  128x64 tiles, 8 warps of 32x32, 32-deep K stages double-buffered, 2 CTAs/SM:
-    //      beta=0 85.0 / 87.8% of the DMMA peak, beta=1 83.9 / 87.0%; the default
+    //      beta=0 86.9 / 89.4%, beta=1 85.5 / 88.4%; the default for every shape
     //   4  128x64 tiles, 4 warps of 64x32 (half the fragment loads per DMMA), 16-deep
-    //      stages in a 3-deep ring, 2 CTAs/SM: beta=0 86.7 / 89.5%, beta=1 83.9 / 87.9%;
-    //      the Stream shape (the window products) -- slower on the factorization's
-    //      short, ragged updates and on the SYRK in the engine
+    //      stages in a 3-deep ring, 2 CTAs/SM: beta=0 86.3 / 88.9%, beta=1 83.7 / 87.6%
+    //      (better than 2 before the copy-issue move; equal in the engine since)
     //   1  as 2 with 16-deep stages in a 3-deep ring (1.2% slower per batch)
     //   0  128x128 (Big) / 128x64 (Narrow) tiles, 1 CTA/SM, 16-deep 4-deep ring (9% slower)
     // Measured and dropped: 64x128 tiles of 4 warps of 32x64 (16- or 32-deep), 4 warps
     // with 32-deep double-buffered stages, 128x128 with 32-deep stages (1 CTA/SM).
+    // For reference, cuBLAS's FP64 GEMM on this GPU is an sm80 CUTLASS kernel (64x128
+    // tiles, 4 warps, 16-deep 3-stage ring, 2 CTAs/SM): 96.5% tensor-pipe active at 8192^3.
     // DIAM_B200_GEMM_CFG forces one configuration for every shape but Square.
     static const int cfg = [] {
         const char* e = std::getenv("DIAM_B200_GEMM_CFG");
         return e ? std::atoi(e) : -1;
     }();
-    const int c = cfg >= 0 ? cfg : shape == GemmShape::Stream ? 4 : 2;
+    const int c = cfg >= 0 ? cfg : 2;
     if (shape == GemmShape::Square) {
         launch<Cfg<128, 128, 16, 4, AK, BKM>, AK, BKM>(g, batch, stream);
         return;

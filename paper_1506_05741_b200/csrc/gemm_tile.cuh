@@ -141,31 +141,35 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
     for (int kt = 0; kt < KT; ++kt) {
         cp_async_wait<CF::STAGES - 2>();
         __syncthreads();
-        {
-            const int nk = kt + CF::STAGES - 1;
-            if (nk < KT) issue(nk, nk % CF::STAGES);
-            cp_async_commit();
-        }
-        if (!compute) continue;
+        const int nk = kt + CF::STAGES - 1;
         const double* a_s = sA + (kt % CF::STAGES) * CF::A_STAGE;
         const double* b_s = sB + (kt % CF::STAGES) * CF::B_STAGE;
 #pragma unroll
         for (int kk = 0; kk < CF::BK; kk += 4) {
-            double af[CF::MI], bf[CF::NI];
+            if (compute) {
+                double af[CF::MI], bf[CF::NI];
 #pragma unroll
-            for (int i = 0; i < CF::MI; ++i) {
-                const int m = wm0 + i * 8 + fr, k = kk + fk;
-                af[i] = AK ? a_s[m * CF::A_STRIDE + k] : a_s[k * CF::A_STRIDE + m];
+                for (int i = 0; i < CF::MI; ++i) {
+                    const int m = wm0 + i * 8 + fr, k = kk + fk;
+                    af[i] = AK ? a_s[m * CF::A_STRIDE + k] : a_s[k * CF::A_STRIDE + m];
+                }
+#pragma unroll
+                for (int j = 0; j < CF::NI; ++j) {
+                    const int n = wn0 + j * 8 + fr, k = kk + fk;
+                    bf[j] = BKM ? b_s[n * CF::B_STRIDE + k] : b_s[k * CF::B_STRIDE + n];
+                }
+#pragma unroll
+                for (int i = 0; i < CF::MI; ++i)
+#pragma unroll
+                    for (int j = 0; j < CF::NI; ++j) dmma(acc[i][j], af[i], bf[j]);
             }
-#pragma unroll
-            for (int j = 0; j < CF::NI; ++j) {
-                const int n = wn0 + j * 8 + fr, k = kk + fk;
-                bf[j] = BKM ? b_s[n * CF::B_STRIDE + k] : b_s[k * CF::B_STRIDE + n];
+            if (kk == 0) {
+                // the next stage's copies go out behind the first DMMAs of this one, so the
+                // tensor pipe restarts right after the barrier (the copy issue is ~150
+                // instructions per thread). Stage nk % STAGES was consumed before the barrier.
+                if (nk < KT) issue(nk, nk % CF::STAGES);
+                cp_async_commit();
             }
-#pragma unroll
-            for (int i = 0; i < CF::MI; ++i)
-#pragma unroll
-                for (int j = 0; j < CF::NI; ++j) dmma(acc[i][j], af[i], bf[j]);
         }
     }
     cp_async_wait<0>();
