@@ -688,13 +688,29 @@ void Engine::end_windows() {
     std::vector<Ladder> lad(groups_.size());
     for (size_t m = 0; m < M; ++m) {
         std::vector<size_t> pending;
-        for (size_t i = 0; i < groups_.size(); ++i) {
-            if (!tail_begin(groups_[i], plans[m], lad[i])) {
-                pending.push_back(i);
-                continue;
+        // groups in the order their factorizations finish (polled), not in index order: a
+        // group whose refactor is done gets its next window at once
+        std::vector<size_t> todo(groups_.size());
+        for (size_t i = 0; i < todo.size(); ++i) todo[i] = i;
+        while (!todo.empty()) {
+            for (auto it = todo.begin(); it != todo.end();) {
+                const size_t i = *it;
+                if (plans[m].refactor) {
+                    const cudaError_t q = cudaEventQuery(groups_[i].status_ev);
+                    if (q == cudaErrorNotReady) {
+                        ++it;
+                        continue;
+                    }
+                    DGB_CUDA(q);
+                }
+                it = todo.erase(it);
+                if (!tail_begin(groups_[i], plans[m], lad[i])) {
+                    pending.push_back(i);
+                    continue;
+                }
+                tail_finish(groups_[i], plans[m]);
+                if (m + 1 < M) enqueue_head(groups_[i], plans[m + 1]);
             }
-            tail_finish(groups_[i], plans[m]);
-            if (m + 1 < M) enqueue_head(groups_[i], plans[m + 1]);
         }
         while (!pending.empty()) {
             std::vector<size_t> still;
