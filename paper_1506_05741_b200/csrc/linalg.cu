@@ -33,34 +33,45 @@ __global__ void mean_update_kernel(double* mean, int64_t mean_stride, const doub
 }
 
 // C = wg*Sg + wl*Sl - mb mb^T on the lower triangle, 0 above; optional jitter on the diagonal.
+// One CTA per pair of rows (p, d-1-p) of one chain: the two rows hold d+1 lower entries
+// together, so every CTA moves the same bytes and all threads work (a CTA per row left
+// half the threads idle and made ~2d tiny CTAs per chain).
 __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const double* mg, const double* Sl,
                                  int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl,
                                  double* mb, int64_t mb_stride, int d, int64_t ld, const int* mask,
                                  double jitter_eps, const double* tr, const double* ax, const double* axr) {
     const int c = blockIdx.z;
     if (mask && !mask[c]) return;
-    const int i = blockIdx.y;  // row
-    double* Crow = C_out[c] + (int64_t)i * ld;
-    if (i == d) {  // augmented row r = x - x_ref (solved by the POTRF for the usable guard)
-        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x)
-            Crow[j] = ax[c * ld + j] - (axr ? axr[c * ld + j] : 0.0);
+    const int npairs = (d + 1) / 2;
+    const int p = blockIdx.y;
+    if (p == npairs) {  // augmented row r = x - x_ref (solved by the POTRF for the usable guard)
+        double* Crow = C_out[c] + (int64_t)d * ld;
+        for (int j = threadIdx.x; j < d; j += blockDim.x) Crow[j] = ax[c * ld + j] - (axr ? axr[c * ld + j] : 0.0);
         return;
     }
-    const double* Sgr = Sg + (int64_t)i * ld;
-    const double* Slr = Sl + c * sl_stride + (int64_t)i * ld;
+    const int r1 = p, r2 = d - 1 - p;  // r1 == r2: the middle row of an odd d
     const double* mlc = ml + c * ml_stride;
-    // blended mean (proj/src/moments.cpp:44); every row block recomputes what it needs
-    const double mbi = wg * mg[i] + wl * mlc[i];
-    if (blockIdx.x == 0 && threadIdx.x == 0) mb[c * mb_stride + i] = mbi;
+    // blended mean (proj/src/moments.cpp:44)
+    const double mb1 = wg * mg[r1] + wl * mlc[r1];
+    const double mb2 = wg * mg[r2] + wl * mlc[r2];
+    if (threadIdx.x == 0) {
+        mb[c * mb_stride + r1] = mb1;
+        mb[c * mb_stride + r2] = mb2;
+    }
     // Lower triangle only. The strict upper part of a workspace factor is zero already
     // (zeroed at allocation and by set_identity; the POTRF zeroes the strict upper part of
     // every diagonal block it factors, the only upper entries its GEMMs touch), and it
     // stays zero through factor/workspace pointer swaps.
-    // Pairs of columns per thread (rows are 64-byte aligned: ld is a multiple of 8).
+    // Column pairs (rows are 64-byte aligned: ld is a multiple of 8), both rows flattened.
     const double jit = jitter_eps > 0.0 ? jitter_eps * (tr[c] / (double)d) : 0.0;  // proposal.cpp:229-231
-    for (int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x); j <= i; j += 2 * gridDim.x * blockDim.x) {
-        const double2 sg = *reinterpret_cast<const double2*>(Sgr + j);
-        const double2 sl = *reinterpret_cast<const double2*>(Slr + j);
+    const int q1 = (r1 + 2) / 2, q2 = r2 == r1 ? 0 : (r2 + 2) / 2;
+    for (int q = threadIdx.x; q < q1 + q2; q += blockDim.x) {
+        const bool first = q < q1;
+        const int i = first ? r1 : r2;
+        const int j = 2 * (first ? q : q - q1);
+        const double mbi = first ? mb1 : mb2;
+        const double2 sg = *reinterpret_cast<const double2*>(Sg + (int64_t)i * ld + j);
+        const double2 sl = *reinterpret_cast<const double2*>(Sl + c * sl_stride + (int64_t)i * ld + j);
         const double2 g2 = *reinterpret_cast<const double2*>(mg + j);
         const double2 l2 = *reinterpret_cast<const double2*>(mlc + j);
         // covariance :90-101 (S exactly symmetric) of the blend :45-46
@@ -68,6 +79,7 @@ __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const d
         double v1 = (wg * sg.y + wl * sl.y) - mbi * (wg * g2.y + wl * l2.y);
         if (j == i) v0 += jit;
         if (j + 1 == i) v1 += jit;
+        double* Crow = C_out[c] + (int64_t)i * ld;
         if (j + 1 <= i)
             *reinterpret_cast<double2*>(Crow + j) = make_double2(v0, v1);
         else
@@ -481,7 +493,7 @@ void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg, 
                       int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl, double* mb,
                       int64_t mb_stride, int chains, int d, int64_t ld, const int* mask, double jitter_eps,
                       const double* tr, cudaStream_t s, const double* aug_x, const double* aug_xr) {
-    dim3 grid((unsigned)ceil_div(ceil_div(d, 2), 256), d + (aug_x ? 1 : 0), chains);
+    dim3 grid(1, (unsigned)((d + 1) / 2 + (aug_x ? 1 : 0)), chains);
     blend_cov_kernel<<<grid, 256, 0, s>>>(C_out, Sg, mg, Sl, sl_stride, ml, ml_stride, wg, wl, mb, mb_stride, d, ld,
                                           mask, jitter_eps, tr, aug_x, aug_xr);
     DGB_LAUNCH_CHECK();
