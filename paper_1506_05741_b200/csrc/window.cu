@@ -434,11 +434,12 @@ bool try_tma(const StepParams& p, cudaStream_t s) {
     const size_t table = (size_t)p.n_lag * sizeof(double);
     constexpr size_t kMaxSmem = 220 * 1024;
     if (table + 2 * stage > kMaxSmem) return false;
-    // ring depth: deep enough to hide HBM latency, shallow enough that a 92 KB GEMM CTA of
-    // another chain group can share the SM (DIAM_B200_STEP_STAGES overrides)
+    // ring depth: deep enough to hide HBM latency, shallow enough that a 110 KB GEMM CTA of
+    // another chain group can share the SM (d=1024: 6 stages = 100 KB; 6 vs 8 stages
+    // measured equal within 0.3%; DIAM_B200_STEP_STAGES overrides)
     static const int max_ns = [] {
         const char* e = std::getenv("DIAM_B200_STEP_STAGES");
-        return e ? std::max(2, std::atoi(e)) : 8;
+        return e ? std::max(2, std::atoi(e)) : 6;
     }();
     const int NS = (int)std::min<size_t>((size_t)max_ns, (kMaxSmem - table) / stage);
     const size_t smem = NS * stage + table;
