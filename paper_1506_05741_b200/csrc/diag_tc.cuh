@@ -58,8 +58,11 @@ __device__ __forceinline__ void tc_tile(double (&acc)[2], const double* A, int r
     acc[1] = e[1] + o[1];
 }
 
+// pre_L (optional): the 64 columns left of the block (same rows, stride ld), already
+// final; the block is first updated A -= pre_L pre_L^T (the right-looking step a
+// 128-wide block column's second half needs), in shared memory.
 __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_t ld, int jb, double* out,
-                                            int zero_above, int out_ld) {
+                                            int zero_above, int out_ld, const double* pre_L = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int fr = lane >> 2, fk = lane & 3;
     constexpr unsigned kAll = 0xffffffffu;
@@ -79,6 +82,34 @@ __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_
         for (int i = 0; i < 16; ++i) {
             const int e = tid + 256 * i;
             sa[(e >> 6) * kTcS + (e & 63)] = v[i];
+        }
+        if (pre_L) {  // stage pre_L (rows past jb: zero) in the inverse's buffer, free until then
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int e = tid + 256 * i, r = e >> 6, q = e & 63;
+                v[i] = r < jb ? __ldcg(pre_L + (int64_t)r * ld + q) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int e = tid + 256 * i;
+                sx[(e >> 6) * kTcS + (e & 63)] = v[i];
+            }
+        }
+    }
+    if (pre_L) {
+        __syncthreads();
+        // lower 8x8 tiles (ct <= rt) of A -= pre_L pre_L^T, up to 5 per warp
+        for (int t = warp; t < 36; t += 8) {
+            int rt = 0, base = 0;
+            while (base + rt + 1 <= t) {
+                base += rt + 1;
+                ++rt;
+            }
+            const int ct = t - base;
+            double acc[2];
+            tc_tile(acc, sx, 8 * rt, sx, 8 * ct, 64, lane);
+            sa[(8 * rt + fr) * kTcS + 8 * ct + 2 * fk] -= acc[0];
+            sa[(8 * rt + fr) * kTcS + 8 * ct + 2 * fk + 1] -= acc[1];
         }
     }
     if (tid == 0) sc.bad = 0;

@@ -141,7 +141,7 @@ def oracle_chol(m):
     return st, out
 
 
-@pytest.mark.parametrize("mode", ["wide", "narrow", "narrow+regdiag", "dag", "cluster"])
+@pytest.mark.parametrize("mode", ["wide", "fused", "narrow", "narrow+regdiag", "dag", "cluster"])
 @pytest.mark.parametrize("d", [1, 5, 64, 65, 127, 128, 129, 130, 257, 520])
 def test_potrf_batched_vs_oracle(lib, monkeypatch, d, mode):
     # every factorization path: the launch-per-phase blocked POTRF with 128-wide diagonal

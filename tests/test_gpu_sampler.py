@@ -130,7 +130,7 @@ def test_lockstep_chunked_windows_shared_workspace(b200, tmp_path, monkeypatch, 
     assert ties == 0
 
 
-@pytest.mark.parametrize("mode", ["narrow", "dag", "cluster"])
+@pytest.mark.parametrize("mode", ["narrow", "fused", "wide", "dag", "cluster"])
 def test_lockstep_alternative_potrf(b200, tmp_path, monkeypatch, mode):
     # the alternative factorization paths under the full engine (augmented usable-guard
     # row, a ragged last tile: d = 133 = 128 + 5, two chain groups)
