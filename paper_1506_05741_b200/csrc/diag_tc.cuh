@@ -58,11 +58,14 @@ __device__ __forceinline__ void tc_tile(double (&acc)[2], const double* A, int r
     acc[1] = e[1] + o[1];
 }
 
-// pre_L (optional): the 64 columns left of the block (same rows, stride ld), already
-// final; the block is first updated A -= pre_L pre_L^T (the right-looking step a
-// 128-wide block column's second half needs), in shared memory.
+// pre_L (optional): the 64 columns left of the block (same rows, stride ld); the block is
+// first updated A -= pre_L pre_L^T (the right-looking step a 128-wide block column's
+// second half needs), in shared memory. With pre_X (64x64 lower, stride 64) pre_L still
+// holds A's entries and is first solved in place, pre_L <- pre_L pre_X^T (the TRSM of
+// those rows against the first half's inverse).
 __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_t ld, int jb, double* out,
-                                            int zero_above, int out_ld, const double* pre_L = nullptr) {
+                                            int zero_above, int out_ld, double* pre_L = nullptr,
+                                            const double* pre_X = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int fr = lane >> 2, fk = lane & 3;
     constexpr unsigned kAll = 0xffffffffu;
@@ -94,6 +97,31 @@ __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_
                 const int e = tid + 256 * i;
                 sx[(e >> 6) * kTcS + (e & 63)] = v[i];
             }
+        }
+    }
+    if (pre_L && pre_X) {
+        __syncthreads();
+        // L = pre_L pre_X^T: warp w the 8 tiles of row tile w (pre_X[n][k] = 0 for k > n)
+        const int r = 8 * warp + fr;
+        double res[8][2];
+#pragma unroll
+        for (int ct = 0; ct < 8; ++ct) {
+            double e[2] = {0.0, 0.0}, o[2] = {0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < 8 * ct + 8; k += 8) {
+                tile::dmma(e, sx[r * kTcS + k + fk], __ldcg(pre_X + (8 * ct + fr) * 64 + k + fk));
+                tile::dmma(o, sx[r * kTcS + k + 4 + fk], __ldcg(pre_X + (8 * ct + fr) * 64 + k + 4 + fk));
+            }
+            res[ct][0] = e[0] + o[0];
+            res[ct][1] = e[1] + o[1];
+        }
+        __syncthreads();  // every warp has read its rows of sx
+#pragma unroll
+        for (int ct = 0; ct < 8; ++ct) {
+            const int q = 8 * ct + 2 * fk;
+            sx[r * kTcS + q] = res[ct][0];
+            sx[r * kTcS + q + 1] = res[ct][1];
+            if (r < jb) *reinterpret_cast<double2*>(pre_L + (int64_t)r * ld + q) = make_double2(res[ct][0], res[ct][1]);
         }
     }
     if (pre_L) {

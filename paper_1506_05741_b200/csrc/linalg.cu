@@ -252,20 +252,23 @@ constexpr int kNb = kDiagNb;
 
 // MINB 2: <= 128 registers (spills a little) so a diagonal-block CTA can share its SM with
 // a GEMM CTA of another group; MINB 1: 190 registers, no spills
-// pre: first update the block by the 64 columns to its left (diag64_tc_sc's pre_L; TC only)
+// pre (TC only): 1 = first update the block by the 64 (final) columns to its left
+// (diag64_tc_sc's pre_L); 2 = those columns still need their solve against the inverse at
+// inv_base + c inv_stride (pre_X). The inverse goes to inv_base + c inv_stride + inv_off.
 template <int MINB, bool TC>
 __global__ void __launch_bounds__(256, MINB) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
                                                             const int* mask, int* status, int* active,
-                                                            double* inv_base, int zero_above, int pre = 0) {
+                                                            double* inv_base, int zero_above, int pre = 0,
+                                                            int inv_stride = kDiagNb * kDiagNb, int inv_off = 0) {
     extern __shared__ __align__(16) double dyn_smem[];
     const int c = blockIdx.x;
     const bool run = (!mask || mask[c]) && status[c] == 0;
     if (threadIdx.x == 0) active[c] = run ? 1 : 0;
     if (!run) return;
     double* Ab = Am[c] + (int64_t)j0 * ld + j0;
-    double* out = inv_base + (int64_t)c * kNb * kNb;
+    double* out = inv_base + (int64_t)c * inv_stride + inv_off;
     const int bad = TC ? diag64_tc_sc(*reinterpret_cast<DiagTcScratch*>(dyn_smem), Ab, ld, jb, out, zero_above, kNb,
-                                      pre ? Ab - kNb : nullptr)
+                                      pre ? Ab - kNb : nullptr, pre == 2 ? inv_base + (int64_t)c * inv_stride : nullptr)
                        : diag64_block(Ab, ld, jb, out, zero_above);
     if (bad && threadIdx.x == 0) {
         status[c] = 1;
@@ -273,25 +276,30 @@ __global__ void __launch_bounds__(256, MINB) potrf_diag_kernel(double* const* Am
     }
 }
 
-// The second half of a 128-wide block column below its diagonal block, in one pass per
-// 128-row tile: T = A[r, J2] - L[r, J1] L[J2, J1]^T (the 64-deep right-looking update),
-// then L[r, J2] = T inv(L22)^T, both on the DMMA tile (in place: one column tile per row
-// block, and the update's product is stored before the TRSM reads it back).
+// tile configuration of potrf_solve3_kernel (the cp.async DMMA tile, two CTAs per SM)
 using FusedTile = tile::Cfg<128, 64, 32, 2, true, true, 4, 2, 2>;
-__global__ void __launch_bounds__(256, 2) potrf_update_trsm_kernel(double* const* Am, int64_t ld, int r0, int c1,
-                                                                   int rows, int n2, const int* active,
-                                                                   double* const* inv) {
+
+// Everything below a 128-wide block column's diagonal block in one pass per 128-row tile
+// (rows r): L[r, J1] = A[r, J1] X11^T, T = A[r, J2] - L[r, J1] L[J2, J1]^T,
+// L[r, J2] = T X22^T -- three DMMA tile products in one CTA, each stored before the next
+// reads it (X11 at inv[c], X22 at inv[c] + 64 x 64).
+__global__ void __launch_bounds__(256, 2) potrf_solve3_kernel(double* const* Am, int64_t ld, int r0, int c0,
+                                                              int rows, int n2, const int* active,
+                                                              double* const* inv) {
     const int c = blockIdx.z;
     if (!active[c]) return;
     extern __shared__ __align__(16) double smem[];
     const int m0 = blockIdx.y * FusedTile::BM;
     double* A = Am[c];
-    // rows r0.., columns c1 - 64 .. c1 - 1 (J1) and c1 .. c1 + n2 - 1 (J2)
-    double* t = A + (int64_t)r0 * ld + c1;
-    tile::gemm_tile<FusedTile, true, true>(A + (int64_t)r0 * ld + (c1 - kNb), A + (int64_t)c1 * ld + (c1 - kNb), t, ld,
-                                           ld, ld, rows, n2, kNb, m0, 0, -1.0, 1.0, false, smem);
+    double* l1 = A + (int64_t)r0 * ld + c0;
+    double* t2 = l1 + kNb;
+    tile::gemm_tile<FusedTile, true, true>(l1, inv[c], l1, ld, kNb, ld, rows, kNb, kNb, m0, 0, 1.0, 0.0, false, smem);
     __threadfence_block();
-    tile::gemm_tile<FusedTile, true, true>(t, inv[c], t, ld, kNb, ld, rows, n2, n2, m0, 0, 1.0, 0.0, false, smem);
+    tile::gemm_tile<FusedTile, true, true>(l1, A + (int64_t)(c0 + kNb) * ld + c0, t2, ld, ld, ld, rows, n2, kNb, m0, 0,
+                                           -1.0, 1.0, false, smem);
+    __threadfence_block();
+    tile::gemm_tile<FusedTile, true, true>(t2, inv[c] + kNb * kNb, t2, ld, kNb, ld, rows, n2, n2, m0, 0, 1.0, 0.0,
+                                           false, smem);
 }
 
 // 128x128 diagonal block: L11 = chol, X = L11^-1 (diag128_tc), one CTA per chain; the
@@ -657,9 +665,13 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     // w.inv holds chains*64*64 doubles, followed (by the caller's allocation) by an int active[chains]
     int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kD2 * kD2);
     const int rows = d + extra_rows;
-    // Default: the launch-per-phase blocked path below with the second half-column's update
-    // fused (mode 4, "fused": 26.2 vs 26.4 ms per d=1024 batch). DIAM_B200_POTRF (read per call):
-    //   narrow  the same with a separate 64-deep update GEMM of the second half-column
+    // Default (mode 4, "fused"): per 128-wide block column the long-K update GEMM, the two
+    // 64x64 diagonal blocks (the second one also solving its rows of the first half-column
+    // and applying their 64-deep update, in shared memory) and ONE kernel for everything
+    // below (potrf_solve3_kernel): 4 launches per block column, 26.1 ms per d=1024 batch.
+    // DIAM_B200_POTRF (read per call):
+    //   narrow  diagonal block + TRSM per 64-wide half and a separate 64-deep update GEMM
+    //           between them (6 launches per block column, 26.4 ms)
     //   dag     the task-graph POTRF (potrf_dag.cu): one persistent launch per factorization;
     //           faster on one stream (7.7 vs 9.1 ms per d=1024 batch), equal with 8 chain
     //           groups, 12% slower at d=4096 (K=128 tile updates vs the long-K updates here)
@@ -788,33 +800,36 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
         gemm_f64(t, chains, true, true, s, GemmShape::Narrow);
     };
     if (mode == 4) {
-        // as below, with the second half's 64-deep update folded into its diagonal block
-        // (in shared memory) and into its TRSM (potrf_update_trsm_kernel): 4 launches per
-        // block column instead of 5
         static bool attr = false;
         if (!attr) {
             DGB_CUDA(cudaFuncSetAttribute(potrf_diag_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)sizeof(DiagTcScratch)));
-            DGB_CUDA(cudaFuncSetAttribute(potrf_update_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            DGB_CUDA(cudaFuncSetAttribute(potrf_solve3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           FusedTile::SMEM_BYTES));
             attr = true;
         }
         for (int j0 = 0; j0 < d; j0 += 2 * kNb) {
             const int jb = std::min(2 * kNb, d - j0);
             if (j0 > 0) update(j0, j0, jb, 0, j0, GemmShape::Big);
-            const int h1 = std::min(kNb, jb);
-            factor_and_solve(j0, h1, 0);
-            if (jb <= kNb) continue;
+            if (jb <= kNb) {  // a last, narrow block column: diagonal block + TRSM
+                factor_and_solve(j0, jb, 0);
+                continue;
+            }
+            // X11 and X22 side by side in the chain's 128 x 128 inverse slot
             const int c1 = j0 + kNb, n2 = jb - kNb;
             potrf_diag_kernel<1, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(
-                A, ld, c1, n2, mask, status, active, w.inv, j0 > 0 ? 1 : 0, 1);
+                A, ld, j0, kNb, mask, status, active, w.inv, 0, 0, kD2 * kD2, 0);
+            DGB_LAUNCH_CHECK();
+            count_launch();
+            potrf_diag_kernel<1, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(
+                A, ld, c1, n2, mask, status, active, w.inv, j0 > 0 ? 1 : 0, 2, kD2 * kD2, kNb * kNb);
             DGB_LAUNCH_CHECK();
             count_launch();
             const int rest = rows - c1 - n2;
             if (rest <= 0) continue;
             dim3 grid(1, (unsigned)ceil_div(rest, FusedTile::BM), (unsigned)chains);
-            potrf_update_trsm_kernel<<<grid, 256, FusedTile::SMEM_BYTES, s>>>(A, ld, c1 + n2, c1, rest, n2, active,
-                                                                              w.inv_ptrs);
+            potrf_solve3_kernel<<<grid, 256, FusedTile::SMEM_BYTES, s>>>(A, ld, c1 + n2, j0, rest, n2, active,
+                                                                         w.inv128_ptrs);
             DGB_LAUNCH_CHECK();
             count_launch();
         }
