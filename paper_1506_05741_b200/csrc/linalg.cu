@@ -810,7 +810,9 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
         }
         for (int j0 = 0; j0 < d; j0 += 2 * kNb) {
             const int jb = std::min(2 * kNb, d - j0);
-            if (j0 > 0) update(j0, j0, jb, 0, j0, GemmShape::Big);
+            // lower part of the diagonal tile only: the warps above the diagonal skip their
+            // DMMAs (25.9 vs 26.1 ms per d=1024 batch) and the upper quarter keeps its zeros
+            if (j0 > 0) update(j0, j0, jb, 0, j0, GemmShape::Big, 1);
             if (jb <= kNb) {  // a last, narrow block column: diagonal block + TRSM
                 factor_and_solve(j0, jb, 0);
                 continue;
