@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) gemm_f64_kernel(GemmBat
     double alpha = p.alpha;
     if (p.alpha_vec) alpha *= p.alpha_vec[b] * p.alpha_vec_mul;
     tile::gemm_tile<CF, AK, BKM>(p.A[b] + p.a_off, p.B[b] + p.b_off, p.C[b] + p.c_off, p.lda, p.ldb, p.ldc, p.M, p.N,
-                                 K, m0, n0, alpha, p.beta, p.tri_c_lower != 0, smem);
+                                 K, m0, n0, alpha, p.beta, p.tri_c_lower != 0, smem, p.tri_b_lower != 0);
 }
 
 template <class CF, bool AK, bool BKM>

@@ -84,7 +84,7 @@ __device__ __forceinline__ void load_tile(double* s, const double* g, int64_t ld
 template <class CF, bool AK, bool BKM>
 __device__ __forceinline__ void gemm_tile(const double* A, const double* B, double* Cp, int64_t lda, int64_t ldb,
                                           int64_t ldc, int M, int N, int K, int m0, int n0, double alpha,
-                                          double beta, bool tri_c_lower, double* smem) {
+                                          double beta, bool tri_c_lower, double* smem, bool tri_b_lower = false) {
     __syncthreads();
     double* sA = smem;
     double* sB = smem + CF::STAGES * CF::A_STAGE;
@@ -144,9 +144,12 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
         const int nk = kt + CF::STAGES - 1;
         const double* a_s = sA + (kt % CF::STAGES) * CF::A_STAGE;
         const double* b_s = sB + (kt % CF::STAGES) * CF::B_STAGE;
+        // B lower-triangular (B(k,n) = 0 for k > n): a stage entirely below this warp's
+        // columns multiplies zeros only
+        const bool live = compute && !(tri_b_lower && kt * CF::BK > n0 + wn0 + CF::WN - 1);
 #pragma unroll
         for (int kk = 0; kk < CF::BK; kk += 4) {
-            if (compute) {
+            if (live) {
                 double af[CF::MI], bf[CF::NI];
 #pragma unroll
                 for (int i = 0; i < CF::MI; ++i) {

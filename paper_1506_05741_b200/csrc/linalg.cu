@@ -293,13 +293,14 @@ __global__ void __launch_bounds__(256, 2) potrf_solve3_kernel(double* const* Am,
     double* A = Am[c];
     double* l1 = A + (int64_t)r0 * ld + c0;
     double* t2 = l1 + kNb;
-    tile::gemm_tile<FusedTile, true, true>(l1, inv[c], l1, ld, kNb, ld, rows, kNb, kNb, m0, 0, 1.0, 0.0, false, smem);
+    tile::gemm_tile<FusedTile, true, true>(l1, inv[c], l1, ld, kNb, ld, rows, kNb, kNb, m0, 0, 1.0, 0.0, false, smem,
+                                           true);
     __threadfence_block();
     tile::gemm_tile<FusedTile, true, true>(l1, A + (int64_t)(c0 + kNb) * ld + c0, t2, ld, ld, ld, rows, n2, kNb, m0, 0,
                                            -1.0, 1.0, false, smem);
     __threadfence_block();
     tile::gemm_tile<FusedTile, true, true>(t2, inv[c] + kNb * kNb, t2, ld, kNb, ld, rows, n2, n2, m0, 0, 1.0, 0.0,
-                                           false, smem);
+                                           false, smem, true);
 }
 
 // 128x128 diagonal block: L11 = chol, X = L11^-1 (diag128_tc), one CTA per chain; the
