@@ -337,16 +337,9 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
     identity_ = all_identity;
 
     // derived device state: G x, G x_ref and y = L^-1 (x - x_ref)
-    {
-        double** dp = nullptr;  // {x, g, x_ref, g_ref} as one-element operand arrays
-        DGB_CUDA(cudaMalloc(&dp, 4 * sizeof(double*)));
-        double* hp[4] = {x_, g_, xr_, gr_};
-        DGB_CUDA(cudaMemcpy(dp, hp, sizeof hp, cudaMemcpyHostToDevice));
-        refresh_g(dp, dp + 1, C, stream_);
-        if (k_.adaptive_ref) refresh_g(dp + 2, dp + 3, C, stream_);
-        DGB_CUDA(cudaStreamSynchronize(stream_));
-        cudaFree(dp);
-    }
+    refresh_g(x_, g_, C, stream_);
+    if (k_.adaptive_ref) refresh_g(xr_, gr_, C, stream_);
+    DGB_CUDA(cudaStreamSynchronize(stream_));
     bool have_y = false;
     if (!r.at_end()) {
         char magic[8];

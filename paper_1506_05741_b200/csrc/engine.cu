@@ -410,8 +410,6 @@ void Engine::init_chains() {
     DGB_CUDA(cudaMemcpy(ukeys_, uk.data(), C * sizeof(PhiloxKey), cudaMemcpyHostToDevice));
     DGB_CUDA(cudaMemcpy(ikeys_, ik.data(), C * sizeof(PhiloxKey), cudaMemcpyHostToDevice));
 
-    double** xp = ptr_array(A, x_, 0, 1);
-    double** gp = ptr_array(A, g_, 0, 1);
     DGB_CUDA(cudaStreamSynchronize(0));  // the buffers above are zeroed before stream_ uses them
     // x0 = dispersion * N(0, I) from the "init" stream (runner.cpp:131-132)
     launch_normal_vec(x_, ld_, C, d_, ikeys_, 0, cfg_.init_dispersion, stream_);
@@ -421,7 +419,7 @@ void Engine::init_chains() {
     DGB_CUDA(cudaMemcpyAsync(beta_, b.data(), C * 8, cudaMemcpyHostToDevice, stream_));
     identity_ = true;
     // log pi(x0), quad(x0) (proposal.cpp:107-108)
-    refresh_g(xp, gp, C, stream_);
+    refresh_g(x_, g_, C, stream_);
     launch_eval_logpi(x_, g_, inv_eig_, bcoef_, twisted_, logpi_, C, d_, ld_, stream_);
     if (k_.pcn_form()) {
         const double infl = k_.noise_infl();
@@ -474,10 +472,6 @@ void Engine::make_groups(int n) {
         g.Wp = Wp_ + g.off;
         g.Xip = Xip_ + g.off;
         g.Sp = Sp_ + g.off;
-        g.xp = ptr_array(A, x_ + g.off * ld_, 0, 1);
-        g.gp = ptr_array(A, g_ + g.off * ld_, 0, 1);
-        g.xrp = ptr_array(A, xr_ + g.off * ld_, 0, 1);
-        g.grp = ptr_array(A, gr_ + g.off * ld_, 0, 1);
         g.Xib = ptr_array(A, Xi_ + g.off * win_, 0, 1);
         g.Hb = ptr_array(A, H_ + g.off * win_, 0, 1);
         // per-group inverse-block scratch (+ int active[C] tail): groups factor concurrently
@@ -490,21 +484,11 @@ void Engine::make_groups(int n) {
     }
 }
 
-void Engine::refresh_g(double* const* vec, double* const* out, int chains, cudaStream_t s) {
-    // out = vec G^T: rows = chains (G x for every chain of the group)
-    GemmBatch g{};
-    g.A = (const double* const*)vec;
-    g.B = (const double* const*)Gp_;
-    g.C = out;
-    g.lda = ld_;
-    g.ldb = ld_;
-    g.ldc = ld_;
-    g.M = chains;
-    g.N = d_;
-    g.K = d_;
-    g.alpha = 1.0;
-    g.beta = 0.0;
-    gemm("gemv_state", g, 1, true, true, s, GemmShape::Narrow);
+void Engine::refresh_g(const double* x, double* out, int chains, cudaStream_t s) {
+    // out = x G^T: G x for every chain of the group (rows of stride ld)
+    timed_begin(s);
+    launch_gemv_rows(G_, ld_, d_, x, out, chains, s);
+    timed_end("gemv_state", 2.0 * chains * (double)d_ * d_, s);
 }
 
 void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s, GemmShape sh) {
@@ -989,7 +973,7 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
     if (p.move_ref) {
         if (!p.refactor) launch_blend_mean(mg_, mean_ + o * ld_, p.wg, p.wl, mb_ + o * ld_, C, d_, ld_, s);
         DGB_CUDA(cudaMemcpyAsync(xr_ + o * ld_, mb_ + o * ld_, (size_t)C * ld_ * 8, cudaMemcpyDeviceToDevice, s));
-        refresh_g(g.xrp, g.grp, C, s);
+        refresh_g(xr_ + o * ld_, gr_ + o * ld_, C, s);
     }
     // quad with the current factor (proposal.cpp:211) and y for the next window's recursion.
     // With a fixed reference point y = L^-1 (x - x_ref) is carried exactly through the
@@ -1002,7 +986,7 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
         timed_end("trsv", 0.0, s);
     }
     // G x re-anchored at every boundary so the step recursion never drifts
-    refresh_g(g.xp, g.gp, C, s);
+    refresh_g(x_ + o * ld_, g_ + o * ld_, C, s);
     if (g.sr != g.s) {  // the next window's steps follow the tail
         DGB_CUDA(cudaEventRecord(g.ev_ref, g.sr));
         DGB_CUDA(cudaStreamWaitEvent(g.s, g.ev_ref, 0));

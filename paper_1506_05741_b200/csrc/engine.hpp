@@ -90,7 +90,6 @@ private:
         cudaStream_t s = nullptr;
         cudaEvent_t done = nullptr;
         double **Lp = nullptr, **Lnp = nullptr, **Wp = nullptr, **Xip = nullptr, **Sp = nullptr;
-        double **xp = nullptr, **gp = nullptr, **xrp = nullptr, **grp = nullptr;  // 1-element arrays
         double **Xib = nullptr, **Hb = nullptr;                                     // 1-element arrays
         PotrfWork pw{};
         cudaEvent_t status_ev = nullptr;  // POTRF statuses of the group's last window landed in h_status_
@@ -162,7 +161,7 @@ private:
     void save_checkpoint(double wall);
     void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s,
               GemmShape sh = GemmShape::Big);
-    void refresh_g(double* const* vec, double* const* out, int chains, cudaStream_t s);
+    void refresh_g(const double* x, double* out, int chains, cudaStream_t s);
     void timed_begin(cudaStream_t s);
     void timed_end(const char* name, double flops, cudaStream_t s);
     void resolve_events();

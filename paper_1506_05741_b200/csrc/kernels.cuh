@@ -152,6 +152,8 @@ void launch_eval_logpi(const double* x, const double* g, const double* inv_eig, 
 void launch_blend_mean(const double* mg, const double* ml, double wg, double wl, double* mb, int chains,
                        int d, int64_t ld, cudaStream_t s);
 // out[c][t][0..1] = proj[0..1] . X_c[t], t in [t0, rows)
+// out[c] = G X[c] (G d x d row-major; X, out: one row per chain; stride ld)
+void launch_gemv_rows(const double* G, int64_t ld, int d, const double* X, double* out, int chains, cudaStream_t s);
 void launch_project_rows(const double* X, int64_t win_stride, int64_t ld, int chains, int rows, int t0,
                          int d, const double* proj, double* out, int out_ld, cudaStream_t s);
 void launch_copy_vecs(double* dst, const double* src, int64_t n, const int* mask_per_chain,

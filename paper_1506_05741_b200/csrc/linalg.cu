@@ -246,6 +246,56 @@ __global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(double* const* Lm, i
     }
 }
 
+// ------------------------------------------------------------------ G x for a chain group
+// out[c] = G X[c] for C chains (G: d x d row-major; X, out: one row per chain; all with
+// stride ld): a CTA takes 16 rows of G
+// and 8 chains, a warp two rows; lanes stride along k with 16-byte loads, and the 16
+// (row, chain) partial sums are combined by recursive halving (16 shuffles per warp).
+// One pass over G per 8 chains instead of a 128-row DMMA tile with 4 valid rows.
+__global__ void __launch_bounds__(256) gemv_rows_kernel(const double* G, int64_t ld, int d, const double* X,
+                                                        double* out, int chains) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * 16 + 2 * warp;
+    const int c0 = blockIdx.y * 8;
+    const int nc = min(8, chains - c0);
+    const double* xs[8];
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) xs[ch] = ch < nc ? X + (int64_t)(c0 + ch) * ld : nullptr;
+    const double* g0 = G + (int64_t)min(n0, d - 1) * ld;
+    const double* g1 = G + (int64_t)min(n0 + 1, d - 1) * ld;
+    double v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = 0.0;
+    const int dk = (d + 1) & ~1;  // rows are zero-padded to ld (a multiple of 8)
+    for (int k = 2 * lane; k < dk; k += 64) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(g0 + k));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(g1 + k));
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+            if (ch >= nc) break;
+            const double2 x = *reinterpret_cast<const double2*>(xs[ch] + k);
+            v[ch] = fma(a.y, x.y, fma(a.x, x.x, v[ch]));
+            v[8 + ch] = fma(b.y, x.y, fma(b.x, x.x, v[8 + ch]));
+        }
+    }
+    // recursive halving: after the xor-16/8/4/2 steps lane l holds slot l >> 1 summed over 16
+    // lanes; the xor-1 step completes the sum over the warp
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1) {
+        const int x = w * 2;  // partner distance 16, 8, 4, 2
+        const bool upper = lane & x;
+#pragma unroll
+        for (int i = 0; i < w; ++i) {
+            const double send = upper ? v[i] : v[i + w];
+            const double keep = upper ? v[i + w] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, x);
+        }
+    }
+    const double tot = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+    const int slot = lane >> 1, r = slot >> 3, ch = slot & 7;
+    if (!(lane & 1) && ch < nc && n0 + r < d) out[(int64_t)(c0 + ch) * ld + n0 + r] = tot;
+}
+
 // ------------------------------------------------------------------ Cholesky diagonal block
 constexpr int kNb = kDiagNb;
 
@@ -517,6 +567,14 @@ void launch_mean_update(double* mean, int64_t mean_stride, const double* X, int6
     dim3 grid((unsigned)ceil_div(d, 128), chains);
     mean_update_kernel<<<grid, 128, 0, s>>>(mean, mean_stride, X, win_stride, ld, d, k_off, k, n_prev / total,
                                             1.0 / total);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_gemv_rows(const double* G, int64_t ld, int d, const double* X, double* out, int chains, cudaStream_t s) {
+    if (chains <= 0 || d <= 0) return;
+    dim3 grid((unsigned)ceil_div(d, 16), (unsigned)ceil_div(chains, 8));
+    gemv_rows_kernel<<<grid, 256, 0, s>>>(G, ld, d, X, out, chains);
     DGB_LAUNCH_CHECK();
     count_launch();
 }
