@@ -20,16 +20,30 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ------------------------------------------------------------------ moments
-__global__ void mean_update_kernel(double* mean, int64_t mean_stride, const double* X, int64_t win_stride,
-                                   int64_t ld, int d, int k_off, int k, double keep, double add) {
+// mean <- keep * mean + add * (sum of rows k_off .. k_off + k - 1 of the chain's window).
+// A CTA takes 32 columns: its 8 warps sum interleaved rows (coalesced 256-byte row pieces,
+// k/8 independent loads per thread), then the 8 partial sums are added in warp order.
+__global__ void __launch_bounds__(256) mean_update_kernel(double* mean, int64_t mean_stride, const double* X,
+                                                          int64_t win_stride, int64_t ld, int d, int k_off, int k,
+                                                          double keep, double add) {
+    __shared__ double part[8][32];
     const int c = blockIdx.y;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= d) return;
-    const double* Xc = X + c * win_stride + (int64_t)k_off * ld + i;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int i = blockIdx.x * 32 + lane;
     double s = 0.0;
-    for (int r = 0; r < k; ++r) s += Xc[(int64_t)r * ld];
-    double* m = mean + c * mean_stride + i;
-    *m = keep * *m + add * s;
+    if (i < d) {
+        const double* Xc = X + c * win_stride + (int64_t)k_off * ld + i;
+        for (int r = warp; r < k; r += 8) s += Xc[(int64_t)r * ld];
+    }
+    part[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && i < d) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += part[w][lane];
+        double* m = mean + c * mean_stride + i;
+        *m = keep * *m + add * t;
+    }
 }
 
 // C = wg*Sg + wl*Sl - mb mb^T on the lower triangle, 0 above; optional jitter on the diagonal.
@@ -564,8 +578,8 @@ void launch_mean_update(double* mean, int64_t mean_stride, const double* X, int6
                         int chains, int d, int k_off, int k, double n_prev, cudaStream_t s) {
     if (k <= 0) return;
     const double total = n_prev + k;
-    dim3 grid((unsigned)ceil_div(d, 128), chains);
-    mean_update_kernel<<<grid, 128, 0, s>>>(mean, mean_stride, X, win_stride, ld, d, k_off, k, n_prev / total,
+    dim3 grid((unsigned)ceil_div(d, 32), chains);
+    mean_update_kernel<<<grid, 256, 0, s>>>(mean, mean_stride, X, win_stride, ld, d, k_off, k, n_prev / total,
                                             1.0 / total);
     DGB_LAUNCH_CHECK();
     count_launch();
