@@ -22,12 +22,13 @@ for k in mh_window normals blend_cov; do
     $full -k regex:$k -s 4 -o gpurun_out/${tag}_${k} $cmd > gpurun_out/${tag}_${k}.log 2>&1
 done
 fi
-# the POTRF's largest left-looking update (block column 512 of 1024) and a diagonal block,
-# from the third batch (the first batch's adaptations are rank-deficient: jitter ladder,
-# chains that fail early skip the remaining launches)
+# the POTRF kernels from the third batch (the first batch's adaptations are rank-deficient:
+# jitter ladder, chains that fail early skip the remaining launches): a long-K update GEMM,
+# a diagonal block and the below-diagonal solve kernel
 cmd3="python tools/profile_step.py --batches 2"
 $cmd3 > gpurun_out/${tag}_plain3.log 2>&1
-$full --nvtx --nvtx-include "potrf/" -k regex:gemm_f64 -s 325 -o gpurun_out/${tag}_potrf_update $cmd3 \
+$full --nvtx --nvtx-include "potrf/" -k regex:gemm_f64 -s 45 -o gpurun_out/${tag}_potrf_update $cmd3 \
     > gpurun_out/${tag}_potrf_update.log 2>&1
 $full -k regex:potrf_diag -s 200 -o gpurun_out/${tag}_potrf_diag $cmd3 > gpurun_out/${tag}_potrf_diag.log 2>&1
+$full -k regex:potrf_solve3 -s 100 -o gpurun_out/${tag}_potrf_solve3 $cmd3 > gpurun_out/${tag}_potrf_solve3.log 2>&1
 echo captured
