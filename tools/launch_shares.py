@@ -22,9 +22,10 @@ def cls(name, grid):
         if gz == 1 and gy == 1:
             return "gemv_state"
         return "potrf"  # the factorization's update / TRSM GEMMs
-    for k in ("potrf_diag", "mh_window", "normals", "blend_cov", "mean_update", "trace_floor", "sum_chains"):
+    for k in ("potrf_diag", "potrf_solve3", "gemv_rows", "mh_window", "normals", "blend_cov", "mean_update",
+              "trace_floor", "sum_chains"):
         if k in name:
-            return "potrf" if k == "potrf_diag" else k
+            return "potrf" if k.startswith("potrf") else "gemv_state" if k == "gemv_rows" else k
     return "other"
 
 
