@@ -1,6 +1,7 @@
 // engine.cu — B200 sampler engine (see engine.hpp). Reference semantics cited inline
 // (paths relative to /root/reference/proj/).
 #include "engine.hpp"
+#include "blas.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -762,7 +763,18 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         h.K = d_;
         h.alpha = 1.0;
         h.beta = 0.0;
-        if (rows == Lc_) {
+        // DIAM_B200_TARGET_GEMM=dmma|cublas: the plain (C Lc) x d x d product on the DMMA
+        // kernel or through cuBLAS (read once per process)
+        static const bool use_cublas = [] {
+            const char* e = std::getenv("DIAM_B200_TARGET_GEMM");
+            return e && std::string(e) == "cublas";
+        }();
+        if (rows == Lc_ && use_cublas) {
+            timed_begin(s);
+            const bool ok = cublas_gemm_abt(s, C * Lc_, d_, d_, Xi_ + o * win_, ld_, G_, ld_, H_ + o * win_, ld_);
+            timed_end("gemm_target", 2.0 * C * Lc_ * (double)d_ * d_, s);
+            require(ok, Err::Unknown, "DIAM_B200_TARGET_GEMM=cublas: libcublas.so.12 not available");
+        } else if (rows == Lc_) {
             h.A = (const double* const*)g.Xib;
             h.C = g.Hb;
             h.M = C * Lc_;  // the group's window chunks are one contiguous (C Lc) x ld matrix
