@@ -115,6 +115,40 @@ void pinned_release(void* p) {
     g_pinned_free.emplace(g_pinned_size[p], p);
 }
 
+// Streams are kept for the process too (creating and destroying the 33 prioritised streams
+// of a 16-group engine costs ~3 ms per diam_sample call); an engine returns its streams
+// idle. Keyed by device and priority.
+std::mutex g_stream_mu;
+std::multimap<std::pair<int, int>, cudaStream_t> g_stream_free;
+
+cudaStream_t stream_acquire(int priority) {
+    int dev = 0;
+    DGB_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(g_stream_mu);
+        auto it = g_stream_free.find({dev, priority});
+        if (it != g_stream_free.end()) {
+            cudaStream_t st = it->second;
+            g_stream_free.erase(it);
+            return st;
+        }
+    }
+    cudaStream_t st = nullptr;
+    DGB_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, priority));
+    return st;
+}
+
+void stream_release(cudaStream_t st, int priority) {
+    if (!st) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaStreamDestroy(st);
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    g_stream_free.emplace(std::make_pair(dev, priority), st);
+}
+
 struct DeferAllocSync {
     DeferAllocSync() { g_defer_alloc_sync = true; }
     ~DeferAllocSync() { g_defer_alloc_sync = false; }
@@ -149,7 +183,7 @@ Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shar
     fmat_ = (int64_t)(d_ + 1) * ld_;
     twisted_ = tgt_.twisted();
     require(d_ <= 8192, Err::InvalidDimension, "the B200 engine supports d <= 8192");
-    DGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    stream_ = stream_acquire(0);
     DGB_CUDA(cudaEventCreateWithFlags(&main_ev_, cudaEventDisableTiming));
     DeferAllocSync defer;
     static const bool tinit = std::getenv("DIAM_B200_INIT_TIMING") != nullptr;  // phases to stderr
@@ -275,14 +309,8 @@ Engine::~Engine() {
     };
     if (stream_) cudaStreamSynchronize(stream_);
     for (auto& g : groups_) {
-        if (g.sr && g.sr != g.s) {
-            cudaStreamSynchronize(g.sr);
-            cudaStreamDestroy(g.sr);
-        }
-        if (g.s) {
-            cudaStreamSynchronize(g.s);
-            cudaStreamDestroy(g.s);
-        }
+        if (g.sr && g.sr != g.s) stream_release(g.sr, g.prio_sr);
+        if (g.s) stream_release(g.s, g.prio_s);
         if (g.ev_steps) cudaEventDestroy(g.ev_steps);
         if (g.ev_ref) cudaEventDestroy(g.ev_ref);
         if (g.done) cudaEventDestroy(g.done);
@@ -305,7 +333,7 @@ Engine::~Engine() {
     pinned_release(h_stats_);
     pinned_release(h_out_);
     if (out_ev_) cudaEventDestroy(out_ev_);
-    if (stream_) cudaStreamDestroy(stream_);
+    stream_release(stream_, 0);
     mark("done");
 }
 
@@ -457,9 +485,14 @@ void Engine::make_groups(int n) {
             DGB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
             const int ps = prio == 1 ? least : (prio == 2 ? greatest : 0);
             const int pr = prio == 1 ? greatest : (prio == 2 ? least : 0);
-            DGB_CUDA(cudaStreamCreateWithPriority(&g.s, cudaStreamNonBlocking, ps));
-            if (prio) DGB_CUDA(cudaStreamCreateWithPriority(&g.sr, cudaStreamNonBlocking, pr));
-            else g.sr = g.s;
+            g.s = stream_acquire(ps);
+            g.prio_s = ps;
+            if (prio) {
+                g.sr = stream_acquire(pr);
+                g.prio_sr = pr;
+            } else {
+                g.sr = g.s;
+            }
             DGB_CUDA(cudaEventCreateWithFlags(&g.ev_steps, cudaEventDisableTiming));
             DGB_CUDA(cudaEventCreateWithFlags(&g.ev_ref, cudaEventDisableTiming));
         }

@@ -88,6 +88,7 @@ private:
     struct Group {
         int off = 0, C = 0;
         cudaStream_t s = nullptr;
+        int prio_s = 0, prio_sr = 0;  // stream priorities (the pool's keys)
         cudaEvent_t done = nullptr;
         double **Lp = nullptr, **Lnp = nullptr, **Wp = nullptr, **Xip = nullptr, **Sp = nullptr;
         double **Xib = nullptr, **Hb = nullptr;                                     // 1-element arrays
