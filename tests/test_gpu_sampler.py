@@ -259,6 +259,23 @@ def test_stopping_rules_and_histories(b200, tmp_path):
     assert doc["schema"] == "diam-run-result/1" and doc["batches"] == 3 and len(doc["iact"]) == 2
 
 
+def test_engines_reuse_pooled_streams_and_host_buffers(b200, monkeypatch):
+    """Engines of different shapes created back to back (and concurrently alive) reuse
+    the process-wide stream and pinned-buffer pools; every run equals a fresh one."""
+    t = b200.target_build("pi1", 24, 2)
+    kw = dict(kernel="diam", chains=8, intervals_per_batch=2, max_batches=2, n_lag=12, n0=0, master_seed=5)
+    ref = b200.sample(t, **kw)
+    for groups in ("1", "2", "4", "8", "3"):
+        monkeypatch.setenv("DIAM_B200_GROUPS", groups)
+        held = b200.engine(t, **kw)  # alive while the next run takes streams from the pool
+        held.run_batches(1)
+        r = b200.sample(t, **kw)
+        del held
+        assert np.array_equal(r.cov(), ref.cov()) and np.array_equal(r.mean(), ref.mean())
+        for p in range(8):
+            assert np.array_equal(r.chain_history(p, "acceptance"), ref.chain_history(p, "acceptance"))
+
+
 def test_launch_counter_moves(b200):
     t = b200.target_build("pi1", 8, 1)
     before = b200.launch_count()
