@@ -333,6 +333,8 @@ Engine::~Engine() {
     pinned_release(h_stats_);
     pinned_release(h_out_);
     if (out_ev_) cudaEventDestroy(out_ev_);
+    if (join_ev_) cudaEventDestroy(join_ev_);
+    if (merge_ev_) cudaEventDestroy(merge_ev_);
     stream_release(stream_, 0);
     mark("done");
 }
@@ -850,6 +852,8 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     sp.trace_lp = p.record ? trace_lp_ + (p.w * C_ + o) * (size_t)Lw_ + r0 : nullptr;
     sp.accept_out = capture_ ? dbg_acc_ + (size_t)o * Lw_ + r0 : nullptr;
     sp.log_ratio_out = capture_ ? dbg_ratio_ + (size_t)o * Lw_ + r0 : nullptr;
+    // the previous batch's trace copies read the buffers the MH steps write
+    if (merge_pending_ && p.record) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
     timed_begin(s);
     launch_mh_window(sp, twisted_, s);
     timed_end("mh_window", 0.0, s);
@@ -860,6 +864,8 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     const int lf = std::clamp(p.first - r0, 0, rows);
     const int kc = rows - lf;
     const uint64_t cb = p.cnt_before + (uint64_t)std::max(0, r0 - p.first);
+    // the merge reads S_ / mean_ and clears mean_; the histories' copies read hist_*
+    if (merge_pending_) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
     if (kc > 0) {
         const double total = (double)(cb + (uint64_t)kc);
         GemmBatch m{};
@@ -1272,14 +1278,30 @@ double Engine::run_batches_timed(int k) {
         if (!timeline_base_) DGB_CUDA(cudaEventCreate(&timeline_base_));
         DGB_CUDA(cudaEventRecord(timeline_base_, stream_));
     }
+    // as the pipelined run loop: batch i + 1's first windows start at batch i's join
+    const bool early = !comm_ && !capture_ && !pool_;
+    if (early && !join_ev_) {
+        DGB_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
+        DGB_CUDA(cudaEventCreateWithFlags(&merge_ev_, cudaEventDisableTiming));
+    }
     for (int i = 0; i < k; ++i) {
-        fork_groups();
-        run_batch_windows(false);
+        if (early && i > 0) {
+            for (auto& g : groups_) DGB_CUDA(cudaStreamWaitEvent(g.s, join_ev_, 0));
+            merge_pending_ = true;
+            begin_windows(false);
+            merge_pending_ = false;
+            end_windows();
+        } else {
+            fork_groups();
+            run_batch_windows(false);
+        }
         join_groups();
+        if (early) DGB_CUDA(cudaEventRecord(join_ev_, stream_));
         merge_batch();
         // the batch statistics and the history copies of a diam_sample batch (on one GPU;
         // the host reads nothing here)
         if (!comm_) enqueue_batch_outputs(M);
+        if (early) DGB_CUDA(cudaEventRecord(merge_ev_, stream_));
         ++batches_done_;
     }
     DGB_CUDA(cudaEventRecord(b, stream_));
@@ -1335,13 +1357,22 @@ RunResult Engine::run() {  // runner.cpp:216-279
             }
             end_windows();
             join_groups();
+            if (!join_ev_) {
+                DGB_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
+                DGB_CUDA(cudaEventCreateWithFlags(&merge_ev_, cudaEventDisableTiming));
+            }
+            DGB_CUDA(cudaEventRecord(join_ev_, stream_));
             merge_batch();
             enqueue_batch_outputs(M);
+            DGB_CUDA(cudaEventRecord(merge_ev_, stream_));
             ++batches_done_;
             head_queued = cap_reason(batches_done_) == nullptr;
             if (head_queued) {
-                fork_groups();
+                // the next batch's first windows start at the join, not after the merge
+                for (auto& g : groups_) DGB_CUDA(cudaStreamWaitEvent(g.s, join_ev_, 0));
+                merge_pending_ = true;
                 begin_windows(cfg_.record_traces);
+                merge_pending_ = false;
             }
             read_batch_outputs(M, ce, me, ps);
         } else {

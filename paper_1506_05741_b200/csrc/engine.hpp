@@ -148,6 +148,11 @@ private:
     void capture_chunk(const Group& g, int r0, int rows);
     void capture_window(size_t w);
     void fork_groups();  // groups wait for the main stream
+    // pipelined loop: the next batch's first windows start right after the join; only
+    // their moment updates (and MH steps when traces are recorded) wait for merge_ev_,
+    // the end of the batch's merge, statistics and output copies
+    cudaEvent_t join_ev_ = nullptr, merge_ev_ = nullptr;
+    bool merge_pending_ = false;
     void join_groups();  // main stream waits for every group
     void merge_batch();
     void batch_stats(double& cov_err, double& mean_err, double& psrf);
