@@ -49,7 +49,8 @@ struct GemmBatch {
 // Big / Narrow: the tile configuration DIAM_B200_GEMM_CFG selects; Square: 128x128 tiles
 // always (one column tile per 128 columns: in-place products whose tile reads columns
 // another tile of the same row block writes)
-// Stream: long-K, write-only window products (TRMM noise, target GEMM)
+// Stream: long-K, write-only window products (TRMM noise, target GEMM); the same tile as
+// Big today (measured equal or better than the 4-warp 64x32 tile), kept apart for tuning
 enum class GemmShape { Big, Narrow, Square, Stream };
 
 // Launch the batched GEMM on `stream`. Layout flags select the template instance.
