@@ -175,6 +175,33 @@ def test_potrf_batched_vs_oracle(lib, monkeypatch, d, mode):
         assert np.linalg.norm(lg @ lg.T - m) / np.linalg.norm(m) <= 1e-10
 
 
+@pytest.mark.parametrize("d", [1024, 1089])
+def test_potrf_default_path_large(lib, d):
+    # the default (fused) factorization at the bench dimension and at a ragged size whose
+    # last block column is narrow (1089 = 8 x 128 + 65)
+    rng = np.random.default_rng(d)
+    batch = 2
+    ld = (d + 7) // 8 * 8
+    mats, host = [], np.zeros((batch, d, ld))
+    for i in range(batch):
+        a = rng.normal(size=(d, d + 16))
+        m = a @ a.T / d + (0.5 + i) * np.eye(d)
+        mats.append(m)
+        host[i, :, :d] = np.tril(m)
+    A = cu(host)
+    status = torch.zeros(batch, dtype=torch.int32, device="cuda")
+    lib.check(lib.lib.diamx_potrf(ptr(A), d * ld, ld, d, batch, ptr(status), None))
+    assert status.cpu().numpy().tolist() == [0] * batch
+    got = A.cpu().numpy()
+    for i, m in enumerate(mats):
+        st, lref = oracle_chol(m)
+        assert st == 0
+        lg = got[i, :, :d]
+        assert np.array_equal(np.triu(lg, 1), np.zeros((d, d)))
+        assert np.linalg.norm(lg - lref) / np.linalg.norm(lref) <= 1e-12
+        assert np.linalg.norm(lg @ lg.T - m) / np.linalg.norm(m) <= 1e-12
+
+
 def test_potrf_detects_not_positive_definite(lib):
     d, ld = 100, 104
     rng = np.random.default_rng(1)
