@@ -841,11 +841,11 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
         if (tc) {
             static bool attr = false;
             if (!attr) {
-                DGB_CUDA(cudaFuncSetAttribute(potrf_diag_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                DGB_CUDA(cudaFuncSetAttribute(potrf_diag_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)sizeof(DiagTcScratch)));
                 attr = true;
             }
-            potrf_diag_kernel<1, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(A, ld, c0, n, mask, status, active,
+            potrf_diag_kernel<2, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(A, ld, c0, n, mask, status, active,
                                                                                   w.inv, zero_above);
         } else {
             potrf_diag_kernel<2, false><<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
@@ -875,7 +875,7 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     if (mode == 4) {
         static bool attr = false;
         if (!attr) {
-            DGB_CUDA(cudaFuncSetAttribute(potrf_diag_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            DGB_CUDA(cudaFuncSetAttribute(potrf_diag_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)sizeof(DiagTcScratch)));
             DGB_CUDA(cudaFuncSetAttribute(potrf_solve3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           FusedTile::SMEM_BYTES));
@@ -892,11 +892,11 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
             }
             // X11 and X22 side by side in the chain's 128 x 128 inverse slot
             const int c1 = j0 + kNb, n2 = jb - kNb;
-            potrf_diag_kernel<1, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(
+            potrf_diag_kernel<2, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(
                 A, ld, j0, kNb, mask, status, active, w.inv, 0, 0, kD2 * kD2, 0);
             DGB_LAUNCH_CHECK();
             count_launch();
-            potrf_diag_kernel<1, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(
+            potrf_diag_kernel<2, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(
                 A, ld, c1, n2, mask, status, active, w.inv, j0 > 0 ? 1 : 0, 2, kD2 * kD2, kNb * kNb);
             DGB_LAUNCH_CHECK();
             count_launch();
