@@ -183,7 +183,13 @@ Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shar
     fmat_ = (int64_t)(d_ + 1) * ld_;
     twisted_ = tgt_.twisted();
     require(d_ <= 8192, Err::InvalidDimension, "the B200 engine supports d <= 8192");
-    stream_ = stream_acquire(0);
+    {  // the main stream (batch merge, statistics) at the highest priority: the next
+       // batch's moment updates wait for it
+        int least = 0, greatest = 0;
+        DGB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        stream_prio_ = greatest;
+        stream_ = stream_acquire(stream_prio_);
+    }
     DGB_CUDA(cudaEventCreateWithFlags(&main_ev_, cudaEventDisableTiming));
     DeferAllocSync defer;
     static const bool tinit = std::getenv("DIAM_B200_INIT_TIMING") != nullptr;  // phases to stderr
@@ -335,7 +341,7 @@ Engine::~Engine() {
     if (out_ev_) cudaEventDestroy(out_ev_);
     if (join_ev_) cudaEventDestroy(join_ev_);
     if (merge_ev_) cudaEventDestroy(merge_ev_);
-    stream_release(stream_, 0);
+    stream_release(stream_, stream_prio_);
     mark("done");
 }
 

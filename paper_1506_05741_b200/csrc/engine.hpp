@@ -192,6 +192,7 @@ private:
     int64_t fmat_ = 0;  // factor stride: d rows + the augmented row r = x - x_ref
     bool twisted_ = false, identity_ = true;
     cudaStream_t stream_ = nullptr;
+    int stream_prio_ = 0;
     cudaEvent_t main_ev_ = nullptr;
     std::vector<Group> groups_;
 
