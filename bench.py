@@ -259,7 +259,7 @@ def impl_b200(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world:
-        log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     lib = pkg.load()
     dist = None
@@ -274,6 +274,10 @@ def impl_b200(args):
         uid = uid.cuda()
         dist.broadcast(uid, 0)
         lib.check(lib.lib.diamx_comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world))
+        ranks = C.c_int(0)
+        lib.check(lib.lib.diamx_comm_size(C.byref(ranks)))
+        assert ranks.value == world, f"NCCL communicator has {ranks.value} ranks, expected {world}"
+        log(f"rank {rank}: NCCL communicator of {ranks.value} ranks on cuda:{local}")
 
     cfg = CONFIGS[args.config]
     kind, d, per_gpu, n_lag, M = cfg
@@ -403,6 +407,20 @@ def impl_b200(args):
     return 0
 
 
+def relaunch(args) -> int:
+    """`bench.py --gpus N` run directly (no torchrun): start the N ranks ourselves, one
+    process per GPU, with the same arguments (the driver's own launch line is the same
+    torch.distributed.run command)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -412,6 +430,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="d1024")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     if args.impl == "reference":
         return impl_reference(args)
     return impl_b200(args)

@@ -44,6 +44,8 @@ diam_status diamx_psrf_max(const double* means, const double* diags, int64_t cha
 diam_status diamx_nccl_unique_id(char out[128]);
 diam_status diamx_comm_init(const char id[128], int rank, int world);
 void diamx_comm_destroy(void);
+/* ranks of the communicator diam_sample uses (0 = none set) */
+diam_status diamx_comm_size(int* out);
 
 /* ---- engine handle for device-resident timing (bench.py) ------------------- */
 typedef struct diamx_engine diamx_engine;

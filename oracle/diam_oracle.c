@@ -11,6 +11,7 @@
 #include "diam_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -617,19 +618,101 @@ int or_lag_update(const or_kernel_cfg* cfg, or_chain* c, const or_moments* globa
 /* ------------------------------------------------------------------------- */
 /* engine: src/runner.cpp:122-279, 326-396                                    */
 /* ------------------------------------------------------------------------- */
-int or_run(const or_run_cfg* cfg, const or_target* t, const double* const* inject_w, or_run_out* out) {
+/* One chain's batch (run_chain_batch, src/runner.cpp:359-373, + record_trace :375-379). */
+typedef struct or_batch_job {
+    const or_run_cfg* cfg;
+    const or_target* t;
+    or_chain* ch;
+    const double* const* inject_w;
+    size_t* win_used;
+    or_run_out* out;
+    const or_moments* global;
+    size_t P, batches, step_idx, total_steps_cap;
+    int threads, tid;
+    int status;
+} or_batch_job;
+
+static int run_chain_batch(or_batch_job* j, size_t p) {
+    const or_run_cfg* cfg = j->cfg;
     const or_kernel_cfg* k = &cfg->kernel;
-    const size_t d = k->dim, P = cfg->chains, M = cfg->intervals_per_batch;
-    const size_t win = k->n_lag * d;
+    const size_t d = k->dim, M = cfg->intervals_per_batch, win = k->n_lag * d;
+    or_run_out* out = j->out;
+    or_chain* c = &j->ch[p];
+    size_t s_local = j->step_idx;
+    for (size_t m = 0; m < M; ++m) {
+        for (size_t s = 0; s < k->n_lag; ++s) {
+            double lr = 0.0;
+            double u = -1.0;
+            if (out->log_u) {
+                or_stream peek = c->uniform_rng;
+                u = or_uniform_open(&peek);
+            }
+            const int acc = or_mh_step(k, j->t, c, -1.0, &lr);
+            if (acc < 0) return -acc;
+            if (out->accept_bits) out->accept_bits[p * j->total_steps_cap + s_local] = acc;
+            if (out->log_ratio) out->log_ratio[p * j->total_steps_cap + s_local] = lr;
+            if (out->log_u) out->log_u[p * j->total_steps_cap + s_local] = log(u);
+            ++s_local;
+            if (out->traces && cfg->record_traces && c->n > k->n0 && (c->n - k->n0 - 1) % cfg->trace_thin == 0) {
+                /* the entry index is the same for every chain (same n) */
+                const size_t i = (size_t)((c->n - k->n0 - 1) / cfg->trace_thin);
+                if (i < out->trace_cap) {
+                    double* tr = out->traces + p * 3 * out->trace_cap;
+                    tr[i] = c->log_pi;
+                    if (cfg->trace_eigen_projections) {
+                        tr[out->trace_cap + i] = or_lane_dot(j->t->proj_min, c->x, d);
+                        tr[2 * out->trace_cap + i] = or_lane_dot(j->t->proj_max, c->x, d);
+                    }
+                }
+            }
+        }
+        double rate = 0.0;
+        const double* w = j->inject_w ? j->inject_w[p] + j->win_used[p] * win : NULL;
+        const int st = or_lag_update(k, c, j->global, w, &rate);
+        if (st != OR_OK) return st;
+        j->win_used[p]++;
+        const size_t h = j->batches * M + m;
+        out->beta_hist[p * cfg->max_batches * M + h] = c->beta;
+        out->acc_hist[p * cfg->max_batches * M + h] = rate;
+    }
+    return OR_OK;
+}
+
+static void* batch_worker(void* arg) {
+    or_batch_job* j = (or_batch_job*)arg;
+    j->status = OR_OK;
+    for (size_t p = (size_t)j->tid; p < j->P; p += (size_t)j->threads) {
+        const int st = run_chain_batch(j, p);
+        if (st != OR_OK) {
+            j->status = st;
+            break;
+        }
+    }
+    return NULL;
+}
+
+int or_run(const or_run_cfg* cfg, const or_target* t, const double* const* inject_w, or_run_out* out) {
+    return or_run_ex(cfg, t, inject_w, out, NULL);
+}
+
+int or_run_ex(const or_run_cfg* cfg, const or_target* t, const double* const* inject_w, or_run_out* out,
+              const or_run_opts* opts) {
+    const or_kernel_cfg* k = &cfg->kernel;
+    const size_t d = k->dim, M = cfg->intervals_per_batch;
+    const size_t P = opts && opts->n_ids ? opts->n_ids : cfg->chains; /* chains run here */
+    const int threads = opts && opts->threads > 1 ? (opts->threads < (int)P ? opts->threads : (int)P) : 1;
     or_chain* ch = (or_chain*)calloc(P, sizeof(or_chain));
     size_t* win_used = (size_t*)calloc(P, sizeof(size_t));
     double* x0 = (double*)malloc(sizeof(double) * d);
+    or_batch_job* jobs = (or_batch_job*)calloc((size_t)threads, sizeof(or_batch_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
     int st = OR_OK;
     for (size_t p = 0; p < P; ++p) { /* Engine ctor :122-137 */
+        const size_t gp = opts && opts->n_ids ? opts->chain_ids[p] : p; /* global chain index */
         or_stream init;
-        or_stream_init(&init, cfg->master_seed, p, "init");
+        or_stream_init(&init, cfg->master_seed, gp, "init");
         for (size_t i = 0; i < d; ++i) x0[i] = cfg->init_dispersion * or_normal(&init);
-        or_chain_init(&ch[p], k, t, x0, cfg->master_seed, p, inject_w ? inject_w[p] : NULL);
+        or_chain_init(&ch[p], k, t, x0, cfg->master_seed, gp, inject_w ? inject_w[p] : NULL);
         win_used[p] = 1;
     }
     or_moments global;
@@ -639,7 +722,7 @@ int or_run(const or_run_cfg* cfg, const or_target* t, const double* const* injec
     const size_t total_steps_cap = cfg->max_batches * M * k->n_lag;
     int reason = 0;
     for (;;) { /* Engine::run :216-279 */
-        const uint64_t iters = (uint64_t)P * M * batches * k->n_lag;
+        const uint64_t iters = (uint64_t)cfg->chains * M * batches * k->n_lag;
         if (cfg->max_samples >= 0 && iters >= (uint64_t)cfg->max_samples) {
             reason = 1;
             break;
@@ -648,36 +731,31 @@ int or_run(const or_run_cfg* cfg, const or_target* t, const double* const* injec
             reason = 0;
             break;
         }
-        for (size_t p = 0; p < P; ++p) { /* run_chain_batch :359-373 */
-            size_t s_local = step_idx;
-            for (size_t m = 0; m < M; ++m) {
-                for (size_t j = 0; j < k->n_lag; ++j) {
-                    double lr = 0.0;
-                    double u = -1.0;
-                    if (out->log_u) {
-                        or_stream peek = ch[p].uniform_rng;
-                        u = or_uniform_open(&peek);
-                    }
-                    const int acc = or_mh_step(k, t, &ch[p], -1.0, &lr);
-                    if (acc < 0) {
-                        st = -acc;
-                        goto done;
-                    }
-                    if (out->accept_bits) out->accept_bits[p * total_steps_cap + s_local] = acc;
-                    if (out->log_ratio) out->log_ratio[p * total_steps_cap + s_local] = lr;
-                    if (out->log_u) out->log_u[p * total_steps_cap + s_local] = log(u);
-                    ++s_local;
-                }
-                double rate = 0.0;
-                st = or_lag_update(k, &ch[p], &global,
-                                   inject_w ? inject_w[p] + win_used[p] * win : NULL, &rate);
-                if (st != OR_OK) goto done;
-                win_used[p]++;
-                const size_t h = batches * M + m;
-                out->beta_hist[p * cfg->max_batches * M + h] = ch[p].beta;
-                out->acc_hist[p * cfg->max_batches * M + h] = rate;
-            }
+        /* run_batch :326-357: the chains of a batch are independent (they read only the
+         * frozen global snapshot), so workers take them round-robin */
+        for (int i = 0; i < threads; ++i) {
+            or_batch_job* j = &jobs[i];
+            j->cfg = cfg;
+            j->t = t;
+            j->ch = ch;
+            j->inject_w = inject_w;
+            j->win_used = win_used;
+            j->out = out;
+            j->global = &global;
+            j->P = P;
+            j->batches = batches;
+            j->step_idx = step_idx;
+            j->total_steps_cap = total_steps_cap;
+            j->threads = threads;
+            j->tid = i;
+            if (threads > 1) pthread_create(&th[i], NULL, batch_worker, j);
+            else batch_worker(j);
         }
+        for (int i = 0; i < threads; ++i) {
+            if (threads > 1) pthread_join(th[i], NULL);
+            if (jobs[i].status != OR_OK && st == OR_OK) st = jobs[i].status;
+        }
+        if (st != OR_OK) goto done;
         step_idx += M * k->n_lag;
         { /* merge :237-245 */
             or_moments* locals = (or_moments*)malloc(sizeof(or_moments) * P);
@@ -723,9 +801,13 @@ int or_run(const or_run_cfg* cfg, const or_target* t, const double* const* injec
         }
     }
     out->batches = batches;
-    out->total_samples = (uint64_t)P * M * batches * k->n_lag;
+    out->total_samples = (uint64_t)cfg->chains * M * batches * k->n_lag;
     out->accumulated_samples = global.count;
     out->stop_reason = reason;
+    if (out->traces && cfg->record_traces) {
+        const uint64_t n = (uint64_t)batches * M * k->n_lag;
+        out->trace_len = n > k->n0 ? (size_t)((n - k->n0 - 1) / cfg->trace_thin + 1) : 0;
+    }
     memcpy(out->global_mean, global.mean, sizeof(double) * d);
     or_covariance(global.second, global.mean, d, out->global_cov);
     if (out->final_x)
@@ -735,6 +817,8 @@ done:
     free(ch);
     free(win_used);
     free(x0);
+    free(jobs);
+    free(th);
     moments_free(&global);
     return st;
 }

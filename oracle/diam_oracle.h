@@ -173,7 +173,25 @@ typedef struct or_run_out {
     double* log_ratio;        /* optional: chains × total steps or NULL */
     double* log_u;            /* optional: chains × total steps or NULL */
     double* final_x;          /* optional: chains × d or NULL */
+    /* optional traces (src/runner.cpp:363-379): chains × 3 × trace_cap, functional f of
+     * chain p at traces[(p·3 + f)·trace_cap + i]; trace_len = entries per chain */
+    double* traces;
+    size_t trace_cap, trace_len;
 } or_run_out;
+
+/* Run options beyond the reference's: `threads` workers run the chains of a batch
+ * concurrently (chains are independent within a batch; results do not depend on it);
+ * `chain_ids` (n_ids > 0) runs only those global chain indices, their RNG streams keyed
+ * by the global index -- valid for per-chain quantities of the FIRST batch only (the
+ * merge pools just the listed chains). Per-chain outputs are indexed by position in
+ * chain_ids. */
+typedef struct or_run_opts {
+    int threads;
+    const size_t* chain_ids;
+    size_t n_ids;
+} or_run_opts;
+int or_run_ex(const or_run_cfg* cfg, const or_target* t, const double* const* inject_w, or_run_out* out,
+              const or_run_opts* opts);
 
 /* Full run. `inject_w`, when non-NULL, supplies every window's normals:
  * inject_w[p] points at chain p's stream of windows, each n_lag×d, in the order

@@ -53,6 +53,7 @@ class B200(DiamABI):
             "diamx_nccl_unique_id": (st, [C.c_char_p]),
             "diamx_comm_init": (st, [C.c_char_p, C.c_int, C.c_int]),
             "diamx_comm_destroy": (None, []),
+            "diamx_comm_size": (st, [C.POINTER(C.c_int)]),
             "diamx_engine_create": (st, [_vp, C.POINTER(RunOptions), C.POINTER(_vp)]),
             "diamx_engine_run_batches": (st, [_vp, i64, _dp]),
             "diamx_engine_set_profiling": (st, [_vp, C.c_int]),

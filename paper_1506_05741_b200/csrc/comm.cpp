@@ -140,6 +140,25 @@ struct ThreadComm final : Comm {
 
 }  // namespace
 
+Comm::~Comm() {
+    if (scratch_) cudaFree(scratch_);
+}
+
+bool Comm::any(bool flag, cudaStream_t s) {
+    int dev = 0;
+    DGB_CUDA(cudaGetDevice(&dev));
+    if (!scratch_ || scratch_dev_ != dev) {
+        DGB_CUDA(cudaMalloc(&scratch_, sizeof(double)));
+        scratch_dev_ = dev;
+    }
+    double h = flag ? 1.0 : 0.0;
+    DGB_CUDA(cudaMemcpyAsync(scratch_, &h, sizeof(double), cudaMemcpyHostToDevice, s));
+    allreduce_sum(scratch_, 1, s);
+    DGB_CUDA(cudaMemcpyAsync(&h, scratch_, sizeof(double), cudaMemcpyDeviceToHost, s));
+    DGB_CUDA(cudaStreamSynchronize(s));
+    return h > 0.5;
+}
+
 std::vector<std::shared_ptr<Comm>> make_thread_comms(int world) {
     auto sh = std::make_shared<ThreadShared>();
     sh->world = world;

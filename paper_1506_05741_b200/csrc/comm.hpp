@@ -17,12 +17,25 @@
 namespace dgb {
 
 struct Comm {
-    virtual ~Comm() = default;
+    virtual ~Comm();
     virtual int rank() const = 0;
     virtual int size() const = 0;
     virtual void allreduce_sum(double* buf, int64_t n, cudaStream_t s) = 0;
     // dst holds size()*n doubles, rank r's block at r*n
     virtual void allgather(const double* src, double* dst, int64_t n, cudaStream_t s) = 0;
+    // Collective OR of a host flag (every rank must call it at the same point): the
+    // engine's stop decisions and rank-local failures go through it, so all ranks leave
+    // the batch loop together instead of one rank waiting in a collective forever.
+    bool any(bool flag, cudaStream_t s);
+
+private:
+    double* scratch_ = nullptr;  // one device double (allocated on first use)
+    int scratch_dev_ = -1;
+
+public:
+    Comm() = default;
+    Comm(const Comm&) = delete;
+    Comm& operator=(const Comm&) = delete;
 };
 
 // Process-wide communicator used by diam_sample when set (diamx_comm_init).

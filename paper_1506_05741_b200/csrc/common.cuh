@@ -36,6 +36,10 @@ inline void launch_check(const char* file, int line) {
 extern std::atomic<uint64_t> g_launch_count;
 inline void count_launch(uint64_t n = 1) { g_launch_count.fetch_add(n, std::memory_order_relaxed); }
 
+// Raise a kernel's dynamic shared-memory limit to `bytes` on the CURRENT device (the
+// attribute is per device; engines on several devices or threads share the table).
+void set_smem_attr(const void* func, int bytes);
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Leading dimension used for every device d-vector/d×d row: a multiple of 8

@@ -1,9 +1,7 @@
 // diag_tc.cuh — Cholesky + inverse of one 64x64 diagonal block in shared memory, with the
 // serial part on one warp and the rest on the FP64 tensor pipe (DMMA m8n8k4).
 //
-// The register-blocked factorization (diag_block.cuh) spends ~3500 cycles per 4-column
-// step: every warp runs a long dependent instruction stream for its 4x4 tiles. Here the
-// 64 columns are taken 8 at a time (left-looking, proj/src/linalg.cpp:74-93 reordered):
+// The 64 columns are taken 8 at a time (left-looking, proj/src/linalg.cpp:74-93 reordered):
 //   (a) panel update  A[k0:, k0:k0+8] -= L[k0:, :k0] L[k0:k0+8, :k0]^T    one 8x8 DMMA tile
 //       per warp, K = k0;
 //   (b) panel factor  the 8 columns of rows k0..63 by ONE warp (two rows per lane):
@@ -11,17 +9,18 @@
 //       panel's remaining columns through shuffles -- no barriers inside the panel;
 // then X = L^-1 by block forward substitution: the eight 8x8 diagonal inverses in
 // parallel (one warp each), then block rows 1..7 in turn, each X_ij = -X_ii sum L_im X_mj
-// on the DMMA pipe. Same interface and results (to rounding) as diag64_block.
+// on the DMMA pipe.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "diag_block.cuh"
 #include "gemm_tile.cuh"
 
 namespace dgb {
 
+constexpr int kDiagNb = 64;  // diagonal block size
+constexpr int kD2 = 128;     // POTRF block column width (two diagonal blocks)
 constexpr int kTcS = 68;
 #ifdef DIAG_TC_PROFILE
 __device__ long long g_tc_prof[16];
@@ -258,143 +257,6 @@ __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_
     return 0;
 }
 
-constexpr int kD2 = 128;
 
-// L = chol(A) and X = L^-1 of one 128x128 diagonal block (jb <= 128 valid rows) by the
-// 256 threads of a CTA, X row-major with stride kD2, zero outside the lower jb x jb part;
-// `smem` holds a DiagTcScratch followed by a 64 x kL21S block (kDiag128SmemBytes).
-// Two DMMA diagonal blocks (diag64_tc_sc) joined by 8x8 DMMA tiles with every operand in
-// shared memory (8 row tiles per product, one per warp):
-//   L21 = A21 X11^T                (A21 staged over L11, X11 still in the scratch)
-//   A22 -= L21 L21^T, U = L21 X11  (U parked in X's X21 block)
-//   chol / inverse of A22          (X22 in the scratch)
-//   X21 = -X22 U                   (U staged over L22)
-// The triangular factors' zero blocks are skipped in every K loop.
-constexpr int kL21S = 68;  // stride of the L21 block (4 mod 16)
-
-__device__ __forceinline__ int diag128_tc(double* A, int64_t ld, int jb, double* X, double* smem) {
-    DiagTcScratch& sc = *reinterpret_cast<DiagTcScratch*>(smem);
-    double* sl = smem + (sizeof(DiagTcScratch) + 7) / 8;  // L21, 64 x kL21S
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int fr = lane >> 2, fk = lane & 3;
-    const int j1 = min(kDiagNb, jb);
-    TC_MARK(8);
-    if (diag64_tc_sc(sc, A, ld, j1, X, 0, kD2)) return 1;
-    TC_MARK(9);
-    for (int e = tid; e < 64 * 64; e += 256) X[(e >> 6) * kD2 + 64 + (e & 63)] = 0.0;  // upper-right block
-    if (jb <= kDiagNb) {
-        for (int e = tid; e < 64 * kD2; e += 256) X[64 * kD2 + e] = 0.0;
-        return 0;
-    }
-    const int j2 = jb - kDiagNb;
-    const int rt = warp, r = 8 * rt + fr;
-    {
-        double v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int e = tid + 256 * i, rr = e >> 6, q = e & 63;
-            v[i] = rr < j2 ? __ldcg(A + (int64_t)(64 + rr) * ld + q) : 0.0;
-        }
-        __syncthreads();  // diag64_tc_sc's stores have read sc.a
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int e = tid + 256 * i;
-            sc.a[(e >> 6) * kTcS + (e & 63)] = v[i];
-        }
-    }
-    __syncthreads();
-    // L21 = A21 X11^T (X11[n][k] = 0 for k > n)
-    for (int ct = 0; ct < 8; ++ct) {
-        double acc[2];
-        tc_tile(acc, sc.a, 8 * rt, sc.x, 8 * ct, 8 * ct + 8, lane);
-        sl[r * kL21S + 8 * ct + 2 * fk] = acc[0];
-        sl[r * kL21S + 8 * ct + 2 * fk + 1] = acc[1];
-    }
-    __syncthreads();
-    TC_MARK(10);
-    for (int e = tid; e < 64 * 64; e += 256) {
-        const int rr = e >> 6, q = e & 63;
-        if (rr < j2) A[(int64_t)(64 + rr) * ld + q] = sl[rr * kL21S + q];
-    }
-    // A22 -= L21 L21^T on the lower tiles (ct <= rt), in place in global memory: a warp's
-    // (up to 5) tiles are multiplied first, then all their loads issued, then the stores
-    {
-        double acc[5][2], old[5][2];
-        int tr[5], tc[5];
-#pragma unroll
-        for (int u = 0; u < 5; ++u) {
-            const int t = warp + 8 * u;
-            int a = 0, base = 0;
-            while (base + a + 1 <= t) {
-                base += a + 1;
-                ++a;
-            }
-            tr[u] = a;
-            tc[u] = t - base;
-            acc[u][0] = acc[u][1] = 0.0;
-            if (t < 36) tc_tile(acc[u], sl, 8 * tr[u], sl, 8 * tc[u], 64, lane);
-        }
-#pragma unroll
-        for (int u = 0; u < 5; ++u)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int rr = 8 * tr[u] + fr, q = 8 * tc[u] + 2 * fk + h;
-                old[u][h] = (warp + 8 * u < 36 && rr < j2 && q <= rr) ? __ldcg(A + (int64_t)(64 + rr) * ld + 64 + q) : 0.0;
-            }
-#pragma unroll
-        for (int u = 0; u < 5; ++u)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int rr = 8 * tr[u] + fr, q = 8 * tc[u] + 2 * fk + h;
-                if (warp + 8 * u < 36 && rr < j2 && q <= rr) A[(int64_t)(64 + rr) * ld + 64 + q] = old[u][h] - acc[u][h];
-            }
-    }
-    // U = L21 X11 (X11[k][n] = 0 for k < n), parked in X21
-    for (int ct = 0; ct < 8; ++ct) {
-        double e[2] = {0.0, 0.0}, o[2] = {0.0, 0.0};
-        int k = 8 * ct;
-        for (; k + 8 <= 64; k += 8) {
-            tile::dmma(e, sl[r * kL21S + k + fk], sc.x[(k + fk) * kTcS + 8 * ct + fr]);
-            tile::dmma(o, sl[r * kL21S + k + 4 + fk], sc.x[(k + 4 + fk) * kTcS + 8 * ct + fr]);
-        }
-        X[(64 + r) * kD2 + 8 * ct + 2 * fk] = e[0] + o[0];
-        X[(64 + r) * kD2 + 8 * ct + 2 * fk + 1] = e[1] + o[1];
-    }
-    __syncthreads();  // A22 and U stores visible to the CTA; sc.x (X11) no longer read
-    TC_MARK(11);
-    if (diag64_tc_sc(sc, A + 64 * ld + 64, ld, j2, X + 64 * kD2 + 64, 0, kD2)) return 1;
-    {
-        double v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int e = tid + 256 * i;
-            v[i] = __ldcg(X + (64 + (e >> 6)) * kD2 + (e & 63));
-        }
-        __syncthreads();  // the second diag64_tc_sc has read sc.a
-        TC_MARK(12);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int e = tid + 256 * i;
-            sc.a[(e >> 6) * kTcS + (e & 63)] = v[i];
-        }
-    }
-    __syncthreads();
-    // X21 = -X22 U (X22[r][k] = 0 for k > r)
-    for (int ct = 0; ct < 8; ++ct) {
-        double e[2] = {0.0, 0.0}, o[2] = {0.0, 0.0};
-        int k = 0;
-        for (; k + 8 <= 8 * rt + 8; k += 8) {
-            tile::dmma(e, sc.x[r * kTcS + k + fk], sc.a[(k + fk) * kTcS + 8 * ct + fr]);
-            tile::dmma(o, sc.x[r * kTcS + k + 4 + fk], sc.a[(k + 4 + fk) * kTcS + 8 * ct + fr]);
-        }
-        const int q = 8 * ct + 2 * fk;
-        X[(64 + r) * kD2 + q] = r < j2 ? -(e[0] + o[0]) : 0.0;
-        X[(64 + r) * kD2 + q + 1] = r < j2 ? -(e[1] + o[1]) : 0.0;
-    }
-    TC_MARK(13);
-    return 0;
-}
-
-constexpr int kDiag128SmemBytes = (int)((sizeof(DiagTcScratch) + 7) / 8 * 8) + 64 * kL21S * 8;
 
 }  // namespace dgb

@@ -1,7 +1,6 @@
 // engine.cu — B200 sampler engine (see engine.hpp). Reference semantics cited inline
 // (paths relative to /root/reference/proj/).
 #include "engine.hpp"
-#include "blas.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -26,6 +25,18 @@ bool sync_check_enabled() {
         return e && std::atoi(e) != 0;
     }();
     return on;
+}
+
+void set_smem_attr(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> set;  // (device, kernel) -> bytes allowed
+    int dev = 0;
+    DGB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    int& cur = set[{dev, func}];
+    if (bytes <= cur) return;
+    DGB_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    cur = bytes;
 }
 
 namespace {
@@ -105,6 +116,7 @@ void* pinned_acquire(size_t bytes, bool zero = true) {
     void* p = nullptr;
     DGB_CUDA(cudaMallocHost(&p, bytes));
     std::memset(p, 0, bytes);
+    std::lock_guard<std::mutex> lk(g_pinned_mu);  // engines of several rank threads share the maps
     g_pinned_size[p] = bytes;
     return p;
 }
@@ -112,7 +124,8 @@ void* pinned_acquire(size_t bytes, bool zero = true) {
 void pinned_release(void* p) {
     if (!p) return;
     std::lock_guard<std::mutex> lk(g_pinned_mu);
-    g_pinned_free.emplace(g_pinned_size[p], p);
+    const auto it = g_pinned_size.find(p);
+    if (it != g_pinned_size.end()) g_pinned_free.emplace(it->second, p);
 }
 
 // Streams are kept for the process too (creating and destroying the 33 prioritised streams
@@ -259,7 +272,6 @@ int Engine::plan_memory() {
         n += 2.0 * mat_ + 3.0 * ld_;              // global snapshot, reduction buffer
         n += 3.0 * M * C_ * Lw_;                  // per-batch traces
         n += 16.0 * C_ * ld_ + 16400.0 * C_;      // chain vectors, POTRF inverse blocks
-        n += (double)potrf_dag_bytes(d_, C_) / 8;  // task-graph POTRF inverse tiles
         return 8.0 * n;
     };
     auto gmax = [&](int groups) { return (C_ + groups - 1) / groups; };
@@ -315,13 +327,12 @@ Engine::~Engine() {
     };
     if (stream_) cudaStreamSynchronize(stream_);
     for (auto& g : groups_) {
-        if (g.sr && g.sr != g.s) stream_release(g.sr, g.prio_sr);
+        if (g.sr) stream_release(g.sr, g.prio_sr);
         if (g.s) stream_release(g.s, g.prio_s);
         if (g.ev_steps) cudaEventDestroy(g.ev_steps);
         if (g.ev_ref) cudaEventDestroy(g.ev_ref);
         if (g.done) cudaEventDestroy(g.done);
         if (g.pool_ev) cudaEventDestroy(g.pool_ev);
-        potrf_work_release(g.pw);
     }
     mark("streams");
     for (void* p : allocs_.blocks) cudaFreeAsync(p, 0);
@@ -415,7 +426,7 @@ void Engine::init_chains() {
     h_flags_ = static_cast<int*>(pinned_acquire(3 * (size_t)C * sizeof(int)));
     Sg_ = dalloc<double>(A, mat_);
     mg_ = dalloc<double>(A, ld_);
-    Ssum_ = dalloc<double>(A, mat_ + ld_);
+    Ssum_ = dalloc<double>(A, (size_t)d_ * (d_ + 1) / 2 + ld_);  // packed lower sum + mean sum
     cov_part_ = dalloc<double>(A, 2 * (size_t)d_);
     if (!cfg_.checkpoint_path.empty()) cS_ = dalloc<double>(A, (size_t)C * mat_);
     const size_t M = cfg_.intervals_per_batch;
@@ -483,24 +494,15 @@ void Engine::make_groups(int n) {
         g.off = (int)((int64_t)C_ * i / n);
         g.C = (int)((int64_t)C_ * (i + 1) / n) - g.off;
         {
-            // steps at the lowest priority, the refactorization at the highest
-            // (DIAM_B200_PRIO=0: one stream per group)
-            static const int prio = [] {
-                const char* e = std::getenv("DIAM_B200_PRIO");
-                return e ? std::atoi(e) : 1;
-            }();
+            // steps at the lowest priority, the refactorization at the highest: the
+            // latency-bound POTRF launches of one group are scheduled ahead of the other
+            // groups' GEMM tiles
             int least = 0, greatest = 0;
             DGB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-            const int ps = prio == 1 ? least : (prio == 2 ? greatest : 0);
-            const int pr = prio == 1 ? greatest : (prio == 2 ? least : 0);
-            g.s = stream_acquire(ps);
-            g.prio_s = ps;
-            if (prio) {
-                g.sr = stream_acquire(pr);
-                g.prio_sr = pr;
-            } else {
-                g.sr = g.s;
-            }
+            g.s = stream_acquire(least);
+            g.prio_s = least;
+            g.sr = stream_acquire(greatest);
+            g.prio_sr = greatest;
             DGB_CUDA(cudaEventCreateWithFlags(&g.ev_steps, cudaEventDisableTiming));
             DGB_CUDA(cudaEventCreateWithFlags(&g.ev_ref, cudaEventDisableTiming));
         }
@@ -518,11 +520,7 @@ void Engine::make_groups(int n) {
         g.Hb = ptr_array(A, H_ + g.off * win_, 0, 1);
         // per-group inverse-block scratch (+ int active[C] tail): groups factor concurrently
         g.pw.inv = dalloc<double>(A, potrf_work_doubles(g.C));
-        g.pw.inv_ptrs = ptr_array(A, g.pw.inv, 64 * 64, g.C);
         g.pw.inv128_ptrs = ptr_array(A, g.pw.inv, 128 * 128, g.C);
-        // task-graph POTRF: the groups refactor at about the same time, so each gets its
-        // share of the SMs as persistent workers
-        g.pw.workers = std::max(8, 2 * ((kNumSMs + n - 1) / n));  // two resident per SM
     }
 }
 
@@ -533,13 +531,13 @@ void Engine::refresh_g(const double* x, double* out, int chains, cudaStream_t s)
     timed_end("gemv_state", 2.0 * chains * (double)d_ * d_, s);
 }
 
-void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s, GemmShape sh) {
+void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s) {
     double flops = 2.0 * g.M * (double)g.N * g.K * batch;
     if (g.tri_c_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
     if (g.tri_b_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
     nvtxRangePushA(name);  // `ncu --nvtx --nvtx-include "<name>/"` selects one GEMM class
     timed_begin(s);
-    gemm_f64(g, batch, ak, bk, s, sh);
+    gemm_f64(g, batch, ak, bk, s);
     timed_end(name, flops, s);
     nvtxRangePop();
 }
@@ -792,7 +790,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         t.alpha_vec_mul = infl;
         t.beta = 0.0;
         t.tri_b_lower = 1;
-        gemm("trmm_noise", t, C, true, true, s, GemmShape::Stream);
+        gemm("trmm_noise", t, C, true, true, s);
     }
     {
         GemmBatch h{};
@@ -804,28 +802,17 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         h.K = d_;
         h.alpha = 1.0;
         h.beta = 0.0;
-        // DIAM_B200_TARGET_GEMM=dmma|cublas: the plain (C Lc) x d x d product on the DMMA
-        // kernel or through cuBLAS (read once per process)
-        static const bool use_cublas = [] {
-            const char* e = std::getenv("DIAM_B200_TARGET_GEMM");
-            return e && std::string(e) == "cublas";
-        }();
-        if (rows == Lc_ && use_cublas) {
-            timed_begin(s);
-            const bool ok = cublas_gemm_abt(s, C * Lc_, d_, d_, Xi_ + o * win_, ld_, G_, ld_, H_ + o * win_, ld_);
-            timed_end("gemm_target", 2.0 * C * Lc_ * (double)d_ * d_, s);
-            require(ok, Err::Unknown, "DIAM_B200_TARGET_GEMM=cublas: libcublas.so.12 not available");
-        } else if (rows == Lc_) {
+        if (rows == Lc_) {
             h.A = (const double* const*)g.Xib;
             h.C = g.Hb;
             h.M = C * Lc_;  // the group's window chunks are one contiguous (C Lc) x ld matrix
-            gemm("gemm_target", h, 1, true, true, s, GemmShape::Stream);
+            gemm("gemm_target", h, 1, true, true, s);
         } else {            // ragged last chunk: per-chain pieces
             h.B = (const double* const*)Gpc_;
             h.A = (const double* const*)g.Xip;
             h.C = Hp_ + o;
             h.M = rows;
-            gemm("gemm_target", h, C, true, true, s, GemmShape::Stream);
+            gemm("gemm_target", h, C, true, true, s);
         }
     }
 
@@ -900,10 +887,9 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
 void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {
     const int C = g.C, o = g.off;
     const cudaStream_t s = g.sr;
-    if (g.sr != g.s) {  // the refactor stream continues after the window's steps
-        DGB_CUDA(cudaEventRecord(g.ev_steps, g.s));
-        DGB_CUDA(cudaStreamWaitEvent(g.sr, g.ev_steps, 0));
-    }
+    // the refactor stream continues after the window's steps
+    DGB_CUDA(cudaEventRecord(g.ev_steps, g.s));
+    DGB_CUDA(cudaStreamWaitEvent(g.sr, g.ev_steps, 0));
     if (p.refactor) {
         // blend -> covariance into the workspace factor, trace floor, POTRF (proposal.cpp:176-184).
         // pCN-form kernels append r = x - x_ref as row d: the factorization then also
@@ -947,7 +933,6 @@ bool Engine::tail_begin(Group& g, const WindowPlan& p, Ladder& st) {
     if (!p.refactor) return true;
     const int C = g.C, o = g.off;
     DGB_CUDA(cudaEventSynchronize(g.status_ev));
-    require(!potrf_dag_aborted(g.pw), Err::Unknown, "task-graph POTRF aborted (dependency wait limit)");
     st.failing.assign(C, 0);
     bool any = false;
     for (int c = 0; c < C; ++c) {
@@ -963,7 +948,6 @@ bool Engine::tail_begin(Group& g, const WindowPlan& p, Ladder& st) {
 bool Engine::tail_step(Group& g, const WindowPlan& p, Ladder& st) {
     const int C = g.C, o = g.off;
     DGB_CUDA(cudaEventSynchronize(g.status_ev));
-    require(!potrf_dag_aborted(g.pw), Err::Unknown, "task-graph POTRF aborted (dependency wait limit)");
     bool any = false;
     for (int c = 0; c < C; ++c) {
         if (st.failing[c] && !h_flags_[o + c]) st.failing[c] = 0;
@@ -1044,10 +1028,9 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
     }
     // G x re-anchored at every boundary so the step recursion never drifts
     refresh_g(x_ + o * ld_, g_ + o * ld_, C, s);
-    if (g.sr != g.s) {  // the next window's steps follow the tail
-        DGB_CUDA(cudaEventRecord(g.ev_ref, g.sr));
-        DGB_CUDA(cudaStreamWaitEvent(g.s, g.ev_ref, 0));
-    }
+    // the next window's steps follow the tail
+    DGB_CUDA(cudaEventRecord(g.ev_ref, g.sr));
+    DGB_CUDA(cudaStreamWaitEvent(g.s, g.ev_ref, 0));
 }
 
 void Engine::capture_chunk(const Group& g, int r0, int rows) {
@@ -1083,17 +1066,20 @@ void Engine::capture_window(size_t) {
 }
 
 void Engine::merge_batch() {
-    // proj/src/moments.cpp:51-88 with the P-chain sum pooled across GPUs
+    // proj/src/moments.cpp:51-88 with the P-chain sum pooled across GPUs: each GPU sums its
+    // chains' packed lower triangles and means, one all-reduce (sum) of d(d+1)/2 + d doubles
+    // over NVLink, and every rank applies the merge weights to its replica of the snapshot
     const uint64_t incoming = (uint64_t)P_ * cnt_local_;
     if (incoming > 0) {
         double keep = 1.0, wp = 0.0;
         merge_weights(cnt_g_, (uint64_t)P_, cnt_local_, &keep, &wp);
+        const int64_t tri = (int64_t)d_ * (d_ + 1) / 2;
         timed_begin(stream_);
-        launch_sum_chains(Ssum_, S_, mat_, C_, mat_, 1.0, stream_);
-        launch_sum_chains(Ssum_ + mat_, mean_, ld_, C_, ld_, 1.0, stream_);
-        if (comm_) comm_->allreduce_sum(Ssum_, mat_ + ld_, stream_);
-        launch_axpby(Sg_, Ssum_, mat_, wp, keep, stream_);
-        launch_axpby(mg_, Ssum_ + mat_, ld_, wp, keep, stream_);
+        launch_sum_chains_lower(Ssum_, S_, mat_, C_, d_, ld_, stream_);
+        launch_sum_chains(Ssum_ + tri, mean_, ld_, C_, ld_, 1.0, stream_);
+        if (comm_) comm_->allreduce_sum(Ssum_, tri + ld_, stream_);
+        launch_merge_lower(Sg_, ld_, Ssum_, d_, keep, wp, stream_);
+        launch_axpby(mg_, Ssum_ + tri, ld_, wp, keep, stream_);
         timed_end("merge", 0.0, stream_);
         cnt_g_ += incoming;
         const double ct = (double)(cum_cnt_ + cnt_local_);
@@ -1109,106 +1095,6 @@ void Engine::merge_batch() {
     // (beta = 0), and nothing reads S_ with a nonzero weight before that update
     DGB_CUDA(cudaMemsetAsync(mean_, 0, (size_t)C_ * ld_ * 8, stream_));
     cnt_local_ = 0;
-}
-
-void Engine::batch_stats(double& cov_err, double& mean_err, double& psrf) {
-    cov_err = mean_err = psrf = NAN;
-    if (!comm_) {
-        // one GPU: everything on the device, four scalars back (same summation orders as
-        // the host path below, which the sharded run keeps for its gathered shards)
-        const bool want_err = cnt_g_ >= 2, want_psrf = P_ >= 2 && cum_cnt_ >= 2;
-        if (want_err) launch_cov_error(Sg_, mg_, Ct_, d_, ld_, cov_part_, stream_);
-        launch_batch_stats(cov_part_, mg_, tmean_, d_, cmean_, cdiag_, ld_, C_, cum_cnt_, want_err, want_psrf,
-                           dstats_, stream_);
-        DGB_CUDA(cudaMemcpyAsync(h_stats_, dstats_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
-        DGB_CUDA(cudaStreamSynchronize(stream_));
-        require(!((int)h_stats_[3] & 1), Err::InvalidArgument, "cov_error: zero reference norm");
-        cov_err = h_stats_[0];
-        mean_err = h_stats_[1];
-        psrf = h_stats_[2];
-        return;
-    }
-    if (cnt_g_ >= 2) {  // runner.cpp:249-256
-        launch_cov_error(Sg_, mg_, Ct_, d_, ld_, cov_part_, stream_);
-        std::vector<double> part(2 * (size_t)d_), mg(d_);
-        DGB_CUDA(cudaMemcpyAsync(part.data(), cov_part_, part.size() * 8, cudaMemcpyDeviceToHost, stream_));
-        DGB_CUDA(cudaMemcpyAsync(mg.data(), mg_, d_ * 8, cudaMemcpyDeviceToHost, stream_));
-        DGB_CUDA(cudaStreamSynchronize(stream_));
-        double num = 0.0, den = 0.0;
-        for (int i = 0; i < d_; ++i) {
-            num += part[2 * i];
-            den += part[2 * i + 1];
-        }
-        require(den > 0.0, Err::InvalidArgument, "cov_error: zero reference norm");
-        cov_err = std::sqrt(num / den);
-        double s = 0.0;
-        for (int i = 0; i < d_; ++i) {
-            const double df = mg[i] - tgt_.mean[i];
-            s += df * df;
-        }
-        mean_err = std::sqrt(s);
-    }
-    if (P_ >= 2) {  // runner.cpp:381-396 on (cum mean, cum diag) of every chain
-        std::vector<double> cm, cd;
-        const int64_t nloc = (int64_t)C_ * ld_;
-        if (comm_) {
-            // equal shards required for a plain all-gather; pad to the largest shard
-            const int64_t maxc = (P_ + world_ - 1) / world_;
-            if (!gather_) gather_ = dalloc<double>(allocs_, (size_t)2 * maxc * ld_ * (world_ + 1));
-            double* src = gather_;
-            double* dst = gather_ + 2 * maxc * ld_;
-            DGB_CUDA(cudaMemsetAsync(src, 0, 2 * maxc * ld_ * 8, stream_));
-            DGB_CUDA(cudaMemcpyAsync(src, cmean_, nloc * 8, cudaMemcpyDeviceToDevice, stream_));
-            DGB_CUDA(cudaMemcpyAsync(src + maxc * ld_, cdiag_, nloc * 8, cudaMemcpyDeviceToDevice, stream_));
-            comm_->allgather(src, dst, 2 * maxc * ld_, stream_);
-            std::vector<double> all((size_t)world_ * 2 * maxc * ld_);
-            DGB_CUDA(cudaMemcpyAsync(all.data(), dst, all.size() * 8, cudaMemcpyDeviceToHost, stream_));
-            DGB_CUDA(cudaStreamSynchronize(stream_));
-            for (int r = 0; r < world_; ++r) {
-                int64_t f = 0, cr = 0;
-                shard_range(P_, world_, r, &f, &cr);
-                const double* base = all.data() + (size_t)r * 2 * maxc * ld_;
-                cm.insert(cm.end(), base, base + (size_t)cr * ld_);
-                cd.insert(cd.end(), base + maxc * ld_, base + maxc * ld_ + (size_t)cr * ld_);
-            }
-        } else {
-            cm.resize(nloc);
-            cd.resize(nloc);
-            DGB_CUDA(cudaMemcpyAsync(cm.data(), cmean_, nloc * 8, cudaMemcpyDeviceToHost, stream_));
-            DGB_CUDA(cudaMemcpyAsync(cd.data(), cdiag_, nloc * 8, cudaMemcpyDeviceToHost, stream_));
-            DGB_CUDA(cudaStreamSynchronize(stream_));
-        }
-        std::vector<const double*> means, diags;
-        for (int c = 0; c < P_; ++c) {
-            means.push_back(cm.data() + (size_t)c * ld_);
-            diags.push_back(cd.data() + (size_t)c * ld_);
-        }
-        try {
-            psrf = psrf_max(means, diags, d_, cum_cnt_);
-        } catch (const Error& e) {
-            if (e.code != Err::ZeroWithinVariance && e.code != Err::InvalidArgument) throw;
-            psrf = NAN;
-        }
-    }
-}
-
-void Engine::collect_batch_host(size_t windows) {
-    // beta / acceptance histories and the traces of this batch (runner.cpp:365-371)
-    const int C = C_;
-    std::vector<double> rate(windows * C), beta(windows * C);
-    DGB_CUDA(cudaMemcpyAsync(rate.data(), hist_rate_, rate.size() * 8, cudaMemcpyDeviceToHost, stream_));
-    DGB_CUDA(cudaMemcpyAsync(beta.data(), hist_beta_, beta.size() * 8, cudaMemcpyDeviceToHost, stream_));
-    std::vector<double> lp, pj;
-    if (cfg_.record_traces) {
-        lp.resize(windows * C * (size_t)Lw_);
-        DGB_CUDA(cudaMemcpyAsync(lp.data(), trace_lp_, lp.size() * 8, cudaMemcpyDeviceToHost, stream_));
-        if (cfg_.trace_eigen_projections) {
-            pj.resize(windows * C * (size_t)Lw_ * 2);
-            DGB_CUDA(cudaMemcpyAsync(pj.data(), trace_pj_, pj.size() * 8, cudaMemcpyDeviceToHost, stream_));
-        }
-    }
-    DGB_CUDA(cudaStreamSynchronize(stream_));
-    collect_histories(windows, window_n_start_, rate.data(), beta.data(), lp.data(), pj.data());
 }
 
 void Engine::collect_histories(size_t windows, const std::vector<uint64_t>& n_start, const double* rate,
@@ -1238,7 +1124,12 @@ void Engine::collect_histories(size_t windows, const std::vector<uint64_t>& n_st
 }
 
 void Engine::enqueue_batch_outputs(size_t windows) {
-    // one GPU only (the sharded run gathers on the host: batch_stats / collect_batch_host)
+    // The batch statistics (cov / mean error from the merged snapshot, the PSRF over every
+    // chain's cumulative mean and diagonal) on the device, and every per-batch output's copy
+    // into pinned memory, in stream order; read_batch_outputs waits for them. With several
+    // ranks the PSRF inputs are all-gathered first (device to device, stream-ordered) and
+    // compacted into global chain order, so the statistics kernel sums over the same chains
+    // in the same order as a one-GPU run (runner.cpp:249-256, 381-396).
     const int C = C_;
     const size_t mc = windows * C, tr = cfg_.record_traces ? mc * (size_t)Lw_ : 0;
     if (!h_out_) {
@@ -1247,8 +1138,30 @@ void Engine::enqueue_batch_outputs(size_t windows) {
     }
     const bool want_err = cnt_g_ >= 2, want_psrf = P_ >= 2 && cum_cnt_ >= 2;
     if (want_err) launch_cov_error(Sg_, mg_, Ct_, d_, ld_, cov_part_, stream_);
-    launch_batch_stats(cov_part_, mg_, tmean_, d_, cmean_, cdiag_, ld_, C_, cum_cnt_, want_err, want_psrf, dstats_,
-                       stream_);
+    const double* cm = cmean_;
+    const double* cd = cdiag_;
+    if (comm_ && want_psrf) {
+        const int64_t maxc = (P_ + world_ - 1) / world_, blk = 2 * maxc * ld_;
+        if (!gather_) gather_ = dalloc<double>(allocs_, (size_t)blk * (world_ + 1) + 2 * (size_t)P_ * ld_);
+        double* src = gather_;
+        double* dst = gather_ + blk;
+        double* all = dst + blk * world_;  // P x ld cumulative means, then P x ld diagonals
+        DGB_CUDA(cudaMemcpyAsync(src, cmean_, (size_t)C_ * ld_ * 8, cudaMemcpyDeviceToDevice, stream_));
+        DGB_CUDA(cudaMemcpyAsync(src + maxc * ld_, cdiag_, (size_t)C_ * ld_ * 8, cudaMemcpyDeviceToDevice, stream_));
+        comm_->allgather(src, dst, blk, stream_);
+        for (int r = 0; r < world_; ++r) {
+            int64_t f = 0, cr = 0;
+            shard_range(P_, world_, r, &f, &cr);
+            DGB_CUDA(cudaMemcpyAsync(all + f * ld_, dst + r * blk, (size_t)cr * ld_ * 8, cudaMemcpyDeviceToDevice,
+                                     stream_));
+            DGB_CUDA(cudaMemcpyAsync(all + (P_ + f) * ld_, dst + r * blk + maxc * ld_, (size_t)cr * ld_ * 8,
+                                     cudaMemcpyDeviceToDevice, stream_));
+        }
+        cm = all;
+        cd = all + (int64_t)P_ * ld_;
+    }
+    launch_batch_stats(cov_part_, mg_, tmean_, d_, cm, cd, ld_, comm_ ? P_ : C_, cum_cnt_, want_err, want_psrf,
+                       dstats_, stream_);
     DGB_CUDA(cudaMemcpyAsync(h_stats_, dstats_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
     DGB_CUDA(cudaMemcpyAsync(h_out_, hist_rate_, mc * 8, cudaMemcpyDeviceToHost, stream_));
     DGB_CUDA(cudaMemcpyAsync(h_out_ + mc, hist_beta_, mc * 8, cudaMemcpyDeviceToHost, stream_));
@@ -1285,7 +1198,7 @@ double Engine::run_batches_timed(int k) {
         DGB_CUDA(cudaEventRecord(timeline_base_, stream_));
     }
     // as the pipelined run loop: batch i + 1's first windows start at batch i's join
-    const bool early = !comm_ && !capture_ && !pool_;
+    const bool early = !capture_ && !pool_;
     if (early && !join_ev_) {
         DGB_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
         DGB_CUDA(cudaEventCreateWithFlags(&merge_ev_, cudaEventDisableTiming));
@@ -1304,9 +1217,9 @@ double Engine::run_batches_timed(int k) {
         join_groups();
         if (early) DGB_CUDA(cudaEventRecord(join_ev_, stream_));
         merge_batch();
-        // the batch statistics and the history copies of a diam_sample batch (on one GPU;
-        // the host reads nothing here)
-        if (!comm_) enqueue_batch_outputs(M);
+        // the batch statistics and the history copies of a diam_sample batch (the host reads
+        // nothing here)
+        enqueue_batch_outputs(M);
         if (early) DGB_CUDA(cudaEventRecord(merge_ev_, stream_));
         ++batches_done_;
     }
@@ -1331,11 +1244,11 @@ RunResult Engine::run() {  // runner.cpp:216-279
         dbg_ratio_ = dalloc<double>(allocs_, (size_t)C_ * Lw_);
         dbg_acc_ = dalloc<uint8_t>(allocs_, (size_t)C_ * Lw_);
     }
-    // Pipelined on one GPU when no rule needs a batch's statistics or state before the next
-    // batch may start (no tolerance, wall-clock limit or checkpoint): the next batch's first
-    // windows are enqueued before the host waits for this batch's outputs, so the GPU does
-    // not idle while the host reads them. Otherwise batch by batch, as runner.cpp:216-279.
-    const bool pipelined = !comm_ && !capture_ && !pool_ && cfg_.checkpoint_path.empty() && !cfg_.max_wall_seconds &&
+    // Pipelined when no rule needs a batch's statistics or state before the next batch may
+    // start (no tolerance, wall-clock limit or checkpoint): the next batch's first windows
+    // are enqueued before the host waits for this batch's outputs, so the GPU does not idle
+    // while the host reads them. Otherwise batch by batch, as runner.cpp:216-279.
+    const bool pipelined = !capture_ && !pool_ && cfg_.checkpoint_path.empty() && !cfg_.max_wall_seconds &&
                            !cfg_.psrf_tol && !cfg_.cov_tol && !cfg_.mean_tol;
     auto cap_reason = [&](size_t done) -> const char* {  // loop-top rules known without the GPU
         const uint64_t iters = (uint64_t)P_ * M * done * k_.n_lag;
@@ -1343,70 +1256,101 @@ RunResult Engine::run() {  // runner.cpp:216-279
         if (done >= cfg_.max_batches) return "batch_cap";
         return nullptr;
     };
+    // Several ranks: every decision to leave the loop is collective. The wall-clock rule is
+    // OR-ed over the ranks at the top of each batch (each rank reads its own clock), and a
+    // rank-local failure (jitter ladder exhausted, a launch error) is announced to the others
+    // at the point where they check, right before the merge's all-reduce, so every rank
+    // throws instead of waiting in a collective the failed rank never joins.
+    bool announced = false;  // this rank's failure has been announced
+    auto check_peers = [&] {
+        if (comm_ && comm_->any(false, stream_)) {
+            announced = true;  // the others know already
+            fail(Err::Unknown, "sampling failed on another rank (rank " + std::to_string(rank_) + " stops too)");
+        }
+    };
     bool head_queued = false;  // the next batch's plans and first windows are enqueued
     std::string reason;
-    for (;;) {
-        if (const char* cr = cap_reason(batches_done_)) {
-            reason = cr;
-            break;
-        }
-        if (cfg_.max_wall_seconds && elapsed() >= *cfg_.max_wall_seconds) {
-            reason = "wall_time";
-            break;
-        }
-        const auto b0 = std::chrono::steady_clock::now();
-        double ce, me, ps;
-        if (pipelined) {
-            if (!head_queued) {
+    try {
+        for (;;) {
+            if (const char* cr = cap_reason(batches_done_)) {
+                reason = cr;
+                break;
+            }
+            if (cfg_.max_wall_seconds) {
+                bool stop = elapsed() >= *cfg_.max_wall_seconds;
+                if (comm_) stop = comm_->any(stop, stream_);
+                if (stop) {
+                    reason = "wall_time";
+                    break;
+                }
+            }
+            const auto b0 = std::chrono::steady_clock::now();
+            double ce, me, ps;
+            if (pipelined) {
+                if (!head_queued) {
+                    fork_groups();
+                    begin_windows(cfg_.record_traces);
+                }
+                end_windows();
+                join_groups();
+                if (!join_ev_) {
+                    DGB_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
+                    DGB_CUDA(cudaEventCreateWithFlags(&merge_ev_, cudaEventDisableTiming));
+                }
+                DGB_CUDA(cudaEventRecord(join_ev_, stream_));
+                check_peers();
+                merge_batch();
+                enqueue_batch_outputs(M);
+                DGB_CUDA(cudaEventRecord(merge_ev_, stream_));
+                ++batches_done_;
+                head_queued = cap_reason(batches_done_) == nullptr;
+                if (head_queued) {
+                    // the next batch's first windows start at the join, not after the merge
+                    for (auto& g : groups_) DGB_CUDA(cudaStreamWaitEvent(g.s, join_ev_, 0));
+                    merge_pending_ = true;
+                    begin_windows(cfg_.record_traces);
+                    merge_pending_ = false;
+                }
+                read_batch_outputs(M, ce, me, ps);
+            } else {
                 fork_groups();
-                begin_windows(cfg_.record_traces);
+                run_batch_windows(cfg_.record_traces);
+                join_groups();
+                check_peers();
+                merge_batch();
+                enqueue_batch_outputs(M);
+                ++batches_done_;
+                read_batch_outputs(M, ce, me, ps);
             }
-            end_windows();
-            join_groups();
-            if (!join_ev_) {
-                DGB_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
-                DGB_CUDA(cudaEventCreateWithFlags(&merge_ev_, cudaEventDisableTiming));
+            batch_seconds_.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - b0).count());
+            cov_hist_.push_back(ce);
+            mean_hist_.push_back(me);
+            psrf_hist_.push_back(ps);
+            if (!cfg_.checkpoint_path.empty()) save_checkpoint(elapsed());  // runner.cpp:259
+            // the tolerance rules read statistics that are identical on every rank (the
+            // snapshot is all-reduced, the PSRF inputs all-gathered): no exchange needed
+            if (cfg_.psrf_tol && std::isfinite(ps) && ps <= *cfg_.psrf_tol) {
+                reason = "psrf";
+                break;
             }
-            DGB_CUDA(cudaEventRecord(join_ev_, stream_));
-            merge_batch();
-            enqueue_batch_outputs(M);
-            DGB_CUDA(cudaEventRecord(merge_ev_, stream_));
-            ++batches_done_;
-            head_queued = cap_reason(batches_done_) == nullptr;
-            if (head_queued) {
-                // the next batch's first windows start at the join, not after the merge
-                for (auto& g : groups_) DGB_CUDA(cudaStreamWaitEvent(g.s, join_ev_, 0));
-                merge_pending_ = true;
-                begin_windows(cfg_.record_traces);
-                merge_pending_ = false;
+            if (cfg_.cov_tol && std::isfinite(ce) && ce <= *cfg_.cov_tol) {
+                reason = "cov_tol";
+                break;
             }
-            read_batch_outputs(M, ce, me, ps);
-        } else {
-            fork_groups();
-            run_batch_windows(cfg_.record_traces);
-            join_groups();
-            merge_batch();
-            collect_batch_host(M);
-            ++batches_done_;
-            batch_stats(ce, me, ps);
+            if (cfg_.mean_tol && std::isfinite(me) && me <= *cfg_.mean_tol) {
+                reason = "mean_tol";
+                break;
+            }
         }
-        batch_seconds_.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - b0).count());
-        cov_hist_.push_back(ce);
-        mean_hist_.push_back(me);
-        psrf_hist_.push_back(ps);
-        if (!cfg_.checkpoint_path.empty()) save_checkpoint(elapsed());  // runner.cpp:259
-        if (cfg_.psrf_tol && std::isfinite(ps) && ps <= *cfg_.psrf_tol) {
-            reason = "psrf";
-            break;
+    } catch (...) {
+        if (comm_ && !announced) {
+            announced = true;
+            try {
+                comm_->any(true, stream_);
+            } catch (...) {
+            }
         }
-        if (cfg_.cov_tol && std::isfinite(ce) && ce <= *cfg_.cov_tol) {
-            reason = "cov_tol";
-            break;
-        }
-        if (cfg_.mean_tol && std::isfinite(me) && me <= *cfg_.mean_tol) {
-            reason = "mean_tol";
-            break;
-        }
+        throw;
     }
     const double wall = elapsed();
     wall_accum_ = wall;
@@ -1459,20 +1403,26 @@ RunResult Engine::build_result(const std::string& reason, double wall) {  // run
     r.mean_error_history = mean_hist_;
     r.psrf_history = psrf_hist_;
     r.functional_names = fnames_;
-    // histories of every chain (gathered across ranks); traces of the local chains only
+    // histories and traces of every chain: with several ranks each rank's chains are
+    // all-gathered (runner.cpp:459-489 returns every chain's). Every chain has the same
+    // number of history entries and of trace entries per functional.
     r.beta_history.assign(P_, {});
     r.acceptance_history.assign(P_, {});
     r.traces.assign(P_, std::vector<std::vector<double>>(fnames_.size()));
     const size_t nb = beta_hist_.empty() ? 0 : beta_hist_[0].size();
+    const size_t nf = fnames_.size();
+    const size_t nt = (traces_.empty() || traces_[0].empty()) ? 0 : traces_[0][0].size();
     if (comm_) {
         const int64_t maxc = (P_ + world_ - 1) / world_;
-        const int64_t blk = 2 * maxc * (int64_t)nb;
-        std::vector<double> mine(std::max<int64_t>(blk, 1), 0.0);
-        for (int c = 0; c < C_; ++c)
-            for (size_t j = 0; j < nb; ++j) {
-                mine[c * nb + j] = beta_hist_[c][j];
-                mine[maxc * nb + c * nb + j] = acc_hist_[c][j];
-            }
+        const int64_t per = 2 * (int64_t)nb + (int64_t)(nf * nt);  // doubles per chain
+        const int64_t blk = std::max<int64_t>(maxc * per, 1);
+        std::vector<double> mine(blk, 0.0);
+        for (int c = 0; c < C_; ++c) {
+            double* o = mine.data() + c * per;
+            std::copy(beta_hist_[c].begin(), beta_hist_[c].end(), o);
+            std::copy(acc_hist_[c].begin(), acc_hist_[c].end(), o + nb);
+            for (size_t f = 0; f < nf; ++f) std::copy(traces_[c][f].begin(), traces_[c][f].end(), o + 2 * nb + f * nt);
+        }
         double* dsrc = dalloc<double>(allocs_, blk);
         double* ddst = dalloc<double>(allocs_, blk * world_);
         DGB_CUDA(cudaMemcpyAsync(dsrc, mine.data(), blk * 8, cudaMemcpyHostToDevice, stream_));
@@ -1484,18 +1434,20 @@ RunResult Engine::build_result(const std::string& reason, double wall) {  // run
             int64_t base = 0, cr = 0;
             shard_range(P_, world_, rk, &base, &cr);
             for (int c = 0; c < cr; ++c) {
-                const double* b = all.data() + rk * blk + c * nb;
+                const double* b = all.data() + rk * blk + c * per;
                 r.beta_history[base + c].assign(b, b + nb);
-                r.acceptance_history[base + c].assign(b + maxc * nb, b + maxc * nb + nb);
+                r.acceptance_history[base + c].assign(b + nb, b + 2 * nb);
+                for (size_t f = 0; f < nf; ++f)
+                    r.traces[base + c][f].assign(b + 2 * nb + f * nt, b + 2 * nb + (f + 1) * nt);
             }
         }
     } else {
         for (int c = 0; c < C_; ++c) {
             r.beta_history[c0_ + c] = beta_hist_[c];
             r.acceptance_history[c0_ + c] = acc_hist_[c];
+            r.traces[c0_ + c] = std::move(traces_[c]);
         }
     }
-    for (int c = 0; c < C_; ++c) r.traces[c0_ + c] = std::move(traces_[c]);
     return r;
 }
 

@@ -155,18 +155,15 @@ private:
     bool merge_pending_ = false;
     void join_groups();  // main stream waits for every group
     void merge_batch();
-    void batch_stats(double& cov_err, double& mean_err, double& psrf);
-    // the same in two halves on one GPU: enqueue the statistics kernels and every per-batch
-    // output's copy into pinned memory (stream order), then read them once the stream got there
+    // per batch: enqueue the statistics kernels and every per-batch output's copy into
+    // pinned memory (stream order), then read them once the stream got there
     void enqueue_batch_outputs(size_t windows);
     void read_batch_outputs(size_t windows, double& cov_err, double& mean_err, double& psrf);
-    void collect_batch_host(size_t windows);
     void collect_histories(size_t windows, const std::vector<uint64_t>& n_start, const double* rate,
                            const double* beta, const double* lp, const double* pj);
     std::vector<uint64_t> out_n_start_;  // window start counts of the batch in h_out_
     void save_checkpoint(double wall);
-    void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s,
-              GemmShape sh = GemmShape::Big);
+    void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s);
     void refresh_g(const double* x, double* out, int chains, cudaStream_t s);
     void timed_begin(cudaStream_t s);
     void timed_end(const char* name, double flops, cudaStream_t s);

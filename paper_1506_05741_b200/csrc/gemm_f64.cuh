@@ -46,15 +46,7 @@ struct GemmBatch {
     int tri_c_lower;           // compute/store only n <= m
 };
 
-// Big / Narrow: the tile configuration DIAM_B200_GEMM_CFG selects; Square: 128x128 tiles
-// always (one column tile per 128 columns: in-place products whose tile reads columns
-// another tile of the same row block writes)
-// Stream: long-K, write-only window products (TRMM noise, target GEMM); the same tile as
-// Big today (measured equal or better than the 4-warp 64x32 tile), kept apart for tuning
-enum class GemmShape { Big, Narrow, Square, Stream };
-
 // Launch the batched GEMM on `stream`. Layout flags select the template instance.
-void gemm_f64(const GemmBatch& g, int batch, bool a_kmajor, bool b_kmajor, cudaStream_t stream,
-              GemmShape shape = GemmShape::Big);
+void gemm_f64(const GemmBatch& g, int batch, bool a_kmajor, bool b_kmajor, cudaStream_t stream);
 
 }  // namespace dgb

@@ -86,6 +86,11 @@ void launch_trace_floor(double* const* Cm, int64_t ld, const double* mb, int64_t
 // Merge helpers (proj/src/moments.cpp:51-88)
 void launch_sum_chains(double* out, const double* in, int64_t chain_stride, int chains, int64_t n,
                        double weight, cudaStream_t s);
+// packed lower triangle of sum_c S_c (chains ascending), and the merge of such a sum into Sg
+void launch_sum_chains_lower(double* out, const double* S, int64_t stride, int chains, int d, int64_t ld,
+                             cudaStream_t s);
+void launch_merge_lower(double* Sg, int64_t ld, const double* packed, int d, double keep, double wp,
+                        cudaStream_t s);
 void launch_axpby(double* y, const double* x, int64_t n, double a, double b, cudaStream_t s);
 // cum mean/diag fold (merge_into restricted to the PSRF inputs)
 void launch_cum_fold(double* cmean, double* cdiag, const double* lmean, const double* S,
@@ -109,25 +114,14 @@ void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr
 // Cholesky of the lower part of A_c (in place), blocked right-looking with the
 // diagonal blocks factored in shared memory, TRSM and SYRK through gemm_f64.
 // status[c] = 0 ok, 1 not positive definite. Only chains with mask[c] != 0.
-struct DagState;
 struct PotrfWork {
-    double* inv;  // potrf_work_doubles(chains): inverse diagonal blocks (64x64 or 128x128
-                  // per chain), then int active[chains]
-    double** inv_ptrs;     // chain i: inv + i * 64 * 64
+    double* inv;           // potrf_work_doubles(chains): per chain a 128x128 slot holding the two
+                           // 64x64 inverse diagonal blocks of a block column, then int active[chains]
     double** inv128_ptrs;  // chain i: inv + i * 128 * 128
-    int workers = 0;          // task-graph POTRF: persistent CTAs (0 = one per SM)
-    DagState* dag = nullptr;  // task-graph POTRF: task order, flags, inverse tiles (lazy)
 };
 inline size_t potrf_work_doubles(int chains) { return (size_t)chains * 128 * 128 + chains; }
 void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status,
                    PotrfWork& w, cudaStream_t s, int extra_rows = 0);
-// the task-graph POTRF (potrf_dag.cu); potrf_batched routes here unless DIAM_B200_POTRF
-// selects the launch-per-phase paths
-void potrf_dag(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status, PotrfWork& w,
-               cudaStream_t s, int extra_rows);
-bool potrf_dag_aborted(const PotrfWork& w);  // valid once the POTRF's stream work completed
-size_t potrf_dag_bytes(int d, int chains);   // inverse tiles kept per factorization
-void potrf_work_release(PotrfWork& w);
 // q_c = half_inv_infl2 * |row d of L_c|^2 (the augmented row = L^{-1}(x - x_ref))
 void launch_aug_quad(double* const* L, int64_t ld, int d, int chains, double half_inv_infl2, const int* mask,
                      double* q, cudaStream_t s);

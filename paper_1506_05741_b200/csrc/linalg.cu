@@ -5,7 +5,6 @@
 
 #include "gemm_f64.cuh"
 #include "gemm_tile.cuh"
-#include "diag_block.cuh"
 #include "diag_tc.cuh"
 #include "kernels.cuh"
 
@@ -84,17 +83,21 @@ __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const d
         const int i = first ? r1 : r2;
         const int j = 2 * (first ? q : q - q1);
         const double mbi = first ? mb1 : mb2;
-        const double2 sg = *reinterpret_cast<const double2*>(Sg + (int64_t)i * ld + j);
-        const double2 sl = *reinterpret_cast<const double2*>(Sl + c * sl_stride + (int64_t)i * ld + j);
-        const double2 g2 = *reinterpret_cast<const double2*>(mg + j);
-        const double2 l2 = *reinterpret_cast<const double2*>(mlc + j);
+        // the pair (j, j+1) is loaded as one double2 unless j+1 lies past the diagonal: at
+        // j = i = d-1 with ld == d it would be past the end of the row (and of the buffer)
+        const bool pair = j + 1 <= i;
+        auto ld2 = [&](const double* p) { return pair ? *reinterpret_cast<const double2*>(p) : make_double2(*p, 0.0); };
+        const double2 sg = ld2(Sg + (int64_t)i * ld + j);
+        const double2 sl = ld2(Sl + c * sl_stride + (int64_t)i * ld + j);
+        const double2 g2 = ld2(mg + j);
+        const double2 l2 = ld2(mlc + j);
         // covariance :90-101 (S exactly symmetric) of the blend :45-46
         double v0 = (wg * sg.x + wl * sl.x) - mbi * (wg * g2.x + wl * l2.x);
         double v1 = (wg * sg.y + wl * sl.y) - mbi * (wg * g2.y + wl * l2.y);
         if (j == i) v0 += jit;
         if (j + 1 == i) v1 += jit;
         double* Crow = C_out[c] + (int64_t)i * ld;
-        if (j + 1 <= i)
+        if (pair)
             *reinterpret_cast<double2*>(Crow + j) = make_double2(v0, v1);
         else
             Crow[j] = v0;
@@ -127,6 +130,36 @@ __global__ void sum_chains_kernel(double* out, const double* in, int64_t chain_s
         double s = 0.0;
         for (int c = 0; c < chains; ++c) s += in[c * chain_stride + e];
         out[e] = weight * s;
+    }
+}
+
+// out[i (i+1) / 2 + j] = sum_c S_c[i][j] for j <= i (chains in ascending order): the
+// packed lower triangle of the local moment sum, the only part the merge needs (half the
+// bytes of the square, and of the all-reduce on several GPUs). CTA p takes rows p and
+// d-1-p, so every CTA moves the same number of entries.
+__global__ void sum_chains_lower_kernel(double* out, const double* S, int64_t stride, int chains, int d,
+                                        int64_t ld) {
+    const int p = blockIdx.x, r1 = p, r2 = d - 1 - p;
+    const int q1 = r1 + 1, q2 = r2 == r1 ? 0 : r2 + 1;
+    for (int q = threadIdx.x; q < q1 + q2; q += blockDim.x) {
+        const bool first = q < q1;
+        const int i = first ? r1 : r2, j = first ? q : q - q1;
+        const double* src = S + (int64_t)i * ld + j;
+        double s = 0.0;
+        for (int c = 0; c < chains; ++c) s += src[c * stride];
+        out[(int64_t)i * (i + 1) / 2 + j] = s;
+    }
+}
+
+// Sg[i][j] = keep Sg[i][j] + wp packed[i (i+1) / 2 + j], j <= i (proj/src/moments.cpp:63-74)
+__global__ void merge_lower_kernel(double* Sg, int64_t ld, const double* packed, int d, double keep, double wp) {
+    const int p = blockIdx.x, r1 = p, r2 = d - 1 - p;
+    const int q1 = r1 + 1, q2 = r2 == r1 ? 0 : r2 + 1;
+    for (int q = threadIdx.x; q < q1 + q2; q += blockDim.x) {
+        const bool first = q < q1;
+        const int i = first ? r1 : r2, j = first ? q : q - q1;
+        double* y = Sg + (int64_t)i * ld + j;
+        *y = keep * *y + wp * packed[(int64_t)i * (i + 1) / 2 + j];
     }
 }
 
@@ -314,13 +347,12 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const double* G, int64_t
 constexpr int kNb = kDiagNb;
 
 
-// MINB 2: <= 128 registers (spills a little) so a diagonal-block CTA can share its SM with
-// a GEMM CTA of another group; MINB 1: 190 registers, no spills
-// pre (TC only): 1 = first update the block by the 64 (final) columns to its left
-// (diag64_tc_sc's pre_L); 2 = those columns still need their solve against the inverse at
-// inv_base + c inv_stride (pre_X). The inverse goes to inv_base + c inv_stride + inv_off.
-template <int MINB, bool TC>
-__global__ void __launch_bounds__(256, MINB) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
+// Two CTAs per SM (<= 128 registers) so a diagonal-block CTA can share its SM with a GEMM
+// CTA of another chain group. pre: 1 = first update the block by the 64 (final) columns to
+// its left (diag64_tc_sc's pre_L); 2 = those columns still need their solve against the
+// inverse at inv_base + c inv_stride (pre_X). The inverse goes to inv_base + c inv_stride +
+// inv_off.
+__global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
                                                             const int* mask, int* status, int* active,
                                                             double* inv_base, int zero_above, int pre = 0,
                                                             int inv_stride = kDiagNb * kDiagNb, int inv_off = 0) {
@@ -331,9 +363,8 @@ __global__ void __launch_bounds__(256, MINB) potrf_diag_kernel(double* const* Am
     if (!run) return;
     double* Ab = Am[c] + (int64_t)j0 * ld + j0;
     double* out = inv_base + (int64_t)c * inv_stride + inv_off;
-    const int bad = TC ? diag64_tc_sc(*reinterpret_cast<DiagTcScratch*>(dyn_smem), Ab, ld, jb, out, zero_above, kNb,
-                                      pre ? Ab - kNb : nullptr, pre == 2 ? inv_base + (int64_t)c * inv_stride : nullptr)
-                       : diag64_block(Ab, ld, jb, out, zero_above);
+    const int bad = diag64_tc_sc(*reinterpret_cast<DiagTcScratch*>(dyn_smem), Ab, ld, jb, out, zero_above, kNb,
+                                 pre ? Ab - kNb : nullptr, pre == 2 ? inv_base + (int64_t)c * inv_stride : nullptr);
     if (bad && threadIdx.x == 0) {
         status[c] = 1;
         active[c] = 0;
@@ -365,80 +396,6 @@ __global__ void __launch_bounds__(256, 2) potrf_solve3_kernel(double* const* Am,
     __threadfence_block();
     tile::gemm_tile<FusedTile, true, true>(t2, inv[c] + kNb * kNb, t2, ld, kNb, ld, rows, n2, n2, m0, 0, 1.0, 0.0,
                                            false, smem, true);
-}
-
-// 128x128 diagonal block: L11 = chol, X = L11^-1 (diag128_tc), one CTA per chain; the
-// block's upper-right 64x64 quarter is zeroed (the factor's strict upper part is exact zeros)
-__global__ void __launch_bounds__(256, 1) potrf_diag128_kernel(double* const* Am, int64_t ld, int j0, int jb,
-                                                               const int* mask, int* status, int* active,
-                                                               double* inv_base) {
-    extern __shared__ __align__(16) double dyn_smem[];
-    const int c = blockIdx.x;
-    const bool run = (!mask || mask[c]) && status[c] == 0;
-    if (threadIdx.x == 0) active[c] = run ? 1 : 0;
-    if (!run) return;
-    double* Ab = Am[c] + (int64_t)j0 * ld + j0;
-    if (jb > kNb)
-        for (int e = threadIdx.x; e < kNb * (jb - kNb); e += blockDim.x)
-            Ab[(int64_t)(e / (jb - kNb)) * ld + kNb + e % (jb - kNb)] = 0.0;
-    const int bad = diag128_tc(Ab, ld, jb, inv_base + (int64_t)c * kD2 * kD2, dyn_smem);
-    if (bad && threadIdx.x == 0) {
-        status[c] = 1;
-        active[c] = 0;
-    }
-}
-
-// ------------------------------------------------------------------ persistent per-chain POTRF
-// One 2-CTA cluster per chain walks the whole left-looking factorization (64-wide block
-// columns): both CTAs split the panel-update and TRSM tiles of a block column, CTA 0
-// factors the diagonal block in between, and cluster barriers (release/acquire at cluster
-// scope) order the phases. One launch per factorization instead of three per block column,
-// and a group of chains occupies only 2 SMs per chain, leaving the rest of the GPU to the
-// other chain groups' GEMMs.
-using PotrfTile = tile::Cfg<128, 64, 16, 4, true, true, 4, 2, 1>;  // 123 KB ring: one CTA per SM
-
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-__device__ __forceinline__ unsigned cluster_rank() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-    return r;
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
-    potrf_cluster_kernel(double* const* Am, int64_t ld, int d, int rows, const int* mask, int* status,
-                         double* inv_base) {
-    const int c = blockIdx.x >> 1;
-    const int rank = (int)cluster_rank();
-    if ((mask && !mask[c]) || status[c] != 0) return;  // uniform for both CTAs of the cluster
-    extern __shared__ __align__(16) double ring[];
-    double* A = Am[c];
-    double* inv = inv_base + (int64_t)c * kNb * kNb;
-    for (int j0 = 0; j0 < d; j0 += kNb) {
-        const int jb = min(kNb, d - j0);
-        if (j0 > 0) {  // A[j0:, J] -= L[j0:, :j0] L[J, :j0]^T, row tiles split over the pair
-            const int M = rows - j0;
-            for (int t = rank; t * PotrfTile::BM < M; t += 2)
-                tile::gemm_tile<PotrfTile, true, true>(A + (int64_t)j0 * ld, A + (int64_t)j0 * ld,
-                                                       A + (int64_t)j0 * ld + j0, ld, ld, ld, M, jb, j0,
-                                                       t * PotrfTile::BM, 0, -1.0, 1.0, false, ring);
-        }
-        cluster_sync_all();
-        if (rank == 0) {
-            const int failed = diag64_block(A + (int64_t)j0 * ld + j0, ld, jb, inv, 0);
-            if (failed && threadIdx.x == 0) status[c] = 1;
-        }
-        cluster_sync_all();
-        if (*(volatile int*)(status + c) != 0) return;  // both CTAs leave at the same point
-        const int M3 = rows - j0 - jb;
-        for (int t = rank; t * PotrfTile::BM < M3; t += 2)  // L21 = A21 inv(L11)^T in place
-            tile::gemm_tile<PotrfTile, true, true>(A + (int64_t)(j0 + jb) * ld + j0, inv,
-                                                   A + (int64_t)(j0 + jb) * ld + j0, ld, kNb, ld, M3, jb, jb,
-                                                   t * PotrfTile::BM, 0, 1.0, 0.0, false, ring);
-        cluster_sync_all();
-    }
 }
 
 __global__ void aug_quad_kernel(double* const* Lm, int64_t ld, int d, double hq, const int* mask, double* q) {
@@ -618,6 +575,20 @@ void launch_sum_chains(double* out, const double* in, int64_t chain_stride, int 
     count_launch();
 }
 
+void launch_sum_chains_lower(double* out, const double* S, int64_t stride, int chains, int d, int64_t ld,
+                             cudaStream_t s) {
+    sum_chains_lower_kernel<<<(d + 1) / 2, 256, 0, s>>>(out, S, stride, chains, d, ld);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+void launch_merge_lower(double* Sg, int64_t ld, const double* packed, int d, double keep, double wp,
+                        cudaStream_t s) {
+    merge_lower_kernel<<<(d + 1) / 2, 256, 0, s>>>(Sg, ld, packed, d, keep, wp);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
 void launch_axpby(double* y, const double* x, int64_t n, double a, double b, cudaStream_t s) {
     axpby_kernel<<<grid_for(n, 256), 256, 0, s>>>(y, x, n, a, b);
     DGB_LAUNCH_CHECK();
@@ -716,11 +687,7 @@ void launch_cov_error(const double* Sg, const double* mg, const double* Ctrue, i
 void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr, int64_t vstride, double* y,
                  double* quad_out, int chains, int d, double half_inv_infl2, const int* mask, cudaStream_t s) {
     const size_t smem = sizeof(double) * (((d + 1) & ~1) + kTrsvB * (kTrsvB + 1) + kTrsvB);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        DGB_CUDA(cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
-    }
+    if (smem > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(trsv_kernel), (int)smem);
     trsv_kernel<<<chains, kTrsvThreads, smem, s>>>(L, ld, x, xr, vstride, y, quad_out, d, half_inv_infl2, mask);
     DGB_LAUNCH_CHECK();
     count_launch();
@@ -728,97 +695,63 @@ void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr
 
 void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status, PotrfWork& w,
                    cudaStream_t s, int extra_rows) {
-    // Left-looking blocked Cholesky, 64-wide block columns J = [j0, j0+64):
-    //   (1) A[j0:, J] -= L[j0:, :j0] L[J, :j0]^T   DMMA GEMM, K = j0 (large), N = 64
-    //   (2) L[J, J] = chol(A[J, J]), inv(L[J, J])  one CTA per chain, registers
-    //   (3) L[j0+64:, J] = A[j0+64:, J] inv(L[J,J])^T   DMMA GEMM (TRSM via the inverse)
+    // Left-looking blocked Cholesky over 128-wide block columns J = [j0, j0+128):
+    //   (1) A[j0:, J] -= L[j0:, :j0] L[J, :j0]^T    one long-K DMMA GEMM (lower tiles of the
+    //                                               diagonal block only)
+    //   (2) the first 64x64 diagonal block: L11 = chol, X11 = L11^-1 (one CTA per chain,
+    //       shared memory, diag_tc.cuh)
+    //   (3) the second one: its rows of the first half-column solved against X11 and their
+    //       64-deep update applied first, then L22, X22
+    //   (4) everything below (potrf_solve3_kernel): L[r, J1] = A[r, J1] X11^T, the 64-deep
+    //       update, L[r, J2] = T X22^T as three chained DMMA tile products per 128-row tile
+    // A last block column of width <= 64 is a diagonal block + one TRSM GEMM.
     // `extra_rows` augmented rows r^T below row d-1 ride along as ordinary rows of the
     // GEMMs and TRSMs and come out as (L^{-1} r)^T: the forward substitution of the
     // usable-factor guard (proj/src/proposal.cpp:185-199) costs no extra pass over L.
-    // w.inv holds chains*64*64 doubles, followed (by the caller's allocation) by an int active[chains]
+    // w.inv holds chains*128*128 doubles, followed by an int active[chains]
     int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kD2 * kD2);
     const int rows = d + extra_rows;
-    // Default (mode 4, "fused"): per 128-wide block column the long-K update GEMM, the two
-    // 64x64 diagonal blocks (the second one also solving its rows of the first half-column
-    // and applying their 64-deep update, in shared memory) and ONE kernel for everything
-    // below (potrf_solve3_kernel): 4 launches per block column, 26.1 ms per d=1024 batch.
-    // DIAM_B200_POTRF (read per call):
-    //   narrow  diagonal block + TRSM per 64-wide half and a separate 64-deep update GEMM
-    //           between them (6 launches per block column, 26.4 ms)
-    //   dag     the task-graph POTRF (potrf_dag.cu): one persistent launch per factorization;
-    //           faster on one stream (7.7 vs 9.1 ms per d=1024 batch), equal with 8 chain
-    //           groups, 12% slower at d=4096 (K=128 tile updates vs the long-K updates here)
-    //   cluster the persistent 2-CTA-cluster kernel: 6% slower at d=1024 with 4 groups
-    //   wide    128-wide diagonal blocks (diag128_tc) and 128-deep TRSMs: 24 launches per
-    //           factorization instead of 40; its diagonal block (61 us) costs about as much
-    //           as two 64-wide ones plus the 64-deep update between them: equal at d=1024,
-    //           2040 and 4096
-    const char* pe = std::getenv("DIAM_B200_POTRF");
-    const std::string pm = pe ? pe : "";
-    const int mode = pm == "dag" ? 0 : pm == "cluster" ? 2 : pm == "wide" ? 3 : pm == "narrow" ? 1 : 4;
-    if (mode == 0) {
-        potrf_dag(A, ld, d, chains, mask, status, w, s, extra_rows);
-        return;
-    }
-    if (mode == 2) {
-        static bool attr = false;
-        if (!attr) {
-            DGB_CUDA(cudaFuncSetAttribute(potrf_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          PotrfTile::SMEM_BYTES));
-            attr = true;
+    set_smem_attr(reinterpret_cast<const void*>(potrf_diag_kernel), (int)sizeof(DiagTcScratch));
+    set_smem_attr(reinterpret_cast<const void*>(potrf_solve3_kernel), FusedTile::SMEM_BYTES);
+    for (int j0 = 0; j0 < d; j0 += 2 * kNb) {
+        const int jb = std::min(2 * kNb, d - j0);
+        if (j0 > 0) {
+            // A[j0:rows, J] -= L[j0:rows, :j0] L[J, :j0]^T; the warps above the diagonal of
+            // the diagonal tile skip their DMMAs and its upper quarter keeps its zeros
+            GemmBatch p{};
+            p.A = (const double* const*)A;
+            p.B = (const double* const*)A;
+            p.C = A;
+            p.a_off = (int64_t)j0 * ld;
+            p.b_off = (int64_t)j0 * ld;
+            p.c_off = (int64_t)j0 * ld + j0;
+            p.lda = p.ldb = p.ldc = ld;
+            p.M = rows - j0;
+            p.N = jb;
+            p.K = j0;
+            p.alpha = -1.0;
+            p.beta = 1.0;
+            p.active = active;
+            p.tri_c_lower = 1;
+            gemm_f64(p, chains, true, true, s);
         }
-        potrf_cluster_kernel<<<2 * chains, 256, PotrfTile::SMEM_BYTES, s>>>(A, ld, d, rows, mask, status, w.inv);
+        const int n1 = std::min(kNb, jb);
+        // X11 (and X22) side by side in the chain's 128 x 128 inverse slot
+        potrf_diag_kernel<<<chains, 256, sizeof(DiagTcScratch), s>>>(A, ld, j0, n1, mask, status, active, w.inv, 0,
+                                                                      0, kD2 * kD2, 0);
         DGB_LAUNCH_CHECK();
         count_launch();
-        return;
-    }
-    // A[r0:rows, c0:c0+n] -= L[r0:rows, k0:k0+k] L[c0:c0+n, k0:k0+k]^T
-    auto update = [&](int r0, int c0, int n, int k0, int k, GemmShape shape, int tri_c = 0) {
-        GemmBatch p{};
-        p.A = (const double* const*)A;
-        p.B = (const double* const*)A;
-        p.C = A;
-        p.a_off = (int64_t)r0 * ld + k0;
-        p.b_off = (int64_t)c0 * ld + k0;
-        p.c_off = (int64_t)r0 * ld + c0;
-        p.lda = p.ldb = p.ldc = ld;
-        p.M = rows - r0;
-        p.N = n;
-        p.K = k;
-        p.alpha = -1.0;
-        p.beta = 1.0;
-        p.active = active;
-        p.tri_c_lower = tri_c;
-        gemm_f64(p, chains, true, true, s, shape);
-    };
-    if (mode == 3) {
-        // 128-wide block columns, each: (1) the left-looking update A[j0:, J] -= L[j0:, :j0]
-        // L[J, :j0]^T (lower part of the diagonal tile only), (2) chol + inverse of the
-        // 128x128 diagonal block in one CTA per chain, (3) L21 = A21 inv(L11)^T as one
-        // 128-deep GEMM on 128x128 tiles (in place: one column tile per row block), the
-        // inverse's upper zeros skipped. 24 launches per factorization instead of 40.
-        static bool attr = false;
-        if (!attr) {
-            DGB_CUDA(cudaFuncSetAttribute(potrf_diag128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kDiag128SmemBytes));
-            attr = true;
-        }
-        for (int j0 = 0; j0 < d; j0 += kD2) {
-            const int jb = std::min(kD2, d - j0);
-            if (j0 > 0) update(j0, j0, jb, 0, j0, GemmShape::Big, 1);
-            potrf_diag128_kernel<<<chains, 256, kDiag128SmemBytes, s>>>(A, ld, j0, jb, mask, status, active, w.inv);
-            DGB_LAUNCH_CHECK();
-            count_launch();
+        if (jb <= kNb) {  // a last, narrow block column: TRSM L21 = A21 X11^T below it
             const int rest = rows - j0 - jb;
             if (rest <= 0) continue;
             GemmBatch t{};
             t.A = (const double* const*)A;
-            t.B = (const double* const*)w.inv128_ptrs;
+            t.B = (const double* const*)w.inv128_ptrs;  // X11 with stride 64 at the slot start
             t.C = A;
             t.a_off = (int64_t)(j0 + jb) * ld + j0;
             t.c_off = t.a_off;
             t.lda = ld;
-            t.ldb = kD2;
+            t.ldb = kNb;
             t.ldc = ld;
             t.M = rest;
             t.N = jb;
@@ -826,102 +759,21 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
             t.alpha = 1.0;
             t.beta = 0.0;
             t.active = active;
-            t.tri_b_lower = 1;
-            gemm_f64(t, chains, true, true, s, GemmShape::Square);
+            gemm_f64(t, chains, true, true, s);  // one 64-wide column tile per CTA: safe in place
+            continue;
         }
-        return;
-    }
-    // factor the 64-wide diagonal block at (c0, c0) and solve the rows below it (in place)
-    auto factor_and_solve = [&](int c0, int n, int zero_above) {
-        // the diagonal block: panel-by-warp + DMMA (diag_tc.cuh, default: 23 vs 27 us per
-        // block, 4.5% off the POTRF), or DIAM_B200_DIAG=block (read per call) for the
-        // register-blocked version (diag_block.cuh)
-        const char* de = std::getenv("DIAM_B200_DIAG");
-        const bool tc = !(de && std::string(de) == "block");
-        if (tc) {
-            static bool attr = false;
-            if (!attr) {
-                DGB_CUDA(cudaFuncSetAttribute(potrf_diag_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)sizeof(DiagTcScratch)));
-                attr = true;
-            }
-            potrf_diag_kernel<2, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(A, ld, c0, n, mask, status, active,
-                                                                                  w.inv, zero_above);
-        } else {
-            potrf_diag_kernel<2, false><<<chains, 256, 0, s>>>(A, ld, c0, n, mask, status, active, w.inv, zero_above);
-        }
+        const int c1 = j0 + kNb, n2 = jb - kNb;
+        potrf_diag_kernel<<<chains, 256, sizeof(DiagTcScratch), s>>>(A, ld, c1, n2, mask, status, active, w.inv,
+                                                                      j0 > 0 ? 1 : 0, 2, kD2 * kD2, kNb * kNb);
         DGB_LAUNCH_CHECK();
         count_launch();
-        const int rest = rows - c0 - n;
-        if (rest <= 0) return;
-        // TRSM: L21 = A21 inv(L11)^T  (one 64-wide column tile per CTA -> safe in place)
-        GemmBatch t{};
-        t.A = (const double* const*)A;
-        t.B = (const double* const*)w.inv_ptrs;
-        t.C = A;
-        t.a_off = (int64_t)(c0 + n) * ld + c0;
-        t.c_off = t.a_off;
-        t.lda = ld;
-        t.ldb = kNb;
-        t.ldc = ld;
-        t.M = rest;
-        t.N = n;
-        t.K = n;
-        t.alpha = 1.0;
-        t.beta = 0.0;
-        t.active = active;
-        gemm_f64(t, chains, true, true, s, GemmShape::Narrow);
-    };
-    if (mode == 4) {
-        static bool attr = false;
-        if (!attr) {
-            DGB_CUDA(cudaFuncSetAttribute(potrf_diag_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)sizeof(DiagTcScratch)));
-            DGB_CUDA(cudaFuncSetAttribute(potrf_solve3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          FusedTile::SMEM_BYTES));
-            attr = true;
-        }
-        for (int j0 = 0; j0 < d; j0 += 2 * kNb) {
-            const int jb = std::min(2 * kNb, d - j0);
-            // lower part of the diagonal tile only: the warps above the diagonal skip their
-            // DMMAs (25.9 vs 26.1 ms per d=1024 batch) and the upper quarter keeps its zeros
-            if (j0 > 0) update(j0, j0, jb, 0, j0, GemmShape::Big, 1);
-            if (jb <= kNb) {  // a last, narrow block column: diagonal block + TRSM
-                factor_and_solve(j0, jb, 0);
-                continue;
-            }
-            // X11 and X22 side by side in the chain's 128 x 128 inverse slot
-            const int c1 = j0 + kNb, n2 = jb - kNb;
-            potrf_diag_kernel<2, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(
-                A, ld, j0, kNb, mask, status, active, w.inv, 0, 0, kD2 * kD2, 0);
-            DGB_LAUNCH_CHECK();
-            count_launch();
-            potrf_diag_kernel<2, true><<<chains, 256, sizeof(DiagTcScratch), s>>>(
-                A, ld, c1, n2, mask, status, active, w.inv, j0 > 0 ? 1 : 0, 2, kD2 * kD2, kNb * kNb);
-            DGB_LAUNCH_CHECK();
-            count_launch();
-            const int rest = rows - c1 - n2;
-            if (rest <= 0) continue;
-            dim3 grid(1, (unsigned)ceil_div(rest, FusedTile::BM), (unsigned)chains);
-            potrf_solve3_kernel<<<grid, 256, FusedTile::SMEM_BYTES, s>>>(A, ld, c1 + n2, j0, rest, n2, active,
-                                                                         w.inv128_ptrs);
-            DGB_LAUNCH_CHECK();
-            count_launch();
-        }
-        return;
-    }
-    // 128-wide block columns: the bulk of the flops is one left-looking DMMA GEMM per
-    // block column with K = j0 on full 128x128 tiles; inside, two 64-wide halves are
-    // factored right-looking (diag + TRSM, 64-deep update of the second half).
-    for (int j0 = 0; j0 < d; j0 += 2 * kNb) {
-        const int jb = std::min(2 * kNb, d - j0);
-        if (j0 > 0) update(j0, j0, jb, 0, j0, GemmShape::Big);
-        const int h1 = std::min(kNb, jb);
-        factor_and_solve(j0, h1, 0);
-        if (jb > kNb) {
-            update(j0 + kNb, j0 + kNb, jb - kNb, j0, kNb, GemmShape::Narrow);
-            factor_and_solve(j0 + kNb, jb - kNb, j0 > 0 ? 1 : 0);
-        }
+        const int rest = rows - c1 - n2;
+        if (rest <= 0) continue;
+        dim3 grid(1, (unsigned)ceil_div(rest, FusedTile::BM), (unsigned)chains);
+        potrf_solve3_kernel<<<grid, 256, FusedTile::SMEM_BYTES, s>>>(A, ld, c1 + n2, j0, rest, n2, active,
+                                                                     w.inv128_ptrs);
+        DGB_LAUNCH_CHECK();
+        count_launch();
     }
 }
 

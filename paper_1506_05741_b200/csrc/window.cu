@@ -13,8 +13,6 @@
 // each step is one fused pass (candidate, two dot products, CTA reduction with
 // a single barrier, accept/reject from the chain's Philox uniform) — the
 // "fused warp-level accept/reject" of the design.
-#include <cstdlib>
-
 #include "kernels.cuh"
 
 namespace dgb {
@@ -57,6 +55,7 @@ __global__ void draws_kernel(int kind, double* out_f64, uint64_t* out_u64, int64
 }
 
 constexpr int kStepThreads = 512;
+constexpr int kMaxStages = 8;  // TMA ring depth bound (one mbarrier per stage)
 constexpr int kStepWarps = kStepThreads / 32;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -269,7 +268,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     const bool pcn = p.pcn != 0;
     const int nrows = pcn ? 3 : 2;  // xi, h (+ w for the pCN-form y recursion)
     extern __shared__ __align__(128) double ring[];  // NS stages, then the log-uniform table
-    __shared__ __align__(8) uint64_t full[8];
+    __shared__ __align__(8) uint64_t full[kMaxStages];
     __shared__ double red[2][NW][2];
     const uint32_t row_bytes = (uint32_t)(ld * sizeof(double));
     double* stage0 = ring;
@@ -436,15 +435,11 @@ bool try_tma(const StepParams& p, cudaStream_t s) {
     if (table + 2 * stage > kMaxSmem) return false;
     // ring depth: deep enough to hide HBM latency, shallow enough that a 110 KB GEMM CTA of
     // another chain group can share the SM (d=1024: 6 stages = 100 KB; 6 vs 8 stages
-    // measured equal within 0.3%; DIAM_B200_STEP_STAGES overrides)
-    static const int max_ns = [] {
-        const char* e = std::getenv("DIAM_B200_STEP_STAGES");
-        return e ? std::max(2, std::atoi(e)) : 6;
-    }();
-    const int NS = (int)std::min<size_t>((size_t)max_ns, (kMaxSmem - table) / stage);
+    // measured equal within 0.3%); at most kMaxStages (the mbarrier array)
+    const int NS = (int)std::min<size_t>((size_t)std::min(6, kMaxStages), (kMaxSmem - table) / stage);
     const size_t smem = NS * stage + table;
     auto kern = mh_window_tma_kernel<R, TW, T>;
-    DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_smem_attr(reinterpret_cast<const void*>(kern), (int)smem);
     kern<<<p.chains, T, smem, s>>>(p, NS);
     return true;
 }
@@ -456,16 +451,9 @@ void launch_r(const StepParams& p, cudaStream_t s) {
     dim3 grid(p.chains), block(kStepThreads);
     // 256 threads (2 double2 pairs each) up to d = 1024, then 512 threads: fewer warps per
     // step barrier and reduction for the small dimensions where the step loop matters most
+    // (128 threads measured slower at d = 1024)
     bool done = false;
-    static const int small_threads = [] {
-        const char* e = std::getenv("DIAM_B200_STEP_THREADS");  // experiments: 128 | 256
-        return e ? std::atoi(e) : 256;
-    }();
-    if (small_threads == 128 && pairs <= 512) {
-        if (pairs <= 128) done = try_tma<1, TW, 128>(p, s);
-        else if (pairs <= 256) done = try_tma<2, TW, 128>(p, s);
-        else done = try_tma<4, TW, 128>(p, s);
-    } else if (pairs <= 256) done = try_tma<1, TW, 256>(p, s);
+    if (pairs <= 256) done = try_tma<1, TW, 256>(p, s);
     else if (pairs <= 512) done = try_tma<2, TW, 256>(p, s);
     else if (R <= 2) done = try_tma<2, TW, 512>(p, s);
     else if (R <= 4) done = try_tma<4, TW, 512>(p, s);

@@ -141,16 +141,10 @@ def oracle_chol(m):
     return st, out
 
 
-@pytest.mark.parametrize("mode", ["wide", "fused", "narrow", "narrow+regdiag", "dag", "cluster"])
-@pytest.mark.parametrize("d", [1, 5, 64, 65, 127, 128, 129, 130, 257, 520])
-def test_potrf_batched_vs_oracle(lib, monkeypatch, d, mode):
-    # every factorization path: the launch-per-phase blocked POTRF with 128-wide diagonal
-    # blocks (default), with 64-wide ones (DMMA diagonal block of diag_tc.cuh; also the
-    # register-blocked one), the task-graph persistent kernel (potrf_dag.cu), the
-    # 2-CTA-cluster kernel
-    monkeypatch.setenv("DIAM_B200_POTRF", mode.split("+")[0])
-    if mode.endswith("regdiag"):
-        monkeypatch.setenv("DIAM_B200_DIAG", "block")
+@pytest.mark.parametrize("d", [1, 5, 63, 64, 65, 127, 128, 129, 130, 191, 192, 193, 257, 520, 1024])
+def test_potrf_batched_vs_oracle(lib, d):
+    # the blocked POTRF at every block-column shape: one or two 64-wide diagonal blocks per
+    # 128-wide block column, ragged and narrow last block columns
     rng = np.random.default_rng(d)
     batch = 3
     ld = (d + 7) // 8 * 8

@@ -130,13 +130,13 @@ def test_lockstep_chunked_windows_shared_workspace(b200, tmp_path, monkeypatch, 
     assert ties == 0
 
 
-@pytest.mark.parametrize("mode", ["narrow", "fused", "wide", "dag", "cluster"])
-def test_lockstep_alternative_potrf(b200, tmp_path, monkeypatch, mode):
-    # the alternative factorization paths under the full engine (augmented usable-guard
-    # row, a ragged last tile: d = 133 = 128 + 5, two chain groups)
-    monkeypatch.setenv("DIAM_B200_POTRF", mode)
+@pytest.mark.parametrize("d", [133, 180, 200])
+def test_lockstep_potrf_block_shapes(b200, tmp_path, monkeypatch, d):
+    # the blocked factorization's edge shapes under the full engine (augmented usable-guard
+    # row, two chain groups): 133 = 128 + 5 (a narrow last block column), 180 = 128 + 52,
+    # 200 = 128 + 64 + 8 (a last block column with two diagonal blocks, the second ragged)
     monkeypatch.setenv("DIAM_B200_GROUPS", "2")
-    _, _, ties = lockstep(b200, tmp_path, "pi2", 133, "diam", P=4, M=2, K=2, n_lag=150, n0=0, seed=9)
+    _, _, ties = lockstep(b200, tmp_path, "pi2", d, "diam", P=4, M=2, K=2, n_lag=150, n0=0, seed=9)
     assert ties == 0
 
 
