@@ -270,7 +270,7 @@ int Engine::plan_memory() {
         n += 3.0 * C_ * (double)lc * ld_;         // W, Xi, H
         if (!cfg_.checkpoint_path.empty()) n += (double)C_ * mat_;  // cumulative S
         n += 2.0 * mat_ + 3.0 * ld_;              // global snapshot, reduction buffer
-        n += 3.0 * M * C_ * Lw_;                  // per-batch traces
+        n += 3.0 * M * C_ * Lw_ + 0.5 * C_ * Lw_;  // per-batch traces, compacted-row map
         n += 16.0 * C_ * ld_ + 16400.0 * C_;      // chain vectors, POTRF inverse blocks
         return 8.0 * n;
     };
@@ -431,6 +431,8 @@ void Engine::init_chains() {
     if (!cfg_.checkpoint_path.empty()) cS_ = dalloc<double>(A, (size_t)C * mat_);
     const size_t M = cfg_.intervals_per_batch;
     trace_lp_ = dalloc<double>(A, M * C * Lw_);
+    kcount_ = dalloc<int>(A, C);
+    row_of_ = dalloc<int>(A, (size_t)C * Lw_);
     trace_pj_ = dalloc<double>(A, M * C * Lw_ * 2);
     hist_rate_ = dalloc<double>(A, M * C);
     hist_beta_ = dalloc<double>(A, M * C);
@@ -845,6 +847,15 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     sp.trace_lp = p.record ? trace_lp_ + (p.w * C_ + o) * (size_t)Lw_ + r0 : nullptr;
     sp.accept_out = capture_ ? dbg_acc_ + (size_t)o * Lw_ + r0 : nullptr;
     sp.log_ratio_out = capture_ ? dbg_ratio_ + (size_t)o * Lw_ + r0 : nullptr;
+    // post-burn-in rows: window rows t >= first count (proj/src/proposal.cpp:153-155), so the
+    // chunk holds rows [lf, rows) after cb earlier samples
+    const int lf = std::clamp(p.first - r0, 0, rows);
+    const int kc = rows - lf;
+    const uint64_t cb = p.cnt_before + (uint64_t)std::max(0, r0 - p.first);
+    const bool project = p.record && cfg_.trace_eigen_projections;
+    sp.first = lf;
+    sp.kcount = kcount_ + o;
+    sp.row_of = project ? row_of_ + (size_t)o * Lw_ + r0 : nullptr;
     // the previous batch's trace copies read the buffers the MH steps write
     if (merge_pending_ && p.record) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
     timed_begin(s);
@@ -852,36 +863,35 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     timed_end("mh_window", 0.0, s);
     if (capture_) capture_chunk(g, r0, rows);
 
-    // ---- moments of the chunk's post-burn-in states (proposal.cpp:153-155): window rows
-    // t >= first count, so the chunk holds rows [lf, rows) after cb earlier samples
-    const int lf = std::clamp(p.first - r0, 0, rows);
-    const int kc = rows - lf;
-    const uint64_t cb = p.cnt_before + (uint64_t)std::max(0, r0 - p.first);
+    // ---- moments of the chunk's counted states (proposal.cpp:153-155, moments.cpp:5-20): the
+    // MH kernel compacted them into kcount_c distinct states x_j (rows of Xi) and their
+    // weighted copies m_j x_j (rows of H), so S <- (cb S + sum_j m_j x_j x_j^T) / (cb + kc)
+    // is a SYRK over about acceptance x kc rows instead of kc
     // the merge reads S_ / mean_ and clears mean_; the histories' copies read hist_*
     if (merge_pending_) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
     if (kc > 0) {
         const double total = (double)(cb + (uint64_t)kc);
         GemmBatch m{};
-        m.A = (const double* const*)g.Xip;
+        m.A = (const double* const*)(Hp_ + o);
         m.B = (const double* const*)g.Xip;
         m.C = g.Sp;
-        m.a_off = (int64_t)lf * ld_;
-        m.b_off = (int64_t)lf * ld_;
         m.lda = ld_;
         m.ldb = ld_;
         m.ldc = ld_;
         m.M = d_;
         m.N = d_;
         m.K = kc;
+        m.k_vec = kcount_ + o;
         m.alpha = 1.0 / total;
         m.beta = (double)cb / total;
         m.tri_c_lower = 1;
         gemm("syrk_moments", m, C, false, false, s);
-        launch_mean_update(mean_ + o * ld_, ld_, Xi_ + o * win_, win_, ld_, C, d_, lf, kc, (double)cb, s);
+        launch_mean_update(mean_ + o * ld_, ld_, H_ + o * win_, win_, ld_, C, d_, kcount_ + o, kc, (double)cb, s);
     }
-    if (p.record && cfg_.trace_eigen_projections)
+    if (project)
         launch_project_rows(Xi_ + o * win_, win_, ld_, C, rows, lf, d_, proj_,
-                            trace_pj_ + ((p.w * C_ + o) * (size_t)Lw_ + r0) * 2, Lw_, s);
+                            trace_pj_ + ((p.w * C_ + o) * (size_t)Lw_ + r0) * 2, Lw_, row_of_ + (size_t)o * Lw_ + r0,
+                            s);
 }
 
 void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {

@@ -215,6 +215,8 @@ private:
     double *logpi_ = nullptr, *quad_ = nullptr, *beta_ = nullptr, *tr_ = nullptr, *qtmp_ = nullptr;
     uint64_t *nacc_ = nullptr, *uctr_ = nullptr;
     int *status_ = nullptr, *try_ = nullptr, *usable_ = nullptr, *mask_ = nullptr;
+    int* kcount_ = nullptr;  // per chain: distinct counted states of the last window chunk
+    int* row_of_ = nullptr;  // C x n_lag: compacted row of each step's state (trace projections)
     int* h_flags_ = nullptr;  // pinned host mirror: status[C], try[C], ladder mask[C]
     PhiloxKey *nkeys_ = nullptr, *ukeys_ = nullptr, *ikeys_ = nullptr;
     double **Lp_ = nullptr, **Lnp_ = nullptr;  // factor / workspace pointer arrays (swapped on device)

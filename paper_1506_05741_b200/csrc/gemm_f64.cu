@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) gemm_f64_kernel(GemmBat
     if (n0 >= p.N || m0 >= p.M) return;
     if (p.tri_c_lower && n0 > m0 + CF::BM - 1) return;
     extern __shared__ __align__(16) double smem[];
-    int K = p.K;
+    int K = p.k_vec ? p.k_vec[b] : p.K;
     if (p.tri_b_lower) K = min(K, n0 + CF::BN);
     double alpha = p.alpha;
     if (p.alpha_vec) alpha *= p.alpha_vec[b] * p.alpha_vec_mul;

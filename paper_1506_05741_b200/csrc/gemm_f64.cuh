@@ -44,6 +44,8 @@ struct GemmBatch {
     const int* active;         // optional per-batch mask (0 = skip)
     int tri_b_lower;           // B(k,n) == 0 for k > n  (K-loop clipped per n-tile)
     int tri_c_lower;           // compute/store only n <= m
+    const int* k_vec;          // optional per-batch contraction length (<= K); 0 leaves
+                               // C = beta C
 };
 
 // Launch the batched GEMM on `stream`. Layout flags select the template instance.

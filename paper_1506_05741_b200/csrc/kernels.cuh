@@ -42,8 +42,13 @@ struct StepParams {
     int d, n_lag, chains;
     int64_t ld, win_stride;
     const double* W;
-    double* Xi;       // in: increments; out: post-step states (row t <- x after step t)
-    const double* H;  // G * increments
+    double* Xi;       // in: increments; out: the window's DISTINCT counted post-step states,
+                      // compacted: row j = the j-th distinct state from step `first` on
+    double* H;        // G * increments; consumed rows are overwritten with the weighted
+                      // states, row j = m_j * (row j of Xi), m_j = steps spent in state j
+    int first;        // first counted step of this chunk (proj/src/proposal.cpp:153-155)
+    int* kcount;      // [chain]: distinct counted states of the chunk (rows of Xi / H)
+    int* row_of;      // [chain][out_ld], nullable: the Xi row holding the state after step t
     double* x;
     double* g;
     double* y;
@@ -68,10 +73,12 @@ struct StepParams {
 void launch_mh_window(const StepParams& p, bool twisted, cudaStream_t s);
 
 // ---------------------------------------------------------------- moments
-// S_c/mean_c running update with the window's accepted rows [k_off, n_lag):
-// mean <- (n mean + sum_rows x) / (n + k). (The S part is a SYRK through gemm_f64.)
-void launch_mean_update(double* mean, int64_t mean_stride, const double* X, int64_t win_stride,
-                        int64_t ld, int chains, int d, int k_off, int k, double n_prev, cudaStream_t s);
+// Running mean over the chunk's k counted steps: mean <- (n mean + sum_j Xw_j) / (n + k),
+// Xw_j = m_j x_j the weighted distinct states (rows [0, kcount_c) of chain c's window).
+// (The second moment is the weighted SYRK through gemm_f64.)
+void launch_mean_update(double* mean, int64_t mean_stride, const double* Xw, int64_t win_stride,
+                        int64_t ld, int chains, int d, const int* kcount, int k, double n_prev,
+                        cudaStream_t s);
 // Blend (count weights) and covariance, written as a lower matrix with zero upper part
 // into C_out (the refactor workspace); blended mean -> mb. jitter_eps > 0 adds
 // eps*trace_c/d on the diagonal (trace from tr[c]). mask: chains to process.
@@ -148,8 +155,9 @@ void launch_blend_mean(const double* mg, const double* ml, double wg, double wl,
 // out[c][t][0..1] = proj[0..1] . X_c[t], t in [t0, rows)
 // out[c] = G X[c] (G d x d row-major; X, out: one row per chain; stride ld)
 void launch_gemv_rows(const double* G, int64_t ld, int d, const double* X, double* out, int chains, cudaStream_t s);
+// through row_of (the compacted window): out[c][t] = proj . X_c[row_of[c][t]]
 void launch_project_rows(const double* X, int64_t win_stride, int64_t ld, int chains, int rows, int t0,
-                         int d, const double* proj, double* out, int out_ld, cudaStream_t s);
+                         int d, const double* proj, double* out, int out_ld, const int* row_of, cudaStream_t s);
 void launch_copy_vecs(double* dst, const double* src, int64_t n, const int* mask_per_chain,
                       int64_t stride, int chains, cudaStream_t s);
 

@@ -19,19 +19,20 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ------------------------------------------------------------------ moments
-// mean <- keep * mean + add * (sum of rows k_off .. k_off + k - 1 of the chain's window).
+// mean <- keep * mean + add * (sum of the chain's weighted rows 0 .. kcount[c] - 1).
 // A CTA takes 32 columns: its 8 warps sum interleaved rows (coalesced 256-byte row pieces,
 // k/8 independent loads per thread), then the 8 partial sums are added in warp order.
 __global__ void __launch_bounds__(256) mean_update_kernel(double* mean, int64_t mean_stride, const double* X,
-                                                          int64_t win_stride, int64_t ld, int d, int k_off, int k,
+                                                          int64_t win_stride, int64_t ld, int d, const int* kcount,
                                                           double keep, double add) {
     __shared__ double part[8][32];
     const int c = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int i = blockIdx.x * 32 + lane;
+    const int k = kcount[c];
     double s = 0.0;
     if (i < d) {
-        const double* Xc = X + c * win_stride + (int64_t)k_off * ld + i;
+        const double* Xc = X + c * win_stride + i;
         for (int r = warp; r < k; r += 8) s += Xc[(int64_t)r * ld];
     }
     part[warp][lane] = s;
@@ -86,11 +87,20 @@ __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const d
         // the pair (j, j+1) is loaded as one double2 unless j+1 lies past the diagonal: at
         // j = i = d-1 with ld == d it would be past the end of the row (and of the buffer)
         const bool pair = j + 1 <= i;
-        auto ld2 = [&](const double* p) { return pair ? *reinterpret_cast<const double2*>(p) : make_double2(*p, 0.0); };
-        const double2 sg = ld2(Sg + (int64_t)i * ld + j);
-        const double2 sl = ld2(Sl + c * sl_stride + (int64_t)i * ld + j);
-        const double2 g2 = ld2(mg + j);
-        const double2 l2 = ld2(mlc + j);
+        const double* sgp = Sg + (int64_t)i * ld + j;
+        const double* slp = Sl + c * sl_stride + (int64_t)i * ld + j;
+        double2 sg, sl, g2, l2;
+        if (pair) {
+            sg = *reinterpret_cast<const double2*>(sgp);
+            sl = *reinterpret_cast<const double2*>(slp);
+            g2 = *reinterpret_cast<const double2*>(mg + j);
+            l2 = *reinterpret_cast<const double2*>(mlc + j);
+        } else {
+            sg = make_double2(*sgp, 0.0);
+            sl = make_double2(*slp, 0.0);
+            g2 = make_double2(mg[j], 0.0);
+            l2 = make_double2(mlc[j], 0.0);
+        }
         // covariance :90-101 (S exactly symmetric) of the blend :45-46
         double v0 = (wg * sg.x + wl * sl.x) - mbi * (wg * g2.x + wl * l2.x);
         double v1 = (wg * sg.y + wl * sl.y) - mbi * (wg * g2.y + wl * l2.y);
@@ -506,12 +516,12 @@ __global__ void blend_mean_kernel(const double* mg, const double* ml, double wg,
 }
 
 __global__ void project_rows_kernel(const double* X, int64_t win_stride, int64_t ld, int rows, int t0, int d,
-                                    const double* proj, double* out, int out_ld) {
+                                    const double* proj, double* out, int out_ld, const int* row_of) {
     const int c = blockIdx.y;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int t = t0 + warp;
     if (t >= rows) return;
-    const double* xr = X + c * win_stride + (int64_t)t * ld;
+    const double* xr = X + c * win_stride + (int64_t)row_of[(int64_t)c * out_ld + t] * ld;
     double a = 0.0, b = 0.0;
     for (int i = lane; i < d; i += 32) {
         a += proj[i] * xr[i];
@@ -531,12 +541,12 @@ unsigned grid_for(int64_t n, int threads, int cap_per_sm = 8) {
 
 }  // namespace
 
-void launch_mean_update(double* mean, int64_t mean_stride, const double* X, int64_t win_stride, int64_t ld,
-                        int chains, int d, int k_off, int k, double n_prev, cudaStream_t s) {
+void launch_mean_update(double* mean, int64_t mean_stride, const double* Xw, int64_t win_stride, int64_t ld,
+                        int chains, int d, const int* kcount, int k, double n_prev, cudaStream_t s) {
     if (k <= 0) return;
     const double total = n_prev + k;
     dim3 grid((unsigned)ceil_div(d, 32), chains);
-    mean_update_kernel<<<grid, 256, 0, s>>>(mean, mean_stride, X, win_stride, ld, d, k_off, k, n_prev / total,
+    mean_update_kernel<<<grid, 256, 0, s>>>(mean, mean_stride, Xw, win_stride, ld, d, kcount, n_prev / total,
                                             1.0 / total);
     DGB_LAUNCH_CHECK();
     count_launch();
@@ -831,11 +841,11 @@ void launch_blend_mean(const double* mg, const double* ml, double wg, double wl,
 }
 
 void launch_project_rows(const double* X, int64_t win_stride, int64_t ld, int chains, int rows, int t0, int d,
-                         const double* proj, double* out, int out_ld, cudaStream_t s) {
+                         const double* proj, double* out, int out_ld, const int* row_of, cudaStream_t s) {
     if (t0 >= rows) return;
     const int warps = rows - t0;
     dim3 grid((unsigned)ceil_div((int64_t)warps * 32, 256), chains);
-    project_rows_kernel<<<grid, 256, 0, s>>>(X, win_stride, ld, rows, t0, d, proj, out, out_ld);
+    project_rows_kernel<<<grid, 256, 0, s>>>(X, win_stride, ld, rows, t0, d, proj, out, out_ld, row_of);
     DGB_LAUNCH_CHECK();
     count_launch();
 }

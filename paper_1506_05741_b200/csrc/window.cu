@@ -64,6 +64,33 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 
+// scale * v (this thread's pairs of a state vector) -> one window row
+template <int R, int T>
+__device__ __forceinline__ void store_row(double* row, const double2 (&v)[R], const bool (&valid)[R], int tid, int d,
+                                          double scale) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = 2 * (tid + r * T);
+        if (!valid[r]) continue;
+        const double2 w = make_double2(scale * v[r].x, scale * v[r].y);
+        if (e + 1 < d) st2(row + e, w);
+        else row[e] = w.x;
+    }
+}
+
+// Window compaction of the counted post-step states (steps t >= first; the reference
+// accumulates x after every such step, proj/src/proposal.cpp:153-155): a rejected step
+// repeats the previous state, so the window holds only about acceptance x n_lag DISTINCT
+// states. Row j of Xi gets the j-th distinct state x_j, row j of H the weighted m_j x_j
+// (m_j = the number of counted steps spent in it), and the moment SYRK and mean run over
+// those rows: S += sum_j m_j x_j x_j^T -- the same sum, in fewer, exact-integer-weighted
+// terms. Both rows are written only once consumed (j <= t), so the TMA ring and the
+// register prefetch of the rows ahead are never overwritten.
+struct Compactor {
+    int j = -1;         // current distinct row
+    double mult = 0.0;  // counted steps spent in it so far
+};
+
 // R = double2 pairs per thread; PREF = prefetch the next step's rows into registers
 template <int R, bool TWISTED, bool PREF>
 __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p) {
@@ -81,7 +108,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
 
     const double* Wc = p.W + c * p.win_stride;
     double* Xc = p.Xi + c * p.win_stride;
-    const double* Hc = p.H + c * p.win_stride;
+    double* Hc = p.H + c * p.win_stride;
+    Compactor cp;
 
     double2 x[R], g[R], y[R], xr[R], gr[R], ie[R], bc[R];
     bool valid[R];
@@ -171,6 +199,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
         const double qc = pcn ? hq * tb : 0.0;
         const double ratio = pcn ? (lpc + qc) - (lp + q) : lpc - lp;  // proj/src/proposal.cpp:77-82
         const bool acc = logu < ratio;                               // strict, :146
+        // counted post-step state -> the compacted window (Compactor)
+        const bool counted = t >= p.first;
+        const bool fresh = counted && (acc || t == p.first);
+        if (fresh) {
+            if (cp.j >= 0) store_row<R, kStepThreads>(Hc + (int64_t)cp.j * ld, x, valid, tid, d, cp.mult);
+            ++cp.j;
+            cp.mult = 0.0;
+        }
         if (acc) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -182,19 +218,13 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
             q = qc;
             ++nacc;
         }
-        // post-step state -> row t of the window (SYRK / trace input); xi row t is consumed
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int e = 2 * (tid + r * kStepThreads);
-            if (valid[r]) {
-                if (e + 1 < d) st2(Xc + (int64_t)t * ld + e, x[r]);
-                else Xc[(int64_t)t * ld + e] = x[r].x;
-            }
-        }
+        if (fresh) store_row<R, kStepThreads>(Xc + (int64_t)cp.j * ld, x, valid, tid, d, 1.0);
+        if (counted) cp.mult += 1.0;
         if (tid == 0) {
             if (p.trace_lp) p.trace_lp[(int64_t)c * p.out_ld + t] = lp;
             if (p.accept_out) p.accept_out[(int64_t)c * p.out_ld + t] = acc ? 1 : 0;
             if (p.log_ratio_out) p.log_ratio_out[(int64_t)c * p.out_ld + t] = ratio;
+            if (p.row_of && counted) p.row_of[(int64_t)c * p.out_ld + t] = cp.j;
         }
         if (PREF) {
 #pragma unroll
@@ -207,6 +237,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
             load_row(t + 1, xi, w, h);
         }
     }
+    if (cp.j >= 0) store_row<R, kStepThreads>(Hc + (int64_t)cp.j * ld, x, valid, tid, d, cp.mult);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = 2 * (tid + r * kStepThreads);
@@ -226,6 +257,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
         if (pcn) p.quad[c] = q;
         p.n_accepted[c] = nacc;
         p.uctr[c] = u0 + (uint64_t)p.n_lag;
+        p.kcount[c] = cp.j + 1;
     }
 }
 
@@ -280,7 +312,8 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     const double hq = 0.5 / (p.infl * p.infl);
     const double* Wc = p.W + c * p.win_stride;
     double* Xc = p.Xi + c * p.win_stride;
-    const double* Hc = p.H + c * p.win_stride;
+    double* Hc = p.H + c * p.win_stride;
+    Compactor cp;
 
     auto issue = [&](int t) {  // producer: row t of the window into stage t % NS
         const int s = t % NS;
@@ -379,6 +412,14 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
         const double qc = pcn ? hq * tb : 0.0;
         const double ratio = pcn ? (lpc + qc) - (lp + q) : lpc - lp;  // proj/src/proposal.cpp:77-82
         const bool acc = logu < ratio;                               // strict, :146
+        // counted post-step state -> the compacted window (Compactor)
+        const bool counted = t >= p.first;
+        const bool fresh = counted && (acc || t == p.first);
+        if (fresh) {
+            if (cp.j >= 0) store_row<R, T>(Hc + (int64_t)cp.j * ld, x, valid, tid, d, cp.mult);
+            ++cp.j;
+            cp.mult = 0.0;
+        }
         if (acc) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -390,20 +431,16 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
             q = qc;
             ++nacc;
         }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int e = 2 * (tid + r * T);
-            if (valid[r]) {
-                if (e + 1 < d) st2(Xc + (int64_t)t * ld + e, x[r]);
-                else Xc[(int64_t)t * ld + e] = x[r].x;
-            }
-        }
+        if (fresh) store_row<R, T>(Xc + (int64_t)cp.j * ld, x, valid, tid, d, 1.0);
+        if (counted) cp.mult += 1.0;
         if (tid == 0) {
             if (p.trace_lp) p.trace_lp[(int64_t)c * p.out_ld + t] = lp;
             if (p.accept_out) p.accept_out[(int64_t)c * p.out_ld + t] = acc ? 1 : 0;
             if (p.log_ratio_out) p.log_ratio_out[(int64_t)c * p.out_ld + t] = ratio;
+            if (p.row_of && counted) p.row_of[(int64_t)c * p.out_ld + t] = cp.j;
         }
     }
+    if (cp.j >= 0) store_row<R, T>(Hc + (int64_t)cp.j * ld, x, valid, tid, d, cp.mult);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = 2 * (tid + r * T);
@@ -423,6 +460,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
         if (pcn) p.quad[c] = q;
         p.n_accepted[c] = nacc;
         p.uctr[c] = u0 + (uint64_t)p.n_lag;
+        p.kcount[c] = cp.j + 1;
     }
 }
 

@@ -62,7 +62,12 @@ class OrRunOut(C.Structure):
                 ("accumulated_samples", C.c_uint64), ("stop_reason", C.c_int),
                 ("global_mean", _dp), ("global_cov", _dp), ("cov_error_hist", _dp),
                 ("mean_error_hist", _dp), ("psrf_hist", _dp), ("beta_hist", _dp), ("acc_hist", _dp),
-                ("accept_bits", _dp), ("log_ratio", _dp), ("log_u", _dp), ("final_x", _dp)]
+                ("accept_bits", _dp), ("log_ratio", _dp), ("log_u", _dp), ("final_x", _dp),
+                ("traces", _dp), ("trace_cap", C.c_size_t), ("trace_len", C.c_size_t)]
+
+
+class OrRunOpts(C.Structure):
+    _fields_ = [("threads", C.c_int), ("chain_ids", C.POINTER(C.c_size_t)), ("n_ids", C.c_size_t)]
 
 
 KIND = {"rw": 0, "pcn": 1, "am": 2, "diam": 3}
@@ -228,30 +233,47 @@ def kernel_cfg(kind: str, dim: int, **over) -> OrKernelCfg:
 
 def run(target: TargetData, kind: str = "diam", chains: int = 1, M: int = 1, K: int = 1,
         seed: int = 1, inject_w=None, record_decisions: bool = False, cov_tol=-1.0,
-        mean_tol=-1.0, psrf_tol=-1.0, max_samples=-1, dispersion=1.0, **kover):
+        mean_tol=-1.0, psrf_tol=-1.0, max_samples=-1, dispersion=1.0, threads: int = 1,
+        chain_ids=None, traces: bool = False, trace_thin: int = 1, **kover):
+    """or_run_ex: the whole run (proj/src/runner.cpp:216-279) on `threads` host threads.
+    chain_ids: replay only those global chains (per-chain outputs of the first batch;
+    inject_w then lists their windows in the same order). traces: record log pi and the
+    two eigen projections (runner.cpp:363-379)."""
     d = target.dim
     cfg = OrRunCfg()
     cfg.kernel = kernel_cfg(kind, d, **kover)
     cfg.chains, cfg.intervals_per_batch, cfg.max_batches = chains, M, K
     cfg.cov_tol, cfg.mean_tol, cfg.psrf_tol, cfg.max_samples = cov_tol, mean_tol, psrf_tol, max_samples
     cfg.init_dispersion, cfg.master_seed = dispersion, seed
-    cfg.record_traces, cfg.trace_thin, cfg.trace_eigen_projections = 0, 1, 0
+    cfg.record_traces, cfg.trace_thin, cfg.trace_eigen_projections = int(traces), trace_thin, int(traces)
     nl = cfg.kernel.n_lag
+    nrun = len(chain_ids) if chain_ids is not None else chains
     res = dict(global_mean=np.zeros(d), global_cov=np.zeros((d, d)), cov_error_hist=np.zeros(K),
-               mean_error_hist=np.zeros(K), psrf_hist=np.zeros(K), beta_hist=np.zeros((chains, K * M)),
-               acc_hist=np.zeros((chains, K * M)), final_x=np.zeros((chains, d)))
+               mean_error_hist=np.zeros(K), psrf_hist=np.zeros(K), beta_hist=np.zeros((nrun, K * M)),
+               acc_hist=np.zeros((nrun, K * M)), final_x=np.zeros((nrun, d)))
     if record_decisions:
         for key in ("accept_bits", "log_ratio", "log_u"):
-            res[key] = np.zeros((chains, K * M * nl))
+            res[key] = np.zeros((nrun, K * M * nl))
+    cap = K * M * nl
+    if traces:
+        res["traces"] = np.zeros((nrun, 3, cap))
     out = OrRunOut()
     for key, a in res.items():
         setattr(out, key, dptr(a))
+    out.trace_cap = cap if traces else 0
     tgt = target.or_target()
     w_arr = None
     if inject_w is not None:
         w_list = [np.ascontiguousarray(w, dtype=np.float64) for w in inject_w]
-        w_arr = (_dp * chains)(*[dptr(w) for w in w_list])
-    st = oracle().or_run(C.byref(cfg), C.byref(tgt), w_arr, C.byref(out))
+        w_arr = (_dp * nrun)(*[dptr(w) for w in w_list])
+    opts = OrRunOpts()
+    opts.threads = threads
+    ids = None
+    if chain_ids is not None:
+        ids = (C.c_size_t * nrun)(*chain_ids)
+        opts.chain_ids = ids
+        opts.n_ids = nrun
+    st = oracle().or_run_ex(C.byref(cfg), C.byref(tgt), w_arr, C.byref(out), C.byref(opts))
     if st != 0:
         raise RuntimeError(f"oracle run failed {st}: {oracle().or_last_error().decode()}")
     n = out.batches
@@ -261,4 +283,6 @@ def run(target: TargetData, kind: str = "diam", chains: int = 1, M: int = 1, K: 
         res[key] = res[key][:n]
     res["beta_hist"] = res["beta_hist"][:, : n * M]
     res["acc_hist"] = res["acc_hist"][:, : n * M]
+    if traces:
+        res["traces"] = res["traces"][:, :, : out.trace_len]
     return res
