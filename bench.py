@@ -331,6 +331,11 @@ def impl_b200(args):
     peak = C.c_double()
     lib.check(lib.lib.diamx_fp64_peak(C.byref(peak)))
     achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
+    # the SYRK runs over each window's distinct states only (rejected steps repeat a state):
+    # the step's algorithmic flops count the rows the profiled batch actually had
+    syrk_full = prof_chains * M * n_lag * d * (d + 1.0)
+    distinct = st["syrk_moments"][1] / syrk_full if syrk_full else 1.0
+    alg_flops -= (1.0 - distinct) * syrk_full * chains / prof_chains / world
     del eng
 
     # ---- end-to-end through the C ABI (host target, result back to host)
@@ -389,6 +394,7 @@ def impl_b200(args):
                          "peak_source": "diamx_fp64_peak: DMMA m8n8k4 loop measured live (MEASURED_PEAKS.json "
                                         "has no FP64 entry)",
                          "step_alg_tflops": alg_flops / (ms / args.steps / 1e3) / 1e12,
+                         "syrk_distinct_row_fraction": distinct,
                          "profile_chains": prof_chains,
                          "per_class_ms": {c: round(v[0], 4) for c, v in st.items()}},
             "cpu_baseline": cpu,

@@ -171,7 +171,15 @@ void Engine::save_checkpoint(double wall) {
         w.pod<uint64_t>(d_);
         for (int i = 0; i < d_; ++i)
             for (int j = 0; j < d_; ++j) w.pod<double>(j <= i ? L[(size_t)i * ld_ + j] : 0.0);
-        w.pod<uint32_t>(0);  // no explicit inverse kept
+        if (Xinv_) {  // factor_inv (runner.cpp:444-445)
+            const auto X = fetch_d(Xinv_ + (size_t)c * mat_, (size_t)d_ * ld_);
+            w.pod<uint32_t>(1);
+            w.pod<uint64_t>(d_);
+            for (int i = 0; i < d_; ++i)
+                for (int j = 0; j < d_; ++j) w.pod<double>(j <= i ? X[(size_t)i * ld_ + j] : 0.0);
+        } else {
+            w.pod<uint32_t>(0);
+        }
         w.vec(k_.adaptive_ref ? Vec(xr.begin() + (size_t)c * ld_, xr.begin() + (size_t)c * ld_ + d_) : Vec(d_, 0.0));
         w.pod<uint64_t>(nctr);
         w.pod<uint64_t>(uc[c]);
@@ -262,7 +270,7 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
     uint64_t nctr = 0, n = 0, cnt_local = 0, cum = 0;
     std::vector<double*> lptr(C);
     DGB_CUDA(cudaMemcpy(lptr.data(), Lp_, C * sizeof(double*), cudaMemcpyDeviceToHost));
-    bool all_identity = true;
+    bool all_identity = true, need_inverse = false;
     for (int c = 0; c < C; ++c) {
         std::vector<double> row(ld_, 0.0);
         const Vec x = r.vec();
@@ -287,10 +295,13 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
                     break;
                 }
         put_lower(lptr[c], L);
-        if (r.pod<uint32_t>() != 0) {  // explicit inverse: not needed by this engine
-            r.pod<uint64_t>();
-            std::vector<double> skip((size_t)d_ * d_);
-            r.raw(skip.data(), skip.size() * 8);
+        if (r.pod<uint32_t>() != 0) {  // factor_inv (runner.cpp:186)
+            require(r.pod<uint64_t>() == (uint64_t)d_, Err::Io, "corrupt checkpoint: inverse factor");
+            Mat X(d_, d_);
+            r.raw(X.a.data(), X.a.size() * 8);
+            if (Xinv_) put_lower(Xinv_ + (size_t)c * mat_, X);
+        } else if (Xinv_) {  // a file without the inverse: recomputed below from the factor
+            need_inverse = true;
         }
         const Vec xr = r.vec();
         std::fill(row.begin(), row.end(), 0.0);
@@ -336,7 +347,8 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
     cum_cnt_ = cum;
     identity_ = all_identity;
 
-    // derived device state: G x, G x_ref and y = L^-1 (x - x_ref)
+    // derived device state: G x, G x_ref, X = L^-1 (a file without it) and y = L^-1 (x - x_ref)
+    if (need_inverse) trtri_batched(Lp_, Xinvp_, Tinvp_, ld_, d_, C, nullptr, stream_);
     refresh_g(x_, g_, C, stream_);
     if (k_.adaptive_ref) refresh_g(xr_, gr_, C, stream_);
     DGB_CUDA(cudaStreamSynchronize(stream_));

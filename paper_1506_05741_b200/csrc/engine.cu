@@ -178,6 +178,12 @@ void upload_padded(double* dst, int64_t ld, const Mat& m) {
 Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shared_ptr<Comm> comm)
     : tgtp_(std::move(t)), tgt_(*tgtp_), cfg_(cfg), k_(cfg.kernel), comm_(std::move(comm)) {
     validate_run_cfg(cfg_, tgt_);
+    if (const char* e = std::getenv("DIAM_B200_SKIP")) {
+        const std::string v = e;
+        const char* names[] = {"normals", "trmm", "target", "mh", "syrk", "potrf"};
+        for (int i = 0; i < 6; ++i)
+            if (v.find(names[i]) != std::string::npos) skip_ |= 1u << i;
+    }
     if (comm_) {
         rank_ = comm_->rank();
         world_ = comm_->size();
@@ -269,6 +275,7 @@ int Engine::plan_memory() {
         n += (double)C_ * mat_;                   // local moments S
         n += 3.0 * C_ * (double)lc * ld_;         // W, Xi, H
         if (!cfg_.checkpoint_path.empty()) n += (double)C_ * mat_;  // cumulative S
+        if (k_.use_explicit_inverse) n += (double)C_ * (mat_ + (double)((d_ + 1) / 2) * ld_);  // X, TRTRI scratch
         n += 2.0 * mat_ + 3.0 * ld_;              // global snapshot, reduction buffer
         n += 3.0 * M * C_ * Lw_ + 0.5 * C_ * Lw_;  // per-batch traces, compacted-row map
         n += 16.0 * C_ * ld_ + 16400.0 * C_;      // chain vectors, POTRF inverse blocks
@@ -429,6 +436,10 @@ void Engine::init_chains() {
     Ssum_ = dalloc<double>(A, (size_t)d_ * (d_ + 1) / 2 + ld_);  // packed lower sum + mean sum
     cov_part_ = dalloc<double>(A, 2 * (size_t)d_);
     if (!cfg_.checkpoint_path.empty()) cS_ = dalloc<double>(A, (size_t)C * mat_);
+    if (k_.use_explicit_inverse) {
+        Xinv_ = dalloc<double>(A, (size_t)C * mat_);
+        Tinv_ = dalloc<double>(A, (size_t)C * ((d_ + 1) / 2) * ld_);
+    }
     const size_t M = cfg_.intervals_per_batch;
     trace_lp_ = dalloc<double>(A, M * C * Lw_);
     kcount_ = dalloc<int>(A, C);
@@ -444,6 +455,10 @@ void Engine::init_chains() {
     Hp_ = ptr_array(A, H_, win_, C);
     Gpc_ = ptr_array(A, G_, 0, C);  // G once per chain (batched GEMMs)
     Sp_ = ptr_array(A, S_, mat_, C);
+    if (Xinv_) {
+        Xinvp_ = ptr_array(A, Xinv_, mat_, C);
+        Tinvp_ = ptr_array(A, Tinv_, ((d_ + 1) / 2) * ld_, C);
+    }
 
     // RNG keys: global chain index p = c0 + i (runner.cpp:128-130, 556-559)
     std::vector<PhiloxKey> nk(C), uk(C), ik(C);
@@ -465,6 +480,7 @@ void Engine::init_chains() {
     launch_normal_vec(x_, ld_, C, d_, ikeys_, 0, cfg_.init_dispersion, stream_);
     // factor = I, beta = beta_init (proposal.cpp:95-97)
     launch_set_identity(L_, fmat_, C, d_, ld_, stream_);
+    if (Xinv_) launch_set_identity(Xinv_, mat_, C, d_, ld_, stream_);  // I^{-1} (proposal.cpp:98)
     std::vector<double> b(C, k_.beta_init);
     DGB_CUDA(cudaMemcpyAsync(beta_, b.data(), C * 8, cudaMemcpyHostToDevice, stream_));
     identity_ = true;
@@ -473,7 +489,8 @@ void Engine::init_chains() {
     launch_eval_logpi(x_, g_, inv_eig_, bcoef_, twisted_, logpi_, C, d_, ld_, stream_);
     if (k_.pcn_form()) {
         const double infl = k_.noise_infl();
-        launch_trsv(Lp_, ld_, x_, nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl), nullptr, stream_);
+        if (Xinv_) launch_trmv_quad(Xinvp_, ld_, x_, nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl), stream_);
+        else launch_trsv(Lp_, ld_, x_, nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl), nullptr, stream_);
     }
     DGB_CUDA(cudaStreamSynchronize(stream_));
 
@@ -533,10 +550,12 @@ void Engine::refresh_g(const double* x, double* out, int chains, cudaStream_t s)
     timed_end("gemv_state", 2.0 * chains * (double)d_ * d_, s);
 }
 
-void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s) {
-    double flops = 2.0 * g.M * (double)g.N * g.K * batch;
-    if (g.tri_c_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
-    if (g.tri_b_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
+void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s, double flops) {
+    if (flops < 0.0) {
+        flops = 2.0 * g.M * (double)g.N * g.K * batch;
+        if (g.tri_c_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
+        if (g.tri_b_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
+    }
     nvtxRangePushA(name);  // `ncu --nvtx --nvtx-include "<name>/"` selects one GEMM class
     timed_begin(s);
     gemm_f64(g, batch, ak, bk, s);
@@ -773,7 +792,8 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     // ---- noise: W from Philox, Xi = s W L^T, H = Xi G^T (proposal.cpp:254-266); row r of
     // the window draws counters nctr + r d .. nctr + (r + 1) d - 1 of the chain's stream
     timed_begin(s);
-    launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, rows, d_, ld_, nkeys_ + o,
+    if (!(skip_ & kSkipNormals))
+        launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, rows, d_, ld_, nkeys_ + o,
                    p.nctr + (uint64_t)r0 * d_, beta_ + o, infl, s);
     timed_end("normals", 0.0, s);
     if (!p.identity) {
@@ -792,9 +812,9 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         t.alpha_vec_mul = infl;
         t.beta = 0.0;
         t.tri_b_lower = 1;
-        gemm("trmm_noise", t, C, true, true, s);
+        if (!(skip_ & kSkipTrmm)) gemm("trmm_noise", t, C, true, true, s);
     }
-    {
+    if (!(skip_ & kSkipTarget)) {
         GemmBatch h{};
         h.B = (const double* const*)Gp_;
         h.lda = ld_;
@@ -859,7 +879,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     // the previous batch's trace copies read the buffers the MH steps write
     if (merge_pending_ && p.record) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
     timed_begin(s);
-    launch_mh_window(sp, twisted_, s);
+    if (!(skip_ & kSkipMh)) launch_mh_window(sp, twisted_, s);
     timed_end("mh_window", 0.0, s);
     if (capture_) capture_chunk(g, r0, rows);
 
@@ -869,7 +889,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     // is a SYRK over about acceptance x kc rows instead of kc
     // the merge reads S_ / mean_ and clears mean_; the histories' copies read hist_*
     if (merge_pending_) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
-    if (kc > 0) {
+    if (kc > 0 && !(skip_ & kSkipSyrk)) {
         const double total = (double)(cb + (uint64_t)kc);
         GemmBatch m{};
         m.A = (const double* const*)(Hp_ + o);
@@ -885,7 +905,17 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         m.alpha = 1.0 / total;
         m.beta = (double)cb / total;
         m.tri_c_lower = 1;
-        gemm("syrk_moments", m, C, false, false, s);
+        double fl = -1.0;
+        if (profiling_) {
+            // the SYRK runs over each chain's distinct states only (kcount_, written by the
+            // MH kernel): count those rows, d (d+1) flops each
+            std::vector<int> kc_h(C);
+            DGB_CUDA(cudaStreamSynchronize(s));
+            DGB_CUDA(cudaMemcpy(kc_h.data(), kcount_ + o, C * sizeof(int), cudaMemcpyDeviceToHost));
+            fl = 0.0;
+            for (int v : kc_h) fl += (double)v * d_ * (d_ + 1.0);
+        }
+        gemm("syrk_moments", m, C, false, false, s, fl);
         launch_mean_update(mean_ + o * ld_, ld_, H_ + o * win_, win_, ld_, C, d_, kcount_ + o, kc, (double)cb, s);
     }
     if (project)
@@ -917,7 +947,7 @@ void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {
         DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
         nvtxRangePushA("potrf");
         timed_begin(s);
-        potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+        if (!(skip_ & kSkipPotrf)) potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
         timed_end("potrf", (double)C * d_ * (double)d_ * d_ / 3.0, s);
         nvtxRangePop();
         DGB_CUDA(cudaMemcpyAsync(h_flags_ + o, status_ + o, C * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1016,8 +1046,10 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
             DGB_CUDA(cudaEventRecord(g.pool_ev, s));
             pool_last_ = g.pool_ev;
         }
+        // explicit inverse: X = L^{-1} of every adopted factor (proposal.cpp:202)
+        if (Xinv_) trtri_batched(g.Lp, Xinvp_ + o, Tinvp_ + o, ld_, d_, C, usable_ + o, s);
         // adopted factors come with y = L^-1 (x - x_ref) and the quad term for free
-        if (aug && !k_.adaptive_ref)
+        else if (aug && !k_.adaptive_ref)
             launch_aug_adopt(g.Lp, ld_, d_, C, usable_ + o, qtmp_ + o, y_ + o * ld_, quad_ + o, s);
     }
     // adaptive reference point (proposal.cpp:206-208)
@@ -1030,7 +1062,12 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
     // With a fixed reference point y = L^-1 (x - x_ref) is carried exactly through the
     // steps (c y + s w) and re-anchored from the augmented POTRF row whenever the factor
     // changes, so only a moving reference point needs a fresh triangular solve.
-    if (k_.pcn_form() && k_.adaptive_ref) {
+    if (k_.pcn_form() && Xinv_) {
+        // the reference's quad_term through factor_inv (tri_matvec, proposal.cpp:55) at every
+        // boundary, whether or not the factor changed
+        launch_trmv_quad(Xinvp_ + o, ld_, x_ + o * ld_, k_.adaptive_ref ? xr_ + o * ld_ : nullptr, ld_, y_ + o * ld_,
+                         quad_ + o, C, d_, 0.5 / (infl * infl), s);
+    } else if (k_.pcn_form() && k_.adaptive_ref) {
         timed_begin(s);
         launch_trsv(g.Lp, ld_, x_ + o * ld_, xr_ + o * ld_, ld_, y_ + o * ld_, quad_ + o, C, d_, 0.5 / (infl * infl),
                     nullptr, s);

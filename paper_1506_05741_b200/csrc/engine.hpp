@@ -163,7 +163,9 @@ private:
                            const double* beta, const double* lp, const double* pj);
     std::vector<uint64_t> out_n_start_;  // window start counts of the batch in h_out_
     void save_checkpoint(double wall);
-    void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s);
+    // flops < 0: the algorithmic count from the shape (triangular halves included)
+    void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s,
+              double flops = -1.0);
     void refresh_g(const double* x, double* out, int chains, cudaStream_t s);
     void timed_begin(cudaStream_t s);
     void timed_end(const char* name, double flops, cudaStream_t s);
@@ -231,6 +233,11 @@ private:
     cudaEvent_t out_ev_ = nullptr;  // the copies into h_out_ / h_stats_ are done
     double* gather_ = nullptr;                                // PSRF all-gather buffer
     double* cS_ = nullptr;  // cumulative raw second moments (lower), kept only for checkpoints
+    // use_explicit_inverse: X = L^{-1} per chain (upper part zero) and the TRTRI scratch
+    double* Xinv_ = nullptr;
+    double* Tinv_ = nullptr;
+    double** Xinvp_ = nullptr;
+    double** Tinvp_ = nullptr;
     double wall_accum_ = 0.0;  // wall seconds of earlier (checkpointed) segments of the run
 
     // host-side counters (uniform across chains)
@@ -263,6 +270,11 @@ private:
     std::map<cudaStream_t, cudaEvent_t> open_;
 
     bool capture_ = false;
+    // timing experiments only (DIAM_B200_SKIP=normals,trmm,target,mh,syrk,potrf): the named
+    // kernel classes are not launched, so a batch's time without them can be measured;
+    // results are meaningless with any bit set
+    unsigned skip_ = 0;
+    enum : unsigned { kSkipNormals = 1, kSkipTrmm = 2, kSkipTarget = 4, kSkipMh = 8, kSkipSyrk = 16, kSkipPotrf = 32 };
     std::vector<std::vector<double>> cap_w_, cap_ratio_;
     std::vector<std::vector<uint8_t>> cap_acc_;
     std::vector<double> cap_wbuf_;  // C x n_lag x d: the current window's W, filled chunk by chunk

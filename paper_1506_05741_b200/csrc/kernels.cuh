@@ -115,6 +115,12 @@ void launch_cov_error(const double* Sg, const double* mg, const double* Ctrue, i
 // ---------------------------------------------------------------- triangular
 // y_c = L_c^{-1} (x_c - xr_c); quad_c = half_inv_infl2 * sum y^2 (pcn) and, if
 // qmax >= 0, usable_c &= (0.5*y.y/infl^2 <= qmax). mask: chains to process.
+// explicit inverse (use_explicit_inverse): X = L^{-1} for the masked chains (T: r2 x d/2
+// scratch per chain), and y = X (x - xr), quad = hq |y|^2
+void trtri_batched(double* const* L, double* const* X, double* const* T, int64_t ld, int d, int chains,
+                   const int* mask, cudaStream_t s);
+void launch_trmv_quad(double* const* X, int64_t ld, const double* x, const double* xr, int64_t vstride, double* y,
+                      double* quad_out, int chains, int d, double half_inv_infl2, cudaStream_t s);
 void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr, int64_t vstride,
                  double* y, double* quad_out, int chains, int d, double half_inv_infl2,
                  const int* mask, cudaStream_t s);

@@ -703,6 +703,127 @@ void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr
     count_launch();
 }
 
+// ------------------------------------------------------------------ explicit inverse
+// use_explicit_inverse (proj/src/proposal.cpp:98, 202, 241-252): X = L^{-1} kept beside the
+// factor, and the quadratic term taken as |X (x - x_ref)|^2 (proposal.cpp:51-61) instead of a
+// triangular solve. The reference inverts by d column solves; here by recursive doubling of
+// 64x64 diagonal inverses, [L11 0; L21 L22]^{-1} = [X11 0; -X22 L21 X11  X22], the two
+// products of every level on the DMMA GEMM.
+constexpr int kInvB = 64;
+
+// one CTA per (64-block, chain): thread j solves column j of the block by forward substitution
+__global__ void __launch_bounds__(kInvB) trtri_diag_kernel(double* const* Lm, double* const* Xm, int64_t ld, int d,
+                                                           const int* mask) {
+    const int c = blockIdx.y;
+    if (mask && !mask[c]) return;
+    const int b0 = blockIdx.x * kInvB, n = min(kInvB, d - b0);
+    extern __shared__ double inv_smem[];
+    auto sl = reinterpret_cast<double(*)[kInvB + 1]>(inv_smem);
+    auto sx = reinterpret_cast<double(*)[kInvB + 1]>(inv_smem + kInvB * (kInvB + 1));
+    const double* L = Lm[c] + (int64_t)b0 * ld + b0;
+    for (int e = threadIdx.x; e < kInvB * kInvB; e += kInvB) {
+        const int r = e / kInvB, q = e % kInvB;
+        sl[r][q] = (r < n && q <= r) ? L[(int64_t)r * ld + q] : 0.0;
+    }
+    __syncthreads();
+    const int j = threadIdx.x;
+    for (int i = 0; i < n; ++i) {
+        if (i >= j) {
+            double s = i == j ? 1.0 : 0.0;
+            for (int k = j; k < i; ++k) s -= sl[i][k] * sx[k][j];
+            sx[i][j] = s / sl[i][i];
+        }
+    }
+    __syncthreads();
+    double* X = Xm[c] + (int64_t)b0 * ld + b0;
+    for (int e = threadIdx.x; e < n * kInvB; e += kInvB) {
+        const int r = e / kInvB, q = e % kInvB;
+        if (q < n) X[(int64_t)r * ld + q] = q <= r ? sx[r][q] : 0.0;
+    }
+}
+
+// y = X (x - xr) (lower-triangular X), quad = hq |y|^2: one CTA per chain, a warp per row
+__global__ void __launch_bounds__(256) trmv_quad_kernel(double* const* Xm, int64_t ld, const double* x,
+                                                        const double* xr, int64_t vstride, double* y,
+                                                        double* quad_out, int d, double hq) {
+    const int c = blockIdx.x;
+    extern __shared__ double rs[];
+    const double* X = Xm[c];
+    const double* xc = x + c * vstride;
+    const double* xrc = xr ? xr + c * vstride : nullptr;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < d; i += blockDim.x) rs[i] = xc[i] - (xrc ? xrc[i] : 0.0);
+    __syncthreads();
+    double q = 0.0;
+    for (int i = warp; i < d; i += 8) {
+        const double* Xr = X + (int64_t)i * ld;
+        double s = 0.0;
+        for (int j = lane; j <= i; j += 32) s += Xr[j] * rs[j];
+        s = warp_sum(s);
+        if (lane == 0) {
+            y[c * vstride + i] = s;
+            q += s * s;
+        }
+    }
+    __shared__ double red[8];
+    if (lane == 0) red[warp] = q;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        quad_out[c] = hq * t;
+    }
+}
+
+void trtri_batched(double* const* L, double* const* X, double* const* T, int64_t ld, int d, int chains,
+                   const int* mask, cudaStream_t s) {
+    const int smem = 2 * kInvB * (kInvB + 1) * (int)sizeof(double);
+    set_smem_attr(reinterpret_cast<const void*>(trtri_diag_kernel), smem);
+    trtri_diag_kernel<<<dim3((unsigned)ceil_div(d, kInvB), (unsigned)chains), kInvB, smem, s>>>(L, X, ld, d, mask);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+    for (int h = kInvB; h < d; h *= 2) {
+        for (int b0 = 0; b0 + h < d; b0 += 2 * h) {
+            const int r2 = std::min(h, d - b0 - h);
+            GemmBatch t{};  // T = L21 X11 (r2 x h)
+            t.A = (const double* const*)L;
+            t.B = (const double* const*)X;
+            t.C = T;
+            t.a_off = (int64_t)(b0 + h) * ld + b0;
+            t.b_off = (int64_t)b0 * ld + b0;
+            t.lda = t.ldb = t.ldc = ld;
+            t.M = r2;
+            t.N = h;
+            t.K = h;
+            t.alpha = 1.0;
+            t.active = mask;
+            gemm_f64(t, chains, true, false, s);
+            GemmBatch x{};  // X21 = -X22 T
+            x.A = (const double* const*)X;
+            x.B = (const double* const*)T;
+            x.C = X;
+            x.a_off = (int64_t)(b0 + h) * ld + b0 + h;
+            x.c_off = (int64_t)(b0 + h) * ld + b0;
+            x.lda = x.ldb = x.ldc = ld;
+            x.M = r2;
+            x.N = h;
+            x.K = r2;
+            x.alpha = -1.0;
+            x.active = mask;
+            gemm_f64(x, chains, true, false, s);
+        }
+    }
+}
+
+void launch_trmv_quad(double* const* X, int64_t ld, const double* x, const double* xr, int64_t vstride, double* y,
+                      double* quad_out, int chains, int d, double half_inv_infl2, cudaStream_t s) {
+    const size_t smem = sizeof(double) * (size_t)d;
+    if (smem > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(trmv_quad_kernel), (int)smem);
+    trmv_quad_kernel<<<chains, 256, smem, s>>>(X, ld, x, xr, vstride, y, quad_out, d, half_inv_infl2);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
 void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status, PotrfWork& w,
                    cudaStream_t s, int extra_rows) {
     // Left-looking blocked Cholesky over 128-wide block columns J = [j0, j0+128):

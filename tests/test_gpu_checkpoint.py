@@ -62,3 +62,19 @@ def test_reference_resumes_b200_checkpoint_and_vice_versa(b200, ref_abi, tmp_pat
         assert np.array_equal(r_b.chain_history(p, "beta")[:4], r_ref2.chain_history(p, "beta"))
     # and the continuation is statistically the same process
     assert np.isfinite(r_b.final_cov_error) and r_b.final_cov_error < 10 * r_ref.final_cov_error + 1.0
+
+
+def test_explicit_inverse_checkpoint(b200, ref_abi, tmp_path):
+    # factor_inv travels in the DIAMCKPT file (proj/src/runner.cpp:186, 444-445): resume is
+    # bit-exact, and the reference resumes the file
+    t = b200.target_build("pi2", 70, 6)
+    kw = dict(kernel="diam", chains=3, intervals_per_batch=2, n_lag=40, n0=0, master_seed=12, use_explicit_inverse=1)
+    full = b200.sample(t, max_batches=4, **kw)
+    ck = str(tmp_path / "inv.ckpt")
+    b200.sample(t, max_batches=2, checkpoint_path=ck, **kw)
+    import shutil
+    ck2 = str(tmp_path / "inv_copy.ckpt")
+    shutil.copy(ck, ck2)  # the resumed run keeps checkpointing into `ck`
+    _same(full, b200.resume(ck, b200.options(max_batches=4)), 3)
+    r_ref = ref_abi.resume(ck2, ref_abi.options(max_batches=3))
+    assert r_ref.batches == 3 and np.isfinite(r_ref.final_cov_error)

@@ -219,24 +219,36 @@ def test_golden_target_runs_statistics(b200):
         assert em <= 1e-8 and ec <= 1e-8 and et <= 1e-8, i
 
 
-def test_chain_statistics_vs_reference(b200, ref_abi, tmp_path):
-    """Acceptance rate and cov error agree with the reference within Monte Carlo error."""
+@pytest.mark.parametrize("target", ["pi2", "pi1"])
+def test_chain_statistics_vs_reference(b200, ref_abi, tmp_path, target):
+    """north_star's chain-level bar: acceptance rate, cov error, mean error and ESS per sample
+    of log pi (proj/src/diagnostics.cpp:50-70, the reference's own estimator applied to both
+    sides' traces) agree with the reference within Monte Carlo error: 12 independent seeds
+    per side (the same seeds -- the normals differ in the last bits, so after a few hundred
+    steps the trajectories are independent draws of the same process), 3 standard errors."""
     d = 32
-    t_ref = ref_abi.target_build("pi2", d, 4)
+    t_ref = ref_abi.target_build(target, d, 4)
     p = str(tmp_path / "t.bin")
     t_ref.save(p)
     t = b200.target_load(p)
-    kw = dict(kernel="diam", chains=4, intervals_per_batch=4, max_batches=6, n_lag=64, n0=0, record_traces=0)
+    kw = dict(kernel="diam", chains=4, intervals_per_batch=4, max_batches=6, n_lag=64, n0=0, record_traces=1,
+              trace_thin=1, trace_eigen_projections=0)
     stats = {"gpu": [], "ref": []}
-    for seed in range(10):
+    for seed in range(12):
         for name, lib, tt in (("gpu", b200, t), ("ref", ref_abi, t_ref)):
             r = lib.sample(tt, master_seed=100 + seed, threads=4, **kw) if name == "ref" else \
                 lib.sample(tt, master_seed=100 + seed, **kw)
             acc = np.mean([r.chain_history(c, "acceptance")[-8:].mean() for c in range(4)])
-            stats[name].append((acc, r.final_cov_error))
+            # ESS/N of the second half of each chain's log-density trace (post-adaptation)
+            ess = []
+            for c in range(4):
+                tr = r.trace(c, 0)
+                tail = np.ascontiguousarray(tr[tr.size // 2:])
+                ess.append(ref_abi.ess(tail) / tail.size)
+            stats[name].append((acc, r.final_cov_error, r.final_mean_error, float(np.mean(ess))))
     a = np.array(stats["gpu"])
     b = np.array(stats["ref"])
-    for j, what in enumerate(["acceptance", "cov_error"]):
+    for j, what in enumerate(["acceptance", "cov_error", "mean_error", "ess_per_sample"]):
         se = np.sqrt(a[:, j].var(ddof=1) / len(a) + b[:, j].var(ddof=1) / len(b))
         print(f"{what}: gpu {a[:, j].mean():.4f} ref {b[:, j].mean():.4f} (3se {3 * se:.4f})")
         assert abs(a[:, j].mean() - b[:, j].mean()) <= 3 * se + 1e-12
@@ -357,3 +369,52 @@ def test_engine_error_paths(b200):
     # the library stays usable afterwards
     r = b200.sample(t, kernel="diam", chains=2, max_batches=1, n_lag=8, n0=0)
     assert r.batches == 1
+
+
+@pytest.mark.parametrize("kern,n_lag,n0,extra", [("diam", 40, 0, {}), ("pcn", 40, 0, {}),
+                                                 ("diam", 60, 60, dict(adaptive_ref=1, n_ref_start=120))])
+def test_lockstep_explicit_inverse(b200, tmp_path, kern, n_lag, n0, extra):
+    # use_explicit_inverse (proj/src/proposal.cpp:98, 202, 241-252): the factor's inverse is
+    # kept (GPU: recursive-doubling TRTRI on the DMMA GEMM) and the boundary quad term goes
+    # through it (tri_matvec, proposal.cpp:55); the oracle runs the reference's own
+    # invert_lower path on the same draws. The option changes rounding only, amplified by
+    # cond(L): the moving-reference case uses a burn-in so the first adapted covariance is
+    # well conditioned (with n0 = 0 and a 40-step first window the reference's own two modes
+    # already differ by 5e-8 in log alpha, and the step recursion vs a per-step TRSV by 1e-5)
+    _, _, ties = lockstep(b200, tmp_path, "pi1", 12, kern, P=3, M=2, K=3, n_lag=n_lag, n0=n0, seed=9,
+                          use_explicit_inverse=1, **extra)
+    assert ties == 0
+
+
+def test_lockstep_explicit_inverse_multi_level(b200, tmp_path):
+    # d = 150: three 64-blocks (a ragged last one) -> two doubling levels of the TRTRI
+    _, _, ties = lockstep(b200, tmp_path, "pi2", 150, "diam", P=2, M=2, K=2, n_lag=160, n0=0, seed=4,
+                          use_explicit_inverse=1)
+    assert ties == 0
+
+
+@pytest.mark.parametrize("case", ["diam_traces", "am_no_traces", "rw_stop_max_samples", "pcn_psrf_single_chain",
+                                  "pi5_projections"])
+def test_json_report_matches_contract(b200, tmp_path, case):
+    """diam_result_write_json of GPU runs satisfies the reference's report schema
+    (proj/docs/result.schema.json via tests/golden/result_contract.json), including NaN
+    statistics written as null (one chain: PSRF undefined) and runs without traces."""
+    import _schema
+    t = b200.target_build("pi5", 20, 3) if case == "pi5_projections" else b200.target_build("pi2", 10, 2)
+    kw = dict(diam_traces=dict(kernel="diam", chains=3, intervals_per_batch=2, max_batches=3, n_lag=12, n0=10),
+              am_no_traces=dict(kernel="am", chains=2, intervals_per_batch=2, max_batches=2, n_lag=12, n0=0,
+                                record_traces=0),
+              rw_stop_max_samples=dict(kernel="rw", chains=2, max_batches=50, n_lag=10, max_samples=120),
+              pcn_psrf_single_chain=dict(kernel="pcn", chains=1, intervals_per_batch=2, max_batches=2, n_lag=10,
+                                         n0=0),
+              pi5_projections=dict(kernel="diam", chains=2, intervals_per_batch=1, max_batches=2, n_lag=20, n0=0,
+                                   trace_thin=3, inflation=1.2))[case]
+    r = b200.sample(t, master_seed=8, **kw)
+    js = str(tmp_path / "r.json")
+    r.write_json(js)
+    doc = json.load(open(js))
+    assert _schema.violations(doc) == []
+    assert doc["chains"] == kw["chains"] and doc["batches"] == r.batches
+    assert len(doc["beta_history"]) == kw["chains"] and len(doc["ess"]) == kw["chains"]
+    if case == "pcn_psrf_single_chain":
+        assert all(v is None for v in doc["psrf_history"])
