@@ -97,6 +97,10 @@ diam_status diamx_gemm(const double* d_a, const double* d_b, double* d_c, int m,
  * (0 ok, 1 not positive definite) into d_status (int32, device) */
 diam_status diamx_potrf(double* d_a, int64_t stride, int64_t ld, int d, int batch, int* d_status,
                         void* stream);
+/* timing tool: `groups` concurrent streams each refactoring `chains` copies of the SPD matrix
+ * d_src (d + extra_rows rows of stride ld) `rounds` times; device milliseconds */
+diam_status diamx_potrf_bench(const double* d_src, int64_t ld, int d, int extra_rows, int groups, int chains,
+                              int rounds, double* ms);
 /* y_i = L_i^{-1} x_i (batched, L_i = d_l + i*stride), quad_i = 0.5*|y_i|^2 */
 diam_status diamx_trsv(const double* d_l, int64_t stride, int64_t ld, const double* d_x, double* d_y,
                        double* d_quad, int d, int batch, void* stream);

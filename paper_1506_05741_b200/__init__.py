@@ -71,6 +71,7 @@ class B200(DiamABI):
                                 C.c_double, C.c_double, C.c_int, C.c_int, _vp]),
             "diamx_potrf": (st, [_vp, i64, i64, C.c_int, C.c_int, _vp, _vp]),
             "diamx_trsv": (st, [_vp, i64, i64, _vp, _vp, _vp, C.c_int, C.c_int, _vp]),
+            "diamx_potrf_bench": (st, [_vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp]),
         }
         for name, (res, args) in spec.items():
             f = getattr(L, name)

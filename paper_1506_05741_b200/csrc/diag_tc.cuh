@@ -38,6 +38,7 @@ struct DiagTcScratch {
     double a[64 * kTcS];  // the block, then L
     double x[64 * kTcS];  // X = L^-1
     double t[8][64];      // per-warp staging of an 8x8 product
+    double rdiag[64];     // 1 / L_kk (the panel's rsqrt of each pivot)
     int bad;
 };
 
@@ -59,12 +60,12 @@ __device__ __forceinline__ void tc_tile(double (&acc)[2], const double* A, int r
 
 // pre_L (optional): the 64 columns left of the block (same rows, stride ld); the block is
 // first updated A -= pre_L pre_L^T (the right-looking step a 128-wide block column's
-// second half needs), in shared memory. With pre_X (64x64 lower, stride 64) pre_L still
+// second half needs), in shared memory. With pre_X (64x64 lower, stride px_ld) pre_L still
 // holds A's entries and is first solved in place, pre_L <- pre_L pre_X^T (the TRSM of
 // those rows against the first half's inverse).
 __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_t ld, int jb, double* out,
                                             int zero_above, int out_ld, double* pre_L = nullptr,
-                                            const double* pre_X = nullptr) {
+                                            const double* pre_X = nullptr, int px_ld = 64) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int fr = lane >> 2, fk = lane & 3;
     constexpr unsigned kAll = 0xffffffffu;
@@ -108,8 +109,8 @@ __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_
             double e[2] = {0.0, 0.0}, o[2] = {0.0, 0.0};
 #pragma unroll
             for (int k = 0; k < 8 * ct + 8; k += 8) {
-                tile::dmma(e, sx[r * kTcS + k + fk], __ldcg(pre_X + (8 * ct + fr) * 64 + k + fk));
-                tile::dmma(o, sx[r * kTcS + k + 4 + fk], __ldcg(pre_X + (8 * ct + fr) * 64 + k + 4 + fk));
+                tile::dmma(e, sx[r * kTcS + k + fk], __ldcg(pre_X + (8 * ct + fr) * px_ld + k + fk));
+                tile::dmma(o, sx[r * kTcS + k + 4 + fk], __ldcg(pre_X + (8 * ct + fr) * px_ld + k + 4 + fk));
             }
             res[ct][0] = e[0] + o[0];
             res[ct][1] = e[1] + o[1];
@@ -164,18 +165,18 @@ __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_
                 pb[j] = v2 ? sa[r2 * kTcS + k0 + j] : 0.0;
             }
             int bad = 0;
+            // the pivot chain per column: shuffle the pivot, rsqrt, scale, and the next pivot's
+            // own update (lane c+1: L[c+1][c]^2 from its own register, no shuffle); the other
+            // columns' updates (one shuffle each) are off that chain
+            double piv = __shfl_sync(kAll, pa[0], 0);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                double rl = 0.0;
-                if (lane == c) {
-                    const double piv = pa[c];
-                    if (!(piv > 0.0) || !isfinite(piv)) bad = 1;  // proj/src/linalg.cpp:82-84
-                    rl = rsqrt(piv);
-                    pa[c] = piv * rl;
-                }
-                rl = __shfl_sync(kAll, rl, c);
-                if (lane > c) pa[c] *= rl;
+                if (!(piv > 0.0) || !isfinite(piv)) bad = 1;  // proj/src/linalg.cpp:82-84
+                const double rl = rsqrt(piv);
+                pa[c] = lane == c ? piv * rl : pa[c] * rl;
                 pb[c] *= rl;
+                if (lane == 0) sc.rdiag[k0 + c] = rl;
+                if (c + 1 < 8) piv = __shfl_sync(kAll, pa[c + 1] - pa[c] * pa[c], c + 1);
 #pragma unroll
                 for (int j = c + 1; j < 8; ++j) {
                     const double lj = __shfl_sync(kAll, pa[c], j);  // L[k0+j][k0+c]
@@ -207,7 +208,7 @@ __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_
                 double s = (i == j) ? 1.0 : 0.0;
 #pragma unroll
                 for (int k = 0; k < i; ++k) s -= sa[(b0 + i) * kTcS + b0 + k] * xcol[k];
-                xcol[i] = s / sa[(b0 + i) * kTcS + b0 + i];
+                xcol[i] = s * sc.rdiag[b0 + i];  // 1 / L_ii from the panel (no division chain)
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) sx[(b0 + i) * kTcS + b0 + j] = (i >= j) ? xcol[i] : 0.0;
@@ -247,11 +248,18 @@ __device__ __forceinline__ int diag64_tc_sc(DiagTcScratch& sc, double* A, int64_
     }
     TC_MARK(6);
     // store L (exact zeros above the diagonal: the left-looking GEMM's garbage) and X
-    for (int e = tid; e < 64 * 64; e += 256) {
+    for (int e = 2 * tid; e < 64 * 64; e += 512) {  // pairs of columns (ld, out_ld even)
         const int r = e >> 6, q = e & 63;
-        if (r < jb && q < jb) A[(int64_t)r * ld + q] = q <= r ? sa[r * kTcS + q] : 0.0;
-        out[r * out_ld + q] = (r < jb && q < jb && q <= r) ? sx[r * kTcS + q] : 0.0;
-        if (zero_above && q < jb) A[(int64_t)(r - kDiagNb) * ld + q] = 0.0;
+        const bool v0 = r < jb && q < jb, v1 = r < jb && q + 1 < jb;
+        const double2 l = make_double2(q <= r ? sa[r * kTcS + q] : 0.0, q + 1 <= r ? sa[r * kTcS + q + 1] : 0.0);
+        const double2 x = make_double2(v0 && q <= r ? sx[r * kTcS + q] : 0.0, v1 && q + 1 <= r ? sx[r * kTcS + q + 1] : 0.0);
+        if (v1) *reinterpret_cast<double2*>(A + (int64_t)r * ld + q) = l;
+        else if (v0) A[(int64_t)r * ld + q] = l.x;
+        *reinterpret_cast<double2*>(out + r * out_ld + q) = x;
+        if (zero_above) {
+            if (v1) *reinterpret_cast<double2*>(A + (int64_t)(r - kDiagNb) * ld + q) = make_double2(0.0, 0.0);
+            else if (v0) A[(int64_t)(r - kDiagNb) * ld + q] = 0.0;
+        }
     }
     TC_MARK(7);
     return 0;

@@ -178,11 +178,11 @@ void upload_padded(double* dst, int64_t ld, const Mat& m) {
 Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shared_ptr<Comm> comm)
     : tgtp_(std::move(t)), tgt_(*tgtp_), cfg_(cfg), k_(cfg.kernel), comm_(std::move(comm)) {
     validate_run_cfg(cfg_, tgt_);
-    if (const char* e = std::getenv("DIAM_B200_SKIP")) {
+    if (const char* e = std::getenv("DIAM_B200_TWICE")) {
         const std::string v = e;
         const char* names[] = {"normals", "trmm", "target", "mh", "syrk", "potrf"};
         for (int i = 0; i < 6; ++i)
-            if (v.find(names[i]) != std::string::npos) skip_ |= 1u << i;
+            if (v.find(names[i]) != std::string::npos) twice_ |= 1u << i;
     }
     if (comm_) {
         rank_ = comm_->rank();
@@ -738,6 +738,8 @@ void Engine::end_windows() {
         std::vector<size_t> todo(groups_.size());
         for (size_t i = 0; i < todo.size(); ++i) todo[i] = i;
         while (!todo.empty()) {
+            const auto tw0 = std::chrono::steady_clock::now();
+            const size_t before = todo.size();
             for (auto it = todo.begin(); it != todo.end();) {
                 const size_t i = *it;
                 if (plans[m].refactor) {
@@ -756,6 +758,8 @@ void Engine::end_windows() {
                 tail_finish(groups_[i], plans[m]);
                 if (m + 1 < M) enqueue_head(groups_[i], plans[m + 1]);
             }
+            if (todo.size() == before)  // a pass with nothing ready: the host waited
+                host_wait_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - tw0).count();
         }
         while (!pending.empty()) {
             std::vector<size_t> still;
@@ -792,7 +796,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     // ---- noise: W from Philox, Xi = s W L^T, H = Xi G^T (proposal.cpp:254-266); row r of
     // the window draws counters nctr + r d .. nctr + (r + 1) d - 1 of the chain's stream
     timed_begin(s);
-    if (!(skip_ & kSkipNormals))
+    for (int rep = (twice_ & kTwiceNormals) ? 2 : 1; rep > 0; --rep)
         launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, rows, d_, ld_, nkeys_ + o,
                    p.nctr + (uint64_t)r0 * d_, beta_ + o, infl, s);
     timed_end("normals", 0.0, s);
@@ -812,9 +816,10 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         t.alpha_vec_mul = infl;
         t.beta = 0.0;
         t.tri_b_lower = 1;
-        if (!(skip_ & kSkipTrmm)) gemm("trmm_noise", t, C, true, true, s);
+        gemm("trmm_noise", t, C, true, true, s);
+        if (twice_ & kTwiceTrmm) gemm("trmm_noise", t, C, true, true, s);
     }
-    if (!(skip_ & kSkipTarget)) {
+    {
         GemmBatch h{};
         h.B = (const double* const*)Gp_;
         h.lda = ld_;
@@ -829,6 +834,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
             h.C = g.Hb;
             h.M = C * Lc_;  // the group's window chunks are one contiguous (C Lc) x ld matrix
             gemm("gemm_target", h, 1, true, true, s);
+            if (twice_ & kTwiceTarget) gemm("gemm_target", h, 1, true, true, s);
         } else {            // ragged last chunk: per-chain pieces
             h.B = (const double* const*)Gpc_;
             h.A = (const double* const*)g.Xip;
@@ -879,7 +885,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     // the previous batch's trace copies read the buffers the MH steps write
     if (merge_pending_ && p.record) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
     timed_begin(s);
-    if (!(skip_ & kSkipMh)) launch_mh_window(sp, twisted_, s);
+    launch_mh_window(sp, twisted_, s);
     timed_end("mh_window", 0.0, s);
     if (capture_) capture_chunk(g, r0, rows);
 
@@ -889,7 +895,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     // is a SYRK over about acceptance x kc rows instead of kc
     // the merge reads S_ / mean_ and clears mean_; the histories' copies read hist_*
     if (merge_pending_) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
-    if (kc > 0 && !(skip_ & kSkipSyrk)) {
+    if (kc > 0) {
         const double total = (double)(cb + (uint64_t)kc);
         GemmBatch m{};
         m.A = (const double* const*)(Hp_ + o);
@@ -947,7 +953,14 @@ void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {
         DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
         nvtxRangePushA("potrf");
         timed_begin(s);
-        if (!(skip_ & kSkipPotrf)) potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+        potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+        if (twice_ & kTwicePotrf) {  // blend + factorization again: same inputs, same factor
+            launch_blend_cov(g.Lnp, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, mb_ + o * ld_, ld_,
+                             C, d_, ld_, nullptr, 0.0, nullptr, s, ax, axr);
+            launch_trace_floor(g.Lnp, ld_, mb_ + o * ld_, ld_, C, d_, tr_ + o, try_ + o, s);
+            DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
+            potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+        }
         timed_end("potrf", (double)C * d_ * (double)d_ * d_ / 3.0, s);
         nvtxRangePop();
         DGB_CUDA(cudaMemcpyAsync(h_flags_ + o, status_ + o, C * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -972,7 +985,9 @@ void Engine::enqueue_tail(Group& g, const WindowPlan& p) {
 bool Engine::tail_begin(Group& g, const WindowPlan& p, Ladder& st) {
     if (!p.refactor) return true;
     const int C = g.C, o = g.off;
+    const auto tw0 = std::chrono::steady_clock::now();
     DGB_CUDA(cudaEventSynchronize(g.status_ev));
+    host_wait_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - tw0).count();
     st.failing.assign(C, 0);
     bool any = false;
     for (int c = 0; c < C; ++c) {
@@ -1239,6 +1254,8 @@ double Engine::run_batches_timed(int k) {
     DGB_CUDA(cudaEventCreate(&b));
     DGB_CUDA(cudaDeviceSynchronize());
     DGB_CUDA(cudaEventRecord(a, stream_));
+    const auto th0 = std::chrono::steady_clock::now();
+    host_wait_s_ = 0.0;
     if (profiling_) {
         resolve_events();
         if (!timeline_base_) DGB_CUDA(cudaEventCreate(&timeline_base_));
@@ -1271,6 +1288,12 @@ double Engine::run_batches_timed(int k) {
         ++batches_done_;
     }
     DGB_CUDA(cudaEventRecord(b, stream_));
+    {  // host time to enqueue the k batches, and how much of it was spent waiting on the GPU
+        const double enq = std::chrono::duration<double>(std::chrono::steady_clock::now() - th0).count();
+        stats_["host_enqueue"].ms += 1e3 * enq;
+        stats_["host_enqueue"].launches += k;
+        stats_["host_wait"].ms += 1e3 * host_wait_s_;
+    }
     DGB_CUDA(cudaEventSynchronize(b));
     float ms = 0.f;
     DGB_CUDA(cudaEventElapsedTime(&ms, a, b));

@@ -270,11 +270,13 @@ private:
     std::map<cudaStream_t, cudaEvent_t> open_;
 
     bool capture_ = false;
-    // timing experiments only (DIAM_B200_SKIP=normals,trmm,target,mh,syrk,potrf): the named
-    // kernel classes are not launched, so a batch's time without them can be measured;
-    // results are meaningless with any bit set
-    unsigned skip_ = 0;
-    enum : unsigned { kSkipNormals = 1, kSkipTrmm = 2, kSkipTarget = 4, kSkipMh = 8, kSkipSyrk = 16, kSkipPotrf = 32 };
+    // timing tool (DIAM_B200_TWICE=normals,trmm,target,potrf; tools/twice_sweep.py): the named
+    // idempotent steps are launched twice -- the second launch recomputes the same values, so
+    // the run is unchanged and the batch time grows by what one more instance costs in the
+    // overlapped schedule
+    unsigned twice_ = 0;
+    enum : unsigned { kTwiceNormals = 1, kTwiceTrmm = 2, kTwiceTarget = 4, kTwicePotrf = 32 };
+    double host_wait_s_ = 0.0;  // run_batches_timed: host time blocked on the GPU (statuses)
     std::vector<std::vector<double>> cap_w_, cap_ratio_;
     std::vector<std::vector<uint8_t>> cap_acc_;
     std::vector<double> cap_wbuf_;  // C x n_lag x d: the current window's W, filled chunk by chunk

@@ -50,6 +50,16 @@ using GemmCfgT = Cfg<128, 64, 32, 2, AK, BKM, 4, 2, 2>;
 
 }  // namespace
 
+// 64 x 64 tiles, 4 warps of 32 x 32, up to 3 CTAs per SM: half the long-K latency of one tile
+// (the factorization's left-looking updates sit on the refactor's critical path)
+template <bool AK, bool BKM>
+using GemmCfgS = Cfg<64, 64, 32, 2, AK, BKM, 2, 2, 3>;
+
+void gemm_f64_small(const GemmBatch& g, int batch, cudaStream_t stream) {
+    if (batch <= 0 || g.M <= 0 || g.N <= 0) return;
+    launch<GemmCfgS<true, true>, true, true>(g, batch, stream);
+}
+
 void gemm_f64(const GemmBatch& g, int batch, bool a_kmajor, bool b_kmajor, cudaStream_t stream) {
     if (batch <= 0 || g.M <= 0 || g.N <= 0) return;
     if (a_kmajor && b_kmajor) launch<GemmCfgT<true, true>, true, true>(g, batch, stream);

@@ -50,5 +50,7 @@ struct GemmBatch {
 
 // Launch the batched GEMM on `stream`. Layout flags select the template instance.
 void gemm_f64(const GemmBatch& g, int batch, bool a_kmajor, bool b_kmajor, cudaStream_t stream);
+// the same with 64 x 64 tiles (both operands K-major): shorter per-CTA latency for long K
+void gemm_f64_small(const GemmBatch& g, int batch, cudaStream_t stream);
 
 }  // namespace dgb

@@ -471,10 +471,20 @@ bool try_tma(const StepParams& p, cudaStream_t s) {
     const size_t table = (size_t)p.n_lag * sizeof(double);
     constexpr size_t kMaxSmem = 220 * 1024;
     if (table + 2 * stage > kMaxSmem) return false;
-    // ring depth: deep enough to hide HBM latency, shallow enough that a 110 KB GEMM CTA of
-    // another chain group can share the SM (d=1024: 6 stages = 100 KB; 6 vs 8 stages
-    // measured equal within 0.3%); at most kMaxStages (the mbarrier array)
-    const int NS = (int)std::min<size_t>((size_t)std::min(6, kMaxStages), (kMaxSmem - table) / stage);
+    // ring depth: deep enough to hide HBM latency (>= 3 steps ahead), shallow enough that a
+    // 110 KB GEMM CTA of another chain group can share the SM: the step loop leaves the DMMA
+    // pipe idle, so an MH CTA that fills the SM's shared memory idles it for the whole window
+    // (d=1024 pCN form: 3 rows of 8 KB per stage -> 4 stages + the log-u table = 100 KB);
+    // at most kMaxStages (the mbarrier array)
+    static const int env_ns = [] {
+        const char* e = std::getenv("DIAM_B200_STEP_STAGES");
+        return e ? std::atoi(e) : 0;
+    }();
+    constexpr size_t kShareBudget = 112 * 1024;  // 227 KB - one 110.6 KB GEMM CTA - reserves
+    int NS = (int)std::min<size_t>(kMaxStages, (kMaxSmem - table) / stage);
+    if (table + 3 * stage <= kShareBudget) NS = std::min<int>(NS, (int)((kShareBudget - table) / stage));
+    NS = std::min(NS, 6);
+    if (env_ns > 0) NS = std::min<int>(env_ns, (int)std::min<size_t>(kMaxStages, (kMaxSmem - table) / stage));
     const size_t smem = NS * stage + table;
     auto kern = mh_window_tma_kernel<R, TW, T>;
     set_smem_attr(reinterpret_cast<const void*>(kern), (int)smem);

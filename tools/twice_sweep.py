@@ -1,11 +1,11 @@
 """Marginal cost of each kernel class in the grouped engine (timing experiment).
 
-    python tools/skip_sweep.py [--config d1024] [--batches 5]
+    python tools/twice_sweep.py [--config d1024] [--batches 5]
 
-Runs the bench workload with DIAM_B200_SKIP=<class> (the class is not launched at all;
-results are discarded) and prints the batch time against the full run: the difference is
-what the class costs on the critical path of the real, overlapped schedule -- unlike the
-single-stream per-class times of bench.py's profile pass.
+Runs the bench workload with DIAM_B200_TWICE=<class> (the class's idempotent step is
+launched twice, so the run itself is unchanged) and prints the batch time against the plain
+run: the difference is what one instance of the class costs in the real, overlapped
+schedule -- unlike the single-stream per-class times of bench.py's profile pass.
 """
 import argparse
 import os
@@ -22,7 +22,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="d1024", choices=sorted(bench.CONFIGS))
     ap.add_argument("--batches", type=int, default=5)
-    ap.add_argument("--sets", default="none,normals,trmm,target,mh,syrk,potrf,normals+trmm+target,potrf+mh")
+    ap.add_argument("--sets", default="none,normals,trmm,target,potrf")
+    ap.add_argument("--twice", action="store_true", default=True, help="DIAM_B200_TWICE (the only mode)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     kind, d, per_gpu, n_lag, M = cfg
@@ -31,18 +32,19 @@ def main():
     t = lib.target_load(path)
     base = None
     for s in args.sets.split(","):
+        var = "DIAM_B200_TWICE"
         if s == "none":
-            os.environ.pop("DIAM_B200_SKIP", None)
+            os.environ.pop(var, None)
         else:
-            os.environ["DIAM_B200_SKIP"] = s
+            os.environ[var] = s
         eng = lib.engine(t, **bench.run_options(cfg, per_gpu))
         eng.run_batches(2)
         ms = eng.run_batches(args.batches) / args.batches
         del eng
         if base is None:
             base = ms
-        print(f"skip {s:24s} {ms:7.2f} ms/batch  (saves {base - ms:6.2f})", flush=True)
-    os.environ.pop("DIAM_B200_SKIP", None)
+        print(f"{'twice' if args.twice else 'skip'} {s:24s} {ms:7.2f} ms/batch  (delta {ms - base:+6.2f})", flush=True)
+    os.environ.pop(var, None)
     os.unlink(path)
 
 
