@@ -54,6 +54,20 @@ __global__ void draws_kernel(int kind, double* out_f64, uint64_t* out_u64, int64
     }
 }
 
+#ifdef MH_PROFILE  // tools/mh_lat.cu: per-phase cycle sums of block 0, thread 0
+__device__ long long g_mh_prof[8];
+#define MH_PROF(i)                                                       \
+    do {                                                                 \
+        const long long now = clock64();                                 \
+        mh_acc[i] += now - mh_t0;                                        \
+        mh_t0 = now;                                                     \
+    } while (0)
+#else
+#define MH_PROF(i) \
+    do {           \
+    } while (0)
+#endif
+
 constexpr int kStepThreads = 512;
 constexpr int kMaxStages = 8;  // TMA ring depth bound (one mbarrier per stage)
 constexpr int kStepWarps = kStepThreads / 32;
@@ -290,8 +304,27 @@ __device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t byt
                  : "memory");
 }
 
-template <int R, bool TWISTED, int T>
+// Two partial sums of a warp in one butterfly: the first exchange leaves lanes 0-15 with
+// partial sums of `a` and lanes 16-31 with partial sums of `b`, four more levels finish each
+// (5 double shuffles instead of 10); lane 0 ends with sum(a), lane 16 with sum(b).
+__device__ __forceinline__ double warp_sum2(double a, double b, int lane) {
+    const bool hi = lane & 16;
+    double v = (hi ? b : a) + __shfl_xor_sync(0xffffffffu, hi ? a : b, 16);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// PRE: the parts of the candidate that only change on acceptance are kept ready --
+// a = x_ref + c (x - x_ref) (the reference's exact bits), ga = G x_ref + c (G x - G x_ref) and
+// cy = c y -- so a step is xc = a + xi, gc = ga + h, yc = cy + s w: 5 FP64 ops per entry
+// instead of 10 (the register cost rules it out above 2 pairs per thread).
+// ZREF: the reference point is the origin (p.xr == nullptr): x_ref and G x_ref are the
+// constant 0 instead of registers. TWG: the twisted target's per-entry constants are read
+// through L1 each step instead of held in registers (wide rows: 4 pairs per thread).
+template <int R, bool TWISTED, int T, bool PRE, bool ZREF>
 __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int NS) {
+    constexpr bool TWG = TWISTED && R >= 4;
     constexpr int NW = T / 32;
     const int c = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -301,7 +334,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     const int nrows = pcn ? 3 : 2;  // xi, h (+ w for the pCN-form y recursion)
     extern __shared__ __align__(128) double ring[];  // NS stages, then the log-uniform table
     __shared__ __align__(8) uint64_t full[kMaxStages];
-    __shared__ double red[2][NW][2];
+    __shared__ __align__(16) double red[2][NW][2];
     const uint32_t row_bytes = (uint32_t)(ld * sizeof(double));
     double* stage0 = ring;
     const int64_t stage_len = (int64_t)nrows * ld;
@@ -315,8 +348,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     double* Hc = p.H + c * p.win_stride;
     Compactor cp;
 
-    auto issue = [&](int t) {  // producer: row t of the window into stage t % NS
-        const int s = t % NS;
+    auto issue = [&](int t, int s) {  // producer: row t of the window into stage s = t % NS
         double* st = stage0 + s * stage_len;
         mbar_expect_tx(&full[s], row_bytes * nrows);
         tma_row(st, Xc + (int64_t)t * ld, row_bytes, &full[s]);
@@ -329,10 +361,30 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     }
     __syncthreads();
     if (tid == 0)
-        for (int t = 0; t < NS && t < p.n_lag; ++t) issue(t);
+        for (int t = 0; t < NS && t < p.n_lag; ++t) issue(t, t);
 
-    double2 x[R], g[R], y[R], xr[R], gr[R], ie[R], bc[R];
+    double2 x[R], g[R], y[R], xrv[ZREF ? 1 : R], grv[ZREF ? 1 : R], iev[TWG ? 1 : R], bcv[TWG ? 1 : R], a[R], ga[R],
+        cy[R];
     bool valid[R];
+    auto XR = [&](int r) -> double2 { return ZREF ? make_double2(0.0, 0.0) : xrv[ZREF ? 0 : r]; };
+    auto GR = [&](int r) -> double2 { return ZREF ? make_double2(0.0, 0.0) : grv[ZREF ? 0 : r]; };
+    auto IE = [&](int r) -> double2 {
+        return TWG ? __ldg(reinterpret_cast<const double2*>(p.inv_eig) + tid + r * T) : iev[TWG ? 0 : r];
+    };
+    auto BC = [&](int r) -> double2 {
+        return TWG ? __ldg(reinterpret_cast<const double2*>(p.bcoef) + tid + r * T) : bcv[TWG ? 0 : r];
+    };
+    // candidate parts that change only on acceptance (exact reference bits for a)
+    auto refresh = [&](int r) {
+        if (!PRE) return;
+        const double2 xr = XR(r), gr = GR(r);
+        a[r].x = __dadd_rn(xr.x, __dmul_rn(cc, __dadd_rn(x[r].x, -xr.x)));
+        a[r].y = __dadd_rn(xr.y, __dmul_rn(cc, __dadd_rn(x[r].y, -xr.y)));
+        ga[r].x = gr.x + cc * (g[r].x - gr.x);
+        ga[r].y = gr.y + cc * (g[r].y - gr.y);
+        cy[r].x = cc * y[r].x;
+        cy[r].y = cc * y[r].y;
+    };
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = 2 * (tid + r * T);
@@ -341,12 +393,15 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
         x[r] = valid[r] ? ld2(p.x + c * ld + e) : z2;
         g[r] = valid[r] ? ld2(p.g + c * ld + e) : z2;
         y[r] = (valid[r] && pcn) ? ld2(p.y + c * ld + e) : z2;
-        xr[r] = (valid[r] && p.xr) ? ld2(p.xr + c * ld + e) : z2;
-        gr[r] = (valid[r] && p.gr) ? ld2(p.gr + c * ld + e) : z2;
-        if (TWISTED) {
-            ie[r] = valid[r] ? ld2(p.inv_eig + e) : z2;
-            bc[r] = valid[r] ? ld2(p.bcoef + e) : z2;
+        if (!ZREF) {
+            xrv[ZREF ? 0 : r] = (valid[r] && p.xr) ? ld2(p.xr + c * ld + e) : z2;
+            grv[ZREF ? 0 : r] = (valid[r] && p.gr) ? ld2(p.gr + c * ld + e) : z2;
         }
+        if (TWISTED && !TWG) {
+            iev[TWG ? 0 : r] = valid[r] ? ld2(p.inv_eig + e) : z2;
+            bcv[TWG ? 0 : r] = valid[r] ? ld2(p.bcoef + e) : z2;
+        }
+        refresh(r);
     }
     double lp = p.log_pi[c], q = pcn ? p.quad[c] : 0.0;
     uint64_t nacc = p.n_accepted[c];
@@ -358,56 +413,110 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     for (int t = tid; t < p.n_lag; t += T) logu_tab[t] = log(philox_uniform_open(uk, u0 + (uint64_t)t));
     __syncthreads();
 
+    // one entry's candidate from the stage (xi, h, w rows): the same operations whether called
+    // for the dot products or, after the decision, to adopt the candidate (bit-identical)
+    auto cand = [&](const double* pxi, const double* ph, const double* pw, int r, double2& xc, double2& gc,
+                    double2& yc) {
+        const int e = 2 * (tid + r * T);
+        const double2 xi = valid[r] ? ld2(pxi + e) : make_double2(0.0, 0.0);
+        const double2 h = valid[r] ? ld2(ph + e) : make_double2(0.0, 0.0);
+        // exact reference candidate (proj/src/proposal.cpp:119-124), no FMA contraction
+        if (PRE) {
+            xc.x = __dadd_rn(a[r].x, xi.x);
+            xc.y = __dadd_rn(a[r].y, xi.y);
+            gc.x = ga[r].x + h.x;
+            gc.y = ga[r].y + h.y;
+        } else {
+            const double2 xr = XR(r), gr = GR(r);
+            xc.x = __dadd_rn(__dadd_rn(xr.x, __dmul_rn(cc, __dadd_rn(x[r].x, -xr.x))), xi.x);
+            xc.y = __dadd_rn(__dadd_rn(xr.y, __dmul_rn(cc, __dadd_rn(x[r].y, -xr.y))), xi.y);
+            gc.x = gr.x + cc * (g[r].x - gr.x) + h.x;
+            gc.y = gr.y + cc * (g[r].y - gr.y) + h.y;
+        }
+        if (pcn) {
+            const double2 w = valid[r] ? ld2(pw + e) : make_double2(0.0, 0.0);
+            if (PRE) {
+                yc.x = cy[r].x + sc * w.x;
+                yc.y = cy[r].y + sc * w.y;
+            } else {
+                yc.x = cc * y[r].x + sc * w.x;
+                yc.y = cc * y[r].y + sc * w.y;
+            }
+        }
+    };
+    // With 3 or more stages a stage is refilled one step late, so an accepted candidate is
+    // re-read from shared memory; with 2 (wide rows) the refill cannot wait and the accepted
+    // row is re-read from global memory (row t of Xi / H is overwritten by the compaction
+    // only after the adoption, j <= t)
+    const bool late = NS >= 3;
+#ifdef MH_PROFILE
+    long long mh_t0 = clock64(), mh_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+    int s = 0;           // t % NS, kept incrementally (no integer division in the step)
+    uint32_t phase = 0;  // (t / NS) & 1
     for (int t = 0; t < p.n_lag; ++t) {
         const double logu = logu_tab[t];
-        const int s = t % NS;
-        mbar_wait(&full[s], (uint32_t)((t / NS) & 1));
+        MH_PROF(0);
+        mbar_wait(&full[s], phase);
+        MH_PROF(1);
         const double* st = stage0 + s * stage_len;
-        double2 xc[R], gc[R], yc[R];
-        double sa = 0.0, sb = 0.0;
+        double sa0 = 0.0, sa1 = 0.0, sb0 = 0.0, sb1 = 0.0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int e = 2 * (tid + r * T);
-            const double2 xi = valid[r] ? ld2(st + e) : make_double2(0.0, 0.0);
-            const double2 h = valid[r] ? ld2(st + ld + e) : make_double2(0.0, 0.0);
-            // exact reference candidate (proj/src/proposal.cpp:119-124), no FMA contraction
-            xc[r].x = __dadd_rn(__dadd_rn(xr[r].x, __dmul_rn(cc, __dadd_rn(x[r].x, -xr[r].x))), xi.x);
-            xc[r].y = __dadd_rn(__dadd_rn(xr[r].y, __dmul_rn(cc, __dadd_rn(x[r].y, -xr[r].y))), xi.y);
-            gc[r].x = gr[r].x + cc * (g[r].x - gr[r].x) + h.x;
-            gc[r].y = gr[r].y + cc * (g[r].y - gr[r].y) + h.y;
+            double2 xc, gc, yc;
+            cand(st, st + ld, st + 2 * ld, r, xc, gc, yc);
             if (TWISTED) {
-                const double w0 = gc[r].x;
-                const double w1 = gc[r].y + bc[r].x * gc[r].x * gc[r].x;
-                sa += w0 * w0 * ie[r].x + w1 * w1 * ie[r].y;
+                const double2 ie = IE(r), bc = BC(r);
+                const double w0 = gc.x;
+                const double w1 = gc.y + bc.x * gc.x * gc.x;
+                sa0 += w0 * w0 * ie.x;
+                sa1 += w1 * w1 * ie.y;
             } else {
-                sa += xc[r].x * gc[r].x + xc[r].y * gc[r].y;
+                sa0 += xc.x * gc.x;
+                sa1 += xc.y * gc.y;
             }
             if (pcn) {
-                const double2 w = valid[r] ? ld2(st + 2 * ld + e) : make_double2(0.0, 0.0);
-                yc[r].x = cc * y[r].x + sc * w.x;
-                yc[r].y = cc * y[r].y + sc * w.y;
-                sb += yc[r].x * yc[r].x + yc[r].y * yc[r].y;
+                sb0 += yc.x * yc.x;
+                sb1 += yc.y * yc.y;
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            sa += __shfl_xor_sync(0xffffffffu, sa, o);
-            sb += __shfl_xor_sync(0xffffffffu, sb, o);
-        }
+        MH_PROF(2);
+        const double ws = warp_sum2(sa0 + sa1, sb0 + sb1, lane);
         const int buf = t & 1;
-        if (lane == 0) {
-            red[buf][warp][0] = sa;
-            red[buf][warp][1] = sb;
-        }
+        if ((lane & 15) == 0) red[buf][warp][lane >> 4] = ws;
+        MH_PROF(3);
         __syncthreads();
-        // every thread is done with stage s: refill it NS steps ahead
-        if (tid == 0 && t + NS < p.n_lag) issue(t + NS);
-        double ta = 0.0, tb = 0.0;
-#pragma unroll
-        for (int k = 0; k < NW; ++k) {
-            ta += red[buf][k][0];
-            tb += red[buf][k][1];
+        MH_PROF(4);
+        // every thread is done with step t-1 (its stage may be re-read for an adoption until
+        // this barrier): refill that stage NS - 1 steps ahead
+        if (tid == 0) {
+            if (late && t > 0 && t - 1 + NS < p.n_lag) issue(t - 1 + NS, s == 0 ? NS - 1 : s - 1);
+            if (!late && t + NS < p.n_lag) issue(t + NS, s);
         }
+        double ta = 0.0, tb = 0.0;
+        {
+            // the warps' partial sums in 4 independent chains (few registers even at 16 warps)
+            constexpr int NA = NW < 4 ? NW : 4;
+            double2 v[NA];
+#pragma unroll
+            for (int k = 0; k < NA; ++k) v[k] = *reinterpret_cast<const double2*>(&red[buf][k][0]);
+#pragma unroll
+            for (int k = NA; k < NW; ++k) {
+                const double2 u = *reinterpret_cast<const double2*>(&red[buf][k][0]);
+                v[k % NA].x += u.x;
+                v[k % NA].y += u.y;
+            }
+#pragma unroll
+            for (int k = NA / 2; k > 0; k >>= 1)
+#pragma unroll
+                for (int i = 0; i < k; ++i) {
+                    v[i].x += v[i + k].x;
+                    v[i].y += v[i + k].y;
+                }
+            ta = v[0].x;
+            tb = v[0].y;
+        }
+        MH_PROF(5);
         const double lpc = -0.5 * ta;
         const double qc = pcn ? hq * tb : 0.0;
         const double ratio = pcn ? (lpc + qc) - (lp + q) : lpc - lp;  // proj/src/proposal.cpp:77-82
@@ -423,9 +532,13 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
         if (acc) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                x[r] = xc[r];
-                g[r] = gc[r];
-                if (pcn) y[r] = yc[r];
+                double2 xc, gc, yc;
+                if (late) cand(st, st + ld, st + 2 * ld, r, xc, gc, yc);
+                else cand(Xc + (int64_t)t * ld, Hc + (int64_t)t * ld, Wc + (int64_t)t * ld, r, xc, gc, yc);
+                x[r] = xc;
+                g[r] = gc;
+                if (pcn) y[r] = yc;
+                refresh(r);
             }
             lp = lpc;
             q = qc;
@@ -439,7 +552,16 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
             if (p.log_ratio_out) p.log_ratio_out[(int64_t)c * p.out_ld + t] = ratio;
             if (p.row_of && counted) p.row_of[(int64_t)c * p.out_ld + t] = cp.j;
         }
+        MH_PROF(6);
+        if (++s == NS) {
+            s = 0;
+            phase ^= 1u;
+        }
     }
+#ifdef MH_PROFILE
+    if (blockIdx.x == 0 && tid == 32)  // a thread of warp 1: not the TMA producer
+        for (int i = 0; i < 7; ++i) g_mh_prof[i] = mh_acc[i];
+#endif
     if (cp.j >= 0) store_row<R, T>(Hc + (int64_t)cp.j * ld, x, valid, tid, d, cp.mult);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -464,7 +586,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     }
 }
 
-template <int R, bool TW, int T>
+template <int R, bool TW, int T, bool PRE = (R * T <= 512)>
 bool try_tma(const StepParams& p, cudaStream_t s) {
     const int nrows = p.pcn ? 3 : 2;
     const size_t stage = (size_t)nrows * p.ld * sizeof(double);
@@ -486,7 +608,7 @@ bool try_tma(const StepParams& p, cudaStream_t s) {
     NS = std::min(NS, 6);
     if (env_ns > 0) NS = std::min<int>(env_ns, (int)std::min<size_t>(kMaxStages, (kMaxSmem - table) / stage));
     const size_t smem = NS * stage + table;
-    auto kern = mh_window_tma_kernel<R, TW, T>;
+    auto kern = p.xr ? mh_window_tma_kernel<R, TW, T, PRE, false> : mh_window_tma_kernel<R, TW, T, PRE, true>;
     set_smem_attr(reinterpret_cast<const void*>(kern), (int)smem);
     kern<<<p.chains, T, smem, s>>>(p, NS);
     return true;
