@@ -73,6 +73,10 @@ void diamx_engine_free(diamx_engine* e);
  * 0's result (chain histories all-gathered, traces merged). For parity tests. */
 diam_status diamx_sample_threads(const diam_target* target, const diam_run_options* options, int world,
                                  diam_result** out);
+/* diam_resume with `world` in-process ranks: the sharded restore of a DIAMCKPT file (every
+ * rank reads the file and keeps its block of chains) */
+diam_status diamx_resume_threads(const char* path, const diam_run_options* overrides, int world,
+                                 diam_result** out);
 
 /* parity capture: run a full diam_sample-equivalent and keep every window's
  * standard normals W (n_windows x n_lag x d per chain) and per-step log alpha /

@@ -64,6 +64,7 @@ class B200(DiamABI):
             "diamx_engine_free": (None, [_vp]),
             "diamx_sample_capture": (st, [_vp, C.POINTER(RunOptions), C.POINTER(_vp), C.POINTER(_vp)]),
             "diamx_sample_threads": (st, [_vp, C.POINTER(RunOptions), C.c_int, C.POINTER(_vp)]),
+            "diamx_resume_threads": (st, [C.c_char_p, C.POINTER(RunOptions), C.c_int, C.POINTER(_vp)]),
             "diamx_capture_len": (i64, [_vp, i64, C.c_char_p]),
             "diamx_capture_copy": (st, [_vp, i64, C.c_char_p, _dp, i64]),
             "diamx_draws": (st, [C.c_int, _vp, _vp, i64, u64, u64, C.c_char_p, u64, _vp]),
@@ -98,6 +99,14 @@ class B200(DiamABI):
         o = self.options(**opts)
         r = C.c_void_p()
         self.check(self.lib.diamx_sample_threads(target.h, C.byref(o), world, C.byref(r)))
+        return Result(self, r)
+
+    def resume_threads(self, path: str, world: int, overrides=None):
+        """diam_resume with `world` in-process ranks (the sharded restore)."""
+        from .abi import Result
+        r = C.c_void_p()
+        self.check(self.lib.diamx_resume_threads(path.encode(), C.byref(overrides) if overrides else None, world,
+                                                 C.byref(r)))
         return Result(self, r)
 
     def launch_count(self) -> int:

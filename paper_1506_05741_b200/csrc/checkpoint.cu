@@ -101,7 +101,6 @@ Mat mirror_lower(const double* h, int d, int64_t ld) {
 }  // namespace
 
 void Engine::save_checkpoint(double wall) {
-    require(!comm_, Err::InvalidArgument, "checkpointing a multi-GPU run is not supported yet");
     DGB_CUDA(cudaDeviceSynchronize());
     const int C = C_;
     auto fetch = [&](const void* src, size_t bytes) {
@@ -123,6 +122,63 @@ void Engine::save_checkpoint(double wall) {
     std::vector<double*> lptr(C);
     DGB_CUDA(cudaMemcpy(lptr.data(), Lp_, C * sizeof(double*), cudaMemcpyDeviceToHost));
 
+    // this rank's chain records (rank order = global chain order under the block sharding)
+    // and its part of the B200 extension, in memory; rank 0 writes the file
+    BinOut rec, ext;
+    const uint64_t nctr = nctr_;
+    for (int c = 0; c < C; ++c) {
+        rec.vec(Vec(x.begin() + (size_t)c * ld_, x.begin() + (size_t)c * ld_ + d_));
+        rec.pod<double>(lp[c]);
+        rec.pod<double>(k_.pcn_form() ? qd[c] : 0.0);
+        rec.pod<double>(bt[c]);
+        rec.pod<uint64_t>(n_);
+        rec.pod<uint64_t>(0);  // n_accepted: reset at every lag boundary
+        // a lower factor as the reference's full square (zero upper part), row by row
+        auto write_lower = [&](const std::vector<double>& m) {
+            rec.pod<uint64_t>(d_);
+            std::vector<double> row(d_);
+            for (int i = 0; i < d_; ++i) {
+                for (int j = 0; j < d_; ++j) row[j] = j <= i ? m[(size_t)i * ld_ + j] : 0.0;
+                rec.raw(row.data(), row.size() * 8);
+            }
+        };
+        write_lower(fetch_d(lptr[c], (size_t)d_ * ld_));
+        if (Xinv_) {  // factor_inv (runner.cpp:444-445)
+            rec.pod<uint32_t>(1);
+            write_lower(fetch_d(Xinv_ + (size_t)c * mat_, (size_t)d_ * ld_));
+        } else {
+            rec.pod<uint32_t>(0);
+        }
+        rec.vec(k_.adaptive_ref ? Vec(xr.begin() + (size_t)c * ld_, xr.begin() + (size_t)c * ld_ + d_) : Vec(d_, 0.0));
+        rec.pod<uint64_t>(nctr);
+        rec.pod<uint64_t>(uc[c]);
+        // batch accumulator (empty at a batch boundary unless resumed mid-batch)
+        const auto S = fetch_d(S_ + (size_t)c * mat_, mat_);
+        write_acc(rec, d_, cnt_local_, Vec(mean.begin() + (size_t)c * ld_, mean.begin() + (size_t)c * ld_ + d_),
+                  mirror_lower(S.data(), d_, ld_));
+        // cumulative accumulator
+        Mat cs(d_, d_);
+        if (cS_) {
+            const auto cum = fetch_d(cS_ + (size_t)c * mat_, mat_);
+            cs = mirror_lower(cum.data(), d_, ld_);
+        }
+        write_acc(rec, d_, cum_cnt_, Vec(cm.begin() + (size_t)c * ld_, cm.begin() + (size_t)c * ld_ + d_), cs);
+        rec.vec(beta_hist_[c]);
+        rec.vec(acc_hist_[c]);
+        rec.pod<uint64_t>(fnames_.size());
+        for (size_t f = 0; f < fnames_.size(); ++f) rec.vec(traces_[c][f]);
+    }
+    for (int c = 0; c < C; ++c) ext.vec(Vec(y.begin() + (size_t)c * ld_, y.begin() + (size_t)c * ld_ + d_));
+    std::vector<char> recs = std::move(rec.mem), exts = std::move(ext.mem);
+    if (comm_) {  // a sharded run: every rank's records to rank 0
+        auto all_r = comm_->gather_bytes(recs, stream_);
+        auto all_e = comm_->gather_bytes(exts, stream_);
+        if (rank_ != 0) return;
+        for (int k = 1; k < world_; ++k) {
+            recs.insert(recs.end(), all_r[k].begin(), all_r[k].end());
+            exts.insert(exts.end(), all_e[k].begin(), all_e[k].end());
+        }
+    }
     BinOut w(cfg_.checkpoint_path);
     w.raw(kCkptMagic, 8);
     w.pod<uint32_t>(kVersion);
@@ -158,50 +214,11 @@ void Engine::save_checkpoint(double wall) {
     w.vec(mean_hist_);
     w.vec(psrf_hist_);
 
-    w.pod<uint64_t>((uint64_t)C);
-    const uint64_t nctr = nctr_;
-    for (int c = 0; c < C; ++c) {
-        w.vec(Vec(x.begin() + (size_t)c * ld_, x.begin() + (size_t)c * ld_ + d_));
-        w.pod<double>(lp[c]);
-        w.pod<double>(k_.pcn_form() ? qd[c] : 0.0);
-        w.pod<double>(bt[c]);
-        w.pod<uint64_t>(n_);
-        w.pod<uint64_t>(0);  // n_accepted: reset at every lag boundary
-        const auto L = fetch_d(lptr[c], (size_t)d_ * ld_);
-        w.pod<uint64_t>(d_);
-        for (int i = 0; i < d_; ++i)
-            for (int j = 0; j < d_; ++j) w.pod<double>(j <= i ? L[(size_t)i * ld_ + j] : 0.0);
-        if (Xinv_) {  // factor_inv (runner.cpp:444-445)
-            const auto X = fetch_d(Xinv_ + (size_t)c * mat_, (size_t)d_ * ld_);
-            w.pod<uint32_t>(1);
-            w.pod<uint64_t>(d_);
-            for (int i = 0; i < d_; ++i)
-                for (int j = 0; j < d_; ++j) w.pod<double>(j <= i ? X[(size_t)i * ld_ + j] : 0.0);
-        } else {
-            w.pod<uint32_t>(0);
-        }
-        w.vec(k_.adaptive_ref ? Vec(xr.begin() + (size_t)c * ld_, xr.begin() + (size_t)c * ld_ + d_) : Vec(d_, 0.0));
-        w.pod<uint64_t>(nctr);
-        w.pod<uint64_t>(uc[c]);
-        // batch accumulator (empty at a batch boundary unless resumed mid-batch)
-        const auto S = fetch_d(S_ + (size_t)c * mat_, mat_);
-        write_acc(w, d_, cnt_local_, Vec(mean.begin() + (size_t)c * ld_, mean.begin() + (size_t)c * ld_ + d_),
-                  mirror_lower(S.data(), d_, ld_));
-        // cumulative accumulator
-        Mat cs(d_, d_);
-        if (cS_) {
-            const auto cum = fetch_d(cS_ + (size_t)c * mat_, mat_);
-            cs = mirror_lower(cum.data(), d_, ld_);
-        }
-        write_acc(w, d_, cum_cnt_, Vec(cm.begin() + (size_t)c * ld_, cm.begin() + (size_t)c * ld_ + d_), cs);
-        w.vec(beta_hist_[c]);
-        w.vec(acc_hist_[c]);
-        w.pod<uint64_t>(fnames_.size());
-        for (size_t f = 0; f < fnames_.size(); ++f) w.vec(traces_[c][f]);
-    }
+    w.pod<uint64_t>((uint64_t)P_);
+    w.raw(recs.data(), recs.size());
     // B200 extension: the recursively carried y
     w.raw(kExtMagic, 8);
-    for (int c = 0; c < C; ++c) w.vec(Vec(y.begin() + (size_t)c * ld_, y.begin() + (size_t)c * ld_ + d_));
+    w.raw(exts.data(), exts.size());
     w.close();
 }
 
@@ -235,8 +252,9 @@ void Engine::read_checkpoint_header(BinIn& r, HostTarget& t, RunCfg& cfg) {
 }
 
 void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
+    // a sharded engine (rank r of N) reads every chain's record and keeps its own
+    // [c0, c0 + C); the shared state (global moments, histories) is the same for every rank
     const int C = C_;
-    require(world_ == 1 && C == P_, Err::InvalidArgument, "resuming a multi-GPU run is not supported yet");
     batches_done_ = r.pod<uint64_t>();
     r.pod<uint64_t>();  // global.batches
     cnt_g_ = r.pod<uint64_t>();
@@ -248,7 +266,7 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
     cov_hist_ = r.vec();
     mean_hist_ = r.vec();
     psrf_hist_ = r.vec();
-    require(r.pod<uint64_t>() == (uint64_t)C, Err::Io, "checkpoint chain count mismatch");
+    require(r.pod<uint64_t>() == (uint64_t)P_, Err::Io, "checkpoint chain count mismatch");
 
     auto put = [&](double* dst, const double* src, size_t n) {
         DGB_CUDA(cudaMemcpy(dst, src, n * 8, cudaMemcpyHostToDevice));
@@ -271,50 +289,70 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
     std::vector<double*> lptr(C);
     DGB_CUDA(cudaMemcpy(lptr.data(), Lp_, C * sizeof(double*), cudaMemcpyDeviceToHost));
     bool all_identity = true, need_inverse = false;
-    for (int c = 0; c < C; ++c) {
+    for (int pg = 0; pg < P_; ++pg) {
+        const bool mine = pg >= c0_ && pg < c0_ + C;
+        const int c = mine ? pg - c0_ : 0;
         std::vector<double> row(ld_, 0.0);
         const Vec x = r.vec();
         require(x.size() == (size_t)d_, Err::Io, "corrupt checkpoint: state");
         std::copy(x.begin(), x.end(), row.begin());
-        put(x_ + (size_t)c * ld_, row.data(), ld_);
-        lp[c] = r.pod<double>();
-        qd[c] = r.pod<double>();
-        bt[c] = r.pod<double>();
+        if (mine) put(x_ + (size_t)c * ld_, row.data(), ld_);
+        const double lpv = r.pod<double>(), qdv = r.pod<double>(), btv = r.pod<double>();
+        if (mine) {
+            lp[c] = lpv;
+            qd[c] = qdv;
+            bt[c] = btv;
+        }
         const uint64_t nc = r.pod<uint64_t>();
-        require(c == 0 || nc == n, Err::Io, "chains at different iteration counts");
+        require(pg == 0 || nc == n, Err::Io, "chains at different iteration counts");
         n = nc;
         r.pod<uint64_t>();  // n_accepted
         const uint64_t dim = r.pod<uint64_t>();
         require(dim == (uint64_t)d_, Err::Io, "corrupt checkpoint: factor");
-        Mat L(d_, d_);
-        r.raw(L.a.data(), L.a.size() * 8);
-        for (int i = 0; i < d_ && all_identity; ++i)
-            for (int j = 0; j <= i; ++j)
-                if (L(i, j) != (i == j ? 1.0 : 0.0)) {
-                    all_identity = false;
-                    break;
-                }
-        put_lower(lptr[c], L);
+        if (mine) {
+            Mat L(d_, d_);
+            r.raw(L.a.data(), L.a.size() * 8);
+            for (int i = 0; i < d_ && all_identity; ++i)
+                for (int j = 0; j <= i; ++j)
+                    if (L(i, j) != (i == j ? 1.0 : 0.0)) {
+                        all_identity = false;
+                        break;
+                    }
+            put_lower(lptr[c], L);
+        } else {
+            r.skip((size_t)d_ * d_ * 8);
+        }
         if (r.pod<uint32_t>() != 0) {  // factor_inv (runner.cpp:186)
             require(r.pod<uint64_t>() == (uint64_t)d_, Err::Io, "corrupt checkpoint: inverse factor");
-            Mat X(d_, d_);
-            r.raw(X.a.data(), X.a.size() * 8);
-            if (Xinv_) put_lower(Xinv_ + (size_t)c * mat_, X);
+            if (mine) {
+                Mat X(d_, d_);
+                r.raw(X.a.data(), X.a.size() * 8);
+                if (Xinv_) put_lower(Xinv_ + (size_t)c * mat_, X);
+            } else {
+                r.skip((size_t)d_ * d_ * 8);
+            }
         } else if (Xinv_) {  // a file without the inverse: recomputed below from the factor
             need_inverse = true;
         }
         const Vec xr = r.vec();
         std::fill(row.begin(), row.end(), 0.0);
         std::copy(xr.begin(), xr.end(), row.begin());
-        put(xr_ + (size_t)c * ld_, row.data(), ld_);
+        if (mine) put(xr_ + (size_t)c * ld_, row.data(), ld_);
         const uint64_t nc_ctr = r.pod<uint64_t>();
-        require(c == 0 || nc_ctr == nctr, Err::Io, "chains at different noise-stream positions");
+        require(pg == 0 || nc_ctr == nctr, Err::Io, "chains at different noise-stream positions");
         nctr = nc_ctr;
-        uc[c] = r.pod<uint64_t>();
+        const uint64_t ucv = r.pod<uint64_t>();
+        if (mine) uc[c] = ucv;
         for (int which = 0; which < 2; ++which) {  // batch, then cumulative accumulator
             r.pod<uint64_t>();
             const uint64_t cnt = r.pod<uint64_t>();
             const Vec m = r.vec();
+            if (!mine) {
+                r.skip_mat();
+                if (which == 0) cnt_local = cnt;
+                else cum = cnt;
+                continue;
+            }
             const Mat s = r.mat();
             std::fill(row.begin(), row.end(), 0.0);
             std::copy(m.begin(), m.end(), row.begin());
@@ -331,11 +369,16 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
                 if (cS_) put_lower(cS_ + (size_t)c * mat_, s);
             }
         }
-        beta_hist_[c] = r.vec();
-        acc_hist_[c] = r.vec();
+        Vec bh = r.vec(), ah = r.vec();
         const uint64_t nf = r.pod<uint64_t>();
         require(nf == fnames_.size(), Err::Io, "checkpoint functional count mismatch");
-        for (size_t f = 0; f < nf; ++f) traces_[c][f] = r.vec();
+        std::vector<Vec> tr(nf);
+        for (size_t f = 0; f < nf; ++f) tr[f] = r.vec();
+        if (mine) {
+            beta_hist_[c] = std::move(bh);
+            acc_hist_[c] = std::move(ah);
+            for (size_t f = 0; f < nf; ++f) traces_[c][f] = std::move(tr[f]);
+        }
     }
     put(logpi_, lp.data(), C);
     put(quad_, qd.data(), C);
@@ -357,11 +400,12 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
         char magic[8];
         r.raw(magic, 8);
         if (std::memcmp(magic, kExtMagic, 8) == 0) {
-            for (int c = 0; c < C; ++c) {
+            for (int pg = 0; pg < P_; ++pg) {
                 const Vec y = r.vec();
+                if (pg < c0_ || pg >= c0_ + C) continue;
                 std::vector<double> row(ld_, 0.0);
                 std::copy(y.begin(), y.end(), row.begin());
-                put(y_ + (size_t)c * ld_, row.data(), ld_);
+                put(y_ + (size_t)(pg - c0_) * ld_, row.data(), ld_);
             }
             have_y = true;
         }

@@ -3,6 +3,7 @@
 
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <cstdio>
@@ -33,6 +34,7 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     std::string err;
@@ -49,9 +51,10 @@ struct NcclApi {
         CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
         AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
         AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+        Broadcast = (decltype(Broadcast))dlsym(h, "ncclBroadcast");
         CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
         GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
-        if (!GetUniqueId || !CommInitRank || !AllReduce || !AllGather || !CommDestroy) {
+        if (!GetUniqueId || !CommInitRank || !AllReduce || !AllGather || !Broadcast || !CommDestroy) {
             err = "libnccl.so.2 lacks expected symbols";
             h = nullptr;
             return false;
@@ -82,6 +85,9 @@ struct NcclComm final : Comm {
     }
     void allgather(const double* src, double* dst, int64_t cnt, cudaStream_t s) override {
         api().check(api().AllGather(src, dst, (size_t)cnt, ncclFloat64, comm, s), "allgather");
+    }
+    void broadcast(double* buf, int64_t cnt, int root, cudaStream_t s) override {
+        api().check(api().Broadcast(buf, buf, (size_t)cnt, ncclFloat64, root, comm, s), "broadcast");
     }
 };
 
@@ -136,6 +142,19 @@ struct ThreadComm final : Comm {
         DGB_CUDA(cudaStreamSynchronize(s));
         sh->barrier();
     }
+    void broadcast(double* buf, int64_t cnt, int root, cudaStream_t s) override {
+        if (r == root) {
+            sh->stage[root].resize(cnt);
+            DGB_CUDA(cudaMemcpyAsync(sh->stage[root].data(), buf, cnt * 8, cudaMemcpyDeviceToHost, s));
+            DGB_CUDA(cudaStreamSynchronize(s));
+        }
+        sh->barrier();
+        if (r != root) {
+            DGB_CUDA(cudaMemcpyAsync(buf, sh->stage[root].data(), cnt * 8, cudaMemcpyHostToDevice, s));
+            DGB_CUDA(cudaStreamSynchronize(s));
+        }
+        sh->barrier();
+    }
 };
 
 }  // namespace
@@ -157,6 +176,51 @@ bool Comm::any(bool flag, cudaStream_t s) {
     DGB_CUDA(cudaMemcpyAsync(&h, scratch_, sizeof(double), cudaMemcpyDeviceToHost, s));
     DGB_CUDA(cudaStreamSynchronize(s));
     return h > 0.5;
+}
+
+std::vector<std::vector<char>> Comm::gather_bytes(const std::vector<char>& mine, cudaStream_t s) {
+    const int n = size(), me = rank();
+    constexpr int64_t kChunk = 8ll << 20;  // doubles per broadcast (64 MB)
+    double* dev = nullptr;
+    DGB_CUDA(cudaMalloc(&dev, (size_t)std::max<int64_t>(n, kChunk) * sizeof(double)));
+    std::vector<double> sizes(n);
+    {
+        double* one = dev + kChunk - 1;  // any spare slot for this rank's size
+        const double v = (double)mine.size();
+        DGB_CUDA(cudaMemcpyAsync(one, &v, sizeof(double), cudaMemcpyHostToDevice, s));
+        double* all = nullptr;
+        DGB_CUDA(cudaMalloc(&all, n * sizeof(double)));
+        allgather(one, all, 1, s);
+        DGB_CUDA(cudaMemcpyAsync(sizes.data(), all, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        DGB_CUDA(cudaStreamSynchronize(s));
+        cudaFree(all);
+    }
+    std::vector<std::vector<char>> out;
+    if (me == 0) {
+        out.resize(n);
+        out[0] = mine;
+    }
+    std::vector<double> host(kChunk);
+    for (int k = 1; k < n; ++k) {
+        const int64_t bytes = (int64_t)sizes[k];
+        if (me == 0) out[k].resize((size_t)bytes);
+        for (int64_t off = 0; off < bytes; off += kChunk * 8) {
+            const int64_t nb = std::min<int64_t>(kChunk * 8, bytes - off), nd = (nb + 7) / 8;
+            if (me == k) {
+                std::memcpy(host.data(), mine.data() + off, (size_t)nb);
+                DGB_CUDA(cudaMemcpyAsync(dev, host.data(), nd * 8, cudaMemcpyHostToDevice, s));
+            }
+            broadcast(dev, nd, k, s);
+            if (me == 0) {
+                DGB_CUDA(cudaMemcpyAsync(host.data(), dev, nd * 8, cudaMemcpyDeviceToHost, s));
+                DGB_CUDA(cudaStreamSynchronize(s));
+                std::memcpy(out[k].data() + off, host.data(), (size_t)nb);
+            }
+        }
+    }
+    DGB_CUDA(cudaStreamSynchronize(s));
+    cudaFree(dev);
+    return out;
 }
 
 std::vector<std::shared_ptr<Comm>> make_thread_comms(int world) {

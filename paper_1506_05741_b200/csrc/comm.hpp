@@ -23,6 +23,12 @@ struct Comm {
     virtual void allreduce_sum(double* buf, int64_t n, cudaStream_t s) = 0;
     // dst holds size()*n doubles, rank r's block at r*n
     virtual void allgather(const double* src, double* dst, int64_t n, cudaStream_t s) = 0;
+    // buf (n doubles, device) of rank `root` to every rank
+    virtual void broadcast(double* buf, int64_t n, int root, cudaStream_t s) = 0;
+    // Host byte blobs of every rank to rank 0, in rank order (every rank calls it; the other
+    // ranks get an empty result). Staged through the device in 64 MB broadcasts: the
+    // checkpoint of a sharded run (Engine::save_checkpoint).
+    std::vector<std::vector<char>> gather_bytes(const std::vector<char>& mine, cudaStream_t s);
     // Collective OR of a host flag (every rank must call it at the same point): the
     // engine's stop decisions and rank-local failures go through it, so all ranks leave
     // the batch loop together instead of one rank waiting in a collective forever.

@@ -45,10 +45,16 @@ struct Mat {
 struct BinOut {
     std::ofstream f;
     std::string path;
+    std::vector<char> mem;  // memory mode (no path): the bytes a rank contributes to a file
+    bool to_mem = false;
     explicit BinOut(const std::string& p) : f(p, std::ios::binary), path(p) {
         require(f.good(), Err::Io, "cannot open for writing: " + p);
     }
-    void raw(const void* p, size_t n) { f.write(static_cast<const char*>(p), (std::streamsize)n); }
+    BinOut() : to_mem(true) {}
+    void raw(const void* p, size_t n) {
+        if (to_mem) mem.insert(mem.end(), static_cast<const char*>(p), static_cast<const char*>(p) + n);
+        else f.write(static_cast<const char*>(p), (std::streamsize)n);
+    }
     template <class T>
     void pod(T v) {
         raw(&v, sizeof v);
@@ -67,6 +73,7 @@ struct BinOut {
         raw(s.data(), s.size());
     }
     void close() {
+        if (to_mem) return;
         f.flush();
         require(f.good(), Err::Io, "write failed: " + path);
         f.close();
@@ -98,6 +105,15 @@ struct BinIn {
         Vec v(count());
         raw(v.data(), v.size() * 8);
         return v;
+    }
+    void skip(size_t n) {
+        f.seekg((std::streamoff)n, std::ios::cur);
+        require(f.good(), Err::Io, "truncated file: " + path);
+    }
+    void skip_vec() { skip(count() * 8); }
+    void skip_mat() {
+        const size_t r = count(), c = count();
+        skip(r * c * 8);
     }
     Mat mat() {
         const size_t r = count(), c = count();

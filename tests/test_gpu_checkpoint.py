@@ -78,3 +78,37 @@ def test_explicit_inverse_checkpoint(b200, ref_abi, tmp_path):
     _same(full, b200.resume(ck, b200.options(max_batches=4)), 3)
     r_ref = ref_abi.resume(ck2, ref_abi.options(max_batches=3))
     assert r_ref.batches == 3 and np.isfinite(r_ref.final_cov_error)
+
+
+def _close(r0, r1, chains):
+    """A sharded run against the single engine: per-chain decisions identical, pooled moments
+    to rounding (the merge sums in a different order)."""
+    assert r0.batches == r1.batches and r0.total_samples == r1.total_samples
+    for p in range(chains):
+        assert np.array_equal(r0.chain_history(p, "beta"), r1.chain_history(p, "beta")), p
+        assert np.array_equal(r0.chain_history(p, "acceptance"), r1.chain_history(p, "acceptance")), p
+    assert np.linalg.norm(r0.cov() - r1.cov()) <= 1e-12 * np.linalg.norm(r0.cov())
+    assert np.linalg.norm(r0.mean() - r1.mean()) <= 1e-12 * max(1.0, np.linalg.norm(r0.mean()))
+    assert np.allclose(r0.history("cov_error"), r1.history("cov_error"), rtol=1e-10)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_checkpoint_resume(b200, ref_abi, tmp_path, world):
+    # a run sharded over `world` ranks (in-process exchange, uneven shards for 3) checkpoints
+    # into ONE reference-format file written by rank 0 (runner.cpp:398-457 for any P); the
+    # file resumes on one engine, on `world` ranks again, and in the reference library
+    import shutil
+    t = b200.target_build("pi2", 24, 6)
+    kw = dict(kernel="diam", chains=5, intervals_per_batch=2, n_lag=30, n0=20, master_seed=12)
+    full = b200.sample(t, max_batches=4, **kw)
+    ck = str(tmp_path / "shard.ckpt")
+    part = b200.sample_threads(t, world, max_batches=2, checkpoint_path=ck, **kw)
+    assert part.batches == 2 and part.chains == 5
+    copies = []
+    for i in range(3):
+        copies.append(str(tmp_path / f"c{i}.ckpt"))
+        shutil.copy(ck, copies[-1])
+    _close(full, b200.resume(copies[0], b200.options(max_batches=4)), 5)
+    _close(full, b200.resume_threads(copies[1], world, b200.options(max_batches=4)), 5)
+    r_ref = ref_abi.resume(copies[2], ref_abi.options(max_batches=3))
+    assert r_ref.batches == 3 and np.isfinite(r_ref.final_cov_error)
