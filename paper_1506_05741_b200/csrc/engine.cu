@@ -798,7 +798,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     timed_begin(s);
     for (int rep = (twice_ & kTwiceNormals) ? 2 : 1; rep > 0; --rep)
         launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, rows, d_, ld_, nkeys_ + o,
-                   p.nctr + (uint64_t)r0 * d_, beta_ + o, infl, s);
+                       p.nctr + (uint64_t)r0 * d_, beta_ + o, infl, s);
     timed_end("normals", 0.0, s);
     if (!p.identity) {
         GemmBatch t{};
