@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <set>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -45,15 +46,19 @@ namespace {
 // between runs (release threshold = max): a second diam_sample on the same GPU reuses
 // the first one's HBM instead of paying cudaMalloc/cudaFree for gigabytes again.
 void keep_pool_resident() {
-    static bool done = false;
-    if (done) return;
+    // per device (the attribute belongs to the device's default pool); engines of several
+    // rank threads may get here concurrently
+    static std::mutex mu;
+    static std::set<int> done;
     int dev = 0;
     DGB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(dev)) return;
     cudaMemPool_t pool;
     DGB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t keep = ~0ull;
     DGB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    done = true;
+    done.insert(dev);
 }
 
 // While an engine is being built, allocations are zeroed on stream 0 without a sync
@@ -382,7 +387,24 @@ void Engine::upload_target() {
         DGB_CUDA(cudaMemcpy(inv_eig_, ie.data(), ld_ * 8, cudaMemcpyHostToDevice));
         DGB_CUDA(cudaMemcpy(bcoef_, bc.data(), ld_ * 8, cudaMemcpyHostToDevice));
     } else {
-        upload_padded(G_, ld_, tgt_.precision);
+        // whitened form: G lower with G^T G = P, log pi(x) = -1/2 |G x|^2 -- every target is
+        // then -1/2 sum_i twist(G x)_i^2 / sigma_i^2 (Gaussian: sigma = 1, no twist), and the
+        // window's target product is triangular
+        Mat rev(d_, d_);
+        for (int i = 0; i < d_; ++i)
+            for (int j = 0; j < d_; ++j) rev(i, j) = tgt_.precision(d_ - 1 - i, d_ - 1 - j);
+        double* prev = nullptr;
+        DGB_CUDA(cudaMalloc(&prev, (size_t)mat_ * sizeof(double)));
+        upload_padded(prev, ld_, rev);
+        whitening_factor(prev, G_, d_, ld_, stream_);
+        cudaFree(prev);
+        std::vector<double> ie(ld_, 0.0), bc(ld_, 0.0);
+        for (int i = 0; i < d_; ++i) ie[i] = 1.0;
+        inv_eig_ = dalloc<double>(A, ld_);
+        bcoef_ = dalloc<double>(A, ld_);
+        DGB_CUDA(cudaMemcpy(inv_eig_, ie.data(), ld_ * 8, cudaMemcpyHostToDevice));
+        DGB_CUDA(cudaMemcpy(bcoef_, bc.data(), ld_ * 8, cudaMemcpyHostToDevice));
+        tri_target_ = true;
     }
     Ct_ = dalloc<double>(A, (size_t)d_ * d_);
     DGB_CUDA(cudaMemcpy(Ct_, tgt_.covariance.a.data(), (size_t)d_ * d_ * 8, cudaMemcpyHostToDevice));
@@ -486,7 +508,7 @@ void Engine::init_chains() {
     identity_ = true;
     // log pi(x0), quad(x0) (proposal.cpp:107-108)
     refresh_g(x_, g_, C, stream_);
-    launch_eval_logpi(x_, g_, inv_eig_, bcoef_, twisted_, logpi_, C, d_, ld_, stream_);
+    launch_eval_logpi(x_, g_, inv_eig_, bcoef_, true, logpi_, C, d_, ld_, stream_);  // whitened form
     if (k_.pcn_form()) {
         const double infl = k_.noise_infl();
         if (Xinv_) launch_trmv_quad(Xinvp_, ld_, x_, nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl), stream_);
@@ -619,9 +641,12 @@ const std::map<std::string, KernelStat>& Engine::stats() {
 
 double Engine::flops_per_batch() const {
     // algorithmic FP64 flops of one batch over the local chains:
-    // TRMM d(d+1) per row, target GEMM 2 d^2 per row, SYRK d(d+1) per row, POTRF d^3/3 per window
+    // TRMM d(d+1) per row, target product d(d+1) per row (whitened Gaussian: triangular G) or
+    // 2 d^2 (twisted: V^T), SYRK d(d+1) per row (bench.py scales it to the distinct rows),
+    // POTRF d^3/3 per window
     const double d = d_, L = Lw_, C = C_, M = (double)cfg_.intervals_per_batch;
-    const double per_window = C * (L * d * (d + 1) + L * 2.0 * d * d + L * d * (d + 1) + d * d * d / 3.0);
+    const double tgt = tri_target_ ? d * (d + 1) : 2.0 * d * d;
+    const double per_window = C * (L * d * (d + 1) + L * tgt + L * d * (d + 1) + d * d * d / 3.0);
     return per_window * M;
 }
 
@@ -829,6 +854,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         h.K = d_;
         h.alpha = 1.0;
         h.beta = 0.0;
+        h.tri_b_lower = tri_target_ ? 1 : 0;  // whitened Gaussian: G lower, K clipped per tile
         if (rows == Lc_) {
             h.A = (const double* const*)g.Xib;
             h.C = g.Hb;
@@ -885,7 +911,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     // the previous batch's trace copies read the buffers the MH steps write
     if (merge_pending_ && p.record) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
     timed_begin(s);
-    launch_mh_window(sp, twisted_, s);
+    launch_mh_window(sp, true, s);  // every target in whitened form: -1/2 sum twist(G x)^2 / sigma^2
     timed_end("mh_window", 0.0, s);
     if (capture_) capture_chunk(g, r0, rows);
 

@@ -190,6 +190,10 @@ private:
     int64_t ld_ = 0, win_ = 0, mat_ = 0;
     int64_t fmat_ = 0;  // factor stride: d rows + the augmented row r = x - x_ref
     bool twisted_ = false, identity_ = true;
+    // Gaussian targets are stepped in whitened form: G = a lower-triangular factor of the
+    // precision (G^T G = P), log pi(x) = -1/2 |G x|^2 -- the target product H = Xi G^T is
+    // then triangular (half the flops of the full product with P)
+    bool tri_target_ = false;
     cudaStream_t stream_ = nullptr;
     int stream_prio_ = 0;
     cudaEvent_t main_ev_ = nullptr;

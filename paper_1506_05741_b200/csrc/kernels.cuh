@@ -135,6 +135,9 @@ struct PotrfWork {
 inline size_t potrf_work_doubles(int chains) { return (size_t)chains * 128 * 128 + chains; }
 void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status,
                    PotrfWork& w, cudaStream_t s, int extra_rows = 0);
+// G (lower, G^T G = P) from the precision reversed in P_rev (J P J, overwritten by its
+// factor); the whitened Gaussian target of the engine (Engine::upload_target)
+void whitening_factor(double* P_rev, double* G, int d, int64_t ld, cudaStream_t s);
 // q_c = half_inv_infl2 * |row d of L_c|^2 (the augmented row = L^{-1}(x - x_ref))
 void launch_aug_quad(double* const* L, int64_t ld, int d, int chains, double half_inv_infl2, const int* mask,
                      double* q, cudaStream_t s);

@@ -362,6 +362,9 @@ constexpr int kNb = kDiagNb;
 // its left (diag64_tc_sc's pre_L); 2 = those columns still need their solve against the
 // inverse at inv_base + c inv_stride (pre_X). The inverse goes to inv_base + c inv_stride +
 // inv_off.
+using X21Tile = tile::Cfg<64, 64, 32, 2, true, false, 2, 4, 1>;  // X21's two 64 x 64 products (8 warps)
+static_assert(X21Tile::SMEM_BYTES <= (int)sizeof(DiagTcScratch), "X21 products reuse the diagonal scratch");
+
 __global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
                                                             const int* mask, int* status, int* active,
                                                             double* inv_base, int zero_above, int pre = 0,
@@ -373,40 +376,42 @@ __global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, i
     if (!run) return;
     double* Ab = Am[c] + (int64_t)j0 * ld + j0;
     double* out = inv_base + (int64_t)c * inv_stride + inv_off;
-    const int bad = diag64_tc_sc(*reinterpret_cast<DiagTcScratch*>(dyn_smem), Ab, ld, jb, out, zero_above, kNb,
-                                 pre ? Ab - kNb : nullptr, pre == 2 ? inv_base + (int64_t)c * inv_stride : nullptr);
-
-    if (bad && threadIdx.x == 0) {
-        status[c] = 1;
-        active[c] = 0;
+    // the chain's 128 x 128 inverse slot X_J (row stride 128): X11 at [0, 0), X22 at [64, 64)
+    double* xj = inv_base + (int64_t)c * inv_stride;
+    const int bad = diag64_tc_sc(*reinterpret_cast<DiagTcScratch*>(dyn_smem), Ab, ld, jb, out, zero_above, kD2,
+                                 pre ? Ab - kNb : nullptr, pre == 2 ? xj : nullptr, kD2);
+    if (bad) {
+        if (threadIdx.x == 0) {
+            status[c] = 1;
+            active[c] = 0;
+        }
+        return;
+    }
+    if (pre == 2) {
+        // X21 = -X22 (L21 X11), completing X_J = L_JJ^{-1} for the block column's one 128-deep
+        // TRSM: T = L21 X11 into X21's place, then in place (L21 was solved by this CTA)
+        __threadfence_block();
+        tile::gemm_tile<X21Tile, true, false>(Ab - kNb, xj, xj + kNb * kD2, ld, kD2, kD2, jb, kNb, kNb, 0, 0, 1.0, 0.0,
+                                              false, dyn_smem);
+        __threadfence_block();
+        tile::gemm_tile<X21Tile, true, false>(xj + kNb * kD2 + kNb, xj + kNb * kD2, xj + kNb * kD2, kD2, kD2, kD2, jb,
+                                              kNb, jb, 0, 0, -1.0, 0.0, false, dyn_smem);
     }
 }
 
-// tile configuration of potrf_solve3_kernel (the cp.async DMMA tile, two CTAs per SM)
-using FusedTile = tile::Cfg<128, 64, 32, 2, true, true, 4, 2, 2>;
+// The rows below a block column's diagonal block: L[r, J] = A[r, J] X_J^T, one 128-deep
+// triangular DMMA product per 64-row tile (B(k, n) = X_J[n][k] = 0 for k > n), in place:
+// a CTA owns all of J's columns for its rows, so it reads its whole A tile before writing.
+using TrsmTile = tile::Cfg<64, 128, 32, 2, true, true, 2, 4, 2>;  // 8 warps of 32 x 32, 2 CTAs / SM
 
-// Everything below a 128-wide block column's diagonal block in one pass per 128-row tile
-// (rows r): L[r, J1] = A[r, J1] X11^T, T = A[r, J2] - L[r, J1] L[J2, J1]^T,
-// L[r, J2] = T X22^T -- three DMMA tile products in one CTA, each stored before the next
-// reads it (X11 at inv[c], X22 at inv[c] + 64 x 64).
-__global__ void __launch_bounds__(256, 2) potrf_solve3_kernel(double* const* Am, int64_t ld, int r0, int c0,
-                                                              int rows, int n2, const int* active,
-                                                              double* const* inv) {
+__global__ void __launch_bounds__(256, 2) potrf_trsm_kernel(double* const* Am, int64_t ld, int r0, int c0, int rows,
+                                                            int nb, const int* active, double* const* inv) {
     const int c = blockIdx.z;
     if (!active[c]) return;
     extern __shared__ __align__(16) double smem[];
-    const int m0 = blockIdx.y * FusedTile::BM;
-    double* A = Am[c];
-    double* l1 = A + (int64_t)r0 * ld + c0;
-    double* t2 = l1 + kNb;
-    tile::gemm_tile<FusedTile, true, true>(l1, inv[c], l1, ld, kNb, ld, rows, kNb, kNb, m0, 0, 1.0, 0.0, false, smem,
-                                           true);
-    __threadfence_block();
-    tile::gemm_tile<FusedTile, true, true>(l1, A + (int64_t)(c0 + kNb) * ld + c0, t2, ld, ld, ld, rows, n2, kNb, m0, 0,
-                                           -1.0, 1.0, false, smem);
-    __threadfence_block();
-    tile::gemm_tile<FusedTile, true, true>(t2, inv[c] + kNb * kNb, t2, ld, kNb, ld, rows, n2, n2, m0, 0, 1.0, 0.0,
-                                           false, smem, true);
+    double* a = Am[c] + (int64_t)r0 * ld + c0;
+    tile::gemm_tile<TrsmTile, true, true>(a, inv[c], a, ld, kD2, ld, rows, nb, nb, blockIdx.y * TrsmTile::BM, 0, 1.0,
+                                          0.0, false, smem, true);
 }
 
 __global__ void aug_quad_kernel(double* const* Lm, int64_t ld, int d, double hq, const int* mask, double* q) {
@@ -833,19 +838,20 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
     //   (2) the first 64x64 diagonal block: L11 = chol, X11 = L11^-1 (one CTA per chain,
     //       shared memory, diag_tc.cuh)
     //   (3) the second one: its rows of the first half-column solved against X11 and their
-    //       64-deep update applied first, then L22, X22
-    //   (4) everything below (potrf_solve3_kernel): L[r, J1] = A[r, J1] X11^T, the 64-deep
-    //       update, L[r, J2] = T X22^T as three chained DMMA tile products per 128-row tile
+    //       64-deep update applied first, then L22, X22, and X21 = -X22 L21 X11, so the
+    //       chain's slot holds X_J = L_JJ^{-1} (128 x 128)
+    //   (4) everything below (potrf_trsm_kernel): L[r, J] = A[r, J] X_J^T, one 128-deep
+    //       triangular DMMA product per 64-row tile, in place
     // A last block column of width <= 64 is a diagonal block + one TRSM GEMM.
     // `extra_rows` augmented rows r^T below row d-1 ride along as ordinary rows of the
     // GEMMs and TRSMs and come out as (L^{-1} r)^T: the forward substitution of the
     // usable-factor guard (proj/src/proposal.cpp:185-199) costs no extra pass over L.
-    // w.inv holds chains*128*128 doubles, followed by an int active[chains]
+    // w.inv holds chains*128*128 doubles (X_J per chain), followed by an int active[chains]
     int* active = reinterpret_cast<int*>(w.inv + (int64_t)chains * kD2 * kD2);
 
     const int rows = d + extra_rows;
     set_smem_attr(reinterpret_cast<const void*>(potrf_diag_kernel), (int)sizeof(DiagTcScratch));
-    set_smem_attr(reinterpret_cast<const void*>(potrf_solve3_kernel), FusedTile::SMEM_BYTES);
+    set_smem_attr(reinterpret_cast<const void*>(potrf_trsm_kernel), TrsmTile::SMEM_BYTES);
     for (int j0 = 0; j0 < d; j0 += 2 * kNb) {
         const int jb = std::min(2 * kNb, d - j0);
         if (j0 > 0) {
@@ -882,12 +888,12 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
             if (rest <= 0) continue;
             GemmBatch t{};
             t.A = (const double* const*)A;
-            t.B = (const double* const*)w.inv128_ptrs;  // X11 with stride 64 at the slot start
+            t.B = (const double* const*)w.inv128_ptrs;  // X11 at the slot start (row stride 128)
             t.C = A;
             t.a_off = (int64_t)(j0 + jb) * ld + j0;
             t.c_off = t.a_off;
             t.lda = ld;
-            t.ldb = kNb;
+            t.ldb = kD2;
             t.ldc = ld;
             t.M = rest;
             t.N = jb;
@@ -900,19 +906,54 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
         }
         const int c1 = j0 + kNb, n2 = jb - kNb;
         potrf_diag_kernel<<<chains, 256, sizeof(DiagTcScratch), s>>>(A, ld, c1, n2, mask, status, active, w.inv,
-                                                                      j0 > 0 ? 1 : 0, 2, kD2 * kD2, kNb * kNb);
+                                                                      j0 > 0 ? 1 : 0, 2, kD2 * kD2, kNb * kD2 + kNb);
         DGB_LAUNCH_CHECK();
         count_launch();
         const int rest = rows - c1 - n2;
         if (rest <= 0) continue;
-        dim3 grid(1, (unsigned)ceil_div(rest, FusedTile::BM), (unsigned)chains);
-        potrf_solve3_kernel<<<grid, 256, FusedTile::SMEM_BYTES, s>>>(A, ld, c1 + n2, j0, rest, n2, active,
-                                                                     w.inv128_ptrs);
+        dim3 grid(1, (unsigned)ceil_div(rest, TrsmTile::BM), (unsigned)chains);
+        potrf_trsm_kernel<<<grid, 256, TrsmTile::SMEM_BYTES, s>>>(A, ld, c1 + n2, j0, rest, jb, active,
+                                                                  w.inv128_ptrs);
         DGB_LAUNCH_CHECK();
         count_launch();
     }
 }
 
+
+// G[i][j] = F[d-1-j][d-1-i] (j <= i), zero above: from the Cholesky factor F of the reversed
+// precision J P J = F F^T, G = (J F J)^T is lower triangular with G^T G = P
+__global__ void reverse_factor_kernel(const double* F, double* G, int d, int64_t ld) {
+    const int i = blockIdx.x;
+    for (int j = threadIdx.x; j < ld; j += blockDim.x)
+        G[(int64_t)i * ld + j] = (j <= i && j < d) ? F[(int64_t)(d - 1 - j) * ld + (d - 1 - i)] : 0.0;
+}
+
+void whitening_factor(double* P_rev, double* G, int d, int64_t ld, cudaStream_t s) {
+    // P_rev: the reversed precision (lower part used), factored in place
+    double** pa = nullptr;
+    int* status = nullptr;
+    double* inv = nullptr;
+    double** invp = nullptr;
+    DGB_CUDA(cudaMalloc(&pa, 2 * sizeof(double*)));
+    invp = pa + 1;
+    DGB_CUDA(cudaMalloc(&status, sizeof(int)));
+    DGB_CUDA(cudaMalloc(&inv, potrf_work_doubles(1) * sizeof(double)));
+    DGB_CUDA(cudaMemcpyAsync(pa, &P_rev, sizeof(double*), cudaMemcpyHostToDevice, s));
+    DGB_CUDA(cudaMemcpyAsync(invp, &inv, sizeof(double*), cudaMemcpyHostToDevice, s));
+    DGB_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
+    PotrfWork w{inv, invp};
+    potrf_batched(pa, ld, d, 1, nullptr, status, w, s, 0);
+    reverse_factor_kernel<<<d, 256, 0, s>>>(P_rev, G, d, ld);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+    int st = 0;
+    DGB_CUDA(cudaMemcpyAsync(&st, status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DGB_CUDA(cudaStreamSynchronize(s));
+    cudaFree(inv);
+    cudaFree(status);
+    cudaFree(pa);
+    if (st != 0) throw CudaError("target precision is not positive definite");
+}
 
 void launch_aug_quad(double* const* L, int64_t ld, int d, int chains, double half_inv_infl2, const int* mask,
                      double* q, cudaStream_t s) {
