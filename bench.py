@@ -127,9 +127,9 @@ def run_options(cfg, chains, **over):
     return o
 
 
-def ncu_gemm_traffic(cfg_name, chains, d, n_lag):
+def ncu_gemm_traffic(cfg_name, chains, d, n_lag, distinct=1.0):
     """DRAM bytes per launch of the three DMMA GEMM classes from the committed `ncu --set
-    full` captures (profiles/r01_ncu_<class>.csv, tools/ncu_capture.sh: d=1024, 64 chains),
+    full` captures (profiles/r02_ncu_<class>.csv, tools/ncu_capture.sh: d=1024, 64 chains),
     against their algorithmic bytes (operands in once, results out once)."""
     import csv
     if cfg_name != "d1024" or chains != 64:
@@ -137,9 +137,13 @@ def ncu_gemm_traffic(cfg_name, chains, d, n_lag):
     out, alg = {}, {}
     w = chains * n_lag * d * 8       # one window matrix (W, Xi, H or X) of all chains
     tri = chains * d * (d + 1) // 2 * 8  # the lower triangles of all chains' L or S
-    alg_bytes = {"gemm_target": 2 * w + d * d * 8, "trmm_noise": 2 * w + tri, "syrk_moments": w + 2 * tri}
+    # gemm_target: Xi in, H out, the whitening factor G (lower triangle) once
+    # syrk_moments: the window's distinct states (the profiled fraction of the rows) in, the
+    # lower S read and written
+    alg_bytes = {"gemm_target": 2 * w + d * (d + 1) // 2 * 8, "trmm_noise": 2 * w + tri,
+                 "syrk_moments": int(distinct * w) + 2 * tri}
     for cls in ("gemm_target", "trmm_noise", "syrk_moments"):
-        path = os.path.join(ROOT, "profiles", f"r01_ncu_{cls}.csv")
+        path = os.path.join(ROOT, "profiles", f"r02_ncu_{cls}.csv")
         if not os.path.exists(path):
             return None
         rows = list(csv.reader(open(path)))
@@ -152,7 +156,7 @@ def ncu_gemm_traffic(cfg_name, chains, d, n_lag):
         out[cls] = tot
         alg[cls] = alg_bytes[cls]
     return {"dram_bytes_per_launch": out, "algorithmic_bytes_per_launch": alg,
-            "source": "profiles/r01_ncu_*.csv (one steady-state launch each, single stream)"}
+            "source": "profiles/r02_ncu_*.csv (one steady-state launch each, single stream)"}
 
 
 def time_to_cov_error(lib, with_reference: bool):
@@ -388,7 +392,7 @@ def impl_b200(args):
                              f"{(3 * d * d + 3 * n_lag * d) * 8 * per_gpu / 1e9:.1f} GB >> 126 MB L2"},
             "roofline": {"bound": "fp64-dmma", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                          "frac": achieved / peak.value if peak.value else None,
-                         "traffic": ncu_gemm_traffic(args.config, per_gpu, d, n_lag),
+                         "traffic": ncu_gemm_traffic(args.config, per_gpu, d, n_lag, distinct),
                          "kernel": "gemm_f64 (TRMM noise + target GEMM + SYRK moments)",
                          "share_of_step": g_ms / prof_total if prof_total else None,
                          "peak_source": "diamx_fp64_peak: DMMA m8n8k4 loop measured live (MEASURED_PEAKS.json "

@@ -79,25 +79,18 @@ __device__ __forceinline__ void load_tile(double* s, const double* g, int64_t ld
     }
 }
 
-// One BM x BN tile of C. K is the (possibly triangle-clipped) contraction length.
-// Starts with a barrier so back-to-back calls may reuse the shared ring.
+// The main loop of one BM x BN tile: acc = sum_k A(m,k) B(k,n) over k < K (the possibly
+// triangle-clipped contraction length). Starts with a barrier so back-to-back calls may reuse
+// the shared ring.
 template <class CF, bool AK, bool BKM>
-__device__ __forceinline__ void gemm_tile(const double* A, const double* B, double* Cp, int64_t lda, int64_t ldb,
-                                          int64_t ldc, int M, int N, int K, int m0, int n0, double alpha,
-                                          double beta, bool tri_c_lower, double* smem, bool tri_b_lower = false) {
+__device__ __forceinline__ void gemm_mainloop(const double* A, const double* B, int64_t lda, int64_t ldb, int M,
+                                              int N, int K, int m0, int n0, bool tri_c_lower, double* smem,
+                                              bool tri_b_lower, double (&acc)[CF::MI][CF::NI][2]) {
     __syncthreads();
     double* sA = smem;
     double* sB = smem + CF::STAGES * CF::A_STAGE;
     const int KT = (K + CF::BK - 1) / CF::BK;
     const int tid = threadIdx.x;
-    if (beta != 0.0) {
-        // read-modify-write epilogue: pull the C tile towards L2 while the main loop runs
-        constexpr int LINES_PER_ROW = (CF::BN * 8 + 127) / 128;
-        for (int li = tid; li < CF::BM * LINES_PER_ROW; li += CF::THREADS) {
-            const int r = m0 + li / LINES_PER_ROW, cc = n0 + (li % LINES_PER_ROW) * 16;
-            if (r < M && cc < N) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Cp + (int64_t)r * ldc + cc));
-        }
-    }
     const int warp = tid >> 5, lane = tid & 31;
     const int wm0 = (warp / CF::WARPS_N) * CF::WM;
     const int wn0 = (warp % CF::WARPS_N) * CF::WN;
@@ -120,7 +113,6 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
                                                                  N - n0, tid);
     };
 
-    double acc[CF::MI][CF::NI][2];
 #pragma unroll
     for (int i = 0; i < CF::MI; ++i)
 #pragma unroll
@@ -176,10 +168,19 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
         }
     }
     cp_async_wait<0>();
+}
 
-    // Epilogue in batches of IC fragment rows: all of a batch's C loads are issued before
-    // its stores (a store to C may alias a later load, so the compiler would otherwise
-    // serialise one L2 round trip per fragment).
+// C = alpha acc + beta C for the tile at (m0, n0) (lower part only if tri_c_lower).
+// Epilogue in batches of IC fragment rows: all of a batch's C loads are issued before
+// its stores (a store to C may alias a later load, so the compiler would otherwise
+// serialise one L2 round trip per fragment).
+template <class CF>
+__device__ __forceinline__ void gemm_epilogue(const double (&acc)[CF::MI][CF::NI][2], double* Cp, int64_t ldc, int M,
+                                              int N, int m0, int n0, double alpha, double beta, bool tri_c_lower) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm0 = (warp / CF::WARPS_N) * CF::WM;
+    const int wn0 = (warp % CF::WARPS_N) * CF::WN;
+    const int fr = lane >> 2, fk = lane & 3;
     constexpr int IC = CF::MI >= 2 ? 2 : 1;
 #pragma unroll
     for (int i0 = 0; i0 < CF::MI; i0 += IC) {
@@ -221,6 +222,24 @@ __device__ __forceinline__ void gemm_tile(const double* A, const double* B, doub
             }
         }
     }
+}
+
+// One BM x BN tile of C: the main loop, then C = alpha acc + beta C.
+template <class CF, bool AK, bool BKM>
+__device__ __forceinline__ void gemm_tile(const double* A, const double* B, double* Cp, int64_t lda, int64_t ldb,
+                                          int64_t ldc, int M, int N, int K, int m0, int n0, double alpha,
+                                          double beta, bool tri_c_lower, double* smem, bool tri_b_lower = false) {
+    if (beta != 0.0) {
+        // read-modify-write epilogue: pull the C tile towards L2 while the main loop runs
+        constexpr int LINES_PER_ROW = (CF::BN * 8 + 127) / 128;
+        for (int li = threadIdx.x; li < CF::BM * LINES_PER_ROW; li += CF::THREADS) {
+            const int r = m0 + li / LINES_PER_ROW, cc = n0 + (li % LINES_PER_ROW) * 16;
+            if (r < M && cc < N) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Cp + (int64_t)r * ldc + cc));
+        }
+    }
+    double acc[CF::MI][CF::NI][2];
+    gemm_mainloop<CF, AK, BKM>(A, B, lda, ldb, M, N, K, m0, n0, tri_c_lower, smem, tri_b_lower, acc);
+    gemm_epilogue<CF>(acc, Cp, ldc, M, N, m0, n0, alpha, beta, tri_c_lower);
 }
 
 }  // namespace tile

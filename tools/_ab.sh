@@ -1,3 +1,1 @@
-python -m pytest tests -q -m gpu -x 2>&1 | tail -4
-python tools/host_bound.py --batches 8
-DIAM_B200_GROUPS=1 python tools/profile_step.py --classes 2>&1 | grep -E "gemm_target|trmm|batch"
+for g in 16 8 12 24 32 16; do DIAM_B200_GROUPS=$g python tools/host_bound.py --batches 8; done
