@@ -207,6 +207,16 @@ Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shar
     fmat_ = (int64_t)(d_ + 1) * ld_;
     twisted_ = tgt_.twisted();
     require(d_ <= 8192, Err::InvalidDimension, "the B200 engine supports d <= 8192");
+    {
+        int T = 0;  // the twist pairs (i, i+1), b_i != 0 (proj/src/target.cpp:167-173)
+        if (twisted_)
+            for (size_t i = 0; i < tgt_.b_coeffs.size(); ++i)
+                if (tgt_.b_coeffs[i] != 0.0) T = std::max(T, (int)i + 2);
+        T = (T + 1) & ~1;
+        require(d_ % 2 == 0 || T == 0, Err::InvalidDimension, "twisted targets need an even dimension");
+        dg_ = d_ + T;
+        ldg_ = pad_ld(dg_);
+    }
     {  // the main stream (batch merge, statistics) at the highest priority: the next
        // batch's moment updates wait for it
         int least = 0, greatest = 0;
@@ -278,7 +288,7 @@ int Engine::plan_memory() {
         double n = (double)C_ * fmat_;            // factors L
         n += (double)ws_factors * fmat_;          // refactor workspace
         n += (double)C_ * mat_;                   // local moments S
-        n += 3.0 * C_ * (double)lc * ld_;         // W, Xi, H
+        n += (double)C_ * lc * (2.0 * ld_ + ldg_);  // W, Xi, H
         if (!cfg_.checkpoint_path.empty()) n += (double)C_ * mat_;  // cumulative S
         if (k_.use_explicit_inverse) n += (double)C_ * (mat_ + (double)((d_ + 1) / 2) * ld_);  // X, TRTRI scratch
         n += 2.0 * mat_ + 3.0 * ld_;              // global snapshot, reduction buffer
@@ -323,6 +333,7 @@ int Engine::plan_memory() {
     }
     Lc_ = lc;
     win_ = (int64_t)Lc_ * ld_;
+    winh_ = (int64_t)Lc_ * ldg_;
     pool_ = pool && ng > 1;
     pool_n_ = pool_ ? gmax(ng) : 0;
     arena_bytes_ = (size_t)need(lc, pool_ ? pool_n_ : C_);
@@ -370,42 +381,67 @@ Engine::~Engine() {
 
 void Engine::upload_target() {
     auto& A = allocs_;
-    G_ = dalloc<double>(A, mat_);
+    // whitened form of every target: G (dg x ld) with rows 0..d-1 = a lower-triangular factor of
+    // the precision P (G^T G = P, reversed Cholesky on the GPU), so that x^T P x = |G x|^2, and
+    // for twisted targets rows d..d+T-1 = the first T eigenvectors (z_i = (V^T x)_i). Then
+    //   log pi(x) = -1/2 [ |G x|_d^2 + sum_{i<T} (w_i^2 - z_i^2) / sigma_i^2 ],
+    // w the twisted z (proj/src/target.cpp:154-173): one step formula for every target, and a
+    // window target product of d(d+1) + 2dT flops per row instead of 2d^2
+    G_ = dalloc<double>(A, (size_t)dg_ * ld_);
+    double* prev = nullptr;
+    DGB_CUDA(cudaMalloc(&prev, (size_t)mat_ * sizeof(double)));
     if (twisted_) {
-        // G = V^T: row i is eigenvector column i
-        Mat vt(d_, d_);
+        // P_rev = A_rev A_rev^T, A_rev[i][k] = V[d-1-i][k] / sigma_k
+        Mat ar(d_, d_);
         for (int i = 0; i < d_; ++i)
-            for (int k = 0; k < d_; ++k) vt(i, k) = tgt_.eigvecs(k, i);
-        upload_padded(G_, ld_, vt);
-        std::vector<double> ie(ld_, 0.0), bc(ld_, 0.0);
-        for (int i = 0; i < d_; ++i) {
-            ie[i] = 1.0 / tgt_.eigvals[i];
-            bc[i] = tgt_.b_coeffs[i];
-        }
-        inv_eig_ = dalloc<double>(A, ld_);
-        bcoef_ = dalloc<double>(A, ld_);
-        DGB_CUDA(cudaMemcpy(inv_eig_, ie.data(), ld_ * 8, cudaMemcpyHostToDevice));
-        DGB_CUDA(cudaMemcpy(bcoef_, bc.data(), ld_ * 8, cudaMemcpyHostToDevice));
+            for (int k = 0; k < d_; ++k) ar(i, k) = tgt_.eigvecs(d_ - 1 - i, k) / std::sqrt(tgt_.eigvals[k]);
+        double* dar = nullptr;
+        DGB_CUDA(cudaMalloc(&dar, (size_t)mat_ * sizeof(double)));
+        upload_padded(dar, ld_, ar);
+        double** pp = nullptr;
+        DGB_CUDA(cudaMalloc(&pp, 2 * sizeof(double*)));
+        const double* hp[2] = {dar, prev};
+        DGB_CUDA(cudaMemcpy(pp, hp, sizeof(hp), cudaMemcpyHostToDevice));
+        GemmBatch g{};
+        g.A = (const double* const*)pp;
+        g.B = (const double* const*)pp;
+        g.C = pp + 1;
+        g.lda = g.ldb = g.ldc = ld_;
+        g.M = g.N = g.K = d_;
+        g.alpha = 1.0;
+        gemm_f64(g, 1, true, true, stream_);
+        DGB_CUDA(cudaStreamSynchronize(stream_));
+        cudaFree(pp);
+        cudaFree(dar);
     } else {
-        // whitened form: G lower with G^T G = P, log pi(x) = -1/2 |G x|^2 -- every target is
-        // then -1/2 sum_i twist(G x)_i^2 / sigma_i^2 (Gaussian: sigma = 1, no twist), and the
-        // window's target product is triangular
         Mat rev(d_, d_);
         for (int i = 0; i < d_; ++i)
             for (int j = 0; j < d_; ++j) rev(i, j) = tgt_.precision(d_ - 1 - i, d_ - 1 - j);
-        double* prev = nullptr;
-        DGB_CUDA(cudaMalloc(&prev, (size_t)mat_ * sizeof(double)));
         upload_padded(prev, ld_, rev);
-        whitening_factor(prev, G_, d_, ld_, stream_);
-        cudaFree(prev);
-        std::vector<double> ie(ld_, 0.0), bc(ld_, 0.0);
-        for (int i = 0; i < d_; ++i) ie[i] = 1.0;
-        inv_eig_ = dalloc<double>(A, ld_);
-        bcoef_ = dalloc<double>(A, ld_);
-        DGB_CUDA(cudaMemcpy(inv_eig_, ie.data(), ld_ * 8, cudaMemcpyHostToDevice));
-        DGB_CUDA(cudaMemcpy(bcoef_, bc.data(), ld_ * 8, cudaMemcpyHostToDevice));
-        tri_target_ = true;
     }
+    whitening_factor(prev, G_, d_, ld_, stream_);
+    cudaFree(prev);
+    const int T = dg_ - d_;
+    std::vector<double> ie(ldg_, 0.0), bc(ldg_, 0.0);
+    for (int i = 0; i < d_; ++i) ie[i] = 1.0;
+    if (T > 0) {
+        Mat vt(T, d_);  // rows d.. of G: V^T
+        for (int i = 0; i < T; ++i)
+            for (int k = 0; k < d_; ++k) vt(i, k) = tgt_.eigvecs(k, i);
+        upload_padded(G_ + (size_t)d_ * ld_, ld_, vt);
+        // pair (d + i, d + i + 1), i even: w_{i+1} = z_{i+1} + b_i z_i^2 contributes
+        // (w_{i+1}^2 - z_{i+1}^2) / sigma_{i+1}^2; w_i = z_i contributes nothing
+        for (int i = 0; i < T; i += 2) {
+            bc[d_ + i] = tgt_.b_coeffs[i];
+            ie[d_ + i + 1] = 1.0 / tgt_.eigvals[i + 1];
+            bc[d_ + i + 1] = 1.0;  // subtract z_{i+1}^2 (its Gaussian term is inside |G x|^2)
+        }
+    }
+    inv_eig_ = dalloc<double>(A, ldg_);
+    bcoef_ = dalloc<double>(A, ldg_);
+    DGB_CUDA(cudaMemcpy(inv_eig_, ie.data(), ldg_ * 8, cudaMemcpyHostToDevice));
+    DGB_CUDA(cudaMemcpy(bcoef_, bc.data(), ldg_ * 8, cudaMemcpyHostToDevice));
+    tri_target_ = true;
     Ct_ = dalloc<double>(A, (size_t)d_ * d_);
     DGB_CUDA(cudaMemcpy(Ct_, tgt_.covariance.a.data(), (size_t)d_ * d_ * 8, cudaMemcpyHostToDevice));
     std::vector<double> pj(2 * ld_, 0.0);
@@ -431,12 +467,12 @@ void Engine::init_chains() {
     S_ = dalloc<double>(A, (size_t)C * mat_);
     W_ = dalloc<double>(A, (size_t)C * win_);
     Xi_ = dalloc<double>(A, (size_t)C * win_);
-    H_ = dalloc<double>(A, (size_t)C * win_);
+    H_ = dalloc<double>(A, (size_t)C * winh_);
     x_ = dalloc<double>(A, (size_t)C * ld_);
-    g_ = dalloc<double>(A, (size_t)C * ld_);
+    g_ = dalloc<double>(A, (size_t)C * ldg_);
     y_ = dalloc<double>(A, (size_t)C * ld_);
     xr_ = dalloc<double>(A, (size_t)C * ld_);
-    gr_ = dalloc<double>(A, (size_t)C * ld_);
+    gr_ = dalloc<double>(A, (size_t)C * ldg_);
     mean_ = dalloc<double>(A, (size_t)C * ld_);
     cmean_ = dalloc<double>(A, (size_t)C * ld_);
     cdiag_ = dalloc<double>(A, (size_t)C * ld_);
@@ -474,7 +510,7 @@ void Engine::init_chains() {
     Lnp_ = ptr_array(A, Lw2_, fmat_, nws);
     Wp_ = ptr_array(A, W_, win_, C);
     Xip_ = ptr_array(A, Xi_, win_, C);
-    Hp_ = ptr_array(A, H_, win_, C);
+    Hp_ = ptr_array(A, H_, winh_, C);
     Gpc_ = ptr_array(A, G_, 0, C);  // G once per chain (batched GEMMs)
     Sp_ = ptr_array(A, S_, mat_, C);
     if (Xinv_) {
@@ -508,7 +544,7 @@ void Engine::init_chains() {
     identity_ = true;
     // log pi(x0), quad(x0) (proposal.cpp:107-108)
     refresh_g(x_, g_, C, stream_);
-    launch_eval_logpi(x_, g_, inv_eig_, bcoef_, true, logpi_, C, d_, ld_, stream_);  // whitened form
+    launch_eval_logpi(g_, inv_eig_, bcoef_, logpi_, C, dg_, ldg_, stream_);  // whitened form
     if (k_.pcn_form()) {
         const double infl = k_.noise_infl();
         if (Xinv_) launch_trmv_quad(Xinvp_, ld_, x_, nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl), stream_);
@@ -558,7 +594,7 @@ void Engine::make_groups(int n) {
         g.Xip = Xip_ + g.off;
         g.Sp = Sp_ + g.off;
         g.Xib = ptr_array(A, Xi_ + g.off * win_, 0, 1);
-        g.Hb = ptr_array(A, H_ + g.off * win_, 0, 1);
+        g.Hb = ptr_array(A, H_ + g.off * winh_, 0, 1);
         // per-group inverse-block scratch (+ int active[C] tail): groups factor concurrently
         g.pw.inv = dalloc<double>(A, potrf_work_doubles(g.C));
         g.pw.inv128_ptrs = ptr_array(A, g.pw.inv, 128 * 128, g.C);
@@ -568,8 +604,8 @@ void Engine::make_groups(int n) {
 void Engine::refresh_g(const double* x, double* out, int chains, cudaStream_t s) {
     // out = x G^T: G x for every chain of the group (rows of stride ld)
     timed_begin(s);
-    launch_gemv_rows(G_, ld_, d_, x, out, chains, s);
-    timed_end("gemv_state", 2.0 * chains * (double)d_ * d_, s);
+    launch_gemv_rows(G_, ld_, d_, dg_, x, out, ldg_, chains, s);
+    timed_end("gemv_state", 2.0 * chains * (double)d_ * dg_, s);
 }
 
 void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s, double flops) {
@@ -645,7 +681,7 @@ double Engine::flops_per_batch() const {
     // 2 d^2 (twisted: V^T), SYRK d(d+1) per row (bench.py scales it to the distinct rows),
     // POTRF d^3/3 per window
     const double d = d_, L = Lw_, C = C_, M = (double)cfg_.intervals_per_batch;
-    const double tgt = tri_target_ ? d * (d + 1) : 2.0 * d * d;
+    const double tgt = d * (d + 1) + 2.0 * d * (dg_ - d_);  // whitening factor + twisted rows
     const double per_window = C * (L * d * (d + 1) + L * tgt + L * d * (d + 1) + d * d * d / 3.0);
     return per_window * M;
 }
@@ -849,24 +885,27 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         h.B = (const double* const*)Gp_;
         h.lda = ld_;
         h.ldb = ld_;
-        h.ldc = ld_;
-        h.N = d_;
+        h.ldc = ldg_;
+        h.N = dg_;
         h.K = d_;
         h.alpha = 1.0;
         h.beta = 0.0;
-        h.tri_b_lower = tri_target_ ? 1 : 0;  // whitened Gaussian: G lower, K clipped per tile
+        // G lower over its first d rows (the whitening factor): K clipped per column tile;
+        // the twisted rows below are full (K = d)
+        h.tri_b_lower = tri_target_ ? 1 : 0;
+        const double tfl = (double)rows * C * ((double)d_ * (d_ + 1) + 2.0 * d_ * (dg_ - d_));
         if (rows == Lc_) {
             h.A = (const double* const*)g.Xib;
             h.C = g.Hb;
             h.M = C * Lc_;  // the group's window chunks are one contiguous (C Lc) x ld matrix
-            gemm("gemm_target", h, 1, true, true, s);
-            if (twice_ & kTwiceTarget) gemm("gemm_target", h, 1, true, true, s);
+            gemm("gemm_target", h, 1, true, true, s, tfl);
+            if (twice_ & kTwiceTarget) gemm("gemm_target", h, 1, true, true, s, tfl);
         } else {            // ragged last chunk: per-chain pieces
             h.B = (const double* const*)Gpc_;
             h.A = (const double* const*)g.Xip;
             h.C = Hp_ + o;
             h.M = rows;
-            gemm("gemm_target", h, C, true, true, s);
+            gemm("gemm_target", h, C, true, true, s, tfl);
         }
     }
 
@@ -880,12 +919,15 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     sp.win_stride = win_;
     sp.W = W_ + o * win_;
     sp.Xi = Xi_ + o * win_;
-    sp.H = H_ + o * win_;
+    sp.H = H_ + o * winh_;
+    sp.dg = dg_;
+    sp.ldg = ldg_;
+    sp.hwin_stride = winh_;
     sp.x = x_ + o * ld_;
-    sp.g = g_ + o * ld_;
+    sp.g = g_ + o * ldg_;
     sp.y = y_ + o * ld_;
     sp.xr = k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
-    sp.gr = k_.adaptive_ref ? gr_ + o * ld_ : nullptr;
+    sp.gr = k_.adaptive_ref ? gr_ + o * ldg_ : nullptr;
     sp.log_pi = logpi_ + o;
     sp.quad = quad_ + o;
     sp.beta = beta_ + o;
@@ -927,7 +969,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         m.A = (const double* const*)(Hp_ + o);
         m.B = (const double* const*)g.Xip;
         m.C = g.Sp;
-        m.lda = ld_;
+        m.lda = ldg_;
         m.ldb = ld_;
         m.ldc = ld_;
         m.M = d_;
@@ -948,7 +990,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
             for (int v : kc_h) fl += (double)v * d_ * (d_ + 1.0);
         }
         gemm("syrk_moments", m, C, false, false, s, fl);
-        launch_mean_update(mean_ + o * ld_, ld_, H_ + o * win_, win_, ld_, C, d_, kcount_ + o, kc, (double)cb, s);
+        launch_mean_update(mean_ + o * ld_, ld_, H_ + o * winh_, winh_, ldg_, C, d_, kcount_ + o, kc, (double)cb, s);
     }
     if (project)
         launch_project_rows(Xi_ + o * win_, win_, ld_, C, rows, lf, d_, proj_,
@@ -1097,7 +1139,7 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
     if (p.move_ref) {
         if (!p.refactor) launch_blend_mean(mg_, mean_ + o * ld_, p.wg, p.wl, mb_ + o * ld_, C, d_, ld_, s);
         DGB_CUDA(cudaMemcpyAsync(xr_ + o * ld_, mb_ + o * ld_, (size_t)C * ld_ * 8, cudaMemcpyDeviceToDevice, s));
-        refresh_g(xr_ + o * ld_, gr_ + o * ld_, C, s);
+        refresh_g(xr_ + o * ld_, gr_ + o * ldg_, C, s);
     }
     // quad with the current factor (proposal.cpp:211) and y for the next window's recursion.
     // With a fixed reference point y = L^-1 (x - x_ref) is carried exactly through the
@@ -1115,7 +1157,7 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
         timed_end("trsv", 0.0, s);
     }
     // G x re-anchored at every boundary so the step recursion never drifts
-    refresh_g(x_ + o * ld_, g_ + o * ld_, C, s);
+    refresh_g(x_ + o * ld_, g_ + o * ldg_, C, s);
     // the next window's steps follow the tail
     DGB_CUDA(cudaEventRecord(g.ev_ref, g.sr));
     DGB_CUDA(cudaStreamWaitEvent(g.s, g.ev_ref, 0));

@@ -194,6 +194,10 @@ private:
     // precision (G^T G = P), log pi(x) = -1/2 |G x|^2 -- the target product H = Xi G^T is
     // then triangular (half the flops of the full product with P)
     bool tri_target_ = false;
+    // twisted targets add the T = d/10 twisted coordinates z_i = (V^T x)_i as rows of G below
+    // the whitening factor: g = G x has dg_ = d + T entries (stride ldg_; H rows likewise)
+    int dg_ = 0;
+    int64_t ldg_ = 0, winh_ = 0;
     cudaStream_t stream_ = nullptr;
     int stream_prio_ = 0;
     cudaEvent_t main_ev_ = nullptr;

@@ -41,6 +41,9 @@ void launch_draws(int kind, double* out_f64, uint64_t* out_u64, int64_t n, Philo
 struct StepParams {
     int d, n_lag, chains;
     int64_t ld, win_stride;
+    int dg;               // entries of g = G x and of the H rows (d + the twisted rows)
+    int64_t ldg;          // their stride
+    int64_t hwin_stride;  // per-chain stride of the H window
     const double* W;
     double* Xi;       // in: increments; out: the window's DISTINCT counted post-step states,
                       // compacted: row j = the j-th distinct state from step `first` on
@@ -156,14 +159,18 @@ void launch_accept_factor(double** L, double** Lnew, const int* try_flag, const 
 // L_c = I
 void launch_set_identity(double* base, int64_t mat_stride, int chains, int d, int64_t ld, cudaStream_t s);
 // log pi from x and g = G x (Gaussian: -1/2 x.g; twisted: -1/2 sum twist(g)^2 / sigma^2)
-void launch_eval_logpi(const double* x, const double* g, const double* inv_eig, const double* bcoef,
-                       bool twisted, double* out, int chains, int d, int64_t ld, cudaStream_t s);
+// log pi = -1/2 sum over pairs (e, e+1) of ie_e w_e^2 + ie_{e+1} (w_{e+1}^2 - bc_{e+1} g_{e+1}^2),
+// w = (g_e, g_{e+1} + bc_e g_e^2): the whitened form of every target (Engine::upload_target)
+void launch_eval_logpi(const double* g, const double* inv_eig, const double* bcoef, double* out, int chains, int dg,
+                       int64_t ldg, cudaStream_t s);
 // mb_c = wg*mg + wl*ml_c
 void launch_blend_mean(const double* mg, const double* ml, double wg, double wl, double* mb, int chains,
                        int d, int64_t ld, cudaStream_t s);
 // out[c][t][0..1] = proj[0..1] . X_c[t], t in [t0, rows)
 // out[c] = G X[c] (G d x d row-major; X, out: one row per chain; stride ld)
-void launch_gemv_rows(const double* G, int64_t ld, int d, const double* X, double* out, int chains, cudaStream_t s);
+// out[c][n] = sum_k G[n][k] X[c][k], n < nrows (G rows and X rows of stride ld, out rows of out_ld)
+void launch_gemv_rows(const double* G, int64_t ld, int d, int nrows, const double* X, double* out, int64_t out_ld,
+                      int chains, cudaStream_t s);
 // through row_of (the compacted window): out[c][t] = proj . X_c[row_of[c][t]]
 void launch_project_rows(const double* X, int64_t win_stride, int64_t ld, int chains, int rows, int t0,
                          int d, const double* proj, double* out, int out_ld, const int* row_of, cudaStream_t s);

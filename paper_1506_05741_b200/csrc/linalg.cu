@@ -309,8 +309,8 @@ __global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(double* const* Lm, i
 // and 8 chains, a warp two rows; lanes stride along k with 16-byte loads, and the 16
 // (row, chain) partial sums are combined by recursive halving (16 shuffles per warp).
 // One pass over G per 8 chains instead of a 128-row DMMA tile with 4 valid rows.
-__global__ void __launch_bounds__(256) gemv_rows_kernel(const double* G, int64_t ld, int d, const double* X,
-                                                        double* out, int chains) {
+__global__ void __launch_bounds__(256) gemv_rows_kernel(const double* G, int64_t ld, int d, int nrows,
+                                                        const double* X, double* out, int64_t out_ld, int chains) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = blockIdx.x * 16 + 2 * warp;
     const int c0 = blockIdx.y * 8;
@@ -318,8 +318,8 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const double* G, int64_t
     const double* xs[8];
 #pragma unroll
     for (int ch = 0; ch < 8; ++ch) xs[ch] = ch < nc ? X + (int64_t)(c0 + ch) * ld : nullptr;
-    const double* g0 = G + (int64_t)min(n0, d - 1) * ld;
-    const double* g1 = G + (int64_t)min(n0 + 1, d - 1) * ld;
+    const double* g0 = G + (int64_t)min(n0, nrows - 1) * ld;
+    const double* g1 = G + (int64_t)min(n0 + 1, nrows - 1) * ld;
     double v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = 0.0;
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const double* G, int64_t
     }
     const double tot = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
     const int slot = lane >> 1, r = slot >> 3, ch = slot & 7;
-    if (!(lane & 1) && ch < nc && n0 + r < d) out[(int64_t)(c0 + ch) * ld + n0 + r] = tot;
+    if (!(lane & 1) && ch < nc && n0 + r < nrows) out[(int64_t)(c0 + ch) * out_ld + n0 + r] = tot;
 }
 
 // ------------------------------------------------------------------ Cholesky diagonal block
@@ -488,20 +488,15 @@ __global__ void set_identity_kernel(double* base, int64_t mat_stride, int d, int
     }
 }
 
-__global__ void eval_logpi_kernel(const double* x, const double* g, const double* inv_eig, const double* bcoef,
-                                  int twisted, double* out, int d, int64_t ld) {
+__global__ void eval_logpi_kernel(const double* g, const double* inv_eig, const double* bcoef, double* out, int dg,
+                                  int64_t ldg) {
     const int c = blockIdx.x;
-    const double* xc = x + c * ld;
-    const double* gc = g + c * ld;
+    const double* gc = g + c * ldg;
     double s = 0.0;
-    for (int i = 2 * threadIdx.x; i < d; i += 2 * blockDim.x) {
-        const double g0 = gc[i], g1 = i + 1 < d ? gc[i + 1] : 0.0;
-        if (twisted) {
-            const double w1 = g1 + bcoef[i] * g0 * g0;
-            s += g0 * g0 * inv_eig[i] + (i + 1 < d ? w1 * w1 * inv_eig[i + 1] : 0.0);
-        } else {
-            s += xc[i] * g0 + (i + 1 < d ? xc[i + 1] * g1 : 0.0);
-        }
+    for (int i = 2 * threadIdx.x; i < dg; i += 2 * blockDim.x) {
+        const double g0 = gc[i], g1 = i + 1 < dg ? gc[i + 1] : 0.0;
+        const double w1 = g1 + bcoef[i] * g0 * g0;
+        s += g0 * g0 * inv_eig[i] + (i + 1 < dg ? (w1 * w1 - bcoef[i + 1] * g1 * g1) * inv_eig[i + 1] : 0.0);
     }
     __shared__ double red[32];
     s = warp_sum(s);
@@ -558,10 +553,11 @@ void launch_mean_update(double* mean, int64_t mean_stride, const double* Xw, int
     count_launch();
 }
 
-void launch_gemv_rows(const double* G, int64_t ld, int d, const double* X, double* out, int chains, cudaStream_t s) {
+void launch_gemv_rows(const double* G, int64_t ld, int d, int nrows, const double* X, double* out, int64_t out_ld,
+                      int chains, cudaStream_t s) {
     if (chains <= 0 || d <= 0) return;
-    dim3 grid((unsigned)ceil_div(d, 16), (unsigned)ceil_div(chains, 8));
-    gemv_rows_kernel<<<grid, 256, 0, s>>>(G, ld, d, X, out, chains);
+    dim3 grid((unsigned)ceil_div(nrows, 16), (unsigned)ceil_div(chains, 8));
+    gemv_rows_kernel<<<grid, 256, 0, s>>>(G, ld, d, nrows, X, out, out_ld, chains);
     DGB_LAUNCH_CHECK();
     count_launch();
 }
@@ -993,9 +989,9 @@ void launch_set_identity(double* base, int64_t mat_stride, int chains, int d, in
     count_launch();
 }
 
-void launch_eval_logpi(const double* x, const double* g, const double* inv_eig, const double* bcoef, bool twisted,
-                       double* out, int chains, int d, int64_t ld, cudaStream_t s) {
-    eval_logpi_kernel<<<chains, 256, 0, s>>>(x, g, inv_eig, bcoef, twisted ? 1 : 0, out, d, ld);
+void launch_eval_logpi(const double* g, const double* inv_eig, const double* bcoef, double* out, int chains, int dg,
+                       int64_t ldg, cudaStream_t s) {
+    eval_logpi_kernel<<<chains, 256, 0, s>>>(g, inv_eig, bcoef, out, dg, ldg);
     DGB_LAUNCH_CHECK();
     count_launch();
 }

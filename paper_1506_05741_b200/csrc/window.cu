@@ -120,26 +120,29 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
     const double sc = beta * p.infl;
     const double hq = 0.5 / (p.infl * p.infl);
 
+    const int dg = p.dg;
+    const int64_t ldg = p.ldg;
     const double* Wc = p.W + c * p.win_stride;
     double* Xc = p.Xi + c * p.win_stride;
-    double* Hc = p.H + c * p.win_stride;
+    double* Hc = p.H + c * p.hwin_stride;
     Compactor cp;
 
     double2 x[R], g[R], y[R], xr[R], gr[R], ie[R], bc[R];
-    bool valid[R];
+    bool valid[R], vg[R];  // entry pair e in x-space (e < d) / in g-space (e < dg)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = 2 * (tid + r * kStepThreads);
         valid[r] = e < d;
+        vg[r] = e < dg;
         const double2 z2 = make_double2(0.0, 0.0);
         x[r] = valid[r] ? ld2(p.x + c * ld + e) : z2;
-        g[r] = valid[r] ? ld2(p.g + c * ld + e) : z2;
+        g[r] = vg[r] ? ld2(p.g + c * ldg + e) : z2;
         y[r] = (valid[r] && pcn) ? ld2(p.y + c * ld + e) : z2;
         xr[r] = (valid[r] && p.xr) ? ld2(p.xr + c * ld + e) : z2;
-        gr[r] = (valid[r] && p.gr) ? ld2(p.gr + c * ld + e) : z2;
+        gr[r] = (vg[r] && p.gr) ? ld2(p.gr + c * ldg + e) : z2;
         if (TWISTED) {
-            ie[r] = valid[r] ? ld2(p.inv_eig + e) : z2;
-            bc[r] = valid[r] ? ld2(p.bcoef + e) : z2;
+            ie[r] = vg[r] ? ld2(p.inv_eig + e) : z2;
+            bc[r] = vg[r] ? ld2(p.bcoef + e) : z2;
         }
     }
     double lp = p.log_pi[c], q = pcn ? p.quad[c] : 0.0;
@@ -152,13 +155,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int e = 2 * (tid + r * kStepThreads);
-            if (valid[r]) {
-                a[r] = ld2(Xc + (int64_t)t * ld + e);
-                b[r] = pcn ? ld2(Wc + (int64_t)t * ld + e) : make_double2(0.0, 0.0);
-                hh[r] = ld2(Hc + (int64_t)t * ld + e);
-            } else {
-                a[r] = b[r] = hh[r] = make_double2(0.0, 0.0);
-            }
+            const double2 z2 = make_double2(0.0, 0.0);
+            a[r] = valid[r] ? ld2(Xc + (int64_t)t * ld + e) : z2;
+            b[r] = (valid[r] && pcn) ? ld2(Wc + (int64_t)t * ld + e) : z2;
+            hh[r] = vg[r] ? ld2(Hc + (int64_t)t * ldg + e) : z2;
         }
     };
     load_row(0, xi, w, h);
@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
                 // w_{2j+1} = z_{2j+1} + b_{2j} z_{2j}^2 (proj/src/target.cpp:167-173)
                 const double w0 = gc[r].x;
                 const double w1 = gc[r].y + bc[r].x * gc[r].x * gc[r].x;
-                sa += w0 * w0 * ie[r].x + w1 * w1 * ie[r].y;
+                // whitened form: ie w0^2 + ie' (w1^2 - bc' g1^2) (Engine::upload_target)
+                sa += w0 * w0 * ie[r].x + (w1 * w1 - bc[r].y * gc[r].y * gc[r].y) * ie[r].y;
             } else {
                 sa += xc[r].x * gc[r].x + xc[r].y * gc[r].y;
             }
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
         const bool counted = t >= p.first;
         const bool fresh = counted && (acc || t == p.first);
         if (fresh) {
-            if (cp.j >= 0) store_row<R, kStepThreads>(Hc + (int64_t)cp.j * ld, x, valid, tid, d, cp.mult);
+            if (cp.j >= 0) store_row<R, kStepThreads>(Hc + (int64_t)cp.j * ldg, x, valid, tid, d, cp.mult);
             ++cp.j;
             cp.mult = 0.0;
         }
@@ -251,18 +252,20 @@ __global__ void __launch_bounds__(kStepThreads, 1) mh_window_kernel(StepParams p
             load_row(t + 1, xi, w, h);
         }
     }
-    if (cp.j >= 0) store_row<R, kStepThreads>(Hc + (int64_t)cp.j * ld, x, valid, tid, d, cp.mult);
+    if (cp.j >= 0) store_row<R, kStepThreads>(Hc + (int64_t)cp.j * ldg, x, valid, tid, d, cp.mult);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = 2 * (tid + r * kStepThreads);
+        if (vg[r]) {
+            if (e + 1 < dg) st2(p.g + c * ldg + e, g[r]);
+            else p.g[c * ldg + e] = g[r].x;
+        }
         if (!valid[r]) continue;
         if (e + 1 < d) {
             st2(p.x + c * ld + e, x[r]);
-            st2(p.g + c * ld + e, g[r]);
             if (pcn) st2(p.y + c * ld + e, y[r]);
         } else {
             p.x[c * ld + e] = x[r].x;
-            p.g[c * ld + e] = g[r].x;
             if (pcn) p.y[c * ld + e] = y[r].x;
         }
     }
@@ -332,12 +335,16 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     const int64_t ld = p.ld;
     const bool pcn = p.pcn != 0;
     const int nrows = pcn ? 3 : 2;  // xi, h (+ w for the pCN-form y recursion)
+    (void)nrows;
+    const int dg = p.dg;
+    const int64_t ldg = p.ldg;
     extern __shared__ __align__(128) double ring[];  // NS stages, then the log-uniform table
     __shared__ __align__(8) uint64_t full[kMaxStages];
     __shared__ __align__(16) double red[2][NW][2];
-    const uint32_t row_bytes = (uint32_t)(ld * sizeof(double));
+    // a stage: the xi row (ld), the h row (ldg: d + the twisted rows), the w row (ld)
+    const uint32_t row_bytes = (uint32_t)(ld * sizeof(double)), hrow_bytes = (uint32_t)(ldg * sizeof(double));
     double* stage0 = ring;
-    const int64_t stage_len = (int64_t)nrows * ld;
+    const int64_t stage_len = ld + ldg + (pcn ? ld : 0);
 
     const double beta = p.beta[c];
     const double cc = pcn ? sqrt(fmax(0.0, 1.0 - beta * beta)) : 1.0;  // proj/src/proposal.cpp:120
@@ -345,15 +352,15 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     const double hq = 0.5 / (p.infl * p.infl);
     const double* Wc = p.W + c * p.win_stride;
     double* Xc = p.Xi + c * p.win_stride;
-    double* Hc = p.H + c * p.win_stride;
+    double* Hc = p.H + c * p.hwin_stride;
     Compactor cp;
 
     auto issue = [&](int t, int s) {  // producer: row t of the window into stage s = t % NS
         double* st = stage0 + s * stage_len;
-        mbar_expect_tx(&full[s], row_bytes * nrows);
+        mbar_expect_tx(&full[s], row_bytes * (pcn ? 2 : 1) + hrow_bytes);
         tma_row(st, Xc + (int64_t)t * ld, row_bytes, &full[s]);
-        tma_row(st + ld, Hc + (int64_t)t * ld, row_bytes, &full[s]);
-        if (pcn) tma_row(st + 2 * ld, Wc + (int64_t)t * ld, row_bytes, &full[s]);
+        tma_row(st + ld, Hc + (int64_t)t * ldg, hrow_bytes, &full[s]);
+        if (pcn) tma_row(st + ld + ldg, Wc + (int64_t)t * ld, row_bytes, &full[s]);
     };
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
 
     double2 x[R], g[R], y[R], xrv[ZREF ? 1 : R], grv[ZREF ? 1 : R], iev[TWG ? 1 : R], bcv[TWG ? 1 : R], a[R], ga[R],
         cy[R];
-    bool valid[R];
+    bool valid[R], vg[R];  // entry pair e in x-space (e < d) / in g-space (e < dg)
     auto XR = [&](int r) -> double2 { return ZREF ? make_double2(0.0, 0.0) : xrv[ZREF ? 0 : r]; };
     auto GR = [&](int r) -> double2 { return ZREF ? make_double2(0.0, 0.0) : grv[ZREF ? 0 : r]; };
     auto IE = [&](int r) -> double2 {
@@ -389,17 +396,18 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     for (int r = 0; r < R; ++r) {
         const int e = 2 * (tid + r * T);
         valid[r] = e < d;
+        vg[r] = e < dg;
         const double2 z2 = make_double2(0.0, 0.0);
         x[r] = valid[r] ? ld2(p.x + c * ld + e) : z2;
-        g[r] = valid[r] ? ld2(p.g + c * ld + e) : z2;
+        g[r] = vg[r] ? ld2(p.g + c * ldg + e) : z2;
         y[r] = (valid[r] && pcn) ? ld2(p.y + c * ld + e) : z2;
         if (!ZREF) {
             xrv[ZREF ? 0 : r] = (valid[r] && p.xr) ? ld2(p.xr + c * ld + e) : z2;
-            grv[ZREF ? 0 : r] = (valid[r] && p.gr) ? ld2(p.gr + c * ld + e) : z2;
+            grv[ZREF ? 0 : r] = (vg[r] && p.gr) ? ld2(p.gr + c * ldg + e) : z2;
         }
         if (TWISTED && !TWG) {
-            iev[TWG ? 0 : r] = valid[r] ? ld2(p.inv_eig + e) : z2;
-            bcv[TWG ? 0 : r] = valid[r] ? ld2(p.bcoef + e) : z2;
+            iev[TWG ? 0 : r] = vg[r] ? ld2(p.inv_eig + e) : z2;
+            bcv[TWG ? 0 : r] = vg[r] ? ld2(p.bcoef + e) : z2;
         }
         refresh(r);
     }
@@ -419,7 +427,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
                     double2& yc) {
         const int e = 2 * (tid + r * T);
         const double2 xi = valid[r] ? ld2(pxi + e) : make_double2(0.0, 0.0);
-        const double2 h = valid[r] ? ld2(ph + e) : make_double2(0.0, 0.0);
+        const double2 h = vg[r] ? ld2(ph + e) : make_double2(0.0, 0.0);
         // exact reference candidate (proj/src/proposal.cpp:119-124), no FMA contraction
         if (PRE) {
             xc.x = __dadd_rn(a[r].x, xi.x);
@@ -464,13 +472,14 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             double2 xc, gc, yc;
-            cand(st, st + ld, st + 2 * ld, r, xc, gc, yc);
+            cand(st, st + ld, st + ld + ldg, r, xc, gc, yc);
             if (TWISTED) {
+                // whitened form: ie w0^2 + ie' (w1^2 - bc' g1^2), w1 = g1 + bc g0^2 (upload_target)
                 const double2 ie = IE(r), bc = BC(r);
                 const double w0 = gc.x;
                 const double w1 = gc.y + bc.x * gc.x * gc.x;
                 sa0 += w0 * w0 * ie.x;
-                sa1 += w1 * w1 * ie.y;
+                sa1 += (w1 * w1 - bc.y * gc.y * gc.y) * ie.y;
             } else {
                 sa0 += xc.x * gc.x;
                 sa1 += xc.y * gc.y;
@@ -525,7 +534,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
         const bool counted = t >= p.first;
         const bool fresh = counted && (acc || t == p.first);
         if (fresh) {
-            if (cp.j >= 0) store_row<R, T>(Hc + (int64_t)cp.j * ld, x, valid, tid, d, cp.mult);
+            if (cp.j >= 0) store_row<R, T>(Hc + (int64_t)cp.j * ldg, x, valid, tid, d, cp.mult);
             ++cp.j;
             cp.mult = 0.0;
         }
@@ -533,8 +542,8 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 double2 xc, gc, yc;
-                if (late) cand(st, st + ld, st + 2 * ld, r, xc, gc, yc);
-                else cand(Xc + (int64_t)t * ld, Hc + (int64_t)t * ld, Wc + (int64_t)t * ld, r, xc, gc, yc);
+                if (late) cand(st, st + ld, st + ld + ldg, r, xc, gc, yc);
+                else cand(Xc + (int64_t)t * ld, Hc + (int64_t)t * ldg, Wc + (int64_t)t * ld, r, xc, gc, yc);
                 x[r] = xc;
                 g[r] = gc;
                 if (pcn) y[r] = yc;
@@ -562,18 +571,20 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
     if (blockIdx.x == 0 && tid == 32)  // a thread of warp 1: not the TMA producer
         for (int i = 0; i < 7; ++i) g_mh_prof[i] = mh_acc[i];
 #endif
-    if (cp.j >= 0) store_row<R, T>(Hc + (int64_t)cp.j * ld, x, valid, tid, d, cp.mult);
+    if (cp.j >= 0) store_row<R, T>(Hc + (int64_t)cp.j * ldg, x, valid, tid, d, cp.mult);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = 2 * (tid + r * T);
+        if (vg[r]) {
+            if (e + 1 < dg) st2(p.g + c * ldg + e, g[r]);
+            else p.g[c * ldg + e] = g[r].x;
+        }
         if (!valid[r]) continue;
         if (e + 1 < d) {
             st2(p.x + c * ld + e, x[r]);
-            st2(p.g + c * ld + e, g[r]);
             if (pcn) st2(p.y + c * ld + e, y[r]);
         } else {
             p.x[c * ld + e] = x[r].x;
-            p.g[c * ld + e] = g[r].x;
             if (pcn) p.y[c * ld + e] = y[r].x;
         }
     }
@@ -588,8 +599,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_tma_kernel(StepParams p, int N
 
 template <int R, bool TW, int T, bool PRE = (R * T <= 512)>
 bool try_tma(const StepParams& p, cudaStream_t s) {
-    const int nrows = p.pcn ? 3 : 2;
-    const size_t stage = (size_t)nrows * p.ld * sizeof(double);
+    const size_t stage = (size_t)(p.ld * (p.pcn ? 2 : 1) + p.ldg) * sizeof(double);
     const size_t table = (size_t)p.n_lag * sizeof(double);
     constexpr size_t kMaxSmem = 220 * 1024;
     if (table + 2 * stage > kMaxSmem) return false;
@@ -616,7 +626,7 @@ bool try_tma(const StepParams& p, cudaStream_t s) {
 
 template <bool TW>
 void launch_r(const StepParams& p, cudaStream_t s) {
-    const int pairs = (p.d + 1) / 2;
+    const int pairs = (p.dg + 1) / 2;  // the g-space entries (d + the twisted rows) set the width
     const int R = (pairs + kStepThreads - 1) / kStepThreads;
     dim3 grid(p.chains), block(kStepThreads);
     // 256 threads (2 double2 pairs each) up to d = 1024, then 512 threads: fewer warps per

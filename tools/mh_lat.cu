@@ -64,6 +64,9 @@ int main(int argc, char** argv) {
     p.chains = C;
     p.ld = ld;
     p.win_stride = win;
+    p.dg = d;
+    p.ldg = ld;
+    p.hwin_stride = win;
     p.W = W;
     p.Xi = Xi;
     p.H = H;
