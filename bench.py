@@ -326,20 +326,22 @@ def impl_b200(args):
     eng.set_profiling(True)
     eng.run_batches(1)
     classes = ["gemm_target", "trmm_noise", "syrk_moments", "potrf", "mh_window", "normals", "trsv", "blend_cov",
-               "merge", "gemv_state"]
+               "merge", "gemv_state", "xi_accepted", "reconstruct"]
     st = {c: eng.stat(c) for c in classes}
     prof_total = sum(v[0] for v in st.values())
-    gemm_cls = ["gemm_target", "trmm_noise", "syrk_moments"]
+    gemm_cls = ["gemm_target", "trmm_noise", "syrk_moments", "xi_accepted"]
     g_ms = sum(st[c][0] for c in gemm_cls)
     g_fl = sum(st[c][1] for c in gemm_cls)
     peak = C.c_double()
     lib.check(lib.lib.diamx_fp64_peak(C.byref(peak)))
     achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
-    # the SYRK runs over each window's distinct states only (rejected steps repeat a state):
-    # the step's algorithmic flops count the rows the profiled batch actually had
+    # the step's algorithmic flops: every class's count from the profiled batch (the SYRK over
+    # the window's distinct states and the accepted steps' increments count the rows they ran
+    # over), scaled to the timed run's chains per GPU
     syrk_full = prof_chains * M * n_lag * d * (d + 1.0)
     distinct = st["syrk_moments"][1] / syrk_full if syrk_full else 1.0
-    alg_flops -= (1.0 - distinct) * syrk_full * chains / prof_chains / world
+    accepted = st["xi_accepted"][1] / syrk_full if syrk_full else 0.0
+    alg_flops = sum(v[1] for v in st.values()) * (chains / world) / prof_chains
     del eng
 
     # ---- end-to-end through the C ABI (host target, result back to host)
@@ -393,12 +395,14 @@ def impl_b200(args):
             "roofline": {"bound": "fp64-dmma", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                          "frac": achieved / peak.value if peak.value else None,
                          "traffic": ncu_gemm_traffic(args.config, per_gpu, d, n_lag, distinct),
-                         "kernel": "gemm_f64 (TRMM noise + target GEMM + SYRK moments)",
+                         "kernel": "gemm_f64 (window TRMM H = s W L_z^T, twisted rows, SYRK moments, "
+                                   "accepted increments)",
                          "share_of_step": g_ms / prof_total if prof_total else None,
                          "peak_source": "diamx_fp64_peak: DMMA m8n8k4 loop measured live (MEASURED_PEAKS.json "
                                         "has no FP64 entry)",
                          "step_alg_tflops": alg_flops / (ms / args.steps / 1e3) / 1e12,
                          "syrk_distinct_row_fraction": distinct,
+                         "accepted_row_fraction": accepted,
                          "profile_chains": prof_chains,
                          "per_class_ms": {c: round(v[0], 4) for c, v in st.items()}},
             "cpu_baseline": cpu,

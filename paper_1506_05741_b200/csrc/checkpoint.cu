@@ -17,6 +17,10 @@ namespace {
 
 constexpr char kCkptMagic[8] = {'D', 'I', 'A', 'M', 'C', 'K', 'P', 'T'};
 constexpr char kExtMagic[8] = {'B', '2', '0', '0', 'E', 'X', 'T', '1'};
+// the engine's whitened state exactly (the reference's x-space fields are its image through
+// G^-1, which a resume could only invert to rounding): global S_z / m_z, then per chain L_z,
+// [L_z^-1], S_z, [cumulative S_z], m_z, the x-space raw diagonal, the cumulative one
+constexpr char kExt2Magic[8] = {'B', '2', '0', '0', 'E', 'X', 'T', '2'};
 constexpr uint32_t kVersion = 1;
 constexpr uint32_t kEndian = 0x01020304u;
 
@@ -100,6 +104,32 @@ Mat mirror_lower(const double* h, int d, int64_t ld) {
 
 }  // namespace
 
+// One product of device matrices (d x d, row stride ld) on the engine stream, for the
+// conversions between the whitened engine state and the checkpoint's x-space fields:
+// out = A B (A K-major rows; B rows K-major when bk, else B[k][n]); lower part only if tri.
+void Engine::dev_gemm(const double* A, const double* B, bool bk, double* out, bool tri) {
+    const double* h[3] = {A, B, out};
+    DGB_CUDA(cudaMemcpy(ptr_gen_, h, sizeof(h), cudaMemcpyHostToDevice));
+    GemmBatch g{};
+    g.A = (const double* const*)ptr_gen_;
+    g.B = (const double* const*)(ptr_gen_ + 1);
+    g.C = ptr_gen_ + 2;
+    g.lda = g.ldb = g.ldc = ld_;
+    g.M = g.N = g.K = d_;
+    g.alpha = 1.0;
+    g.tri_c_lower = tri ? 1 : 0;
+    gemm_f64(g, 1, true, bk, stream_);
+    DGB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// out (lower) = M sym(S) M^T, S given by its lower triangle (M = G: x -> whitened; M = G^-1:
+// whitened -> x); Sfull_ / Stmp_ are the scratch, out may be Sfull_ (not Stmp_)
+void Engine::congruence(const double* S, const double* M, double* out) {
+    launch_mirror_lower(S, Sfull_, d_, ld_, stream_);
+    dev_gemm(Sfull_, M, true, Stmp_, false);  // Sfull M^T (B(k, n) = M[n][k])
+    dev_gemm(M, Stmp_, false, out, true);     // M (Sfull M^T), lower
+}
+
 void Engine::save_checkpoint(double wall) {
     DGB_CUDA(cudaDeviceSynchronize());
     const int C = C_;
@@ -115,7 +145,8 @@ void Engine::save_checkpoint(double wall) {
     };
     const auto x = fetch_d(x_, (size_t)C * ld_), xr = fetch_d(xr_, (size_t)C * ld_), y = fetch_d(y_, (size_t)C * ld_);
     const auto lp = fetch_d(logpi_, C), qd = fetch_d(quad_, C), bt = fetch_d(beta_, C);
-    const auto mean = fetch_d(mean_, (size_t)C * ld_), cm = fetch_d(cmean_, (size_t)C * ld_);
+    // the batch accumulator's x-space mean (the whitened engine keeps it beside its z mean)
+    const auto mean = fetch_d(mean_x_, (size_t)C * ld_), cm = fetch_d(cmean_, (size_t)C * ld_);
     const auto sg = fetch_d(Sg_, mat_), mg = fetch_d(mg_, ld_);
     std::vector<uint64_t> uc(C);
     DGB_CUDA(cudaMemcpy(uc.data(), uctr_, C * 8, cudaMemcpyDeviceToHost));
@@ -142,10 +173,13 @@ void Engine::save_checkpoint(double wall) {
                 rec.raw(row.data(), row.size() * 8);
             }
         };
-        write_lower(fetch_d(lptr[c], (size_t)d_ * ld_));
-        if (Xinv_) {  // factor_inv (runner.cpp:444-445)
+        // x-space factor L = G^-1 L_z (the engine factors in whitened space)
+        dev_gemm(Ginv_, lptr[c], false, Stmp_, true);
+        write_lower(fetch_d(Stmp_, (size_t)d_ * ld_));
+        if (Xinv_) {  // factor_inv (runner.cpp:444-445): L^-1 = L_z^-1 G
             rec.pod<uint32_t>(1);
-            write_lower(fetch_d(Xinv_ + (size_t)c * mat_, (size_t)d_ * ld_));
+            dev_gemm(Xinv_ + (size_t)c * mat_, G_, false, Stmp_, true);
+            write_lower(fetch_d(Stmp_, (size_t)d_ * ld_));
         } else {
             rec.pod<uint32_t>(0);
         }
@@ -153,14 +187,17 @@ void Engine::save_checkpoint(double wall) {
         rec.pod<uint64_t>(nctr);
         rec.pod<uint64_t>(uc[c]);
         // batch accumulator (empty at a batch boundary unless resumed mid-batch)
-        const auto S = fetch_d(S_ + (size_t)c * mat_, mat_);
-        write_acc(rec, d_, cnt_local_, Vec(mean.begin() + (size_t)c * ld_, mean.begin() + (size_t)c * ld_ + d_),
-                  mirror_lower(S.data(), d_, ld_));
+        Mat sx(d_, d_);
+        if (cnt_local_ > 0) {  // the whitened second moments in x-space: G^-1 S_z G^-T
+            congruence(S_ + (size_t)c * mat_, Ginv_, Sfull_);
+            sx = mirror_lower(fetch_d(Sfull_, mat_).data(), d_, ld_);
+        }
+        write_acc(rec, d_, cnt_local_, Vec(mean.begin() + (size_t)c * ld_, mean.begin() + (size_t)c * ld_ + d_), sx);
         // cumulative accumulator
         Mat cs(d_, d_);
         if (cS_) {
-            const auto cum = fetch_d(cS_ + (size_t)c * mat_, mat_);
-            cs = mirror_lower(cum.data(), d_, ld_);
+            congruence(cS_ + (size_t)c * mat_, Ginv_, Sfull_);
+            cs = mirror_lower(fetch_d(Sfull_, mat_).data(), d_, ld_);
         }
         write_acc(rec, d_, cum_cnt_, Vec(cm.begin() + (size_t)c * ld_, cm.begin() + (size_t)c * ld_ + d_), cs);
         rec.vec(beta_hist_[c]);
@@ -169,14 +206,32 @@ void Engine::save_checkpoint(double wall) {
         for (size_t f = 0; f < fnames_.size(); ++f) rec.vec(traces_[c][f]);
     }
     for (int c = 0; c < C; ++c) ext.vec(Vec(y.begin() + (size_t)c * ld_, y.begin() + (size_t)c * ld_ + d_));
-    std::vector<char> recs = std::move(rec.mem), exts = std::move(ext.mem);
+    BinOut ext2;
+    {
+        auto raw_dev = [&](const double* src, size_t n) {
+            const auto v = fetch_d(src, n);
+            ext2.raw(v.data(), n * 8);
+        };
+        for (int c = 0; c < C; ++c) {
+            raw_dev(lptr[c], (size_t)mat_);
+            if (Xinv_) raw_dev(Xinv_ + (size_t)c * mat_, (size_t)mat_);
+            raw_dev(S_ + (size_t)c * mat_, (size_t)mat_);
+            if (cS_) raw_dev(cS_ + (size_t)c * mat_, (size_t)mat_);
+            raw_dev(mean_ + (size_t)c * ld_, (size_t)ld_);
+            raw_dev(diag_x_ + (size_t)c * ld_, (size_t)ld_);
+            raw_dev(cdiag_ + (size_t)c * ld_, (size_t)ld_);
+        }
+    }
+    std::vector<char> recs = std::move(rec.mem), exts = std::move(ext.mem), ext2s = std::move(ext2.mem);
     if (comm_) {  // a sharded run: every rank's records to rank 0
         auto all_r = comm_->gather_bytes(recs, stream_);
         auto all_e = comm_->gather_bytes(exts, stream_);
+        auto all_e2 = comm_->gather_bytes(ext2s, stream_);
         if (rank_ != 0) return;
         for (int k = 1; k < world_; ++k) {
             recs.insert(recs.end(), all_r[k].begin(), all_r[k].end());
             exts.insert(exts.end(), all_e[k].begin(), all_e[k].end());
+            ext2s.insert(ext2s.end(), all_e2[k].begin(), all_e2[k].end());
         }
     }
     BinOut w(cfg_.checkpoint_path);
@@ -219,6 +274,13 @@ void Engine::save_checkpoint(double wall) {
     // B200 extension: the recursively carried y
     w.raw(kExtMagic, 8);
     w.raw(exts.data(), exts.size());
+    w.raw(kExt2Magic, 8);
+    {
+        const auto sgz = fetch_d(Sgz_, (size_t)mat_), mgz = fetch_d(mgz_, (size_t)ld_);
+        w.raw(sgz.data(), sgz.size() * 8);
+        w.raw(mgz.data(), mgz.size() * 8);
+    }
+    w.raw(ext2s.data(), ext2s.size());
     w.close();
 }
 
@@ -282,6 +344,9 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
         std::copy(gmean.begin(), gmean.end(), m.begin());
         put(mg_, m.data(), ld_);
         put_lower(Sg_, gsec);
+        // the whitened snapshot: Sgz = G Sg G^T, mgz = G mg
+        congruence(Sg_, G_, Sgz_);
+        launch_gemv_rows(G_, ld_, d_, d_, mg_, mgz_, ld_, 1, stream_);
     }
     std::vector<double> lp(C), qd(C), bt(C);
     std::vector<uint64_t> uc(C);
@@ -319,6 +384,8 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
                         break;
                     }
             put_lower(lptr[c], L);
+            dev_gemm(G_, lptr[c], false, Stmp_, true);  // whitened factor L_z = G L
+            DGB_CUDA(cudaMemcpyAsync(lptr[c], Stmp_, (size_t)mat_ * 8, cudaMemcpyDeviceToDevice, stream_));
         } else {
             r.skip((size_t)d_ * d_ * 8);
         }
@@ -327,7 +394,12 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
             if (mine) {
                 Mat X(d_, d_);
                 r.raw(X.a.data(), X.a.size() * 8);
-                if (Xinv_) put_lower(Xinv_ + (size_t)c * mat_, X);
+                if (Xinv_) {  // L_z^-1 = L^-1 G^-1
+                    put_lower(Xinv_ + (size_t)c * mat_, X);
+                    dev_gemm(Xinv_ + (size_t)c * mat_, Ginv_, false, Stmp_, true);
+                    DGB_CUDA(cudaMemcpyAsync(Xinv_ + (size_t)c * mat_, Stmp_, (size_t)mat_ * 8, cudaMemcpyDeviceToDevice,
+                                             stream_));
+                }
             } else {
                 r.skip((size_t)d_ * d_ * 8);
             }
@@ -356,17 +428,22 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
             const Mat s = r.mat();
             std::fill(row.begin(), row.end(), 0.0);
             std::copy(m.begin(), m.end(), row.begin());
-            if (which == 0) {
+            std::vector<double> dg(ld_, 0.0);
+            for (int i = 0; i < d_; ++i) dg[i] = s(i, i);
+            if (which == 0) {  // x-space mean and raw diagonal; whitened S_z = G S G^T
                 cnt_local = cnt;
-                put(mean_ + (size_t)c * ld_, row.data(), ld_);
+                put(mean_x_ + (size_t)c * ld_, row.data(), ld_);
+                put(diag_x_ + (size_t)c * ld_, dg.data(), ld_);
                 put_lower(S_ + (size_t)c * mat_, s);
+                congruence(S_ + (size_t)c * mat_, G_, S_ + (size_t)c * mat_);
             } else {
                 cum = cnt;
                 put(cmean_ + (size_t)c * ld_, row.data(), ld_);
-                std::vector<double> dg(ld_, 0.0);
-                for (int i = 0; i < d_; ++i) dg[i] = s(i, i);
                 put(cdiag_ + (size_t)c * ld_, dg.data(), ld_);
-                if (cS_) put_lower(cS_ + (size_t)c * mat_, s);
+                if (cS_) {
+                    put_lower(cS_ + (size_t)c * mat_, s);
+                    congruence(cS_ + (size_t)c * mat_, G_, cS_ + (size_t)c * mat_);
+                }
             }
         }
         Vec bh = r.vec(), ah = r.vec();
@@ -390,7 +467,9 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
     cum_cnt_ = cum;
     identity_ = all_identity;
 
-    // derived device state: G x, G x_ref, X = L^-1 (a file without it) and y = L^-1 (x - x_ref)
+    // derived device state: the whitened batch mean, G x, G x_ref, X_z = L_z^-1 (a file
+    // without it) and y = L^-1 (x - x_ref) = L_z^-1 (z - z_ref)
+    launch_gemv_rows(G_, ld_, d_, d_, mean_x_, mean_, ld_, C, stream_);
     if (need_inverse) trtri_batched(Lp_, Xinvp_, Tinvp_, ld_, d_, C, nullptr, stream_);
     refresh_g(x_, g_, C, stream_);
     if (k_.adaptive_ref) refresh_g(xr_, gr_, C, stream_);
@@ -408,12 +487,39 @@ void Engine::restore(BinIn& r) {  // proj/src/runner.cpp:164-206
                 put(y_ + (size_t)(pg - c0_) * ld_, row.data(), ld_);
             }
             have_y = true;
+            if (!r.at_end()) {
+                r.raw(magic, 8);
+                if (std::memcmp(magic, kExt2Magic, 8) == 0) {  // this engine's exact whitened state
+                    std::vector<double> buf((size_t)mat_);
+                    auto get = [&](double* dst, size_t n, bool keep) {
+                        if (!keep) {
+                            r.skip(n * 8);
+                            return;
+                        }
+                        r.raw(buf.data(), n * 8);
+                        put(dst, buf.data(), n);
+                    };
+                    get(Sgz_, (size_t)mat_, true);
+                    get(mgz_, (size_t)ld_, true);
+                    for (int pg = 0; pg < P_; ++pg) {
+                        const bool mine = pg >= c0_ && pg < c0_ + C;
+                        const int c = mine ? pg - c0_ : 0;
+                        get(lptr[c], (size_t)mat_, mine);
+                        if (Xinv_) get(Xinv_ + (size_t)c * mat_, (size_t)mat_, mine);
+                        get(S_ + (size_t)c * mat_, (size_t)mat_, mine);
+                        if (cS_) get(cS_ + (size_t)c * mat_, (size_t)mat_, mine);
+                        get(mean_ + (size_t)c * ld_, (size_t)ld_, mine);
+                        get(diag_x_ + (size_t)c * ld_, (size_t)ld_, mine);
+                        get(cdiag_ + (size_t)c * ld_, (size_t)ld_, mine);
+                    }
+                }
+            }
         }
     }
     if (k_.pcn_form() && !have_y) {
         // reference-written checkpoint: solve y; keep the saved quad (the reference's value)
         const double infl = k_.noise_infl();
-        launch_trsv(Lp_, ld_, x_, k_.adaptive_ref ? xr_ : nullptr, ld_, y_, qtmp_, C, d_, 0.5 / (infl * infl),
+        launch_trsv(Lp_, ld_, g_, k_.adaptive_ref ? gr_ : nullptr, ldg_, y_, ld_, qtmp_, C, d_, 0.5 / (infl * infl),
                     nullptr, stream_);
     }
     DGB_CUDA(cudaStreamSynchronize(stream_));

@@ -442,6 +442,47 @@ void Engine::upload_target() {
     DGB_CUDA(cudaMemcpy(inv_eig_, ie.data(), ldg_ * 8, cudaMemcpyHostToDevice));
     DGB_CUDA(cudaMemcpy(bcoef_, bc.data(), ldg_ * 8, cudaMemcpyHostToDevice));
     tri_target_ = true;
+    // G^-1 (accepted increments xi = G^-1 h, the x-space snapshot), G G^T (the jitter of the
+    // whitened covariance: G (C + eps I) G^T = C_z + eps G G^T) and, for twisted targets,
+    // B_T = V_T^T G^-1 (the twisted coordinates of an increment from its whitened h)
+    Ginv_ = dalloc<double>(A, mat_);
+    GG_ = dalloc<double>(A, mat_);
+    {
+        double** pa = ptr_array(A, G_, 0, 1);
+        Ginvp_ = ptr_array(A, Ginv_, 0, 1);
+        double* tscr = nullptr;
+        DGB_CUDA(cudaMalloc(&tscr, (size_t)((d_ + 1) / 2) * ld_ * sizeof(double)));
+        double** tp = nullptr;
+        DGB_CUDA(cudaMalloc(&tp, sizeof(double*)));
+        DGB_CUDA(cudaMemcpy(tp, &tscr, sizeof(double*), cudaMemcpyHostToDevice));
+        trtri_batched(pa, Ginvp_, tp, ld_, d_, 1, nullptr, stream_);
+        GemmBatch gg{};
+        gg.A = (const double* const*)pa;
+        gg.B = (const double* const*)pa;
+        gg.C = ptr_array(A, GG_, 0, 1);
+        gg.lda = gg.ldb = gg.ldc = ld_;
+        gg.M = gg.N = gg.K = d_;
+        gg.alpha = 1.0;
+        gg.tri_b_lower = 1;
+        gg.tri_c_lower = 1;
+        gemm_f64(gg, 1, true, true, stream_);
+        if (T > 0) {
+            BT_ = dalloc<double>(A, (size_t)T * ld_);
+            GemmBatch b{};
+            b.A = (const double* const*)ptr_array(A, G_ + (size_t)d_ * ld_, 0, 1);
+            b.B = (const double* const*)Ginvp_;
+            b.C = ptr_array(A, BT_, 0, 1);
+            b.lda = b.ldb = b.ldc = ld_;
+            b.M = T;
+            b.N = d_;
+            b.K = d_;
+            b.alpha = 1.0;
+            gemm_f64(b, 1, true, false, stream_);
+        }
+        DGB_CUDA(cudaStreamSynchronize(stream_));
+        cudaFree(tp);
+        cudaFree(tscr);
+    }
     Ct_ = dalloc<double>(A, (size_t)d_ * d_);
     DGB_CUDA(cudaMemcpy(Ct_, tgt_.covariance.a.data(), (size_t)d_ * d_ * 8, cudaMemcpyHostToDevice));
     std::vector<double> pj(2 * ld_, 0.0);
@@ -491,13 +532,22 @@ void Engine::init_chains() {
     h_flags_ = static_cast<int*>(pinned_acquire(3 * (size_t)C * sizeof(int)));
     Sg_ = dalloc<double>(A, mat_);
     mg_ = dalloc<double>(A, ld_);
-    Ssum_ = dalloc<double>(A, (size_t)d_ * (d_ + 1) / 2 + ld_);  // packed lower sum + mean sum
+    Ssum_ = dalloc<double>(A, (size_t)d_ * (d_ + 1) / 2 + 2 * ld_);  // packed lower sum, z mean, x mean
     cov_part_ = dalloc<double>(A, 2 * (size_t)d_);
     if (!cfg_.checkpoint_path.empty()) cS_ = dalloc<double>(A, (size_t)C * mat_);
     if (k_.use_explicit_inverse) {
         Xinv_ = dalloc<double>(A, (size_t)C * mat_);
         Tinv_ = dalloc<double>(A, (size_t)C * ((d_ + 1) / 2) * ld_);
     }
+    mean_x_ = dalloc<double>(A, (size_t)C * ld_);
+    diag_x_ = dalloc<double>(A, (size_t)C * ld_);
+    Sgz_ = dalloc<double>(A, mat_);
+    mgz_ = dalloc<double>(A, ld_);
+    Sfull_ = dalloc<double>(A, mat_);
+    Stmp_ = dalloc<double>(A, mat_);
+    state_src_ = dalloc<int>(A, (size_t)C * Lw_);
+    state_mult_ = dalloc<int>(A, (size_t)C * Lw_);
+    acc_cnt_ = dalloc<int>(A, C);
     const size_t M = cfg_.intervals_per_batch;
     trace_lp_ = dalloc<double>(A, M * C * Lw_);
     kcount_ = dalloc<int>(A, C);
@@ -512,6 +562,12 @@ void Engine::init_chains() {
     Xip_ = ptr_array(A, Xi_, win_, C);
     Hp_ = ptr_array(A, H_, winh_, C);
     Gpc_ = ptr_array(A, G_, 0, C);  // G once per chain (batched GEMMs)
+    Ginvpc_ = ptr_array(A, Ginv_, 0, C);
+    ptr_gen_ = ptr_array(A, Sfull_, 0, 3);
+    ptr_tmp_[0] = ptr_array(A, Sfull_, 0, 1);
+    ptr_tmp_[1] = ptr_array(A, Stmp_, 0, 1);
+    ptr_tmp_[2] = ptr_array(A, Sg_, 0, 1);
+    if (BT_) BTpc_ = ptr_array(A, BT_, 0, C);
     Sp_ = ptr_array(A, S_, mat_, C);
     if (Xinv_) {
         Xinvp_ = ptr_array(A, Xinv_, mat_, C);
@@ -536,19 +592,23 @@ void Engine::init_chains() {
     DGB_CUDA(cudaStreamSynchronize(0));  // the buffers above are zeroed before stream_ uses them
     // x0 = dispersion * N(0, I) from the "init" stream (runner.cpp:131-132)
     launch_normal_vec(x_, ld_, C, d_, ikeys_, 0, cfg_.init_dispersion, stream_);
-    // factor = I, beta = beta_init (proposal.cpp:95-97)
-    launch_set_identity(L_, fmat_, C, d_, ld_, stream_);
-    if (Xinv_) launch_set_identity(Xinv_, mat_, C, d_, ld_, stream_);  // I^{-1} (proposal.cpp:98)
+    // factor = I, beta = beta_init (proposal.cpp:95-97): in whitened space L_z = G I = G, and the
+    // explicit inverse L_z^-1 = G^-1
+    for (int c = 0; c < C; ++c) {
+        DGB_CUDA(cudaMemcpyAsync(L_ + (size_t)c * fmat_, G_, (size_t)mat_ * 8, cudaMemcpyDeviceToDevice, stream_));
+        if (Xinv_)
+            DGB_CUDA(cudaMemcpyAsync(Xinv_ + (size_t)c * mat_, Ginv_, (size_t)mat_ * 8, cudaMemcpyDeviceToDevice,
+                                     stream_));
+    }
     std::vector<double> b(C, k_.beta_init);
     DGB_CUDA(cudaMemcpyAsync(beta_, b.data(), C * 8, cudaMemcpyHostToDevice, stream_));
-    identity_ = true;
-    // log pi(x0), quad(x0) (proposal.cpp:107-108)
+    identity_ = false;
+    // log pi(x0), quad(x0) (proposal.cpp:107-108); with the identity factor y = x - 0 exactly
     refresh_g(x_, g_, C, stream_);
     launch_eval_logpi(g_, inv_eig_, bcoef_, logpi_, C, dg_, ldg_, stream_);  // whitened form
     if (k_.pcn_form()) {
         const double infl = k_.noise_infl();
-        if (Xinv_) launch_trmv_quad(Xinvp_, ld_, x_, nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl), stream_);
-        else launch_trsv(Lp_, ld_, x_, nullptr, ld_, y_, quad_, C, d_, 0.5 / (infl * infl), nullptr, stream_);
+        launch_init_yq(x_, ld_, y_, quad_, C, d_, 0.5 / (infl * infl), stream_);
     }
     DGB_CUDA(cudaStreamSynchronize(stream_));
 
@@ -676,14 +736,13 @@ const std::map<std::string, KernelStat>& Engine::stats() {
 }
 
 double Engine::flops_per_batch() const {
-    // algorithmic FP64 flops of one batch over the local chains:
-    // TRMM d(d+1) per row, target product d(d+1) per row (whitened Gaussian: triangular G) or
-    // 2 d^2 (twisted: V^T), SYRK d(d+1) per row (bench.py scales it to the distinct rows),
-    // POTRF d^3/3 per window
+    // algorithmic FP64 flops of one batch over the local chains, upper bound:
+    // the window product H = s W L_z^T d(d+1) per row, the twisted rows 2dT, the SYRK d(d+1)
+    // and the accepted increments d(d+1) per row if every step were accepted (bench.py counts
+    // the rows they actually ran over), POTRF d^3/3 per window
     const double d = d_, L = Lw_, C = C_, M = (double)cfg_.intervals_per_batch;
-    const double tgt = d * (d + 1) + 2.0 * d * (dg_ - d_);  // whitening factor + twisted rows
-    const double per_window = C * (L * d * (d + 1) + L * tgt + L * d * (d + 1) + d * d * d / 3.0);
-    return per_window * M;
+    const double per_row = d * (d + 1) + 2.0 * d * (dg_ - d_) + 2.0 * d * (d + 1);
+    return M * C * (L * per_row + d * d * d / 3.0);
 }
 
 void Engine::fork_groups() {
@@ -854,21 +913,23 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     const int C = g.C, o = g.off;
     const cudaStream_t s = g.s;
     const double infl = k_.noise_infl();
-    // ---- noise: W from Philox, Xi = s W L^T, H = Xi G^T (proposal.cpp:254-266); row r of
-    // the window draws counters nctr + r d .. nctr + (r + 1) d - 1 of the chain's stream
+    // ---- noise (proposal.cpp:254-266): W from Philox, row r of the window drawing counters
+    // nctr + r d .. nctr + (r + 1) d - 1 of the chain's stream; then H = s W L_z^T, i.e.
+    // h_t = G xi_t with xi_t = s L w_t: the factor is kept in whitened space (L_z = G L), so
+    // this one triangular product gives the target's coordinates of every increment
     timed_begin(s);
     for (int rep = (twice_ & kTwiceNormals) ? 2 : 1; rep > 0; --rep)
-        launch_normals(W_ + o * win_, p.identity ? Xi_ + o * win_ : nullptr, win_, C, rows, d_, ld_, nkeys_ + o,
-                       p.nctr + (uint64_t)r0 * d_, beta_ + o, infl, s);
+        launch_normals(W_ + o * win_, nullptr, win_, C, rows, d_, ld_, nkeys_ + o, p.nctr + (uint64_t)r0 * d_,
+                       beta_ + o, infl, s);
     timed_end("normals", 0.0, s);
-    if (!p.identity) {
+    {
         GemmBatch t{};
         t.A = (const double* const*)g.Wp;
         t.B = (const double* const*)g.Lp;
-        t.C = g.Xip;
+        t.C = Hp_ + o;
         t.lda = ld_;
         t.ldb = ld_;
-        t.ldc = ld_;
+        t.ldc = ldg_;
         t.M = rows;
         t.N = d_;
         t.K = d_;
@@ -880,36 +941,28 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         gemm("trmm_noise", t, C, true, true, s);
         if (twice_ & kTwiceTrmm) gemm("trmm_noise", t, C, true, true, s);
     }
-    {
-        GemmBatch h{};
-        h.B = (const double* const*)Gp_;
-        h.lda = ld_;
-        h.ldb = ld_;
-        h.ldc = ldg_;
-        h.N = dg_;
-        h.K = d_;
-        h.alpha = 1.0;
-        h.beta = 0.0;
-        // G lower over its first d rows (the whitening factor): K clipped per column tile;
-        // the twisted rows below are full (K = d)
-        h.tri_b_lower = tri_target_ ? 1 : 0;
-        const double tfl = (double)rows * C * ((double)d_ * (d_ + 1) + 2.0 * d_ * (dg_ - d_));
-        if (rows == Lc_) {
-            h.A = (const double* const*)g.Xib;
-            h.C = g.Hb;
-            h.M = C * Lc_;  // the group's window chunks are one contiguous (C Lc) x ld matrix
-            gemm("gemm_target", h, 1, true, true, s, tfl);
-            if (twice_ & kTwiceTarget) gemm("gemm_target", h, 1, true, true, s, tfl);
-        } else {            // ragged last chunk: per-chain pieces
-            h.B = (const double* const*)Gpc_;
-            h.A = (const double* const*)g.Xip;
-            h.C = Hp_ + o;
-            h.M = rows;
-            gemm("gemm_target", h, C, true, true, s, tfl);
-        }
+    if (BT_) {
+        // twisted targets: the T twisted coordinates of each increment, V_T^T xi = B_T h
+        // (B_T = V_T^T G^-1), into columns d.. of the H rows
+        GemmBatch b{};
+        b.A = (const double* const*)(Hp_ + o);
+        b.B = (const double* const*)(BTpc_ + o);
+        b.C = Hp_ + o;
+        b.c_off = d_;
+        b.lda = ldg_;
+        b.ldb = ld_;
+        b.ldc = ldg_;
+        b.M = rows;
+        b.N = dg_ - d_;
+        b.K = d_;
+        b.alpha = 1.0;
+        gemm("gemm_target", b, C, true, true, s);
+        if (twice_ & kTwiceTarget) gemm("gemm_target", b, C, true, true, s);
     }
+    // parity capture: W before the steps reuse its consumed rows
+    if (capture_) capture_chunk(g, r0, rows);
 
-    // ---- the chunk's MH steps (proposal.cpp:137-157, runner.cpp:363-368)
+    // ---- the chunk's MH steps (proposal.cpp:137-157, runner.cpp:363-368), in whitened space
     StepParams sp{};
     sp.d = d_;
     sp.n_lag = rows;
@@ -923,10 +976,8 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     sp.dg = dg_;
     sp.ldg = ldg_;
     sp.hwin_stride = winh_;
-    sp.x = x_ + o * ld_;
     sp.g = g_ + o * ldg_;
     sp.y = y_ + o * ld_;
-    sp.xr = k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
     sp.gr = k_.adaptive_ref ? gr_ + o * ldg_ : nullptr;
     sp.log_pi = logpi_ + o;
     sp.quad = quad_ + o;
@@ -949,25 +1000,35 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
     const bool project = p.record && cfg_.trace_eigen_projections;
     sp.first = lf;
     sp.kcount = kcount_ + o;
+    sp.acc_count = acc_cnt_ + o;
+    sp.state_src = state_src_ + (size_t)o * Lw_;
+    sp.state_mult = state_mult_ + (size_t)o * Lw_;
     sp.row_of = project ? row_of_ + (size_t)o * Lw_ + r0 : nullptr;
     // the previous batch's trace copies read the buffers the MH steps write
     if (merge_pending_ && p.record) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
     timed_begin(s);
-    launch_mh_window(sp, true, s);  // every target in whitened form: -1/2 sum twist(G x)^2 / sigma^2
+    launch_mh_window(sp, s);
     timed_end("mh_window", 0.0, s);
-    if (capture_) capture_chunk(g, r0, rows);
 
-    // ---- moments of the chunk's counted states (proposal.cpp:153-155, moments.cpp:5-20): the
-    // MH kernel compacted them into kcount_c distinct states x_j (rows of Xi) and their
-    // weighted copies m_j x_j (rows of H), so S <- (cb S + sum_j m_j x_j x_j^T) / (cb + kc)
-    // is a SYRK over about acceptance x kc rows instead of kc
+    // ---- moments of the chunk's counted states (proposal.cpp:153-155, moments.cpp:5-20) in
+    // whitened space: the MH kernel compacted them into kcount_c distinct states z_j (rows of W)
+    // and their weighted copies m_j z_j (rows of H), so S_z <- (cb S_z + sum_j m_j z_j z_j^T)
+    // / (cb + kc) is a SYRK over about acceptance x kc rows instead of kc
     // the merge reads S_ / mean_ and clears mean_; the histories' copies read hist_*
     if (merge_pending_) DGB_CUDA(cudaStreamWaitEvent(s, merge_ev_, 0));
+    auto device_count = [&](const int* v) {  // profiling: the rows a data-dependent GEMM ran over
+        std::vector<int> h(C);
+        DGB_CUDA(cudaStreamSynchronize(s));
+        DGB_CUDA(cudaMemcpy(h.data(), v, C * sizeof(int), cudaMemcpyDeviceToHost));
+        double n = 0.0;
+        for (int x : h) n += x;
+        return n;
+    };
     if (kc > 0) {
         const double total = (double)(cb + (uint64_t)kc);
         GemmBatch m{};
         m.A = (const double* const*)(Hp_ + o);
-        m.B = (const double* const*)g.Xip;
+        m.B = (const double* const*)g.Wp;
         m.C = g.Sp;
         m.lda = ldg_;
         m.ldb = ld_;
@@ -979,18 +1040,34 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         m.alpha = 1.0 / total;
         m.beta = (double)cb / total;
         m.tri_c_lower = 1;
-        double fl = -1.0;
-        if (profiling_) {
-            // the SYRK runs over each chain's distinct states only (kcount_, written by the
-            // MH kernel): count those rows, d (d+1) flops each
-            std::vector<int> kc_h(C);
-            DGB_CUDA(cudaStreamSynchronize(s));
-            DGB_CUDA(cudaMemcpy(kc_h.data(), kcount_ + o, C * sizeof(int), cudaMemcpyDeviceToHost));
-            fl = 0.0;
-            for (int v : kc_h) fl += (double)v * d_ * (d_ + 1.0);
-        }
+        const double fl = profiling_ ? device_count(kcount_ + o) * d_ * (d_ + 1.0) : -1.0;
         gemm("syrk_moments", m, C, false, false, s, fl);
         launch_mean_update(mean_ + o * ld_, ld_, H_ + o * winh_, winh_, ldg_, C, d_, kcount_ + o, kc, (double)cb, s);
+    }
+    // ---- the chunk's x-space states: xi_k = G^-1 h_k for its accepted steps only (rows of Xi
+    // into rows of H), then the reference's exact recursion x <- x_ref + c (x - x_ref) + xi_k
+    {
+        GemmBatch a{};
+        a.A = (const double* const*)g.Xip;
+        a.B = (const double* const*)(Ginvpc_ + o);
+        a.C = Hp_ + o;
+        a.lda = ld_;
+        a.ldb = ld_;
+        a.ldc = ldg_;
+        a.M = rows;
+        a.m_vec = acc_cnt_ + o;
+        a.N = d_;
+        a.K = d_;
+        a.alpha = 1.0;
+        a.tri_b_lower = 1;
+        const double fl = profiling_ ? device_count(acc_cnt_ + o) * d_ * (d_ + 1.0) : -1.0;
+        gemm("xi_accepted", a, C, true, true, s, fl);
+        timed_begin(s);
+        launch_reconstruct(x_ + o * ld_, k_.adaptive_ref ? xr_ + o * ld_ : nullptr, beta_ + o, k_.pcn_form() ? 1 : 0,
+                           H_ + o * winh_, winh_, ldg_, Xi_ + o * win_, win_, ld_, state_src_ + (size_t)o * Lw_,
+                           state_mult_ + (size_t)o * Lw_, Lw_, kcount_ + o, acc_cnt_ + o, mean_x_ + o * ld_,
+                           diag_x_ + o * ld_, (double)cb, kc, C, d_, s);
+        timed_end("reconstruct", 0.0, s);
     }
     if (project)
         launch_project_rows(Xi_ + o * win_, win_, ld_, C, rows, lf, d_, proj_,
@@ -1004,28 +1081,35 @@ void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {
     // the refactor stream continues after the window's steps
     DGB_CUDA(cudaEventRecord(g.ev_steps, g.s));
     DGB_CUDA(cudaStreamWaitEvent(g.sr, g.ev_steps, 0));
+    // g = G x re-anchored from the reconstructed x-space state at every boundary (the steps
+    // carry g by recursion); the augmented row, the quad and the next window start from it
+    refresh_g(x_ + o * ld_, g_ + o * ldg_, C, s);
     if (p.refactor) {
-        // blend -> covariance into the workspace factor, trace floor, POTRF (proposal.cpp:176-184).
-        // pCN-form kernels append r = x - x_ref as row d: the factorization then also
-        // delivers L'^{-1} r for the usable guard (no separate triangular solve).
+        // blend -> covariance into the workspace factor, trace floor, POTRF (proposal.cpp:176-184),
+        // in whitened space: C_z = G C G^T from the whitened moments, so the factor is L_z = G L;
+        // the trace floor and the blended mean (adaptive reference) from the x-space statistics.
+        // pCN-form kernels append r = z - z_ref (the whitened x - x_ref) as row d: the
+        // factorization then also delivers L_z'^{-1} r = L'^{-1} (x - x_ref) for the usable guard.
         const bool aug = k_.pcn_form();
-        const double* ax = aug ? x_ + o * ld_ : nullptr;
-        const double* axr = aug && k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
+        const double* ax = aug ? g_ + o * ldg_ : nullptr;
+        const double* axr = aug && k_.adaptive_ref ? gr_ + o * ldg_ : nullptr;
         // shared workspace: wait until the previous group's tail has released it
         if (pool_ && pool_last_) DGB_CUDA(cudaStreamWaitEvent(s, pool_last_, 0));
+        auto blend = [&] {
+            launch_trace_x(Sg_, mg_, diag_x_ + o * ld_, mean_x_ + o * ld_, p.wg, p.wl, mb_ + o * ld_, tr_ + o, try_ + o,
+                           C, d_, ld_, s);
+            launch_blend_cov(g.Lnp, Sgz_, mgz_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, nullptr, ld_, C,
+                             d_, ld_, nullptr, 0.0, nullptr, GG_, s, ax, axr, ldg_);
+        };
         timed_begin(s);
-        launch_blend_cov(g.Lnp, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, mb_ + o * ld_, ld_, C,
-                         d_, ld_, nullptr, 0.0, nullptr, s, ax, axr);
+        blend();
         timed_end("blend_cov", 0.0, s);
-        launch_trace_floor(g.Lnp, ld_, mb_ + o * ld_, ld_, C, d_, tr_ + o, try_ + o, s);
         DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
         nvtxRangePushA("potrf");
         timed_begin(s);
         potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
         if (twice_ & kTwicePotrf) {  // blend + factorization again: same inputs, same factor
-            launch_blend_cov(g.Lnp, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, mb_ + o * ld_, ld_,
-                             C, d_, ld_, nullptr, 0.0, nullptr, s, ax, axr);
-            launch_trace_floor(g.Lnp, ld_, mb_ + o * ld_, ld_, C, d_, tr_ + o, try_ + o, s);
+            blend();
             DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
             potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
         }
@@ -1095,14 +1179,15 @@ void Engine::ladder_retry(Group& g, const WindowPlan& p, Ladder& st) {
     const int C = g.C, o = g.off;
     const cudaStream_t s = g.sr;
     const bool aug = k_.pcn_form();
-    const double* ax = aug ? x_ + o * ld_ : nullptr;
-    const double* axr = aug && k_.adaptive_ref ? xr_ + o * ld_ : nullptr;
+    const double* ax = aug ? g_ + o * ldg_ : nullptr;
+    const double* axr = aug && k_.adaptive_ref ? gr_ + o * ldg_ : nullptr;
     // mask through the pinned status mirror's third block (the copy is stream-ordered)
     int* hm = h_flags_ + 2 * C_ + o;
     std::copy(st.failing.begin(), st.failing.end(), hm);
     DGB_CUDA(cudaMemcpyAsync(mask_ + o, hm, C * sizeof(int), cudaMemcpyHostToDevice, s));
-    launch_blend_cov(g.Lnp, Sg_, mg_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, mb_ + o * ld_, ld_, C,
-                     d_, ld_, mask_ + o, st.eps, tr_ + o, s, ax, axr);
+    // C_z + eps (tr / d) G G^T = G (C + eps (tr / d) I) G^T: the reference's jitter, whitened
+    launch_blend_cov(g.Lnp, Sgz_, mgz_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, nullptr, ld_, C, d_,
+                     ld_, mask_ + o, st.eps, tr_ + o, GG_, s, ax, axr, ldg_);
     DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
     potrf_batched(g.Lnp, ld_, d_, C, mask_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
     DGB_CUDA(cudaMemcpyAsync(h_flags_ + o, status_ + o, C * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1137,7 +1222,7 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
     }
     // adaptive reference point (proposal.cpp:206-208)
     if (p.move_ref) {
-        if (!p.refactor) launch_blend_mean(mg_, mean_ + o * ld_, p.wg, p.wl, mb_ + o * ld_, C, d_, ld_, s);
+        if (!p.refactor) launch_blend_mean(mg_, mean_x_ + o * ld_, p.wg, p.wl, mb_ + o * ld_, C, d_, ld_, s);
         DGB_CUDA(cudaMemcpyAsync(xr_ + o * ld_, mb_ + o * ld_, (size_t)C * ld_ * 8, cudaMemcpyDeviceToDevice, s));
         refresh_g(xr_ + o * ld_, gr_ + o * ldg_, C, s);
     }
@@ -1145,19 +1230,18 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
     // With a fixed reference point y = L^-1 (x - x_ref) is carried exactly through the
     // steps (c y + s w) and re-anchored from the augmented POTRF row whenever the factor
     // changes, so only a moving reference point needs a fresh triangular solve.
+    // In whitened coordinates: L^-1 (x - x_ref) = L_z^-1 (z - z_ref), z = G x.
     if (k_.pcn_form() && Xinv_) {
         // the reference's quad_term through factor_inv (tri_matvec, proposal.cpp:55) at every
-        // boundary, whether or not the factor changed
-        launch_trmv_quad(Xinvp_ + o, ld_, x_ + o * ld_, k_.adaptive_ref ? xr_ + o * ld_ : nullptr, ld_, y_ + o * ld_,
-                         quad_ + o, C, d_, 0.5 / (infl * infl), s);
+        // boundary, whether or not the factor changed (X_z = L_z^-1)
+        launch_trmv_quad(Xinvp_ + o, ld_, g_ + o * ldg_, k_.adaptive_ref ? gr_ + o * ldg_ : nullptr, ldg_,
+                         y_ + o * ld_, ld_, quad_ + o, C, d_, 0.5 / (infl * infl), s);
     } else if (k_.pcn_form() && k_.adaptive_ref) {
         timed_begin(s);
-        launch_trsv(g.Lp, ld_, x_ + o * ld_, xr_ + o * ld_, ld_, y_ + o * ld_, quad_ + o, C, d_, 0.5 / (infl * infl),
-                    nullptr, s);
+        launch_trsv(g.Lp, ld_, g_ + o * ldg_, gr_ + o * ldg_, ldg_, y_ + o * ld_, ld_, quad_ + o, C, d_,
+                    0.5 / (infl * infl), nullptr, s);
         timed_end("trsv", 0.0, s);
     }
-    // G x re-anchored at every boundary so the step recursion never drifts
-    refresh_g(x_ + o * ld_, g_ + o * ldg_, C, s);
     // the next window's steps follow the tail
     DGB_CUDA(cudaEventRecord(g.ev_ref, g.sr));
     DGB_CUDA(cudaStreamWaitEvent(g.s, g.ev_ref, 0));
@@ -1203,18 +1287,23 @@ void Engine::merge_batch() {
     if (incoming > 0) {
         double keep = 1.0, wp = 0.0;
         merge_weights(cnt_g_, (uint64_t)P_, cnt_local_, &keep, &wp);
+        // whitened packed S_z and mean m_z (the blend's snapshot), the x-space mean and raw
+        // diagonal (the reported snapshot's mean, the trace floor); one all-reduce
         const int64_t tri = (int64_t)d_ * (d_ + 1) / 2;
         timed_begin(stream_);
         launch_sum_chains_lower(Ssum_, S_, mat_, C_, d_, ld_, stream_);
         launch_sum_chains(Ssum_ + tri, mean_, ld_, C_, ld_, 1.0, stream_);
-        if (comm_) comm_->allreduce_sum(Ssum_, tri + ld_, stream_);
-        launch_merge_lower(Sg_, ld_, Ssum_, d_, keep, wp, stream_);
-        launch_axpby(mg_, Ssum_ + tri, ld_, wp, keep, stream_);
+        launch_sum_chains(Ssum_ + tri + ld_, mean_x_, ld_, C_, ld_, 1.0, stream_);
+        if (comm_) comm_->allreduce_sum(Ssum_, tri + 2 * ld_, stream_);
+        launch_merge_lower(Sgz_, ld_, Ssum_, d_, keep, wp, stream_);
+        launch_axpby(mgz_, Ssum_ + tri, ld_, wp, keep, stream_);
+        launch_axpby(mg_, Ssum_ + tri + ld_, ld_, wp, keep, stream_);
+        update_x_snapshot();  // Sg_ = G^-1 Sgz_ G^-T
         timed_end("merge", 0.0, stream_);
         cnt_g_ += incoming;
         const double ct = (double)(cum_cnt_ + cnt_local_);
-        launch_cum_fold(cmean_, cdiag_, mean_, S_, mat_, C_, d_, ld_, (double)cum_cnt_ / ct, (double)cnt_local_ / ct,
-                        stream_);
+        launch_cum_fold(cmean_, cdiag_, mean_x_, diag_x_, ld_, C_, d_, ld_, (double)cum_cnt_ / ct,
+                        (double)cnt_local_ / ct, stream_);
         // full cumulative second moments only when they must be checkpointed (merge_into,
         // proj/src/moments.cpp:77-88); the PSRF needs just the diagonal kept above
         if (cS_) launch_axpby(cS_, S_, (int64_t)C_ * mat_, (double)cnt_local_ / ct, (double)cum_cnt_ / ct, stream_);
@@ -1224,7 +1313,34 @@ void Engine::merge_batch() {
     // update runs with weight cb/total = 0 on the old value, which the GEMM then never reads
     // (beta = 0), and nothing reads S_ with a nonzero weight before that update
     DGB_CUDA(cudaMemsetAsync(mean_, 0, (size_t)C_ * ld_ * 8, stream_));
+    DGB_CUDA(cudaMemsetAsync(mean_x_, 0, (size_t)C_ * ld_ * 8, stream_));
+    DGB_CUDA(cudaMemsetAsync(diag_x_, 0, (size_t)C_ * ld_ * 8, stream_));
     cnt_local_ = 0;
+}
+
+void Engine::update_x_snapshot() {
+    // the reported snapshot from the whitened one: Sg_ = G^-1 Sgz_ G^-T (raw second moments
+    // transform by congruence; mg_ is merged directly). Sgz_ holds the lower triangle: mirrored
+    // into Sfull_, then Stmp_ = Sfull_ G^-T and Sg_ = lower(G^-1 Stmp_)
+    launch_mirror_lower(Sgz_, Sfull_, d_, ld_, stream_);
+    GemmBatch a{};
+    a.A = (const double* const*)ptr_tmp_[0];
+    a.B = (const double* const*)Ginvp_;
+    a.C = ptr_tmp_[1];
+    a.lda = a.ldb = a.ldc = ld_;
+    a.M = a.N = a.K = d_;
+    a.alpha = 1.0;
+    a.tri_b_lower = 1;
+    gemm_f64(a, 1, true, true, stream_);
+    GemmBatch b{};
+    b.A = (const double* const*)Ginvp_;
+    b.B = (const double* const*)ptr_tmp_[1];
+    b.C = ptr_tmp_[2];
+    b.lda = b.ldb = b.ldc = ld_;
+    b.M = b.N = b.K = d_;
+    b.alpha = 1.0;
+    b.tri_c_lower = 1;
+    gemm_f64(b, 1, true, false, stream_);
 }
 
 void Engine::collect_histories(size_t windows, const std::vector<uint64_t>& n_start, const double* rate,

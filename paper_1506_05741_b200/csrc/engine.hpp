@@ -240,7 +240,22 @@ private:
     double* h_out_ = nullptr;  // pinned per-batch outputs: rate, beta (M x C), traces (M x C x Lw x 3)
     cudaEvent_t out_ev_ = nullptr;  // the copies into h_out_ / h_stats_ are done
     double* gather_ = nullptr;                                // PSRF all-gather buffer
-    double* cS_ = nullptr;  // cumulative raw second moments (lower), kept only for checkpoints
+    double* cS_ = nullptr;  // cumulative raw second moments (whitened, lower), kept only for checkpoints
+    // whitened-space factorization: the factors L_ are L_z = G L, the local and
+    // global second moments S_ / Sgz_ and means mean_ / mgz_ are in whitened coordinates; the
+    // x-space statistics the reference reports are kept beside them: per chain the running mean
+    // and raw diagonal (mean_x_, diag_x_; PSRF, trace floor, adaptive reference), globally the
+    // snapshot Sg_ / mg_ (Sg_ = G^-1 Sgz_ G^-T once per batch; cov error, results, checkpoints)
+    double *Ginv_ = nullptr, *GG_ = nullptr, *BT_ = nullptr;  // G^-1, G G^T (jitter), V_T^T G^-1
+    double **Ginvp_ = nullptr, **Ginvpc_ = nullptr, **BTpc_ = nullptr;
+    double *mean_x_ = nullptr, *diag_x_ = nullptr, *Sgz_ = nullptr, *mgz_ = nullptr;
+    double *Sfull_ = nullptr, *Stmp_ = nullptr;  // per-batch x-space transform scratch
+    double** ptr_tmp_[3] = {nullptr, nullptr, nullptr};  // Sfull_, Stmp_, Sg_ as GEMM operands
+    int *state_src_ = nullptr, *state_mult_ = nullptr, *acc_cnt_ = nullptr;
+    void update_x_snapshot();  // Sg_ = G^-1 Sgz_ G^-T
+    double** ptr_gen_ = nullptr;  // 3 device pointers for dev_gemm
+    void dev_gemm(const double* A, const double* B, bool bk, double* out, bool tri);
+    void congruence(const double* S, const double* M, double* out);
     // use_explicit_inverse: X = L^{-1} per chain (upper part zero) and the TRTRI scratch
     double* Xinv_ = nullptr;
     double* Tinv_ = nullptr;

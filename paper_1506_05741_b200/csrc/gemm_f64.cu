@@ -18,15 +18,16 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) gemm_f64_kernel(GemmBat
     const int nt = p.tri_b_lower ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
     const int n0 = nt * CF::BN;
     const int m0 = blockIdx.y * CF::BM;
-    if (n0 >= p.N || m0 >= p.M) return;
+    const int M = p.m_vec ? min(p.M, p.m_vec[b]) : p.M;
+    if (n0 >= p.N || m0 >= M) return;
     if (p.tri_c_lower && n0 > m0 + CF::BM - 1) return;
     extern __shared__ __align__(16) double smem[];
     int K = p.k_vec ? p.k_vec[b] : p.K;
     if (p.tri_b_lower) K = min(K, n0 + CF::BN);
     double alpha = p.alpha;
     if (p.alpha_vec) alpha *= p.alpha_vec[b] * p.alpha_vec_mul;
-    tile::gemm_tile<CF, AK, BKM>(p.A[b] + p.a_off, p.B[b] + p.b_off, p.C[b] + p.c_off, p.lda, p.ldb, p.ldc, p.M, p.N,
-                                 K, m0, n0, alpha, p.beta, p.tri_c_lower != 0, smem, p.tri_b_lower != 0);
+    tile::gemm_tile<CF, AK, BKM>(p.A[b] + p.a_off, p.B[b] + p.b_off, p.C[b] + p.c_off, p.lda, p.ldb, p.ldc, M, p.N, K,
+                                 m0, n0, alpha, p.beta, p.tri_c_lower != 0, smem, p.tri_b_lower != 0);
 }
 
 template <class CF, bool AK, bool BKM>

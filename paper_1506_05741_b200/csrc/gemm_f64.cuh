@@ -46,6 +46,7 @@ struct GemmBatch {
     int tri_c_lower;           // compute/store only n <= m
     const int* k_vec;          // optional per-batch contraction length (<= K); 0 leaves
                                // C = beta C
+    const int* m_vec;          // optional per-batch row count (<= M): rows past it untouched
 };
 
 // Launch the batched GEMM on `stream`. Layout flags select the template instance.

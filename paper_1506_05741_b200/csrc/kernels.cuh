@@ -44,19 +44,20 @@ struct StepParams {
     int dg;               // entries of g = G x and of the H rows (d + the twisted rows)
     int64_t ldg;          // their stride
     int64_t hwin_stride;  // per-chain stride of the H window
-    const double* W;
-    double* Xi;       // in: increments; out: the window's DISTINCT counted post-step states,
-                      // compacted: row j = the j-th distinct state from step `first` on
-    double* H;        // G * increments; consumed rows are overwritten with the weighted
-                      // states, row j = m_j * (row j of Xi), m_j = steps spent in state j
+    double* W;        // in: the window's normals; out: row j = z_j (the j-th distinct counted
+                      // state's whitened coordinates, the moment SYRK's B operand)
+    double* Xi;       // out: row k = the z part of h_t of the k-th accepted step
+    double* H;        // in: h_t = G xi_t rows (s W L_z^T); out: row j = m_j z_j, m_j = the
+                      // counted steps spent in state j
     int first;        // first counted step of this chunk (proj/src/proposal.cpp:153-155)
-    int* kcount;      // [chain]: distinct counted states of the chunk (rows of Xi / H)
-    int* row_of;      // [chain][out_ld], nullable: the Xi row holding the state after step t
-    double* x;
+    int* kcount;      // [chain]: distinct counted states of the chunk
+    int* acc_count;   // [chain]: accepted steps of the chunk
+    int* state_src;   // [chain][out_ld]: distinct state j = the state after accepted step src_j (-1: start)
+    int* state_mult;  // [chain][out_ld]: m_j
+    int* row_of;      // [chain][out_ld], nullable: the distinct state after step t
     double* g;
     double* y;
-    const double* xr;  // null: zero reference point
-    const double* gr;
+    const double* gr;  // null: zero reference point
     double* log_pi;
     double* quad;
     const double* beta;
@@ -65,15 +66,22 @@ struct StepParams {
     uint64_t* uctr;  // advanced by n_lag
     double infl;
     int pcn;  // pCN-form kernels (pCN, DIAM)
-    const double* inv_eig;  // twisted: 1/sigma^2 (len d)
-    const double* bcoef;    // twisted: twist coefficients (len d)
+    const double* inv_eig;  // per g entry: the whitened log density's weights (Engine::upload_target)
+    const double* bcoef;    // per g entry: twist coefficients / subtraction flags
     double* trace_lp;       // [chain][out_ld], nullable
     uint8_t* accept_out;    // [chain][out_ld], nullable
     double* log_ratio_out;  // [chain][out_ld], nullable (parity tests)
     int out_ld;             // per-chain stride of the outputs above (the window length: a
                             // chunk of a window writes at its row offset); 0 = n_lag
 };
-void launch_mh_window(const StepParams& p, bool twisted, cudaStream_t s);
+void launch_mh_window(const StepParams& p, cudaStream_t s);
+// x-space states of a chunk from its accepted increments XA (rows k, xi_k = G^-1 h_k): the final
+// x, the distinct counted states x_j into Xout rows, and the running x-space mean / raw
+// diagonal over the chunk's kc counted steps after n_prev earlier ones
+void launch_reconstruct(double* x, const double* xr, const double* beta, int pcn, const double* XA, int64_t xa_stride,
+                        int64_t xa_ld, double* Xout, int64_t xo_stride, int64_t ld, const int* state_src,
+                        const int* state_mult, int out_ld, const int* kcount, const int* acc_count, double* mean_x,
+                        double* diag_x, double n_prev, int kc, int chains, int d, cudaStream_t s);
 
 // ---------------------------------------------------------------- moments
 // Running mean over the chunk's k counted steps: mean <- (n mean + sum_j Xw_j) / (n + k),
@@ -89,7 +97,11 @@ void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg,
                       const double* Sl, int64_t sl_stride, const double* ml, int64_t ml_stride,
                       double wg, double wl, double* mb, int64_t mb_stride, int chains, int d,
                       int64_t ld, const int* mask, double jitter_eps, const double* tr,
-                      cudaStream_t s, const double* aug_x = nullptr, const double* aug_xr = nullptr);
+                      const double* jitter_mat, cudaStream_t s, const double* aug_x = nullptr,
+                      const double* aug_xr = nullptr, int64_t aug_stride = 0);
+// the x-space blended mean mb, trace tr and trace-floor flag try from the x-space statistics
+void launch_trace_x(const double* Sg, const double* mg, const double* dl, const double* ml, double wg, double wl,
+                    double* mb, double* tr, int* try_flag, int chains, int d, int64_t ld, cudaStream_t s);
 // tr[c] = sum_i C_ii (sequential order); try[c] = trace > 1e-12(1 + mb.mb) && finite
 void launch_trace_floor(double* const* Cm, int64_t ld, const double* mb, int64_t mb_stride,
                         int chains, int d, double* tr, int* try_flag, cudaStream_t s);
@@ -103,7 +115,9 @@ void launch_merge_lower(double* Sg, int64_t ld, const double* packed, int d, dou
                         cudaStream_t s);
 void launch_axpby(double* y, const double* x, int64_t n, double a, double b, cudaStream_t s);
 // cum mean/diag fold (merge_into restricted to the PSRF inputs)
-void launch_cum_fold(double* cmean, double* cdiag, const double* lmean, const double* S,
+// cumulative per-chain x-space mean and raw diagonal (PSRF inputs) from the batch's
+// (ldiag: chain c's diagonal at ldiag + c s_stride)
+void launch_cum_fold(double* cmean, double* cdiag, const double* lmean, const double* ldiag,
                      int64_t s_stride, int chains, int d, int64_t ld, double keep, double add,
                      cudaStream_t s);
 // the batch's convergence statistics on the device (single GPU): out4 = {cov error, mean
@@ -123,10 +137,13 @@ void launch_cov_error(const double* Sg, const double* mg, const double* Ctrue, i
 void trtri_batched(double* const* L, double* const* X, double* const* T, int64_t ld, int d, int chains,
                    const int* mask, cudaStream_t s);
 void launch_trmv_quad(double* const* X, int64_t ld, const double* x, const double* xr, int64_t vstride, double* y,
-                      double* quad_out, int chains, int d, double half_inv_infl2, cudaStream_t s);
+                      int64_t ystride, double* quad_out, int chains, int d, double half_inv_infl2, cudaStream_t s);
 void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr, int64_t vstride,
-                 double* y, double* quad_out, int chains, int d, double half_inv_infl2,
+                 double* y, int64_t ystride, double* quad_out, int chains, int d, double half_inv_infl2,
                  const int* mask, cudaStream_t s);
+// y_c = x_c (rows of stride ld), quad_c = hq |x_c|^2: the identity factor's y and quad
+void launch_init_yq(const double* x, int64_t ld, double* y, double* quad, int chains, int d, double hq,
+                    cudaStream_t s);
 // Cholesky of the lower part of A_c (in place), blocked right-looking with the
 // diagonal blocks factored in shared memory, TRSM and SYRK through gemm_f64.
 // status[c] = 0 ok, 1 not positive definite. Only chains with mask[c] != 0.
@@ -138,6 +155,8 @@ struct PotrfWork {
 inline size_t potrf_work_doubles(int chains) { return (size_t)chains * 128 * 128 + chains; }
 void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* mask, int* status,
                    PotrfWork& w, cudaStream_t s, int extra_rows = 0);
+// F = the symmetric matrix whose lower triangle S holds (d x ld)
+void launch_mirror_lower(const double* S, double* F, int d, int64_t ld, cudaStream_t s);
 // G (lower, G^T G = P) from the precision reversed in P_rev (J P J, overwritten by its
 // factor); the whitened Gaussian target of the engine (Engine::upload_target)
 void whitening_factor(double* P_rev, double* G, int d, int64_t ld, cudaStream_t s);

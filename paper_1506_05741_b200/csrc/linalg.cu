@@ -53,14 +53,16 @@ __global__ void __launch_bounds__(256) mean_update_kernel(double* mean, int64_t 
 __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const double* mg, const double* Sl,
                                  int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl,
                                  double* mb, int64_t mb_stride, int d, int64_t ld, const int* mask,
-                                 double jitter_eps, const double* tr, const double* ax, const double* axr) {
+                                 double jitter_eps, const double* tr, const double* jm, const double* ax,
+                                 const double* axr, int64_t ax_stride) {
     const int c = blockIdx.z;
     if (mask && !mask[c]) return;
     const int npairs = (d + 1) / 2;
     const int p = blockIdx.y;
     if (p == npairs) {  // augmented row r = x - x_ref (solved by the POTRF for the usable guard)
         double* Crow = C_out[c] + (int64_t)d * ld;
-        for (int j = threadIdx.x; j < d; j += blockDim.x) Crow[j] = ax[c * ld + j] - (axr ? axr[c * ld + j] : 0.0);
+        for (int j = threadIdx.x; j < d; j += blockDim.x)
+            Crow[j] = ax[c * ax_stride + j] - (axr ? axr[c * ax_stride + j] : 0.0);
         return;
     }
     const int r1 = p, r2 = d - 1 - p;  // r1 == r2: the middle row of an odd d
@@ -68,7 +70,7 @@ __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const d
     // blended mean (proj/src/moments.cpp:44)
     const double mb1 = wg * mg[r1] + wl * mlc[r1];
     const double mb2 = wg * mg[r2] + wl * mlc[r2];
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && mb) {
         mb[c * mb_stride + r1] = mb1;
         mb[c * mb_stride + r2] = mb2;
     }
@@ -104,8 +106,13 @@ __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const d
         // covariance :90-101 (S exactly symmetric) of the blend :45-46
         double v0 = (wg * sg.x + wl * sl.x) - mbi * (wg * g2.x + wl * l2.x);
         double v1 = (wg * sg.y + wl * sl.y) - mbi * (wg * g2.y + wl * l2.y);
-        if (j == i) v0 += jit;
-        if (j + 1 == i) v1 += jit;
+        if (jm) {  // jitter eps (tr / d) J: the whitened space's image of eps (tr / d) I
+            v0 += jit * jm[(int64_t)i * ld + j];
+            if (pair) v1 += jit * jm[(int64_t)i * ld + j + 1];
+        } else {
+            if (j == i) v0 += jit;
+            if (j + 1 == i) v1 += jit;
+        }
         double* Crow = C_out[c] + (int64_t)i * ld;
         if (pair)
             *reinterpret_cast<double2*>(Crow + j) = make_double2(v0, v1);
@@ -178,14 +185,14 @@ __global__ void axpby_kernel(double* y, const double* x, int64_t n, double a, do
         y[e] = b * y[e] + a * x[e];
 }
 
-__global__ void cum_fold_kernel(double* cmean, double* cdiag, const double* lmean, const double* S,
+__global__ void cum_fold_kernel(double* cmean, double* cdiag, const double* lmean, const double* ldiag,
                                 int64_t s_stride, int d, int64_t ld, double keep, double add) {
     const int c = blockIdx.y;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d) return;
     const int64_t v = c * ld + i;
     cmean[v] = keep * cmean[v] + add * lmean[v];
-    cdiag[v] = keep * cdiag[v] + add * S[c * s_stride + (int64_t)i * ld + i];
+    cdiag[v] = keep * cdiag[v] + add * ldiag[c * s_stride + i];
 }
 
 // partial sums for ||C_emp - C*||_F^2 and ||C*||_F^2 over the full symmetric matrix
@@ -231,7 +238,8 @@ constexpr int kTrsvB = 64;
 
 __global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(double* const* Lm, int64_t ld, const double* x,
                                                             const double* xr, int64_t vstride, double* y,
-                                                            double* quad_out, int d, double hq, const int* mask) {
+                                                            int64_t ystride, double* quad_out, int d, double hq,
+                                                            const int* mask) {
     const int c = blockIdx.x;
     if (mask && !mask[c]) return;
     extern __shared__ double sh[];
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(kTrsvThreads) trsv_kernel(double* const* Lm, i
     double s = 0.0;
     for (int i = tid; i < d; i += kTrsvThreads) {
         const double v = ys[i];
-        if (y) y[c * vstride + i] = v;
+        if (y) y[c * ystride + i] = v;
         s += v * v;
     }
     __shared__ double red[NW];
@@ -565,10 +573,52 @@ void launch_gemv_rows(const double* G, int64_t ld, int d, int nrows, const doubl
 void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg, const double* Sl,
                       int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl, double* mb,
                       int64_t mb_stride, int chains, int d, int64_t ld, const int* mask, double jitter_eps,
-                      const double* tr, cudaStream_t s, const double* aug_x, const double* aug_xr) {
+                      const double* tr, const double* jitter_mat, cudaStream_t s, const double* aug_x,
+                      const double* aug_xr, int64_t aug_stride) {
     dim3 grid(1, (unsigned)((d + 1) / 2 + (aug_x ? 1 : 0)), chains);
     blend_cov_kernel<<<grid, 256, 0, s>>>(C_out, Sg, mg, Sl, sl_stride, ml, ml_stride, wg, wl, mb, mb_stride, d, ld,
-                                          mask, jitter_eps, tr, aug_x, aug_xr);
+                                          mask, jitter_eps, tr, jitter_mat, aug_x, aug_xr,
+                                          aug_stride > 0 ? aug_stride : ld);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+// The x-space trace floor of the blended covariance (proj/src/proposal.cpp:177-183) from the
+// x-space statistics the whitened engine keeps: mb = wg mg + wl ml (the blended mean, also the
+// adaptive reference), tr = sum_i (wg Sg_ii + wl dl_i) - mb_i^2, try = tr > 1e-12 (1 + mb.mb)
+__global__ void trace_x_kernel(const double* Sg, const double* mg, const double* dl, const double* ml, double wg,
+                               double wl, double* mb, double* tr, int* try_flag, int d, int64_t ld) {
+    const int c = blockIdx.x;
+    double t = 0.0, mm = 0.0;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        const double m = wg * mg[i] + wl * ml[c * ld + i];
+        const double sii = wg * Sg[(int64_t)i * ld + i] + wl * dl[c * ld + i];
+        mb[c * ld + i] = m;
+        t += sii - m * m;
+        mm += m * m;
+    }
+    __shared__ double red[2][8];
+    t = warp_sum(t);
+    mm = warp_sum(mm);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = t;
+        red[1][threadIdx.x >> 5] = mm;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            a += red[0][w];
+            b += red[1][w];
+        }
+        tr[c] = a;
+        if (try_flag) try_flag[c] = (a > 1e-12 * (1.0 + b) && isfinite(a)) ? 1 : 0;
+    }
+}
+
+void launch_trace_x(const double* Sg, const double* mg, const double* dl, const double* ml, double wg, double wl,
+                    double* mb, double* tr, int* try_flag, int chains, int d, int64_t ld, cudaStream_t s) {
+    trace_x_kernel<<<chains, 256, 0, s>>>(Sg, mg, dl, ml, wg, wl, mb, tr, try_flag, d, ld);
     DGB_LAUNCH_CHECK();
     count_launch();
 }
@@ -607,10 +657,10 @@ void launch_axpby(double* y, const double* x, int64_t n, double a, double b, cud
     count_launch();
 }
 
-void launch_cum_fold(double* cmean, double* cdiag, const double* lmean, const double* S, int64_t s_stride,
+void launch_cum_fold(double* cmean, double* cdiag, const double* lmean, const double* ldiag, int64_t s_stride,
                      int chains, int d, int64_t ld, double keep, double add, cudaStream_t s) {
     dim3 grid((unsigned)ceil_div(d, 128), chains);
-    cum_fold_kernel<<<grid, 128, 0, s>>>(cmean, cdiag, lmean, S, s_stride, d, ld, keep, add);
+    cum_fold_kernel<<<grid, 128, 0, s>>>(cmean, cdiag, lmean, ldiag, s_stride, d, ld, keep, add);
     DGB_LAUNCH_CHECK();
     count_launch();
 }
@@ -697,10 +747,12 @@ void launch_cov_error(const double* Sg, const double* mg, const double* Ctrue, i
 }
 
 void launch_trsv(double* const* L, int64_t ld, const double* x, const double* xr, int64_t vstride, double* y,
-                 double* quad_out, int chains, int d, double half_inv_infl2, const int* mask, cudaStream_t s) {
+                 int64_t ystride, double* quad_out, int chains, int d, double half_inv_infl2, const int* mask,
+                 cudaStream_t s) {
     const size_t smem = sizeof(double) * (((d + 1) & ~1) + kTrsvB * (kTrsvB + 1) + kTrsvB);
     if (smem > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(trsv_kernel), (int)smem);
-    trsv_kernel<<<chains, kTrsvThreads, smem, s>>>(L, ld, x, xr, vstride, y, quad_out, d, half_inv_infl2, mask);
+    trsv_kernel<<<chains, kTrsvThreads, smem, s>>>(L, ld, x, xr, vstride, y, ystride, quad_out, d, half_inv_infl2,
+                                                   mask);
     DGB_LAUNCH_CHECK();
     count_launch();
 }
@@ -746,7 +798,7 @@ __global__ void __launch_bounds__(kInvB) trtri_diag_kernel(double* const* Lm, do
 
 // y = X (x - xr) (lower-triangular X), quad = hq |y|^2: one CTA per chain, a warp per row
 __global__ void __launch_bounds__(256) trmv_quad_kernel(double* const* Xm, int64_t ld, const double* x,
-                                                        const double* xr, int64_t vstride, double* y,
+                                                        const double* xr, int64_t vstride, double* y, int64_t ystride,
                                                         double* quad_out, int d, double hq) {
     const int c = blockIdx.x;
     extern __shared__ double rs[];
@@ -763,7 +815,7 @@ __global__ void __launch_bounds__(256) trmv_quad_kernel(double* const* Xm, int64
         for (int j = lane; j <= i; j += 32) s += Xr[j] * rs[j];
         s = warp_sum(s);
         if (lane == 0) {
-            y[c * vstride + i] = s;
+            y[c * ystride + i] = s;
             q += s * s;
         }
     }
@@ -818,10 +870,10 @@ void trtri_batched(double* const* L, double* const* X, double* const* T, int64_t
 }
 
 void launch_trmv_quad(double* const* X, int64_t ld, const double* x, const double* xr, int64_t vstride, double* y,
-                      double* quad_out, int chains, int d, double half_inv_infl2, cudaStream_t s) {
+                      int64_t ystride, double* quad_out, int chains, int d, double half_inv_infl2, cudaStream_t s) {
     const size_t smem = sizeof(double) * (size_t)d;
     if (smem > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(trmv_quad_kernel), (int)smem);
-    trmv_quad_kernel<<<chains, 256, smem, s>>>(X, ld, x, xr, vstride, y, quad_out, d, half_inv_infl2);
+    trmv_quad_kernel<<<chains, 256, smem, s>>>(X, ld, x, xr, vstride, y, ystride, quad_out, d, half_inv_infl2);
     DGB_LAUNCH_CHECK();
     count_launch();
 }
@@ -949,6 +1001,44 @@ void whitening_factor(double* P_rev, double* G, int d, int64_t ld, cudaStream_t 
     cudaFree(status);
     cudaFree(pa);
     if (st != 0) throw CudaError("target precision is not positive definite");
+}
+
+__global__ void init_yq_kernel(const double* x, int64_t ld, double* y, double* quad, int d, double hq) {
+    const int c = blockIdx.x;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        const double v = x[c * ld + i];
+        y[c * ld + i] = v;
+        s += v * v;
+    }
+    __shared__ double red[8];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        quad[c] = hq * t;
+    }
+}
+
+void launch_init_yq(const double* x, int64_t ld, double* y, double* quad, int chains, int d, double hq,
+                    cudaStream_t s) {
+    init_yq_kernel<<<chains, 256, 0, s>>>(x, ld, y, quad, d, hq);
+    DGB_LAUNCH_CHECK();
+    count_launch();
+}
+
+__global__ void mirror_lower_kernel(const double* S, double* F, int d, int64_t ld) {
+    const int i = blockIdx.x;
+    for (int j = threadIdx.x; j < ld; j += blockDim.x)
+        F[(int64_t)i * ld + j] = j >= d ? 0.0 : (j <= i ? S[(int64_t)i * ld + j] : S[(int64_t)j * ld + i]);
+}
+
+void launch_mirror_lower(const double* S, double* F, int d, int64_t ld, cudaStream_t s) {
+    mirror_lower_kernel<<<d, 256, 0, s>>>(S, F, d, ld);
+    DGB_LAUNCH_CHECK();
+    count_launch();
 }
 
 void launch_aug_quad(double* const* L, int64_t ld, int d, int chains, double half_inv_infl2, const int* mask,

@@ -25,9 +25,9 @@ int main(int argc, char** argv) {
     std::vector<double> h((size_t)C * win);
     srand(3);
     auto rnd = [] { return (rand() / (double)RAND_MAX - 0.5) * 0.02; };
-    double *W, *Xi, *H, *x, *g, *y, *lp, *qd, *beta;
+    double *W, *Xi, *H, *g, *y, *lp, *qd, *beta, *ie, *bc;
     uint64_t *nacc, *uctr;
-    int* kcount;
+    int *kcount, *acnt, *src, *mult;
     PhiloxKey* keys;
     cudaMalloc(&W, h.size() * 8);
     cudaMalloc(&Xi, h.size() * 8);
@@ -36,10 +36,13 @@ int main(int argc, char** argv) {
     cudaMemcpy(W, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(Xi, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(H, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
-    cudaMalloc(&x, C * ld * 8);
     cudaMalloc(&g, C * ld * 8);
     cudaMalloc(&y, C * ld * 8);
-    cudaMemset(x, 0, C * ld * 8);
+    cudaMalloc(&ie, ld * 8);
+    cudaMalloc(&bc, ld * 8);
+    std::vector<double> ones(ld, 1.0);
+    cudaMemcpy(ie, ones.data(), ld * 8, cudaMemcpyHostToDevice);
+    cudaMemset(bc, 0, ld * 8);
     cudaMemset(g, 0, C * ld * 8);
     cudaMemset(y, 0, C * ld * 8);
     cudaMalloc(&lp, C * 8);
@@ -54,6 +57,9 @@ int main(int argc, char** argv) {
     cudaMemset(nacc, 0, C * 8);
     cudaMemset(uctr, 0, C * 8);
     cudaMalloc(&kcount, C * 4);
+    cudaMalloc(&acnt, C * 4);
+    cudaMalloc(&src, (size_t)C * L * 4);
+    cudaMalloc(&mult, (size_t)C * L * 4);
     std::vector<PhiloxKey> k(C);
     for (int i = 0; i < C; ++i) k[i] = make_philox_key(7, i, "uniform");
     cudaMalloc(&keys, C * sizeof(PhiloxKey));
@@ -72,7 +78,9 @@ int main(int argc, char** argv) {
     p.H = H;
     p.first = 0;
     p.kcount = kcount;
-    p.x = x;
+    p.acc_count = acnt;
+    p.state_src = src;
+    p.state_mult = mult;
     p.g = g;
     p.y = y;
     p.log_pi = lp;
@@ -83,16 +91,18 @@ int main(int argc, char** argv) {
     p.uctr = uctr;
     p.infl = 1.0;
     p.pcn = 1;
+    p.inv_eig = ie;
+    p.bcoef = bc;
     p.out_ld = L;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    launch_mh_window(p, false, 0);
+    launch_mh_window(p, 0);
     cudaDeviceSynchronize();
     std::vector<long long> z(8, 0);
     cudaMemcpyToSymbol(g_mh_prof, z.data(), 64);
     cudaEventRecord(e0);
-    launch_mh_window(p, false, 0);
+    launch_mh_window(p, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;

@@ -36,7 +36,7 @@ def main():
         eng.set_profiling(True)
         eng.run_batches(1)
         for c in ["gemm_target", "trmm_noise", "syrk_moments", "potrf", "mh_window", "normals", "blend_cov",
-                  "gemv_state", "trsv", "merge"]:
+                  "gemv_state", "trsv", "merge", "xi_accepted", "reconstruct"]:
             t, fl, k = eng.stat(c)
             print(f"  {c:14s} {t:8.3f} ms {k:5d} launches" + (f" {fl / t / 1e9:6.2f} TFLOP/s" if fl and t else ""))
 
