@@ -668,7 +668,8 @@ void Engine::refresh_g(const double* x, double* out, int chains, cudaStream_t s)
     timed_end("gemv_state", 2.0 * chains * (double)d_ * dg_, s);
 }
 
-void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s, double flops) {
+void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s, double flops,
+                  bool small) {
     if (flops < 0.0) {
         flops = 2.0 * g.M * (double)g.N * g.K * batch;
         if (g.tri_c_lower) flops *= 0.5 * (1.0 + 1.0 / std::max(1, g.N));
@@ -676,7 +677,8 @@ void Engine::gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool
     }
     nvtxRangePushA(name);  // `ncu --nvtx --nvtx-include "<name>/"` selects one GEMM class
     timed_begin(s);
-    gemm_f64(g, batch, ak, bk, s);
+    if (small) gemm_f64_small(g, batch, s);
+    else gemm_f64(g, batch, ak, bk, s);
     timed_end(name, flops, s);
     nvtxRangePop();
 }
@@ -1061,7 +1063,9 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         a.alpha = 1.0;
         a.tri_b_lower = 1;
         const double fl = profiling_ ? device_count(acc_cnt_ + o) * d_ * (d_ + 1.0) : -1.0;
-        gemm("xi_accepted", a, C, true, true, s, fl);
+        // 64-row tiles: a chain's accepted rows (about acceptance x n_lag, ~50 at the d=1024
+        // bench) fill one such tile, where a 128-row tile would leave half its warps idle
+        gemm("xi_accepted", a, C, true, true, s, fl, true);
         timed_begin(s);
         launch_reconstruct(x_ + o * ld_, k_.adaptive_ref ? xr_ + o * ld_ : nullptr, beta_ + o, k_.pcn_form() ? 1 : 0,
                            H_ + o * winh_, winh_, ldg_, Xi_ + o * win_, win_, ld_, state_src_ + (size_t)o * Lw_,
@@ -1095,22 +1099,21 @@ void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {
         const double* axr = aug && k_.adaptive_ref ? gr_ + o * ldg_ : nullptr;
         // shared workspace: wait until the previous group's tail has released it
         if (pool_ && pool_last_) DGB_CUDA(cudaStreamWaitEvent(s, pool_last_, 0));
+        // one launch: the z-space covariance (and augmented row) plus, per chain, the x-space
+        // trace floor (tr, try, the blended mean mb) and the status reset
+        const TraceX tx{Sg_, mg_, diag_x_ + o * ld_, mean_x_ + o * ld_, mb_ + o * ld_, tr_ + o, try_ + o, status_ + o};
         auto blend = [&] {
-            launch_trace_x(Sg_, mg_, diag_x_ + o * ld_, mean_x_ + o * ld_, p.wg, p.wl, mb_ + o * ld_, tr_ + o, try_ + o,
-                           C, d_, ld_, s);
             launch_blend_cov(g.Lnp, Sgz_, mgz_, S_ + o * mat_, mat_, mean_ + o * ld_, ld_, p.wg, p.wl, nullptr, ld_, C,
-                             d_, ld_, nullptr, 0.0, nullptr, GG_, s, ax, axr, ldg_);
+                             d_, ld_, nullptr, 0.0, nullptr, GG_, s, ax, axr, ldg_, &tx);
         };
         timed_begin(s);
         blend();
         timed_end("blend_cov", 0.0, s);
-        DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
         nvtxRangePushA("potrf");
         timed_begin(s);
         potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
         if (twice_ & kTwicePotrf) {  // blend + factorization again: same inputs, same factor
             blend();
-            DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
             potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
         }
         timed_end("potrf", (double)C * d_ * (double)d_ * d_ / 3.0, s);
@@ -1200,25 +1203,20 @@ void Engine::tail_finish(Group& g, const WindowPlan& p) {
     const double infl = k_.noise_infl();
     if (p.refactor) {
         const bool aug = k_.pcn_form();
-        // every tried chain has factored by now
-        DGB_CUDA(cudaMemsetAsync(status_ + o, 0, C * sizeof(int), s));
-        double qmax = -1.0;
-        if (aug) {
-            // usable guard: 1/2 |L'^-1 (x - x_ref)|^2 / infl^2 <= 5 d (proposal.cpp:185-199),
-            // L'^-1 (x - x_ref) being the augmented row the POTRF just solved
-            launch_aug_quad(g.Lnp, ld_, d_, C, 0.5 / (infl * infl), try_ + o, qtmp_ + o, s);
-            qmax = 5.0 * d_;
-        }
-        launch_accept_factor(g.Lp, g.Lnp, try_ + o, status_ + o, qtmp_ + o, qmax, C, usable_ + o, s);
+        // every tried chain has factored by now. Usable guard (pCN forms, proposal.cpp:185-199):
+        // 1/2 |L'^-1 (x - x_ref)|^2 / infl^2 <= 5 d, L'^-1 (x - x_ref) being the augmented row
+        // the POTRF just solved; adopted factors come with y = that row and the quad term for
+        // free when the reference point is fixed and no explicit inverse is kept
+        const bool adopt_y = aug && !Xinv_ && !k_.adaptive_ref;
+        launch_adopt_factor(g.Lp, g.Lnp, ld_, d_, C, try_ + o, status_ + o, aug ? 0.5 / (infl * infl) : -1.0,
+                            aug ? 5.0 * d_ : -1.0, usable_ + o, adopt_y ? y_ + o * ld_ : nullptr,
+                            adopt_y ? quad_ + o : nullptr, s);
         if (pool_) {  // the shared workspace is free for the next group
             DGB_CUDA(cudaEventRecord(g.pool_ev, s));
             pool_last_ = g.pool_ev;
         }
         // explicit inverse: X = L^{-1} of every adopted factor (proposal.cpp:202)
         if (Xinv_) trtri_batched(g.Lp, Xinvp_ + o, Tinvp_ + o, ld_, d_, C, usable_ + o, s);
-        // adopted factors come with y = L^-1 (x - x_ref) and the quad term for free
-        else if (aug && !k_.adaptive_ref)
-            launch_aug_adopt(g.Lp, ld_, d_, C, usable_ + o, qtmp_ + o, y_ + o * ld_, quad_ + o, s);
     }
     // adaptive reference point (proposal.cpp:206-208)
     if (p.move_ref) {

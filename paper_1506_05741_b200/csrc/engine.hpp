@@ -165,7 +165,7 @@ private:
     void save_checkpoint(double wall);
     // flops < 0: the algorithmic count from the shape (triangular halves included)
     void gemm(const char* name, const GemmBatch& g, int batch, bool ak, bool bk, cudaStream_t s,
-              double flops = -1.0);
+              double flops = -1.0, bool small = false);
     void refresh_g(const double* x, double* out, int chains, cudaStream_t s);
     void timed_begin(cudaStream_t s);
     void timed_end(const char* name, double flops, cudaStream_t s);

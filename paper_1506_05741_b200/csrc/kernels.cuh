@@ -98,13 +98,20 @@ void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg,
                       double wg, double wl, double* mb, int64_t mb_stride, int chains, int d,
                       int64_t ld, const int* mask, double jitter_eps, const double* tr,
                       const double* jitter_mat, cudaStream_t s, const double* aug_x = nullptr,
-                      const double* aug_xr = nullptr, int64_t aug_stride = 0);
-// the x-space blended mean mb, trace tr and trace-floor flag try from the x-space statistics
-void launch_trace_x(const double* Sg, const double* mg, const double* dl, const double* ml, double wg, double wl,
-                    double* mb, double* tr, int* try_flag, int chains, int d, int64_t ld, cudaStream_t s);
-// tr[c] = sum_i C_ii (sequential order); try[c] = trace > 1e-12(1 + mb.mb) && finite
-void launch_trace_floor(double* const* Cm, int64_t ld, const double* mb, int64_t mb_stride,
-                        int chains, int d, double* tr, int* try_flag, cudaStream_t s);
+                      const double* aug_xr = nullptr, int64_t aug_stride = 0, const struct TraceX* tx = nullptr);
+// The x-space side of a refactor's first attempt, done by one extra CTA per chain of the blend
+// launch: the blended mean mb, trace tr and trace-floor flag try from the x-space statistics
+// (proj/src/proposal.cpp:177-183), and the factorization status reset
+struct TraceX {
+    const double* Sg;
+    const double* mg;
+    const double* dl;
+    const double* ml;
+    double* mb;
+    double* tr;
+    int* try_flag;
+    int* status;
+};
 // Merge helpers (proj/src/moments.cpp:51-88)
 void launch_sum_chains(double* out, const double* in, int64_t chain_stride, int chains, int64_t n,
                        double weight, cudaStream_t s);
@@ -160,21 +167,18 @@ void launch_mirror_lower(const double* S, double* F, int d, int64_t ld, cudaStre
 // G (lower, G^T G = P) from the precision reversed in P_rev (J P J, overwritten by its
 // factor); the whitened Gaussian target of the engine (Engine::upload_target)
 void whitening_factor(double* P_rev, double* G, int d, int64_t ld, cudaStream_t s);
-// q_c = half_inv_infl2 * |row d of L_c|^2 (the augmented row = L^{-1}(x - x_ref))
-void launch_aug_quad(double* const* L, int64_t ld, int d, int chains, double half_inv_infl2, const int* mask,
-                     double* q, cudaStream_t s);
-// for chains with usable[c]: y_c = row d of L_c (post-swap), quad_c = q_c
-void launch_aug_adopt(double* const* L, int64_t ld, int d, int chains, const int* usable, const double* q,
-                      double* y, double* quad, cudaStream_t s);
 
 // ---------------------------------------------------------------- lag update
 // beta adaptation + rate (proj/src/proposal.cpp:163-173)
 void launch_beta_update(double* beta, uint64_t* n_acc, double* rate_out, double* beta_out,
                         int chains, int n_lag, int adapt, double lo, double hi, double factor,
                         double bmin, double bmax, cudaStream_t s);
-// usable[c] = try[c] && status[c]==0 && (qcheck[c] <= qmax); swap factor pointers where usable
-void launch_accept_factor(double** L, double** Lnew, const int* try_flag, const int* status,
-                          const double* q, double qmax, int chains, int* usable, cudaStream_t s);
+// The adoption of a refactor's new factors in one launch (proposal.cpp:185-202): q_c =
+// hq |row d of Lnew_c|^2 (the augmented row L'^-1 (x - x_ref); hq < 0: no augmented row),
+// usable[c] = try[c] && (q_c <= qmax or qmax < 0), pointers swapped where usable, status reset;
+// with y: y_c = that row and quad_c = q_c for the usable chains
+void launch_adopt_factor(double** L, double** Lnew, int64_t ld, int d, int chains, const int* try_flag, int* status,
+                         double hq, double qmax, int* usable, double* y, double* quad, cudaStream_t s);
 // L_c = I
 void launch_set_identity(double* base, int64_t mat_stride, int chains, int d, int64_t ld, cudaStream_t s);
 // log pi from x and g = G x (Gaussian: -1/2 x.g; twisted: -1/2 sum twist(g)^2 / sigma^2)

@@ -46,6 +46,39 @@ __global__ void __launch_bounds__(256) mean_update_kernel(double* mean, int64_t 
     }
 }
 
+// The x-space trace floor of the blended covariance (proj/src/proposal.cpp:177-183) from the
+// x-space statistics the whitened engine keeps: mb = wg mg + wl ml (the blended mean, also the
+// adaptive reference), tr = sum_i (wg Sg_ii + wl dl_i) - mb_i^2, try = tr > 1e-12 (1 + mb.mb)
+__device__ __forceinline__ void trace_x_block(const double* Sg, const double* mg, const double* dl, const double* ml,
+                                              double wg, double wl, double* mb, double* tr, int* try_flag, int d,
+                                              int64_t ld, int c) {
+    double t = 0.0, mm = 0.0;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        const double m = wg * mg[i] + wl * ml[c * ld + i];
+        const double sii = wg * Sg[(int64_t)i * ld + i] + wl * dl[c * ld + i];
+        mb[c * ld + i] = m;
+        t += sii - m * m;
+        mm += m * m;
+    }
+    __shared__ double red[2][8];
+    t = warp_sum(t);
+    mm = warp_sum(mm);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = t;
+        red[1][threadIdx.x >> 5] = mm;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            a += red[0][w];
+            b += red[1][w];
+        }
+        tr[c] = a;
+        if (try_flag) try_flag[c] = (a > 1e-12 * (1.0 + b) && isfinite(a)) ? 1 : 0;
+    }
+}
+
 // C = wg*Sg + wl*Sl - mb mb^T on the lower triangle, 0 above; optional jitter on the diagonal.
 // One CTA per pair of rows (p, d-1-p) of one chain: the two rows hold d+1 lower entries
 // together, so every CTA moves the same bytes and all threads work (a CTA per row left
@@ -54,11 +87,16 @@ __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const d
                                  int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl,
                                  double* mb, int64_t mb_stride, int d, int64_t ld, const int* mask,
                                  double jitter_eps, const double* tr, const double* jm, const double* ax,
-                                 const double* axr, int64_t ax_stride) {
+                                 const double* axr, int64_t ax_stride, TraceX tx, int has_tx) {
     const int c = blockIdx.z;
     if (mask && !mask[c]) return;
     const int npairs = (d + 1) / 2;
     const int p = blockIdx.y;
+    if (has_tx && p == (int)gridDim.y - 1) {
+        trace_x_block(tx.Sg, tx.mg, tx.dl, tx.ml, wg, wl, tx.mb, tx.tr, tx.try_flag, d, ld, c);
+        if (threadIdx.x == 0) tx.status[c] = 0;
+        return;
+    }
     if (p == npairs) {  // augmented row r = x - x_ref (solved by the POTRF for the usable guard)
         double* Crow = C_out[c] + (int64_t)d * ld;
         for (int j = threadIdx.x; j < d; j += blockDim.x)
@@ -118,26 +156,6 @@ __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const d
             *reinterpret_cast<double2*>(Crow + j) = make_double2(v0, v1);
         else
             Crow[j] = v0;
-    }
-}
-
-__global__ void trace_floor_kernel(double* const* Cm, int64_t ld, const double* mb, int64_t mb_stride, int d,
-                                   double* tr, int* try_flag) {
-    const int c = blockIdx.x;
-    const int lane = threadIdx.x;
-    const double* C = Cm[c];
-    const double* m = mb + c * mb_stride;
-    double t = 0.0, mm = 0.0;
-    for (int i = lane; i < d; i += 32) {
-        t += C[(int64_t)i * ld + i];
-        mm += m[i] * m[i];
-    }
-    t = warp_sum(t);
-    mm = warp_sum(mm);
-    if (lane == 0) {
-        tr[c] = t;
-        const double floor = 1e-12 * (1.0 + mm);  // proj/src/proposal.cpp:181
-        try_flag[c] = (t > floor && isfinite(t)) ? 1 : 0;
     }
 }
 
@@ -365,87 +383,160 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const double* G, int64_t
 constexpr int kNb = kDiagNb;
 
 
+// The 128 x 128 diagonal block of block column J = [j0, j0 + n1 + n2) in one CTA per chain
+// (n1 = 64, n2 <= 64; n2 = 0 for a last block column of width <= 64), from shared memory:
+//   (1) L11 = chol(A11), X11 = L11^-1 (diag_tc.cuh)
+//   (2) L21 = A21 X11^T, A22 -= L21 L21^T, L22 = chol(A22), X22 = L22^-1 (the same routine
+//       with its pre-solve and pre-update)
+//   (3) X21 = -X22 (L21 X11), completing X_J = L_JJ^{-1} in the chain's 128 x 128 slot (row
+//       stride 128) for the block column's one 128-deep TRSM
 // Two CTAs per SM (<= 128 registers) so a diagonal-block CTA can share its SM with a GEMM
-// CTA of another chain group. pre: 1 = first update the block by the 64 (final) columns to
-// its left (diag64_tc_sc's pre_L); 2 = those columns still need their solve against the
-// inverse at inv_base + c inv_stride (pre_X). The inverse goes to inv_base + c inv_stride +
-// inv_off.
+// CTA of another chain group.
 using X21Tile = tile::Cfg<64, 64, 32, 2, true, false, 2, 4, 1>;  // X21's two 64 x 64 products (8 warps)
 static_assert(X21Tile::SMEM_BYTES <= (int)sizeof(DiagTcScratch), "X21 products reuse the diagonal scratch");
 
-__global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int jb,
+__global__ void __launch_bounds__(256, 2) potrf_diag_kernel(double* const* Am, int64_t ld, int j0, int n1, int n2,
                                                             const int* mask, int* status, int* active,
-                                                            double* inv_base, int zero_above, int pre = 0,
-                                                            int inv_stride = kDiagNb * kDiagNb, int inv_off = 0) {
+                                                            double* inv_base) {
     extern __shared__ __align__(16) double dyn_smem[];
     const int c = blockIdx.x;
     const bool run = (!mask || mask[c]) && status[c] == 0;
     if (threadIdx.x == 0) active[c] = run ? 1 : 0;
     if (!run) return;
-    double* Ab = Am[c] + (int64_t)j0 * ld + j0;
-    double* out = inv_base + (int64_t)c * inv_stride + inv_off;
+    DiagTcScratch& sc = *reinterpret_cast<DiagTcScratch*>(dyn_smem);
+    double* A11 = Am[c] + (int64_t)j0 * ld + j0;
     // the chain's 128 x 128 inverse slot X_J (row stride 128): X11 at [0, 0), X22 at [64, 64)
-    double* xj = inv_base + (int64_t)c * inv_stride;
-    const int bad = diag64_tc_sc(*reinterpret_cast<DiagTcScratch*>(dyn_smem), Ab, ld, jb, out, zero_above, kD2,
-                                 pre ? Ab - kNb : nullptr, pre == 2 ? xj : nullptr, kD2);
-    if (bad) {
-        if (threadIdx.x == 0) {
-            status[c] = 1;
-            active[c] = 0;
+    double* xj = inv_base + (int64_t)c * kD2 * kD2;
+    int bad = diag64_tc_sc(sc, A11, ld, n1, xj, 0, kD2);
+    if (!bad && n2 > 0) {
+        __syncthreads();  // the first block's stores have read the scratch; X11 is in the slot
+        double* A22 = A11 + (int64_t)kNb * ld + kNb;
+        bad = diag64_tc_sc(sc, A22, ld, n2, xj + kNb * kD2 + kNb, j0 > 0 ? 1 : 0, kD2, A22 - kNb, xj, kD2);
+        if (!bad) {
+            // X21 = -X22 (L21 X11): T = L21 X11 into X21's place, then in place (L21 was
+            // solved by this CTA)
+            __threadfence_block();
+            tile::gemm_tile<X21Tile, true, false>(A22 - kNb, xj, xj + kNb * kD2, ld, kD2, kD2, n2, kNb, kNb, 0, 0,
+                                                  1.0, 0.0, false, dyn_smem);
+            __threadfence_block();
+            tile::gemm_tile<X21Tile, true, false>(xj + kNb * kD2 + kNb, xj + kNb * kD2, xj + kNb * kD2, kD2, kD2, kD2,
+                                                  n2, kNb, n2, 0, 0, -1.0, 0.0, false, dyn_smem);
         }
-        return;
     }
-    if (pre == 2) {
-        // X21 = -X22 (L21 X11), completing X_J = L_JJ^{-1} for the block column's one 128-deep
-        // TRSM: T = L21 X11 into X21's place, then in place (L21 was solved by this CTA)
-        __threadfence_block();
-        tile::gemm_tile<X21Tile, true, false>(Ab - kNb, xj, xj + kNb * kD2, ld, kD2, kD2, jb, kNb, kNb, 0, 0, 1.0, 0.0,
-                                              false, dyn_smem);
-        __threadfence_block();
-        tile::gemm_tile<X21Tile, true, false>(xj + kNb * kD2 + kNb, xj + kNb * kD2, xj + kNb * kD2, kD2, kD2, kD2, jb,
-                                              kNb, jb, 0, 0, -1.0, 0.0, false, dyn_smem);
+    if (bad && threadIdx.x == 0) {
+        status[c] = 1;
+        active[c] = 0;
     }
 }
 
 // The rows below a block column's diagonal block: L[r, J] = A[r, J] X_J^T, one 128-deep
 // triangular DMMA product per 64-row tile (B(k, n) = X_J[n][k] = 0 for k > n), in place:
 // a CTA owns all of J's columns for its rows, so it reads its whole A tile before writing.
-using TrsmTile = tile::Cfg<64, 128, 32, 2, true, true, 2, 4, 2>;  // 8 warps of 32 x 32, 2 CTAs / SM
+// Column n needs k <= n only, so a warp owning 32 consecutive columns would do between 1/4
+// and all of the work and the per-stage barrier would pace every warp at the slowest: each
+// warp instead owns two 16-column blocks from opposite ends, {w, 7 - w} (w = warp % 4), and
+// skips the k steps past each 8-column fragment's last column: 272 DMMAs for every warp (and
+// every SM sub-partition, which hosts warps w and w + 4) against 128 (w + 1) before.
+using TrsmTile = tile::Cfg<64, 128, 32, 2, true, true, 2, 4, 2>;  // stage layout: 64 x 32 A, 128 x 32 B
+
+// fragment j of warp column wn, in descending column order: the fragments still live at a
+// given k are always the first ones
+__device__ __forceinline__ int trsm_frag_col(int wn, int j) {
+    return j < 2 ? 16 * (7 - wn) + 8 * (1 - j) : 16 * wn + 8 * (3 - j);
+}
+
+// 8 k (two k4 steps) of the NL live fragments: a separate body per live count, selected by a
+// warp-uniform switch, so the dead fragments' DMMAs are not issued (if-converted, they would
+// still occupy the tensor pipe)
+template <int NL>
+__device__ __forceinline__ void trsm_chunk(double (&acc)[4][4][2], const double* a_s, const double* b_s, int kk0,
+                                           int wm0, int wn, int fr, int fk) {
+#pragma unroll
+    for (int kk = kk0; kk < kk0 + 8; kk += 4) {
+        double af[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = a_s[(wm0 + i * 8 + fr) * TrsmTile::A_STRIDE + kk + fk];
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            const double bf = b_s[(trsm_frag_col(wn, j) + fr) * TrsmTile::B_STRIDE + kk + fk];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) tile::dmma(acc[i][j], af[i], bf);
+        }
+    }
+}
 
 __global__ void __launch_bounds__(256, 2) potrf_trsm_kernel(double* const* Am, int64_t ld, int r0, int c0, int rows,
                                                             int nb, const int* active, double* const* inv) {
+    using CF = TrsmTile;
     const int c = blockIdx.z;
     if (!active[c]) return;
     extern __shared__ __align__(16) double smem[];
     double* a = Am[c] + (int64_t)r0 * ld + c0;
-    tile::gemm_tile<TrsmTile, true, true>(a, inv[c], a, ld, kD2, ld, rows, nb, nb, blockIdx.y * TrsmTile::BM, 0, 1.0,
-                                          0.0, false, smem, true);
-}
-
-__global__ void aug_quad_kernel(double* const* Lm, int64_t ld, int d, double hq, const int* mask, double* q) {
-    const int c = blockIdx.x;
-    if (mask && !mask[c]) return;
-    const double* row = Lm[c] + (int64_t)d * ld;
-    double s = 0.0;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) s += row[i] * row[i];
-    __shared__ double red[32];
-    s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-        q[c] = hq * t;
+    const double* X = inv[c];  // B(k, n) = X[n * kD2 + k]
+    const int m0 = blockIdx.y * CF::BM;
+    const int N = nb, K = nb;
+    double* sA = smem;
+    double* sB = smem + CF::STAGES * CF::A_STAGE;
+    const int KT = (K + CF::BK - 1) / CF::BK;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm0 = (warp / 4) * 32, wn = warp % 4;
+    const int fr = lane >> 2, fk = lane & 3;
+    auto issue = [&](int kt, int stage) {
+        const int k0 = kt * CF::BK;
+        tile::load_tile<CF::A_ROWS, CF::A_COLS, CF::A_STRIDE, CF::THREADS>(sA + stage * CF::A_STAGE,
+                                                                        a + (int64_t)m0 * ld + k0, ld, rows - m0,
+                                                                        K - k0, tid);
+        tile::load_tile<CF::B_ROWS, CF::B_COLS, CF::B_STRIDE, CF::THREADS>(sB + stage * CF::B_STAGE, X + k0, kD2, N,
+                                                                        K - k0, tid);
+    };
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    issue(0, 0);
+    tile::cp_async_commit();
+    const bool compute = m0 + wm0 < rows;
+    for (int kt = 0; kt < KT; ++kt) {
+        tile::cp_async_wait<0>();
+        __syncthreads();
+        if (kt + 1 < KT) issue(kt + 1, (kt + 1) % CF::STAGES);
+        tile::cp_async_commit();
+        const double* a_s = sA + (kt % CF::STAGES) * CF::A_STAGE;
+        const double* b_s = sB + (kt % CF::STAGES) * CF::B_STAGE;
+        if (compute) {
+#pragma unroll
+            for (int kk0 = 0; kk0 < CF::BK; kk0 += 8) {
+                // fragments with a column >= k (B(k, n) = 0 for k > n)
+                const int kg = kt * CF::BK + kk0;
+                int nl = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) nl += trsm_frag_col(wn, j) + 8 > kg ? 1 : 0;
+                switch (nl) {
+                    case 4: trsm_chunk<4>(acc, a_s, b_s, kk0, wm0, wn, fr, fk); break;
+                    case 3: trsm_chunk<3>(acc, a_s, b_s, kk0, wm0, wn, fr, fk); break;
+                    case 2: trsm_chunk<2>(acc, a_s, b_s, kk0, wm0, wn, fr, fk); break;
+                    case 1: trsm_chunk<1>(acc, a_s, b_s, kk0, wm0, wn, fr, fk); break;
+                    default: break;
+                }
+            }
+        }
     }
-}
-
-__global__ void aug_adopt_kernel(double* const* Lm, int64_t ld, int d, const int* usable, const double* q, double* y,
-                                 double* quad) {
-    const int c = blockIdx.y;
-    if (!usable[c]) return;
-    const double* row = Lm[c] + (int64_t)d * ld;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x) y[c * ld + i] = row[i];
-    if (blockIdx.x == 0 && threadIdx.x == 0) quad[c] = q[c];
+    tile::cp_async_wait<0>();
+    __syncthreads();  // every warp has read its A rows: the tile may be overwritten
+    if (!compute) return;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = m0 + wm0 + i * 8 + fr;
+        if (r >= rows) continue;
+        double* crow = a + (int64_t)r * ld;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int q = trsm_frag_col(wn, j) + 2 * fk;
+            if (q + 1 < N) *reinterpret_cast<double2*>(crow + q) = make_double2(acc[i][j][0], acc[i][j][1]);
+            else if (q < N) crow[q] = acc[i][j][0];
+        }
+    }
 }
 
 __global__ void beta_update_kernel(double* beta, uint64_t* n_acc, double* rate_out, double* beta_out, int chains,
@@ -466,18 +557,43 @@ __global__ void beta_update_kernel(double* beta, uint64_t* n_acc, double* rate_o
     if (beta_out) beta_out[c] = b;
 }
 
-__global__ void accept_factor_kernel(double** L, double** Lnew, const int* try_flag, const int* status,
-                                     const double* q, double qmax, int chains, int* usable) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= chains) return;
-    bool ok = try_flag[c] && status[c] == 0;
-    if (ok && qmax >= 0.0) ok = q[c] <= qmax;  // proj/src/proposal.cpp:185-199
-    if (ok) {
-        double* t = L[c];
-        L[c] = Lnew[c];
-        Lnew[c] = t;
+__global__ void __launch_bounds__(256) adopt_factor_kernel(double** L, double** Lnew, int64_t ld, int d,
+                                                           const int* try_flag, int* status, double hq, double qmax,
+                                                           int* usable, double* y, double* quad) {
+    const int c = blockIdx.x;
+    const bool tried = try_flag[c] != 0;
+    const double* row = Lnew[c] + (int64_t)d * ld;  // read before thread 0 may swap the pointers
+    __shared__ double red[8];
+    __shared__ int s_ok;
+    double q = 0.0;
+    if (hq >= 0.0 && tried) {  // proj/src/proposal.cpp:190-196
+        double t = 0.0;
+        for (int i = threadIdx.x; i < d; i += blockDim.x) t += row[i] * row[i];
+        t = warp_sum(t);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double u = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) u += red[w];
+            q = hq * u;
+        }
     }
-    if (usable) usable[c] = ok ? 1 : 0;
+    if (threadIdx.x == 0) {
+        bool ok = tried;
+        if (ok && qmax >= 0.0) ok = q <= qmax;  // proj/src/proposal.cpp:197-199
+        if (ok) {
+            double* t = L[c];
+            L[c] = Lnew[c];
+            Lnew[c] = t;
+        }
+        usable[c] = ok ? 1 : 0;
+        status[c] = 0;
+        if (ok && quad) quad[c] = q;
+        s_ok = ok;
+    }
+    __syncthreads();
+    if (s_ok && y)
+        for (int i = threadIdx.x; i < d; i += blockDim.x) y[c * ld + i] = row[i];
 }
 
 __global__ void copy_vecs_kernel(double* dst, const double* src, int64_t n, const int* mask, int64_t stride) {
@@ -574,58 +690,11 @@ void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg, 
                       int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl, double* mb,
                       int64_t mb_stride, int chains, int d, int64_t ld, const int* mask, double jitter_eps,
                       const double* tr, const double* jitter_mat, cudaStream_t s, const double* aug_x,
-                      const double* aug_xr, int64_t aug_stride) {
-    dim3 grid(1, (unsigned)((d + 1) / 2 + (aug_x ? 1 : 0)), chains);
+                      const double* aug_xr, int64_t aug_stride, const TraceX* tx) {
+    dim3 grid(1, (unsigned)((d + 1) / 2 + (aug_x ? 1 : 0) + (tx ? 1 : 0)), chains);
     blend_cov_kernel<<<grid, 256, 0, s>>>(C_out, Sg, mg, Sl, sl_stride, ml, ml_stride, wg, wl, mb, mb_stride, d, ld,
                                           mask, jitter_eps, tr, jitter_mat, aug_x, aug_xr,
-                                          aug_stride > 0 ? aug_stride : ld);
-    DGB_LAUNCH_CHECK();
-    count_launch();
-}
-
-// The x-space trace floor of the blended covariance (proj/src/proposal.cpp:177-183) from the
-// x-space statistics the whitened engine keeps: mb = wg mg + wl ml (the blended mean, also the
-// adaptive reference), tr = sum_i (wg Sg_ii + wl dl_i) - mb_i^2, try = tr > 1e-12 (1 + mb.mb)
-__global__ void trace_x_kernel(const double* Sg, const double* mg, const double* dl, const double* ml, double wg,
-                               double wl, double* mb, double* tr, int* try_flag, int d, int64_t ld) {
-    const int c = blockIdx.x;
-    double t = 0.0, mm = 0.0;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) {
-        const double m = wg * mg[i] + wl * ml[c * ld + i];
-        const double sii = wg * Sg[(int64_t)i * ld + i] + wl * dl[c * ld + i];
-        mb[c * ld + i] = m;
-        t += sii - m * m;
-        mm += m * m;
-    }
-    __shared__ double red[2][8];
-    t = warp_sum(t);
-    mm = warp_sum(mm);
-    if ((threadIdx.x & 31) == 0) {
-        red[0][threadIdx.x >> 5] = t;
-        red[1][threadIdx.x >> 5] = mm;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-        for (int w = 0; w < 8; ++w) {
-            a += red[0][w];
-            b += red[1][w];
-        }
-        tr[c] = a;
-        if (try_flag) try_flag[c] = (a > 1e-12 * (1.0 + b) && isfinite(a)) ? 1 : 0;
-    }
-}
-
-void launch_trace_x(const double* Sg, const double* mg, const double* dl, const double* ml, double wg, double wl,
-                    double* mb, double* tr, int* try_flag, int chains, int d, int64_t ld, cudaStream_t s) {
-    trace_x_kernel<<<chains, 256, 0, s>>>(Sg, mg, dl, ml, wg, wl, mb, tr, try_flag, d, ld);
-    DGB_LAUNCH_CHECK();
-    count_launch();
-}
-
-void launch_trace_floor(double* const* Cm, int64_t ld, const double* mb, int64_t mb_stride, int chains, int d,
-                        double* tr, int* try_flag, cudaStream_t s) {
-    trace_floor_kernel<<<chains, 32, 0, s>>>(Cm, ld, mb, mb_stride, d, tr, try_flag);
+                                          aug_stride > 0 ? aug_stride : ld, tx ? *tx : TraceX{}, tx ? 1 : 0);
     DGB_LAUNCH_CHECK();
     count_launch();
 }
@@ -925,13 +994,11 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
             // 0.83 -> 0.72 ms per factorization; 22.45 -> 22.21 ms per 16-group batch)
             gemm_f64_small(p, chains, s);
         }
-        const int n1 = std::min(kNb, jb);
-        // X11 (and X22) side by side in the chain's 128 x 128 inverse slot
-        potrf_diag_kernel<<<chains, 256, sizeof(DiagTcScratch), s>>>(A, ld, j0, n1, mask, status, active, w.inv, 0,
-                                                                      0, kD2 * kD2, 0);
+        const int n1 = std::min(kNb, jb), n2 = jb - n1;
+        potrf_diag_kernel<<<chains, 256, sizeof(DiagTcScratch), s>>>(A, ld, j0, n1, n2, mask, status, active, w.inv);
         DGB_LAUNCH_CHECK();
         count_launch();
-        if (jb <= kNb) {  // a last, narrow block column: TRSM L21 = A21 X11^T below it
+        if (n2 == 0) {  // a last, narrow block column: TRSM L21 = A21 X11^T below it
             const int rest = rows - j0 - jb;
             if (rest <= 0) continue;
             GemmBatch t{};
@@ -952,11 +1019,7 @@ void potrf_batched(double* const* A, int64_t ld, int d, int chains, const int* m
             gemm_f64(t, chains, true, true, s);  // one 64-wide column tile per CTA: safe in place
             continue;
         }
-        const int c1 = j0 + kNb, n2 = jb - kNb;
-        potrf_diag_kernel<<<chains, 256, sizeof(DiagTcScratch), s>>>(A, ld, c1, n2, mask, status, active, w.inv,
-                                                                      j0 > 0 ? 1 : 0, 2, kD2 * kD2, kNb * kD2 + kNb);
-        DGB_LAUNCH_CHECK();
-        count_launch();
+        const int c1 = j0 + kNb;
         const int rest = rows - c1 - n2;
         if (rest <= 0) continue;
         dim3 grid(1, (unsigned)ceil_div(rest, TrsmTile::BM), (unsigned)chains);
@@ -1041,21 +1104,6 @@ void launch_mirror_lower(const double* S, double* F, int d, int64_t ld, cudaStre
     count_launch();
 }
 
-void launch_aug_quad(double* const* L, int64_t ld, int d, int chains, double half_inv_infl2, const int* mask,
-                     double* q, cudaStream_t s) {
-    aug_quad_kernel<<<chains, 256, 0, s>>>(L, ld, d, half_inv_infl2, mask, q);
-    DGB_LAUNCH_CHECK();
-    count_launch();
-}
-
-void launch_aug_adopt(double* const* L, int64_t ld, int d, int chains, const int* usable, const double* q, double* y,
-                      double* quad, cudaStream_t s) {
-    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(d, 256), 16)), chains);
-    aug_adopt_kernel<<<grid, 256, 0, s>>>(L, ld, d, usable, q, y, quad);
-    DGB_LAUNCH_CHECK();
-    count_launch();
-}
-
 void launch_beta_update(double* beta, uint64_t* n_acc, double* rate_out, double* beta_out, int chains, int n_lag,
                         int adapt, double lo, double hi, double factor, double bmin, double bmax, cudaStream_t s) {
     beta_update_kernel<<<(unsigned)ceil_div(chains, 128), 128, 0, s>>>(beta, n_acc, rate_out, beta_out, chains, n_lag,
@@ -1064,10 +1112,9 @@ void launch_beta_update(double* beta, uint64_t* n_acc, double* rate_out, double*
     count_launch();
 }
 
-void launch_accept_factor(double** L, double** Lnew, const int* try_flag, const int* status, const double* q,
-                          double qmax, int chains, int* usable, cudaStream_t s) {
-    accept_factor_kernel<<<(unsigned)ceil_div(chains, 128), 128, 0, s>>>(L, Lnew, try_flag, status, q, qmax, chains,
-                                                                        usable);
+void launch_adopt_factor(double** L, double** Lnew, int64_t ld, int d, int chains, const int* try_flag, int* status,
+                         double hq, double qmax, int* usable, double* y, double* quad, cudaStream_t s) {
+    adopt_factor_kernel<<<chains, 256, 0, s>>>(L, Lnew, ld, d, try_flag, status, hq, qmax, usable, y, quad);
     DGB_LAUNCH_CHECK();
     count_launch();
 }

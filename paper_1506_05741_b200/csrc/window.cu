@@ -198,9 +198,18 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
     if (tid == 0)
         for (int t = 0; t < NS && t < p.n_lag; ++t) issue(t, t);
 
-    double2 g[R], y[R], grv[ZREF ? 1 : R], iev[TWG ? 1 : R], bcv[TWG ? 1 : R], ga[R], cy[R];
+    // GRL: the reference point read through L1 each step (8 pairs per thread: registers would spill)
+    constexpr bool GRL = !ZREF && R >= 8;
+    double2 g[R], y[R], grv[(ZREF || GRL) ? 1 : R], iev[TWG ? 1 : R], bcv[TWG ? 1 : R], ga[R], cy[R];
     bool vx[R], vg[R];  // entry pair e in x-space (e < d) / in g-space (e < dg)
-    auto GR = [&](int r) -> double2 { return ZREF ? make_double2(0.0, 0.0) : grv[ZREF ? 0 : r]; };
+    auto GR = [&](int r) -> double2 {
+        if (ZREF) return make_double2(0.0, 0.0);
+        if (GRL) {
+            const int e = 2 * (tid + r * T);
+            return e < dg ? __ldg(reinterpret_cast<const double2*>(p.gr + c * ldg + e)) : make_double2(0.0, 0.0);
+        }
+        return grv[(ZREF || GRL) ? 0 : r];
+    };
     auto IE = [&](int r) -> double2 {
         return TWG ? __ldg(reinterpret_cast<const double2*>(p.inv_eig) + tid + r * T) : iev[TWG ? 0 : r];
     };
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
         const double2 z2 = make_double2(0.0, 0.0);
         g[r] = vg[r] ? ld2(p.g + c * ldg + e) : z2;
         y[r] = (vx[r] && pcn) ? ld2(p.y + c * ld + e) : z2;
-        if (!ZREF) grv[ZREF ? 0 : r] = (vg[r] && p.gr) ? ld2(p.gr + c * ldg + e) : z2;
+        if (!ZREF && !GRL) grv[(ZREF || GRL) ? 0 : r] = (vg[r] && p.gr) ? ld2(p.gr + c * ldg + e) : z2;
         if (!TWG) {
             iev[TWG ? 0 : r] = vg[r] ? ld2(p.inv_eig + e) : z2;
             bcv[TWG ? 0 : r] = vg[r] ? ld2(p.bcoef + e) : z2;
@@ -474,14 +483,15 @@ void launch_r(const StepParams& p, cudaStream_t s) {
 // x <- x_ref + c (x - x_ref) + xi_k over the chunk's accepted steps k (xi_k = G^-1 h_k, rows of
 // XA); the distinct counted states x_j (rows of Xout, for the eigen-projection traces) and the
 // x-space running mean and raw diagonal (PSRF, trace floor, adaptive reference) with their
-// multiplicities. One CTA per chain, threads over the entries (no cross-thread dependence).
-__global__ void __launch_bounds__(256) reconstruct_kernel(double* x, const double* xr, const double* beta, int pcn,
+// multiplicities. Threads over the entries (no cross-thread dependence), 128 per CTA so a
+// chain spreads over d/128 CTAs.
+__global__ void __launch_bounds__(128) reconstruct_kernel(double* x, const double* xr, const double* beta, int pcn,
                                                           const double* XA, int64_t xa_stride, int64_t xa_ld,
                                                           double* Xout, int64_t xo_stride, int64_t ld,
                                                           const int* state_src, const int* state_mult, int out_ld,
                                                           const int* kcount, const int* acc_count, double* mean_x,
                                                           double* diag_x, double keep, double add, int d) {
-    const int c = blockIdx.x;
+    const int c = blockIdx.y;
     const double b = beta[c];
     const double cc = pcn ? sqrt(fmax(0.0, 1.0 - b * b)) : 1.0;
     const int nk = acc_count[c], nj = kcount[c];
@@ -489,7 +499,7 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(double* x, const doubl
     const int* mul = state_mult + (int64_t)c * out_ld;
     const double* xa = XA + c * xa_stride;
     double* xo = Xout + c * xo_stride;
-    for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d; e += gridDim.x * blockDim.x) {
         double v = x[c * ld + e];
         const double r = xr ? xr[c * ld + e] : 0.0;
         double s1 = 0.0, s2 = 0.0;
@@ -561,7 +571,8 @@ void launch_reconstruct(double* x, const double* xr, const double* beta, int pcn
                         double* diag_x, double n_prev, int kc, int chains, int d, cudaStream_t s) {
     if (chains <= 0) return;
     const double total = n_prev + kc;
-    reconstruct_kernel<<<chains, 256, 0, s>>>(x, xr, beta, pcn, XA, xa_stride, xa_ld, Xout, xo_stride, ld, state_src,
+    const dim3 grid((unsigned)std::max(1, (d + 127) / 128), (unsigned)chains);
+    reconstruct_kernel<<<grid, 128, 0, s>>>(x, xr, beta, pcn, XA, xa_stride, xa_ld, Xout, xo_stride, ld, state_src,
                                               state_mult, out_ld, kcount, acc_count, mean_x, diag_x,
                                               total > 0 ? n_prev / total : 0.0, total > 0 ? 1.0 / total : 0.0, d);
     DGB_LAUNCH_CHECK();
