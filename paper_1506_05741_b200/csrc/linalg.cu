@@ -79,10 +79,12 @@ __device__ __forceinline__ void trace_x_block(const double* Sg, const double* mg
     }
 }
 
+constexpr int kBlendPairs = 4;  // row pairs per CTA
+
 // C = wg*Sg + wl*Sl - mb mb^T on the lower triangle, 0 above; optional jitter on the diagonal.
-// One CTA per pair of rows (p, d-1-p) of one chain: the two rows hold d+1 lower entries
-// together, so every CTA moves the same bytes and all threads work (a CTA per row left
-// half the threads idle and made ~2d tiny CTAs per chain).
+// Rows are taken in pairs (p, d-1-p): the two hold d+1 lower entries together, so every
+// pair moves the same bytes and all threads work; a CTA handles kBlendPairs pairs of one
+// chain (a CTA per pair made d/2 short-lived CTAs per chain: 42% warps active, 3.1 TB/s).
 __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const double* mg, const double* Sl,
                                  int64_t sl_stride, const double* ml, int64_t ml_stride, double wg, double wl,
                                  double* mb, int64_t mb_stride, int d, int64_t ld, const int* mask,
@@ -90,72 +92,78 @@ __global__ void blend_cov_kernel(double* const* C_out, const double* Sg, const d
                                  const double* axr, int64_t ax_stride, TraceX tx, int has_tx) {
     const int c = blockIdx.z;
     if (mask && !mask[c]) return;
-    const int npairs = (d + 1) / 2;
+    const int npairs = (d + 1) / 2, nblk = (npairs + kBlendPairs - 1) / kBlendPairs;
     const int p = blockIdx.y;
     if (has_tx && p == (int)gridDim.y - 1) {
         trace_x_block(tx.Sg, tx.mg, tx.dl, tx.ml, wg, wl, tx.mb, tx.tr, tx.try_flag, d, ld, c);
         if (threadIdx.x == 0) tx.status[c] = 0;
         return;
     }
-    if (p == npairs) {  // augmented row r = x - x_ref (solved by the POTRF for the usable guard)
+    if (p == nblk) {  // augmented row r = x - x_ref (solved by the POTRF for the usable guard)
         double* Crow = C_out[c] + (int64_t)d * ld;
         for (int j = threadIdx.x; j < d; j += blockDim.x)
             Crow[j] = ax[c * ax_stride + j] - (axr ? axr[c * ax_stride + j] : 0.0);
         return;
     }
-    const int r1 = p, r2 = d - 1 - p;  // r1 == r2: the middle row of an odd d
     const double* mlc = ml + c * ml_stride;
-    // blended mean (proj/src/moments.cpp:44)
-    const double mb1 = wg * mg[r1] + wl * mlc[r1];
-    const double mb2 = wg * mg[r2] + wl * mlc[r2];
-    if (threadIdx.x == 0 && mb) {
-        mb[c * mb_stride + r1] = mb1;
-        mb[c * mb_stride + r2] = mb2;
-    }
-    // Lower triangle only. The strict upper part of a workspace factor is zero already
-    // (zeroed at allocation and by set_identity; the POTRF zeroes the strict upper part of
-    // every diagonal block it factors, the only upper entries its GEMMs touch), and it
-    // stays zero through factor/workspace pointer swaps.
-    // Column pairs (rows are 64-byte aligned: ld is a multiple of 8), both rows flattened.
-    const double jit = jitter_eps > 0.0 ? jitter_eps * (tr[c] / (double)d) : 0.0;  // proposal.cpp:229-231
-    const int q1 = (r1 + 2) / 2, q2 = r2 == r1 ? 0 : (r2 + 2) / 2;
-    for (int q = threadIdx.x; q < q1 + q2; q += blockDim.x) {
-        const bool first = q < q1;
-        const int i = first ? r1 : r2;
-        const int j = 2 * (first ? q : q - q1);
-        const double mbi = first ? mb1 : mb2;
-        // the pair (j, j+1) is loaded as one double2 unless j+1 lies past the diagonal: at
-        // j = i = d-1 with ld == d it would be past the end of the row (and of the buffer)
-        const bool pair = j + 1 <= i;
-        const double* sgp = Sg + (int64_t)i * ld + j;
-        const double* slp = Sl + c * sl_stride + (int64_t)i * ld + j;
-        double2 sg, sl, g2, l2;
-        if (pair) {
-            sg = *reinterpret_cast<const double2*>(sgp);
-            sl = *reinterpret_cast<const double2*>(slp);
-            g2 = *reinterpret_cast<const double2*>(mg + j);
-            l2 = *reinterpret_cast<const double2*>(mlc + j);
-        } else {
-            sg = make_double2(*sgp, 0.0);
-            sl = make_double2(*slp, 0.0);
-            g2 = make_double2(mg[j], 0.0);
-            l2 = make_double2(mlc[j], 0.0);
+    // jitter eps (tr / d) (proposal.cpp:229-231); with jm, eps (tr / d) J -- the whitened
+    // space's image of eps (tr / d) I -- read only when there is jitter
+    const double jit = jitter_eps > 0.0 ? jitter_eps * (tr[c] / (double)d) : 0.0;
+    for (int pp = p * kBlendPairs; pp < min(npairs, (p + 1) * kBlendPairs); ++pp) {
+        const int r1 = pp, r2 = d - 1 - pp;  // r1 == r2: the middle row of an odd d
+        // blended mean (proj/src/moments.cpp:44)
+        const double mb1 = wg * mg[r1] + wl * mlc[r1];
+        const double mb2 = wg * mg[r2] + wl * mlc[r2];
+        if (threadIdx.x == 0 && mb) {
+            mb[c * mb_stride + r1] = mb1;
+            mb[c * mb_stride + r2] = mb2;
         }
-        // covariance :90-101 (S exactly symmetric) of the blend :45-46
-        double v0 = (wg * sg.x + wl * sl.x) - mbi * (wg * g2.x + wl * l2.x);
-        double v1 = (wg * sg.y + wl * sl.y) - mbi * (wg * g2.y + wl * l2.y);
-        if (jm) {  // jitter eps (tr / d) J: the whitened space's image of eps (tr / d) I
-            v0 += jit * jm[(int64_t)i * ld + j];
-            if (pair) v1 += jit * jm[(int64_t)i * ld + j + 1];
-        } else {
-            if (j == i) v0 += jit;
-            if (j + 1 == i) v1 += jit;
+        // Lower triangle only. The strict upper part of a workspace factor is zero already
+        // (zeroed at allocation and by set_identity; the POTRF zeroes the strict upper part
+        // of every diagonal block it factors, the only upper entries its GEMMs touch), and
+        // it stays zero through factor/workspace pointer swaps.
+        // Column pairs (rows are 64-byte aligned: ld is a multiple of 8), both rows flattened.
+        const int q1 = (r1 + 2) / 2, q2 = r2 == r1 ? 0 : (r2 + 2) / 2;
+        for (int q = threadIdx.x; q < q1 + q2; q += blockDim.x) {
+            const bool first = q < q1;
+            const int i = first ? r1 : r2;
+            const int j = 2 * (first ? q : q - q1);
+            const double mbi = first ? mb1 : mb2;
+            // the pair (j, j+1) is loaded as one double2 unless j+1 lies past the diagonal: at
+            // j = i = d-1 with ld == d it would be past the end of the row (and of the buffer)
+            const bool pair = j + 1 <= i;
+            const double* sgp = Sg + (int64_t)i * ld + j;
+            const double* slp = Sl + c * sl_stride + (int64_t)i * ld + j;
+            double2 sg, sl, g2, l2;
+            if (pair) {
+                sg = *reinterpret_cast<const double2*>(sgp);
+                sl = __ldcs(reinterpret_cast<const double2*>(slp));  // read once: stream it
+                g2 = *reinterpret_cast<const double2*>(mg + j);
+                l2 = *reinterpret_cast<const double2*>(mlc + j);
+            } else {
+                sg = make_double2(*sgp, 0.0);
+                sl = make_double2(*slp, 0.0);
+                g2 = make_double2(mg[j], 0.0);
+                l2 = make_double2(mlc[j], 0.0);
+            }
+            // covariance :90-101 (S exactly symmetric) of the blend :45-46
+            double v0 = (wg * sg.x + wl * sl.x) - mbi * (wg * g2.x + wl * l2.x);
+            double v1 = (wg * sg.y + wl * sl.y) - mbi * (wg * g2.y + wl * l2.y);
+            if (jit != 0.0) {
+                if (jm) {
+                    v0 += jit * jm[(int64_t)i * ld + j];
+                    if (pair) v1 += jit * jm[(int64_t)i * ld + j + 1];
+                } else {
+                    if (j == i) v0 += jit;
+                    if (j + 1 == i) v1 += jit;
+                }
+            }
+            double* Crow = C_out[c] + (int64_t)i * ld;
+            if (pair)
+                *reinterpret_cast<double2*>(Crow + j) = make_double2(v0, v1);
+            else
+                Crow[j] = v0;
         }
-        double* Crow = C_out[c] + (int64_t)i * ld;
-        if (pair)
-            *reinterpret_cast<double2*>(Crow + j) = make_double2(v0, v1);
-        else
-            Crow[j] = v0;
     }
 }
 
@@ -691,7 +699,8 @@ void launch_blend_cov(double* const* C_out, const double* Sg, const double* mg, 
                       int64_t mb_stride, int chains, int d, int64_t ld, const int* mask, double jitter_eps,
                       const double* tr, const double* jitter_mat, cudaStream_t s, const double* aug_x,
                       const double* aug_xr, int64_t aug_stride, const TraceX* tx) {
-    dim3 grid(1, (unsigned)((d + 1) / 2 + (aug_x ? 1 : 0) + (tx ? 1 : 0)), chains);
+    const int nblk = ((d + 1) / 2 + kBlendPairs - 1) / kBlendPairs;
+    dim3 grid(1, (unsigned)(nblk + (aug_x ? 1 : 0) + (tx ? 1 : 0)), chains);
     blend_cov_kernel<<<grid, 256, 0, s>>>(C_out, Sg, mg, Sl, sl_stride, ml, ml_stride, wg, wl, mb, mb_stride, d, ld,
                                           mask, jitter_eps, tr, jitter_mat, aug_x, aug_xr,
                                           aug_stride > 0 ? aug_stride : ld, tx ? *tx : TraceX{}, tx ? 1 : 0);
