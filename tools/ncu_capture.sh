@@ -13,12 +13,12 @@ full="ncu --set full --clock-control none --import-source on -f -c 1"
 if [ "$only" = all ]; then
 # the plain run first (ncu only after the same command exited 0 without it)
 $cmd > gpurun_out/${tag}_plain.log 2>&1
-for cls in gemm_target trmm_noise syrk_moments; do
+for cls in trmm_noise syrk_moments xi_accepted; do
     # skip the warm-up batch's launches of the class (4 windows; TRMM: 3, window 0 is the identity)
     $full --nvtx --nvtx-include "$cls/" -k regex:gemm_f64 -s 3 -o gpurun_out/${tag}_${cls} $cmd \
         > gpurun_out/${tag}_${cls}.log 2>&1
 done
-for k in mh_window normals blend_cov; do
+for k in mh_window normals blend_cov reconstruct; do
     $full -k regex:$k -s 4 -o gpurun_out/${tag}_${k} $cmd > gpurun_out/${tag}_${k}.log 2>&1
 done
 fi
