@@ -13,6 +13,8 @@
 // each step is one fused pass (candidate, two dot products, CTA reduction with
 // a single barrier, accept/reject from the chain's Philox uniform) — the
 // "fused warp-level accept/reject" of the design.
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace dgb {
@@ -78,20 +80,6 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 
-// scale * v (this thread's pairs of a state vector) -> one window row
-template <int R, int T>
-__device__ __forceinline__ void store_row(double* row, const double2 (&v)[R], const bool (&valid)[R], int tid, int d,
-                                          double scale) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int e = 2 * (tid + r * T);
-        if (!valid[r]) continue;
-        const double2 w = make_double2(scale * v[r].x, scale * v[r].y);
-        if (e + 1 < d) st2(row + e, w);
-        else row[e] = w.x;
-    }
-}
-
 // The window in whitened coordinates. The proposal factor is kept as L_z = G L (the Cholesky
 // factor of the whitened covariance G C G^T, Engine::enqueue_refactor), so the window's
 // product H = s W L_z^T gives h_t = G xi_t directly and the step needs no x-space row:
@@ -156,22 +144,45 @@ __device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t byt
 // cy = c y) are kept ready (2 pairs per thread at most: registers). ZREF: the reference point
 // is the origin (G x_ref = 0, no registers). TWG: the per-entry log-density constants are
 // read through L1 each step instead of held in registers (4 pairs per thread).
-template <int R, int T, bool PRE, bool ZREF>
+// pairs of entries per CTA when a chain of dg entries is split over CL CTAs: an even split,
+// rounded up to 4 pairs (64-byte slices for the bulk copies)
+__host__ __device__ inline int cluster_span(int dg, int CL) {
+    const int pairs = (dg + 1) / 2;
+    return ((pairs + CL - 1) / CL + 3) & ~3;
+}
+
+// CL > 1: a chain is split over a thread-block cluster of CL CTAs, CTA r owning an even slice
+// of the entries (cluster_span; every CTA keeps R <= 2 pairs per thread in registers and its
+// own TMA ring of row slices); the per-step partial sums are exchanged through
+// distributed shared memory -- every warp stores its partial into each CTA of the cluster --
+// and one cluster barrier per step replaces the CTA barrier. Every CTA sums the CL x NW
+// partials in the same order, so all take the same accept decision.
+template <int R, int T, bool PRE, bool ZREF, int CL>
 __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
     constexpr bool TWG = R >= 4;
     constexpr int NW = T / 32;
-    const int c = blockIdx.x;
+    namespace cg = cooperative_groups;
+    const int rank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    const int c = blockIdx.x / CL;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int d = p.d, dg = p.dg;
     const int64_t ld = p.ld, ldg = p.ldg;
     const bool pcn = p.pcn != 0;
     extern __shared__ __align__(128) double ring[];  // NS stages, then the log-uniform table
     __shared__ __align__(8) uint64_t full[kMaxStages];
-    __shared__ __align__(16) double red[2][NW][2];
-    // a stage: the h row (ldg: d + the twisted rows) and, for the pCN form, the w row (ld)
-    const uint32_t hrow_bytes = (uint32_t)(ldg * sizeof(double)), wrow_bytes = (uint32_t)(ld * sizeof(double));
+    __shared__ __align__(16) double red[2][CL * NW][2];
+    // a stage: this CTA's slice of the h row (ldg: d + the twisted rows) and, for the pCN
+    // form, of the w row (ld); e0 = the slice's first entry
+    const int span = CL > 1 ? cluster_span(dg, CL) : R * T;  // pairs of this CTA's slice
+    const int e0 = CL > 1 ? rank * 2 * span : 0, e_end = CL > 1 ? e0 + 2 * span : 2 * R * T;
+    auto clip = [](int64_t v, int64_t hi) -> int64_t { return v < 0 ? 0 : (v > hi ? hi : v); };
+    const int64_t h_len = CL > 1 ? clip(ldg - e0, 2 * span) : ldg;
+    const int64_t w_len = CL > 1 ? clip(ld - e0, 2 * span) : ld;
+    const int64_t stage_h = CL > 1 ? 2 * span : ldg;
+    const uint32_t hrow_bytes = (uint32_t)(h_len * sizeof(double)), wrow_bytes = (uint32_t)(w_len * sizeof(double));
     double* stage0 = ring;
-    const int64_t stage_len = ldg + (pcn ? ld : 0);
+    const int64_t stage_len = stage_h + (pcn ? (CL > 1 ? 2 * span : ld) : 0);
+    const bool lead = rank == 0;  // writes the chain's scalars
 
     const double beta = p.beta[c];
     const double cc = pcn ? sqrt(fmax(0.0, 1.0 - beta * beta)) : 1.0;  // proj/src/proposal.cpp:120
@@ -186,35 +197,38 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
 
     auto issue = [&](int t, int s) {  // producer: row t of the window into stage s = t % NS
         double* st = stage0 + s * stage_len;
-        mbar_expect_tx(&full[s], hrow_bytes + (pcn ? wrow_bytes : 0));
-        tma_row(st, Hc + (int64_t)t * ldg, hrow_bytes, &full[s]);
-        if (pcn) tma_row(st + ldg, Wc + (int64_t)t * ld, wrow_bytes, &full[s]);
+        const uint32_t wb = (pcn && w_len > 0) ? wrow_bytes : 0u;
+        mbar_expect_tx(&full[s], hrow_bytes + wb);
+        if (hrow_bytes) tma_row(st, Hc + (int64_t)t * ldg + e0, hrow_bytes, &full[s]);
+        if (wb) tma_row(st + stage_h, Wc + (int64_t)t * ld + e0, wb, &full[s]);
     };
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    if constexpr (CL > 1)  // every CTA of the cluster runs before any stores into its shared memory
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
     if (tid == 0)
         for (int t = 0; t < NS && t < p.n_lag; ++t) issue(t, t);
 
-    // GRL: the reference point read through L1 each step (8 pairs per thread: registers would spill)
-    constexpr bool GRL = !ZREF && R >= 8;
+    // GRL: the reference point read through L1 each step (4+ pairs per thread: registers would spill)
+    constexpr bool GRL = !ZREF && R >= 4;
     double2 g[R], y[R], grv[(ZREF || GRL) ? 1 : R], iev[TWG ? 1 : R], bcv[TWG ? 1 : R], ga[R], cy[R];
     bool vx[R], vg[R];  // entry pair e in x-space (e < d) / in g-space (e < dg)
     auto GR = [&](int r) -> double2 {
         if (ZREF) return make_double2(0.0, 0.0);
         if (GRL) {
-            const int e = 2 * (tid + r * T);
+            const int e = e0 + 2 * (tid + r * T);
             return e < dg ? __ldg(reinterpret_cast<const double2*>(p.gr + c * ldg + e)) : make_double2(0.0, 0.0);
         }
         return grv[(ZREF || GRL) ? 0 : r];
     };
     auto IE = [&](int r) -> double2 {
-        return TWG ? __ldg(reinterpret_cast<const double2*>(p.inv_eig) + tid + r * T) : iev[TWG ? 0 : r];
+        return TWG ? __ldg(reinterpret_cast<const double2*>(p.inv_eig) + e0 / 2 + tid + r * T) : iev[TWG ? 0 : r];
     };
     auto BC = [&](int r) -> double2 {
-        return TWG ? __ldg(reinterpret_cast<const double2*>(p.bcoef) + tid + r * T) : bcv[TWG ? 0 : r];
+        return TWG ? __ldg(reinterpret_cast<const double2*>(p.bcoef) + e0 / 2 + tid + r * T) : bcv[TWG ? 0 : r];
     };
     auto refresh = [&](int r) {
         if (!PRE) return;
@@ -226,9 +240,9 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
     };
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int e = 2 * (tid + r * T);
-        vx[r] = e < d;
-        vg[r] = e < dg;
+        const int e = e0 + 2 * (tid + r * T);
+        vx[r] = e < d && e < e_end;
+        vg[r] = e < dg && e < e_end;
         const double2 z2 = make_double2(0.0, 0.0);
         g[r] = vg[r] ? ld2(p.g + c * ldg + e) : z2;
         y[r] = (vx[r] && pcn) ? ld2(p.y + c * ld + e) : z2;
@@ -252,7 +266,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
     // one entry pair's candidate from the h and w rows: the same operations whether called for
     // the dot products or, after the decision, to adopt the candidate (bit-identical)
     auto cand = [&](const double* ph, const double* pw, int r, double2& gc, double2& yc) {
-        const int e = 2 * (tid + r * T);
+        const int e = e0 + 2 * (tid + r * T);
         const double2 h = vg[r] ? ld2(ph + e) : make_double2(0.0, 0.0);
         if (PRE) {
             gc.x = ga[r].x + h.x;
@@ -277,7 +291,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
     auto store_z = [&](double* row, double scale) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int e = 2 * (tid + r * T);
+            const int e = e0 + 2 * (tid + r * T);
             if (!vx[r]) continue;
             const double2 v = make_double2(scale * g[r].x, scale * g[r].y);
             if (e + 1 < d) st2(row + e, v);
@@ -305,7 +319,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             double2 gc, yc;
-            cand(st, st + ldg, r, gc, yc);
+            cand(st - e0, st + stage_h - e0, r, gc, yc);
             // whitened log density: ie w0^2 + ie' (w1^2 - bc' g1^2), w1 = g1 + bc g0^2
             // (Engine::upload_target)
             const double2 ie = IE(r), bc = BC(r);
@@ -320,9 +334,21 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
         MH_PROF(2);
         const double ws = warp_sum2(sa0 + sa1, sb0 + sb1, lane);
         const int buf = t & 1;
-        if ((lane & 15) == 0) red[buf][warp][lane >> 4] = ws;
-        MH_PROF(3);
-        __syncthreads();
+        if constexpr (CL > 1) {
+            // this warp's partial into slot (rank, warp) of every CTA of the cluster
+            if ((lane & 15) == 0) {
+                namespace cg = cooperative_groups;
+                cg::cluster_group cl = cg::this_cluster();
+#pragma unroll
+                for (int q = 0; q < CL; ++q) cl.map_shared_rank(&red[buf][rank * NW + warp][0], q)[lane >> 4] = ws;
+            }
+            MH_PROF(3);
+            asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        } else {
+            if ((lane & 15) == 0) red[buf][warp][lane >> 4] = ws;
+            MH_PROF(3);
+            __syncthreads();
+        }
         MH_PROF(4);
         // every thread is done with step t-1 (its stage may be re-read for an adoption until
         // this barrier): refill that stage NS - 1 steps ahead
@@ -338,7 +364,7 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
 #pragma unroll
             for (int k = 0; k < NA; ++k) v[k] = *reinterpret_cast<const double2*>(&red[buf][k][0]);
 #pragma unroll
-            for (int k = NA; k < NW; ++k) {
+            for (int k = NA; k < CL * NW; ++k) {
                 const double2 u = *reinterpret_cast<const double2*>(&red[buf][k][0]);
                 v[k % NA].x += u.x;
                 v[k % NA].y += u.y;
@@ -364,19 +390,19 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
         if (fresh) {
             if (cp.j >= 0) {
                 store_z(Hc + (int64_t)cp.j * ldg, cp.mult);
-                if (tid == 0) mul[cp.j] = (int)cp.mult;
+                if (tid == 0 && lead) mul[cp.j] = (int)cp.mult;
             }
             ++cp.j;
             cp.mult = 0.0;
         }
         if (acc) {
-            const double* ph = late ? st : Hc + (int64_t)t * ldg;
-            const double* pw = late ? st + ldg : Wc + (int64_t)t * ld;
+            const double* ph = late ? st - e0 : Hc + (int64_t)t * ldg;
+            const double* pw = late ? st + stage_h - e0 : Wc + (int64_t)t * ld;
             // keep h_t (its z part) for the x-space increment xi_t = G^-1 h_t of this step
             double* keep = Xc + (int64_t)acc_k * ld;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const int e = 2 * (tid + r * T);
+                const int e = e0 + 2 * (tid + r * T);
                 if (vx[r]) {
                     if (e + 1 < d) st2(keep + e, ld2(ph + e));
                     else keep[e] = ph[e];
@@ -394,10 +420,10 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
         }
         if (fresh) {
             store_z(Wc + (int64_t)cp.j * ld, 1.0);
-            if (tid == 0) src[cp.j] = acc_k - 1;  // the state after accepted step acc_k - 1 (-1: the start)
+            if (tid == 0 && lead) src[cp.j] = acc_k - 1;  // the state after accepted step acc_k - 1 (-1: the start)
         }
         if (counted) cp.mult += 1.0;
-        if (tid == 0) {
+        if (tid == 0 && lead) {
             if (p.trace_lp) p.trace_lp[(int64_t)c * p.out_ld + t] = lp;
             if (p.accept_out) p.accept_out[(int64_t)c * p.out_ld + t] = acc ? 1 : 0;
             if (p.log_ratio_out) p.log_ratio_out[(int64_t)c * p.out_ld + t] = ratio;
@@ -415,11 +441,11 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
 #endif
     if (cp.j >= 0) {
         store_z(Hc + (int64_t)cp.j * ldg, cp.mult);
-        if (tid == 0) mul[cp.j] = (int)cp.mult;
+        if (tid == 0 && lead) mul[cp.j] = (int)cp.mult;
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int e = 2 * (tid + r * T);
+        const int e = e0 + 2 * (tid + r * T);
         if (vg[r]) {
             if (e + 1 < dg) st2(p.g + c * ldg + e, g[r]);
             else p.g[c * ldg + e] = g[r].x;
@@ -429,7 +455,9 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
             else p.y[c * ld + e] = y[r].x;
         }
     }
-    if (tid == 0) {
+    if constexpr (CL > 1)  // no CTA leaves while a partner may still store into its shared memory
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (tid == 0 && lead) {
         p.log_pi[c] = lp;
         if (pcn) p.quad[c] = q;
         p.n_accepted[c] = nacc;
@@ -439,9 +467,12 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
     }
 }
 
-template <int R, int T, bool PRE = (R * T <= 512)>
+template <int R, int T, bool PRE = (R * T <= 512), int CL = 1>
 bool try_tma(const StepParams& p, cudaStream_t s) {
-    const size_t stage = (size_t)(p.ldg + (p.pcn ? p.ld : 0)) * sizeof(double);
+    if (CL > 1 && cluster_span(p.dg, CL) > R * T) return false;
+    const size_t stage = (CL > 1 ? (size_t)2 * cluster_span(p.dg, CL) * (p.pcn ? 2 : 1)
+                                 : (size_t)(p.ldg + (p.pcn ? p.ld : 0))) *
+                         sizeof(double);
     const size_t table = (size_t)p.n_lag * sizeof(double);
     constexpr size_t kMaxSmem = 220 * 1024;
     if (table + stage > kMaxSmem) return false;
@@ -458,22 +489,43 @@ bool try_tma(const StepParams& p, cudaStream_t s) {
     NS = std::min(NS, 6);
     if (env_ns > 0) NS = std::min<int>(env_ns, (int)std::min<size_t>(kMaxStages, (kMaxSmem - table) / stage));
     const size_t smem = NS * stage + table;
-    auto kern = p.gr ? mh_window_kernel<R, T, PRE, false> : mh_window_kernel<R, T, PRE, true>;
+    auto kern = p.gr ? mh_window_kernel<R, T, PRE, false, CL> : mh_window_kernel<R, T, PRE, true, CL>;
     set_smem_attr(reinterpret_cast<const void*>(kern), (int)smem);
-    kern<<<p.chains, T, smem, s>>>(p, NS);
+    if constexpr (CL == 1) {
+        kern<<<p.chains, T, smem, s>>>(p, NS);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(p.chains * CL));
+        cfg.blockDim = dim3(T);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        DGB_CUDA(cudaLaunchKernelEx(&cfg, kern, p, NS));
+    }
     return true;
 }
 
 void launch_r(const StepParams& p, cudaStream_t s) {
     const int pairs = (p.dg + 1) / 2;  // the g-space entries (d + the twisted rows) set the width
     // 256 threads (up to 2 double2 pairs each) up to d = 1024, then 512 threads: fewer warps
-    // per step barrier and reduction for the small dimensions where the step loop matters most
+    // per step barrier and reduction for the small dimensions where the step loop matters most.
+    // Wider rows (d > 4096) split each chain over a cluster of 4 CTAs of 512 threads x 2 pairs:
+    // no thread holds more than 2 pairs of each state vector (one CTA with 8 pairs per thread
+    // spilled 420 B) and the chain's row stream is read by 4 SMs. (A 2-CTA cluster at
+    // d = 2040 -- 1122 pairs with the twisted rows -- measured 4% slower per batch than one
+    // CTA with 4 pairs per thread: twice the CTAs of the 1-CTA-per-SM step kernel.)
     bool done = false;
     if (pairs <= 256) done = try_tma<1, 256>(p, s);
     else if (pairs <= 512) done = try_tma<2, 256>(p, s);
     else if (pairs <= 1024) done = try_tma<2, 512>(p, s);
     else if (pairs <= 2048) done = try_tma<4, 512>(p, s);
-    else if (pairs <= 4096) done = try_tma<8, 512, false>(p, s);
+    else if (pairs <= 4096) done = try_tma<2, 512, false, 4>(p, s);
     if (!done) throw CudaError("mh_window: dimension above 8192 is not supported by this build");
     DGB_LAUNCH_CHECK();
     count_launch();

@@ -136,3 +136,27 @@ def test_twisted_pi5_d2040_window(b200, tmp_path):
               inflation=1.2, threads=min(THREADS, P), traces=True, trace_thin=7)
     for p in range(P):
         assert check_chain(res, cap, o, p, p, traces=True) > 0
+
+
+@pytest.mark.parametrize("d,adaptive", [(4100, False), (4100, True), (2100, True)])
+def test_wide_rows_window(b200, tmp_path, d, adaptive):
+    """The wide-row MH kernels. d = 4100 > 4096 entries: each chain is split over a 4-CTA
+    cluster (partial sums through distributed shared memory, one cluster barrier per step,
+    every CTA deciding from the same ordered sum); d = 2100: one CTA with 4 pairs per thread,
+    the reference point read through L1. Two short windows on two chains, the GPU-built pi1
+    target loaded by the oracle; with the adaptive reference point the second window steps
+    around a moved x_ref (the kernel variants that carry G x_ref)."""
+    t = b200.target_build("pi1", d, 5)
+    path = str(tmp_path / f"pi1_{d}.bin")
+    t.save(path)
+    td = O.read_target(path)
+    P, nl, M, seed = 2, 48, 2, 17
+    extra = dict(adaptive_ref=1, n_ref_start=nl) if adaptive else {}
+    res, cap = b200.sample_capture(t, kernel="diam", chains=P, intervals_per_batch=M, max_batches=1, n_lag=nl,
+                                   n0=0, master_seed=seed, record_traces=1, trace_thin=5,
+                                   trace_eigen_projections=1, **extra)
+    ws = [captured_windows(cap, p, M, nl, d) for p in range(P)]
+    o = O.run(td, kind="diam", chains=P, M=M, K=1, seed=seed, inject_w=ws, record_decisions=True, n_lag=nl, n0=0,
+              threads=min(THREADS, P), traces=True, trace_thin=5, **extra)
+    for p in range(P):
+        check_chain(res, cap, o, p, p, traces=True)
