@@ -127,23 +127,24 @@ def run_options(cfg, chains, **over):
     return o
 
 
-def ncu_gemm_traffic(cfg_name, chains, d, n_lag, distinct=1.0):
-    """DRAM bytes per launch of the three DMMA GEMM classes from the committed `ncu --set
-    full` captures (profiles/r02_ncu_<class>.csv, tools/ncu_capture.sh: d=1024, 64 chains),
-    against their algorithmic bytes (operands in once, results out once)."""
+def ncu_gemm_traffic(cfg_name, chains, d, n_lag, distinct=1.0, accepted=0.0):
+    """DRAM bytes per launch of the DMMA GEMM classes from the committed `ncu --set full`
+    captures (profiles/r02b_ncu_<class>.csv, tools/ncu_capture.sh: d=1024, 64 chains, single
+    stream), against their algorithmic bytes (operands in once, results out once)."""
     import csv
     if cfg_name != "d1024" or chains != 64:
         return None
     out, alg = {}, {}
-    w = chains * n_lag * d * 8       # one window matrix (W, Xi, H or X) of all chains
-    tri = chains * d * (d + 1) // 2 * 8  # the lower triangles of all chains' L or S
-    # gemm_target: Xi in, H out, the whitening factor G (lower triangle) once
-    # syrk_moments: the window's distinct states (the profiled fraction of the rows) in, the
-    # lower S read and written
-    alg_bytes = {"gemm_target": 2 * w + d * (d + 1) // 2 * 8, "trmm_noise": 2 * w + tri,
-                 "syrk_moments": int(distinct * w) + 2 * tri}
-    for cls in ("gemm_target", "trmm_noise", "syrk_moments"):
-        path = os.path.join(ROOT, "profiles", f"r02_ncu_{cls}.csv")
+    w = chains * n_lag * d * 8       # one window matrix (W, Xi or H) of all chains
+    tri = chains * d * (d + 1) // 2 * 8  # the lower triangles of all chains' L_z or S_z
+    # trmm_noise: W in, H out, the factors' lower triangles once
+    # syrk_moments: the window's distinct states (rows of H and W) in, the lower S_z read and
+    # written
+    # xi_accepted: the accepted h rows in, their increments out, the shared G^-1 once
+    alg_bytes = {"trmm_noise": 2 * w + tri, "syrk_moments": int(2 * distinct * w) + 2 * tri,
+                 "xi_accepted": int(2 * accepted * w) + tri // chains}
+    for cls in ("trmm_noise", "syrk_moments", "xi_accepted"):
+        path = os.path.join(ROOT, "profiles", f"r02b_ncu_{cls}.csv")
         if not os.path.exists(path):
             return None
         rows = list(csv.reader(open(path)))
@@ -156,7 +157,8 @@ def ncu_gemm_traffic(cfg_name, chains, d, n_lag, distinct=1.0):
         out[cls] = tot
         alg[cls] = alg_bytes[cls]
     return {"dram_bytes_per_launch": out, "algorithmic_bytes_per_launch": alg,
-            "source": "profiles/r02_ncu_*.csv (one steady-state launch each, single stream)"}
+            "source": "profiles/r02b_ncu_*.csv (one steady-state launch each, single stream; writes still "
+                      "in L2 when the kernel ends are not counted)"}
 
 
 def time_to_cov_error(lib, with_reference: bool):
@@ -342,6 +344,7 @@ def impl_b200(args):
     distinct = st["syrk_moments"][1] / syrk_full if syrk_full else 1.0
     accepted = st["xi_accepted"][1] / syrk_full if syrk_full else 0.0
     alg_flops = sum(v[1] for v in st.values()) * (chains / world) / prof_chains
+    traffic = ncu_gemm_traffic(args.config, per_gpu, d, n_lag, distinct, accepted)
     del eng
 
     # ---- end-to-end through the C ABI (host target, result back to host)
@@ -392,9 +395,12 @@ def impl_b200(args):
                        "memory_plan": layout,
                        "l2": "no flush needed: per-step working set "
                              f"{(3 * d * d + 3 * n_lag * d) * 8 * per_gpu / 1e9:.1f} GB >> 126 MB L2"},
-            "roofline": {"bound": "fp64-dmma", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+            "roofline": {"bound": "tensor", "pipe": "FP64 DMMA (mma.sync.m8n8k4.f64; tcgen05 has no f64 kind)",
+                         "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                          "frac": achieved / peak.value if peak.value else None,
-                         "traffic": ncu_gemm_traffic(args.config, per_gpu, d, n_lag, distinct),
+                         "traffic": traffic["dram_bytes_per_launch"]["trmm_noise"] if traffic else None,
+                         "traffic_kernel": "trmm_noise (the largest launch of the class)",
+                         "traffic_detail": traffic,
                          "kernel": "gemm_f64 (window TRMM H = s W L_z^T, twisted rows, SYRK moments, "
                                    "accepted increments)",
                          "share_of_step": g_ms / prof_total if prof_total else None,

@@ -29,6 +29,6 @@ cmd3="python tools/profile_step.py --batches 2"
 $cmd3 > gpurun_out/${tag}_plain3.log 2>&1
 $full --nvtx --nvtx-include "potrf/" -k regex:gemm_f64 -s 45 -o gpurun_out/${tag}_potrf_update $cmd3 \
     > gpurun_out/${tag}_potrf_update.log 2>&1
-$full -k regex:potrf_diag -s 200 -o gpurun_out/${tag}_potrf_diag $cmd3 > gpurun_out/${tag}_potrf_diag.log 2>&1
+$full -k regex:potrf_diag -s 20 -o gpurun_out/${tag}_potrf_diag $cmd3 > gpurun_out/${tag}_potrf_diag.log 2>&1
 $full -k regex:potrf_trsm -s 100 -o gpurun_out/${tag}_potrf_trsm $cmd3 > gpurun_out/${tag}_potrf_trsm.log 2>&1
 echo captured

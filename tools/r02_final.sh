@@ -8,7 +8,7 @@ python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r02_bench_ref
 for c in d2040 d4096 d8192; do
     timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r02_bench_$c.json 2> gpurun_out/r02_bench_$c.err
 done
-ncu --metrics gpu__time_duration.sum --clock-control none -c 2500 --csv --log-file gpurun_out/r02_launches_d1024.csv \
+DIAM_B200_GROUPS=1 ncu --metrics gpu__time_duration.sum --clock-control none -c 2500 --csv --log-file gpurun_out/r02_launches_d1024.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/r02_launches.log 2>&1
 bash tools/ncu_capture.sh r02b > gpurun_out/r02b_capture.log 2>&1
 echo done
