@@ -34,7 +34,12 @@ inline void launch_check(const char* file, int line) {
 
 // Process-wide count of our own kernel launches (bench.py reports it as gpu_launches).
 extern std::atomic<uint64_t> g_launch_count;
-inline void count_launch(uint64_t n = 1) { g_launch_count.fetch_add(n, std::memory_order_relaxed); }
+// this thread's share (a stream capture counts the kernels it records, not launches)
+extern thread_local uint64_t t_launch_count;
+inline void count_launch(uint64_t n = 1) {
+    g_launch_count.fetch_add(n, std::memory_order_relaxed);
+    t_launch_count += n;
+}
 
 // Raise a kernel's dynamic shared-memory limit to `bytes` on the CURRENT device (the
 // attribute is per device; engines on several devices or threads share the table).

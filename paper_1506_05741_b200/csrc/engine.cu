@@ -19,6 +19,7 @@
 namespace dgb {
 
 std::atomic<uint64_t> g_launch_count{0};
+thread_local uint64_t t_launch_count = 0;
 
 bool sync_check_enabled() {
     static const bool on = [] {
@@ -189,6 +190,13 @@ Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shar
         for (int i = 0; i < 6; ++i)
             if (v.find(names[i]) != std::string::npos) twice_ |= 1u << i;
     }
+    {
+        static const bool graphs_off = [] {
+            const char* e = std::getenv("DIAM_B200_GRAPHS");
+            return e && std::atoi(e) == 0;
+        }();
+        use_graphs_ = !graphs_off && !sync_check_enabled();
+    }
     if (comm_) {
         rank_ = comm_->rank();
         world_ = comm_->size();
@@ -350,6 +358,7 @@ Engine::~Engine() {
     };
     if (stream_) cudaStreamSynchronize(stream_);
     for (auto& g : groups_) {
+        if (g.potrf_exec) cudaGraphExecDestroy(g.potrf_exec);
         if (g.sr) stream_release(g.sr, g.prio_sr);
         if (g.s) stream_release(g.s, g.prio_s);
         if (g.ev_steps) cudaEventDestroy(g.ev_steps);
@@ -1079,6 +1088,33 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
                             s);
 }
 
+// The group's first attempt at a window's factorization. Its ~3 launches per 128-wide block
+// column take the same arguments every window (device pointer arrays, the group's masks and
+// workspace), so from the second window on they run as one CUDA graph captured on the
+// refactor stream: one host call instead of 22 (d=1024), and graph-internal dependencies
+// instead of stream ones. (The jitter ladder's retries, with their own masks, launch directly.)
+void Engine::factor(Group& g, cudaStream_t s, bool aug) {
+    const int C = g.C, o = g.off;
+    if (!use_graphs_ || g.potrf_calls++ == 0) {  // the first call also sets kernel attributes
+        potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+        return;
+    }
+    if (!g.potrf_exec) {
+        cudaGraph_t graph = nullptr;
+        DGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const uint64_t n0 = t_launch_count;
+        potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+        g.potrf_nodes = t_launch_count - n0;
+        DGB_CUDA(cudaStreamEndCapture(s, &graph));
+        g_launch_count.fetch_sub(g.potrf_nodes, std::memory_order_relaxed);  // recorded, not launched
+        t_launch_count -= g.potrf_nodes;
+        DGB_CUDA(cudaGraphInstantiate(&g.potrf_exec, graph, 0));
+        DGB_CUDA(cudaGraphDestroy(graph));
+    }
+    DGB_CUDA(cudaGraphLaunch(g.potrf_exec, s));
+    count_launch(g.potrf_nodes);
+}
+
 void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {
     const int C = g.C, o = g.off;
     const cudaStream_t s = g.sr;
@@ -1111,10 +1147,10 @@ void Engine::enqueue_refactor(Group& g, const WindowPlan& p) {
         timed_end("blend_cov", 0.0, s);
         nvtxRangePushA("potrf");
         timed_begin(s);
-        potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+        factor(g, s, aug);
         if (twice_ & kTwicePotrf) {  // blend + factorization again: same inputs, same factor
             blend();
-            potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+            factor(g, s, aug);
         }
         timed_end("potrf", (double)C * d_ * (double)d_ * d_ / 3.0, s);
         nvtxRangePop();

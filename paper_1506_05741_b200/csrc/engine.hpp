@@ -99,6 +99,8 @@ private:
         // POTRF launches of one group are scheduled ahead of the other groups' GEMMs
         cudaStream_t sr = nullptr;
         cudaEvent_t ev_steps = nullptr, ev_ref = nullptr;
+        cudaGraphExec_t potrf_exec = nullptr;  // the factorization's launches (Engine::factor)
+        uint64_t potrf_nodes = 0, potrf_calls = 0;
     };
     // host-side scalars of one lag window, identical for every chain
     struct WindowPlan {
@@ -298,6 +300,8 @@ private:
     // the run is unchanged and the batch time grows by what one more instance costs in the
     // overlapped schedule
     unsigned twice_ = 0;
+    bool use_graphs_ = true;  // DIAM_B200_GRAPHS=0 or DIAM_B200_SYNC_CHECK: direct launches
+    void factor(Group& g, cudaStream_t s, bool aug);
     enum : unsigned { kTwiceNormals = 1, kTwiceTrmm = 2, kTwiceTarget = 4, kTwicePotrf = 32 };
     double host_wait_s_ = 0.0;  // run_batches_timed: host time blocked on the GPU (statuses)
     std::vector<std::vector<double>> cap_w_, cap_ratio_;
