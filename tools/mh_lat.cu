@@ -11,6 +11,7 @@
 
 namespace dgb {
 std::atomic<uint64_t> g_launch_count{0};
+thread_local uint64_t t_launch_count = 0;
 bool sync_check_enabled() { return false; }
 void set_smem_attr(const void* f, int bytes) {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
