@@ -1053,7 +1053,6 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         m.tri_c_lower = 1;
         const double fl = profiling_ ? device_count(kcount_ + o) * d_ * (d_ + 1.0) : -1.0;
         gemm("syrk_moments", m, C, false, false, s, fl);
-        launch_mean_update(mean_ + o * ld_, ld_, H_ + o * winh_, winh_, ldg_, C, d_, kcount_ + o, kc, (double)cb, s);
     }
     // ---- the chunk's x-space states: xi_k = G^-1 h_k for its accepted steps only (rows of Xi
     // into rows of H), then the reference's exact recursion x <- x_ref + c (x - x_ref) + xi_k
@@ -1079,7 +1078,7 @@ void Engine::enqueue_chunk(Group& g, const WindowPlan& p, int r0, int rows) {
         launch_reconstruct(x_ + o * ld_, k_.adaptive_ref ? xr_ + o * ld_ : nullptr, beta_ + o, k_.pcn_form() ? 1 : 0,
                            H_ + o * winh_, winh_, ldg_, Xi_ + o * win_, win_, ld_, state_src_ + (size_t)o * Lw_,
                            state_mult_ + (size_t)o * Lw_, Lw_, kcount_ + o, acc_cnt_ + o, mean_x_ + o * ld_,
-                           diag_x_ + o * ld_, (double)cb, kc, C, d_, s);
+                           diag_x_ + o * ld_, (double)cb, kc, C, d_, W_ + o * win_, win_, mean_ + o * ld_, s);
         timed_end("reconstruct", 0.0, s);
     }
     if (project)

@@ -81,15 +81,12 @@ void launch_mh_window(const StepParams& p, cudaStream_t s);
 void launch_reconstruct(double* x, const double* xr, const double* beta, int pcn, const double* XA, int64_t xa_stride,
                         int64_t xa_ld, double* Xout, int64_t xo_stride, int64_t ld, const int* state_src,
                         const int* state_mult, int out_ld, const int* kcount, const int* acc_count, double* mean_x,
-                        double* diag_x, double n_prev, int kc, int chains, int d, cudaStream_t s);
+                        double* diag_x, double n_prev, int kc, int chains, int d, const double* Z, int64_t z_stride,
+                        double* mean_z, cudaStream_t s);
 
 // ---------------------------------------------------------------- moments
-// Running mean over the chunk's k counted steps: mean <- (n mean + sum_j Xw_j) / (n + k),
-// Xw_j = m_j x_j the weighted distinct states (rows [0, kcount_c) of chain c's window).
-// (The second moment is the weighted SYRK through gemm_f64.)
-void launch_mean_update(double* mean, int64_t mean_stride, const double* Xw, int64_t win_stride,
-                        int64_t ld, int chains, int d, const int* kcount, int k, double n_prev,
-                        cudaStream_t s);
+// (The running means are updated by reconstruct_kernel; the second moment is the weighted
+// SYRK through gemm_f64.)
 // Blend (count weights) and covariance, written as a lower matrix with zero upper part
 // into C_out (the refactor workspace); blended mean -> mb. jitter_eps > 0 adds
 // eps*trace_c/d on the diagonal (trace from tr[c]). mask: chains to process.

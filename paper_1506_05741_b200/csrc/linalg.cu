@@ -18,34 +18,6 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// ------------------------------------------------------------------ moments
-// mean <- keep * mean + add * (sum of the chain's weighted rows 0 .. kcount[c] - 1).
-// A CTA takes 32 columns: its 8 warps sum interleaved rows (coalesced 256-byte row pieces,
-// k/8 independent loads per thread), then the 8 partial sums are added in warp order.
-__global__ void __launch_bounds__(256) mean_update_kernel(double* mean, int64_t mean_stride, const double* X,
-                                                          int64_t win_stride, int64_t ld, int d, const int* kcount,
-                                                          double keep, double add) {
-    __shared__ double part[8][32];
-    const int c = blockIdx.y;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int i = blockIdx.x * 32 + lane;
-    const int k = kcount[c];
-    double s = 0.0;
-    if (i < d) {
-        const double* Xc = X + c * win_stride + i;
-        for (int r = warp; r < k; r += 8) s += Xc[(int64_t)r * ld];
-    }
-    part[warp][lane] = s;
-    __syncthreads();
-    if (warp == 0 && i < d) {
-        double t = 0.0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) t += part[w][lane];
-        double* m = mean + c * mean_stride + i;
-        *m = keep * *m + add * t;
-    }
-}
-
 // The x-space trace floor of the blended covariance (proj/src/proposal.cpp:177-183) from the
 // x-space statistics the whitened engine keeps: mb = wg mg + wl ml (the blended mean, also the
 // adaptive reference), tr = sum_i (wg Sg_ii + wl dl_i) - mb_i^2, try = tr > 1e-12 (1 + mb.mb)
@@ -673,17 +645,6 @@ unsigned grid_for(int64_t n, int threads, int cap_per_sm = 8) {
 }
 
 }  // namespace
-
-void launch_mean_update(double* mean, int64_t mean_stride, const double* Xw, int64_t win_stride, int64_t ld,
-                        int chains, int d, const int* kcount, int k, double n_prev, cudaStream_t s) {
-    if (k <= 0) return;
-    const double total = n_prev + k;
-    dim3 grid((unsigned)ceil_div(d, 32), chains);
-    mean_update_kernel<<<grid, 256, 0, s>>>(mean, mean_stride, Xw, win_stride, ld, d, kcount, n_prev / total,
-                                            1.0 / total);
-    DGB_LAUNCH_CHECK();
-    count_launch();
-}
 
 void launch_gemv_rows(const double* G, int64_t ld, int d, int nrows, const double* X, double* out, int64_t out_ld,
                       int chains, cudaStream_t s) {

@@ -533,16 +533,17 @@ void launch_r(const StepParams& p, cudaStream_t s) {
 
 // The x-space states of a chunk, in the reference's exact operations (proposal.cpp:119-124):
 // x <- x_ref + c (x - x_ref) + xi_k over the chunk's accepted steps k (xi_k = G^-1 h_k, rows of
-// XA); the distinct counted states x_j (rows of Xout, for the eigen-projection traces) and the
-// x-space running mean and raw diagonal (PSRF, trace floor, adaptive reference) with their
-// multiplicities. Threads over the entries (no cross-thread dependence), 128 per CTA so a
+// XA); the distinct counted states x_j (rows of Xout, for the eigen-projection traces), the
+// x-space running mean and raw diagonal (PSRF, trace floor, adaptive reference) and the
+// whitened running mean (from the z_j rows of Z, the blend's mean), with their multiplicities. Threads over the entries (no cross-thread dependence), 128 per CTA so a
 // chain spreads over d/128 CTAs.
 __global__ void __launch_bounds__(128) reconstruct_kernel(double* x, const double* xr, const double* beta, int pcn,
                                                           const double* XA, int64_t xa_stride, int64_t xa_ld,
                                                           double* Xout, int64_t xo_stride, int64_t ld,
                                                           const int* state_src, const int* state_mult, int out_ld,
                                                           const int* kcount, const int* acc_count, double* mean_x,
-                                                          double* diag_x, double keep, double add, int d) {
+                                                          double* diag_x, double keep, double add, int d,
+                                                          const double* Z, int64_t z_stride, double* mean_z) {
     const int c = blockIdx.y;
     const double b = beta[c];
     const double cc = pcn ? sqrt(fmax(0.0, 1.0 - b * b)) : 1.0;
@@ -551,16 +552,18 @@ __global__ void __launch_bounds__(128) reconstruct_kernel(double* x, const doubl
     const int* mul = state_mult + (int64_t)c * out_ld;
     const double* xa = XA + c * xa_stride;
     double* xo = Xout + c * xo_stride;
+    const double* zc = Z + c * z_stride;  // row j: the distinct state's whitened z_j
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d; e += gridDim.x * blockDim.x) {
         double v = x[c * ld + e];
         const double r = xr ? xr[c * ld + e] : 0.0;
-        double s1 = 0.0, s2 = 0.0;
+        double s1 = 0.0, s2 = 0.0, sz = 0.0;
         int j = 0;
         // states that predate the chunk's first acceptance
         for (; j < nj && src[j] < 0; ++j) {
             xo[(int64_t)j * ld + e] = v;
             s1 += mul[j] * v;
             s2 += mul[j] * (v * v);
+            sz += mul[j] * zc[(int64_t)j * ld + e];
         }
         for (int k = 0; k < nk; ++k) {
             v = __dadd_rn(__dadd_rn(r, __dmul_rn(cc, __dadd_rn(v, -r))), xa[(int64_t)k * xa_ld + e]);
@@ -568,12 +571,14 @@ __global__ void __launch_bounds__(128) reconstruct_kernel(double* x, const doubl
                 xo[(int64_t)j * ld + e] = v;
                 s1 += mul[j] * v;
                 s2 += mul[j] * (v * v);
+                sz += mul[j] * zc[(int64_t)j * ld + e];
             }
         }
         x[c * ld + e] = v;
         if (nj > 0) {
             mean_x[c * ld + e] = keep * mean_x[c * ld + e] + add * s1;
             diag_x[c * ld + e] = keep * diag_x[c * ld + e] + add * s2;
+            mean_z[c * ld + e] = keep * mean_z[c * ld + e] + add * sz;  // the blend's whitened mean
         }
     }
 }
@@ -620,13 +625,15 @@ void launch_mh_window(const StepParams& p, cudaStream_t s) {
 void launch_reconstruct(double* x, const double* xr, const double* beta, int pcn, const double* XA, int64_t xa_stride,
                         int64_t xa_ld, double* Xout, int64_t xo_stride, int64_t ld, const int* state_src,
                         const int* state_mult, int out_ld, const int* kcount, const int* acc_count, double* mean_x,
-                        double* diag_x, double n_prev, int kc, int chains, int d, cudaStream_t s) {
+                        double* diag_x, double n_prev, int kc, int chains, int d, const double* Z, int64_t z_stride,
+                        double* mean_z, cudaStream_t s) {
     if (chains <= 0) return;
     const double total = n_prev + kc;
     const dim3 grid((unsigned)std::max(1, (d + 127) / 128), (unsigned)chains);
     reconstruct_kernel<<<grid, 128, 0, s>>>(x, xr, beta, pcn, XA, xa_stride, xa_ld, Xout, xo_stride, ld, state_src,
                                               state_mult, out_ld, kcount, acc_count, mean_x, diag_x,
-                                              total > 0 ? n_prev / total : 0.0, total > 0 ? 1.0 / total : 0.0, d);
+                                              total > 0 ? n_prev / total : 0.0, total > 0 ? 1.0 / total : 0.0, d, Z,
+                                              z_stride, mean_z);
     DGB_LAUNCH_CHECK();
     count_launch();
 }
