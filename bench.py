@@ -197,6 +197,30 @@ def time_to_cov_error(lib, with_reference: bool):
     return out
 
 
+def time_to_cov_error_d1024(lib, cpu):
+    """Time-to-cov-error at the benchmark dimension (a reachable tolerance at
+    d <= 1024): config 2 (pi1 d=1024, 64 chains, M=4, n0=0) until cov_err <= 0.5, end to end
+    through diam_sample. The reference would need the same number of samples at its measured
+    rate (cpu_baseline, the same run's host cores): hours, so its time is the composed
+    samples / rate, labelled as such."""
+    path = make_target_file("pi1", 1024)
+    t = lib.target_load(path)
+    kw = dict(kernel="diam", chains=64, intervals_per_batch=4, max_batches=3000, n0=0, cov_tol=0.5, master_seed=3,
+              record_traces=0, trace_eigen_projections=0)
+    t0 = time.perf_counter()
+    r = lib.sample(t, **kw)
+    secs = time.perf_counter() - t0
+    os.unlink(path)
+    out = {"target": "pi1 d=1024 (config 2)", "chains": 64, "cov_tol": 0.5, "gpu_seconds": secs,
+           "gpu_samples": r.total_samples, "gpu_batches": r.batches, "gpu_stop": r.stop_reason,
+           "gpu_final_cov_error": r.final_cov_error}
+    if cpu and cpu.get("value"):
+        out["reference_seconds_composed"] = r.total_samples / cpu["value"]
+        out["reference_note"] = ("composed: the GPU run's sample count at the reference's measured "
+                                 f"{cpu['value']:.0f} chain-samples/s on {cpu.get('cores')} host cores")
+    return out
+
+
 # ---------------------------------------------------------------------------- reference CPU arm
 def reference_sample(cfg_name, target_path, threads, chains, windows=1):
     """One bounded reference run: `chains` chains x `windows` lag windows on the host cores."""
@@ -420,6 +444,8 @@ def impl_b200(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             line["time_to_cov_error"] = time_to_cov_error(lib, with_reference=True)
+            if args.config == "d1024":
+                line["time_to_cov_error_d1024"] = time_to_cov_error_d1024(lib, cpu)
         print(json.dumps(line))
     if dist:
         lib.lib.diamx_comm_destroy()
