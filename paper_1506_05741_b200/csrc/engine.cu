@@ -1102,7 +1102,13 @@ void Engine::factor(Group& g, cudaStream_t s, bool aug) {
         cudaGraph_t graph = nullptr;
         DGB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         const uint64_t n0 = t_launch_count;
-        potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+        try {
+            potrf_batched(g.Lnp, ld_, d_, C, try_ + o, status_ + o, g.pw, s, aug ? 1 : 0);
+        } catch (...) {  // leave the stream out of capture mode before reporting
+            cudaStreamEndCapture(s, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
         g.potrf_nodes = t_launch_count - n0;
         DGB_CUDA(cudaStreamEndCapture(s, &graph));
         g_launch_count.fetch_sub(g.potrf_nodes, std::memory_order_relaxed);  // recorded, not launched
