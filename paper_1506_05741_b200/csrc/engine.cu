@@ -398,17 +398,20 @@ void Engine::upload_target() {
     // window target product of d(d+1) + 2dT flops per row instead of 2d^2
     G_ = dalloc<double>(A, (size_t)dg_ * ld_);
     double* prev = nullptr;
-    DGB_CUDA(cudaMalloc(&prev, (size_t)mat_ * sizeof(double)));
+    // transient buffers from the engine's stream-ordered pool (freed with it): a plain
+    // cudaMalloc/cudaFree pair here synchronised the device and let the driver trim the pool
+    // the previous engine left -- 450 ms of engine construction, every other diam_sample
+    prev = dalloc<double>(A, mat_);
     if (twisted_) {
         // P_rev = A_rev A_rev^T, A_rev[i][k] = V[d-1-i][k] / sigma_k
         Mat ar(d_, d_);
         for (int i = 0; i < d_; ++i)
             for (int k = 0; k < d_; ++k) ar(i, k) = tgt_.eigvecs(d_ - 1 - i, k) / std::sqrt(tgt_.eigvals[k]);
         double* dar = nullptr;
-        DGB_CUDA(cudaMalloc(&dar, (size_t)mat_ * sizeof(double)));
+        dar = dalloc<double>(A, mat_);
         upload_padded(dar, ld_, ar);
         double** pp = nullptr;
-        DGB_CUDA(cudaMalloc(&pp, 2 * sizeof(double*)));
+        pp = dalloc<double*>(A, 2);
         const double* hp[2] = {dar, prev};
         DGB_CUDA(cudaMemcpy(pp, hp, sizeof(hp), cudaMemcpyHostToDevice));
         GemmBatch g{};
@@ -420,8 +423,7 @@ void Engine::upload_target() {
         g.alpha = 1.0;
         gemm_f64(g, 1, true, true, stream_);
         DGB_CUDA(cudaStreamSynchronize(stream_));
-        cudaFree(pp);
-        cudaFree(dar);
+
     } else {
         Mat rev(d_, d_);
         for (int i = 0; i < d_; ++i)
@@ -429,7 +431,6 @@ void Engine::upload_target() {
         upload_padded(prev, ld_, rev);
     }
     whitening_factor(prev, G_, d_, ld_, stream_);
-    cudaFree(prev);
     const int T = dg_ - d_;
     std::vector<double> ie(ldg_, 0.0), bc(ldg_, 0.0);
     for (int i = 0; i < d_; ++i) ie[i] = 1.0;
@@ -460,9 +461,9 @@ void Engine::upload_target() {
         double** pa = ptr_array(A, G_, 0, 1);
         Ginvp_ = ptr_array(A, Ginv_, 0, 1);
         double* tscr = nullptr;
-        DGB_CUDA(cudaMalloc(&tscr, (size_t)((d_ + 1) / 2) * ld_ * sizeof(double)));
+        tscr = dalloc<double>(A, (size_t)((d_ + 1) / 2) * ld_);
         double** tp = nullptr;
-        DGB_CUDA(cudaMalloc(&tp, sizeof(double*)));
+        tp = dalloc<double*>(A, 1);
         DGB_CUDA(cudaMemcpy(tp, &tscr, sizeof(double*), cudaMemcpyHostToDevice));
         trtri_batched(pa, Ginvp_, tp, ld_, d_, 1, nullptr, stream_);
         GemmBatch gg{};
@@ -489,8 +490,7 @@ void Engine::upload_target() {
             gemm_f64(b, 1, true, false, stream_);
         }
         DGB_CUDA(cudaStreamSynchronize(stream_));
-        cudaFree(tp);
-        cudaFree(tscr);
+
     }
     Ct_ = dalloc<double>(A, (size_t)d_ * d_);
     DGB_CUDA(cudaMemcpy(Ct_, tgt_.covariance.a.data(), (size_t)d_ * d_ * 8, cudaMemcpyHostToDevice));
