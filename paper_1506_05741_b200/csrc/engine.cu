@@ -183,6 +183,7 @@ void upload_padded(double* dst, int64_t ld, const Mat& m) {
 
 Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shared_ptr<Comm> comm)
     : tgtp_(std::move(t)), tgt_(*tgtp_), cfg_(cfg), k_(cfg.kernel), comm_(std::move(comm)) {
+    const auto tctor = std::chrono::steady_clock::now();
     validate_run_cfg(cfg_, tgt_);
     if (const char* e = std::getenv("DIAM_B200_TWICE")) {
         const std::string v = e;
@@ -243,6 +244,9 @@ Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shar
         std::fprintf(stderr, "engine init %-14s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
         t0 = t1;
     };
+    if (tinit)
+        std::fprintf(stderr, "engine init %-14s %8.3f ms\n", "prologue",
+                     std::chrono::duration<double, std::milli>(t0 - tctor).count());
     upload_target();
     mark("upload_target");
     const int ng = plan_memory();
@@ -263,6 +267,9 @@ Engine::Engine(std::shared_ptr<const HostTarget> t, const RunCfg& cfg, std::shar
     make_groups(ng);
     DGB_CUDA(cudaStreamSynchronize(0));
     mark("make_groups");
+    if (tinit)
+        std::fprintf(stderr, "engine init %-14s %8.3f ms\n", "total",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tctor).count());
 }
 
 int Engine::plan_memory() {
