@@ -521,7 +521,11 @@ void launch_r(const StepParams& p, cudaStream_t s) {
     // d = 2040 -- 1122 pairs with the twisted rows -- measured 4% slower per batch than one
     // CTA with 4 pairs per thread: twice the CTAs of the 1-CTA-per-SM step kernel.)
     bool done = false;
-    if (pairs <= 256) done = try_tma<1, 256>(p, s);
+    // small d (the time-to-cov-error workloads): as few warps as cover the row, so the
+    // per-step reduction and barrier span 2 or 4 warps instead of 8
+    if (pairs <= 64) done = try_tma<1, 64>(p, s);
+    else if (pairs <= 128) done = try_tma<1, 128>(p, s);
+    else if (pairs <= 256) done = try_tma<1, 256>(p, s);
     else if (pairs <= 512) done = try_tma<2, 256>(p, s);
     else if (pairs <= 1024) done = try_tma<2, 512>(p, s);
     else if (pairs <= 2048) done = try_tma<4, 512>(p, s);
@@ -538,47 +542,71 @@ void launch_r(const StepParams& p, cudaStream_t s) {
 // whitened running mean (from the z_j rows of Z, the blend's mean), with their multiplicities. Threads over the entries (no cross-thread dependence), 128 per CTA so a
 // chain spreads over d/128 CTAs.
 __global__ void __launch_bounds__(128) reconstruct_kernel(double* x, const double* xr, const double* beta, int pcn,
-                                                          const double* XA, int64_t xa_stride, int64_t xa_ld,
-                                                          double* Xout, int64_t xo_stride, int64_t ld,
-                                                          const int* state_src, const int* state_mult, int out_ld,
-                                                          const int* kcount, const int* acc_count, double* mean_x,
-                                                          double* diag_x, double keep, double add, int d,
-                                                          const double* Z, int64_t z_stride, double* mean_z) {
+                                                          const double* __restrict__ XA, int64_t xa_stride,
+                                                          int64_t xa_ld, double* __restrict__ Xout, int64_t xo_stride,
+                                                          int64_t ld, const int* state_src, const int* state_mult,
+                                                          int out_ld, const int* kcount, const int* acc_count,
+                                                          double* mean_x, double* diag_x, double keep, double add,
+                                                          int d, const double* __restrict__ Z, int64_t z_stride,
+                                                          double* mean_z) {
+    // the chain's (src, mult) lists in shared memory: every thread walks them
+    extern __shared__ int rec_sm[];
     const int c = blockIdx.y;
     const double b = beta[c];
     const double cc = pcn ? sqrt(fmax(0.0, 1.0 - b * b)) : 1.0;
     const int nk = acc_count[c], nj = kcount[c];
-    const int* src = state_src + (int64_t)c * out_ld;
-    const int* mul = state_mult + (int64_t)c * out_ld;
+    int* src = rec_sm;
+    int* mul = rec_sm + out_ld;
+    for (int j = threadIdx.x; j < nj; j += blockDim.x) {
+        src[j] = state_src[(int64_t)c * out_ld + j];
+        mul[j] = state_mult[(int64_t)c * out_ld + j];
+    }
+    __syncthreads();
     const double* xa = XA + c * xa_stride;
     double* xo = Xout + c * xo_stride;
     const double* zc = Z + c * z_stride;  // row j: the distinct state's whitened z_j
+    constexpr int PF = 8;                 // accepted increments in flight per thread
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d; e += gridDim.x * blockDim.x) {
         double v = x[c * ld + e];
         const double r = xr ? xr[c * ld + e] : 0.0;
-        double s1 = 0.0, s2 = 0.0, sz = 0.0;
+        double s1 = 0.0, s2 = 0.0;
         int j = 0;
         // states that predate the chunk's first acceptance
         for (; j < nj && src[j] < 0; ++j) {
             xo[(int64_t)j * ld + e] = v;
             s1 += mul[j] * v;
             s2 += mul[j] * (v * v);
-            sz += mul[j] * zc[(int64_t)j * ld + e];
         }
-        for (int k = 0; k < nk; ++k) {
-            v = __dadd_rn(__dadd_rn(r, __dmul_rn(cc, __dadd_rn(v, -r))), xa[(int64_t)k * xa_ld + e]);
-            for (; j < nj && src[j] == k; ++j) {
-                xo[(int64_t)j * ld + e] = v;
-                s1 += mul[j] * v;
-                s2 += mul[j] * (v * v);
-                sz += mul[j] * zc[(int64_t)j * ld + e];
+        // the recursion is serial in v, its increments are not: PF loads issued per block
+        for (int k0 = 0; k0 < nk; k0 += PF) {
+            double inc[PF];
+#pragma unroll
+            for (int i = 0; i < PF; ++i) inc[i] = k0 + i < nk ? xa[(int64_t)(k0 + i) * xa_ld + e] : 0.0;
+#pragma unroll
+            for (int i = 0; i < PF; ++i) {
+                const int k = k0 + i;
+                if (k >= nk) break;
+                v = __dadd_rn(__dadd_rn(r, __dmul_rn(cc, __dadd_rn(v, -r))), inc[i]);
+                for (; j < nj && src[j] == k; ++j) {
+                    xo[(int64_t)j * ld + e] = v;
+                    s1 += mul[j] * v;
+                    s2 += mul[j] * (v * v);
+                }
             }
         }
         x[c * ld + e] = v;
         if (nj > 0) {
+            // the whitened running mean (the blend's) from the z_j rows, loads in flight together
+            double sz[4] = {0.0, 0.0, 0.0, 0.0};
+            int jj = 0;
+            for (; jj + 4 <= nj; jj += 4) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) sz[i] += mul[jj + i] * zc[(int64_t)(jj + i) * ld + e];
+            }
+            for (; jj < nj; ++jj) sz[0] += mul[jj] * zc[(int64_t)jj * ld + e];
             mean_x[c * ld + e] = keep * mean_x[c * ld + e] + add * s1;
             diag_x[c * ld + e] = keep * diag_x[c * ld + e] + add * s2;
-            mean_z[c * ld + e] = keep * mean_z[c * ld + e] + add * sz;  // the blend's whitened mean
+            mean_z[c * ld + e] = keep * mean_z[c * ld + e] + add * ((sz[0] + sz[1]) + (sz[2] + sz[3]));
         }
     }
 }
@@ -630,7 +658,9 @@ void launch_reconstruct(double* x, const double* xr, const double* beta, int pcn
     if (chains <= 0) return;
     const double total = n_prev + kc;
     const dim3 grid((unsigned)std::max(1, (d + 127) / 128), (unsigned)chains);
-    reconstruct_kernel<<<grid, 128, 0, s>>>(x, xr, beta, pcn, XA, xa_stride, xa_ld, Xout, xo_stride, ld, state_src,
+    const size_t smem = 2 * (size_t)out_ld * sizeof(int);
+    if (smem > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(reconstruct_kernel), (int)smem);
+    reconstruct_kernel<<<grid, 128, smem, s>>>(x, xr, beta, pcn, XA, xa_stride, xa_ld, Xout, xo_stride, ld, state_src,
                                               state_mult, out_ld, kcount, acc_count, mean_x, diag_x,
                                               total > 0 ? n_prev / total : 0.0, total > 0 ? 1.0 / total : 0.0, d, Z,
                                               z_stride, mean_z);
