@@ -129,7 +129,7 @@ def run_options(cfg, chains, **over):
 
 def ncu_gemm_traffic(cfg_name, chains, d, n_lag, distinct=1.0, accepted=0.0):
     """DRAM bytes per launch of the DMMA GEMM classes from the committed `ncu --set full`
-    captures (profiles/r02b_ncu_<class>.csv, tools/ncu_capture.sh: d=1024, 64 chains, single
+    captures (profiles/r02c_ncu_<class>.csv, tools/ncu_capture.sh: d=1024, 64 chains, single
     stream), against their algorithmic bytes (operands in once, results out once)."""
     import csv
     if cfg_name != "d1024" or chains != 64:
@@ -144,7 +144,7 @@ def ncu_gemm_traffic(cfg_name, chains, d, n_lag, distinct=1.0, accepted=0.0):
     alg_bytes = {"trmm_noise": 2 * w + tri, "syrk_moments": int(2 * distinct * w) + 2 * tri,
                  "xi_accepted": int(2 * accepted * w) + tri // chains}
     for cls in ("trmm_noise", "syrk_moments", "xi_accepted"):
-        path = os.path.join(ROOT, "profiles", f"r02b_ncu_{cls}.csv")
+        path = os.path.join(ROOT, "profiles", f"r02c_ncu_{cls}.csv")
         if not os.path.exists(path):
             return None
         rows = list(csv.reader(open(path)))
@@ -157,7 +157,7 @@ def ncu_gemm_traffic(cfg_name, chains, d, n_lag, distinct=1.0, accepted=0.0):
         out[cls] = tot
         alg[cls] = alg_bytes[cls]
     return {"dram_bytes_per_launch": out, "algorithmic_bytes_per_launch": alg,
-            "source": "profiles/r02b_ncu_*.csv (one steady-state launch each, single stream; writes still "
+            "source": "profiles/r02c_ncu_*.csv (one steady-state launch each, single stream; writes still "
                       "in L2 when the kernel ends are not counted)"}
 
 
