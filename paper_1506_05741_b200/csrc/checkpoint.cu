@@ -133,11 +133,6 @@ void Engine::congruence(const double* S, const double* M, double* out) {
 void Engine::save_checkpoint(double wall) {
     DGB_CUDA(cudaDeviceSynchronize());
     const int C = C_;
-    auto fetch = [&](const void* src, size_t bytes) {
-        std::vector<char> buf(bytes);
-        DGB_CUDA(cudaMemcpy(buf.data(), src, bytes, cudaMemcpyDeviceToHost));
-        return buf;
-    };
     auto fetch_d = [&](const double* src, size_t n) {
         std::vector<double> v(n);
         DGB_CUDA(cudaMemcpy(v.data(), src, n * 8, cudaMemcpyDeviceToHost));

@@ -70,9 +70,7 @@ __device__ long long g_mh_prof[8];
     } while (0)
 #endif
 
-constexpr int kStepThreads = 512;
 constexpr int kMaxStages = 8;  // TMA ring depth bound (one mbarrier per stage)
-constexpr int kStepWarps = kStepThreads / 32;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -214,7 +212,9 @@ __global__ void __launch_bounds__(T, 1) mh_window_kernel(StepParams p, int NS) {
 
     // GRL: the reference point read through L1 each step (4+ pairs per thread: registers would spill)
     constexpr bool GRL = !ZREF && R >= 4;
-    double2 g[R], y[R], grv[(ZREF || GRL) ? 1 : R], iev[TWG ? 1 : R], bcv[TWG ? 1 : R], ga[R], cy[R];
+    // (value-initialised: the accessor lambdas below capture them before the loading loop)
+    double2 g[R] = {}, y[R] = {}, grv[(ZREF || GRL) ? 1 : R] = {}, iev[TWG ? 1 : R] = {}, bcv[TWG ? 1 : R] = {},
+            ga[R] = {}, cy[R] = {};
     bool vx[R], vg[R];  // entry pair e in x-space (e < d) / in g-space (e < dg)
     auto GR = [&](int r) -> double2 {
         if (ZREF) return make_double2(0.0, 0.0);
