@@ -112,6 +112,54 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB) lab_kernel(Args p) {
     gemm_epilogue<CF>(acc, C, p.ldc, p.M, p.N, m0, n0, 1.0, 0.0, false);
 }
 
+// MODE 2 (triangular B only): CTA x takes column tiles x and NT-1-x, so every CTA has the
+// same total K (64 (x+1) + 64 (NT-x)) -- one kernel of equal-length CTAs
+template <class CF>
+__global__ void __launch_bounds__(CF::THREADS, CF::MINB) lab_pair_kernel(Args p) {
+    extern __shared__ __align__(16) double smem[];
+    const int b = blockIdx.z, m0 = blockIdx.y * CF::BM;
+    const int NT = (p.N + CF::BN - 1) / CF::BN;
+    const double* A = p.A + b * p.a_stride;
+    const double* B = p.B + b * p.b_stride;
+    double* C = p.C + b * p.c_stride;
+    const int tiles[2] = {NT - 1 - (int)blockIdx.x, (int)blockIdx.x};
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+        const int nt = tiles[q];
+        if (q == 1 && nt == tiles[0]) break;
+        const int n0 = nt * CF::BN;
+        const int K = min(p.K, n0 + CF::BN);
+        double acc[CF::MI][CF::NI][2];
+        gemm_mainloop<CF, true, true>(A, B, p.lda, p.ldb, p.M, p.N, K, m0, n0, false, smem, true, acc);
+        gemm_epilogue<CF>(acc, C, p.ldc, p.M, p.N, m0, n0, 1.0, 0.0, false);
+    }
+}
+
+template <class CF>
+double run_pair(const Args& a, int batch, const char* name, double flops) {
+    auto k = lab_pair_kernel<CF>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
+    const int NT = (a.N + CF::BN - 1) / CF::BN;
+    dim3 grid((NT + 1) / 2, (a.M + CF::BM - 1) / CF::BM, batch);
+    for (int i = 0; i < 2; ++i) k<<<grid, CF::THREADS, CF::SMEM_BYTES>>>(a);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        for (int i = 0; i < 5; ++i) k<<<grid, CF::THREADS, CF::SMEM_BYTES>>>(a);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms / 5 < best ? ms / 5 : best;
+    }
+    const double tf = flops / (best * 1e-3) / 1e12;
+    std::printf("%-44s %8.3f ms %6.2f TFLOP/s  (%s)\n", name, best, tf, cudaGetErrorString(cudaGetLastError()));
+    return tf;
+}
+
 template <class CF, int MODE>
 double run(const Args& a, int batch, const char* name, double flops) {
     auto k = lab_kernel<CF, MODE>;
@@ -167,6 +215,10 @@ int main() {
     run<W4b, 1>(dense, 1, "dense 128x64x16x3 4w (64x32) + frag db", fd);
     run<W4c, 1>(dense, 1, "dense 64x128x32x2 4w + frag db", fd);
     run<Kept, 0>(trmm, 64, "trmm kept", ft);
+    run_pair<Kept>(trmm, 64, "trmm kept, paired column tiles", ft);
+    using K64 = Cfg<64, 64, 32, 2, true, true, 2, 2, 3>;
+    run<K64, 0>(trmm, 64, "trmm 64x64x32x2 4w 3/SM", ft);
+    run_pair<K64>(trmm, 64, "trmm 64x64 paired", ft);
     run<Kept, 1>(trmm, 64, "trmm kept + frag db", ft);
     run<W4, 0>(trmm, 64, "trmm 64x128x16x3 4w", ft);
     run<W4, 1>(trmm, 64, "trmm 64x128x16x3 4w + frag db", ft);
