@@ -361,6 +361,9 @@ def impl_b200(args):
     peak = C.c_double()
     lib.check(lib.lib.diamx_fp64_peak(C.byref(peak)))
     achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
+    t_ms, t_fl = st["trmm_noise"][0], st["trmm_noise"][1]
+    t_achieved = t_fl / (t_ms / 1e3) / 1e12 if t_ms > 0 else 0.0
+    f_achieved = st["potrf"][1] / (st["potrf"][0] / 1e3) / 1e12 if st["potrf"][0] > 0 else 0.0
     # the step's algorithmic flops: every class's count from the profiled batch (the SYRK over
     # the window's distinct states and the accepted steps' increments count the rows they ran
     # over), scaled to the timed run's chains per GPU
@@ -420,14 +423,19 @@ def impl_b200(args):
                        "l2": "no flush needed: per-step working set "
                              f"{(3 * d * d + 3 * n_lag * d) * 8 * per_gpu / 1e9:.1f} GB >> 126 MB L2"},
             "roofline": {"bound": "tensor", "pipe": "FP64 DMMA (mma.sync.m8n8k4.f64; tcgen05 has no f64 kind)",
-                         "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                         "frac": achieved / peak.value if peak.value else None,
+                         "achieved": t_achieved, "peak": peak.value, "unit": "TFLOP/s",
+                         "frac": t_achieved / peak.value if peak.value else None,
                          "traffic": traffic["dram_bytes_per_launch"]["trmm_noise"] if traffic else None,
-                         "traffic_kernel": "trmm_noise (the largest launch of the class)",
                          "traffic_detail": traffic,
-                         "kernel": "gemm_f64 (window TRMM H = s W L_z^T, twisted rows, SYRK moments, "
-                                   "accepted increments)",
-                         "share_of_step": g_ms / prof_total if prof_total else None,
+                         "kernel": "trmm_noise: the window TRMM H = s W L_z^T (the step's largest kernel)",
+                         "share_of_step": t_ms / prof_total if prof_total else None,
+                         "gemm_class": {"kernels": "TRMM + twisted rows + SYRK moments + accepted increments",
+                                        "achieved": achieved, "frac": achieved / peak.value if peak.value else None,
+                                        "share_of_step": g_ms / prof_total if prof_total else None},
+                         "factorization_class": {"kernels": "long-K updates + diagonal blocks + TRSMs (d^3/3 flops)",
+                                                 "achieved": f_achieved,
+                                                 "frac": f_achieved / peak.value if peak.value else None,
+                                                 "share_of_step": st["potrf"][0] / prof_total if prof_total else None},
                          "peak_source": "diamx_fp64_peak: DMMA m8n8k4 loop measured live (MEASURED_PEAKS.json "
                                         "has no FP64 entry)",
                          "step_alg_tflops": alg_flops / (ms / args.steps / 1e3) / 1e12,
