@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--config", default="d1024", choices=sorted(bench.CONFIGS))
     ap.add_argument("--batches", type=int, default=5)
     ap.add_argument("--groups", default="")
+    ap.add_argument("--warmup", type=int, default=2)
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     kind, d, per_gpu, n_lag, M = cfg
@@ -33,7 +34,7 @@ def main():
         if g:
             os.environ["DIAM_B200_GROUPS"] = g
         eng = lib.engine(t, **bench.run_options(cfg, per_gpu))
-        eng.run_batches(2)
+        eng.run_batches(args.warmup)
         l0 = lib.launch_count()
         e0 = eng.stat("host_enqueue")[0]
         w0 = eng.stat("host_wait")[0]

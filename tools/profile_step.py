@@ -17,6 +17,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="d1024", choices=sorted(bench.CONFIGS))
     ap.add_argument("--batches", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=1, help="batches before the timed ones (the chains adapt: "
+                    "the per-batch cost settles after ~10)")
     ap.add_argument("--chains", type=int, default=0)
     ap.add_argument("--classes", action="store_true", help="per-kernel-class CUDA-event times of one more batch")
     args = ap.parse_args()
@@ -27,7 +29,7 @@ def main():
     t = lib.target_load(path)
     eng = lib.engine(t, **bench.run_options(cfg, args.chains or per_gpu))
     print(f"layout {eng.layout}", flush=True)
-    eng.run_batches(1)
+    eng.run_batches(args.warmup)
     ms = eng.run_batches(args.batches)
     os.unlink(path)
     n = (args.chains or per_gpu) * M * n_lag * args.batches
