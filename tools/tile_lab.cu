@@ -214,6 +214,24 @@ int main() {
     run<W4, 1>(dense, 1, "dense 64x128x16x3 4w + frag db", fd);
     run<W4b, 1>(dense, 1, "dense 128x64x16x3 4w (64x32) + frag db", fd);
     run<W4c, 1>(dense, 1, "dense 64x128x32x2 4w + frag db", fd);
+    {
+        // the accepted-rows product of one chain group at the adapted acceptance: 4 chains x
+        // ~230 rows against the shared G^-1 (lower): per chain on 64-row tiles (now) against
+        // the 4 chains' rows stacked into one product on 128-row tiles
+        using K64x = Cfg<64, 64, 32, 2, true, true, 2, 2, 3>;
+        Args per{A, B, C, (int64_t)230 * K, 0, (int64_t)230 * N, 230, N, K, K, K, N, 1};
+        Args stacked{A, B, C, 0, 0, 0, 920, N, K, K, K, N, 1};
+        const double fx = 920.0 * N * (N + 1);
+        run<K64x, 0>(per, 4, "xi: 4 x 230 rows, 64x64 tiles", fx);
+        run<Kept, 0>(stacked, 1, "xi: 920 stacked rows, 128x64 tiles", fx);
+        run_pair<Kept>(stacked, 1, "xi: 920 stacked rows, 128x64 paired", fx);
+        Args per64{A, B, C, (int64_t)230 * K, 0, (int64_t)230 * N, 230, N, K, K, K, N, 1};
+        Args st64{A, B, C, 0, 0, 0, 230 * 64, N, K, K, K, N, 1};
+        const double fx64 = 64.0 * 230 * N * (N + 1);
+        run<K64x, 0>(per64, 64, "xi 64 chains: 64x64 tiles per chain", fx64);
+        run<Kept, 0>(st64, 1, "xi 64 chains stacked: 128x64 tiles", fx64);
+        run_pair<Kept>(st64, 1, "xi 64 chains stacked: 128x64 paired", fx64);
+    }
     run<Kept, 0>(trmm, 64, "trmm kept", ft);
     run_pair<Kept>(trmm, 64, "trmm kept, paired column tiles", ft);
     using K64 = Cfg<64, 64, 32, 2, true, true, 2, 2, 3>;
